@@ -1,0 +1,245 @@
+"""Seeded synthetic workloads for the per-RE MMSE detector (shared by tests, bench, smoke).
+
+This module holds NO detection arithmetic. It draws channels, bits and noise,
+maps bits to QAM symbols (the transmitter side), forms y = H x + n in fp64 and
+casts H and y to complex64, which are then the canonical inputs of both the
+CUDA path and the fp64 oracle (SURVEY.md §8(d) "Synthetic inputs").
+
+Workloads stand in for the paper's link-level simulator (§IV:
+"MIMO-OFDM transmission using 15 kHz subcarrier spacing and 60 resource blocks
+... 3GPP TDL-C"). TDL-C and the MCS tables are not available, so
+BASELINE.json's five configs use i.i.d. / Kronecker Rayleigh channels; the
+recipe is stated in DESIGN.md §"Input recipe".
+
+Layouts (DESIGN.md §"Data layout in HBM"):
+  H    complex64 [n_slots][n_fb][n_rx][n_layers]    n_fb = n_sc / sc_per_h, row = rx
+  y    complex64 [n_sym][n_sc][n_rx]                n_sym = 14 * n_slots
+  bits uint8     [n_sym][n_sc][n_layers][qm]        bit j of a symbol = b_j (38.211 order)
+  llr  (any)     [n_sym][n_sc][n_layers][qm]
+An H-unit u = slot * n_fb + fb owns the REs (sym, sc) with sym in the slot's
+14 symbols and sc in block fb; inside a unit REs are ordered symbol-major.
+"""
+from __future__ import annotations
+
+import dataclasses
+import hashlib
+
+import numpy as np
+
+SYM_PER_SLOT = 14  # NR slot, normal cyclic prefix
+
+# BASELINE.json "configs", in order (C1..C5). sigma2 = 10^(-SNR/10), reading R8
+# (C1 states "SNR 10 dB (sigma^2 = 0.1)" explicitly).
+CONFIGS = {
+    1: dict(name="C1", n_rx=2, n_layers=2, qm=2, n_sc=12, n_slots=1, sc_per_h=1,
+            channel="iid", chan_var=1.0, snr_db=10.0, llr="f32"),
+    2: dict(name="C2", n_rx=4, n_layers=4, qm=4, n_sc=3276, n_slots=10, sc_per_h=1,
+            channel="iid", chan_var=1.0, snr_db=15.0, llr="f32"),
+    3: dict(name="C3", n_rx=8, n_layers=4, qm=6, n_sc=3276, n_slots=20, sc_per_h=12,
+            channel="kron", chan_var=1.0, rho=0.5, snr_db=20.0, llr="i8"),
+    4: dict(name="C4", n_rx=16, n_layers=8, qm=8, n_sc=3276, n_slots=20, sc_per_h=1,
+            channel="iid", chan_var=1.0 / 16, snr_db=28.0, llr="f16"),
+    5: dict(name="C5", n_rx=64, n_layers=16, qm=6, n_sc=3276, n_slots=40, sc_per_h=12,
+            channel="iid", chan_var=1.0 / 64, snr_db=20.0, llr="i8"),
+    # Context-only shape of the paper's own timing: 4x4,
+    # 60 RB x 12 = 720 subcarriers, one TTI. Not a BASELINE config.
+    "P": dict(name="P", n_rx=4, n_layers=4, qm=4, n_sc=720, n_slots=1, sc_per_h=1,
+              channel="iid", chan_var=1.0, snr_db=15.0, llr="f32"),
+}
+
+# Per-axis PAM normalisation of the 38.211 constellations (transmitter side).
+_QAM_NORM = {2: 2.0, 4: 10.0, 6: 42.0, 8: 170.0}
+
+
+def sigma2_of(snr_db: float) -> np.float32:
+    """Total complex noise variance sigma^2 = 10^(-SNR/10), rounded to fp32 (reading R8)."""
+    return np.float32(10.0 ** (-snr_db / 10.0))
+
+
+def qam_modulate(bits: np.ndarray, qm: int) -> np.ndarray:
+    """Map bits [..., qm] (b_0 first) to unit-power complex symbols, 3GPP 38.211 §5.1 form.
+
+    Bits b_0, b_2, ... drive I and b_1, b_3, ... drive Q; per axis with m = qm/2
+    bits c_0..c_{m-1}: v = (1-2c_{m-1}); v = (1-2c_i)(2^{m-1-i} - v) for i = m-2..0.
+    """
+    m = qm // 2
+    b = bits.astype(np.int64)
+    axes = []
+    for off in (0, 1):
+        c = [b[..., 2 * i + off] for i in range(m)]
+        v = 1 - 2 * c[m - 1]
+        for i in range(m - 2, -1, -1):
+            v = (1 - 2 * c[i]) * ((1 << (m - 1 - i)) - v)
+        axes.append(v.astype(np.float64))
+    return (axes[0] + 1j * axes[1]) / np.sqrt(_QAM_NORM[qm])
+
+
+def exp_corr_chol(n: int, rho: float) -> np.ndarray:
+    """Lower Cholesky factor C of the exponential correlation matrix R_ij = rho^|i-j|."""
+    idx = np.arange(n)
+    r = rho ** np.abs(idx[:, None] - idx[None, :])
+    return np.linalg.cholesky(r)
+
+
+def _cn(rng: np.random.Generator, shape, var: float) -> np.ndarray:
+    """Circularly-symmetric complex Gaussian CN(0, var), drawn as (re, im) pairs in fp64."""
+    g = rng.standard_normal(tuple(shape) + (2,))
+    return (g[..., 0] + 1j * g[..., 1]) * np.sqrt(var / 2.0)
+
+
+def unit_gather(grid: np.ndarray, n_slots: int, n_sc: int, sc_per_h: int) -> np.ndarray:
+    """[n_sym][n_sc][...] -> [n_units][14*sc_per_h][...] (symbol-major inside a unit). Indexing only."""
+    n_fb = n_sc // sc_per_h
+    tail = grid.shape[2:]
+    g = grid.reshape((n_slots, SYM_PER_SLOT, n_fb, sc_per_h) + tail)
+    g = np.moveaxis(g, 2, 1)  # [slot][fb][sym][f]...
+    return g.reshape((n_slots * n_fb, SYM_PER_SLOT * sc_per_h) + tail)
+
+
+def unit_scatter(units: np.ndarray, n_slots: int, n_sc: int, sc_per_h: int) -> np.ndarray:
+    """Inverse of unit_gather. Indexing only."""
+    n_fb = n_sc // sc_per_h
+    tail = units.shape[2:]
+    g = units.reshape((n_slots, n_fb, SYM_PER_SLOT, sc_per_h) + tail)
+    g = np.moveaxis(g, 1, 2)
+    return np.ascontiguousarray(g.reshape((n_slots * SYM_PER_SLOT, n_sc) + tail))
+
+
+def unit_re_index(u: int, n_sc: int, sc_per_h: int):
+    """(sym, sc) index arrays of the REs of unit u, in unit (symbol-major) order."""
+    n_fb = n_sc // sc_per_h
+    slot, fb = divmod(int(u), n_fb)
+    s = np.repeat(np.arange(SYM_PER_SLOT), sc_per_h) + slot * SYM_PER_SLOT
+    f = np.tile(np.arange(sc_per_h), SYM_PER_SLOT) + fb * sc_per_h
+    return s, f
+
+
+@dataclasses.dataclass
+class Workload:
+    name: str
+    n_rx: int
+    n_layers: int
+    qm: int
+    n_sc: int
+    n_slots: int
+    sc_per_h: int
+    llr: str
+    sigma2: np.float32
+    H: np.ndarray      # complex64 [n_slots][n_fb][nr][nl]
+    y: np.ndarray      # complex64 [n_sym][n_sc][nr]
+    bits: np.ndarray   # uint8 [n_sym][n_sc][nl][qm]
+    seed: int
+
+    @property
+    def n_sym(self) -> int:
+        return self.n_slots * SYM_PER_SLOT
+
+    @property
+    def n_fb(self) -> int:
+        return self.n_sc // self.sc_per_h
+
+    @property
+    def n_units(self) -> int:
+        return self.n_slots * self.n_fb
+
+    @property
+    def n_re(self) -> int:
+        return self.n_sym * self.n_sc
+
+    def H_units(self) -> np.ndarray:
+        return self.H.reshape(self.n_units, self.n_rx, self.n_layers)
+
+    def y_units(self) -> np.ndarray:
+        return unit_gather(self.y, self.n_slots, self.n_sc, self.sc_per_h)
+
+    def sha256(self) -> str:
+        h = hashlib.sha256()
+        h.update(np.ascontiguousarray(self.H).tobytes())
+        h.update(np.ascontiguousarray(self.y).tobytes())
+        h.update(np.float32(self.sigma2).tobytes())
+        return h.hexdigest()
+
+
+def generate(cfg, *, n_sc: int | None = None, n_slots: int | None = None,
+             seed: int | None = None, snr_db: float | None = None,
+             sigma2: float | None = None, H_override: np.ndarray | None = None,
+             noiseless: bool = False) -> Workload:
+    """Draw one seeded workload.
+
+    Recipe: Generator(PCG64(seed)), seed = 1000 + k by default;
+    draws in fp64 in this order: (1) H_w for all units (slot-major, then
+    frequency block), (2) bits for all REs in [n_sym][n_sc][nl][qm] order,
+    (3) noise slot by slot in [n_sym][n_sc][nr] order. Channel: iid CN(0, v),
+    or Kronecker H = C_r H_w C_t^T with C = chol(rho^|i-j|). y = H x + n in fp64,
+    then H and y are cast to complex64.
+    """
+    if isinstance(cfg, dict):
+        c = dict(cfg)
+        key = c.get("name", "custom")
+    else:
+        c = dict(CONFIGS[cfg])
+        key = cfg
+    if n_sc is not None:
+        c["n_sc"] = n_sc
+    if n_slots is not None:
+        c["n_slots"] = n_slots
+    if seed is None:
+        seed = 1000 + (key if isinstance(key, int) else 0)
+    nr, nl, qm, scph = c["n_rx"], c["n_layers"], c["qm"], c["sc_per_h"]
+    nsc, nslots = c["n_sc"], c["n_slots"]
+    if nsc % scph:
+        raise ValueError("n_sc must be a multiple of sc_per_h")
+    s2 = sigma2_of(snr_db if snr_db is not None else c["snr_db"]) if sigma2 is None else np.float32(sigma2)
+    rng = np.random.Generator(np.random.PCG64(seed))
+    n_fb = nsc // scph
+    n_units = nslots * n_fb
+    n_sym = nslots * SYM_PER_SLOT
+
+    # (1) channel per H-unit
+    Hw = _cn(rng, (n_units, nr, nl), 1.0)
+    if H_override is not None:
+        H = np.broadcast_to(np.asarray(H_override, dtype=np.complex128), (n_units, nr, nl)).copy()
+    elif c["channel"] == "kron":
+        cr = exp_corr_chol(nr, c["rho"])
+        ct = exp_corr_chol(nl, c["rho"])
+        H = np.sqrt(c["chan_var"]) * (cr @ Hw @ ct.T)
+    else:
+        H = np.sqrt(c["chan_var"]) * Hw
+    H64 = H.astype(np.complex64)
+
+    # (2) bits and symbols
+    bits = rng.integers(0, 2, size=(n_sym, nsc, nl, qm), dtype=np.uint8)
+    x = qam_modulate(bits, qm)  # [n_sym][n_sc][nl] complex128
+
+    # (3) y = H x + n, fp64, per slot (bounded memory), then complex64.
+    # The noiseless product uses the complex64-rounded H so that H is exactly
+    # the channel the detector sees (noiseless pins compare against x exactly).
+    Hq = H64.astype(np.complex128).reshape(nslots, n_fb, nr, nl)
+    y = np.empty((n_sym, nsc, nr), dtype=np.complex64)
+    for t in range(nslots):
+        xs = x[t * SYM_PER_SLOT:(t + 1) * SYM_PER_SLOT]          # [14][nsc][nl]
+        xs = xs.reshape(SYM_PER_SLOT, n_fb, scph, nl)
+        ys = np.einsum("frl,sfcl->sfcr", Hq[t], xs, optimize=True)  # [14][n_fb][scph][nr]
+        ys = ys.reshape(SYM_PER_SLOT, nsc, nr)
+        if not noiseless:
+            ys = ys + _cn(rng, (SYM_PER_SLOT, nsc, nr), float(s2))
+        y[t * SYM_PER_SLOT:(t + 1) * SYM_PER_SLOT] = ys.astype(np.complex64)
+
+    return Workload(name=c.get("name", str(key)), n_rx=nr, n_layers=nl, qm=qm, n_sc=nsc,
+                    n_slots=nslots, sc_per_h=scph, llr=c["llr"], sigma2=s2,
+                    H=H64.reshape(nslots, n_fb, nr, nl), y=y, bits=bits, seed=seed)
+
+
+def config_algorithmic_bytes(cfg_key, llr_bytes: int | None = None) -> dict:
+    """Algorithmic bytes of one full pass (H read once, y read once, LLRs written once), SURVEY.md §8(d)."""
+    c = CONFIGS[cfg_key]
+    nr, nl, qm, scph = c["n_rx"], c["n_layers"], c["qm"], c["sc_per_h"]
+    n_sym = c["n_slots"] * SYM_PER_SLOT
+    n_re = n_sym * c["n_sc"]
+    n_units = c["n_slots"] * (c["n_sc"] // scph)
+    lb = llr_bytes if llr_bytes is not None else {"f32": 4, "f16": 2, "i8": 1}[c["llr"]]
+    h = n_units * nr * nl * 8
+    yb = n_re * nr * 8
+    lo = n_re * nl * qm * lb
+    return dict(H=h, y=yb, llr=lo, total=h + yb + lo, n_re=n_re, n_units=n_units,
+                n_llr=n_re * nl * qm)
