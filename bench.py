@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 per-RE MMSE detector + max-log demapper.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+
+Metric (BASELINE.json): MIMO-detected REs/s (and LLR Gbit/s) per B200 vs roofline.
+A "step" is one mimo_detect_mmse call over one full batch of the configured
+workload (default configs[1] = C2: 4x4 16-QAM, 3276 sc x 14 sym x 10 slots),
+i.e. every hot-path row a1-a7 for every RE. Inputs are device-resident and
+rotated over enough buffer sets that the working set exceeds 3x L2; the K timed
+steps are replayed from CUDA graphs and timed with CUDA events on the launching
+stream. Multi-GPU (torchrun): weak scaling, rank r detects its own C2-sized
+block of slots; time = max over ranks.
+
+`e2e` times the same metric through the host-buffer C-ABI call
+(mimo_detect_mmse_host: pinned H/y -> device -> kernel -> LLRs back), and
+`cpu_baseline` / `--impl reference` time the fp64 oracle (test infrastructure,
+deliberately slow) on a bounded sample on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2510_07843_b200 import shard, synth  # noqa: E402
+
+METRIC = "MIMO-detected REs/s per B200 (LLR Gbit/s alongside) vs roofline"
+FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=50)
+    ap.add_argument("--config", default="2", help="BASELINE config index 1..5 (default 2 = configs[1])")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU budget of the oracle baseline")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no graphs, no e2e/cpu legs)")
+    return ap.parse_args()
+
+
+def cfg_key(s):
+    return "P" if s == "P" else int(s)
+
+
+def workload_desc(k) -> dict:
+    c = synth.CONFIGS[k]
+    return {"workload": f"{c['name']}: {c['n_rx']}x{c['n_layers']} {2 ** c['qm']}-QAM, {c['n_sc']} sc x "
+                        f"{synth.SYM_PER_SLOT} sym x {c['n_slots']} slots, H per "
+                        f"{'subcarrier' if c['sc_per_h'] == 1 else 'PRB'}, {c['llr']} LLR, SNR {c['snr_db']} dB",
+            "n_rx": c["n_rx"], "n_layers": c["n_layers"], "qm": c["qm"], "n_sc": c["n_sc"],
+            "n_sym": c["n_slots"] * synth.SYM_PER_SLOT, "sc_per_h": c["sc_per_h"], "llr_type": c["llr"]}
+
+
+def measured_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return dict(hbm_gbs=float(d["hbm_gbs"]), src="measured", sm_max_mhz=float(d.get("sm_max_mhz", 1965.0)))
+    return dict(hbm_gbs=FALLBACK_HBM_GBS, src="fallback", sm_max_mhz=1965.0)
+
+
+def ncu_traffic(k) -> float | None:
+    """dram read+write bytes per launch from the committed ncu --set full capture (profiles/)."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    v = d.get(synth.CONFIGS[k]["name"])
+    return float(v["dram_bytes_per_launch"]) if v else None
+
+
+# ----------------------------------------------------------------- clocks --
+class ClockSampler:
+    """Samples SM clock and clock-event reasons through NVML while running."""
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, torch_index: int, period: float = 0.05):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.period = period
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            import torch
+            uuid = str(torch.cuda.get_device_properties(torch_index).uuid)
+            h = None
+            for i in range(pynvml.nvmlDeviceGetCount()):
+                hh = pynvml.nvmlDeviceGetHandleByIndex(i)
+                u = pynvml.nvmlDeviceGetUUID(hh)
+                u = u.decode() if isinstance(u, bytes) else u
+                if u.replace("GPU-", "") == uuid.replace("GPU-", ""):
+                    h = hh
+            if h is None:
+                h = pynvml.nvmlDeviceGetHandleByIndex(torch_index)
+            self.h, self.nvml = h, pynvml
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # no NVML: report nothing rather than guess
+            self.err = repr(e)
+            self.max_mhz = None
+
+    def _run(self):
+        nv = self.nvml
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h) \
+                    if hasattr(nv, "nvmlDeviceGetCurrentClocksEventReasons") \
+                    else nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self._stop.set()
+            self._t.join()
+
+    def result(self) -> dict:
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "note": "NVML unavailable"}
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------ oracle legs --
+def oracle_rate(w: synth.Workload, seconds: float, threads: int) -> dict:
+    """Time the fp64 oracle (as it stands) on a bounded prefix of units, ~`seconds` of CPU work."""
+    import oracle
+    Hu = w.H_units()
+    Yall = synth.unit_gather(w.y, w.n_slots, w.n_sc, w.sc_per_h)
+    n = 1
+    while True:  # calibrate on a growing prefix, then size the sample
+        t0 = time.perf_counter()
+        oracle.detect(Hu[:n], Yall[:n], w.sigma2, w.qm, threads=threads)
+        dt = time.perf_counter() - t0
+        if dt > 0.2 or n >= w.n_units:
+            break
+        n = min(w.n_units, n * 8)
+    n_s = int(min(w.n_units, max(1, n * seconds / max(dt, 1e-6))))
+    t0 = time.perf_counter()
+    oracle.detect(Hu[:n_s], Yall[:n_s], w.sigma2, w.qm, threads=threads)
+    dt = time.perf_counter() - t0
+    n_re = n_s * synth.SYM_PER_SLOT * w.sc_per_h
+    return dict(value=n_re / dt, unit="RE/s", cores=threads, kind="oracle",
+                sample=f"first {n_s} of {w.n_units} H-units ({n_re} REs) of {w.name}, fp64 Gram/Cholesky + "
+                       f"brute-force max-log, OpenMP over units", seconds=dt)
+
+
+def run_reference(args, k):
+    """--impl reference: the fp64 oracle as the reference arm (rank 0 only)."""
+    import oracle
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    w = synth.generate(k)
+    threads = oracle.max_threads()
+    Hu = w.H_units()
+    Yall = synth.unit_gather(w.y, w.n_slots, w.n_sc, w.sc_per_h)
+    # per-step sample sized so that (W + K) steps take ~120 s in total
+    t0 = time.perf_counter()
+    oracle.detect(Hu[:64], Yall[:64], w.sigma2, w.qm, threads=threads)
+    per_unit = (time.perf_counter() - t0) / 64
+    budget = 120.0 / max(1, args.steps + args.warmup)
+    n_s = int(max(1, min(w.n_units, budget / max(per_unit, 1e-9))))
+    for i in range(args.warmup):
+        oracle.detect(Hu[:n_s], Yall[:n_s], w.sigma2, w.qm, threads=threads)
+    t0 = time.perf_counter()
+    for i in range(args.steps):
+        off = (i * n_s) % max(1, w.n_units - n_s + 1)
+        oracle.detect(Hu[off:off + n_s], Yall[off:off + n_s], w.sigma2, w.qm, threads=threads)
+    dt = time.perf_counter() - t0
+    n_re = n_s * synth.SYM_PER_SLOT * w.sc_per_h * args.steps
+    v = n_re / dt
+    c = synth.CONFIGS[k]
+    line = {"impl": "reference", "metric": METRIC, "value": v,
+            "unit": "RE/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE config shapes)",
+            "config": workload_desc(k),
+            "llr_gbit_s": v * c["n_layers"] * c["qm"] / 1e9,
+            "cpu_baseline": {"value": v, "unit": "RE/s", "cores": threads, "kind": "oracle",
+                             "sample": f"{n_s} H-units per step ({n_s * 14 * c['sc_per_h']} REs) of {c['name']}"},
+            "e2e": {"value": v, "unit": "RE/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# -------------------------------------------------------------- ours -------
+def largest_divisor_le(n: int, cap: int) -> int:
+    for d in range(min(n, cap), 0, -1):
+        if n % d == 0:
+            return d
+    return 1
+
+
+def run_ours(args, k):
+    import torch
+    import torch.distributed as dist
+    from paper_2510_07843_b200 import mimo
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    c = synth.CONFIGS[k]
+    base_seed = 1000 + (k if isinstance(k, int) else 0)
+    s0, s1 = shard.weak_slots(c["n_slots"], rank)
+    w = synth.generate(k, seed=shard.shard_seed(base_seed, rank))
+    b = synth.config_algorithmic_bytes(k)
+    plan = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, llr_dtype=w.llr, device=local)
+
+    # rotating buffer sets: working set >= 3x L2 so every step streams from HBM
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    n_sets = max(2, math.ceil(3 * l2 / b["total"]))
+    free = torch.cuda.mem_get_info(dev)[0]
+    n_sets = int(min(n_sets, max(2, (free * 0.5) // b["total"])))
+    H0 = torch.from_numpy(w.H).to(dev)
+    y0 = torch.from_numpy(w.y).to(dev)
+    sets = []
+    for i in range(n_sets):
+        sets.append((H0.clone(), y0.clone(),
+                     torch.empty(plan.shapes(w.n_sc, w.n_sym)["llr"], dtype=plan.llr_dtype, device=dev)))
+    del H0, y0
+    s2 = float(w.sigma2)
+    stream = torch.cuda.Stream(device=dev)
+
+    def step(i):
+        H, y, out = sets[i % n_sets]
+        plan.detect(H, y, s2, out=out)
+
+    if args.profile:
+        with torch.cuda.stream(stream):
+            for i in range(args.warmup + args.steps):
+                step(i)
+        torch.cuda.synchronize(dev)
+        assert plan.sync_status() == 0
+        if rank == 0:
+            print(json.dumps({"profile_run": True, "kernel": plan.kernel_name,
+                              "launches": args.warmup + args.steps}), flush=True)
+        return
+
+    # CUDA graph of S steps (S | K), replayed K/S times in the timed region
+    K, W = args.steps, max(3, args.warmup)
+    S = largest_divisor_le(K, 256)
+    with torch.cuda.stream(stream):
+        for i in range(3):       # eager warm-up (module load, first launches)
+            step(i)
+    stream.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        with torch.cuda.graph(g, stream=stream):
+            for i in range(S):
+                step(i)
+    stream.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    sampler = ClockSampler(local)
+    with sampler:
+        with torch.cuda.stream(stream):
+            # untimed warm-up: W steps, and at least ~0.3 s so clocks settle under load
+            t_end = time.perf_counter() + 0.3
+            done = 0
+            while done < W or time.perf_counter() < t_end:
+                g.replay()
+                done += S
+            stream.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        with torch.cuda.stream(stream):
+            ev0.record(stream)
+            for _ in range(K // S):
+                g.replay()
+            ev1.record(stream)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+    elapsed_ms = ev0.elapsed_time(ev1)
+    n_failed = plan.sync_status()
+    assert n_failed == 0, f"{n_failed} units failed the Cholesky guard"
+    t_max_ms = shard.max_over_ranks(elapsed_ms, device=dev)
+    n_re_all = b["n_re"] * K * world
+    value = n_re_all / (t_max_ms / 1e3)
+    per_launch_s = (elapsed_ms / 1e3) / (K * plan.launches_per_call)
+    peaks = measured_peaks()
+    achieved = b["total"] / per_launch_s / 1e9
+    clocks = sampler.result()
+
+    # e2e: host buffers through mimo_detect_mmse_host (H2D + kernel + D2H per step)
+    e2e = None
+    if not args.no_e2e:
+        Hh = torch.from_numpy(w.H).pin_memory()
+        yh = torch.from_numpy(w.y).pin_memory()
+        lh = torch.empty(plan.shapes(w.n_sc, w.n_sym)["llr"], dtype=plan.llr_dtype).pin_memory()
+        for _ in range(2):
+            plan.detect_host(Hh, yh, s2, out=lh)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            plan.detect_host(Hh, yh, s2, out=lh)
+        dt = time.perf_counter() - t0
+        dt = shard.max_over_ranks(dt, device=dev)
+        e2e = {"value": b["n_re"] * args.e2e_steps * world / dt, "unit": "RE/s",
+               "h2d_bytes_per_step": b["H"] + b["y"], "d2h_bytes_per_step": b["llr"],
+               "ms_per_step": dt * 1e3 / args.e2e_steps,
+               "path": "mimo_detect_mmse_host (pinned host buffers, 2-stream slot-chunk pipeline)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+        cpu = oracle_rate(w, args.cpu_seconds, oracle.max_threads())
+
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+    cfg = workload_desc(k)
+    cfg.update({"global_slots": c["n_slots"] * world, "slots_per_gpu": c["n_slots"],
+                "l2_flush": f"{n_sets} rotating buffer sets x {b['total'] / 1e6:.1f} MB = "
+                            f"{n_sets * b['total'] / 1e6:.0f} MB > 3x L2 ({l2 / 1e6:.0f} MB)",
+                "graph_steps": S, "kernel": plan.kernel_name,
+                "parallelism": f"slot-sharded x{world}, no collective" if world > 1 else "single GPU"})
+    line = {
+        "metric": METRIC,
+        "value": value, "unit": "RE/s", "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": t_max_ms / K, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "setup_dtype": "f64" if plan.kernel_name.startswith("tpu") else "f32",
+        "data": "synthetic (seeded numpy PCG64, BASELINE config shapes; DESIGN.md input recipe)",
+        "config": cfg,
+        "llr_gbit_s": value * w.n_layers * w.qm / 1e9,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / peaks["hbm_gbs"], "traffic": ncu_traffic(k),
+                     "algorithmic_bytes_per_launch": b["total"], "peak_src": peaks["src"],
+                     "kernel_us": per_launch_s * 1e6},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "clocks": clocks,
+        "gpu_launches": K * plan.launches_per_call,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    k = cfg_key(args.config)
+    if args.impl == "reference":
+        run_reference(args, k)
+    else:
+        run_ours(args, k)
+
+
+if __name__ == "__main__":
+    main()

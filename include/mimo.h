@@ -1,0 +1,154 @@
+/*
+ * mimo.h -- C ABI of the B200-native per-RE linear-MMSE MIMO detector and
+ * max-log soft demapper (hot path of arxiv 2510.07843, "Accelerating vRAN and
+ * O-RAN with SIMD", BASELINE.json north_star).
+ *
+ * The operation (§IV; Fig. 4 caption PAPER.md:93): for every
+ * resource element (RE) = (OFDM symbol, subcarrier) of a slot, detect the
+ * n_layers transmitted symbols from the n_rx received samples y with the LMMSE
+ * filter, "which involves inverting the received signal covariance matrix R".
+ * This library computes, per H-unit (one channel H shared by sym_per_h
+ * symbols x sc_per_h subcarriers; "one weight matrix per subcarrier per slot",
+ * SPEC.md:440):
+ *   a2  G = H^H H + sigma2 I                         (Gram form of R; reading R1)
+ *   a3  G = L L^H (Cholesky)                         (replaces the paper's LU; reading R2)
+ *   a4  A_kk = [G^-1]_kk,  W = G^-1 H^H = L^-H L^-1 H^H   (forward/backward substitution)
+ *   a5  mu_k = 1 - sigma2 A_kk,  SINR_k = 1/(sigma2 A_kk) - 1,  W~ = diag(1/mu) W   (readings R3, R4)
+ * and per RE:
+ *   a6  x~ = W~ y                                    (unbiased LMMSE estimate)
+ *   a7  exact max-log LLRs of the 38.211 Gray QAM labels (readings R5, R6):
+ *       LLR(b) = SINR_k * (min_{s: b=1} |x~_k - s|^2 - min_{s: b=0} |x~_k - s|^2) * llr_scale,
+ *       > 0 means bit 0; quantised to fp32 / fp16 / int8 (reading R10).
+ * Everything runs in hand-written sm_100a CUDA kernels; there is no CPU path.
+ *
+ * LAYOUTS (all row-major, complex = interleaved (re, im) float32 = complex64):
+ *   H        [n_sym/sym_per_h][n_sc/sc_per_h][n_rx][n_layers]  complex64 (row = rx antenna)
+ *   y        [n_sym][n_sc][n_rx]                               complex64
+ *   llr_out  [n_sym][n_sc][n_layers][qam_order]                llr_type; bit j = b_j of 38.211
+ *   xhat_out [n_sym][n_sc][n_layers]                           complex64 (unbiased x~; optional)
+ *   sinr_out [n_units][n_layers]                               float32   (optional)
+ * with n_units = (n_sym/sym_per_h) * (n_sc/sc_per_h), unit u = slot * n_fb + fb.
+ *
+ * OWNERSHIP: the caller owns every data buffer. A plan owns only its failure
+ * counter and (for mimo_detect_mmse_host) a device staging workspace. A plan
+ * must outlive all work it enqueued; mimo_plan_destroy synchronises first.
+ *
+ * ERRORS: no call throws. Argument problems are detected synchronously and
+ * return MIMO_ERR_INVALID_ARG without enqueuing anything. Kernel-side numerical
+ * failures (a Cholesky pivot p_j <= 16 * 2^-24 * max_i G_ii, or NaN; reading
+ * R17) never abort: the unit's outputs are written as erasures (LLR 0, x~ 0,
+ * SINR 0) and counted; mimo_plan_sync_status reports them as MIMO_ERR_NOT_PD.
+ *
+ * THREADING: a plan is not thread-safe; use one plan per (host thread, device).
+ * DETERMINISM: outputs are bitwise reproducible for identical inputs and plan
+ * (no floating-point atomics; fixed reduction order).
+ */
+#ifndef MIMO_H
+#define MIMO_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MIMO_ABI_VERSION 1
+
+typedef struct mimo_plan_s* mimo_plan_t;
+
+typedef enum {
+    MIMO_OK = 0,
+    MIMO_ERR_INVALID_ARG = 1, /* null / misaligned pointer, bad dims, dims != plan, sigma2 < 0 or NaN */
+    MIMO_ERR_UNSUPPORTED = 2, /* shape or modulation with no compiled kernel */
+    MIMO_ERR_CUDA = 3,        /* CUDA runtime error; text via mimo_plan_last_error / mimo_last_error */
+    MIMO_ERR_NOT_PD = 4,      /* >= 1 unit failed the Cholesky guard since the last sync_status */
+    MIMO_ERR_OOM = 5          /* host or device allocation failed */
+} mimo_status_t;
+
+typedef enum {
+    MIMO_LLR_F32 = 0, /* float32, saturating at +-FLT_MAX */
+    MIMO_LLR_F16 = 1, /* IEEE binary16, round-to-nearest-even, saturating at +-65504 */
+    MIMO_LLR_I8 = 2   /* int8, rint (half to even), saturating at +-127 (-128 unused) */
+} mimo_llr_type_t;
+
+typedef struct {
+    int device;      /* CUDA device ordinal the plan is bound to */
+    void* stream;    /* cudaStream_t to enqueue on (0 = legacy default stream) */
+    int n_rx;        /* receive antennas, 1..64 */
+    int n_layers;    /* spatial layers, 1..min(16, n_rx) */
+    int qam_order;   /* Qm = bits per symbol in {2,4,6,8} (QPSK..256-QAM), NOT M (reading R7) */
+    int sc_per_h;    /* subcarriers sharing one H: >= 1 (1 = per subcarrier, 12 = per PRB) */
+    int sym_per_h;   /* OFDM symbols sharing one H: >= 1 (14 = one H per slot) */
+    int llr_type;    /* mimo_llr_type_t */
+    float llr_scale; /* multiplier applied to natural-log LLRs before quantisation (> 0, finite) */
+} mimo_plan_desc_t;
+
+/* Create a plan: validates the descriptor, selects the kernel specialisation
+ * for (n_rx, n_layers, qam_order, sc_per_h, sym_per_h, llr_type), allocates the
+ * device failure counter on desc->device. *out_plan is set only on MIMO_OK.
+ * Errors: INVALID_ARG (null args, out-of-range fields), UNSUPPORTED, CUDA (no
+ * device / context creation failed), OOM. */
+mimo_status_t mimo_plan_create(const mimo_plan_desc_t* desc, mimo_plan_t* out_plan);
+
+/* Change the stream later calls enqueue on (e.g. torch's current stream). */
+mimo_status_t mimo_plan_set_stream(mimo_plan_t plan, void* stream);
+
+/* Detect all REs (north_star signature, with the plan as first argument).
+ * H, y, llr_out: DEVICE pointers on the plan's device, 16-byte aligned, in the
+ * layouts above. sigma2: total complex noise variance (CN(0, sigma2) per rx
+ * antenna), finite and >= 0; sigma2 = 0 is zero-forcing with SINR = +inf and
+ * saturated LLRs (reading R11). n_rx, n_layers, qam_order must equal the
+ * plan's; n_sc % sc_per_h == 0 and n_sym % sym_per_h == 0; n_sc, n_sym >= 0
+ * (0 REs is a no-op). Asynchronous: validates, enqueues one kernel on the plan's
+ * stream and returns. Errors: INVALID_ARG, CUDA (launch error). */
+mimo_status_t mimo_detect_mmse(mimo_plan_t plan, const void* H, const void* y, float sigma2,
+                               int n_rx, int n_layers, int n_sc, int n_sym, int qam_order,
+                               void* llr_out);
+
+/* As mimo_detect_mmse, plus optional debug outputs (either may be NULL):
+ * xhat_out complex64 [n_sym][n_sc][n_layers] (unbiased x~), sinr_out float32
+ * [n_units][n_layers] (post-equalisation SINR_k, +inf when sigma2 = 0). llr_out
+ * may be NULL when only the debug outputs are wanted. */
+mimo_status_t mimo_detect_mmse_ex(mimo_plan_t plan, const void* H, const void* y, float sigma2,
+                                  int n_rx, int n_layers, int n_sc, int n_sym, int qam_order,
+                                  void* llr_out, void* xhat_out, float* sinr_out);
+
+/* End-to-end form with HOST buffers (same layouts): copies H and y to a
+ * plan-owned device workspace, detects, copies the LLRs back, and returns after
+ * the stream has drained. Work is split into slot chunks pipelined over two
+ * streams so host->device, kernel and device->host overlap; pinned
+ * (page-locked) host buffers are required for overlap but not for correctness.
+ * Errors: as mimo_detect_mmse, plus OOM. */
+mimo_status_t mimo_detect_mmse_host(mimo_plan_t plan, const void* H_host, const void* y_host,
+                                    float sigma2, int n_rx, int n_layers, int n_sc, int n_sym,
+                                    int qam_order, void* llr_host);
+
+/* Synchronise the plan's stream, return the number of units flagged by the
+ * Cholesky guard since the previous call (and reset the count). Returns
+ * MIMO_ERR_NOT_PD if that number is > 0, MIMO_ERR_CUDA on a sticky CUDA
+ * error. n_failed_units may be NULL. */
+mimo_status_t mimo_plan_sync_status(mimo_plan_t plan, long long* n_failed_units);
+
+/* Synchronise and free the plan. NULL is a no-op returning MIMO_OK. */
+mimo_status_t mimo_plan_destroy(mimo_plan_t plan);
+
+/* Name of the kernel specialisation the plan launches (static string). */
+const char* mimo_plan_kernel_name(mimo_plan_t plan);
+
+/* Number of kernel launches one mimo_detect_mmse call enqueues. */
+int mimo_plan_launches_per_call(mimo_plan_t plan);
+
+/* Text of the last CUDA error seen by this plan ("" if none). */
+const char* mimo_plan_last_error(mimo_plan_t plan);
+
+/* Text of the last error seen by mimo_plan_create on this thread ("" if none). */
+const char* mimo_last_error(void);
+
+/* Static description of a status code. */
+const char* mimo_status_string(mimo_status_t status);
+
+/* MIMO_ABI_VERSION of the loaded library. */
+int mimo_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MIMO_H */

@@ -1,0 +1,252 @@
+// common.cuh -- device building blocks shared by the sm_100a detector kernels.
+//
+// Complex fp32/fp64 helpers, the exact per-axis max-log demapper (SURVEY.md
+// §8(a) row a7), saturating quantisers (reading R10), wide vector stores and
+// the mbarrier / cp.async.bulk wrappers used to stage y tiles in shared memory.
+// Nothing here is shared with oracle/ (DESIGN.md §"Oracle").
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mimo {
+
+constexpr int kLlrF32 = 0;
+constexpr int kLlrF16 = 1;
+constexpr int kLlrI8 = 2;
+
+// Reading R17: Cholesky guard p_j > kPivotTau * max_i G_ii, kPivotTau = 16 * 2^-24.
+constexpr double kPivotTau = 16.0 * 5.9604644775390625e-08;
+
+// Arguments of one detect call (plain pointers; layouts in include/mimo.h).
+struct DetectArgs {
+    const float2* H;      // [n_slots][n_fb][nr][nl]
+    const float2* y;      // [n_sym][n_sc][nr]
+    void* llr;            // [n_sym][n_sc][nl][qm] of llr_type (may be null)
+    float2* xhat;         // [n_sym][n_sc][nl] (may be null)
+    float* sinr;          // [n_units][nl] (may be null)
+    unsigned long long* fail_count;
+    float sigma2;
+    float llr_scale;
+    int n_rx, n_layers, qm;
+    int n_sc, n_sym;
+    int sc_per_h, sym_per_h;
+    int n_fb, n_slots;    // n_fb = n_sc / sc_per_h; n_slots = n_sym / sym_per_h
+    long long n_units;
+    int llr_type;
+};
+
+// Per-axis PAM normalisation of the 38.211 constellations: a = 1/sqrt(norm).
+__host__ __device__ constexpr int qam_norm(int qm) { return qm == 2 ? 2 : qm == 4 ? 10 : qm == 6 ? 42 : 170; }
+
+// ------------------------------------------------------------ complex ----
+__device__ __forceinline__ float2 cmac(float2 acc, float2 a, float2 b) {   // acc + a*b
+    acc.x = fmaf(a.x, b.x, acc.x);
+    acc.x = fmaf(-a.y, b.y, acc.x);
+    acc.y = fmaf(a.x, b.y, acc.y);
+    acc.y = fmaf(a.y, b.x, acc.y);
+    return acc;
+}
+__device__ __forceinline__ double2 dmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 dmac(double2 acc, double2 a, double2 b) {      // acc + a*b
+    acc.x = fma(a.x, b.x, acc.x);
+    acc.x = fma(-a.y, b.y, acc.x);
+    acc.y = fma(a.x, b.y, acc.y);
+    acc.y = fma(a.y, b.x, acc.y);
+    return acc;
+}
+__device__ __forceinline__ double2 dmacc(double2 acc, double2 a, double2 b) {     // acc + conj(a)*b
+    acc.x = fma(a.x, b.x, acc.x);
+    acc.x = fma(a.y, b.y, acc.x);
+    acc.y = fma(a.x, b.y, acc.y);
+    acc.y = fma(-a.y, b.x, acc.y);
+    return acc;
+}
+__device__ __forceinline__ double2 dsub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 dscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+__device__ __forceinline__ double dnorm2(double2 a) { return fma(a.x, a.x, a.y * a.y); }
+
+// ------------------------------------------------------------ demapper ----
+// Exact max-log per axis (equals brute force, pin P10).
+// u: equalised coordinate in PAM level units (levels at odd integers, i.e.
+// Re/Im(x~) * sqrt(norm)); slope = SINR * a^2 * llr_scale. Writes the LLRs of
+// the M bits on this axis (axis bit i is symbol bit 2i on I, 2i+1 on Q):
+//   s_q = clamp(2 floor(u/2) + 1, +-(2^M - 1)), e = u - s_q, D = e^2,
+//   t_0 = u, t_i = 2^(M-i) - |t_{i-1}|,
+//   LLR_i = sgn(t_i) * slope * ((|t_i| + 1)^2 - D)
+// with (|t|+1)^2 - D evaluated as (|t|+1-|e|)(|t|+1+|e|) (no cancellation).
+// slope = +inf (sigma2 = 0) and a zero distance gap give 0, not NaN (reading R11).
+template <int M>
+__device__ __forceinline__ void demap_axis(float u, float slope, float* out, int stride) {
+    constexpr float lim = float((1 << M) - 1);
+    const float sq = fminf(fmaxf(fmaf(2.f, floorf(0.5f * u), 1.f), -lim), lim);
+    const float ae = fabsf(u - sq);
+    float t = u;
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        if (i) t = float(1 << (M - i)) - fabsf(t);
+        const float at = fabsf(t) + 1.f;
+        const float mag = (at - ae) * (at + ae);
+        const float v = mag > 0.f ? slope * mag : 0.f;
+        out[i * stride] = copysignf(v, t);
+    }
+}
+
+// Demap one layer: x = x~ / a (level units), qm bits into out[0..QM).
+template <int QM>
+__device__ __forceinline__ void demap_layer(float2 x, float slope, float* out) {
+    demap_axis<QM / 2>(x.x, slope, out, 2);
+    demap_axis<QM / 2>(x.y, slope, out + 1, 2);
+}
+
+// ---------------------------------------------------------- quantisers ----
+// Reading R10: fp32 saturating at +-FLT_MAX; fp16 RNE saturating at +-65504;
+// int8 rint (half-even) saturating at +-127.
+__device__ __forceinline__ float sat_f32(float v) { return fminf(fmaxf(v, -3.402823466e38f), 3.402823466e38f); }
+__device__ __forceinline__ __half q_f16(float v) { return __float2half_rn(fminf(fmaxf(v, -65504.f), 65504.f)); }
+__device__ __forceinline__ int8_t q_i8(float v) { return (int8_t)__float2int_rn(fminf(fmaxf(v, -127.f), 127.f)); }
+
+template <int LT> struct LlrTraits;
+template <> struct LlrTraits<kLlrF32> { static constexpr int bytes = 4; };
+template <> struct LlrTraits<kLlrF16> { static constexpr int bytes = 2; };
+template <> struct LlrTraits<kLlrI8> { static constexpr int bytes = 1; };
+
+// Pack N float LLRs into little-endian 32-bit words of the output type.
+template <int LT, int N>
+__device__ __forceinline__ void pack_llr(const float* v, uint32_t* w) {
+    if constexpr (LT == kLlrF32) {
+#pragma unroll
+        for (int i = 0; i < N; ++i) w[i] = __float_as_uint(sat_f32(v[i]));
+    } else if constexpr (LT == kLlrF16) {
+#pragma unroll
+        for (int i = 0; i < (N + 1) / 2; ++i) {
+            const uint32_t lo = __half_as_ushort(q_f16(v[2 * i]));
+            const uint32_t hi = (2 * i + 1 < N) ? (uint32_t)__half_as_ushort(q_f16(v[2 * i + 1])) : 0u;
+            w[i] = lo | (hi << 16);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < (N + 3) / 4; ++i) {
+            uint32_t acc = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b)
+                if (4 * i + b < N) acc |= (uint32_t)(uint8_t)q_i8(v[4 * i + b]) << (8 * b);
+            w[i] = acc;
+        }
+    }
+}
+
+// ------------------------------------------------------- vector stores ----
+__device__ __forceinline__ void st_v8(void* p, const uint32_t* w) {
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+                 "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                 : "memory");
+}
+__device__ __forceinline__ void st_v4(void* p, const uint32_t* w) {
+    asm volatile("st.global.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
+                 : "memory");
+}
+__device__ __forceinline__ void st_v2(void* p, const uint32_t* w) {
+    asm volatile("st.global.v2.b32 [%0], {%1,%2};" ::"l"(p), "r"(w[0]), "r"(w[1]) : "memory");
+}
+__device__ __forceinline__ void st_v1(void* p, uint32_t w) {
+    asm volatile("st.global.b32 [%0], %1;" ::"l"(p), "r"(w) : "memory");
+}
+
+// Store NB bytes held in words w to p, with the widest vectors the byte count
+// and the (RE-stride-implied) alignment allow. p must be aligned to
+// min(32, largest power of two dividing NB).
+template <int NB>
+__device__ __forceinline__ void store_bytes(void* p, const uint32_t* w) {
+    if constexpr (NB % 32 == 0) {
+#pragma unroll
+        for (int i = 0; i < NB / 32; ++i) st_v8((char*)p + 32 * i, w + 8 * i);
+    } else if constexpr (NB % 16 == 0) {
+#pragma unroll
+        for (int i = 0; i < NB / 16; ++i) st_v4((char*)p + 16 * i, w + 4 * i);
+    } else if constexpr (NB % 8 == 0) {
+#pragma unroll
+        for (int i = 0; i < NB / 8; ++i) st_v2((char*)p + 8 * i, w + 2 * i);
+    } else if constexpr (NB % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < NB / 4; ++i) st_v1((char*)p + 4 * i, w[i]);
+    } else if constexpr (NB % 2 == 0) {
+#pragma unroll
+        for (int i = 0; i < NB / 2; ++i)
+            *(uint16_t*)((char*)p + 2 * i) = (uint16_t)(w[i / 2] >> (16 * (i & 1)));
+    } else {
+#pragma unroll
+        for (int i = 0; i < NB; ++i) *((uint8_t*)p + i) = (uint8_t)(w[i / 4] >> (8 * (i & 3)));
+    }
+}
+
+// 256-bit read-only global load (sm_100: LDG.E.ENL2.256).
+__device__ __forceinline__ void ld_v8(const void* p, uint32_t* w) {
+    asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+                 : "l"(p));
+}
+__device__ __forceinline__ void ld_v4(const void* p, uint32_t* w) {
+    asm volatile("ld.global.nc.v4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                 : "l"(p));
+}
+
+// Load NB bytes (NB % 16 == 0, p 16- or 32-aligned accordingly) into words.
+template <int NB>
+__device__ __forceinline__ void load_bytes(const void* p, uint32_t* w) {
+    static_assert(NB % 8 == 0, "load_bytes needs 8-byte multiples");
+    if constexpr (NB % 32 == 0) {
+#pragma unroll
+        for (int i = 0; i < NB / 32; ++i) ld_v8((const char*)p + 32 * i, w + 8 * i);
+    } else if constexpr (NB % 16 == 0) {
+#pragma unroll
+        for (int i = 0; i < NB / 16; ++i) ld_v4((const char*)p + 16 * i, w + 4 * i);
+    } else {
+#pragma unroll
+        for (int i = 0; i < NB / 8; ++i) {
+            uint2 v = __ldg((const uint2*)((const char*)p + 8 * i));
+            w[2 * i] = v.x;
+            w[2 * i + 1] = v.y;
+        }
+    }
+}
+
+// ------------------------------------------- mbarrier + bulk async copy ----
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// Global -> shared bulk copy (TMA unit, non-tensor): bytes % 16 == 0, both
+// addresses 16-byte aligned; completes `bytes` tx on bar.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+}  // namespace mimo

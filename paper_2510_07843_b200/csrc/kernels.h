@@ -1,0 +1,34 @@
+// kernels.h -- internal registry of the detector kernels (not part of the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+namespace mimo {
+
+using LaunchFn = cudaError_t (*)(const DetectArgs&, cudaStream_t);
+
+// A specialised kernel serves exactly one (n_rx, n_layers, qm, sc_per_h,
+// sym_per_h, llr_type) tuple; `align` is the byte alignment it needs of H, y,
+// llr and xhat (else the dispatcher falls back to the generic kernel).
+struct KernelEntry {
+    const char* name;
+    int n_rx, n_layers, qm, sc_per_h, sym_per_h, llr_type;
+    int align;
+    int launches;
+    LaunchFn launch;
+    // Optional: configure function attributes once at plan creation.
+    cudaError_t (*prepare)();
+};
+
+// Tables provided by each kernel family (k_*.cu).
+const KernelEntry* tpu_entries(int* n);
+
+// Generic kernel: any n_rx <= 64, n_layers <= min(16, n_rx), qm, sc_per_h,
+// sym_per_h, llr_type; 8-byte alignment.
+cudaError_t launch_generic(const DetectArgs& a, cudaStream_t s);
+constexpr int kGenericMaxRx = 64;
+constexpr int kGenericMaxLayers = 16;
+
+}  // namespace mimo

@@ -1,0 +1,351 @@
+// mimo_api.cu -- the C ABI of include/mimo.h: plan lifecycle, argument
+// validation, kernel dispatch and the host-buffer end-to-end path.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "kernels.h"
+#include "mimo.h"
+
+namespace {
+
+thread_local char g_last_error[512] = "";
+
+struct DeviceGuard {
+    int prev = -1;
+    cudaError_t err;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        err = cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+bool aligned(const void* p, size_t a) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+int llr_bytes(int t) { return t == mimo::kLlrF32 ? 4 : t == mimo::kLlrF16 ? 2 : 1; }
+
+}  // namespace
+
+struct mimo_plan_s {
+    mimo_plan_desc_t d{};
+    cudaStream_t stream = nullptr;
+    unsigned long long* d_fail = nullptr;
+    const mimo::KernelEntry* fast = nullptr;
+    char err[512] = "";
+    // mimo_detect_mmse_host staging
+    char* ws = nullptr;
+    size_t ws_bytes = 0;
+    cudaStream_t hs[2] = {nullptr, nullptr};
+    cudaEvent_t ev = nullptr;
+};
+
+namespace {
+
+mimo_status_t cuda_fail(mimo_plan_t p, cudaError_t e, const char* what) {
+    char* dst = p ? p->err : g_last_error;
+    snprintf(dst, 512, "%s: %s (%s)", what, cudaGetErrorString(e), cudaGetErrorName(e));
+    if (p) snprintf(g_last_error, sizeof(g_last_error), "%s", p->err);
+    return e == cudaErrorMemoryAllocation ? MIMO_ERR_OOM : MIMO_ERR_CUDA;
+}
+
+mimo_status_t arg_fail(mimo_plan_t p, const char* what) {
+    char* dst = p ? p->err : g_last_error;
+    snprintf(dst, 512, "invalid argument: %s", what);
+    return MIMO_ERR_INVALID_ARG;
+}
+
+const mimo::KernelEntry* select_fast(const mimo_plan_desc_t& d) {
+    using LF = const mimo::KernelEntry* (*)(int*);
+    const LF tables[] = {mimo::tpu_entries};
+    for (LF f : tables) {
+        int n = 0;
+        const mimo::KernelEntry* t = f(&n);
+        for (int i = 0; i < n; ++i)
+            if (t[i].n_rx == d.n_rx && t[i].n_layers == d.n_layers && t[i].qm == d.qam_order &&
+                t[i].sc_per_h == d.sc_per_h && t[i].sym_per_h == d.sym_per_h && t[i].llr_type == d.llr_type)
+                return &t[i];
+    }
+    return nullptr;
+}
+
+// Device-pointer sanity check: reject host pointers and pointers on another
+// device before a kernel could fault on them.
+bool is_device_ptr(const void* p, int dev) {
+    if (!p) return true;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) && at.device == dev;
+}
+
+mimo_status_t check_dims(mimo_plan_t p, float sigma2, int n_rx, int n_layers, int n_sc, int n_sym, int qm) {
+    if (n_rx != p->d.n_rx || n_layers != p->d.n_layers || qm != p->d.qam_order)
+        return arg_fail(p, "n_rx / n_layers / qam_order differ from the plan");
+    if (n_sc < 0 || n_sym < 0) return arg_fail(p, "n_sc and n_sym must be >= 0");
+    if (n_sc % p->d.sc_per_h) return arg_fail(p, "n_sc is not a multiple of sc_per_h");
+    if (n_sym % p->d.sym_per_h) return arg_fail(p, "n_sym is not a multiple of sym_per_h");
+    if (!(sigma2 >= 0.f) || !std::isfinite(sigma2)) return arg_fail(p, "sigma2 must be finite and >= 0");
+    return MIMO_OK;
+}
+
+mimo::DetectArgs make_args(mimo_plan_t p, const void* H, const void* y, float sigma2, int n_sc, int n_sym,
+                           void* llr, void* xhat, float* sinr) {
+    mimo::DetectArgs a{};
+    a.H = static_cast<const float2*>(H);
+    a.y = static_cast<const float2*>(y);
+    a.llr = llr;
+    a.xhat = static_cast<float2*>(xhat);
+    a.sinr = sinr;
+    a.fail_count = p->d_fail;
+    a.sigma2 = sigma2;
+    a.llr_scale = p->d.llr_scale;
+    a.n_rx = p->d.n_rx;
+    a.n_layers = p->d.n_layers;
+    a.qm = p->d.qam_order;
+    a.n_sc = n_sc;
+    a.n_sym = n_sym;
+    a.sc_per_h = p->d.sc_per_h;
+    a.sym_per_h = p->d.sym_per_h;
+    a.n_fb = n_sc / p->d.sc_per_h;
+    a.n_slots = n_sym / p->d.sym_per_h;
+    a.n_units = (long long)a.n_fb * a.n_slots;
+    a.llr_type = p->d.llr_type;
+    return a;
+}
+
+mimo_status_t launch(mimo_plan_t p, const mimo::DetectArgs& a, cudaStream_t s) {
+    if (a.n_units == 0) return MIMO_OK;
+    const mimo::KernelEntry* k = p->fast;
+    if (k) {
+        const size_t al = (size_t)k->align;
+        if (!aligned(a.H, al) || !aligned(a.y, al) || !aligned(a.llr, al) || !aligned(a.xhat, al)) k = nullptr;
+    }
+    cudaError_t e = k ? k->launch(a, s) : mimo::launch_generic(a, s);
+    if (e != cudaSuccess) return cuda_fail(p, e, k ? k->name : "generic");
+    return MIMO_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mimo_abi_version(void) { return MIMO_ABI_VERSION; }
+
+const char* mimo_status_string(mimo_status_t s) {
+    switch (s) {
+    case MIMO_OK: return "MIMO_OK";
+    case MIMO_ERR_INVALID_ARG: return "MIMO_ERR_INVALID_ARG: invalid argument";
+    case MIMO_ERR_UNSUPPORTED: return "MIMO_ERR_UNSUPPORTED: no kernel for this shape";
+    case MIMO_ERR_CUDA: return "MIMO_ERR_CUDA: CUDA runtime error";
+    case MIMO_ERR_NOT_PD: return "MIMO_ERR_NOT_PD: Gram matrix not positive definite for >= 1 unit";
+    case MIMO_ERR_OOM: return "MIMO_ERR_OOM: allocation failed";
+    }
+    return "unknown mimo_status_t";
+}
+
+const char* mimo_last_error(void) { return g_last_error; }
+
+const char* mimo_plan_last_error(mimo_plan_t p) { return p ? p->err : ""; }
+
+const char* mimo_plan_kernel_name(mimo_plan_t p) {
+    if (!p) return "";
+    return p->fast ? p->fast->name : "generic";
+}
+
+int mimo_plan_launches_per_call(mimo_plan_t p) {
+    if (!p) return 0;
+    return p->fast ? p->fast->launches : 1;
+}
+
+mimo_status_t mimo_plan_create(const mimo_plan_desc_t* desc, mimo_plan_t* out) {
+    g_last_error[0] = 0;
+    if (!desc || !out) return arg_fail(nullptr, "null descriptor or output");
+    const mimo_plan_desc_t& d = *desc;
+    if (d.n_rx < 1 || d.n_rx > mimo::kGenericMaxRx) return arg_fail(nullptr, "n_rx must be in 1..64");
+    if (d.n_layers < 1 || d.n_layers > d.n_rx || d.n_layers > mimo::kGenericMaxLayers)
+        return arg_fail(nullptr, "n_layers must be in 1..min(16, n_rx)");
+    if (d.qam_order != 2 && d.qam_order != 4 && d.qam_order != 6 && d.qam_order != 8)
+        return arg_fail(nullptr, "qam_order must be Qm in {2,4,6,8}");
+    if (d.sc_per_h < 1 || d.sym_per_h < 1) return arg_fail(nullptr, "sc_per_h and sym_per_h must be >= 1");
+    if (d.llr_type < 0 || d.llr_type > 2) return arg_fail(nullptr, "llr_type must be 0, 1 or 2");
+    if (!(d.llr_scale > 0.f) || !std::isfinite(d.llr_scale)) return arg_fail(nullptr, "llr_scale must be finite > 0");
+    if (d.device < 0) return arg_fail(nullptr, "device must be >= 0");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return cuda_fail(nullptr, e, "cudaGetDeviceCount");
+    }
+    if (d.device >= ndev) return arg_fail(nullptr, "device ordinal out of range");
+    DeviceGuard g(d.device);
+    if (g.err != cudaSuccess) return cuda_fail(nullptr, g.err, "cudaSetDevice");
+
+    mimo_plan_t p = new (std::nothrow) mimo_plan_s;
+    if (!p) return MIMO_ERR_OOM;
+    p->d = d;
+    p->stream = static_cast<cudaStream_t>(d.stream);
+    p->fast = select_fast(d);
+    if (p->fast && p->fast->prepare) {
+        e = p->fast->prepare();
+        if (e != cudaSuccess) {
+            mimo_status_t st = cuda_fail(nullptr, e, "kernel prepare");
+            delete p;
+            return st;
+        }
+    }
+    e = cudaMalloc(&p->d_fail, sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMemset(p->d_fail, 0, sizeof(unsigned long long));
+    if (e != cudaSuccess) {
+        mimo_status_t st = cuda_fail(nullptr, e, "cudaMalloc(fail counter)");
+        if (p->d_fail) cudaFree(p->d_fail);
+        delete p;
+        return st;
+    }
+    *out = p;
+    return MIMO_OK;
+}
+
+mimo_status_t mimo_plan_set_stream(mimo_plan_t p, void* stream) {
+    if (!p) return arg_fail(nullptr, "null plan");
+    p->stream = static_cast<cudaStream_t>(stream);
+    return MIMO_OK;
+}
+
+mimo_status_t mimo_detect_mmse_ex(mimo_plan_t p, const void* H, const void* y, float sigma2, int n_rx,
+                                  int n_layers, int n_sc, int n_sym, int qm, void* llr_out, void* xhat_out,
+                                  float* sinr_out) {
+    if (!p) return arg_fail(nullptr, "null plan");
+    mimo_status_t st = check_dims(p, sigma2, n_rx, n_layers, n_sc, n_sym, qm);
+    if (st != MIMO_OK) return st;
+    if ((long long)n_sc * n_sym == 0) return MIMO_OK;
+    if (!H || !y) return arg_fail(p, "null H or y");
+    if (!llr_out && !xhat_out && !sinr_out) return arg_fail(p, "no output requested");
+    if (!aligned(H, 16) || !aligned(y, 16) || !aligned(llr_out, 16) || !aligned(xhat_out, 16) ||
+        !aligned(sinr_out, 4))
+        return arg_fail(p, "pointer not 16-byte aligned");
+    const int dev = p->d.device;
+    if (!is_device_ptr(H, dev) || !is_device_ptr(y, dev) || !is_device_ptr(llr_out, dev) ||
+        !is_device_ptr(xhat_out, dev) || !is_device_ptr(sinr_out, dev))
+        return arg_fail(p, "pointer is not device memory on the plan's device");
+    DeviceGuard g(dev);
+    if (g.err != cudaSuccess) return cuda_fail(p, g.err, "cudaSetDevice");
+    mimo::DetectArgs a = make_args(p, H, y, sigma2, n_sc, n_sym, llr_out, xhat_out, sinr_out);
+    return launch(p, a, p->stream);
+}
+
+mimo_status_t mimo_detect_mmse(mimo_plan_t p, const void* H, const void* y, float sigma2, int n_rx, int n_layers,
+                               int n_sc, int n_sym, int qm, void* llr_out) {
+    if (p && (long long)n_sc * n_sym > 0 && !llr_out) return arg_fail(p, "null llr_out");
+    return mimo_detect_mmse_ex(p, H, y, sigma2, n_rx, n_layers, n_sc, n_sym, qm, llr_out, nullptr, nullptr);
+}
+
+mimo_status_t mimo_detect_mmse_host(mimo_plan_t p, const void* H_host, const void* y_host, float sigma2, int n_rx,
+                                    int n_layers, int n_sc, int n_sym, int qm, void* llr_host) {
+    if (!p) return arg_fail(nullptr, "null plan");
+    mimo_status_t st = check_dims(p, sigma2, n_rx, n_layers, n_sc, n_sym, qm);
+    if (st != MIMO_OK) return st;
+    if ((long long)n_sc * n_sym == 0) return MIMO_OK;
+    if (!H_host || !y_host || !llr_host) return arg_fail(p, "null host buffer");
+    DeviceGuard g(p->d.device);
+    if (g.err != cudaSuccess) return cuda_fail(p, g.err, "cudaSetDevice");
+
+    const int symph = p->d.sym_per_h;
+    const int n_slots = n_sym / symph;
+    const int n_fb = n_sc / p->d.sc_per_h;
+    const size_t h_slot = (size_t)n_fb * n_rx * n_layers * 8;
+    const size_t y_slot = (size_t)symph * n_sc * n_rx * 8;
+    const size_t l_slot = (size_t)symph * n_sc * n_layers * qm * llr_bytes(p->d.llr_type);
+    // ~4 MiB of input per chunk: large enough to amortise launch + copy
+    // latency, small enough that H2D, kernel and D2H of neighbours overlap.
+    int cs = (int)((4u << 20) / (h_slot + y_slot));
+    if (cs < 1) cs = 1;
+    if (cs > n_slots) cs = n_slots;
+    auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    const size_t bh = up(h_slot * cs), by = up(y_slot * cs), bl = up(l_slot * cs);
+    const size_t need = 2 * (bh + by + bl);
+    cudaError_t e;
+    if (p->ws_bytes < need) {
+        if (p->ws) {
+            cudaStreamSynchronize(p->hs[0]);
+            cudaStreamSynchronize(p->hs[1]);
+            cudaFree(p->ws);
+            p->ws = nullptr;
+            p->ws_bytes = 0;
+        }
+        e = cudaMalloc(&p->ws, need);
+        if (e != cudaSuccess) return cuda_fail(p, e, "cudaMalloc(host-path workspace)");
+        p->ws_bytes = need;
+    }
+    for (int i = 0; i < 2; ++i)
+        if (!p->hs[i] && (e = cudaStreamCreateWithFlags(&p->hs[i], cudaStreamNonBlocking)) != cudaSuccess)
+            return cuda_fail(p, e, "cudaStreamCreate");
+    if (!p->ev && (e = cudaEventCreateWithFlags(&p->ev, cudaEventDisableTiming)) != cudaSuccess)
+        return cuda_fail(p, e, "cudaEventCreate");
+    // order after work already enqueued on the plan's stream
+    if ((e = cudaEventRecord(p->ev, p->stream)) != cudaSuccess) return cuda_fail(p, e, "cudaEventRecord");
+    for (int i = 0; i < 2; ++i) cudaStreamWaitEvent(p->hs[i], p->ev, 0);
+
+    int chunk = 0;
+    for (int s0 = 0; s0 < n_slots; s0 += cs, ++chunk) {
+        const int ns = (n_slots - s0) < cs ? (n_slots - s0) : cs;
+        const int b = chunk & 1;
+        cudaStream_t s = p->hs[b];
+        char* base = p->ws + (size_t)b * (bh + by + bl);
+        char *dH = base, *dy = base + bh, *dl = base + bh + by;
+        e = cudaMemcpyAsync(dH, (const char*)H_host + h_slot * s0, h_slot * ns, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(dy, (const char*)y_host + y_slot * s0, y_slot * ns, cudaMemcpyHostToDevice, s);
+        if (e != cudaSuccess) return cuda_fail(p, e, "cudaMemcpyAsync H2D");
+        mimo::DetectArgs a = make_args(p, dH, dy, sigma2, n_sc, ns * symph, dl, nullptr, nullptr);
+        st = launch(p, a, s);
+        if (st != MIMO_OK) return st;
+        e = cudaMemcpyAsync((char*)llr_host + l_slot * s0, dl, l_slot * ns, cudaMemcpyDeviceToHost, s);
+        if (e != cudaSuccess) return cuda_fail(p, e, "cudaMemcpyAsync D2H");
+    }
+    for (int i = 0; i < 2; ++i)
+        if ((e = cudaStreamSynchronize(p->hs[i])) != cudaSuccess) return cuda_fail(p, e, "cudaStreamSynchronize");
+    return MIMO_OK;
+}
+
+mimo_status_t mimo_plan_sync_status(mimo_plan_t p, long long* n_failed) {
+    if (n_failed) *n_failed = 0;
+    if (!p) return arg_fail(nullptr, "null plan");
+    DeviceGuard g(p->d.device);
+    if (g.err != cudaSuccess) return cuda_fail(p, g.err, "cudaSetDevice");
+    unsigned long long h = 0;
+    cudaError_t e = cudaStreamSynchronize(p->stream);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i)
+        if (p->hs[i]) e = cudaStreamSynchronize(p->hs[i]);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h, p->d_fail, sizeof(h), cudaMemcpyDeviceToHost, p->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p->d_fail, 0, sizeof(h), p->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(p->stream);
+    if (e != cudaSuccess) return cuda_fail(p, e, "sync_status");
+    if (n_failed) *n_failed = (long long)h;
+    return h ? MIMO_ERR_NOT_PD : MIMO_OK;
+}
+
+mimo_status_t mimo_plan_destroy(mimo_plan_t p) {
+    if (!p) return MIMO_OK;
+    {
+        DeviceGuard g(p->d.device);
+        cudaStreamSynchronize(p->stream);
+        for (int i = 0; i < 2; ++i)
+            if (p->hs[i]) {
+                cudaStreamSynchronize(p->hs[i]);
+                cudaStreamDestroy(p->hs[i]);
+            }
+        if (p->ev) cudaEventDestroy(p->ev);
+        if (p->ws) cudaFree(p->ws);
+        if (p->d_fail) cudaFree(p->d_fail);
+    }
+    delete p;
+    return MIMO_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,123 @@
+"""C-ABI error behaviour with a device present (include/mimo.h ERRORS)."""
+import ctypes
+
+import numpy as np
+import pytest
+
+from paper_2510_07843_b200 import mimo, synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture()
+def setup():
+    import torch
+    w = synth.generate(2, n_sc=32, n_slots=1)
+    plan = mimo.Plan(4, 4, 4)
+    H = torch.from_numpy(w.H).cuda()
+    y = torch.from_numpy(w.y).cuda()
+    out = torch.empty((14, 32, 4, 4), dtype=torch.float32, device="cuda")
+    yield plan, H, y, out, w
+    plan.close()
+
+
+def _call(plan, H, y, out, sigma2=0.1, nr=4, nl=4, nsc=32, nsym=14, qm=4):
+    p = lambda t: ctypes.c_void_p(t if isinstance(t, int) else t.data_ptr()) if t is not None else None
+    return plan._lib.mimo_detect_mmse(plan._h, p(H), p(y), ctypes.c_float(sigma2), nr, nl, nsc, nsym, qm, p(out))
+
+
+def test_ok(setup):
+    plan, H, y, out, _ = setup
+    assert _call(plan, H, y, out) == mimo.MIMO_OK
+    assert plan.sync_status() == 0
+
+
+@pytest.mark.parametrize("kw", [dict(nr=2), dict(nl=2), dict(qm=6), dict(nsc=-1), dict(nsym=13),
+                                dict(sigma2=-0.1), dict(sigma2=float("nan")), dict(sigma2=float("inf"))])
+def test_invalid_dims(setup, kw):
+    plan, H, y, out, _ = setup
+    assert _call(plan, H, y, out, **kw) == mimo.MIMO_ERR_INVALID_ARG
+    assert plan._lib.mimo_plan_last_error(plan._h)
+
+
+def test_null_and_misaligned(setup):
+    plan, H, y, out, _ = setup
+    assert _call(plan, None, y, out) == mimo.MIMO_ERR_INVALID_ARG
+    assert _call(plan, H, y, None) == mimo.MIMO_ERR_INVALID_ARG
+    assert _call(plan, H, y.data_ptr() + 8, out) == mimo.MIMO_ERR_INVALID_ARG
+
+
+def test_host_pointer_rejected(setup):
+    plan, H, y, out, w = setup
+    host = np.zeros(w.y.size, np.complex64)
+    assert _call(plan, H, host.ctypes.data, out) == mimo.MIMO_ERR_INVALID_ARG
+
+
+def test_python_shape_checks(setup):
+    import torch
+    plan, H, y, out, _ = setup
+    with pytest.raises(ValueError):
+        plan.detect(H.cpu(), y, 0.1)
+    with pytest.raises(ValueError):
+        plan.detect(H, y.to(torch.complex128), 0.1)
+    with pytest.raises(mimo.MimoError):
+        plan.detect(H, y, -1.0)
+
+
+def test_sync_status_counts_and_resets():
+    import torch
+    w = synth.generate(2, n_sc=32, n_slots=1, sigma2=0.0)
+    H = w.H.copy()
+    H[0, 1, :, 0] = 0
+    plan = mimo.Plan(4, 4, 4)
+    Hd, yd = torch.from_numpy(H).cuda(), torch.from_numpy(w.y).cuda()
+    plan.detect(Hd, yd, 0.0)
+    plan.detect(Hd, yd, 0.0)
+    assert plan.sync_status() == 2
+    assert plan.sync_status() == 0
+    st = plan._lib.mimo_plan_sync_status(plan._h, None)
+    assert st == mimo.MIMO_OK
+
+
+def test_kernel_selection():
+    assert mimo.Plan(4, 4, 4).kernel_name.startswith("tpu_4x4")
+    assert mimo.Plan(2, 2, 2).kernel_name.startswith("tpu_2x2")
+    assert mimo.Plan(7, 3, 4).kernel_name == "generic"
+    assert mimo.Plan(4, 4, 4).launches_per_call == 1
+
+
+def test_stream_ordering():
+    """Work goes on torch's current stream: results are ready after that stream syncs."""
+    import torch
+    w = synth.generate(2, n_sc=64, n_slots=2)
+    plan = mimo.Plan(4, 4, 4)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        H = torch.from_numpy(w.H).cuda()
+        y = torch.from_numpy(w.y).cuda()
+        out = plan.detect(H, y, float(w.sigma2))
+    s.synchronize()
+    ref = plan.detect(H, y, float(w.sigma2))
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)
+
+
+def test_cuda_graph_capture():
+    import torch
+    w = synth.generate(2, n_sc=64, n_slots=2)
+    plan = mimo.Plan(4, 4, 4)
+    H = torch.from_numpy(w.H).cuda()
+    y = torch.from_numpy(w.y).cuda()
+    out = torch.empty((28, 64, 4, 4), device="cuda")
+    ref = plan.detect(H, y, float(w.sigma2)).clone()
+    g = torch.cuda.CUDAGraph()
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        with torch.cuda.graph(g, stream=s):
+            plan.detect(H, y, float(w.sigma2), out=out)
+    torch.cuda.current_stream().wait_stream(s)
+    out.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, ref)

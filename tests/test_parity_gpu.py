@@ -1,0 +1,192 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the
+same seeded inputs, element by element, with the north_star tolerances
+(tests/parity.py). Small sizes span several tiles and a ragged tail; full
+BASELINE sizes are checked on sampled H-units in the bench's launch config."""
+import numpy as np
+import pytest
+
+import parity
+from paper_2510_07843_b200 import synth
+
+pytestmark = pytest.mark.gpu
+
+# reduced shapes: several CTA tiles plus a ragged tail (300 = 9*32 + 12 subcarriers)
+SMALL = {1: dict(), 2: dict(n_sc=300, n_slots=2), 3: dict(n_sc=300, n_slots=2),
+         4: dict(n_sc=300, n_slots=2), 5: dict(n_sc=120, n_slots=1)}
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+def test_config_small_all_outputs(k):
+    w = synth.generate(k, **SMALL[k])
+    g = parity.run_gpu(w)
+    assert g["n_failed"] == 0
+    rep = parity.compare(w, g)
+    print(k, g["kernel"], rep)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+def test_config_full_size_sampled(k):
+    """Full BASELINE size, same launch config as bench.py, oracle on sampled units."""
+    w = synth.generate(k)
+    g = parity.run_gpu(w, xhat=(k != 5), sinr=True)
+    assert g["n_failed"] == 0
+    rng = np.random.default_rng(100 + k)
+    n = min(w.n_units, 400 if k != 5 else 60)
+    units = np.unique(np.concatenate([[0, w.n_units - 1, w.n_fb - 1], rng.choice(w.n_units, n, replace=False)]))
+    rep = parity.compare(w, g, units)
+    # properties that hold at any size: finite outputs everywhere
+    assert np.all(np.isfinite(g["llr"].astype(np.float64)))
+    assert np.all(np.isfinite(g["sinr"])) and np.all(g["sinr"] > 0)
+    print(k, g["kernel"], rep)
+
+
+SHAPES = [(1, 1, 2, 1, "f32"), (2, 1, 4, 1, "f16"), (2, 2, 2, 1, "i8"), (2, 2, 8, 12, "f32"),
+          (3, 2, 6, 1, "f32"), (4, 2, 4, 1, "f32"), (4, 4, 6, 12, "i8"), (4, 4, 8, 1, "f16"),
+          (8, 8, 4, 1, "f32"), (8, 2, 2, 12, "f16"), (16, 4, 6, 1, "i8"), (16, 16, 2, 12, "f32"),
+          (32, 8, 8, 12, "f32"), (64, 1, 4, 1, "f32"), (64, 8, 6, 12, "i8"), (5, 3, 4, 12, "f32")]
+
+
+@pytest.mark.parametrize("nr,nl,qm,scph,llr", SHAPES)
+def test_random_shapes(nr, nl, qm, scph, llr):
+    cfg = dict(name="rand", n_rx=nr, n_layers=nl, qm=qm, n_sc=scph * 7, n_slots=2, sc_per_h=scph,
+               channel="iid", chan_var=1.0 / nr, snr_db=18.0, llr=llr)
+    w = synth.generate(cfg, seed=nr * 1000 + nl * 100 + qm * 10 + scph)
+    g = parity.run_gpu(w)
+    parity.compare(w, g)
+
+
+@pytest.mark.parametrize("qm", [2, 4, 6, 8])
+def test_all_qm_on_fast_4x4(qm):
+    cfg = dict(synth.CONFIGS[2], n_sc=100, n_slots=1, qm=qm)
+    w = synth.generate(cfg, seed=77)
+    g = parity.run_gpu(w)
+    assert g["kernel"].startswith("tpu")
+    parity.compare(w, g)
+
+
+def test_sigma2_zero_is_zero_forcing():
+    w = synth.generate(2, n_sc=64, n_slots=1, sigma2=0.0)
+    g = parity.run_gpu(w)
+    assert np.all(np.isinf(g["sinr"]))
+    # noisy y at sigma2=0 is fine: ZF x~ = H^-1 y; LLRs saturate at +-FLT_MAX (reading R11)
+    rep = parity.compare(w, g)
+    assert np.all(np.abs(g["llr"]) == np.finfo(np.float32).max)
+    print(rep)
+
+
+@pytest.mark.parametrize("k", [2, 3])
+def test_noiseless_exact_bits(k):
+    """Noiseless identity / unitary channels: hard bits equal the transmitted bits."""
+    cfg = dict(synth.CONFIGS[k], n_sc=48, n_slots=1)
+    nr, nl = cfg["n_rx"], cfg["n_layers"]
+    rng = np.random.default_rng(1)
+    for H0 in (np.eye(nr, nl), np.linalg.qr(rng.standard_normal((nr, nr)) + 1j * rng.standard_normal((nr, nr)))[0][:, :nl]):
+        w = synth.generate(cfg, H_override=H0, noiseless=True)
+        g = parity.run_gpu(w)
+        hard = (g["llr"] < 0).astype(np.uint8)
+        assert np.array_equal(hard, w.bits)
+
+
+def test_rank_deficient_units_flagged():
+    w = synth.generate(2, n_sc=40, n_slots=1, sigma2=0.0)
+    H = w.H.copy()
+    H[0, 3, :, 2] = 0                    # zero column -> pivot exactly 0
+    H[0, 7, :, 1] = H[0, 7, :, 0]        # duplicate column
+    g = parity.run_gpu(w, H=H)
+    assert g["n_failed"] == 2
+    for u in (3, 7):
+        s, f = synth.unit_re_index(u, w.n_sc, 1)
+        assert np.all(g["llr"][s, f] == 0) and np.all(g["xhat"][s, f] == 0) and np.all(g["sinr"][u] == 0)
+    ok = [u for u in range(w.n_units) if u not in (3, 7)]
+    parity.compare(w, g, ok, H=H)
+
+
+def test_zero_column_erasure_sigma_positive():
+    w = synth.generate(2, n_sc=40, n_slots=1)
+    H = w.H.copy()
+    H[0, 5, :, 1] = 0
+    g = parity.run_gpu(w, H=H)
+    assert g["n_failed"] == 0
+    s, f = synth.unit_re_index(5, w.n_sc, 1)
+    assert np.all(g["llr"][s, f, 1] == 0)
+    parity.compare(w, g, H=H)
+
+
+def test_nan_input_flagged():
+    w = synth.generate(2, n_sc=40, n_slots=1)
+    H = w.H.copy()
+    H[0, 2, 1, 1] = np.nan
+    g = parity.run_gpu(w, H=H)
+    assert g["n_failed"] == 1
+    s, f = synth.unit_re_index(2, w.n_sc, 1)
+    assert np.all(g["llr"][s, f] == 0)
+
+
+@pytest.mark.parametrize("k", [2, 3, 4])
+def test_power_of_two_scaling_bit_identical(k):
+    w = synth.generate(k, n_sc=96, n_slots=1)
+    g1 = parity.run_gpu(w)
+    w2 = synth.generate(k, n_sc=96, n_slots=1)
+    w2.sigma2 = np.float32(4 * w.sigma2)
+    g2 = parity.run_gpu(w2, H=2 * w.H, y=2 * w.y)
+    assert np.array_equal(g1["llr"], g2["llr"])
+    assert np.array_equal(g1["sinr"], g2["sinr"])
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+def test_deterministic(k):
+    w = synth.generate(k, **SMALL[k])
+    a, b = parity.run_gpu(w), parity.run_gpu(w)
+    assert np.array_equal(a["llr"], b["llr"]) and np.array_equal(a["xhat"], b["xhat"])
+
+
+def test_llr_scale():
+    w = synth.generate(3, n_sc=60, n_slots=1)
+    g = parity.run_gpu(w, llr_scale=0.25)
+    parity.compare(w, g, llr_scale=0.25)
+
+
+def test_misaligned_pointers_use_generic_path():
+    """A 16-B-aligned but not 32-B-aligned y falls back to the generic kernel, same results."""
+    import torch
+    from paper_2510_07843_b200 import mimo
+    w = synth.generate(2, n_sc=64, n_slots=1)
+    plan = mimo.Plan(4, 4, 4)
+    Hd = torch.from_numpy(w.H).cuda()
+    ybuf = torch.zeros(w.y.size + 2, dtype=torch.complex64, device="cuda")
+    ybuf[2:] = torch.from_numpy(w.y.ravel()).cuda()
+    yv = ybuf[2:].view(w.y.shape)  # +16 bytes
+    out = plan.detect(Hd, yv, float(w.sigma2))
+    ref = plan.detect(Hd, torch.from_numpy(w.y).cuda(), float(w.sigma2))
+    assert torch.equal(out, ref) or torch.allclose(out, ref, rtol=1e-5, atol=1e-5)
+    g = dict(llr=out.cpu().numpy())
+    parity.compare(w, g)
+
+
+def test_empty_input_is_noop():
+    import torch
+    from paper_2510_07843_b200 import mimo
+    plan = mimo.Plan(4, 4, 4)
+    H = torch.zeros((0, 0, 4, 4), dtype=torch.complex64, device="cuda")
+    y = torch.zeros((0, 0, 4), dtype=torch.complex64, device="cuda")
+    out = plan.detect(H, y, 0.1)
+    assert out.numel() == 0
+    assert plan.sync_status() == 0
+
+
+def test_host_path_matches_device_path():
+    w = synth.generate(2, n_sc=3276, n_slots=10)
+    g = parity.run_gpu(w, xhat=False, sinr=False)
+    from paper_2510_07843_b200 import mimo
+    plan = mimo.Plan(4, 4, 4)
+    out = plan.detect_host(w.H, w.y, float(w.sigma2))
+    assert np.array_equal(out, g["llr"])
+
+
+def test_host_path_c5_chunked():
+    w = synth.generate(5, n_slots=6)
+    g = parity.run_gpu(w, xhat=False, sinr=False)
+    from paper_2510_07843_b200 import mimo
+    plan = mimo.Plan(64, 16, 6, sc_per_h=12, llr_dtype="i8")
+    out = plan.detect_host(w.H, w.y, float(w.sigma2))
+    assert np.array_equal(out, g["llr"])
