@@ -74,32 +74,36 @@ __device__ __forceinline__ double dnorm2(double2 a) { return fma(a.x, a.x, a.y *
 // u: equalised coordinate in PAM level units (levels at odd integers, i.e.
 // Re/Im(x~) * sqrt(norm)); slope = SINR * a^2 * llr_scale. Writes the LLRs of
 // the M bits on this axis (axis bit i is symbol bit 2i on I, 2i+1 on Q):
-//   s_q = clamp(2 floor(u/2) + 1, +-(2^M - 1)), e = u - s_q, D = e^2,
+//   s_q = clamp(2 floor(u/2) + 1, +-(2^M - 1)), D = (u - s_q)^2,
 //   t_0 = u, t_i = 2^(M-i) - |t_{i-1}|,
 //   LLR_i = sgn(t_i) * slope * ((|t_i| + 1)^2 - D)
-// with (|t|+1)^2 - D evaluated as (|t|+1-|e|)(|t|+1+|e|) (no cancellation).
-// slope = +inf (sigma2 = 0) and a zero distance gap give 0, not NaN (reading R11).
-template <int M>
+// (|t|+1)^2 - D is one FMA, i.e. exactly rounded apart from D's own rounding.
+// ZF = true is the sigma2 = 0 variant (reading R11): slope = +inf, a zero
+// distance gap gives 0 instead of NaN, and the caller saturates.
+template <int M, bool ZF>
 __device__ __forceinline__ void demap_axis(float u, float slope, float* out, int stride) {
     constexpr float lim = float((1 << M) - 1);
     const float sq = fminf(fmaxf(fmaf(2.f, floorf(0.5f * u), 1.f), -lim), lim);
-    const float ae = fabsf(u - sq);
+    const float e = u - sq;
+    const float D = e * e;
     float t = u;
 #pragma unroll
     for (int i = 0; i < M; ++i) {
         if (i) t = float(1 << (M - i)) - fabsf(t);
         const float at = fabsf(t) + 1.f;
-        const float mag = (at - ae) * (at + ae);
-        const float v = mag > 0.f ? slope * mag : 0.f;
+        const float mag = fmaf(at, at, -D);
+        float v;
+        if constexpr (ZF) v = mag > 0.f ? slope * mag : 0.f;
+        else v = slope * mag;
         out[i * stride] = copysignf(v, t);
     }
 }
 
 // Demap one layer: x = x~ / a (level units), qm bits into out[0..QM).
-template <int QM>
+template <int QM, bool ZF = false>
 __device__ __forceinline__ void demap_layer(float2 x, float slope, float* out) {
-    demap_axis<QM / 2>(x.x, slope, out, 2);
-    demap_axis<QM / 2>(x.y, slope, out + 1, 2);
+    demap_axis<QM / 2, ZF>(x.x, slope, out, 2);
+    demap_axis<QM / 2, ZF>(x.y, slope, out + 1, 2);
 }
 
 // ---------------------------------------------------------- quantisers ----
@@ -115,11 +119,13 @@ template <> struct LlrTraits<kLlrF16> { static constexpr int bytes = 2; };
 template <> struct LlrTraits<kLlrI8> { static constexpr int bytes = 1; };
 
 // Pack N float LLRs into little-endian 32-bit words of the output type.
-template <int LT, int N>
+// SAT: saturate fp32 at +-FLT_MAX (only needed when slopes can be infinite,
+// i.e. sigma2 = 0); fp16 / int8 always saturate.
+template <int LT, int N, bool SAT = true>
 __device__ __forceinline__ void pack_llr(const float* v, uint32_t* w) {
     if constexpr (LT == kLlrF32) {
 #pragma unroll
-        for (int i = 0; i < N; ++i) w[i] = __float_as_uint(sat_f32(v[i]));
+        for (int i = 0; i < N; ++i) w[i] = __float_as_uint(SAT ? sat_f32(v[i]) : v[i]);
     } else if constexpr (LT == kLlrF16) {
 #pragma unroll
         for (int i = 0; i < (N + 1) / 2; ++i) {

@@ -42,7 +42,7 @@ __device__ __forceinline__ void store_layer_llr(void* llr, size_t idx, const flo
     }
 }
 
-template <int QM, int LT>
+template <int QM, int LT, bool ZF>
 __device__ void apply_unit(const DetectArgs& a, const float2* __restrict__ sW, const float* __restrict__ sSlope,
                            int slot, int fb, bool failed) {
     const int nr = a.n_rx, nl = a.n_layers;
@@ -68,7 +68,7 @@ __device__ void apply_unit(const DetectArgs& a, const float2* __restrict__ sW, c
             if (k >= nl) break;
             if (a.llr) {
                 float v[QM];
-                demap_layer<QM>(acc[k], sSlope[k], v);
+                demap_layer<QM, ZF>(acc[k], sSlope[k], v);
                 store_layer_llr<QM, LT>(a.llr, (re * nl + k) * QM, v);
             }
             if (a.xhat) {
@@ -199,7 +199,8 @@ __global__ void __launch_bounds__(kThreads) k_generic(DetectArgs a) {
             }
         }
         __syncthreads();
-        apply_unit<QM, LT>(a, sW, sSlope, slot, fb, failed);
+        if (a.sigma2 > 0.f) apply_unit<QM, LT, false>(a, sW, sSlope, slot, fb, failed);
+        else apply_unit<QM, LT, true>(a, sW, sSlope, slot, fb, failed);
         __syncthreads();
     }
 }

@@ -1,19 +1,21 @@
 // k_tpu.cu -- "thread per H-unit" detector for small per-subcarrier channels
-// (C1 2x2 QPSK, C2 4x4 16-QAM; any NR <= 4 even, NL <= NR).
+// (C1 2x2 QPSK, C2 4x4 16-QAM; any even NR <= 4, NL <= NR).
 //
 // Mapping (DESIGN.md §"Kernels"): a CTA owns TU consecutive subcarriers of one
-// slot (TU H-units, 14 x TU REs). One thread per H-unit:
+// slot (TU H-units, 14 x TU REs) and SPLIT warps-worth of threads per unit
+// column: thread (h, u) runs the setup of unit u and the symbols s = h, h +
+// SPLIT, ... of that unit.
 //   1. thread 0 issues 14 cp.async.bulk copies (one per OFDM symbol row, TU*NR*8
-//      contiguous bytes each) of the CTA's y tile into shared memory, each
-//      completing on its own mbarrier -- the whole tile is in flight at once,
-//      with no register cost;
-//   2. meanwhile every thread loads its H (NR*NL*8 B, 256-bit loads) and runs
-//      the setup (rows a2-a5) fully unrolled in fp64 registers (reading R18: an
-//      fp32 setup misses the 1e-4 x~ bound on square 4x4 channels, SURVEY.md
-//      §8(c)), rounding W~ (in PAM level units) and the LLR slopes once to fp32;
-//   3. for each symbol s it waits on mbarrier s, reads its y from shared
-//      memory, computes x~ = W~ y (row a6), demaps exactly (row a7) and writes
-//      the RE's NL*QM LLRs with 256-bit stores (full 32-byte sectors).
+//      contiguous bytes) of the CTA's y tile into shared memory, each completing
+//      on its own mbarrier -- the whole tile is in flight at once with no
+//      register cost;
+//   2. meanwhile every thread loads its H (256-bit loads) and runs rows a2-a5
+//      fully unrolled in registers, in fp64 by default (reading R18: an fp32
+//      setup misses the 1e-4 x~ bound on square 4x4 channels);
+//      W~ (in PAM level units) and the LLR slopes are rounded once to fp32;
+//   3. per symbol it waits on that row's mbarrier, reads y from shared memory,
+//      forms x~ = W~ y (row a6), demaps exactly (row a7) and writes the RE's
+//      NL*QM LLRs with 256-bit stores (whole 32-byte sectors).
 // The 14 REs of a unit reuse one W~ held in registers.
 #include "kernels.h"
 
@@ -21,6 +23,41 @@ namespace mimo {
 namespace {
 
 constexpr int kSym = 14;
+
+template <typename T>
+struct Cx {
+    T x, y;
+};
+template <typename T>
+__device__ __forceinline__ Cx<T> cx(T x, T y) {
+    return Cx<T>{x, y};
+}
+template <typename T>  // acc + a*b
+__device__ __forceinline__ Cx<T> mac(Cx<T> acc, Cx<T> a, Cx<T> b) {
+    acc.x = fma(a.x, b.x, acc.x);
+    acc.x = fma(-a.y, b.y, acc.x);
+    acc.y = fma(a.x, b.y, acc.y);
+    acc.y = fma(a.y, b.x, acc.y);
+    return acc;
+}
+template <typename T>  // acc + conj(a)*b
+__device__ __forceinline__ Cx<T> macc(Cx<T> acc, Cx<T> a, Cx<T> b) {
+    acc.x = fma(a.x, b.x, acc.x);
+    acc.x = fma(a.y, b.y, acc.x);
+    acc.y = fma(a.x, b.y, acc.y);
+    acc.y = fma(-a.y, b.x, acc.y);
+    return acc;
+}
+template <typename T>  // acc - a*conj(b)
+__device__ __forceinline__ Cx<T> msubc(Cx<T> acc, Cx<T> a, Cx<T> b) {
+    acc.x = fma(-a.x, b.x, acc.x);
+    acc.x = fma(-a.y, b.y, acc.x);
+    acc.y = fma(-a.y, b.x, acc.y);
+    acc.y = fma(a.x, b.y, acc.y);
+    return acc;
+}
+__device__ __forceinline__ double rsq(double v) { return rsqrt(v); }
+__device__ __forceinline__ float rsq(float v) { return rsqrtf(v); }
 
 template <int NR, int NL>
 struct SetupOut {
@@ -30,118 +67,160 @@ struct SetupOut {
     bool fail;
 };
 
-// Rows a2-a5 in fp64 registers, fully unrolled.
-template <int NR, int NL>
-__device__ __forceinline__ void setup_f64(const float2 (&hf)[NR][NL], double s2, double norm, float llr_scale,
-                                          SetupOut<NR, NL>& o) {
-    double2 h[NR][NL];
+// Rows a2-a5 in registers, scalar type T (double by default), fully unrolled.
+template <typename T, int NR, int NL>
+__device__ __forceinline__ void setup_unit(const float2 (&hf)[NR][NL], float sigma2, float norm, float llr_scale,
+                                           SetupOut<NR, NL>& o) {
+    const T s2 = (T)sigma2;
+    Cx<T> h[NR][NL];
 #pragma unroll
     for (int r = 0; r < NR; ++r)
 #pragma unroll
-        for (int l = 0; l < NL; ++l) h[r][l] = make_double2(hf[r][l].x, hf[r][l].y);
+        for (int l = 0; l < NL; ++l) h[r][l] = cx<T>((T)hf[r][l].x, (T)hf[r][l].y);
 
-    // a2: G = H^H H + s2 I (lower triangle)
-    double2 L[NL][NL];
-    double gmax = 0.0;
+    // a2: G = H^H H + s2 I (lower triangle), held in L
+    Cx<T> L[NL][NL];
+    T gmax = 0;
 #pragma unroll
     for (int i = 0; i < NL; ++i) {
 #pragma unroll
-        for (int j = 0; j <= i; ++j) {
-            double2 acc = make_double2(0.0, 0.0);
+        for (int j = 0; j < i; ++j) {
+            Cx<T> acc = cx<T>(0, 0);
 #pragma unroll
-            for (int r = 0; r < NR; ++r) acc = dmacc(acc, h[r][i], h[r][j]);
+            for (int r = 0; r < NR; ++r) acc = macc(acc, h[r][i], h[r][j]);
             L[i][j] = acc;
         }
-        L[i][i] = make_double2(L[i][i].x + s2, 0.0);
-        gmax = fmax(gmax, L[i][i].x);
+        T d = s2;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) d = fma(h[r][i].x, h[r][i].x, fma(h[r][i].y, h[r][i].y, d));
+        L[i][i] = cx<T>(d, 0);
+        gmax = gmax > d ? gmax : d;
     }
-    // a3: Cholesky (column by column, in place), keep 1/L_jj
-    double dinv[NL];
+    // a3: Cholesky G = L L^H (left-looking, in place), keep 1/L_jj; guard R17
+    T dinv[NL];
     bool fail = false;
 #pragma unroll
     for (int j = 0; j < NL; ++j) {
-        double p = L[j][j].x;
+        T p = L[j][j].x;
 #pragma unroll
-        for (int k = 0; k < j; ++k) p -= dnorm2(L[j][k]);
-        if (!(p > kPivotTau * gmax)) {
+        for (int k = 0; k < j; ++k) p = fma(-L[j][k].x, L[j][k].x, fma(-L[j][k].y, L[j][k].y, p));
+        if (!(p > (T)kPivotTau * gmax)) {
             fail = true;
-            p = 1.0;
+            p = 1;
         }
-        dinv[j] = rsqrt(p);
+        dinv[j] = rsq(p);
 #pragma unroll
         for (int i = j + 1; i < NL; ++i) {
-            double2 s = L[i][j];
+            Cx<T> s = L[i][j];
 #pragma unroll
-            for (int k = 0; k < j; ++k) {
-                // s -= L_ik conj(L_jk)
-                const double2 a = L[i][k], b = L[j][k];
-                s.x -= fma(a.x, b.x, a.y * b.y);
-                s.y -= fma(a.y, b.x, -a.x * b.y);
-            }
-            L[i][j] = dscale(s, dinv[j]);
+            for (int k = 0; k < j; ++k) s = msubc(s, L[i][k], L[j][k]);
+            L[i][j] = cx<T>(s.x * dinv[j], s.y * dinv[j]);
         }
     }
-    // a4: X = L^-1 (lower), X_jj = 1/L_jj, X_ij = -(1/L_ii) sum_{m=j}^{i-1} L_im X_mj
-    double2 X[NL][NL];
+    // a4: X = L^-1 (lower): X_jj = 1/L_jj, X_ij = -(1/L_ii) sum_{m=j}^{i-1} L_im X_mj
+    Cx<T> X[NL][NL];
 #pragma unroll
     for (int j = 0; j < NL; ++j) {
-        X[j][j] = make_double2(dinv[j], 0.0);
+        X[j][j] = cx<T>(dinv[j], 0);
 #pragma unroll
         for (int i = j + 1; i < NL; ++i) {
-            double2 s = make_double2(0.0, 0.0);
+            Cx<T> s = cx<T>(0, 0);
 #pragma unroll
-            for (int m = j; m < i; ++m) s = dmac(s, L[i][m], X[m][j]);
-            X[i][j] = dscale(s, -dinv[i]);
+            for (int m = j; m < i; ++m) s = mac(s, L[i][m], X[m][j]);
+            X[i][j] = cx<T>(-s.x * dinv[i], -s.y * dinv[i]);
         }
     }
-    // A_kk = [G^-1]_kk = sum_{i>=k} |X_ik|^2
-    // B = X H^H (NL x NR), B_ir = sum_{m<=i} X_im conj(H_rm)
-    double2 B[NL][NR];
+    // B = X H^H (NL x NR): B_ir = sum_{m<=i} X_im conj(H_rm)
+    Cx<T> B[NL][NR];
 #pragma unroll
     for (int i = 0; i < NL; ++i)
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
-            double2 s = make_double2(0.0, 0.0);
+            Cx<T> s = cx<T>(0, 0);
 #pragma unroll
-            for (int m = 0; m <= i; ++m) s = dmac(s, X[i][m], make_double2(h[r][m].x, -h[r][m].y));
+            for (int m = 0; m <= i; ++m) s = mac(s, X[i][m], cx<T>(h[r][m].x, -h[r][m].y));
             B[i][r] = s;
         }
-    const double sqn = sqrt(norm);
+    const float sqn = sqrtf(norm);
 #pragma unroll
     for (int k = 0; k < NL; ++k) {
-        double A = 0.0;
+        // A_kk = [G^-1]_kk = sum_{i>=k} |X_ik|^2 ; mu_k = 1 - s2 A_kk (in T: no cancellation loss)
+        T A = 0;
 #pragma unroll
-        for (int i = k; i < NL; ++i) A += dnorm2(X[i][k]);
-        // a5 (readings R3, R4, R11)
-        double mu, sinr;
-        if (s2 == 0.0) {
-            mu = 1.0;
-            sinr = (double)INFINITY;
+        for (int i = k; i < NL; ++i) A = fma(X[i][k].x, X[i][k].x, fma(X[i][k].y, X[i][k].y, A));
+        const T mu = fma(-s2, A, (T)1);
+        // a5 (readings R3, R4, R11) in fp32: SINR = mu / (s2 A), factor sqrt(norm)/mu
+        float sinr, f;
+        if (sigma2 == 0.f) {
+            sinr = __int_as_float(0x7f800000);
+            f = sqn;
         } else {
-            mu = 1.0 - s2 * A;
-            sinr = 1.0 / (s2 * A) - 1.0;
+            sinr = (float)mu / (float)(s2 * A);
+            f = sqn / (float)mu;
         }
-        double f = sqn / mu;
-        if (!(mu > 0.0) || fail) {
-            sinr = 0.0;
-            f = 0.0;
+        if (!(mu > 0) || fail) {
+            sinr = 0.f;
+            f = 0.f;
         }
-        o.sinr[k] = (float)sinr;
-        o.slope[k] = (float)(sinr / norm) * llr_scale;
-        // W_kr = sum_{i>=k} conj(X_ik) B_ir
+        o.sinr[k] = sinr;
+        o.slope[k] = sinr / norm * llr_scale;
+        // W_kr = sum_{i>=k} conj(X_ik) B_ir, scaled once to fp32 level units
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
-            double2 s = make_double2(0.0, 0.0);
+            Cx<T> s = cx<T>(0, 0);
 #pragma unroll
-            for (int i = k; i < NL; ++i) s = dmacc(s, X[i][k], B[i][r]);
-            o.w[k][r] = make_float2((float)(s.x * f), (float)(s.y * f));
+            for (int i = k; i < NL; ++i) s = macc(s, X[i][k], B[i][r]);
+            o.w[k][r] = make_float2((float)s.x * f, (float)s.y * f);
         }
     }
     o.fail = fail;
 }
 
-template <int NR, int NL, int QM, int LT, int TU>
-__global__ void __launch_bounds__(TU) k_tpu(DetectArgs a) {
+template <int NR, int NL, int QM, int LT, int TU, int SPLIT, bool ZF>
+__device__ __forceinline__ void apply_symbols(const DetectArgs& a, const SetupOut<NR, NL>& o, const float2* sy,
+                                              uint64_t* bars, int slot, int sc, int ul, int h, bool active) {
+    constexpr int kLlrBytes = NL * QM * LlrTraits<LT>::bytes;
+    constexpr int kWords = (kLlrBytes + 3) / 4;
+    const float ia = rsqrtf((float)qam_norm(QM));
+#pragma unroll 1
+    for (int s = h; s < kSym; s += SPLIT) {
+        mbar_wait(&bars[s], 0);
+        if (!active) continue;
+        float2 yv[NR];
+        const float2* ys = sy + (s * TU + ul) * NR;
+#pragma unroll
+        for (int r = 0; r < NR; ++r) yv[r] = ys[r];
+        float2 x[NL];
+#pragma unroll
+        for (int k = 0; k < NL; ++k) {
+            float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int r = 0; r < NR; ++r) acc = cmac(acc, o.w[k][r], yv[r]);
+            x[k] = acc;
+        }
+        const size_t re = (size_t)(slot * kSym + s) * a.n_sc + sc;
+        if (a.llr) {
+            float v[NL * QM];
+#pragma unroll
+            for (int k = 0; k < NL; ++k) demap_layer<QM, ZF>(x[k], o.slope[k], v + k * QM);
+            uint32_t w[kWords];
+            pack_llr<LT, NL * QM, ZF>(v, w);
+            store_bytes<kLlrBytes>((char*)a.llr + re * kLlrBytes, w);
+        }
+        if (a.xhat) {
+            uint32_t w[2 * NL];
+#pragma unroll
+            for (int k = 0; k < NL; ++k) {
+                w[2 * k] = __float_as_uint(x[k].x * ia);
+                w[2 * k + 1] = __float_as_uint(x[k].y * ia);
+            }
+            store_bytes<NL * 8>(a.xhat + re * NL, w);
+        }
+    }
+}
+
+template <int NR, int NL, int QM, int LT, int TU, int SPLIT, typename ST>
+__global__ void __launch_bounds__(TU* SPLIT) k_tpu(DetectArgs a) {
     static_assert(NR % 2 == 0, "bulk rows need 16-byte multiples");
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
@@ -151,6 +230,7 @@ __global__ void __launch_bounds__(TU) k_tpu(DetectArgs a) {
     const int sc0 = blockIdx.x * TU;
     const int nvalid = min(TU, a.n_sc - sc0);
     const int t = threadIdx.x;
+    const int ul = t % TU, h = t / TU;
 
     if (t == 0) {
 #pragma unroll
@@ -167,95 +247,71 @@ __global__ void __launch_bounds__(TU) k_tpu(DetectArgs a) {
         }
     }
 
-    const bool active = t < nvalid;
-    const int sc = sc0 + t;
+    const bool active = ul < nvalid;
+    const int sc = sc0 + ul;
     const size_t unit = (size_t)slot * a.n_sc + sc;
     SetupOut<NR, NL> o;
     if (active) {
         float2 hf[NR][NL];
         load_bytes<NR * NL * 8>(a.H + unit * NR * NL, reinterpret_cast<uint32_t*>(&hf[0][0]));
-        setup_f64<NR, NL>(hf, (double)a.sigma2, (double)qam_norm(QM), a.llr_scale, o);
-        if (o.fail) atomicAdd(a.fail_count, 1ull);
-        if (a.sinr) {
+        setup_unit<ST, NR, NL>(hf, a.sigma2, (float)qam_norm(QM), a.llr_scale, o);
+        if (h == 0) {
+            if (o.fail) atomicAdd(a.fail_count, 1ull);
+            if (a.sinr) {
 #pragma unroll
-            for (int k = 0; k < NL; ++k) a.sinr[unit * NL + k] = o.sinr[k];
-        }
-    }
-
-    constexpr int kLlrBytes = NL * QM * LlrTraits<LT>::bytes;
-    constexpr int kWords = (kLlrBytes + 3) / 4;
-    const float ia = rsqrtf((float)qam_norm(QM));
-#pragma unroll 1
-    for (int s = 0; s < kSym; ++s) {
-        mbar_wait(&bars[s], 0);
-        if (!active) continue;
-        float2 yv[NR];
-        const float2* ys = sy + (s * TU + t) * NR;
-#pragma unroll
-        for (int r = 0; r < NR; ++r) yv[r] = ys[r];
-        float2 x[NL];
-#pragma unroll
-        for (int k = 0; k < NL; ++k) {
-            float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int r = 0; r < NR; ++r) acc = cmac(acc, o.w[k][r], yv[r]);
-            x[k] = acc;
-        }
-        const size_t re = (size_t)(slot * kSym + s) * a.n_sc + sc;
-        if (a.llr) {
-            float v[NL * QM];
-#pragma unroll
-            for (int k = 0; k < NL; ++k) demap_layer<QM>(x[k], o.slope[k], v + k * QM);
-            uint32_t w[kWords];
-            pack_llr<LT, NL * QM>(v, w);
-            store_bytes<kLlrBytes>((char*)a.llr + re * kLlrBytes, w);
-        }
-        if (a.xhat) {
-            uint32_t w[2 * NL];
-#pragma unroll
-            for (int k = 0; k < NL; ++k) {
-                w[2 * k] = __float_as_uint(x[k].x * ia);
-                w[2 * k + 1] = __float_as_uint(x[k].y * ia);
+                for (int k = 0; k < NL; ++k) a.sinr[unit * NL + k] = o.sinr[k];
             }
-            store_bytes<NL * 8>(a.xhat + re * NL, w);
         }
     }
+    if (a.sigma2 > 0.f)
+        apply_symbols<NR, NL, QM, LT, TU, SPLIT, false>(a, o, sy, bars, slot, sc, ul, h, active);
+    else
+        apply_symbols<NR, NL, QM, LT, TU, SPLIT, true>(a, o, sy, bars, slot, sc, ul, h, active);
 }
 
-template <int NR, int NL, int QM, int LT, int TU>
+template <int NR, int NL, int QM, int LT, int TU, int SPLIT, typename ST>
 cudaError_t launch(const DetectArgs& a, cudaStream_t s) {
     if (a.n_sc <= 0 || a.n_slots <= 0) return cudaSuccess;
     const size_t smem = 128 + (size_t)kSym * TU * NR * 8;
     dim3 grid((a.n_sc + TU - 1) / TU, a.n_slots);
-    k_tpu<NR, NL, QM, LT, TU><<<grid, TU, smem, s>>>(a);
+    k_tpu<NR, NL, QM, LT, TU, SPLIT, ST><<<grid, TU * SPLIT, smem, s>>>(a);
     return cudaGetLastError();
 }
 
-template <int NR, int NL, int QM, int LT, int TU>
+template <int NR, int NL, int QM, int LT, int TU, int SPLIT, typename ST>
 cudaError_t prepare() {
     const int smem = 128 + kSym * TU * NR * 8;
     if (smem > 48 * 1024)
-        return cudaFuncSetAttribute(k_tpu<NR, NL, QM, LT, TU>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        return cudaFuncSetAttribute(k_tpu<NR, NL, QM, LT, TU, SPLIT, ST>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return cudaSuccess;
 }
 
-#define TPU_ENTRY(NR, NL, QM, LT, TU)                                                                       \
-    KernelEntry {                                                                                           \
-        "tpu_" #NR "x" #NL "_q" #QM "_l" #LT "_tu" #TU, NR, NL, QM, 1, 14, LT, 32, 1,                     \
-            launch<NR, NL, QM, LT, TU>, prepare<NR, NL, QM, LT, TU>                                        \
+#define TPU_ENTRY(NAME, NR, NL, QM, LT, TU, SPLIT, ST)                                       \
+    KernelEntry {                                                                             \
+        NAME, NR, NL, QM, 1, 14, LT, 32, 1, launch<NR, NL, QM, LT, TU, SPLIT, ST>,           \
+            prepare<NR, NL, QM, LT, TU, SPLIT, ST>                                            \
     }
 
+// First entry matching a plan wins; the rest are selectable by name
+// (MIMO_FORCE_KERNEL) for tuning experiments.
 const KernelEntry kEntries[] = {
-    TPU_ENTRY(2, 2, 2, kLlrF32, 32),  // C1
-    TPU_ENTRY(4, 4, 4, kLlrF32, 32),  // C2 (and the paper's own 4x4 shape)
-    TPU_ENTRY(2, 2, 4, kLlrF32, 32),
-    TPU_ENTRY(2, 1, 2, kLlrF32, 32),
-    TPU_ENTRY(4, 2, 4, kLlrF32, 32),
-    TPU_ENTRY(4, 4, 4, kLlrF16, 32),
-    TPU_ENTRY(4, 4, 4, kLlrI8, 32),
-    TPU_ENTRY(4, 4, 2, kLlrF32, 32),
-    TPU_ENTRY(4, 4, 6, kLlrF32, 32),
-    TPU_ENTRY(4, 4, 8, kLlrF32, 32),
+    TPU_ENTRY("tpu_2x2_q2_f32", 2, 2, 2, kLlrF32, 32, 1, double),  // C1
+    TPU_ENTRY("tpu_4x4_q4_f32", 4, 4, 4, kLlrF32, 32, 2, double),  // C2 (and the paper's 4x4 shape)
+    TPU_ENTRY("tpu_2x2_q4_f32", 2, 2, 4, kLlrF32, 32, 1, double),
+    TPU_ENTRY("tpu_2x1_q2_f32", 2, 1, 2, kLlrF32, 32, 1, double),
+    TPU_ENTRY("tpu_4x2_q4_f32", 4, 2, 4, kLlrF32, 32, 1, double),
+    TPU_ENTRY("tpu_4x4_q4_f16", 4, 4, 4, kLlrF16, 32, 2, double),
+    TPU_ENTRY("tpu_4x4_q4_i8", 4, 4, 4, kLlrI8, 32, 2, double),
+    TPU_ENTRY("tpu_4x4_q2_f32", 4, 4, 2, kLlrF32, 32, 2, double),
+    TPU_ENTRY("tpu_4x4_q6_f32", 4, 4, 6, kLlrF32, 32, 2, double),
+    TPU_ENTRY("tpu_4x4_q8_f32", 4, 4, 8, kLlrF32, 32, 2, double),
+    // tuning variants for C2
+    TPU_ENTRY("tpu_4x4_q4_f32_tu32_s1", 4, 4, 4, kLlrF32, 32, 1, double),
+    TPU_ENTRY("tpu_4x4_q4_f32_tu64_s1", 4, 4, 4, kLlrF32, 64, 1, double),
+    TPU_ENTRY("tpu_4x4_q4_f32_tu32_s4", 4, 4, 4, kLlrF32, 32, 4, double),
+    TPU_ENTRY("tpu_4x4_q4_f32_tu64_s2", 4, 4, 4, kLlrF32, 64, 2, double),
+    TPU_ENTRY("tpu_4x4_q4_f32_tu32_s2_fp32setup", 4, 4, 4, kLlrF32, 32, 2, float),
 };
 
 }  // namespace

@@ -2,6 +2,7 @@
 // validation, kernel dispatch and the host-buffer end-to-end path.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 
@@ -58,15 +59,20 @@ mimo_status_t arg_fail(mimo_plan_t p, const char* what) {
     return MIMO_ERR_INVALID_ARG;
 }
 
+// First specialised kernel serving the descriptor. MIMO_FORCE_KERNEL=<name>
+// (a tuning/debug knob) picks a named variant instead, or "generic".
 const mimo::KernelEntry* select_fast(const mimo_plan_desc_t& d) {
     using LF = const mimo::KernelEntry* (*)(int*);
     const LF tables[] = {mimo::tpu_entries};
+    const char* force = getenv("MIMO_FORCE_KERNEL");
+    if (force && strcmp(force, "generic") == 0) return nullptr;
     for (LF f : tables) {
         int n = 0;
         const mimo::KernelEntry* t = f(&n);
         for (int i = 0; i < n; ++i)
             if (t[i].n_rx == d.n_rx && t[i].n_layers == d.n_layers && t[i].qm == d.qam_order &&
-                t[i].sc_per_h == d.sc_per_h && t[i].sym_per_h == d.sym_per_h && t[i].llr_type == d.llr_type)
+                t[i].sc_per_h == d.sc_per_h && t[i].sym_per_h == d.sym_per_h && t[i].llr_type == d.llr_type &&
+                (!force || !*force || strcmp(force, t[i].name) == 0))
                 return &t[i];
     }
     return nullptr;
