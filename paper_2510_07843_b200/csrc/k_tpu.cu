@@ -1,22 +1,25 @@
-// k_tpu.cu -- "thread per H-unit" detector for small per-subcarrier channels
+// k_tpu.cu -- "threads per H-unit" detector for small per-subcarrier channels
 // (C1 2x2 QPSK, C2 4x4 16-QAM; any even NR <= 4, NL <= NR).
 //
 // Mapping (DESIGN.md §"Kernels"): a CTA owns TU consecutive subcarriers of one
-// slot (TU H-units, 14 x TU REs) and SPLIT warps-worth of threads per unit
-// column: thread (h, u) runs the setup of unit u and the symbols s = h, h +
-// SPLIT, ... of that unit.
+// slot (TU H-units, 14 x TU REs) and G warps-worth of threads. Thread (g, u)
+// serves unit u; the G threads of a unit split its work either by layer
+// (LAYER_SPLIT: thread g owns W~ rows [g NL/G, (g+1) NL/G) for all 14 symbols)
+// or by symbol (thread g owns all layers of symbols g, g+G, ...).
 //   1. thread 0 issues 14 cp.async.bulk copies (one per OFDM symbol row, TU*NR*8
 //      contiguous bytes) of the CTA's y tile into shared memory, each completing
 //      on its own mbarrier -- the whole tile is in flight at once with no
 //      register cost;
-//   2. meanwhile every thread loads its H (256-bit loads) and runs rows a2-a5
-//      fully unrolled in registers, in fp64 by default (reading R18: an fp32
-//      setup misses the 1e-4 x~ bound on square 4x4 channels);
-//      W~ (in PAM level units) and the LLR slopes are rounded once to fp32;
+//   2. meanwhile every thread loads its unit's H (256-bit loads) and runs rows
+//      a2-a5 fully unrolled in registers, in fp64 by default (reading R18: an
+//      fp32 setup misses the 1e-4 x~ bound on square 4x4 channels, SURVEY.md
+//      §8(c)); W~ rows (in PAM level units) and LLR slopes are rounded once to
+//      fp32; with LAYER_SPLIT each thread forms only its own rows of
+//      G^-1 and W~;
 //   3. per symbol it waits on that row's mbarrier, reads y from shared memory,
-//      forms x~ = W~ y (row a6), demaps exactly (row a7) and writes the RE's
-//      NL*QM LLRs with 256-bit stores (whole 32-byte sectors).
-// The 14 REs of a unit reuse one W~ held in registers.
+//      forms its x~ = W~ y (row a6), demaps exactly (row a7) and writes its
+//      LLRs with 256-bit stores (whole 32-byte sectors).
+// The 14 REs of a unit reuse W~ held in registers.
 #include "kernels.h"
 
 namespace mimo {
@@ -48,6 +51,14 @@ __device__ __forceinline__ Cx<T> macc(Cx<T> acc, Cx<T> a, Cx<T> b) {
     acc.y = fma(-a.y, b.x, acc.y);
     return acc;
 }
+template <typename T>  // acc + a*conj(b)
+__device__ __forceinline__ Cx<T> macb(Cx<T> acc, Cx<T> a, Cx<T> b) {
+    acc.x = fma(a.x, b.x, acc.x);
+    acc.x = fma(a.y, b.y, acc.x);
+    acc.y = fma(a.y, b.x, acc.y);
+    acc.y = fma(-a.x, b.y, acc.y);
+    return acc;
+}
 template <typename T>  // acc - a*conj(b)
 __device__ __forceinline__ Cx<T> msubc(Cx<T> acc, Cx<T> a, Cx<T> b) {
     acc.x = fma(-a.x, b.x, acc.x);
@@ -59,18 +70,23 @@ __device__ __forceinline__ Cx<T> msubc(Cx<T> acc, Cx<T> a, Cx<T> b) {
 __device__ __forceinline__ double rsq(double v) { return rsqrt(v); }
 __device__ __forceinline__ float rsq(float v) { return rsqrtf(v); }
 
-template <int NR, int NL>
+// Output rows K0 .. K0+NK-1 of the per-unit setup.
+template <int NR, int NK>
 struct SetupOut {
-    float2 w[NL][NR];  // W~ * sqrt(norm), fp32
-    float slope[NL];   // SINR * llr_scale / norm
-    float sinr[NL];
+    float2 w[NK][NR];  // W~ * sqrt(norm), fp32
+    float slope[NK];   // SINR * llr_scale / norm
+    float sinr[NK];
     bool fail;
 };
 
-// Rows a2-a5 in registers, scalar type T (double by default), fully unrolled.
-template <typename T, int NR, int NL>
-__device__ __forceinline__ void setup_unit(const float2 (&hf)[NR][NL], float sigma2, float norm, float llr_scale,
-                                           SetupOut<NR, NL>& o) {
+// Rows a2-a5 in registers, scalar type T (double by default), fully unrolled;
+// produces W~ rows K0..K0+NK-1.
+//   a2 G = H^H H + s2 I;  a3 G = L L^H (guard R17);  a4 X = L^-1,
+//   G^-1_kj = sum_{m >= max(k,j)} conj(X_mk) X_mj,  W_kr = sum_j G^-1_kj conj(H_rj);
+//   a5 mu_k = 1 - s2 G^-1_kk, SINR_k = mu_k / (s2 G^-1_kk), W~_k = W_k sqrt(norm) / mu_k.
+template <typename T, int NR, int NL, int K0, int NK>
+__device__ __forceinline__ void setup_rows(const float2 (&hf)[NR][NL], float sigma2, float norm, float llr_scale,
+                                           SetupOut<NR, NK>& o) {
     const T s2 = (T)sigma2;
     Cx<T> h[NR][NL];
 #pragma unroll
@@ -78,7 +94,7 @@ __device__ __forceinline__ void setup_unit(const float2 (&hf)[NR][NL], float sig
 #pragma unroll
         for (int l = 0; l < NL; ++l) h[r][l] = cx<T>((T)hf[r][l].x, (T)hf[r][l].y);
 
-    // a2: G = H^H H + s2 I (lower triangle), held in L
+    // a2: Gram (lower triangle) into L
     Cx<T> L[NL][NL];
     T gmax = 0;
 #pragma unroll
@@ -96,9 +112,9 @@ __device__ __forceinline__ void setup_unit(const float2 (&hf)[NR][NL], float sig
         L[i][i] = cx<T>(d, 0);
         gmax = gmax > d ? gmax : d;
     }
-    // a3: Cholesky G = L L^H (left-looking, in place), keep 1/L_jj; guard R17
+    // a3: left-looking Cholesky in place, keep 1/L_jj; guard p_j > tau max G_ii (R17, NaN-safe)
     T dinv[NL];
-    bool fail = false;
+    bool fail = !(gmax == gmax);
 #pragma unroll
     for (int j = 0; j < NL; ++j) {
         T p = L[j][j].x;
@@ -130,26 +146,21 @@ __device__ __forceinline__ void setup_unit(const float2 (&hf)[NR][NL], float sig
             X[i][j] = cx<T>(-s.x * dinv[i], -s.y * dinv[i]);
         }
     }
-    // B = X H^H (NL x NR): B_ir = sum_{m<=i} X_im conj(H_rm)
-    Cx<T> B[NL][NR];
-#pragma unroll
-    for (int i = 0; i < NL; ++i)
-#pragma unroll
-        for (int r = 0; r < NR; ++r) {
-            Cx<T> s = cx<T>(0, 0);
-#pragma unroll
-            for (int m = 0; m <= i; ++m) s = mac(s, X[i][m], cx<T>(h[r][m].x, -h[r][m].y));
-            B[i][r] = s;
-        }
     const float sqn = sqrtf(norm);
 #pragma unroll
-    for (int k = 0; k < NL; ++k) {
-        // A_kk = [G^-1]_kk = sum_{i>=k} |X_ik|^2 ; mu_k = 1 - s2 A_kk (in T: no cancellation loss)
-        T A = 0;
+    for (int kk = 0; kk < NK; ++kk) {
+        const int k = K0 + kk;
+        // row k of G^-1 = X^H X
+        Cx<T> gi[NL];
 #pragma unroll
-        for (int i = k; i < NL; ++i) A = fma(X[i][k].x, X[i][k].x, fma(X[i][k].y, X[i][k].y, A));
+        for (int j = 0; j < NL; ++j) {
+            Cx<T> s = cx<T>(0, 0);
+#pragma unroll
+            for (int m = (k > j ? k : j); m < NL; ++m) s = macc(s, X[m][k], X[m][j]);
+            gi[j] = s;
+        }
+        const T A = gi[k].x;
         const T mu = fma(-s2, A, (T)1);
-        // a5 (readings R3, R4, R11) in fp32: SINR = mu / (s2 A), factor sqrt(norm)/mu
         float sinr, f;
         if (sigma2 == 0.f) {
             sinr = __int_as_float(0x7f800000);
@@ -158,41 +169,43 @@ __device__ __forceinline__ void setup_unit(const float2 (&hf)[NR][NL], float sig
             sinr = (float)mu / (float)(s2 * A);
             f = sqn / (float)mu;
         }
-        if (!(mu > 0) || fail) {
+        const bool dead = !(mu > 0) || fail;
+        if (dead) {
             sinr = 0.f;
             f = 0.f;
         }
-        o.sinr[k] = sinr;
-        o.slope[k] = sinr / norm * llr_scale;
-        // W_kr = sum_{i>=k} conj(X_ik) B_ir, scaled once to fp32 level units
+        o.sinr[kk] = sinr;
+        o.slope[kk] = sinr / norm * llr_scale;
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
             Cx<T> s = cx<T>(0, 0);
 #pragma unroll
-            for (int i = k; i < NL; ++i) s = macc(s, X[i][k], B[i][r]);
-            o.w[k][r] = make_float2((float)s.x * f, (float)s.y * f);
+            for (int j = 0; j < NL; ++j) s = macb(s, gi[j], h[r][j]);  // G^-1_kj conj(H_rj)
+            o.w[kk][r] = dead ? make_float2(0.f, 0.f) : make_float2((float)s.x * f, (float)s.y * f);
         }
     }
     o.fail = fail;
 }
 
-template <int NR, int NL, int QM, int LT, int TU, int SPLIT, bool ZF>
-__device__ __forceinline__ void apply_symbols(const DetectArgs& a, const SetupOut<NR, NL>& o, const float2* sy,
-                                              uint64_t* bars, int slot, int sc, int ul, int h, bool active) {
-    constexpr int kLlrBytes = NL * QM * LlrTraits<LT>::bytes;
+template <int NR, int NL, int QM, int LT, int TU, int G, bool LAYER_SPLIT, bool ZF, int NK>
+__device__ __forceinline__ void apply_symbols(const DetectArgs& a, const SetupOut<NR, NK>& o, const float2* sy,
+                                              uint64_t* bars, int slot, int sc, int ul, int g, bool active) {
+    constexpr int kLlrBytes = NK * QM * LlrTraits<LT>::bytes;  // this thread's share of one RE
     constexpr int kWords = (kLlrBytes + 3) / 4;
+    constexpr int s_first_stride = LAYER_SPLIT ? 1 : G;
     const float ia = rsqrtf((float)qam_norm(QM));
+    const int k0 = LAYER_SPLIT ? g * NK : 0;
 #pragma unroll 1
-    for (int s = h; s < kSym; s += SPLIT) {
+    for (int s = LAYER_SPLIT ? 0 : g; s < kSym; s += s_first_stride) {
         mbar_wait(&bars[s], 0);
         if (!active) continue;
         float2 yv[NR];
         const float2* ys = sy + (s * TU + ul) * NR;
 #pragma unroll
         for (int r = 0; r < NR; ++r) yv[r] = ys[r];
-        float2 x[NL];
+        float2 x[NK];
 #pragma unroll
-        for (int k = 0; k < NL; ++k) {
+        for (int k = 0; k < NK; ++k) {
             float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
             for (int r = 0; r < NR; ++r) acc = cmac(acc, o.w[k][r], yv[r]);
@@ -200,28 +213,50 @@ __device__ __forceinline__ void apply_symbols(const DetectArgs& a, const SetupOu
         }
         const size_t re = (size_t)(slot * kSym + s) * a.n_sc + sc;
         if (a.llr) {
-            float v[NL * QM];
+            float v[NK * QM];
 #pragma unroll
-            for (int k = 0; k < NL; ++k) demap_layer<QM, ZF>(x[k], o.slope[k], v + k * QM);
+            for (int k = 0; k < NK; ++k) demap_layer<QM, ZF>(x[k], o.slope[k], v + k * QM);
             uint32_t w[kWords];
-            pack_llr<LT, NL * QM, ZF>(v, w);
-            store_bytes<kLlrBytes>((char*)a.llr + re * kLlrBytes, w);
+            pack_llr<LT, NK * QM, ZF>(v, w);
+            store_bytes<kLlrBytes>((char*)a.llr + (re * NL + k0) * QM * LlrTraits<LT>::bytes, w);
         }
         if (a.xhat) {
-            uint32_t w[2 * NL];
+            uint32_t w[2 * NK];
 #pragma unroll
-            for (int k = 0; k < NL; ++k) {
+            for (int k = 0; k < NK; ++k) {
                 w[2 * k] = __float_as_uint(x[k].x * ia);
                 w[2 * k + 1] = __float_as_uint(x[k].y * ia);
             }
-            store_bytes<NL * 8>(a.xhat + re * NL, w);
+            store_bytes<NK * 8>(a.xhat + re * NL + k0, w);
         }
     }
 }
 
-template <int NR, int NL, int QM, int LT, int TU, int SPLIT, typename ST>
-__global__ void __launch_bounds__(TU* SPLIT) k_tpu(DetectArgs a) {
+template <int NR, int NL, int QM, int LT, int TU, int G, bool LAYER_SPLIT, typename ST, int K0, int NK>
+__device__ __forceinline__ void unit_work(const DetectArgs& a, const float2* sy, uint64_t* bars, int slot, int sc,
+                                          int ul, int g, bool active) {
+    SetupOut<NR, NK> o;
+    const size_t unit = (size_t)slot * a.n_sc + sc;
+    if (active) {
+        float2 hf[NR][NL];
+        load_bytes<NR * NL * 8>(a.H + unit * NR * NL, reinterpret_cast<uint32_t*>(&hf[0][0]));
+        setup_rows<ST, NR, NL, K0, NK>(hf, a.sigma2, (float)qam_norm(QM), a.llr_scale, o);
+        if (g == 0 && o.fail) atomicAdd(a.fail_count, 1ull);
+        if (a.sinr && (LAYER_SPLIT || g == 0)) {
+#pragma unroll
+            for (int k = 0; k < NK; ++k) a.sinr[unit * NL + K0 + k] = o.sinr[k];
+        }
+    }
+    if (a.sigma2 > 0.f)
+        apply_symbols<NR, NL, QM, LT, TU, G, LAYER_SPLIT, false, NK>(a, o, sy, bars, slot, sc, ul, g, active);
+    else
+        apply_symbols<NR, NL, QM, LT, TU, G, LAYER_SPLIT, true, NK>(a, o, sy, bars, slot, sc, ul, g, active);
+}
+
+template <int NR, int NL, int QM, int LT, int TU, int G, bool LAYER_SPLIT, typename ST>
+__global__ void __launch_bounds__(TU* G) k_tpu(DetectArgs a) {
     static_assert(NR % 2 == 0, "bulk rows need 16-byte multiples");
+    static_assert(!LAYER_SPLIT || (NL % G == 0 && G <= 4), "layer split needs G | NL");
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
     float2* sy = reinterpret_cast<float2*>(smem + 128);
@@ -230,7 +265,7 @@ __global__ void __launch_bounds__(TU* SPLIT) k_tpu(DetectArgs a) {
     const int sc0 = blockIdx.x * TU;
     const int nvalid = min(TU, a.n_sc - sc0);
     const int t = threadIdx.x;
-    const int ul = t % TU, h = t / TU;
+    const int ul = t % TU, g = t / TU;
 
     if (t == 0) {
 #pragma unroll
@@ -246,72 +281,64 @@ __global__ void __launch_bounds__(TU* SPLIT) k_tpu(DetectArgs a) {
             bulk_g2s(sy + s * TU * NR, a.y + ((size_t)(slot * kSym + s) * a.n_sc + sc0) * NR, row_bytes, &bars[s]);
         }
     }
-
     const bool active = ul < nvalid;
     const int sc = sc0 + ul;
-    const size_t unit = (size_t)slot * a.n_sc + sc;
-    SetupOut<NR, NL> o;
-    if (active) {
-        float2 hf[NR][NL];
-        load_bytes<NR * NL * 8>(a.H + unit * NR * NL, reinterpret_cast<uint32_t*>(&hf[0][0]));
-        setup_unit<ST, NR, NL>(hf, a.sigma2, (float)qam_norm(QM), a.llr_scale, o);
-        if (h == 0) {
-            if (o.fail) atomicAdd(a.fail_count, 1ull);
-            if (a.sinr) {
-#pragma unroll
-                for (int k = 0; k < NL; ++k) a.sinr[unit * NL + k] = o.sinr[k];
-            }
-        }
+    if constexpr (!LAYER_SPLIT) {
+        unit_work<NR, NL, QM, LT, TU, G, false, ST, 0, NL>(a, sy, bars, slot, sc, ul, g, active);
+    } else {
+        constexpr int NK = NL / G;
+        if (g == 0) unit_work<NR, NL, QM, LT, TU, G, true, ST, 0, NK>(a, sy, bars, slot, sc, ul, g, active);
+        if constexpr (G > 1)
+            if (g == 1) unit_work<NR, NL, QM, LT, TU, G, true, ST, NK, NK>(a, sy, bars, slot, sc, ul, g, active);
+        if constexpr (G > 2)
+            if (g == 2) unit_work<NR, NL, QM, LT, TU, G, true, ST, 2 * NK, NK>(a, sy, bars, slot, sc, ul, g, active);
+        if constexpr (G > 3)
+            if (g == 3) unit_work<NR, NL, QM, LT, TU, G, true, ST, 3 * NK, NK>(a, sy, bars, slot, sc, ul, g, active);
     }
-    if (a.sigma2 > 0.f)
-        apply_symbols<NR, NL, QM, LT, TU, SPLIT, false>(a, o, sy, bars, slot, sc, ul, h, active);
-    else
-        apply_symbols<NR, NL, QM, LT, TU, SPLIT, true>(a, o, sy, bars, slot, sc, ul, h, active);
 }
 
-template <int NR, int NL, int QM, int LT, int TU, int SPLIT, typename ST>
+template <int NR, int NL, int QM, int LT, int TU, int G, bool LS, typename ST>
 cudaError_t launch(const DetectArgs& a, cudaStream_t s) {
     if (a.n_sc <= 0 || a.n_slots <= 0) return cudaSuccess;
     const size_t smem = 128 + (size_t)kSym * TU * NR * 8;
     dim3 grid((a.n_sc + TU - 1) / TU, a.n_slots);
-    k_tpu<NR, NL, QM, LT, TU, SPLIT, ST><<<grid, TU * SPLIT, smem, s>>>(a);
+    k_tpu<NR, NL, QM, LT, TU, G, LS, ST><<<grid, TU * G, smem, s>>>(a);
     return cudaGetLastError();
 }
 
-template <int NR, int NL, int QM, int LT, int TU, int SPLIT, typename ST>
+template <int NR, int NL, int QM, int LT, int TU, int G, bool LS, typename ST>
 cudaError_t prepare() {
     const int smem = 128 + kSym * TU * NR * 8;
     if (smem > 48 * 1024)
-        return cudaFuncSetAttribute(k_tpu<NR, NL, QM, LT, TU, SPLIT, ST>,
+        return cudaFuncSetAttribute(k_tpu<NR, NL, QM, LT, TU, G, LS, ST>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return cudaSuccess;
 }
 
-#define TPU_ENTRY(NAME, NR, NL, QM, LT, TU, SPLIT, ST)                                       \
-    KernelEntry {                                                                             \
-        NAME, NR, NL, QM, 1, 14, LT, 32, 1, launch<NR, NL, QM, LT, TU, SPLIT, ST>,           \
-            prepare<NR, NL, QM, LT, TU, SPLIT, ST>                                            \
+#define TPU_ENTRY(NAME, NR, NL, QM, LT, TU, G, LS, ST)                                        \
+    KernelEntry {                                                                              \
+        NAME, NR, NL, QM, 1, 14, LT, 32, 1, launch<NR, NL, QM, LT, TU, G, LS, ST>,            \
+            prepare<NR, NL, QM, LT, TU, G, LS, ST>                                             \
     }
 
 // First entry matching a plan wins; the rest are selectable by name
 // (MIMO_FORCE_KERNEL) for tuning experiments.
 const KernelEntry kEntries[] = {
-    TPU_ENTRY("tpu_2x2_q2_f32", 2, 2, 2, kLlrF32, 32, 1, double),  // C1
-    TPU_ENTRY("tpu_4x4_q4_f32", 4, 4, 4, kLlrF32, 32, 2, double),  // C2 (and the paper's 4x4 shape)
-    TPU_ENTRY("tpu_2x2_q4_f32", 2, 2, 4, kLlrF32, 32, 1, double),
-    TPU_ENTRY("tpu_2x1_q2_f32", 2, 1, 2, kLlrF32, 32, 1, double),
-    TPU_ENTRY("tpu_4x2_q4_f32", 4, 2, 4, kLlrF32, 32, 1, double),
-    TPU_ENTRY("tpu_4x4_q4_f16", 4, 4, 4, kLlrF16, 32, 2, double),
-    TPU_ENTRY("tpu_4x4_q4_i8", 4, 4, 4, kLlrI8, 32, 2, double),
-    TPU_ENTRY("tpu_4x4_q2_f32", 4, 4, 2, kLlrF32, 32, 2, double),
-    TPU_ENTRY("tpu_4x4_q6_f32", 4, 4, 6, kLlrF32, 32, 2, double),
-    TPU_ENTRY("tpu_4x4_q8_f32", 4, 4, 8, kLlrF32, 32, 2, double),
+    TPU_ENTRY("tpu_2x2_q2_f32", 2, 2, 2, kLlrF32, 32, 1, false, double),   // C1
+    TPU_ENTRY("tpu_4x4_q4_f32", 4, 4, 4, kLlrF32, 32, 2, true, double),    // C2 (and the paper's 4x4 shape)
+    TPU_ENTRY("tpu_2x2_q4_f32", 2, 2, 4, kLlrF32, 32, 1, false, double),
+    TPU_ENTRY("tpu_2x1_q2_f32", 2, 1, 2, kLlrF32, 32, 1, false, double),
+    TPU_ENTRY("tpu_4x2_q4_f32", 4, 2, 4, kLlrF32, 32, 2, true, double),
+    TPU_ENTRY("tpu_4x4_q4_f16", 4, 4, 4, kLlrF16, 32, 2, true, double),
+    TPU_ENTRY("tpu_4x4_q4_i8", 4, 4, 4, kLlrI8, 32, 2, true, double),
+    TPU_ENTRY("tpu_4x4_q2_f32", 4, 4, 2, kLlrF32, 32, 2, true, double),
+    TPU_ENTRY("tpu_4x4_q6_f32", 4, 4, 6, kLlrF32, 32, 2, true, double),
+    TPU_ENTRY("tpu_4x4_q8_f32", 4, 4, 8, kLlrF32, 32, 2, true, double),
     // tuning variants for C2
-    TPU_ENTRY("tpu_4x4_q4_f32_tu32_s1", 4, 4, 4, kLlrF32, 32, 1, double),
-    TPU_ENTRY("tpu_4x4_q4_f32_tu64_s1", 4, 4, 4, kLlrF32, 64, 1, double),
-    TPU_ENTRY("tpu_4x4_q4_f32_tu32_s4", 4, 4, 4, kLlrF32, 32, 4, double),
-    TPU_ENTRY("tpu_4x4_q4_f32_tu64_s2", 4, 4, 4, kLlrF32, 64, 2, double),
-    TPU_ENTRY("tpu_4x4_q4_f32_tu32_s2_fp32setup", 4, 4, 4, kLlrF32, 32, 2, float),
+    TPU_ENTRY("tpu_4x4_q4_f32_sym2", 4, 4, 4, kLlrF32, 32, 2, false, double),
+    TPU_ENTRY("tpu_4x4_q4_f32_lay4", 4, 4, 4, kLlrF32, 32, 4, true, double),
+    TPU_ENTRY("tpu_4x4_q4_f32_lay2_tu64", 4, 4, 4, kLlrF32, 64, 2, true, double),
+    TPU_ENTRY("tpu_4x4_q4_f32_lay2_fp32setup", 4, 4, 4, kLlrF32, 32, 2, true, float),
 };
 
 }  // namespace
