@@ -84,7 +84,7 @@ struct SetupOut {
 //   a2 G = H^H H + s2 I;  a3 G = L L^H (guard R17);  a4 X = L^-1,
 //   G^-1_kj = sum_{m >= max(k,j)} conj(X_mk) X_mj,  W_kr = sum_j G^-1_kj conj(H_rj);
 //   a5 mu_k = 1 - s2 G^-1_kk, SINR_k = mu_k / (s2 G^-1_kk), W~_k = W_k sqrt(norm) / mu_k.
-template <typename T, int NR, int NL, int K0, int NK>
+template <typename T, int NR, int NL, int K0, int NK, bool BROUTE>
 __device__ __forceinline__ void setup_rows(const float2 (&hf)[NR][NL], float sigma2, float norm, float llr_scale,
                                            SetupOut<NR, NK>& o) {
     const T s2 = (T)sigma2;
@@ -147,6 +147,51 @@ __device__ __forceinline__ void setup_rows(const float2 (&hf)[NR][NL], float sig
         }
     }
     const float sqn = sqrtf(norm);
+    if constexpr (BROUTE) {
+        static_assert(K0 == 0 && NK == NL, "B route forms all rows");
+        // B = X H^H (NL x NR): B_ir = sum_{m<=i} X_im conj(H_rm); W_kr = sum_{i>=k} conj(X_ik) B_ir
+        Cx<T> B[NL][NR];
+#pragma unroll
+        for (int i = 0; i < NL; ++i)
+#pragma unroll
+            for (int r = 0; r < NR; ++r) {
+                Cx<T> s = cx<T>(0, 0);
+#pragma unroll
+                for (int m = 0; m <= i; ++m) s = macb(s, X[i][m], h[r][m]);
+                B[i][r] = s;
+            }
+#pragma unroll
+        for (int k = 0; k < NL; ++k) {
+            T A = 0;
+#pragma unroll
+            for (int i = k; i < NL; ++i) A = fma(X[i][k].x, X[i][k].x, fma(X[i][k].y, X[i][k].y, A));
+            const T mu = fma(-s2, A, (T)1);
+            float sinr, f;
+            if (sigma2 == 0.f) {
+                sinr = __int_as_float(0x7f800000);
+                f = sqn;
+            } else {
+                sinr = (float)mu / (float)(s2 * A);
+                f = sqn / (float)mu;
+            }
+            const bool dead = !(mu > 0) || fail;
+            if (dead) {
+                sinr = 0.f;
+                f = 0.f;
+            }
+            o.sinr[k] = sinr;
+            o.slope[k] = sinr / norm * llr_scale;
+#pragma unroll
+            for (int r = 0; r < NR; ++r) {
+                Cx<T> s = cx<T>(0, 0);
+#pragma unroll
+                for (int i = k; i < NL; ++i) s = macc(s, X[i][k], B[i][r]);
+                o.w[k][r] = dead ? make_float2(0.f, 0.f) : make_float2((float)s.x * f, (float)s.y * f);
+            }
+        }
+        o.fail = fail;
+        return;
+    }
 #pragma unroll
     for (int kk = 0; kk < NK; ++kk) {
         const int k = K0 + kk;
@@ -240,7 +285,7 @@ __device__ __forceinline__ void unit_work(const DetectArgs& a, const float2* sy,
     if (active) {
         float2 hf[NR][NL];
         load_bytes<NR * NL * 8>(a.H + unit * NR * NL, reinterpret_cast<uint32_t*>(&hf[0][0]));
-        setup_rows<ST, NR, NL, K0, NK>(hf, a.sigma2, (float)qam_norm(QM), a.llr_scale, o);
+        setup_rows<ST, NR, NL, K0, NK, !LAYER_SPLIT>(hf, a.sigma2, (float)qam_norm(QM), a.llr_scale, o);
         if (g == 0 && o.fail) atomicAdd(a.fail_count, 1ull);
         if (a.sinr && (LAYER_SPLIT || g == 0)) {
 #pragma unroll
