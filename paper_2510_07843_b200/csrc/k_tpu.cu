@@ -20,6 +20,8 @@
 //      forms its x~ = W~ y (row a6), demaps exactly (row a7) and writes its
 //      LLRs with 256-bit stores (whole 32-byte sectors).
 // The 14 REs of a unit reuse W~ held in registers.
+#include <type_traits>
+
 #include "kernels.h"
 
 namespace mimo {
@@ -70,86 +72,96 @@ __device__ __forceinline__ Cx<T> msubc(Cx<T> acc, Cx<T> a, Cx<T> b) {
 __device__ __forceinline__ double rsq(double v) { return rsqrt(v); }
 __device__ __forceinline__ float rsq(float v) { return rsqrtf(v); }
 
-// Output rows K0 .. K0+NK-1 of the per-unit setup.
-template <int NR, int NK>
+// Tag type: skip the setup (W~ = scaled H^T; timing experiments only).
+struct NoSetup {};
+
+template <int NR, int NL>
 struct SetupOut {
-    float2 w[NK][NR];  // W~ * sqrt(norm), fp32
-    float slope[NK];   // SINR * llr_scale / norm
-    float sinr[NK];
+    float2 w[NL][NR];  // W~ * sqrt(norm), fp32
+    float slope[NL];   // SINR * llr_scale / norm
+    float sinr[NL];
     bool fail;
 };
 
-// Rows a2-a5 in registers, scalar type T (double by default), fully unrolled;
-// produces W~ rows K0..K0+NK-1.
-//   a2 G = H^H H + s2 I;  a3 G = L L^H (guard R17);  a4 X = L^-1,
-//   G^-1_kj = sum_{m >= max(k,j)} conj(X_mk) X_mj,  W_kr = sum_j G^-1_kj conj(H_rj);
-//   a5 mu_k = 1 - s2 G^-1_kk, SINR_k = mu_k / (s2 G^-1_kk), W~_k = W_k sqrt(norm) / mu_k.
-template <typename T, int NR, int NL, int K0, int NK, bool BROUTE>
-__device__ __forceinline__ void setup_rows(const float2 (&hf)[NR][NL], float sigma2, float norm, float llr_scale,
-                                           SetupOut<NR, NK>& o) {
-    const T s2 = (T)sigma2;
-    Cx<T> h[NR][NL];
-#pragma unroll
-    for (int r = 0; r < NR; ++r)
-#pragma unroll
-        for (int l = 0; l < NL; ++l) h[r][l] = cx<T>((T)hf[r][l].x, (T)hf[r][l].y);
-
-    // a2: Gram (lower triangle) into L
-    Cx<T> L[NL][NL];
-    T gmax = 0;
-#pragma unroll
-    for (int i = 0; i < NL; ++i) {
-#pragma unroll
-        for (int j = 0; j < i; ++j) {
-            Cx<T> acc = cx<T>(0, 0);
-#pragma unroll
-            for (int r = 0; r < NR; ++r) acc = macc(acc, h[r][i], h[r][j]);
-            L[i][j] = acc;
-        }
-        T d = s2;
-#pragma unroll
-        for (int r = 0; r < NR; ++r) d = fma(h[r][i].x, h[r][i].x, fma(h[r][i].y, h[r][i].y, d));
-        L[i][i] = cx<T>(d, 0);
-        gmax = gmax > d ? gmax : d;
-    }
-    // a3: left-looking Cholesky in place, keep 1/L_jj; guard p_j > tau max G_ii (R17, NaN-safe)
-    T dinv[NL];
-    bool fail = !(gmax == gmax);
-#pragma unroll
-    for (int j = 0; j < NL; ++j) {
-        T p = L[j][j].x;
-#pragma unroll
-        for (int k = 0; k < j; ++k) p = fma(-L[j][k].x, L[j][k].x, fma(-L[j][k].y, L[j][k].y, p));
-        if (!(p > (T)kPivotTau * gmax)) {
-            fail = true;
-            p = 1;
-        }
-        dinv[j] = rsq(p);
-#pragma unroll
-        for (int i = j + 1; i < NL; ++i) {
-            Cx<T> s = L[i][j];
-#pragma unroll
-            for (int k = 0; k < j; ++k) s = msubc(s, L[i][k], L[j][k]);
-            L[i][j] = cx<T>(s.x * dinv[j], s.y * dinv[j]);
-        }
-    }
-    // a4: X = L^-1 (lower): X_jj = 1/L_jj, X_ij = -(1/L_ii) sum_{m=j}^{i-1} L_im X_mj
-    Cx<T> X[NL][NL];
-#pragma unroll
-    for (int j = 0; j < NL; ++j) {
-        X[j][j] = cx<T>(dinv[j], 0);
-#pragma unroll
-        for (int i = j + 1; i < NL; ++i) {
-            Cx<T> s = cx<T>(0, 0);
-#pragma unroll
-            for (int m = j; m < i; ++m) s = mac(s, L[i][m], X[m][j]);
-            X[i][j] = cx<T>(-s.x * dinv[i], -s.y * dinv[i]);
-        }
-    }
+// Rows a2-a5 in registers, scalar type T (double by default), fully unrolled:
+//   a2 G = H^H H + s2 I;  a3 G = L L^H (left-looking, guard R17);
+//   a4 X = L^-1;  B = X H^H;  W = X^H B = G^-1 H^H;  A_kk = sum_i |X_ik|^2;
+//   a5 mu_k = 1 - s2 A_kk, SINR_k = mu_k / (s2 A_kk), W~_k = W_k sqrt(norm) / mu_k.
+template <typename T, int NR, int NL>
+__device__ __forceinline__ void setup_unit(const float2 (&hf)[NR][NL], float sigma2, float norm, float llr_scale,
+                                           SetupOut<NR, NL>& o) {
     const float sqn = sqrtf(norm);
-    if constexpr (BROUTE) {
-        static_assert(K0 == 0 && NK == NL, "B route forms all rows");
-        // B = X H^H (NL x NR): B_ir = sum_{m<=i} X_im conj(H_rm); W_kr = sum_{i>=k} conj(X_ik) B_ir
+    if constexpr (std::is_same<T, NoSetup>::value) {
+#pragma unroll
+        for (int k = 0; k < NL; ++k) {
+#pragma unroll
+            for (int r = 0; r < NR; ++r) o.w[k][r] = make_float2(hf[r][k].x * sqn, -hf[r][k].y * sqn);
+            o.sinr[k] = 10.f;
+            o.slope[k] = 10.f / norm * llr_scale;
+        }
+        o.fail = false;
+        return;
+    } else {
+        const T s2 = (T)sigma2;
+        Cx<T> h[NR][NL];
+#pragma unroll
+        for (int r = 0; r < NR; ++r)
+#pragma unroll
+            for (int l = 0; l < NL; ++l) h[r][l] = cx<T>((T)hf[r][l].x, (T)hf[r][l].y);
+
+        // a2: Gram (lower triangle) into L
+        Cx<T> L[NL][NL];
+        T gmax = 0;
+#pragma unroll
+        for (int i = 0; i < NL; ++i) {
+#pragma unroll
+            for (int j = 0; j < i; ++j) {
+                Cx<T> acc = cx<T>(0, 0);
+#pragma unroll
+                for (int r = 0; r < NR; ++r) acc = macc(acc, h[r][i], h[r][j]);
+                L[i][j] = acc;
+            }
+            T d = s2;
+#pragma unroll
+            for (int r = 0; r < NR; ++r) d = fma(h[r][i].x, h[r][i].x, fma(h[r][i].y, h[r][i].y, d));
+            L[i][i] = cx<T>(d, 0);
+            gmax = gmax > d ? gmax : d;
+        }
+        // a3: left-looking Cholesky in place, keep 1/L_jj; guard p_j > tau max G_ii (R17, NaN-safe)
+        T dinv[NL];
+        bool fail = !(gmax == gmax);
+#pragma unroll
+        for (int j = 0; j < NL; ++j) {
+            T p = L[j][j].x;
+#pragma unroll
+            for (int k = 0; k < j; ++k) p = fma(-L[j][k].x, L[j][k].x, fma(-L[j][k].y, L[j][k].y, p));
+            if (!(p > (T)kPivotTau * gmax)) {
+                fail = true;
+                p = 1;
+            }
+            dinv[j] = rsq(p);
+#pragma unroll
+            for (int i = j + 1; i < NL; ++i) {
+                Cx<T> s = L[i][j];
+#pragma unroll
+                for (int k = 0; k < j; ++k) s = msubc(s, L[i][k], L[j][k]);
+                L[i][j] = cx<T>(s.x * dinv[j], s.y * dinv[j]);
+            }
+        }
+        // a4: X = L^-1 (lower): X_jj = 1/L_jj, X_ij = -(1/L_ii) sum_{m=j}^{i-1} L_im X_mj
+        Cx<T> X[NL][NL];
+#pragma unroll
+        for (int j = 0; j < NL; ++j) {
+            X[j][j] = cx<T>(dinv[j], 0);
+#pragma unroll
+            for (int i = j + 1; i < NL; ++i) {
+                Cx<T> s = cx<T>(0, 0);
+#pragma unroll
+                for (int m = j; m < i; ++m) s = mac(s, L[i][m], X[m][j]);
+                X[i][j] = cx<T>(-s.x * dinv[i], -s.y * dinv[i]);
+            }
+        }
+        // B = X H^H (NL x NR): B_ir = sum_{m<=i} X_im conj(H_rm)
         Cx<T> B[NL][NR];
 #pragma unroll
         for (int i = 0; i < NL; ++i)
@@ -165,7 +177,8 @@ __device__ __forceinline__ void setup_rows(const float2 (&hf)[NR][NL], float sig
             T A = 0;
 #pragma unroll
             for (int i = k; i < NL; ++i) A = fma(X[i][k].x, X[i][k].x, fma(X[i][k].y, X[i][k].y, A));
-            const T mu = fma(-s2, A, (T)1);
+            const T mu = fma(-s2, A, (T)1);  // in T: no cancellation loss
+            // a5 in fp32 (readings R3, R4, R11)
             float sinr, f;
             if (sigma2 == 0.f) {
                 sinr = __int_as_float(0x7f800000);
@@ -181,6 +194,7 @@ __device__ __forceinline__ void setup_rows(const float2 (&hf)[NR][NL], float sig
             }
             o.sinr[k] = sinr;
             o.slope[k] = sinr / norm * llr_scale;
+            // W_kr = sum_{i>=k} conj(X_ik) B_ir, scaled once to fp32 level units
 #pragma unroll
             for (int r = 0; r < NR; ++r) {
                 Cx<T> s = cx<T>(0, 0);
@@ -190,200 +204,250 @@ __device__ __forceinline__ void setup_rows(const float2 (&hf)[NR][NL], float sig
             }
         }
         o.fail = fail;
-        return;
     }
-#pragma unroll
-    for (int kk = 0; kk < NK; ++kk) {
-        const int k = K0 + kk;
-        // row k of G^-1 = X^H X
-        Cx<T> gi[NL];
-#pragma unroll
-        for (int j = 0; j < NL; ++j) {
-            Cx<T> s = cx<T>(0, 0);
-#pragma unroll
-            for (int m = (k > j ? k : j); m < NL; ++m) s = macc(s, X[m][k], X[m][j]);
-            gi[j] = s;
-        }
-        const T A = gi[k].x;
-        const T mu = fma(-s2, A, (T)1);
-        float sinr, f;
-        if (sigma2 == 0.f) {
-            sinr = __int_as_float(0x7f800000);
-            f = sqn;
-        } else {
-            sinr = (float)mu / (float)(s2 * A);
-            f = sqn / (float)mu;
-        }
-        const bool dead = !(mu > 0) || fail;
-        if (dead) {
-            sinr = 0.f;
-            f = 0.f;
-        }
-        o.sinr[kk] = sinr;
-        o.slope[kk] = sinr / norm * llr_scale;
-#pragma unroll
-        for (int r = 0; r < NR; ++r) {
-            Cx<T> s = cx<T>(0, 0);
-#pragma unroll
-            for (int j = 0; j < NL; ++j) s = macb(s, gi[j], h[r][j]);  // G^-1_kj conj(H_rj)
-            o.w[kk][r] = dead ? make_float2(0.f, 0.f) : make_float2((float)s.x * f, (float)s.y * f);
-        }
-    }
-    o.fail = fail;
 }
 
-template <int NR, int NL, int QM, int LT, int TU, int G, bool LAYER_SPLIT, bool ZF, int NK>
-__device__ __forceinline__ void apply_symbols(const DetectArgs& a, const SetupOut<NR, NK>& o, const float2* sy,
-                                              uint64_t* bars, int slot, int sc, int ul, int g, bool active) {
-    constexpr int kLlrBytes = NK * QM * LlrTraits<LT>::bytes;  // this thread's share of one RE
+// y staging modes
+constexpr int kYBulk = 0;    // cp.async.bulk per symbol row into smem, one mbarrier per row
+constexpr int kYLdg = 1;     // direct 256-bit loads, software-pipelined PF symbols ahead
+constexpr int kYAsync = 2;   // per-thread cp.async 16 B into smem, one commit group per symbol
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+// wait until at most n groups are pending (n folds to a constant after unrolling)
+template <int MAXN>
+__device__ __forceinline__ void cp_async_wait_dyn(int n) {
+    if constexpr (MAXN > 0) {
+        if (n >= MAXN) {
+            cp_async_wait<MAXN>();
+            return;
+        }
+        cp_async_wait_dyn<MAXN - 1>(n);
+    } else {
+        cp_async_wait<0>();
+    }
+}
+
+template <int NR, int NL, int QM, int LT, bool ZF>
+__device__ __forceinline__ void apply_re(const DetectArgs& a, const SetupOut<NR, NL>& o, const float2 (&yv)[NR],
+                                         size_t re) {
+    constexpr int kLlrBytes = NL * QM * LlrTraits<LT>::bytes;
     constexpr int kWords = (kLlrBytes + 3) / 4;
-    constexpr int s_first_stride = LAYER_SPLIT ? 1 : G;
-    const float ia = rsqrtf((float)qam_norm(QM));
-    const int k0 = LAYER_SPLIT ? g * NK : 0;
+    float2 x[NL];
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int r = 0; r < NR; ++r) acc = cmac(acc, o.w[k][r], yv[r]);
+        x[k] = acc;
+    }
+    if (a.llr) {
+        float v[NL * QM];
+#pragma unroll
+        for (int k = 0; k < NL; ++k) demap_layer<QM, ZF>(x[k], o.slope[k], v + k * QM);
+        uint32_t w[kWords];
+        pack_llr<LT, NL * QM, ZF>(v, w);
+        store_bytes<kLlrBytes>((char*)a.llr + re * kLlrBytes, w);
+    }
+    if (a.xhat) {
+        const float ia = rsqrtf((float)qam_norm(QM));
+        uint32_t w[2 * NL];
+#pragma unroll
+        for (int k = 0; k < NL; ++k) {
+            w[2 * k] = __float_as_uint(x[k].x * ia);
+            w[2 * k + 1] = __float_as_uint(x[k].y * ia);
+        }
+        store_bytes<NL * 8>(a.xhat + re * NL, w);
+    }
+}
+
+template <int NR, int NL, int QM, int LT, int TU, int G, int YL, bool ZF>
+__device__ __forceinline__ void apply_symbols(const DetectArgs& a, const SetupOut<NR, NL>& o, const float2* sy,
+                                              uint64_t* bars, int slot, int sc, int ul, int g, bool active,
+                                              float2 (*pf)[NR]) {
+    constexpr int NS = (kSym + G - 1) / G;  // symbols per thread (upper bound)
+    if constexpr (YL == kYBulk) {
 #pragma unroll 1
-    for (int s = LAYER_SPLIT ? 0 : g; s < kSym; s += s_first_stride) {
-        mbar_wait(&bars[s], 0);
-        if (!active) continue;
-        float2 yv[NR];
-        const float2* ys = sy + (s * TU + ul) * NR;
+        for (int s = g; s < kSym; s += G) {
+            mbar_wait(&bars[s], 0);
+            if (!active) continue;
+            float2 yv[NR];
+            const float2* ys = sy + (s * TU + ul) * NR;
 #pragma unroll
-        for (int r = 0; r < NR; ++r) yv[r] = ys[r];
-        float2 x[NK];
-#pragma unroll
-        for (int k = 0; k < NK; ++k) {
-            float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int r = 0; r < NR; ++r) acc = cmac(acc, o.w[k][r], yv[r]);
-            x[k] = acc;
+            for (int r = 0; r < NR; ++r) yv[r] = ys[r];
+            apply_re<NR, NL, QM, LT, ZF>(a, o, yv, (size_t)(slot * kSym + s) * a.n_sc + sc);
         }
-        const size_t re = (size_t)(slot * kSym + s) * a.n_sc + sc;
-        if (a.llr) {
-            float v[NK * QM];
+    } else if constexpr (YL == kYAsync) {
+        if (!active) return;
 #pragma unroll
-            for (int k = 0; k < NK; ++k) demap_layer<QM, ZF>(x[k], o.slope[k], v + k * QM);
-            uint32_t w[kWords];
-            pack_llr<LT, NK * QM, ZF>(v, w);
-            store_bytes<kLlrBytes>((char*)a.llr + (re * NL + k0) * QM * LlrTraits<LT>::bytes, w);
-        }
-        if (a.xhat) {
-            uint32_t w[2 * NK];
+        for (int i = 0; i < NS; ++i) {
+            const int s = g + i * G;
+            if (s < kSym) {
+                cp_async_wait_dyn<NS>(NS - 1 - i);
+                float2 yv[NR];
+                const float2* ys = sy + (s * TU + ul) * NR;
 #pragma unroll
-            for (int k = 0; k < NK; ++k) {
-                w[2 * k] = __float_as_uint(x[k].x * ia);
-                w[2 * k + 1] = __float_as_uint(x[k].y * ia);
+                for (int r = 0; r < NR; ++r) yv[r] = ys[r];
+                apply_re<NR, NL, QM, LT, ZF>(a, o, yv, (size_t)(slot * kSym + s) * a.n_sc + sc);
             }
-            store_bytes<NK * 8>(a.xhat + re * NL + k0, w);
         }
-    }
-}
-
-template <int NR, int NL, int QM, int LT, int TU, int G, bool LAYER_SPLIT, typename ST, int K0, int NK>
-__device__ __forceinline__ void unit_work(const DetectArgs& a, const float2* sy, uint64_t* bars, int slot, int sc,
-                                          int ul, int g, bool active) {
-    SetupOut<NR, NK> o;
-    const size_t unit = (size_t)slot * a.n_sc + sc;
-    if (active) {
-        float2 hf[NR][NL];
-        load_bytes<NR * NL * 8>(a.H + unit * NR * NL, reinterpret_cast<uint32_t*>(&hf[0][0]));
-        setup_rows<ST, NR, NL, K0, NK, !LAYER_SPLIT>(hf, a.sigma2, (float)qam_norm(QM), a.llr_scale, o);
-        if (g == 0 && o.fail) atomicAdd(a.fail_count, 1ull);
-        if (a.sinr && (LAYER_SPLIT || g == 0)) {
+    } else {
+        if (!active) return;
+        constexpr int PF = 2;  // prefetch distance (pf holds PF in-flight symbols)
 #pragma unroll
-            for (int k = 0; k < NK; ++k) a.sinr[unit * NL + K0 + k] = o.sinr[k];
+        for (int i = 0; i < NS; ++i) {
+            const int s = g + i * G;
+            if (s < kSym) {
+                float2 yv[NR];
+#pragma unroll
+                for (int r = 0; r < NR; ++r) yv[r] = pf[i % PF][r];
+                const int sn = s + PF * G;
+                if (sn < kSym)
+                    load_bytes<NR * 8>(a.y + ((size_t)(slot * kSym + sn) * a.n_sc + sc) * NR,
+                                       reinterpret_cast<uint32_t*>(&pf[i % PF][0]));
+                apply_re<NR, NL, QM, LT, ZF>(a, o, yv, (size_t)(slot * kSym + s) * a.n_sc + sc);
+            }
         }
     }
-    if (a.sigma2 > 0.f)
-        apply_symbols<NR, NL, QM, LT, TU, G, LAYER_SPLIT, false, NK>(a, o, sy, bars, slot, sc, ul, g, active);
-    else
-        apply_symbols<NR, NL, QM, LT, TU, G, LAYER_SPLIT, true, NK>(a, o, sy, bars, slot, sc, ul, g, active);
 }
 
-template <int NR, int NL, int QM, int LT, int TU, int G, bool LAYER_SPLIT, typename ST>
+template <int NR, int NL, int QM, int LT, int TU, int G, int YL, typename ST>
 __global__ void __launch_bounds__(TU* G) k_tpu(DetectArgs a) {
-    static_assert(NR % 2 == 0, "bulk rows need 16-byte multiples");
-    static_assert(!LAYER_SPLIT || (NL % G == 0 && G <= 4), "layer split needs G | NL");
+    static_assert(NR % 2 == 0, "16-byte y rows");
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
     float2* sy = reinterpret_cast<float2*>(smem + 128);
+    constexpr int NS = (kSym + G - 1) / G;
 
     const int slot = blockIdx.y;
     const int sc0 = blockIdx.x * TU;
     const int nvalid = min(TU, a.n_sc - sc0);
     const int t = threadIdx.x;
     const int ul = t % TU, g = t / TU;
-
-    if (t == 0) {
-#pragma unroll
-        for (int s = 0; s < kSym; ++s) mbar_init(&bars[s], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    if (t == 0) {
-        const uint32_t row_bytes = (uint32_t)nvalid * NR * 8u;
-#pragma unroll 1
-        for (int s = 0; s < kSym; ++s) {
-            mbar_arrive_expect_tx(&bars[s], row_bytes);
-            bulk_g2s(sy + s * TU * NR, a.y + ((size_t)(slot * kSym + s) * a.n_sc + sc0) * NR, row_bytes, &bars[s]);
-        }
-    }
     const bool active = ul < nvalid;
     const int sc = sc0 + ul;
-    if constexpr (!LAYER_SPLIT) {
-        unit_work<NR, NL, QM, LT, TU, G, false, ST, 0, NL>(a, sy, bars, slot, sc, ul, g, active);
+
+    float2 pf[2][NR];
+    if constexpr (YL == kYBulk) {
+        if (t == 0) {
+#pragma unroll
+            for (int s = 0; s < kSym; ++s) mbar_init(&bars[s], 1);
+            fence_mbar_init();
+        }
+        __syncthreads();
+        if (t == 0) {
+            const uint32_t row_bytes = (uint32_t)nvalid * NR * 8u;
+#pragma unroll 1
+            for (int s = 0; s < kSym; ++s) {
+                mbar_arrive_expect_tx(&bars[s], row_bytes);
+                bulk_g2s(sy + s * TU * NR, a.y + ((size_t)(slot * kSym + s) * a.n_sc + sc0) * NR, row_bytes,
+                         &bars[s]);
+            }
+        }
+    } else if constexpr (YL == kYAsync) {
+        if (active) {
+#pragma unroll
+            for (int i = 0; i < NS; ++i) {
+                const int s = g + i * G;
+                if (s < kSym) {
+                    const float2* src = a.y + ((size_t)(slot * kSym + s) * a.n_sc + sc) * NR;
+                    float2* dst = sy + (s * TU + ul) * NR;
+#pragma unroll
+                    for (int c = 0; c < NR / 2; ++c) cp_async16(dst + 2 * c, src + 2 * c);
+                }
+                cp_async_commit();
+            }
+        }
     } else {
-        constexpr int NK = NL / G;
-        if (g == 0) unit_work<NR, NL, QM, LT, TU, G, true, ST, 0, NK>(a, sy, bars, slot, sc, ul, g, active);
-        if constexpr (G > 1)
-            if (g == 1) unit_work<NR, NL, QM, LT, TU, G, true, ST, NK, NK>(a, sy, bars, slot, sc, ul, g, active);
-        if constexpr (G > 2)
-            if (g == 2) unit_work<NR, NL, QM, LT, TU, G, true, ST, 2 * NK, NK>(a, sy, bars, slot, sc, ul, g, active);
-        if constexpr (G > 3)
-            if (g == 3) unit_work<NR, NL, QM, LT, TU, G, true, ST, 3 * NK, NK>(a, sy, bars, slot, sc, ul, g, active);
+        if (active) {
+#pragma unroll
+            for (int i = 0; i < 2; ++i) {
+                const int s = g + i * G;
+                if (s < kSym)
+                    load_bytes<NR * 8>(a.y + ((size_t)(slot * kSym + s) * a.n_sc + sc) * NR,
+                                       reinterpret_cast<uint32_t*>(&pf[i][0]));
+            }
+        }
     }
+
+    SetupOut<NR, NL> o;
+    const size_t unit = (size_t)slot * a.n_sc + sc;
+    if (active) {
+        float2 hf[NR][NL];
+        load_bytes<NR * NL * 8>(a.H + unit * NR * NL, reinterpret_cast<uint32_t*>(&hf[0][0]));
+        setup_unit<ST, NR, NL>(hf, a.sigma2, (float)qam_norm(QM), a.llr_scale, o);
+        if (g == 0) {
+            if (o.fail) atomicAdd(a.fail_count, 1ull);
+            if (a.sinr) {
+#pragma unroll
+                for (int k = 0; k < NL; ++k) a.sinr[unit * NL + k] = o.sinr[k];
+            }
+        }
+    }
+    if (a.sigma2 > 0.f)
+        apply_symbols<NR, NL, QM, LT, TU, G, YL, false>(a, o, sy, bars, slot, sc, ul, g, active, pf);
+    else
+        apply_symbols<NR, NL, QM, LT, TU, G, YL, true>(a, o, sy, bars, slot, sc, ul, g, active, pf);
 }
 
-template <int NR, int NL, int QM, int LT, int TU, int G, bool LS, typename ST>
+template <int NR, int TU, int YL>
+constexpr int smem_bytes() {
+    return YL == kYLdg ? 128 : 128 + kSym * TU * NR * 8;
+}
+
+template <int NR, int NL, int QM, int LT, int TU, int G, int YL, typename ST>
 cudaError_t launch(const DetectArgs& a, cudaStream_t s) {
     if (a.n_sc <= 0 || a.n_slots <= 0) return cudaSuccess;
-    const size_t smem = 128 + (size_t)kSym * TU * NR * 8;
     dim3 grid((a.n_sc + TU - 1) / TU, a.n_slots);
-    k_tpu<NR, NL, QM, LT, TU, G, LS, ST><<<grid, TU * G, smem, s>>>(a);
+    k_tpu<NR, NL, QM, LT, TU, G, YL, ST><<<grid, TU * G, smem_bytes<NR, TU, YL>(), s>>>(a);
     return cudaGetLastError();
 }
 
-template <int NR, int NL, int QM, int LT, int TU, int G, bool LS, typename ST>
+template <int NR, int NL, int QM, int LT, int TU, int G, int YL, typename ST>
 cudaError_t prepare() {
-    const int smem = 128 + kSym * TU * NR * 8;
+    constexpr int smem = smem_bytes<NR, TU, YL>();
     if (smem > 48 * 1024)
-        return cudaFuncSetAttribute(k_tpu<NR, NL, QM, LT, TU, G, LS, ST>,
+        return cudaFuncSetAttribute(k_tpu<NR, NL, QM, LT, TU, G, YL, ST>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return cudaSuccess;
 }
 
-#define TPU_ENTRY(NAME, NR, NL, QM, LT, TU, G, LS, ST)                                        \
+#define TPU_ENTRY(NAME, NR, NL, QM, LT, TU, G, YL, ST)                                        \
     KernelEntry {                                                                              \
-        NAME, NR, NL, QM, 1, 14, LT, 32, 1, launch<NR, NL, QM, LT, TU, G, LS, ST>,            \
-            prepare<NR, NL, QM, LT, TU, G, LS, ST>                                             \
+        NAME, NR, NL, QM, 1, 14, LT, 32, 1, launch<NR, NL, QM, LT, TU, G, YL, ST>,            \
+            prepare<NR, NL, QM, LT, TU, G, YL, ST>                                             \
     }
 
 // First entry matching a plan wins; the rest are selectable by name
 // (MIMO_FORCE_KERNEL) for tuning experiments.
 const KernelEntry kEntries[] = {
-    TPU_ENTRY("tpu_2x2_q2_f32", 2, 2, 2, kLlrF32, 32, 1, false, double),   // C1
-    TPU_ENTRY("tpu_4x4_q4_f32", 4, 4, 4, kLlrF32, 32, 2, true, double),    // C2 (and the paper's 4x4 shape)
-    TPU_ENTRY("tpu_2x2_q4_f32", 2, 2, 4, kLlrF32, 32, 1, false, double),
-    TPU_ENTRY("tpu_2x1_q2_f32", 2, 1, 2, kLlrF32, 32, 1, false, double),
-    TPU_ENTRY("tpu_4x2_q4_f32", 4, 2, 4, kLlrF32, 32, 2, true, double),
-    TPU_ENTRY("tpu_4x4_q4_f16", 4, 4, 4, kLlrF16, 32, 2, true, double),
-    TPU_ENTRY("tpu_4x4_q4_i8", 4, 4, 4, kLlrI8, 32, 2, true, double),
-    TPU_ENTRY("tpu_4x4_q2_f32", 4, 4, 2, kLlrF32, 32, 2, true, double),
-    TPU_ENTRY("tpu_4x4_q6_f32", 4, 4, 6, kLlrF32, 32, 2, true, double),
-    TPU_ENTRY("tpu_4x4_q8_f32", 4, 4, 8, kLlrF32, 32, 2, true, double),
+    TPU_ENTRY("tpu_2x2_q2_f32", 2, 2, 2, kLlrF32, 32, 1, kYBulk, double),   // C1
+    TPU_ENTRY("tpu_4x4_q4_f32", 4, 4, 4, kLlrF32, 32, 2, kYBulk, double),   // C2 (and the paper's 4x4 shape)
+    TPU_ENTRY("tpu_2x2_q4_f32", 2, 2, 4, kLlrF32, 32, 1, kYBulk, double),
+    TPU_ENTRY("tpu_2x1_q2_f32", 2, 1, 2, kLlrF32, 32, 1, kYBulk, double),
+    TPU_ENTRY("tpu_4x2_q4_f32", 4, 2, 4, kLlrF32, 32, 2, kYBulk, double),
+    TPU_ENTRY("tpu_4x4_q4_f16", 4, 4, 4, kLlrF16, 32, 2, kYBulk, double),
+    TPU_ENTRY("tpu_4x4_q4_i8", 4, 4, 4, kLlrI8, 32, 2, kYBulk, double),
+    TPU_ENTRY("tpu_4x4_q2_f32", 4, 4, 2, kLlrF32, 32, 2, kYBulk, double),
+    TPU_ENTRY("tpu_4x4_q6_f32", 4, 4, 6, kLlrF32, 32, 2, kYBulk, double),
+    TPU_ENTRY("tpu_4x4_q8_f32", 4, 4, 8, kLlrF32, 32, 2, kYBulk, double),
     // tuning variants for C2
-    TPU_ENTRY("tpu_4x4_q4_f32_sym2", 4, 4, 4, kLlrF32, 32, 2, false, double),
-    TPU_ENTRY("tpu_4x4_q4_f32_lay4", 4, 4, 4, kLlrF32, 32, 4, true, double),
-    TPU_ENTRY("tpu_4x4_q4_f32_lay2_tu64", 4, 4, 4, kLlrF32, 64, 2, true, double),
-    TPU_ENTRY("tpu_4x4_q4_f32_lay2_fp32setup", 4, 4, 4, kLlrF32, 32, 2, true, float),
+    TPU_ENTRY("tpu_4x4_q4_f32_ldg", 4, 4, 4, kLlrF32, 32, 2, kYLdg, double),
+    TPU_ENTRY("tpu_4x4_q4_f32_async", 4, 4, 4, kLlrF32, 32, 2, kYAsync, double),
+    TPU_ENTRY("tpu_4x4_q4_f32_nosetup", 4, 4, 4, kLlrF32, 32, 2, kYBulk, NoSetup),
+    TPU_ENTRY("tpu_4x4_q4_f32_ldg_nosetup", 4, 4, 4, kLlrF32, 32, 2, kYLdg, NoSetup),
+    TPU_ENTRY("tpu_4x4_q4_f32_async_nosetup", 4, 4, 4, kLlrF32, 32, 2, kYAsync, NoSetup),
+    TPU_ENTRY("tpu_4x4_q4_f32_fp32setup", 4, 4, 4, kLlrF32, 32, 2, kYBulk, float),
+    TPU_ENTRY("tpu_4x4_q4_f32_g1", 4, 4, 4, kLlrF32, 32, 1, kYBulk, double),
+    TPU_ENTRY("tpu_4x4_q4_f32_g4", 4, 4, 4, kLlrF32, 32, 4, kYBulk, double),
+    TPU_ENTRY("tpu_4x4_q4_f32_tu64", 4, 4, 4, kLlrF32, 64, 2, kYBulk, double),
+    TPU_ENTRY("tpu_4x4_q4_f32_tu16", 4, 4, 4, kLlrF32, 16, 2, kYBulk, double),
 };
 
 }  // namespace
