@@ -47,6 +47,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="2")
     ap.add_argument("--kernels", default="")
+    ap.add_argument("--ref", action="store_true", help="also time torch copies of the same byte count")
     args = ap.parse_args()
     k = int(args.config)
     from paper_2510_07843_b200 import mimo
@@ -55,6 +56,17 @@ def main():
     l2 = torch.cuda.get_device_properties(0).L2_cache_size
     n_sets = max(2, math.ceil(3 * l2 / b["total"]))
     H0, y0 = torch.from_numpy(w.H).cuda(), torch.from_numpy(w.y).cuda()
+    if args.ref:
+        for mb in (8, 24, 48, 96, 400):
+            n = int(mb * 1e6 / 2 / 4)
+            nst = max(2, math.ceil(3 * l2 / (mb * 1e6)))
+            bufs = [(torch.empty(n, device="cuda"), torch.empty(n, device="cuda")) for _ in range(nst)]
+            t = time_calls(lambda i: bufs[i][1].copy_(bufs[i][0]), nst)
+            print(f"torch copy {mb:5d} MB traffic: {t:8.2f} us  {mb * 1e6 / t / 1e3:7.1f} GB/s", flush=True)
+            del bufs
+        e = torch.empty(1, device="cuda")
+        t = time_calls(lambda i: e.add_(0), 1)
+        print(f"tiny kernel: {t:8.2f} us", flush=True)
     kernels = [x for x in args.kernels.split(",") if x] or [""]
     for kn in kernels:
         if kn:
