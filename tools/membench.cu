@@ -1,0 +1,60 @@
+// tools/membench.cu -- HBM microbenchmarks used to calibrate the practical
+// roofline of small (tens of MB) streaming kernels on B200.
+// Not part of libmimo.so. Build: nvcc -gencode arch=compute_100a,code=sm_100a
+// -O3 -shared -Xcompiler -fPIC -cudart=static -o tools/libmembench.so tools/membench.cu
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+__device__ __forceinline__ void ld8(const void* p, uint32_t* w) {
+    asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+                 : "l"(p));
+}
+__device__ __forceinline__ void st8(void* p, const uint32_t* w) {
+    asm volatile("st.global.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "r"(w[0]), "r"(w[1]), "r"(w[2]),
+                 "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                 : "memory");
+}
+
+// Read n_rd 32-byte chunks and write n_wr 32-byte chunks (grid-stride, UNR in flight).
+template <int UNR, bool PDL>
+__global__ void rw_kernel(const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, long long n_rd, long long n_wr,
+                          uint32_t* sink) {
+    if (PDL) asm volatile("griddepcontrol.launch_dependents;");
+    const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    const long long nth = (long long)gridDim.x * blockDim.x;
+    uint32_t acc = 0;
+    for (long long i = tid; i < n_rd; i += nth * UNR) {
+        uint32_t w[UNR][8];
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+            if (i + u * nth < n_rd) ld8(src + (i + u * nth) * 32, w[u]);
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+            if (i + u * nth < n_rd) acc ^= w[u][0] ^ w[u][7];
+    }
+    if (PDL) asm volatile("griddepcontrol.wait;" ::: "memory");
+    uint32_t v[8] = {acc, 1, 2, 3, 4, 5, 6, 7};
+    for (long long i = tid; i < n_wr; i += nth) st8(dst + i * 32, v);
+    if (acc == 0x12345678u) sink[0] = acc;
+}
+
+extern "C" int membench_rw(const void* src, void* dst, long long rd_bytes, long long wr_bytes, void* sink,
+                           int blocks, int threads, int pdl, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(threads);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    const uint8_t* a = (const uint8_t*)src;
+    uint8_t* b = (uint8_t*)dst;
+    long long nr = rd_bytes / 32, nw = wr_bytes / 32;
+    cudaError_t e = pdl ? cudaLaunchKernelEx(&cfg, rw_kernel<4, true>, a, b, nr, nw, (uint32_t*)sink)
+                        : cudaLaunchKernelEx(&cfg, rw_kernel<4, false>, a, b, nr, nw, (uint32_t*)sink);
+    return (int)e;
+}
