@@ -79,7 +79,17 @@ typedef struct {
     int sym_per_h;   /* OFDM symbols sharing one H: >= 1 (14 = one H per slot) */
     int llr_type;    /* mimo_llr_type_t */
     float llr_scale; /* multiplier applied to natural-log LLRs before quantisation (> 0, finite) */
+    int flags;       /* bitwise OR of MIMO_PLAN_* flags (0 = none) */
 } mimo_plan_desc_t;
+
+/* Plan flags.
+ * MIMO_PLAN_OVERLAP_CALLS: launch with programmatic dependent launch, so that
+ *   a detect call may start loading H / y and running its per-unit setup while
+ *   the previous detect call on the same stream is still writing its outputs
+ *   (its own writes wait for the previous call to complete). Precondition: a
+ *   call's H and y are not outputs of the immediately preceding detect call on
+ *   the same stream. Work enqueued by anything else orders normally. */
+#define MIMO_PLAN_OVERLAP_CALLS 1
 
 /* Create a plan: validates the descriptor, selects the kernel specialisation
  * for (n_rx, n_layers, qam_order, sc_per_h, sym_per_h, llr_type), allocates the

@@ -35,6 +35,7 @@ struct DetectArgs {
     int n_fb, n_slots;    // n_fb = n_sc / sc_per_h; n_slots = n_sym / sym_per_h
     long long n_units;
     int llr_type;
+    int overlap;          // launch with programmatic dependent launch (MIMO_PLAN_OVERLAP_CALLS)
 };
 
 // Per-axis PAM normalisation of the 38.211 constellations: a = 1/sqrt(norm).
@@ -220,6 +221,15 @@ __device__ __forceinline__ void load_bytes(const void* p, uint32_t* w) {
         }
     }
 }
+
+// ------------------------------------------ programmatic dependent launch ----
+// Kernels call pdl_launch_dependents() first (the next detect call on the
+// stream may start its read-only prologue) and pdl_wait() before their first
+// global write (the previous grid has completed and its writes are visible).
+// Both are no-ops unless the launch carried the programmatic-serialization
+// attribute.
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 // ------------------------------------------- mbarrier + bulk async copy ----
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

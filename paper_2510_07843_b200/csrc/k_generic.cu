@@ -90,6 +90,9 @@ __global__ void __launch_bounds__(kThreads) k_generic(DetectArgs a) {
     __shared__ double sMu[ML];
     __shared__ int sFail;
 
+    // PDL: no overlap here (grid-stride loop writes early), just order after the previous grid
+    pdl_launch_dependents();
+    pdl_wait();
     const int nr = a.n_rx, nl = a.n_layers, tid = threadIdx.x;
     const double s2 = (double)a.sigma2;
     const double norm = (double)qam_norm(QM);
@@ -209,8 +212,7 @@ template <int QM, int LT>
 cudaError_t launch_q(const DetectArgs& a, cudaStream_t s) {
     long long grid = a.n_units < 148LL * 16 ? a.n_units : 148LL * 16;
     if (grid <= 0) return cudaSuccess;
-    k_generic<QM, LT><<<(unsigned)grid, kThreads, 0, s>>>(a);
-    return cudaGetLastError();
+    return launch_kernel(k_generic<QM, LT>, dim3((unsigned)grid), dim3(kThreads), 0, s, a.overlap, a);
 }
 
 template <int QM>

@@ -317,13 +317,27 @@ __device__ __forceinline__ void apply_symbols(const DetectArgs& a, const SetupOu
     }
 }
 
-template <int NR, int NL, int QM, int LT, int TU, int G, int YL, typename ST>
+// Shared-memory layout: [14 mbarriers | pad to 128 B][y tile 14 x TU x NR float2]
+//                       [W~ broadcast: NL*NR float2 x TU][slopes: NL x TU] (SHARE only)
+template <int NR, int NL, int TU, int YL, bool SHARE>
+constexpr int smem_bytes() {
+    return 128 + (YL == kYLdg ? 0 : kSym * TU * NR * 8) + (SHARE ? TU * (NL * NR * 8 + NL * 4) : 0);
+}
+
+// SHARE: only warp 0 runs the setup and broadcasts W~ / slopes through shared
+// memory to the other G-1 warps (no duplicated fp64 work).
+template <int NR, int NL, int QM, int LT, int TU, int G, int YL, typename ST, bool SHARE>
 __global__ void __launch_bounds__(TU* G) k_tpu(DetectArgs a) {
     static_assert(NR % 2 == 0, "16-byte y rows");
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
     float2* sy = reinterpret_cast<float2*>(smem + 128);
+    float2* sW = reinterpret_cast<float2*>(smem + 128 + (YL == kYLdg ? 0 : kSym * TU * NR * 8));
+    float* sSlope = reinterpret_cast<float*>(sW + NL * NR * TU);
     constexpr int NS = (kSym + G - 1) / G;
+
+    // PDL: let the next detect call on this stream start its (read-only) prologue now.
+    pdl_launch_dependents();
 
     const int slot = blockIdx.y;
     const int sc0 = blockIdx.x * TU;
@@ -332,6 +346,12 @@ __global__ void __launch_bounds__(TU* G) k_tpu(DetectArgs a) {
     const int ul = t % TU, g = t / TU;
     const bool active = ul < nvalid;
     const int sc = sc0 + ul;
+    const size_t unit = (size_t)slot * a.n_sc + sc;
+    const bool does_setup = active && (!SHARE || g == 0);
+
+    // a1: H first (it is on the setup's critical path), then the y tile
+    float2 hf[NR][NL];
+    if (does_setup) load_bytes<NR * NL * 8>(a.H + unit * NR * NL, reinterpret_cast<uint32_t*>(&hf[0][0]));
 
     float2 pf[2][NR];
     if constexpr (YL == kYBulk) {
@@ -377,17 +397,33 @@ __global__ void __launch_bounds__(TU* G) k_tpu(DetectArgs a) {
     }
 
     SetupOut<NR, NL> o;
-    const size_t unit = (size_t)slot * a.n_sc + sc;
-    if (active) {
-        float2 hf[NR][NL];
-        load_bytes<NR * NL * 8>(a.H + unit * NR * NL, reinterpret_cast<uint32_t*>(&hf[0][0]));
-        setup_unit<ST, NR, NL>(hf, a.sigma2, (float)qam_norm(QM), a.llr_scale, o);
-        if (g == 0) {
-            if (o.fail) atomicAdd(a.fail_count, 1ull);
-            if (a.sinr) {
+    if (does_setup) setup_unit<ST, NR, NL>(hf, a.sigma2, (float)qam_norm(QM), a.llr_scale, o);
+    if constexpr (SHARE) {
+        if (does_setup) {
 #pragma unroll
-                for (int k = 0; k < NL; ++k) a.sinr[unit * NL + k] = o.sinr[k];
+            for (int k = 0; k < NL; ++k) {
+#pragma unroll
+                for (int r = 0; r < NR; ++r) sW[(k * NR + r) * TU + ul] = o.w[k][r];
+                sSlope[k * TU + ul] = o.slope[k];
             }
+        }
+        __syncthreads();
+        if (active && g != 0) {
+#pragma unroll
+            for (int k = 0; k < NL; ++k) {
+#pragma unroll
+                for (int r = 0; r < NR; ++r) o.w[k][r] = sW[(k * NR + r) * TU + ul];
+                o.slope[k] = sSlope[k * TU + ul];
+            }
+        }
+    }
+    // PDL: all global writes come after the previous grid has completed.
+    pdl_wait();
+    if (does_setup && g == 0) {
+        if (o.fail) atomicAdd(a.fail_count, 1ull);
+        if (a.sinr) {
+#pragma unroll
+            for (int k = 0; k < NL; ++k) a.sinr[unit * NL + k] = o.sinr[k];
         }
     }
     if (a.sigma2 > 0.f)
@@ -396,33 +432,29 @@ __global__ void __launch_bounds__(TU* G) k_tpu(DetectArgs a) {
         apply_symbols<NR, NL, QM, LT, TU, G, YL, true>(a, o, sy, bars, slot, sc, ul, g, active, pf);
 }
 
-template <int NR, int TU, int YL>
-constexpr int smem_bytes() {
-    return YL == kYLdg ? 128 : 128 + kSym * TU * NR * 8;
-}
-
-template <int NR, int NL, int QM, int LT, int TU, int G, int YL, typename ST>
+template <int NR, int NL, int QM, int LT, int TU, int G, int YL, typename ST, bool SH>
 cudaError_t launch(const DetectArgs& a, cudaStream_t s) {
     if (a.n_sc <= 0 || a.n_slots <= 0) return cudaSuccess;
     dim3 grid((a.n_sc + TU - 1) / TU, a.n_slots);
-    k_tpu<NR, NL, QM, LT, TU, G, YL, ST><<<grid, TU * G, smem_bytes<NR, TU, YL>(), s>>>(a);
-    return cudaGetLastError();
+    return launch_kernel(k_tpu<NR, NL, QM, LT, TU, G, YL, ST, SH>, grid, dim3(TU * G),
+                         smem_bytes<NR, NL, TU, YL, SH>(), s, a.overlap, a);
 }
 
-template <int NR, int NL, int QM, int LT, int TU, int G, int YL, typename ST>
+template <int NR, int NL, int QM, int LT, int TU, int G, int YL, typename ST, bool SH>
 cudaError_t prepare() {
-    constexpr int smem = smem_bytes<NR, TU, YL>();
+    constexpr int smem = smem_bytes<NR, NL, TU, YL, SH>();
     if (smem > 48 * 1024)
-        return cudaFuncSetAttribute(k_tpu<NR, NL, QM, LT, TU, G, YL, ST>,
+        return cudaFuncSetAttribute(k_tpu<NR, NL, QM, LT, TU, G, YL, ST, SH>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return cudaSuccess;
 }
 
-#define TPU_ENTRY(NAME, NR, NL, QM, LT, TU, G, YL, ST)                                        \
+#define TPU_ENTRY2(NAME, NR, NL, QM, LT, TU, G, YL, ST, SH)                                   \
     KernelEntry {                                                                              \
-        NAME, NR, NL, QM, 1, 14, LT, 32, 1, launch<NR, NL, QM, LT, TU, G, YL, ST>,            \
-            prepare<NR, NL, QM, LT, TU, G, YL, ST>                                             \
+        NAME, NR, NL, QM, 1, 14, LT, 32, 1, launch<NR, NL, QM, LT, TU, G, YL, ST, SH>,        \
+            prepare<NR, NL, QM, LT, TU, G, YL, ST, SH>                                         \
     }
+#define TPU_ENTRY(NAME, NR, NL, QM, LT, TU, G, YL, ST) TPU_ENTRY2(NAME, NR, NL, QM, LT, TU, G, YL, ST, false)
 
 // First entry matching a plan wins; the rest are selectable by name
 // (MIMO_FORCE_KERNEL) for tuning experiments.
@@ -448,6 +480,9 @@ const KernelEntry kEntries[] = {
     TPU_ENTRY("tpu_4x4_q4_f32_g4", 4, 4, 4, kLlrF32, 32, 4, kYBulk, double),
     TPU_ENTRY("tpu_4x4_q4_f32_tu64", 4, 4, 4, kLlrF32, 64, 2, kYBulk, double),
     TPU_ENTRY("tpu_4x4_q4_f32_tu16", 4, 4, 4, kLlrF32, 16, 2, kYBulk, double),
+    TPU_ENTRY2("tpu_4x4_q4_f32_share2", 4, 4, 4, kLlrF32, 32, 2, kYBulk, double, true),
+    TPU_ENTRY2("tpu_4x4_q4_f32_share4", 4, 4, 4, kLlrF32, 32, 4, kYBulk, double, true),
+    TPU_ENTRY2("tpu_4x4_q4_f32_share2_tu64", 4, 4, 4, kLlrF32, 64, 2, kYBulk, double, true),
 };
 
 }  // namespace

@@ -9,6 +9,24 @@ namespace mimo {
 
 using LaunchFn = cudaError_t (*)(const DetectArgs&, cudaStream_t);
 
+// cudaLaunchKernelEx with the programmatic-stream-serialization attribute when
+// `pdl` is set (the kernel must use pdl_launch_dependents / pdl_wait).
+template <typename K>
+inline cudaError_t launch_kernel(K kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s, int pdl,
+                                 const DetectArgs& a) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, a);
+}
+
 // A specialised kernel serves exactly one (n_rx, n_layers, qm, sc_per_h,
 // sym_per_h, llr_type) tuple; `align` is the byte alignment it needs of H, y,
 // llr and xhat (else the dispatcher falls back to the generic kernel).

@@ -122,6 +122,7 @@ mimo::DetectArgs make_args(mimo_plan_t p, const void* H, const void* y, float si
     a.n_slots = n_sym / p->d.sym_per_h;
     a.n_units = (long long)a.n_fb * a.n_slots;
     a.llr_type = p->d.llr_type;
+    a.overlap = (p->d.flags & MIMO_PLAN_OVERLAP_CALLS) ? 1 : 0;
     return a;
 }
 
@@ -182,6 +183,7 @@ mimo_status_t mimo_plan_create(const mimo_plan_desc_t* desc, mimo_plan_t* out) {
     if (d.llr_type < 0 || d.llr_type > 2) return arg_fail(nullptr, "llr_type must be 0, 1 or 2");
     if (!(d.llr_scale > 0.f) || !std::isfinite(d.llr_scale)) return arg_fail(nullptr, "llr_scale must be finite > 0");
     if (d.device < 0) return arg_fail(nullptr, "device must be >= 0");
+    if (d.flags & ~MIMO_PLAN_OVERLAP_CALLS) return arg_fail(nullptr, "unknown plan flags");
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
     if (e != cudaSuccess) {

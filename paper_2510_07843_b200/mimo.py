@@ -28,6 +28,7 @@ MIMO_ERR_NOT_PD = 4
 MIMO_ERR_OOM = 5
 
 LLR_F32, LLR_F16, LLR_I8 = 0, 1, 2
+PLAN_OVERLAP_CALLS = 1
 SYM_PER_SLOT = 14
 
 
@@ -40,7 +41,8 @@ class MimoError(RuntimeError):
 class _Desc(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("n_rx", ctypes.c_int),
                 ("n_layers", ctypes.c_int), ("qam_order", ctypes.c_int), ("sc_per_h", ctypes.c_int),
-                ("sym_per_h", ctypes.c_int), ("llr_type", ctypes.c_int), ("llr_scale", ctypes.c_float)]
+                ("sym_per_h", ctypes.c_int), ("llr_type", ctypes.c_int), ("llr_scale", ctypes.c_float),
+                ("flags", ctypes.c_int)]
 
 
 _lib = None
@@ -111,7 +113,7 @@ class Plan:
 
     def __init__(self, n_rx: int, n_layers: int, qm: int, *, sc_per_h: int = 1,
                  sym_per_h: int = SYM_PER_SLOT, llr_dtype="f32", llr_scale: float = 1.0,
-                 device=None, stream=None):
+                 device=None, stream=None, overlap_calls: bool = False):
         import torch
         L = load_library()
         if not torch.cuda.is_available():
@@ -130,7 +132,7 @@ class Plan:
         self.llr_dtype = _llr_torch_dtype(self.llr_type)
         self._fixed_stream = stream
         d = _Desc(dev.index, ctypes.c_void_p(self._stream_ptr()), n_rx, n_layers, qm, sc_per_h, sym_per_h,
-                  self.llr_type, float(llr_scale))
+                  self.llr_type, float(llr_scale), PLAN_OVERLAP_CALLS if overlap_calls else 0)
         h = ctypes.c_void_p()
         st = L.mimo_plan_create(ctypes.byref(d), ctypes.byref(h))
         if st != MIMO_OK:

@@ -45,16 +45,16 @@ def test_abi_version_and_status_strings(lib):
 
 def _desc(**kw):
     d = dict(device=0, stream=None, n_rx=4, n_layers=4, qam_order=4, sc_per_h=1, sym_per_h=14,
-             llr_type=0, llr_scale=1.0)
+             llr_type=0, llr_scale=1.0, flags=0)
     d.update(kw)
     return mimo._Desc(d["device"], d["stream"], d["n_rx"], d["n_layers"], d["qam_order"], d["sc_per_h"],
-                      d["sym_per_h"], d["llr_type"], d["llr_scale"])
+                      d["sym_per_h"], d["llr_type"], d["llr_scale"], d["flags"])
 
 
 @pytest.mark.parametrize("bad", [dict(n_rx=0), dict(n_rx=65), dict(n_layers=5), dict(n_layers=0),
                                  dict(qam_order=16), dict(qam_order=3), dict(sc_per_h=0), dict(sym_per_h=0),
                                  dict(llr_type=3), dict(llr_scale=0.0), dict(llr_scale=float("nan")),
-                                 dict(device=-1), dict(n_rx=32, n_layers=17)])
+                                 dict(device=-1), dict(n_rx=32, n_layers=17), dict(flags=2)])
 def test_create_rejects_bad_descriptor(lib, bad):
     h = ctypes.c_void_p()
     st = lib.mimo_plan_create(ctypes.byref(_desc(**bad)), ctypes.byref(h))

@@ -121,3 +121,35 @@ def test_cuda_graph_capture():
     g.replay()
     torch.cuda.synchronize()
     assert torch.equal(out, ref)
+
+
+def test_overlap_calls_same_output_buffer():
+    """MIMO_PLAN_OVERLAP_CALLS: back-to-back calls (PDL) writing one output buffer stay ordered."""
+    import torch
+    ws = [synth.generate(2, n_sc=3276, n_slots=2, seed=s) for s in (1, 2, 3)]
+    ref_plan = mimo.Plan(4, 4, 4)
+    refs = [ref_plan.detect(torch.from_numpy(w.H).cuda(), torch.from_numpy(w.y).cuda(), float(w.sigma2)).clone()
+            for w in ws]
+    plan = mimo.Plan(4, 4, 4, overlap_calls=True)
+    Hs = [torch.from_numpy(w.H).cuda() for w in ws]
+    ys = [torch.from_numpy(w.y).cuda() for w in ws]
+    out = torch.empty_like(refs[0])
+    outs = [torch.empty_like(refs[0]) for _ in ws]
+    torch.cuda.synchronize()
+    for rep in range(20):
+        for i, w in enumerate(ws):
+            plan.detect(Hs[i], ys[i], float(w.sigma2), out=out)
+            plan.detect(Hs[i], ys[i], float(w.sigma2), out=outs[i])
+    torch.cuda.synchronize()
+    assert torch.equal(out, refs[-1])
+    for o, r in zip(outs, refs):
+        assert torch.equal(o, r)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+def test_overlap_mode_parity(k):
+    import parity
+    w = synth.generate(k, n_sc=120 if k != 1 else 12, n_slots=2 if k != 1 else 1)
+    plan = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, llr_dtype=w.llr, overlap_calls=True)
+    g = parity.run_gpu(w, plan=plan)
+    parity.compare(w, g)

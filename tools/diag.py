@@ -48,6 +48,7 @@ def main():
     ap.add_argument("--config", default="2")
     ap.add_argument("--kernels", default="")
     ap.add_argument("--ref", action="store_true", help="also time torch copies of the same byte count")
+    ap.add_argument("--overlap", default="0", help="comma list of overlap modes to time (0,1)")
     args = ap.parse_args()
     k = int(args.config)
     from paper_2510_07843_b200 import mimo
@@ -68,10 +69,10 @@ def main():
         t = time_calls(lambda i: e.add_(0), 1)
         print(f"tiny kernel: {t:8.2f} us", flush=True)
     kernels = [x for x in args.kernels.split(",") if x] or [""]
-    for kn in kernels:
+    for kn, ov in [(kn, int(ov)) for kn in kernels for ov in args.overlap.split(",")]:
         if kn:
             os.environ["MIMO_FORCE_KERNEL"] = kn
-        plan = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, llr_dtype=w.llr)
+        plan = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, llr_dtype=w.llr, overlap_calls=bool(ov))
         sh = plan.shapes(w.n_sc, w.n_sym)
         sets = [(H0.clone(), y0.clone(), torch.empty(sh["llr"], dtype=plan.llr_dtype, device="cuda"),
                  torch.empty(sh["sinr"], device="cuda"), torch.empty(sh["xhat"], dtype=torch.complex64, device="cuda"))
@@ -80,7 +81,7 @@ def main():
         full = time_calls(lambda i: plan.detect(sets[i][0], sets[i][1], s2, out=sets[i][2]), n_sets)
         setup = time_calls(lambda i: plan.detect(sets[i][0], sets[i][1], s2, sinr=sets[i][3], want_llr=False), n_sets)
         dbg = time_calls(lambda i: plan.detect(sets[i][0], sets[i][1], s2, out=sets[i][2], xhat=sets[i][4]), n_sets)
-        print(f"{plan.kernel_name:40s} full {full:8.2f} us ({b['total'] / full / 1e3:7.1f} GB/s)  "
+        print(f"{plan.kernel_name:36s} ov={ov} full {full:8.2f} us ({b['total'] / full / 1e3:7.1f} GB/s)  "
               f"setup-only {setup:8.2f} us  llr+xhat {dbg:8.2f} us", flush=True)
         del sets
         plan.close()
