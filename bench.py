@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU budget of the oracle baseline")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no graphs, no e2e/cpu legs)")
+    ap.add_argument("--overlap", type=int, default=1,
+                    help="1: back-to-back calls overlap via PDL (MIMO_PLAN_OVERLAP_CALLS); 0: serialised")
     return ap.parse_args()
 
 
@@ -246,7 +248,9 @@ def run_ours(args, k):
     s0, s1 = shard.weak_slots(c["n_slots"], rank)
     w = synth.generate(k, seed=shard.shard_seed(base_seed, rank))
     b = synth.config_algorithmic_bytes(k)
-    plan = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, llr_dtype=w.llr, device=local)
+    plan = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, llr_dtype=w.llr, device=local,
+                     overlap_calls=bool(args.overlap))
+    plan1 = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, llr_dtype=w.llr, device=local)
 
     # rotating buffer sets: working set >= 3x L2 so every step streams from HBM
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
@@ -316,6 +320,23 @@ def run_ours(args, k):
             dist.barrier()
     elapsed_ms = ev0.elapsed_time(ev1)
     n_failed = plan.sync_status()
+
+    # context: the same steps with calls serialised (no PDL overlap) -> single-call device time
+    def step1(i):
+        H, y, out = sets[i % n_sets]
+        plan1.detect(H, y, s2, out=out)
+    g1 = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        step1(0)
+        with torch.cuda.graph(g1, stream=stream):
+            for i in range(S):
+                step1(i)
+        g1.replay()
+        ev0.record(stream)
+        g1.replay()
+        ev1.record(stream)
+    stream.synchronize()
+    single_us = ev0.elapsed_time(ev1) * 1e3 / S
     assert n_failed == 0, f"{n_failed} units failed the Cholesky guard"
     t_max_ms = shard.max_over_ranks(elapsed_ms, device=dev)
     n_re_all = b["n_re"] * K * world
@@ -360,6 +381,8 @@ def run_ours(args, k):
                 "l2_flush": f"{n_sets} rotating buffer sets x {b['total'] / 1e6:.1f} MB = "
                             f"{n_sets * b['total'] / 1e6:.0f} MB > 3x L2 ({l2 / 1e6:.0f} MB)",
                 "graph_steps": S, "kernel": plan.kernel_name,
+                "call_overlap": "PDL (MIMO_PLAN_OVERLAP_CALLS): call i+1 loads/sets up while call i stores"
+                                if args.overlap else "none (serialised calls)",
                 "parallelism": f"slot-sharded x{world}, no collective" if world > 1 else "single GPU"})
     line = {
         "metric": METRIC,
@@ -372,7 +395,9 @@ def run_ours(args, k):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"], "traffic": ncu_traffic(k),
                      "algorithmic_bytes_per_launch": b["total"], "peak_src": peaks["src"],
-                     "kernel_us": per_launch_s * 1e6},
+                     "kernel_us": per_launch_s * 1e6,
+                     "serialised_call_us": single_us,
+                     "serialised_frac": b["total"] / (single_us * 1e-6) / 1e9 / peaks["hbm_gbs"]},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "clocks": clocks,

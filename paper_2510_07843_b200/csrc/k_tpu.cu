@@ -459,30 +459,26 @@ cudaError_t prepare() {
 // First entry matching a plan wins; the rest are selectable by name
 // (MIMO_FORCE_KERNEL) for tuning experiments.
 const KernelEntry kEntries[] = {
-    TPU_ENTRY("tpu_2x2_q2_f32", 2, 2, 2, kLlrF32, 32, 1, kYBulk, double),   // C1
-    TPU_ENTRY("tpu_4x4_q4_f32", 4, 4, 4, kLlrF32, 32, 2, kYBulk, double),   // C2 (and the paper's 4x4 shape)
+    TPU_ENTRY("tpu_2x2_q2_f32", 2, 2, 2, kLlrF32, 32, 1, kYBulk, double),                 // C1
+    TPU_ENTRY2("tpu_4x4_q4_f32", 4, 4, 4, kLlrF32, 64, 2, kYBulk, double, true),          // C2, paper 4x4
     TPU_ENTRY("tpu_2x2_q4_f32", 2, 2, 4, kLlrF32, 32, 1, kYBulk, double),
     TPU_ENTRY("tpu_2x1_q2_f32", 2, 1, 2, kLlrF32, 32, 1, kYBulk, double),
-    TPU_ENTRY("tpu_4x2_q4_f32", 4, 2, 4, kLlrF32, 32, 2, kYBulk, double),
-    TPU_ENTRY("tpu_4x4_q4_f16", 4, 4, 4, kLlrF16, 32, 2, kYBulk, double),
-    TPU_ENTRY("tpu_4x4_q4_i8", 4, 4, 4, kLlrI8, 32, 2, kYBulk, double),
-    TPU_ENTRY("tpu_4x4_q2_f32", 4, 4, 2, kLlrF32, 32, 2, kYBulk, double),
-    TPU_ENTRY("tpu_4x4_q6_f32", 4, 4, 6, kLlrF32, 32, 2, kYBulk, double),
-    TPU_ENTRY("tpu_4x4_q8_f32", 4, 4, 8, kLlrF32, 32, 2, kYBulk, double),
-    // tuning variants for C2
-    TPU_ENTRY("tpu_4x4_q4_f32_ldg", 4, 4, 4, kLlrF32, 32, 2, kYLdg, double),
+    TPU_ENTRY2("tpu_4x2_q4_f32", 4, 2, 4, kLlrF32, 64, 2, kYBulk, double, true),
+    TPU_ENTRY2("tpu_4x4_q4_f16", 4, 4, 4, kLlrF16, 64, 2, kYBulk, double, true),
+    TPU_ENTRY2("tpu_4x4_q4_i8", 4, 4, 4, kLlrI8, 64, 2, kYBulk, double, true),
+    TPU_ENTRY2("tpu_4x4_q2_f32", 4, 4, 2, kLlrF32, 64, 2, kYBulk, double, true),
+    TPU_ENTRY2("tpu_4x4_q6_f32", 4, 4, 6, kLlrF32, 64, 2, kYBulk, double, true),
+    TPU_ENTRY2("tpu_4x4_q8_f32", 4, 4, 8, kLlrF32, 64, 2, kYBulk, double, true),
+    // tuning variants for C2 (MIMO_FORCE_KERNEL)
+    TPU_ENTRY("tpu_4x4_q4_f32_dup2_tu32", 4, 4, 4, kLlrF32, 32, 2, kYBulk, double),
     TPU_ENTRY("tpu_4x4_q4_f32_async", 4, 4, 4, kLlrF32, 32, 2, kYAsync, double),
+    TPU_ENTRY("tpu_4x4_q4_f32_ldg", 4, 4, 4, kLlrF32, 32, 2, kYLdg, double),
     TPU_ENTRY("tpu_4x4_q4_f32_nosetup", 4, 4, 4, kLlrF32, 32, 2, kYBulk, NoSetup),
-    TPU_ENTRY("tpu_4x4_q4_f32_ldg_nosetup", 4, 4, 4, kLlrF32, 32, 2, kYLdg, NoSetup),
-    TPU_ENTRY("tpu_4x4_q4_f32_async_nosetup", 4, 4, 4, kLlrF32, 32, 2, kYAsync, NoSetup),
     TPU_ENTRY("tpu_4x4_q4_f32_fp32setup", 4, 4, 4, kLlrF32, 32, 2, kYBulk, float),
-    TPU_ENTRY("tpu_4x4_q4_f32_g1", 4, 4, 4, kLlrF32, 32, 1, kYBulk, double),
-    TPU_ENTRY("tpu_4x4_q4_f32_g4", 4, 4, 4, kLlrF32, 32, 4, kYBulk, double),
-    TPU_ENTRY("tpu_4x4_q4_f32_tu64", 4, 4, 4, kLlrF32, 64, 2, kYBulk, double),
-    TPU_ENTRY("tpu_4x4_q4_f32_tu16", 4, 4, 4, kLlrF32, 16, 2, kYBulk, double),
-    TPU_ENTRY2("tpu_4x4_q4_f32_share2", 4, 4, 4, kLlrF32, 32, 2, kYBulk, double, true),
-    TPU_ENTRY2("tpu_4x4_q4_f32_share4", 4, 4, 4, kLlrF32, 32, 4, kYBulk, double, true),
-    TPU_ENTRY2("tpu_4x4_q4_f32_share2_tu64", 4, 4, 4, kLlrF32, 64, 2, kYBulk, double, true),
+    TPU_ENTRY2("tpu_4x4_q4_f32_share2_tu128", 4, 4, 4, kLlrF32, 128, 2, kYBulk, double, true),
+    TPU_ENTRY2("tpu_4x4_q4_f32_share2_tu64_async", 4, 4, 4, kLlrF32, 64, 2, kYAsync, double, true),
+    TPU_ENTRY2("tpu_4x4_q4_f32_share3_tu64", 4, 4, 4, kLlrF32, 64, 3, kYBulk, double, true),
+    TPU_ENTRY2("tpu_4x4_q4_f32_share2_tu96", 4, 4, 4, kLlrF32, 96, 2, kYBulk, double, true),
 };
 
 }  // namespace
