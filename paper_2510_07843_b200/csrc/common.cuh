@@ -83,6 +83,20 @@ __device__ __forceinline__ double dnorm2(double2 a) { return fma(a.x, a.x, a.y *
 // distance gap gives 0 instead of NaN, and the caller saturates.
 template <int M, bool ZF>
 __device__ __forceinline__ void demap_axis(float u, float slope, float* out, int stride) {
+    if constexpr (!ZF && M <= 2) {
+        // QPSK / 16-QAM: the same max-log values in their linear-region form
+        // (D_1 - D_0 = (b - a)(2u - a - b) between fixed nearest points a, b):
+        //   QPSK      bit 0: 4u
+        //   16-QAM    bit 0: 4(u + sgn(u) max(|u| - 2, 0)),  bit 1: 4(2 - |u|)
+        const float s4 = 4.f * slope;
+        if constexpr (M == 1) {
+            out[0] = s4 * u;
+        } else {
+            out[0] = s4 * (u + copysignf(fmaxf(fabsf(u) - 2.f, 0.f), u));
+            out[stride] = s4 * (2.f - fabsf(u));
+        }
+        return;
+    }
     constexpr float lim = float((1 << M) - 1);
     const float sq = fminf(fmaxf(fmaf(2.f, floorf(0.5f * u), 1.f), -lim), lim);
     const float e = u - sq;

@@ -455,3 +455,23 @@ def test_golden_handworked():
         assert np.allclose(r["xhat"][0], xr, atol=1e-12), c["name"]
         assert np.allclose(r["sinr"], c["sinr"], rtol=1e-12), c["name"]
         assert np.allclose(r["llr"][0], np.array(c["llr"]), rtol=1e-12, atol=1e-12), c["name"]
+
+
+@pytest.mark.parametrize("qm", [2, 4])
+def test_p10_linear_forms_equal_bruteforce(qm):
+    """QPSK / 16-QAM linear-region forms used by the CUDA demapper (sigma2 > 0 path) = brute force."""
+    a = 1 / np.sqrt({2: 2, 4: 10}[qm])
+    grid = np.arange(-7, 7.01, 0.125) * a
+    X = np.concatenate([(grid[:, None] + 1j * grid[None, :]).ravel(), cn(3000) * 2.0])
+    s = 3.25
+    bf = oracle.maxlog(qm, X, s)
+    out = np.zeros(X.shape + (qm,))
+    sa = s * a * a
+    for off, comp in ((0, X.real), (1, X.imag)):
+        u = comp / a
+        if qm == 2:
+            out[:, off] = 4 * sa * u
+        else:
+            out[:, off] = 4 * sa * (u + np.sign(u) * np.maximum(np.abs(u) - 2, 0))
+            out[:, 2 + off] = 4 * sa * (2 - np.abs(u))
+    assert np.abs(bf - out).max() <= 1e-9 * max(1, np.abs(bf).max())
