@@ -131,6 +131,12 @@ mimo_status_t mimo_detect_mmse_host(mimo_plan_t plan, const void* H_host, const 
                                     float sigma2, int n_rx, int n_layers, int n_sc, int n_sym,
                                     int qam_order, void* llr_host);
 
+/* Pre-allocate the plan's kernel workspace for calls of up to n_sc x n_sym
+ * (some kernel families keep per-unit W~ in a plan-owned buffer). Calls grow the
+ * workspace on demand, but not while the stream is being captured into a CUDA
+ * graph: reserve before capturing. Errors: INVALID_ARG, CUDA, OOM. */
+mimo_status_t mimo_plan_reserve(mimo_plan_t plan, int n_sc, int n_sym);
+
 /* Synchronise the plan's stream, return the number of units flagged by the
  * Cholesky guard since the previous call (and reset the count). Returns
  * MIMO_ERR_NOT_PD if that number is > 0, MIMO_ERR_CUDA on a sticky CUDA

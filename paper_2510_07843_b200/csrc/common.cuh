@@ -36,6 +36,7 @@ struct DetectArgs {
     long long n_units;
     int llr_type;
     int overlap;          // launch with programmatic dependent launch (MIMO_PLAN_OVERLAP_CALLS)
+    void* ws;             // plan-owned workspace (kernel families that need one)
 };
 
 // Per-axis PAM normalisation of the 38.211 constellations: a = 1/sqrt(norm).
@@ -214,6 +215,14 @@ __device__ __forceinline__ void ld_v4(const void* p, uint32_t* w) {
     asm volatile("ld.global.nc.v4.b32 {%0,%1,%2,%3}, [%4];"
                  : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
                  : "l"(p));
+}
+
+// Coherent (non-.nc) 256-bit load, for data written by an earlier kernel of the same call.
+__device__ __forceinline__ void ld_v8_coherent(const void* p, uint32_t* w) {
+    asm volatile("ld.global.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7])
+                 : "l"(p)
+                 : "memory");
 }
 
 // Load NB bytes (NB % 16 == 0, p 16- or 32-aligned accordingly) into words.

@@ -38,12 +38,15 @@ struct KernelEntry {
     LaunchFn launch;
     // Optional: configure function attributes once at plan creation.
     cudaError_t (*prepare)();
+    // Optional: bytes of plan-owned workspace one call needs (DetectArgs::ws).
+    size_t (*workspace)(const DetectArgs&);
 };
 
 // Tables provided by each kernel family (k_*.cu).
 const KernelEntry* tpu_entries(int* n);
 const KernelEntry* prb_entries(int* n);
 const KernelEntry* prbp_entries(int* n);
+const KernelEntry* split_entries(int* n);
 
 // Generic kernel: any n_rx <= 64, n_layers <= min(16, n_rx), qm, sc_per_h,
 // sym_per_h, llr_type; 8-byte alignment.

@@ -42,6 +42,9 @@ struct mimo_plan_s {
     size_t ws_bytes = 0;
     cudaStream_t hs[2] = {nullptr, nullptr};
     cudaEvent_t ev = nullptr;
+    // kernel workspaces: slot 0 for the plan's stream, 1..2 for the host path's streams
+    void* kws[3] = {nullptr, nullptr, nullptr};
+    size_t kws_bytes[3] = {0, 0, 0};
 };
 
 namespace {
@@ -63,7 +66,7 @@ mimo_status_t arg_fail(mimo_plan_t p, const char* what) {
 // (a tuning/debug knob) picks a named variant instead, or "generic".
 const mimo::KernelEntry* select_fast(const mimo_plan_desc_t& d) {
     using LF = const mimo::KernelEntry* (*)(int*);
-    const LF tables[] = {mimo::tpu_entries, mimo::prbp_entries, mimo::prb_entries};
+    const LF tables[] = {mimo::tpu_entries, mimo::split_entries, mimo::prb_entries, mimo::prbp_entries};
     const char* force = getenv("MIMO_FORCE_KERNEL");
     if (force && strcmp(force, "generic") == 0) return nullptr;
     for (LF f : tables) {
@@ -126,12 +129,43 @@ mimo::DetectArgs make_args(mimo_plan_t p, const void* H, const void* y, float si
     return a;
 }
 
-mimo_status_t launch(mimo_plan_t p, const mimo::DetectArgs& a, cudaStream_t s) {
+// Make sure workspace slot `slot` holds `need` bytes. Growing is refused while
+// the stream is being captured (call mimo_plan_reserve before capturing).
+mimo_status_t ensure_ws(mimo_plan_t p, int slot, size_t need, cudaStream_t s) {
+    if (p->kws_bytes[slot] >= need) return MIMO_OK;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (s) cudaStreamIsCapturing(s, &cs);
+    if (cs != cudaStreamCaptureStatusNone)
+        return arg_fail(p, "workspace too small while capturing a graph: call mimo_plan_reserve first");
+    cudaError_t e = cudaSuccess;
+    if (p->kws[slot]) {
+        e = cudaStreamSynchronize(s);
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+        cudaFree(p->kws[slot]);
+        p->kws[slot] = nullptr;
+        p->kws_bytes[slot] = 0;
+        if (e != cudaSuccess) return cuda_fail(p, e, "workspace resize");
+    }
+    e = cudaMalloc(&p->kws[slot], need);
+    if (e != cudaSuccess) {
+        p->kws[slot] = nullptr;
+        return cuda_fail(p, e, "cudaMalloc(kernel workspace)");
+    }
+    p->kws_bytes[slot] = need;
+    return MIMO_OK;
+}
+
+mimo_status_t launch(mimo_plan_t p, mimo::DetectArgs a, cudaStream_t s, int ws_slot = 0) {
     if (a.n_units == 0) return MIMO_OK;
     const mimo::KernelEntry* k = p->fast;
     if (k) {
         const size_t al = (size_t)k->align;
         if (!aligned(a.H, al) || !aligned(a.y, al) || !aligned(a.llr, al) || !aligned(a.xhat, al)) k = nullptr;
+    }
+    if (k && k->workspace) {
+        mimo_status_t st = ensure_ws(p, ws_slot, k->workspace(a), s);
+        if (st != MIMO_OK) return st;
+        a.ws = p->kws[ws_slot];
     }
     cudaError_t e = k ? k->launch(a, s) : mimo::launch_generic(a, s);
     if (e != cudaSuccess) return cuda_fail(p, e, k ? k->name : "generic");
@@ -311,7 +345,7 @@ mimo_status_t mimo_detect_mmse_host(mimo_plan_t p, const void* H_host, const voi
             e = cudaMemcpyAsync(dy, (const char*)y_host + y_slot * s0, y_slot * ns, cudaMemcpyHostToDevice, s);
         if (e != cudaSuccess) return cuda_fail(p, e, "cudaMemcpyAsync H2D");
         mimo::DetectArgs a = make_args(p, dH, dy, sigma2, n_sc, ns * symph, dl, nullptr, nullptr);
-        st = launch(p, a, s);
+        st = launch(p, a, s, 1 + b);
         if (st != MIMO_OK) return st;
         e = cudaMemcpyAsync((char*)llr_host + l_slot * s0, dl, l_slot * ns, cudaMemcpyDeviceToHost, s);
         if (e != cudaSuccess) return cuda_fail(p, e, "cudaMemcpyAsync D2H");
@@ -319,6 +353,18 @@ mimo_status_t mimo_detect_mmse_host(mimo_plan_t p, const void* H_host, const voi
     for (int i = 0; i < 2; ++i)
         if ((e = cudaStreamSynchronize(p->hs[i])) != cudaSuccess) return cuda_fail(p, e, "cudaStreamSynchronize");
     return MIMO_OK;
+}
+
+mimo_status_t mimo_plan_reserve(mimo_plan_t p, int n_sc, int n_sym) {
+    if (!p) return arg_fail(nullptr, "null plan");
+    if (n_sc < 0 || n_sym < 0 || n_sc % p->d.sc_per_h || n_sym % p->d.sym_per_h)
+        return arg_fail(p, "n_sc / n_sym not multiples of sc_per_h / sym_per_h");
+    const mimo::KernelEntry* k = p->fast;
+    if (!k || !k->workspace) return MIMO_OK;
+    DeviceGuard g(p->d.device);
+    if (g.err != cudaSuccess) return cuda_fail(p, g.err, "cudaSetDevice");
+    mimo::DetectArgs a = make_args(p, nullptr, nullptr, 0.f, n_sc, n_sym, nullptr, nullptr, nullptr);
+    return ensure_ws(p, 0, k->workspace(a), p->stream);
 }
 
 mimo_status_t mimo_plan_sync_status(mimo_plan_t p, long long* n_failed) {
@@ -350,6 +396,8 @@ mimo_status_t mimo_plan_destroy(mimo_plan_t p) {
             }
         if (p->ev) cudaEventDestroy(p->ev);
         if (p->ws) cudaFree(p->ws);
+        for (int i = 0; i < 3; ++i)
+            if (p->kws[i]) cudaFree(p->kws[i]);
         if (p->d_fail) cudaFree(p->d_fail);
     }
     delete p;

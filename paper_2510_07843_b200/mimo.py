@@ -76,6 +76,8 @@ def load_library(path: str | None = None):
     L.mimo_detect_mmse_ex.restype = i
     L.mimo_detect_mmse_host.argtypes = [vp, vp, vp, f, i, i, i, i, i, vp]
     L.mimo_detect_mmse_host.restype = i
+    L.mimo_plan_reserve.argtypes = [vp, i, i]
+    L.mimo_plan_reserve.restype = i
     L.mimo_plan_sync_status.argtypes = [vp, ctypes.POINTER(ll)]
     L.mimo_plan_sync_status.restype = i
     L.mimo_plan_destroy.argtypes = [vp]
@@ -236,6 +238,10 @@ class Plan:
                                              on.ctypes.data_as(ctypes.c_void_p))
         self._check(st)
         return out
+
+    def reserve(self, n_sc: int, n_sym: int):
+        """Pre-allocate the kernel workspace for calls up to n_sc x n_sym (do this before graph capture)."""
+        self._check(self._lib.mimo_plan_reserve(self._h, n_sc, n_sym))
 
     def sync_status(self) -> int:
         """Synchronise; return the number of units flagged by the Cholesky guard since the last call."""
