@@ -72,54 +72,67 @@ __device__ __forceinline__ double2 dscale(double2 a, double s) { return make_dou
 __device__ __forceinline__ double dnorm2(double2 a) { return fma(a.x, a.x, a.y * a.y); }
 
 // ------------------------------------------------------------ demapper ----
-// Exact max-log per axis (equals brute force, pin P10).
+// Output-type magnitude clamp folded into the demapper (reading R10): int8
+// saturates at 127; fp16 saturates in the packing conversion (satfinite);
+// fp32 needs no clamp unless slopes are infinite (sigma2 = 0).
+template <int LT>
+__device__ __forceinline__ float clamp_mag(float v) {  // v >= 0
+    if constexpr (LT == kLlrI8) return fminf(v, 127.f);
+    else return v;
+}
+template <int LT>
+__device__ __forceinline__ float clamp_signed(float v) {
+    if constexpr (LT == kLlrI8) return fminf(fmaxf(v, -127.f), 127.f);
+    else return v;
+}
+
+// Exact max-log per axis (equals brute force, pins P10).
 // u: equalised coordinate in PAM level units (levels at odd integers, i.e.
 // Re/Im(x~) * sqrt(norm)); slope = SINR * a^2 * llr_scale. Writes the LLRs of
 // the M bits on this axis (axis bit i is symbol bit 2i on I, 2i+1 on Q):
-//   s_q = clamp(2 floor(u/2) + 1, +-(2^M - 1)), D = (u - s_q)^2,
-//   t_0 = u, t_i = 2^(M-i) - |t_{i-1}|,
+//   t_0 = u, t_i = 2^(M-i) - |t_{i-1}|   (Gray folding)
+//   D = (|t_{M-1}| - 1)^2                 (squared distance to the nearest level,
+//                                          = (u - clamp(2 floor(u/2)+1))^2)
 //   LLR_i = sgn(t_i) * slope * ((|t_i| + 1)^2 - D)
-// (|t|+1)^2 - D is one FMA, i.e. exactly rounded apart from D's own rounding.
+// (|t|+1)^2 - D is one FMA. QPSK / 16-QAM use the equal linear-region forms
+// (D_1 - D_0 = (b - a)(2u - a - b) between fixed nearest points a, b):
+//   QPSK bit 0: 4u;  16-QAM bit 0: 4(u + sgn(u) max(|u| - 2, 0)), bit 1: 4(2 - |u|).
 // ZF = true is the sigma2 = 0 variant (reading R11): slope = +inf, a zero
-// distance gap gives 0 instead of NaN, and the caller saturates.
-template <int M, bool ZF>
+// distance gap gives 0 instead of NaN, and packing saturates.
+template <int M, bool ZF, int LT>
 __device__ __forceinline__ void demap_axis(float u, float slope, float* out, int stride) {
     if constexpr (!ZF && M <= 2) {
-        // QPSK / 16-QAM: the same max-log values in their linear-region form
-        // (D_1 - D_0 = (b - a)(2u - a - b) between fixed nearest points a, b):
-        //   QPSK      bit 0: 4u
-        //   16-QAM    bit 0: 4(u + sgn(u) max(|u| - 2, 0)),  bit 1: 4(2 - |u|)
         const float s4 = 4.f * slope;
         if constexpr (M == 1) {
-            out[0] = s4 * u;
+            out[0] = clamp_signed<LT>(s4 * u);
         } else {
-            out[0] = s4 * (u + copysignf(fmaxf(fabsf(u) - 2.f, 0.f), u));
-            out[stride] = s4 * (2.f - fabsf(u));
+            out[0] = clamp_signed<LT>(s4 * (u + copysignf(fmaxf(fabsf(u) - 2.f, 0.f), u)));
+            out[stride] = clamp_signed<LT>(s4 * (2.f - fabsf(u)));
         }
         return;
     }
-    constexpr float lim = float((1 << M) - 1);
-    const float sq = fminf(fmaxf(fmaf(2.f, floorf(0.5f * u), 1.f), -lim), lim);
-    const float e = u - sq;
+    float t[M];
+    t[0] = u;
+#pragma unroll
+    for (int i = 1; i < M; ++i) t[i] = float(1 << (M - i)) - fabsf(t[i - 1]);
+    const float e = fabsf(t[M - 1]) - 1.f;
     const float D = e * e;
-    float t = u;
 #pragma unroll
     for (int i = 0; i < M; ++i) {
-        if (i) t = float(1 << (M - i)) - fabsf(t);
-        const float at = fabsf(t) + 1.f;
+        const float at = fabsf(t[i]) + 1.f;
         const float mag = fmaf(at, at, -D);
         float v;
         if constexpr (ZF) v = mag > 0.f ? slope * mag : 0.f;
-        else v = slope * mag;
-        out[i * stride] = copysignf(v, t);
+        else v = clamp_mag<LT>(slope * mag);
+        out[i * stride] = copysignf(v, t[i]);
     }
 }
 
 // Demap one layer: x = x~ / a (level units), qm bits into out[0..QM).
-template <int QM, bool ZF = false>
+template <int QM, bool ZF = false, int LT = kLlrF32>
 __device__ __forceinline__ void demap_layer(float2 x, float slope, float* out) {
-    demap_axis<QM / 2, ZF>(x.x, slope, out, 2);
-    demap_axis<QM / 2, ZF>(x.y, slope, out + 1, 2);
+    demap_axis<QM / 2, ZF, LT>(x.x, slope, out, 2);
+    demap_axis<QM / 2, ZF, LT>(x.y, slope, out + 1, 2);
 }
 
 // ---------------------------------------------------------- quantisers ----
@@ -129,14 +142,23 @@ __device__ __forceinline__ float sat_f32(float v) { return fminf(fmaxf(v, -3.402
 __device__ __forceinline__ __half q_f16(float v) { return __float2half_rn(fminf(fmaxf(v, -65504.f), 65504.f)); }
 __device__ __forceinline__ int8_t q_i8(float v) { return (int8_t)__float2int_rn(fminf(fmaxf(v, -127.f), 127.f)); }
 
+// two floats -> binary16 x2 (RNE, saturating at +-65504: F2FP.SATFINITE)
+__device__ __forceinline__ uint32_t pack_f16x2_sat(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+// v in [-127, 127] -> float whose low byte is rint(v) as int8 (1.5 * 2^23 magic)
+__device__ __forceinline__ uint32_t i8_magic(float v) { return __float_as_uint(v + 12582912.f); }
+
 template <int LT> struct LlrTraits;
 template <> struct LlrTraits<kLlrF32> { static constexpr int bytes = 4; };
 template <> struct LlrTraits<kLlrF16> { static constexpr int bytes = 2; };
 template <> struct LlrTraits<kLlrI8> { static constexpr int bytes = 1; };
 
 // Pack N float LLRs into little-endian 32-bit words of the output type.
-// SAT: saturate fp32 at +-FLT_MAX (only needed when slopes can be infinite,
-// i.e. sigma2 = 0); fp16 / int8 always saturate.
+// SAT = true: values may be out of range / infinite (sigma2 = 0 path) and are
+// saturated here; SAT = false: the demapper already clamped them.
 template <int LT, int N, bool SAT = true>
 __device__ __forceinline__ void pack_llr(const float* v, uint32_t* w) {
     if constexpr (LT == kLlrF32) {
@@ -144,19 +166,17 @@ __device__ __forceinline__ void pack_llr(const float* v, uint32_t* w) {
         for (int i = 0; i < N; ++i) w[i] = __float_as_uint(SAT ? sat_f32(v[i]) : v[i]);
     } else if constexpr (LT == kLlrF16) {
 #pragma unroll
-        for (int i = 0; i < (N + 1) / 2; ++i) {
-            const uint32_t lo = __half_as_ushort(q_f16(v[2 * i]));
-            const uint32_t hi = (2 * i + 1 < N) ? (uint32_t)__half_as_ushort(q_f16(v[2 * i + 1])) : 0u;
-            w[i] = lo | (hi << 16);
-        }
+        for (int i = 0; i < (N + 1) / 2; ++i) w[i] = pack_f16x2_sat(v[2 * i], (2 * i + 1 < N) ? v[2 * i + 1] : 0.f);
     } else {
 #pragma unroll
         for (int i = 0; i < (N + 3) / 4; ++i) {
-            uint32_t acc = 0;
+            uint32_t q[4];
 #pragma unroll
-            for (int b = 0; b < 4; ++b)
-                if (4 * i + b < N) acc |= (uint32_t)(uint8_t)q_i8(v[4 * i + b]) << (8 * b);
-            w[i] = acc;
+            for (int b = 0; b < 4; ++b) {
+                const float x = (4 * i + b < N) ? v[4 * i + b] : 0.f;
+                q[b] = i8_magic(SAT ? fminf(fmaxf(x, -127.f), 127.f) : x);
+            }
+            w[i] = __byte_perm(__byte_perm(q[0], q[1], 0x0040), __byte_perm(q[2], q[3], 0x0040), 0x5410);
         }
     }
 }

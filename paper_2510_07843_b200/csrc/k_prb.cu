@@ -256,13 +256,13 @@ __global__ void __launch_bounds__(kSc* P* G) k_prb(DetectArgs a) {
             float v[NL * QM];
             if (s2 > 0.f) {
 #pragma unroll
-                for (int k = 0; k < NL; ++k) demap_layer<QM, false>(x[k], slope[k], v + k * QM);
+                for (int k = 0; k < NL; ++k) demap_layer<QM, false, LT>(x[k], slope[k], v + k * QM);
                 uint32_t wd[kWords];
                 pack_llr<LT, NL * QM, false>(v, wd);
                 store_bytes<kLlrBytes>((char*)a.llr + re * kLlrBytes, wd);
             } else {
 #pragma unroll
-                for (int k = 0; k < NL; ++k) demap_layer<QM, true>(x[k], slope[k], v + k * QM);
+                for (int k = 0; k < NL; ++k) demap_layer<QM, true, LT>(x[k], slope[k], v + k * QM);
                 uint32_t wd[kWords];
                 pack_llr<LT, NL * QM, true>(v, wd);
                 store_bytes<kLlrBytes>((char*)a.llr + re * kLlrBytes, wd);

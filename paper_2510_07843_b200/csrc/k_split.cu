@@ -252,11 +252,11 @@ __global__ void __launch_bounds__(128) k_apply_units(DetectArgs a) {
             uint32_t wd[kWords];
             if (a.sigma2 > 0.f) {
 #pragma unroll
-                for (int k = 0; k < NL; ++k) demap_layer<QM, false>(x[k], slope[k], v + k * QM);
+                for (int k = 0; k < NL; ++k) demap_layer<QM, false, LT>(x[k], slope[k], v + k * QM);
                 pack_llr<LT, NL * QM, false>(v, wd);
             } else {
 #pragma unroll
-                for (int k = 0; k < NL; ++k) demap_layer<QM, true>(x[k], slope[k], v + k * QM);
+                for (int k = 0; k < NL; ++k) demap_layer<QM, true, LT>(x[k], slope[k], v + k * QM);
                 pack_llr<LT, NL * QM, true>(v, wd);
             }
             store_bytes<kLlrBytes>((char*)a.llr + re * kLlrBytes, wd);

@@ -250,7 +250,7 @@ __device__ __forceinline__ void apply_re(const DetectArgs& a, const SetupOut<NR,
     if (a.llr) {
         float v[NL * QM];
 #pragma unroll
-        for (int k = 0; k < NL; ++k) demap_layer<QM, ZF>(x[k], o.slope[k], v + k * QM);
+        for (int k = 0; k < NL; ++k) demap_layer<QM, ZF, LT>(x[k], o.slope[k], v + k * QM);
         uint32_t w[kWords];
         pack_llr<LT, NL * QM, ZF>(v, w);
         store_bytes<kLlrBytes>((char*)a.llr + re * kLlrBytes, w);

@@ -369,10 +369,12 @@ def closed_form_llr(x, slope_nat, qm):
         lim = (1 << m) - 1
         sq = np.clip(2 * np.floor(u / 2) + 1, -lim, lim)
         D = (u - sq) ** 2
-        t = u
-        for i in range(m):
-            if i:
-                t = (1 << (m - i)) - np.abs(t)
+        ts = [u]
+        for i in range(1, m):
+            ts.append((1 << (m - i)) - np.abs(ts[-1]))
+        # the kernel takes D from the last fold: (|t_{m-1}| - 1)^2 == (u - s_q)^2
+        assert np.allclose((np.abs(ts[-1]) - 1) ** 2, D, rtol=1e-12, atol=1e-12)
+        for i, t in enumerate(ts):
             out[..., 2 * i + off] = np.sign(t) * slope_nat * a * a * ((np.abs(t) + 1) ** 2 - D)
     return out
 
