@@ -273,6 +273,99 @@ __global__ void __launch_bounds__(128) k_apply_units(DetectArgs a) {
     }
 }
 
+// Streaming apply with a register prefetch ring: thread (g, sc) walks symbols
+// g, g+G, ... of its slot keeping PF y vectors in flight (continuous HBM
+// traffic instead of one burst per thread).
+template <int NR, int NL, int QM, int LT, int G, int PF, int SCPH>
+__global__ void __launch_bounds__(128) k_apply_stream(DetectArgs a) {
+    constexpr int NS = (kSym + G - 1) / G;
+    constexpr int WS = UnitWs<NR, NL>::stride;
+    static_assert(PF >= 1 && PF <= NS, "prefetch distance");
+    pdl_launch_dependents();
+    const int sc = blockIdx.x * blockDim.x + threadIdx.x;
+    const int slot = blockIdx.y / G, g = blockIdx.y % G;
+    const bool active = sc < a.n_sc;
+    float2 ring[PF][NR];
+    if (active) {
+#pragma unroll
+        for (int i = 0; i < PF; ++i) {
+            const int s = g + i * G;
+            if (s < kSym)
+                load_bytes<NR * 8>(a.y + ((size_t)(slot * kSym + s) * a.n_sc + sc) * NR,
+                                   reinterpret_cast<uint32_t*>(&ring[i][0]));
+        }
+    }
+    pdl_wait();
+    if (!active) return;
+    const size_t unit = (size_t)slot * (a.n_sc / SCPH) + sc / SCPH;
+    const float* wsu = reinterpret_cast<const float*>(a.ws) + unit * WS;
+    float2 w[NL][NR];
+#pragma unroll
+    for (int i = 0; i < NL * NR * 8 / 32; ++i)
+        ld_v8_coherent(wsu + 8 * i, reinterpret_cast<uint32_t*>(&w[0][0]) + 8 * i);
+    float slope[NL];
+#pragma unroll
+    for (int k = 0; k < NL; ++k) slope[k] = wsu[NL * NR * 2 + k];
+    constexpr int kLlrBytes = NL * QM * LlrTraits<LT>::bytes;
+    constexpr int kWords = (kLlrBytes + 3) / 4;
+    const bool zf = !(a.sigma2 > 0.f);
+#pragma unroll
+    for (int i = 0; i < NS; ++i) {
+        const int s = g + i * G;
+        if (s >= kSym) break;
+        float2 yv[NR];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) yv[r] = ring[i % PF][r];
+        const int sn = g + (i + PF) * G;
+        if (i + PF < NS && sn < kSym)
+            load_bytes<NR * 8>(a.y + ((size_t)(slot * kSym + sn) * a.n_sc + sc) * NR,
+                               reinterpret_cast<uint32_t*>(&ring[i % PF][0]));
+        float2 x[NL];
+#pragma unroll
+        for (int k = 0; k < NL; ++k) {
+            float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int r = 0; r < NR; ++r) acc = cmac(acc, w[k][r], yv[r]);
+            x[k] = acc;
+        }
+        const size_t re = (size_t)(slot * kSym + s) * a.n_sc + sc;
+        if (a.llr) {
+            float v[NL * QM];
+            uint32_t wd[kWords];
+            if (!zf) {
+#pragma unroll
+                for (int k = 0; k < NL; ++k) demap_layer<QM, false, LT>(x[k], slope[k], v + k * QM);
+                pack_llr<LT, NL * QM, false>(v, wd);
+            } else {
+#pragma unroll
+                for (int k = 0; k < NL; ++k) demap_layer<QM, true, LT>(x[k], slope[k], v + k * QM);
+                pack_llr<LT, NL * QM, true>(v, wd);
+            }
+            store_bytes<kLlrBytes>((char*)a.llr + re * kLlrBytes, wd);
+        }
+        if (a.xhat) {
+            const float ia = rsqrtf((float)qam_norm(QM));
+            uint32_t wd[2 * NL];
+#pragma unroll
+            for (int k = 0; k < NL; ++k) {
+                wd[2 * k] = __float_as_uint(x[k].x * ia);
+                wd[2 * k + 1] = __float_as_uint(x[k].y * ia);
+            }
+            store_bytes<NL * 8>(a.xhat + re * NL, wd);
+        }
+    }
+}
+
+template <int NR, int NL, int QM, int LT, int UPC, int G, int PF, int SCPH>
+cudaError_t launch_stream(const DetectArgs& a, cudaStream_t s) {
+    if (a.n_units <= 0) return cudaSuccess;
+    const unsigned g1 = (unsigned)((a.n_units + UPC - 1) / UPC);
+    cudaError_t e = launch_kernel(k_setup_units<NR, NL, QM, UPC>, dim3(g1), dim3(128), 0, s, a.overlap, a);
+    if (e != cudaSuccess) return e;
+    dim3 g2((a.n_sc + 127) / 128, a.n_slots * G);
+    return launch_kernel(k_apply_stream<NR, NL, QM, LT, G, PF, SCPH>, g2, dim3(128), 0, s, a.overlap, a);
+}
+
 template <int NR, int NL>
 size_t workspace(const DetectArgs& a) {
     return (size_t)a.n_units * UnitWs<NR, NL>::stride * 4;
@@ -294,8 +387,20 @@ cudaError_t launch(const DetectArgs& a, cudaStream_t s) {
             workspace<NR, NL>                                                                        \
     }
 
+#define STREAM_ENTRY(NAME, NR, NL, QM, LT, SCPH, UPC, G, PF)                                        \
+    KernelEntry {                                                                                    \
+        NAME, NR, NL, QM, SCPH, 14, LT, 32, 2, launch_stream<NR, NL, QM, LT, UPC, G, PF, SCPH>, nullptr, \
+            workspace<NR, NL>                                                                        \
+    }
+
 const KernelEntry kEntries[] = {
-    SPLIT_ENTRY("split_8x4_q6_i8", 8, 4, 6, kLlrI8, 12, 32, 7),  // C3
+    STREAM_ENTRY("stream_8x4_q6_i8", 8, 4, 6, kLlrI8, 12, 16, 2, 3),  // C3
+    STREAM_ENTRY("stream_8x4_q6_i8_g1pf4", 8, 4, 6, kLlrI8, 12, 16, 1, 4),
+    STREAM_ENTRY("stream_8x4_q6_i8_g1pf3", 8, 4, 6, kLlrI8, 12, 16, 1, 3),
+    STREAM_ENTRY("stream_8x4_q6_i8_g2pf2", 8, 4, 6, kLlrI8, 12, 16, 2, 2),
+    STREAM_ENTRY("stream_8x4_q6_i8_g2pf4", 8, 4, 6, kLlrI8, 12, 16, 2, 4),
+    STREAM_ENTRY("stream_8x4_q6_i8_g7pf2", 8, 4, 6, kLlrI8, 12, 16, 7, 2),
+    SPLIT_ENTRY("split_8x4_q6_i8", 8, 4, 6, kLlrI8, 12, 32, 7),
     SPLIT_ENTRY("split_8x4_q6_f32", 8, 4, 6, kLlrF32, 12, 32, 7),
     SPLIT_ENTRY("split_8x4_q6_f16", 8, 4, 6, kLlrF16, 12, 32, 7),
     SPLIT_ENTRY("split_8x4_q6_i8_g2", 8, 4, 6, kLlrI8, 12, 32, 2),
