@@ -1,0 +1,287 @@
+// k_lg.cu -- "lane group per H-unit" detector for per-subcarrier channels with
+// many layers (C4: 16 rx x 8 layers, 256-QAM, fp16). W~ (NL x NR) does not fit
+// one thread, so NL lanes of a warp share a unit: lane k owns layer k.
+//
+// Mapping (DESIGN.md §"Kernels"): a CTA owns TU = (32/NL) * NW consecutive
+// subcarriers of one slot. Thread 0 bulk-copies the CTA's H tile (one
+// mbarrier) and its 14 y rows (one mbarrier per row). Per unit, rows a2-a5 run
+// in fp32 (reading R18) inside the lane group, warp-synchronously:
+//   a2  lane k forms row k of G = H^H H + s2 I from the H tile;
+//   a3  right-looking Cholesky: lane k keeps row k of the trailing matrix, the
+//       pivot and column j are broadcast by __shfl_sync (guard R17);
+//   a4  lane j forms column j of X = L^-1 (L rows via shared memory) and
+//       A_jj = sum_i |X_ij|^2; lane k forms row k of B = X H^H; then row k of
+//       W = X^H B = G^-1 H^H;
+//   a5  mu_k, SINR_k, W~_k = W_k sqrt(norm) / mu_k kept in lane k's registers.
+// Per symbol, each lane reads the RE's y from the row tile (broadcast within
+// the group), forms x~_k = W~_k y (row a6), demaps its layer (row a7) and
+// writes its QM LLRs; the NL lanes of a unit write one contiguous RE record.
+#include "kernels.h"
+
+namespace mimo {
+namespace {
+
+constexpr int kSym = 14;
+
+template <int NR, int NL, int NW>
+struct LgSmem {
+    static constexpr int UPW = 32 / NL;
+    static constexpr int TU = UPW * NW;
+    static constexpr size_t bars = 0;                                   // 15 mbarriers
+    static constexpr size_t y = 128;                                    // [14][TU][NR]
+    static constexpr size_t H = y + (size_t)kSym * TU * NR * 8;         // [TU][NR][NL]
+    static constexpr size_t LX = H + (size_t)TU * NR * NL * 8;          // [TU][NL][NL]  L rows, then X
+    static constexpr size_t B = LX + (size_t)TU * NL * NL * 8;          // [TU][NL][NR]
+    static constexpr size_t dinv = B + (size_t)TU * NL * NR * 8;        // [TU][NL] float
+    static constexpr size_t total = dinv + (size_t)TU * NL * 4;
+};
+
+__device__ __forceinline__ float2 shfl2(float2 v, int src) {
+    return make_float2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
+template <int NR, int NL, int QM, int LT, int NW>
+__global__ void __launch_bounds__(32 * NW) k_lg(DetectArgs a) {
+    using SM = LgSmem<NR, NL, NW>;
+    constexpr int UPW = SM::UPW;
+    constexpr int TU = SM::TU;
+    static_assert(32 % NL == 0, "NL must divide 32");
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::bars);
+    float2* sy = reinterpret_cast<float2*>(smem + SM::y);
+    float2* sH = reinterpret_cast<float2*>(smem + SM::H);
+    float2* sLX = reinterpret_cast<float2*>(smem + SM::LX);
+    float2* sB = reinterpret_cast<float2*>(smem + SM::B);
+    float* sDinv = reinterpret_cast<float*>(smem + SM::dinv);
+
+    pdl_launch_dependents();
+    const int slot = blockIdx.y;
+    const int sc0 = blockIdx.x * TU;
+    const int nvalid = min(TU, a.n_sc - sc0);
+    const int t = threadIdx.x;
+    const int lane = t & 31, warp = t >> 5;
+    const int k = lane % NL;                     // this lane's layer
+    const int gbase = lane - k;                  // first lane of the group
+    const int ul = warp * UPW + lane / NL;       // unit within the tile
+    const bool active = ul < nvalid;
+    const int sc = sc0 + ul;
+    const float s2 = a.sigma2;
+    const float norm = (float)qam_norm(QM);
+
+    if (t == 0) {
+#pragma unroll
+        for (int s = 0; s <= kSym; ++s) mbar_init(&bars[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (t == 0) {
+        const uint32_t hb = (uint32_t)nvalid * NR * NL * 8u;
+        mbar_arrive_expect_tx(&bars[kSym], hb);
+        bulk_g2s(sH, a.H + ((size_t)slot * a.n_sc + sc0) * NR * NL, hb, &bars[kSym]);
+        const uint32_t row = (uint32_t)nvalid * NR * 8u;
+#pragma unroll 1
+        for (int s = 0; s < kSym; ++s) {
+            mbar_arrive_expect_tx(&bars[s], row);
+            bulk_g2s(sy + s * TU * NR, a.y + ((size_t)(slot * kSym + s) * a.n_sc + sc0) * NR, row, &bars[s]);
+        }
+    }
+    mbar_wait(&bars[kSym], 0);
+
+    const float2* hU = sH + ul * NR * NL;  // H[r][l] of this lane's unit (garbage but in-bounds if !active)
+    // a2: row k of G
+    float2 g[NL];
+#pragma unroll
+    for (int j = 0; j < NL; ++j) g[j] = make_float2(0.f, 0.f);
+#pragma unroll 4
+    for (int r = 0; r < NR; ++r) {
+        const float2 hk = hU[r * NL + k];
+#pragma unroll
+        for (int j = 0; j < NL; ++j) {  // conj(H_rk) H_rj
+            const float2 hj = hU[r * NL + j];
+            g[j].x = fmaf(hk.x, hj.x, fmaf(hk.y, hj.y, g[j].x));
+            g[j].y = fmaf(hk.x, hj.y, fmaf(-hk.y, hj.x, g[j].y));
+        }
+    }
+    // diagonal: real, + s2
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
+        if (j == k) g[j] = make_float2(g[j].x + s2, 0.f);
+    // max_i G_ii over the group (guard scale)
+    float gmax = 0.f;
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
+        if (j == k) gmax = g[j].x;
+#pragma unroll
+    for (int off = 1; off < NL; off <<= 1) gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, off));
+
+    // a3: right-looking Cholesky, lane k holds row k (entries j <= k meaningful)
+    bool fail = !(gmax == gmax);
+    float my_dinv = 0.f;
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+        float p = __shfl_sync(0xffffffffu, g[j].x, gbase + j);  // G_jj of the trailing matrix
+        if (!(p > (float)kPivotTau * gmax)) {
+            fail = true;
+            p = 1.f;
+        }
+        const float dinv = rsqrtf(p);
+        if (k == j) my_dinv = dinv;
+        if (k > j) g[j] = make_float2(g[j].x * dinv, g[j].y * dinv);  // L_kj
+#pragma unroll
+        for (int m = j + 1; m < NL; ++m) {
+            const float2 lmj = shfl2(g[j], gbase + m);  // L_mj from lane m
+            if (k >= m) {                              // G_km -= L_kj conj(L_mj)
+                g[m].x = fmaf(-g[j].x, lmj.x, fmaf(-g[j].y, lmj.y, g[m].x));
+                g[m].y = fmaf(-g[j].y, lmj.x, fmaf(g[j].x, lmj.y, g[m].y));
+            }
+        }
+    }
+    // L rows to shared memory (strictly lower part), 1/L_kk
+    float2* lU = sLX + ul * NL * NL;
+#pragma unroll
+    for (int j = 0; j < NL; ++j) lU[k * NL + j] = (j < k) ? g[j] : make_float2(0.f, 0.f);
+    sDinv[ul * NL + k] = my_dinv;
+    __syncwarp();
+    // a4: column k of X = L^-1:  X_kk = 1/L_kk, X_ik = -(1/L_ii) sum_{m<i} L_im X_mk
+    float2 x[NL];
+#pragma unroll
+    for (int i = 0; i < NL; ++i) {
+        float2 sv = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int m = 0; m < i; ++m) sv = cmac(sv, lU[i * NL + m], x[m]);
+        const float di = sDinv[ul * NL + i];
+        x[i] = (i == k) ? make_float2(my_dinv, 0.f)
+                        : (i < k ? make_float2(0.f, 0.f) : make_float2(-sv.x * di, -sv.y * di));
+    }
+    float A = 0.f;
+#pragma unroll
+    for (int i = 0; i < NL; ++i) A = fmaf(x[i].x, x[i].x, fmaf(x[i].y, x[i].y, A));
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < NL; ++i) lU[i * NL + k] = x[i];  // X column k (X_ik)
+    __syncwarp();
+    // row k of B = X H^H: B_kr = sum_m X_km conj(H_rm)
+    float2* bU = sB + ul * NL * NR;
+    {
+        float2 xr[NL];
+#pragma unroll
+        for (int m = 0; m < NL; ++m) xr[m] = lU[k * NL + m];
+#pragma unroll 4
+        for (int r = 0; r < NR; ++r) {
+            float2 sv = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int m = 0; m < NL; ++m) {  // X_km conj(H_rm)
+                const float2 h = hU[r * NL + m];
+                sv.x = fmaf(xr[m].x, h.x, fmaf(xr[m].y, h.y, sv.x));
+                sv.y = fmaf(xr[m].y, h.x, fmaf(-xr[m].x, h.y, sv.y));
+            }
+            bU[k * NR + r] = sv;
+        }
+    }
+    __syncwarp();
+    // a5
+    float sinr, fac;
+    const float mu = fmaf(-s2, A, 1.f);
+    if (s2 == 0.f) {
+        sinr = __int_as_float(0x7f800000);
+        fac = sqrtf(norm);
+    } else {
+        sinr = __fdividef(mu, s2 * A);
+        fac = __fdividef(sqrtf(norm), mu);
+    }
+    if (!(mu > 0.f) || fail) {
+        sinr = 0.f;
+        fac = 0.f;
+    }
+    const float slope = sinr / norm * a.llr_scale;
+    // row k of W = X^H B: W_kr = sum_i conj(X_ik) B_ir, scaled to W~ (level units)
+    float2 w[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) w[r] = make_float2(0.f, 0.f);
+#pragma unroll
+    for (int i = 0; i < NL; ++i) {
+        const float2 xi = x[i];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            const float2 b = bU[i * NR + r];  // conj(X_ik) B_ir
+            w[r].x = fmaf(xi.x, b.x, fmaf(xi.y, b.y, w[r].x));
+            w[r].y = fmaf(xi.x, b.y, fmaf(-xi.y, b.x, w[r].y));
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) w[r] = (fac > 0.f) ? make_float2(w[r].x * fac, w[r].y * fac) : make_float2(0.f, 0.f);
+
+    pdl_wait();  // global writes only after the previous grid completed
+    if (active) {
+        const size_t unit = (size_t)slot * a.n_sc + sc;
+        if (k == 0 && fail) atomicAdd(a.fail_count, 1ull);
+        if (a.sinr) a.sinr[unit * NL + k] = sinr;
+    }
+    constexpr int kLlrBytes = QM * LlrTraits<LT>::bytes;  // this lane's layer
+    constexpr int kWords = (kLlrBytes + 3) / 4;
+    const float ia = rsqrtf(norm);
+    const bool zf = !(s2 > 0.f);
+#pragma unroll 1
+    for (int s = 0; s < kSym; ++s) {
+        mbar_wait(&bars[s], 0);
+        if (!active) continue;
+        const float2* ys = sy + (s * TU + ul) * NR;
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int r = 0; r < NR; ++r) acc = cmac(acc, w[r], ys[r]);
+        const size_t re = (size_t)(slot * kSym + s) * a.n_sc + sc;
+        if (a.llr) {
+            float v[QM];
+            uint32_t wd[kWords];
+            if (!zf) {
+                demap_layer<QM, false, LT>(acc, slope, v);
+                pack_llr<LT, QM, false>(v, wd);
+            } else {
+                demap_layer<QM, true, LT>(acc, slope, v);
+                pack_llr<LT, QM, true>(v, wd);
+            }
+            store_bytes<kLlrBytes>((char*)a.llr + (re * NL + k) * kLlrBytes, wd);
+        }
+        if (a.xhat) a.xhat[re * NL + k] = make_float2(acc.x * ia, acc.y * ia);
+    }
+}
+
+template <int NR, int NL, int QM, int LT, int NW>
+cudaError_t launch(const DetectArgs& a, cudaStream_t s) {
+    if (a.n_sc <= 0 || a.n_slots <= 0) return cudaSuccess;
+    constexpr int TU = LgSmem<NR, NL, NW>::TU;
+    dim3 grid((a.n_sc + TU - 1) / TU, a.n_slots);
+    return launch_kernel(k_lg<NR, NL, QM, LT, NW>, grid, dim3(32 * NW), LgSmem<NR, NL, NW>::total, s, a.overlap, a);
+}
+
+template <int NR, int NL, int QM, int LT, int NW>
+cudaError_t prepare() {
+    constexpr size_t smem = LgSmem<NR, NL, NW>::total;
+    if (smem > 48 * 1024)
+        return cudaFuncSetAttribute(k_lg<NR, NL, QM, LT, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return cudaSuccess;
+}
+
+#define LG_ENTRY(NAME, NR, NL, QM, LT, NW) \
+    KernelEntry { NAME, NR, NL, QM, 1, 14, LT, 32, 1, launch<NR, NL, QM, LT, NW>, prepare<NR, NL, QM, LT, NW> }
+
+const KernelEntry kEntries[] = {
+    LG_ENTRY("lg_16x8_q8_f16", 16, 8, 8, kLlrF16, 2),  // C4
+    LG_ENTRY("lg_16x8_q8_f32", 16, 8, 8, kLlrF32, 2),
+    LG_ENTRY("lg_16x8_q8_i8", 16, 8, 8, kLlrI8, 2),
+    LG_ENTRY("lg_16x8_q6_f16", 16, 8, 6, kLlrF16, 2),
+    LG_ENTRY("lg_8x8_q6_f16", 8, 8, 6, kLlrF16, 2),
+    LG_ENTRY("lg_16x16_q8_f16", 16, 16, 8, kLlrF16, 2),
+    // tuning variants for C4
+    LG_ENTRY("lg_16x8_q8_f16_w1", 16, 8, 8, kLlrF16, 1),
+    LG_ENTRY("lg_16x8_q8_f16_w4", 16, 8, 8, kLlrF16, 4),
+};
+
+}  // namespace
+
+const KernelEntry* lg_entries(int* n) {
+    *n = (int)(sizeof(kEntries) / sizeof(kEntries[0]));
+    return kEntries;
+}
+
+}  // namespace mimo

@@ -47,6 +47,7 @@ const KernelEntry* tpu_entries(int* n);
 const KernelEntry* prb_entries(int* n);
 const KernelEntry* prbp_entries(int* n);
 const KernelEntry* split_entries(int* n);
+const KernelEntry* lg_entries(int* n);
 
 // Generic kernel: any n_rx <= 64, n_layers <= min(16, n_rx), qm, sc_per_h,
 // sym_per_h, llr_type; 8-byte alignment.
