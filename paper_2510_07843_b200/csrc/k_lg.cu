@@ -10,8 +10,7 @@
 //   a3  right-looking Cholesky: lane k keeps row k of the trailing matrix, the
 //       pivot and column j are broadcast by __shfl_sync (guard R17);
 //   a4  lane j forms column j of X = L^-1 (L rows via shared memory) and
-//       A_jj = sum_i |X_ij|^2; lane k forms row k of B = X H^H; then row k of
-//       W = X^H B = G^-1 H^H;
+//       A_jj = sum_i |X_ij|^2, then row j of G^-1 = X^H X and of W = G^-1 H^H;
 //   a5  mu_k, SINR_k, W~_k = W_k sqrt(norm) / mu_k kept in lane k's registers.
 // Per symbol, each lane reads the RE's y from the row tile (broadcast within
 // the group), forms x~_k = W~_k y (row a6), demaps its layer (row a7) and
@@ -27,12 +26,15 @@ template <int NR, int NL, int NW>
 struct LgSmem {
     static constexpr int UPW = 32 / NL;
     static constexpr int TU = UPW * NW;
+    // per-unit strides padded by 16-32 B so the UPW units of a warp hit distinct banks
+    static constexpr int YS = NR + 2;                                   // float2 per unit in a y row
+    static constexpr int HS = NR * NL + 4;                              // float2 per unit H
+    static constexpr int LS = NL * NL + 4;                              // float2 per unit L / X
     static constexpr size_t bars = 0;                                   // 15 mbarriers
-    static constexpr size_t y = 128;                                    // [14][TU][NR]
-    static constexpr size_t H = y + (size_t)kSym * TU * NR * 8;         // [TU][NR][NL]
-    static constexpr size_t LX = H + (size_t)TU * NR * NL * 8;          // [TU][NL][NL]  L rows, then X
-    static constexpr size_t B = LX + (size_t)TU * NL * NL * 8;          // [TU][NL][NR]
-    static constexpr size_t dinv = B + (size_t)TU * NL * NR * 8;        // [TU][NL] float
+    static constexpr size_t y = 128;                                    // [14][TU][YS]
+    static constexpr size_t H = y + (size_t)kSym * TU * YS * 8;         // [TU][HS]
+    static constexpr size_t LX = H + (size_t)TU * HS * 8;               // [TU][LS]  L rows, then X
+    static constexpr size_t dinv = LX + (size_t)TU * LS * 8;            // [TU][NL] float
     static constexpr size_t total = dinv + (size_t)TU * NL * 4;
 };
 
@@ -51,7 +53,6 @@ __global__ void __launch_bounds__(32 * NW) k_lg(DetectArgs a) {
     float2* sy = reinterpret_cast<float2*>(smem + SM::y);
     float2* sH = reinterpret_cast<float2*>(smem + SM::H);
     float2* sLX = reinterpret_cast<float2*>(smem + SM::LX);
-    float2* sB = reinterpret_cast<float2*>(smem + SM::B);
     float* sDinv = reinterpret_cast<float*>(smem + SM::dinv);
 
     pdl_launch_dependents();
@@ -75,19 +76,22 @@ __global__ void __launch_bounds__(32 * NW) k_lg(DetectArgs a) {
     }
     __syncthreads();
     if (t == 0) {
-        const uint32_t hb = (uint32_t)nvalid * NR * NL * 8u;
-        mbar_arrive_expect_tx(&bars[kSym], hb);
-        bulk_g2s(sH, a.H + ((size_t)slot * a.n_sc + sc0) * NR * NL, hb, &bars[kSym]);
-        const uint32_t row = (uint32_t)nvalid * NR * 8u;
+        mbar_arrive_expect_tx(&bars[kSym], (uint32_t)nvalid * NR * NL * 8u);
 #pragma unroll 1
-        for (int s = 0; s < kSym; ++s) {
-            mbar_arrive_expect_tx(&bars[s], row);
-            bulk_g2s(sy + s * TU * NR, a.y + ((size_t)(slot * kSym + s) * a.n_sc + sc0) * NR, row, &bars[s]);
-        }
+        for (int s = 0; s < kSym; ++s) mbar_arrive_expect_tx(&bars[s], (uint32_t)nvalid * NR * 8u);
+    }
+    __syncthreads();
+    // the group leader of each unit copies its H and its 14 y vectors into padded slots
+    if (k == 0 && active) {
+        bulk_g2s(sH + ul * SM::HS, a.H + ((size_t)slot * a.n_sc + sc) * NR * NL, NR * NL * 8u, &bars[kSym]);
+#pragma unroll 1
+        for (int s = 0; s < kSym; ++s)
+            bulk_g2s(sy + (s * TU + ul) * SM::YS, a.y + ((size_t)(slot * kSym + s) * a.n_sc + sc) * NR, NR * 8u,
+                     &bars[s]);
     }
     mbar_wait(&bars[kSym], 0);
 
-    const float2* hU = sH + ul * NR * NL;  // H[r][l] of this lane's unit (garbage but in-bounds if !active)
+    const float2* hU = sH + ul * SM::HS;  // H[r][l] of this lane's unit (garbage but in-bounds if !active)
     // a2: row k of G
     float2 g[NL];
 #pragma unroll
@@ -137,7 +141,7 @@ __global__ void __launch_bounds__(32 * NW) k_lg(DetectArgs a) {
         }
     }
     // L rows to shared memory (strictly lower part), 1/L_kk
-    float2* lU = sLX + ul * NL * NL;
+    float2* lU = sLX + ul * SM::LS;
 #pragma unroll
     for (int j = 0; j < NL; ++j) lU[k * NL + j] = (j < k) ? g[j] : make_float2(0.f, 0.f);
     sDinv[ul * NL + k] = my_dinv;
@@ -160,25 +164,19 @@ __global__ void __launch_bounds__(32 * NW) k_lg(DetectArgs a) {
 #pragma unroll
     for (int i = 0; i < NL; ++i) lU[i * NL + k] = x[i];  // X column k (X_ik)
     __syncwarp();
-    // row k of B = X H^H: B_kr = sum_m X_km conj(H_rm)
-    float2* bU = sB + ul * NL * NR;
-    {
-        float2 xr[NL];
+    // row k of G^-1 = X^H X: Gi_kj = sum_{m >= max(k,j)} conj(X_mk) X_mj (X_mk = x[m] here)
+    float2 gi[NL];
 #pragma unroll
-        for (int m = 0; m < NL; ++m) xr[m] = lU[k * NL + m];
-#pragma unroll 4
-        for (int r = 0; r < NR; ++r) {
-            float2 sv = make_float2(0.f, 0.f);
+    for (int j = 0; j < NL; ++j) {
+        float2 sv = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int m = 0; m < NL; ++m) {  // X_km conj(H_rm)
-                const float2 h = hU[r * NL + m];
-                sv.x = fmaf(xr[m].x, h.x, fmaf(xr[m].y, h.y, sv.x));
-                sv.y = fmaf(xr[m].y, h.x, fmaf(-xr[m].x, h.y, sv.y));
-            }
-            bU[k * NR + r] = sv;
+        for (int m = j; m < NL; ++m) {  // x[m] = 0 for m < k
+            const float2 xm = x[m], xmj = lU[m * NL + j];
+            sv.x = fmaf(xm.x, xmj.x, fmaf(xm.y, xmj.y, sv.x));
+            sv.y = fmaf(xm.x, xmj.y, fmaf(-xm.y, xmj.x, sv.y));
         }
+        gi[j] = sv;
     }
-    __syncwarp();
     // a5
     float sinr, fac;
     const float mu = fmaf(-s2, A, 1.f);
@@ -194,22 +192,19 @@ __global__ void __launch_bounds__(32 * NW) k_lg(DetectArgs a) {
         fac = 0.f;
     }
     const float slope = sinr / norm * a.llr_scale;
-    // row k of W = X^H B: W_kr = sum_i conj(X_ik) B_ir, scaled to W~ (level units)
+    // row k of W = G^-1 H^H: W_kr = sum_j Gi_kj conj(H_rj), scaled to W~ (level units)
     float2 w[NR];
 #pragma unroll
-    for (int r = 0; r < NR; ++r) w[r] = make_float2(0.f, 0.f);
+    for (int r = 0; r < NR; ++r) {
+        float2 sv = make_float2(0.f, 0.f);
 #pragma unroll
-    for (int i = 0; i < NL; ++i) {
-        const float2 xi = x[i];
-#pragma unroll
-        for (int r = 0; r < NR; ++r) {
-            const float2 b = bU[i * NR + r];  // conj(X_ik) B_ir
-            w[r].x = fmaf(xi.x, b.x, fmaf(xi.y, b.y, w[r].x));
-            w[r].y = fmaf(xi.x, b.y, fmaf(-xi.y, b.x, w[r].y));
+        for (int j = 0; j < NL; ++j) {
+            const float2 h = hU[r * NL + j];
+            sv.x = fmaf(gi[j].x, h.x, fmaf(gi[j].y, h.y, sv.x));
+            sv.y = fmaf(gi[j].y, h.x, fmaf(-gi[j].x, h.y, sv.y));
         }
+        w[r] = (fac > 0.f) ? make_float2(sv.x * fac, sv.y * fac) : make_float2(0.f, 0.f);
     }
-#pragma unroll
-    for (int r = 0; r < NR; ++r) w[r] = (fac > 0.f) ? make_float2(w[r].x * fac, w[r].y * fac) : make_float2(0.f, 0.f);
 
     pdl_wait();  // global writes only after the previous grid completed
     if (active) {
@@ -225,7 +220,7 @@ __global__ void __launch_bounds__(32 * NW) k_lg(DetectArgs a) {
     for (int s = 0; s < kSym; ++s) {
         mbar_wait(&bars[s], 0);
         if (!active) continue;
-        const float2* ys = sy + (s * TU + ul) * NR;
+        const float2* ys = sy + (s * TU + ul) * SM::YS;
         float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
         for (int r = 0; r < NR; ++r) acc = cmac(acc, w[r], ys[r]);
