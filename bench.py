@@ -44,7 +44,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=50)
-    ap.add_argument("--config", default="2", help="BASELINE config index 1..5 (default 2 = configs[1])")
+    ap.add_argument("--config", default="2",
+                    help="BASELINE config 1..5 (default 2 = configs[1], the headline), P (paper shape) or all")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -343,6 +344,24 @@ def run_ours(args, k):
     value = n_re_all / (t_max_ms / 1e3)
     per_launch_s = (elapsed_ms / 1e3) / (K * plan.launches_per_call)
     peaks = measured_peaks()
+    fl = synth.config_algorithmic_flops(k)
+    step_s = (t_max_ms / 1e3) / K
+    # FP32 SIMT peak: 148 SMs x 128 lanes x 2 flop x max SM clock
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    fp32_tflops = n_sm * 128 * 2 * peaks["sm_max_mhz"] * 1e6 / 1e12
+    t_hbm = b["total"] / (peaks["hbm_gbs"] * 1e9)
+    t_alu = fl["total"] / (fp32_tflops * 1e12)
+    if t_alu > t_hbm:
+        roof = {"bound": "alu", "achieved": fl["total"] / step_s / 1e12, "peak": fp32_tflops, "unit": "TFLOP/s",
+                "frac": (fl["total"] / step_s / 1e12) / fp32_tflops, "algorithmic_flops_per_step": fl["total"],
+                "peak_src": f"derived: {n_sm} SMs x 128 FP32 lanes x 2 x {peaks['sm_max_mhz']:.0f} MHz"}
+    else:
+        ach = b["total"] / step_s / 1e9
+        roof = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / peaks["hbm_gbs"], "peak_src": peaks["src"] + " (MEASURED_PEAKS.json hbm_gbs)"}
+    roof.update({"traffic": ncu_traffic(k), "algorithmic_bytes_per_step": b["total"],
+                 "t_roof_us": max(t_hbm, t_alu) * 1e6, "step_us": step_s * 1e6,
+                 "launches_per_step": plan.launches_per_call})
     achieved = b["total"] / per_launch_s / 1e9
     clocks = sampler.result()
 
@@ -392,12 +411,8 @@ def run_ours(args, k):
         "data": "synthetic (seeded numpy PCG64, BASELINE config shapes; DESIGN.md input recipe)",
         "config": cfg,
         "llr_gbit_s": value * w.n_layers * w.qm / 1e9,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / peaks["hbm_gbs"], "traffic": ncu_traffic(k),
-                     "algorithmic_bytes_per_launch": b["total"], "peak_src": peaks["src"],
-                     "kernel_us": per_launch_s * 1e6,
-                     "serialised_call_us": single_us,
-                     "serialised_frac": b["total"] / (single_us * 1e-6) / 1e9 / peaks["hbm_gbs"]},
+        "roofline": dict(roof, serialised_call_us=single_us,
+                         serialised_frac=max(t_hbm, t_alu) / (single_us * 1e-6)),
         "cpu_baseline": cpu,
         "e2e": e2e,
         "clocks": clocks,
@@ -410,11 +425,12 @@ def run_ours(args, k):
 
 def main():
     args = parse()
-    k = cfg_key(args.config)
-    if args.impl == "reference":
-        run_reference(args, k)
-    else:
-        run_ours(args, k)
+    keys = [1, 2, 3, 4, 5] if args.config == "all" else [cfg_key(args.config)]
+    for k in keys:
+        if args.impl == "reference":
+            run_reference(args, k)
+        else:
+            run_ours(args, k)
 
 
 if __name__ == "__main__":

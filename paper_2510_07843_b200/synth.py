@@ -243,3 +243,22 @@ def config_algorithmic_bytes(cfg_key, llr_bytes: int | None = None) -> dict:
     lo = n_re * nl * qm * lb
     return dict(H=h, y=yb, llr=lo, total=h + yb + lo, n_re=n_re, n_units=n_units,
                 n_llr=n_re * nl * qm)
+
+
+def config_algorithmic_flops(cfg_key) -> dict:
+    """Algorithmic flops of one full pass (SURVEY.md §8(d) counting convention).
+
+    Setup per H-unit (rows a2-a5), in complex MACs (8 real flops each):
+      Gram nr*nl(nl+1)/2 + Cholesky nl^3/6 + L^-1 nl^3/6 + W nl^2*nr;
+    per RE: x~ = W~ y, nl*nr cMAC (row a6), and ~8 flops per LLR bit (row a7).
+    """
+    c = CONFIGS[cfg_key]
+    nr, nl, qm, scph = c["n_rx"], c["n_layers"], c["qm"], c["sc_per_h"]
+    n_sym = c["n_slots"] * SYM_PER_SLOT
+    n_re = n_sym * c["n_sc"]
+    n_units = c["n_slots"] * (c["n_sc"] // scph)
+    unit_cmac = nr * nl * (nl + 1) / 2 + nl ** 3 / 3 + nl * nl * nr
+    setup = 8.0 * unit_cmac * n_units
+    apply = 8.0 * nl * nr * n_re
+    demap = 8.0 * nl * qm * n_re
+    return dict(setup=setup, apply=apply, demap=demap, total=setup + apply + demap)
