@@ -3,12 +3,13 @@
 // (16 x 64 per RE, 1024 cMAC): C5 is FP32-bound, not HBM-bound (SURVEY.md
 // §8(d)), so the kernels are organised around the FFMA pipe.
 //
-//   k_big_setup (rows a2-a5), one CTA (256 threads) per PRB-unit, fp32
-//     (reading R18; cond(G) <= ~10 on C5): G = H^H H + s2 I (one entry per
-//     thread), Cholesky by 16 lanes of warp 0 (lane k holds row k, pivots and
-//     columns by __shfl_sync; guard R17), X = L^-1 column per lane, G^-1 = X^H X,
-//     W~ = diag(sqrt(norm)/mu) G^-1 H^H (4 entries per thread), written to the
-//     plan workspace as [unit][r][k] plus slopes.
+//   k_big_setup (rows a2-a5), one warp per PRB-unit, warp-synchronous, fp32
+//     (reading R18; cond(G) <= ~10 on C5): G = H^H H + s2 I (half a row per
+//     lane, broadcast 128-bit H reads), Cholesky with lane k holding row k
+//     (pivots and columns by __shfl_sync; guard R17), X = L^-1 column per lane,
+//     row k of G^-1 = X^H X per lane, W~ = diag(sqrt(norm)/mu) G^-1 H^H (lane
+//     (k, half) covers half the antennas), written to the plan workspace as
+//     [unit][r][k] plus slopes.
 //   k_big_apply (rows a6-a7), one CTA per PRB-unit: the unit's 168 y vectors
 //     are bulk-copied into shared memory at a padded 528-byte stride
 //     (conflict-free 128-bit reads) and W~ [r][k] next to them; thread
@@ -34,159 +35,173 @@ __device__ __forceinline__ float2 shfl2(float2 v, int src) {
     return make_float2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
 }
 
-template <int NR, int NL, int QM>
-__global__ void __launch_bounds__(256) k_big_setup(DetectArgs a) {
-    static_assert(NL == 16 && NR % 4 == 0, "k_big_setup: 16 layers");
+// One warp per PRB-unit (UPB units per CTA), warp-synchronous, no CTA barriers.
+template <int NR, int NL>
+struct SetupSmem {
+    static constexpr size_t per_unit = (size_t)NR * NL * 8 + 3 * NL * NL * 8 + 3 * NL * 4 + 16;
+};
+
+template <int NR, int NL, int QM, int UPB>
+__global__ void __launch_bounds__(32 * UPB) k_big_setup(DetectArgs a) {
+    static_assert(NL == 16 && NR % 32 == 0, "k_big_setup: 16 layers, NR multiple of 32");
     constexpr int WS = BigWs<NR, NL>::stride;
-    __shared__ __align__(16) float2 sH[NR * NL];      // [r][l]
-    __shared__ float2 sG[NL * NL];                    // G, then X = L^-1 ([i][j]), then G^-1
-    __shared__ float2 sL[NL * NL];
-    __shared__ float sDinv[NL], sFac[NL], sSinr[NL];
-    __shared__ int sFail;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned char* base = smem + (size_t)warp * SetupSmem<NR, NL>::per_unit;
+    float2* sH = reinterpret_cast<float2*>(base);                 // [r][l]
+    float2* sG = sH + NR * NL;                                    // G
+    float2* sX = sG + NL * NL;                                    // L rows, then X = L^-1 [i][j]
+    float2* sGi = sX + NL * NL;                                   // G^-1
+    float* sDinv = reinterpret_cast<float*>(sGi + NL * NL);
 
     pdl_launch_dependents();
-    const int t = threadIdx.x;
-    const long long u = blockIdx.x;
+    const long long u = (long long)blockIdx.x * UPB + warp;
+    const bool valid = u < a.n_units;
     const float s2 = a.sigma2;
     const float norm = (float)qam_norm(QM);
-    {
+    if (valid) {
         const float4* src = reinterpret_cast<const float4*>(a.H + u * NR * NL);
         float4* dst = reinterpret_cast<float4*>(sH);
-        for (int i = t; i < NR * NL / 2; i += 256) dst[i] = __ldg(src + i);
+#pragma unroll 4
+        for (int i = lane; i < NR * NL / 2; i += 32) dst[i] = __ldg(src + i);
     }
-    __syncthreads();
-    // a2: G_ij = sum_r conj(H_ri) H_rj (+ s2 on the diagonal), one entry per thread
+    __syncwarp();
+    // a2: lane -> row i = lane/2, columns 8h .. 8h+7 of G (full rows, broadcast H reads)
     {
-        const int i = t / NL, j = t % NL;
-        float2 acc = make_float2(0.f, 0.f);
-#pragma unroll 8
+        const int i = lane >> 1, h = lane & 1;
+        float2 g[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) g[q] = make_float2(0.f, 0.f);
+#pragma unroll 4
         for (int r = 0; r < NR; ++r) {
-            const float2 hi = sH[r * NL + i], hj = sH[r * NL + j];
-            acc.x = fmaf(hi.x, hj.x, fmaf(hi.y, hj.y, acc.x));
-            acc.y = fmaf(hi.x, hj.y, fmaf(-hi.y, hj.x, acc.y));
-        }
-        if (i == j) acc = make_float2(acc.x + s2, 0.f);
-        sG[i * NL + j] = acc;
-    }
-    __syncthreads();
-    // a3: Cholesky by lanes 0..15 of warp 0 (lane k holds row k, right-looking)
-    if (t < 32) {
-        const int k = t & 15;
-        float2 g[NL];
+            const float2 hi = sH[r * NL + i];
+            const float4* hr = reinterpret_cast<const float4*>(sH + r * NL + 8 * h);
 #pragma unroll
-        for (int j = 0; j < NL; ++j) g[j] = sG[k * NL + j];
-        float gmax = g[0].x;
-#pragma unroll
-        for (int j = 0; j < NL; ++j)
-            if (j == k) gmax = g[j].x;
-#pragma unroll
-        for (int off = 1; off < NL; off <<= 1) gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, off));
-        bool fail = !(gmax == gmax);
-        float my_dinv = 0.f;
-#pragma unroll
-        for (int j = 0; j < NL; ++j) {
-            float p = __shfl_sync(0xffffffffu, g[j].x, j);
-            if (!(p > (float)kPivotTau * gmax)) {
-                fail = true;
-                p = 1.f;
-            }
-            const float dinv = rsqrtf(p);
-            if (k == j) my_dinv = dinv;
-            if (k > j) g[j] = make_float2(g[j].x * dinv, g[j].y * dinv);
-#pragma unroll
-            for (int m = j + 1; m < NL; ++m) {
-                const float2 lmj = shfl2(g[j], m);
-                if (k >= m) {
-                    g[m].x = fmaf(-g[j].x, lmj.x, fmaf(-g[j].y, lmj.y, g[m].x));
-                    g[m].y = fmaf(-g[j].y, lmj.x, fmaf(g[j].x, lmj.y, g[m].y));
-                }
+            for (int q2 = 0; q2 < 4; ++q2) {
+                const float4 v = hr[q2];
+                g[2 * q2].x = fmaf(hi.x, v.x, fmaf(hi.y, v.y, g[2 * q2].x));
+                g[2 * q2].y = fmaf(hi.x, v.y, fmaf(-hi.y, v.x, g[2 * q2].y));
+                g[2 * q2 + 1].x = fmaf(hi.x, v.z, fmaf(hi.y, v.w, g[2 * q2 + 1].x));
+                g[2 * q2 + 1].y = fmaf(hi.x, v.w, fmaf(-hi.y, v.z, g[2 * q2 + 1].y));
             }
         }
-        if (t < NL) {
 #pragma unroll
-            for (int j = 0; j < NL; ++j) sL[k * NL + j] = (j < k) ? g[j] : make_float2(0.f, 0.f);
-            sDinv[k] = my_dinv;
-            if (k == 0) sFail = fail;
+        for (int q = 0; q < 8; ++q) {
+            const int j = 8 * h + q;
+            sG[i * NL + j] = (i == j) ? make_float2(g[q].x + s2, 0.f) : g[q];
         }
     }
-    __syncthreads();
-    // a4: X = L^-1, column k per thread (k < 16): X_kk = 1/L_kk, X_ik = -(1/L_ii) sum_{m<i} L_im X_mk
-    if (t < NL) {
-        const int k = t;
-        float2 x[NL];
+    __syncwarp();
+    // a3: Cholesky, lane k (and its duplicate k+16) holds row k
+    const int k = lane & 15;
+    float2 g[NL];
 #pragma unroll
-        for (int i = 0; i < NL; ++i) {
+    for (int j = 0; j < NL; ++j) g[j] = sG[k * NL + j];
+    float gmax = 0.f;
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
+        if (j == k) gmax = g[j].x;
+#pragma unroll
+    for (int off = 1; off < NL; off <<= 1) gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, off));
+    bool fail = !(gmax == gmax);
+    float my_dinv = 0.f;
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+        float p = __shfl_sync(0xffffffffu, g[j].x, j);
+        if (!(p > (float)kPivotTau * gmax)) {
+            fail = true;
+            p = 1.f;
+        }
+        const float dinv = rsqrtf(p);
+        if (k == j) my_dinv = dinv;
+        if (k > j) g[j] = make_float2(g[j].x * dinv, g[j].y * dinv);
+#pragma unroll
+        for (int m = j + 1; m < NL; ++m) {
+            const float2 lmj = shfl2(g[j], m);
+            if (k >= m) {
+                g[m].x = fmaf(-g[j].x, lmj.x, fmaf(-g[j].y, lmj.y, g[m].x));
+                g[m].y = fmaf(-g[j].y, lmj.x, fmaf(g[j].x, lmj.y, g[m].y));
+            }
+        }
+    }
+    if (lane < NL) {
+#pragma unroll
+        for (int j = 0; j < NL; ++j) sX[k * NL + j] = (j < k) ? g[j] : make_float2(0.f, 0.f);
+        sDinv[k] = my_dinv;
+    }
+    __syncwarp();
+    // a4: X = L^-1, column k per lane (lanes 16..31 duplicate)
+    float2 x[NL];
+#pragma unroll
+    for (int i = 0; i < NL; ++i) {
+        float2 sv = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int m = 0; m < i; ++m) sv = cmac(sv, sX[i * NL + m], x[m]);
+        const float di = sDinv[i];
+        x[i] = (i == k) ? make_float2(di, 0.f) : (i < k ? make_float2(0.f, 0.f) : make_float2(-sv.x * di, -sv.y * di));
+    }
+    __syncwarp();
+    if (lane < NL) {
+#pragma unroll
+        for (int i = 0; i < NL; ++i) sX[i * NL + k] = x[i];
+    }
+    __syncwarp();
+    // row k of G^-1 = X^H X (lane k; x = column k of X), A_kk
+    float2 gi[NL];
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+        float2 sv = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int m = j; m < NL; ++m) {
+            const float2 xm = x[m], xmj = sX[m * NL + j];
+            sv.x = fmaf(xm.x, xmj.x, fmaf(xm.y, xmj.y, sv.x));
+            sv.y = fmaf(xm.x, xmj.y, fmaf(-xm.y, xmj.x, sv.y));
+        }
+        gi[j] = sv;
+    }
+    float A = 0.f;
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
+        if (j == k) A = gi[j].x;
+    const float mu = fmaf(-s2, A, 1.f);
+    float sinr, fac;
+    if (s2 == 0.f) {
+        sinr = __int_as_float(0x7f800000);
+        fac = sqrtf(norm);
+    } else {
+        sinr = __fdividef(mu, s2 * A);
+        fac = __fdividef(sqrtf(norm), mu);
+    }
+    if (!(mu > 0.f) || fail) {
+        sinr = 0.f;
+        fac = 0.f;
+    }
+    // W~[r][k] = fac_k sum_j G^-1_kj conj(H_rj): lane (k, half) covers r in [half*NR/2, (half+1)*NR/2)
+    const int half = lane >> 4;
+    pdl_wait();  // the previous call may still read the workspace
+    if (valid) {
+        float2* ws = reinterpret_cast<float2*>(reinterpret_cast<float*>(a.ws) + u * WS);
+#pragma unroll 2
+        for (int rr = 0; rr < NR / 2; ++rr) {
+            const int r = half * (NR / 2) + rr;
+            const float4* hr = reinterpret_cast<const float4*>(sH + r * NL);
             float2 sv = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int m = 0; m < i; ++m) sv = cmac(sv, sL[i * NL + m], x[m]);
-            const float di = sDinv[i];
-            x[i] = (i == k) ? make_float2(di, 0.f) : (i < k ? make_float2(0.f, 0.f) : make_float2(-sv.x * di, -sv.y * di));
-        }
-#pragma unroll
-        for (int i = 0; i < NL; ++i) sG[i * NL + k] = x[i];
-    }
-    __syncthreads();
-    // G^-1 = X^H X (one entry per thread), mu / SINR / factor
-    float2 gi;
-    {
-        const int i = t / NL, j = t % NL;
-        float2 sv = make_float2(0.f, 0.f);
-        for (int m = (i > j ? i : j); m < NL; ++m) {
-            const float2 xi = sG[m * NL + i], xj = sG[m * NL + j];
-            sv.x = fmaf(xi.x, xj.x, fmaf(xi.y, xj.y, sv.x));
-            sv.y = fmaf(xi.x, xj.y, fmaf(-xi.y, xj.x, sv.y));
-        }
-        gi = sv;
-    }
-    __syncthreads();
-    {
-        const int i = t / NL, j = t % NL;
-        sL[i * NL + j] = gi;  // G^-1 into sL
-        if (i == j) {
-            const float A = gi.x;
-            const float mu = fmaf(-s2, A, 1.f);
-            float sinr, fac;
-            if (s2 == 0.f) {
-                sinr = __int_as_float(0x7f800000);
-                fac = sqrtf(norm);
-            } else {
-                sinr = __fdividef(mu, s2 * A);
-                fac = __fdividef(sqrtf(norm), mu);
+            for (int j2 = 0; j2 < NL / 2; ++j2) {
+                const float4 v = hr[j2];
+                sv.x = fmaf(gi[2 * j2].x, v.x, fmaf(gi[2 * j2].y, v.y, sv.x));
+                sv.y = fmaf(gi[2 * j2].y, v.x, fmaf(-gi[2 * j2].x, v.y, sv.y));
+                sv.x = fmaf(gi[2 * j2 + 1].x, v.z, fmaf(gi[2 * j2 + 1].y, v.w, sv.x));
+                sv.y = fmaf(gi[2 * j2 + 1].y, v.z, fmaf(-gi[2 * j2 + 1].x, v.w, sv.y));
             }
-            if (!(mu > 0.f) || sFail) {
-                sinr = 0.f;
-                fac = 0.f;
-            }
-            sFac[i] = fac;
-            sSinr[i] = sinr;
+            ws[r * NL + k] = fac > 0.f ? make_float2(sv.x * fac, sv.y * fac) : make_float2(0.f, 0.f);
         }
-    }
-    __syncthreads();
-    // W~[r][k] = fac_k sum_j G^-1_kj conj(H_rj): 4 entries per thread, k fastest
-    float2 wv[NR * NL / 256];
-#pragma unroll
-    for (int q = 0; q < NR * NL / 256; ++q) {
-        const int idx = t + 256 * q;
-        const int r = idx / NL, k = idx % NL;
-        float2 sv = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int j = 0; j < NL; ++j) {
-            const float2 g2 = sL[k * NL + j], h = sH[r * NL + j];
-            sv.x = fmaf(g2.x, h.x, fmaf(g2.y, h.y, sv.x));
-            sv.y = fmaf(g2.y, h.x, fmaf(-g2.x, h.y, sv.y));
+        if (lane < NL) {
+            reinterpret_cast<float*>(ws)[NR * NL * 2 + k] = sinr / norm * a.llr_scale;
+            if (a.sinr) a.sinr[u * NL + k] = sinr;
         }
-        const float fac = sFac[k];
-        wv[q] = fac > 0.f ? make_float2(sv.x * fac, sv.y * fac) : make_float2(0.f, 0.f);
+        if (lane == 0 && fail) atomicAdd(a.fail_count, 1ull);
     }
-    pdl_wait();  // the previous call may still read the workspace
-    float* ws = reinterpret_cast<float*>(a.ws) + u * WS;
-#pragma unroll
-    for (int q = 0; q < NR * NL / 256; ++q) reinterpret_cast<float2*>(ws)[t + 256 * q] = wv[q];
-    if (t < NL) {
-        ws[NR * NL * 2 + t] = sSinr[t] / norm * a.llr_scale;
-        if (a.sinr) a.sinr[u * NL + t] = sSinr[t];
-    }
-    if (t == 0 && sFail) atomicAdd(a.fail_count, 1ull);
 }
 
 template <int NR, int NL>
@@ -307,7 +322,9 @@ size_t workspace(const DetectArgs& a) {
 template <int NR, int NL, int QM, int LT>
 cudaError_t launch(const DetectArgs& a, cudaStream_t s) {
     if (a.n_units <= 0) return cudaSuccess;
-    cudaError_t e = launch_kernel(k_big_setup<NR, NL, QM>, dim3((unsigned)a.n_units), dim3(256), 0, s, a.overlap, a);
+    constexpr int UPB = 4;
+    cudaError_t e = launch_kernel(k_big_setup<NR, NL, QM, UPB>, dim3((unsigned)((a.n_units + UPB - 1) / UPB)),
+                                  dim3(32 * UPB), UPB * SetupSmem<NR, NL>::per_unit, s, a.overlap, a);
     if (e != cudaSuccess) return e;
     return launch_kernel(k_big_apply<NR, NL, QM, LT>, dim3((unsigned)a.n_units), dim3(kRe), BigSmem<NR, NL>::total, s,
                          a.overlap, a);
@@ -315,6 +332,9 @@ cudaError_t launch(const DetectArgs& a, cudaStream_t s) {
 
 template <int NR, int NL, int QM, int LT>
 cudaError_t prepare() {
+    cudaError_t e = cudaFuncSetAttribute(k_big_setup<NR, NL, QM, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(4 * SetupSmem<NR, NL>::per_unit));
+    if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(k_big_apply<NR, NL, QM, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)BigSmem<NR, NL>::total);
 }
