@@ -314,6 +314,315 @@ __global__ void __launch_bounds__(kRe) k_big_apply(DetectArgs a) {
     }
 }
 
+// ------------------------------------------------------------------------
+// k_big_tc: the same a6-a7 on the 5th-gen tensor cores (tcgen05, kind::tf32).
+//
+// Per PRB-unit the filter is a real GEMM  X^T[168 x 32] = Y^T[168 x 128] B[128 x 32]
+// with y rows (64 complex = 128 fp32, interleaved re/im) as the K-major A
+// operand and B = [[Wr^T, Wi^T], [-Wi^T, Wr^T]] (rows interleaved re/im, built
+// per unit in shared memory from W~). fp32 accuracy from TF32 units by the
+// 3-pass split A B = A_hi B_hi + A_hi B_lo + A_lo B_hi: the tensor core reads an
+// fp32 operand as TF32 (low 13 mantissa bits ignored, i.e. hi = trunc(x)), so
+// pass 1 uses (y, B), pass 2 (y, B_lo) with B_lo = B - trunc(B), and pass 3
+// (y_lo, B) after y is replaced in place by y - trunc(y). Dropped: lo*lo and
+// the truncation of the lo parts, ~2^-20 relative per product (R21).
+//
+// Persistent CTA (128 threads, one per SM). Shared memory holds two y stages
+// (cp.async with a manual 128-byte swizzle = the canonical SWIZZLE_128B
+// K-major UMMA layout, 4 K-tiles x 168 rows x 128 B each), B and B_lo
+// (4 K-tiles x 32 rows x 128 B). The next unit's y streams in while the current
+// one is computed. Two M=128 MMA tiles cover the 168 RE rows (rows 0-127 and
+// 40-167) with N=32 accumulator columns each in TMEM (64 columns allocated).
+// Epilogue: tcgen05.ld 32x32b.x32 gives each thread one RE's 32 outputs
+// (TMEM lane = RE row), exact max-log demap, 96-byte LLR record stores.
+template <int NR, int NL>
+struct TcSmem {
+    static constexpr int ROWS = kRe;                                       // 168
+    static constexpr int KT = NR * 2 / 32;                                 // K-tiles of 32 fp32 (128 B)
+    static constexpr size_t ktile = (size_t)ROWS * 128;                    // 21504 = 21 KiB
+    static constexpr size_t ystage = (size_t)KT * ktile;                   // 86016
+    static constexpr size_t btile = (size_t)2 * NL * 128;                  // 32 rows x 128 B
+    static constexpr size_t y0 = 0;
+    static constexpr size_t B = 2 * ystage;
+    static constexpr size_t Blo = B + (size_t)KT * btile;
+    static constexpr size_t bars = Blo + (size_t)KT * btile;               // full[2], mma
+    static constexpr size_t tmem = bars + 32;
+    static constexpr size_t total = tmem + 16 + 1024;                      // + alignment slack
+};
+
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+    // start address >> 4 | LBO (unused for swizzled K-major) = 1 | SBO = 1024 B | version 1 | SWIZZLE_128B
+    return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// bounded wait: a descriptor bug must not hang the GPU
+__device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity) {
+    uint32_t ok = 0;
+    for (long long it = 0; it < (1ll << 26); ++it) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+    }
+    __trap();
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+        "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+// y rows of unit u -> stage (128 threads; warp w moves rows w, w+4, ...; lane = 16-byte chunk)
+template <int NR, int NL>
+__device__ __forceinline__ void tc_issue_y(const DetectArgs& a, uint32_t stage, long long u, uint64_t* bar) {
+    using SM = TcSmem<NR, NL>;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);
+    const int kt = lane >> 3, cc = lane & 7;
+#pragma unroll 2
+    for (int i = warp; i < SM::ROWS; i += 4) {
+        const int s = i / kSc, f = i % kSc;
+        const char* src = reinterpret_cast<const char*>(a.y + ((size_t)(slot * kSym + s) * a.n_sc + fb * kSc + f) * NR) +
+                          lane * 16;
+        cp_async16(stage + kt * (uint32_t)SM::ktile + i * 128u + ((cc ^ (i & 7)) << 4), src);
+    }
+    cp_async_arrive(bar);
+}
+
+template <int NR, int NL, int QM, int LT>
+__global__ void __launch_bounds__(128, 1) k_big_tc(DetectArgs a) {
+    static_assert(NL == 16 && NR == 64, "k_big_tc: 64 x 16");
+    using SM = TcSmem<NR, NL>;
+    constexpr int KT = SM::KT;
+    constexpr int WS = BigWs<NR, NL>::stride;
+    extern __shared__ unsigned char smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    unsigned char* gbase = smem_raw + (base - raw);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + SM::bars);  // [0],[1] y stages, [2] mma
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + SM::tmem);
+    float* fB = reinterpret_cast<float*>(gbase + SM::B);
+    float* fBlo = reinterpret_cast<float*>(gbase + SM::Blo);
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+
+    pdl_launch_dependents();
+    if (t == 0) {
+        mbar_init(&bars[0], 128);
+        mbar_init(&bars[1], 128);
+        mbar_init(&bars[2], 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    // instruction descriptor: D f32, A/B tf32, K-major A and B, N = 32, M = 128
+    constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+    const float norm = (float)qam_norm(QM);
+    const bool zf = !(a.sigma2 > 0.f);
+    long long u = blockIdx.x;
+    if (u < a.n_units) tc_issue_y<NR, NL>(a, base + SM::y0, u, &bars[0]);
+    pdl_wait();  // W~ of this call's setup kernel is complete
+    uint32_t mma_phase = 0;
+#pragma unroll 1
+    for (int it = 0; u < a.n_units; ++it, u += gridDim.x) {
+        const int st = it & 1;
+        const uint32_t ys = base + SM::y0 + st * (uint32_t)SM::ystage;
+        float* fy = reinterpret_cast<float*>(gbase + SM::y0 + st * SM::ystage);
+        const long long un = u + gridDim.x;
+        if (un < a.n_units) tc_issue_y<NR, NL>(a, base + SM::y0 + (st ^ 1) * (uint32_t)SM::ystage, un, &bars[st ^ 1]);
+        // B, B_lo from W~ [r][k]: thread -> row n = t / 4 (xr_l or xi_l), K-tile kt = t % 4 (antennas 16kt..16kt+15)
+        const float* wsu = reinterpret_cast<const float*>(a.ws) + u * WS;
+        {
+            const int n = t >> 2, kt = t & 3;
+            const int l = n & 15;
+            const bool im_row = n >= 16;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {  // chunk c = antennas r0, r0+1 (4 floats: yr, yi, yr, yi)
+                const int r0 = kt * 16 + 2 * c;
+                const float2 w0 = *reinterpret_cast<const float2*>(wsu + 2 * (r0 * NL + l));
+                const float2 w1 = *reinterpret_cast<const float2*>(wsu + 2 * ((r0 + 1) * NL + l));
+                float4 v;
+                if (!im_row) v = make_float4(w0.x, -w0.y, w1.x, -w1.y);   // xr += Wr yr - Wi yi
+                else v = make_float4(w0.y, w0.x, w1.y, w1.x);             // xi += Wi yr + Wr yi
+                const float4 lo = make_float4(v.x - tf32_trunc(v.x), v.y - tf32_trunc(v.y), v.z - tf32_trunc(v.z),
+                                              v.w - tf32_trunc(v.w));
+                const int off = kt * (int)(SM::btile / 4) + n * 32 + ((c ^ (n & 7)) << 2);
+                *reinterpret_cast<float4*>(fB + off) = v;
+                *reinterpret_cast<float4*>(fBlo + off) = lo;
+            }
+        }
+        float slope[NL];
+#pragma unroll
+        for (int k = 0; k < NL; ++k) slope[k] = wsu[NR * NL * 2 + k];
+        mbar_wait_bounded(&bars[st], (it >> 1) & 1);
+        fence_proxy_async();
+        __syncthreads();
+        // passes 1 + 2: (y, B) and (y, B_lo); tile 0 rows 0-127 -> TMEM cols 32..63, tile 1 rows 40-167 -> cols 0..31
+        if (t == 0) {
+            tc_fence_after();
+#pragma unroll
+            for (int tile = 0; tile < 2; ++tile) {
+                const uint32_t row0 = tile ? 40u : 0u;
+                const uint32_t dcol = tile ? 0u : 32u;
+#pragma unroll
+                for (int pass = 0; pass < 2; ++pass) {
+                    const uint32_t bb = base + (pass ? (uint32_t)SM::Blo : (uint32_t)SM::B);
+#pragma unroll
+                    for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+                        for (int ks = 0; ks < 4; ++ks) {
+                            const uint64_t da = umma_desc_sw128(ys + kt * (uint32_t)SM::ktile + row0 * 128u + ks * 32u);
+                            const uint64_t db = umma_desc_sw128(bb + kt * (uint32_t)SM::btile + ks * 32u);
+                            umma_tf32(tmem + dcol, da, db, idesc, (pass | kt | ks) ? 1u : 0u);
+                        }
+                }
+            }
+            umma_commit(&bars[2]);
+        }
+        mbar_wait_bounded(&bars[2], mma_phase);
+        mma_phase ^= 1;
+        // y -> y_lo in place (passes 1-2 have consumed y)
+        {
+            float4* y4 = reinterpret_cast<float4*>(fy);
+            constexpr int n4 = (int)(SM::ystage / 16);
+#pragma unroll 4
+            for (int i = t; i < n4; i += 128) {
+                float4 v = y4[i];
+                v.x -= tf32_trunc(v.x);
+                v.y -= tf32_trunc(v.y);
+                v.z -= tf32_trunc(v.z);
+                v.w -= tf32_trunc(v.w);
+                y4[i] = v;
+            }
+        }
+        fence_proxy_async();
+        __syncthreads();
+        if (t == 0) {
+            tc_fence_after();
+#pragma unroll
+            for (int tile = 0; tile < 2; ++tile) {
+                const uint32_t row0 = tile ? 40u : 0u;
+                const uint32_t dcol = tile ? 0u : 32u;
+#pragma unroll
+                for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks) {
+                        const uint64_t da = umma_desc_sw128(ys + kt * (uint32_t)SM::ktile + row0 * 128u + ks * 32u);
+                        const uint64_t db = umma_desc_sw128(base + (uint32_t)SM::B + kt * (uint32_t)SM::btile + ks * 32u);
+                        umma_tf32(tmem + dcol, da, db, idesc, 1u);
+                    }
+            }
+            umma_commit(&bars[2]);
+        }
+        mbar_wait_bounded(&bars[2], mma_phase);
+        mma_phase ^= 1;
+        tc_fence_after();
+        // epilogue: tile 1 lanes -> rows 40..167 (all warps); tile 0 lanes 0..39 -> rows 0..39 (warps 0, 1)
+        const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);
+        constexpr int kRecBytes = NL * QM * LlrTraits<LT>::bytes;
+#pragma unroll 1
+        for (int pass = 0; pass < 2; ++pass) {
+            if (pass == 1 && warp >= 2) break;
+            const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16) + (pass ? 32u : 0u);
+            uint32_t acc[32];
+            tmem_ld32(taddr, acc);  // warp-collective
+            const int row = pass ? 32 * warp + lane : 40 + 32 * warp + lane;
+            if (pass == 1 && row >= 40) continue;
+            const int s = row / kSc, f = row % kSc;
+            const size_t re = (size_t)(slot * kSym + s) * a.n_sc + fb * kSc + f;
+            if (a.llr) {
+#pragma unroll
+                for (int g4 = 0; g4 < NL / 4; ++g4) {  // 4 layers per packed group
+                    float v[4 * QM];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int k = 4 * g4 + q;
+                        const float2 x = make_float2(__uint_as_float(acc[k]), __uint_as_float(acc[16 + k]));
+                        if (!zf) demap_layer<QM, false, LT>(x, slope[k], v + q * QM);
+                        else demap_layer<QM, true, LT>(x, slope[k], v + q * QM);
+                    }
+                    constexpr int gb = 4 * QM * LlrTraits<LT>::bytes;
+                    uint32_t wd[(gb + 3) / 4];
+                    if (!zf) pack_llr<LT, 4 * QM, false>(v, wd);
+                    else pack_llr<LT, 4 * QM, true>(v, wd);
+                    store_bytes<gb>((char*)a.llr + re * kRecBytes + g4 * gb, wd);
+                }
+            }
+            if (a.xhat) {
+                const float ia = rsqrtf(norm);
+#pragma unroll
+                for (int k = 0; k < NL; ++k)
+                    a.xhat[re * NL + k] = make_float2(__uint_as_float(acc[k]) * ia, __uint_as_float(acc[16 + k]) * ia);
+            }
+        }
+        tc_fence_before();
+        __syncthreads();  // TMEM, B and this y stage are free
+    }
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
+}
+
+template <int NR, int NL, int QM, int LT>
+cudaError_t launch_tc(const DetectArgs& a, cudaStream_t s) {
+    if (a.n_units <= 0) return cudaSuccess;
+    static int n_sm = 0;
+    if (!n_sm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    constexpr int UPB = 4;
+    cudaError_t e = launch_kernel(k_big_setup<NR, NL, QM, UPB>, dim3((unsigned)((a.n_units + UPB - 1) / UPB)),
+                                  dim3(32 * UPB), UPB * SetupSmem<NR, NL>::per_unit, s, a.overlap, a);
+    if (e != cudaSuccess) return e;
+    const unsigned grid = (unsigned)(a.n_units < n_sm ? a.n_units : n_sm);
+    return launch_kernel(k_big_tc<NR, NL, QM, LT>, dim3(grid), dim3(128), TcSmem<NR, NL>::total, s, a.overlap, a);
+}
+
+template <int NR, int NL, int QM, int LT>
+cudaError_t prepare_tc() {
+    cudaError_t e = cudaFuncSetAttribute(k_big_setup<NR, NL, QM, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(4 * SetupSmem<NR, NL>::per_unit));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_big_tc<NR, NL, QM, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)TcSmem<NR, NL>::total);
+}
+
 template <int NR, int NL>
 size_t workspace(const DetectArgs& a) {
     return (size_t)a.n_units * BigWs<NR, NL>::stride * 4;
@@ -342,7 +651,14 @@ cudaError_t prepare() {
 #define BIG_ENTRY(NAME, NR, NL, QM, LT) \
     KernelEntry { NAME, NR, NL, QM, kSc, 14, LT, 32, 2, launch<NR, NL, QM, LT>, prepare<NR, NL, QM, LT>, workspace<NR, NL> }
 
+#define BIGTC_ENTRY(NAME, NR, NL, QM, LT)                                                                 \
+    KernelEntry {                                                                                         \
+        NAME, NR, NL, QM, kSc, 14, LT, 32, 2, launch_tc<NR, NL, QM, LT>, prepare_tc<NR, NL, QM, LT>,     \
+            workspace<NR, NL>                                                                             \
+    }
+
 const KernelEntry kEntries[] = {
+    BIGTC_ENTRY("bigtc_64x16_q6_i8", 64, 16, 6, kLlrI8),  // C5 (tensor cores), selectable by name for now
     BIG_ENTRY("big_64x16_q6_i8", 64, 16, 6, kLlrI8),  // C5
     BIG_ENTRY("big_64x16_q6_f16", 64, 16, 6, kLlrF16),
     BIG_ENTRY("big_64x16_q6_f32", 64, 16, 6, kLlrF32),
