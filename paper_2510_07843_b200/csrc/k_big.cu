@@ -399,9 +399,16 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
         : "r"(taddr));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* r) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
 __device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
-// y rows of unit u -> stage (128 threads; warp w moves rows w, w+4, ...; lane = 16-byte chunk)
+constexpr int kTcThreads = 256;  // 8 warps: warps w and w+4 share a TMEM lane window
+
+// y rows of unit u -> stage (warp w moves rows w, w+8, ...; lane = 16-byte chunk)
 template <int NR, int NL>
 __device__ __forceinline__ void tc_issue_y(const DetectArgs& a, uint32_t stage, long long u, uint64_t* bar) {
     using SM = TcSmem<NR, NL>;
@@ -409,7 +416,7 @@ __device__ __forceinline__ void tc_issue_y(const DetectArgs& a, uint32_t stage, 
     const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);
     const int kt = lane >> 3, cc = lane & 7;
 #pragma unroll 2
-    for (int i = warp; i < SM::ROWS; i += 4) {
+    for (int i = warp; i < SM::ROWS; i += kTcThreads / 32) {
         const int s = i / kSc, f = i % kSc;
         const char* src = reinterpret_cast<const char*>(a.y + ((size_t)(slot * kSym + s) * a.n_sc + fb * kSc + f) * NR) +
                           lane * 16;
@@ -419,7 +426,7 @@ __device__ __forceinline__ void tc_issue_y(const DetectArgs& a, uint32_t stage, 
 }
 
 template <int NR, int NL, int QM, int LT>
-__global__ void __launch_bounds__(128, 1) k_big_tc(DetectArgs a) {
+__global__ void __launch_bounds__(kTcThreads, 1) k_big_tc(DetectArgs a) {
     static_assert(NL == 16 && NR == 64, "k_big_tc: 64 x 16");
     using SM = TcSmem<NR, NL>;
     constexpr int KT = SM::KT;
@@ -436,8 +443,8 @@ __global__ void __launch_bounds__(128, 1) k_big_tc(DetectArgs a) {
 
     pdl_launch_dependents();
     if (t == 0) {
-        mbar_init(&bars[0], 128);
-        mbar_init(&bars[1], 128);
+        mbar_init(&bars[0], kTcThreads);
+        mbar_init(&bars[1], kTcThreads);
         mbar_init(&bars[2], 1);
         fence_mbar_init();
     }
@@ -465,14 +472,15 @@ __global__ void __launch_bounds__(128, 1) k_big_tc(DetectArgs a) {
         float* fy = reinterpret_cast<float*>(gbase + SM::y0 + st * SM::ystage);
         const long long un = u + gridDim.x;
         if (un < a.n_units) tc_issue_y<NR, NL>(a, base + SM::y0 + (st ^ 1) * (uint32_t)SM::ystage, un, &bars[st ^ 1]);
-        // B, B_lo from W~ [r][k]: thread -> row n = t / 4 (xr_l or xi_l), K-tile kt = t % 4 (antennas 16kt..16kt+15)
+        // B, B_lo from W~ [r][k]: thread -> row n = t / 8 (xr_l or xi_l), K-tile kt, 4 chunks (8 antennas)
         const float* wsu = reinterpret_cast<const float*>(a.ws) + u * WS;
         {
-            const int n = t >> 2, kt = t & 3;
+            const int n = t >> 3, kt = (t >> 1) & 3, c0 = (t & 1) * 4;
             const int l = n & 15;
             const bool im_row = n >= 16;
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {  // chunk c = antennas r0, r0+1 (4 floats: yr, yi, yr, yi)
+            for (int cq = 0; cq < 4; ++cq) {  // chunk c = antennas r0, r0+1 (4 floats: yr, yi, yr, yi)
+                const int c = c0 + cq;
                 const int r0 = kt * 16 + 2 * c;
                 const float2 w0 = *reinterpret_cast<const float2*>(wsu + 2 * (r0 * NL + l));
                 const float2 w1 = *reinterpret_cast<const float2*>(wsu + 2 * ((r0 + 1) * NL + l));
@@ -486,9 +494,9 @@ __global__ void __launch_bounds__(128, 1) k_big_tc(DetectArgs a) {
                 *reinterpret_cast<float4*>(fBlo + off) = lo;
             }
         }
-        float slope[NL];
+        float slope[NL / 2];  // this warp's layer half (warps 0-3: layers 0-7, warps 4-7: 8-15)
 #pragma unroll
-        for (int k = 0; k < NL; ++k) slope[k] = wsu[NR * NL * 2 + k];
+        for (int k = 0; k < NL / 2; ++k) slope[k] = wsu[NR * NL * 2 + (warp >> 2) * (NL / 2) + k];
         mbar_wait_bounded(&bars[st], (it >> 1) & 1);
         fence_proxy_async();
         __syncthreads();
@@ -521,7 +529,7 @@ __global__ void __launch_bounds__(128, 1) k_big_tc(DetectArgs a) {
             float4* y4 = reinterpret_cast<float4*>(fy);
             constexpr int n4 = (int)(SM::ystage / 16);
 #pragma unroll 4
-            for (int i = t; i < n4; i += 128) {
+            for (int i = t; i < n4; i += kTcThreads) {
                 float4 v = y4[i];
                 v.x -= tf32_trunc(v.x);
                 v.y -= tf32_trunc(v.y);
@@ -552,42 +560,44 @@ __global__ void __launch_bounds__(128, 1) k_big_tc(DetectArgs a) {
         mbar_wait_bounded(&bars[2], mma_phase);
         mma_phase ^= 1;
         tc_fence_after();
-        // epilogue: tile 1 lanes -> rows 40..167 (all warps); tile 0 lanes 0..39 -> rows 0..39 (warps 0, 1)
+        // epilogue: warp w reads TMEM lanes 32(w%4).. ; warps 0-3 take layers 0-7, warps 4-7 layers 8-15.
+        // tile 1 (cols 0..31): lanes -> rows 40..167; tile 0 (cols 32..63): lanes 0..39 -> rows 0..39.
         const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);
+        const int wq = warp & 3, lh = warp >> 2;  // lane window, layer half
+        constexpr int KH = NL / 2;
         constexpr int kRecBytes = NL * QM * LlrTraits<LT>::bytes;
+        constexpr int kHalfBytes = KH * QM * LlrTraits<LT>::bytes;
 #pragma unroll 1
         for (int pass = 0; pass < 2; ++pass) {
-            if (pass == 1 && warp >= 2) break;
-            const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16) + (pass ? 32u : 0u);
-            uint32_t acc[32];
-            tmem_ld32(taddr, acc);  // warp-collective
-            const int row = pass ? 32 * warp + lane : 40 + 32 * warp + lane;
+            if (pass == 1 && wq >= 2) break;
+            const uint32_t taddr = tmem + ((uint32_t)(32 * wq) << 16) + (pass ? 32u : 0u) + KH * lh;
+            uint32_t xr[KH], xi[KH];
+            tmem_ld8(taddr, xr);        // columns KH*lh .. +7      (Re of this half's layers)
+            tmem_ld8(taddr + 16u, xi);  // columns 16 + KH*lh .. +7 (Im)
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            const int row = pass ? 32 * wq + lane : 40 + 32 * wq + lane;
             if (pass == 1 && row >= 40) continue;
             const int s = row / kSc, f = row % kSc;
             const size_t re = (size_t)(slot * kSym + s) * a.n_sc + fb * kSc + f;
             if (a.llr) {
+                float v[KH * QM];
 #pragma unroll
-                for (int g4 = 0; g4 < NL / 4; ++g4) {  // 4 layers per packed group
-                    float v[4 * QM];
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int k = 4 * g4 + q;
-                        const float2 x = make_float2(__uint_as_float(acc[k]), __uint_as_float(acc[16 + k]));
-                        if (!zf) demap_layer<QM, false, LT>(x, slope[k], v + q * QM);
-                        else demap_layer<QM, true, LT>(x, slope[k], v + q * QM);
-                    }
-                    constexpr int gb = 4 * QM * LlrTraits<LT>::bytes;
-                    uint32_t wd[(gb + 3) / 4];
-                    if (!zf) pack_llr<LT, 4 * QM, false>(v, wd);
-                    else pack_llr<LT, 4 * QM, true>(v, wd);
-                    store_bytes<gb>((char*)a.llr + re * kRecBytes + g4 * gb, wd);
+                for (int q = 0; q < KH; ++q) {
+                    const float2 x = make_float2(__uint_as_float(xr[q]), __uint_as_float(xi[q]));
+                    if (!zf) demap_layer<QM, false, LT>(x, slope[q], v + q * QM);
+                    else demap_layer<QM, true, LT>(x, slope[q], v + q * QM);
                 }
+                uint32_t wd[(kHalfBytes + 3) / 4];
+                if (!zf) pack_llr<LT, KH * QM, false>(v, wd);
+                else pack_llr<LT, KH * QM, true>(v, wd);
+                store_bytes<kHalfBytes>((char*)a.llr + re * kRecBytes + lh * kHalfBytes, wd);
             }
             if (a.xhat) {
                 const float ia = rsqrtf(norm);
 #pragma unroll
-                for (int k = 0; k < NL; ++k)
-                    a.xhat[re * NL + k] = make_float2(__uint_as_float(acc[k]) * ia, __uint_as_float(acc[16 + k]) * ia);
+                for (int q = 0; q < KH; ++q)
+                    a.xhat[re * NL + KH * lh + q] =
+                        make_float2(__uint_as_float(xr[q]) * ia, __uint_as_float(xi[q]) * ia);
             }
         }
         tc_fence_before();
@@ -611,7 +621,8 @@ cudaError_t launch_tc(const DetectArgs& a, cudaStream_t s) {
                                   dim3(32 * UPB), UPB * SetupSmem<NR, NL>::per_unit, s, a.overlap, a);
     if (e != cudaSuccess) return e;
     const unsigned grid = (unsigned)(a.n_units < n_sm ? a.n_units : n_sm);
-    return launch_kernel(k_big_tc<NR, NL, QM, LT>, dim3(grid), dim3(128), TcSmem<NR, NL>::total, s, a.overlap, a);
+    return launch_kernel(k_big_tc<NR, NL, QM, LT>, dim3(grid), dim3(kTcThreads), TcSmem<NR, NL>::total, s, a.overlap,
+                         a);
 }
 
 template <int NR, int NL, int QM, int LT>
