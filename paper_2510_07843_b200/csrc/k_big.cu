@@ -345,8 +345,8 @@ struct TcSmem {
     static constexpr size_t y0 = 0;
     static constexpr size_t B = 2 * ystage;
     static constexpr size_t Blo = B + (size_t)KT * btile;
-    static constexpr size_t bars = Blo + (size_t)KT * btile;               // full[2], mma
-    static constexpr size_t tmem = bars + 32;
+    static constexpr size_t bars = Blo + (size_t)KT * btile;               // up to 8 mbarriers
+    static constexpr size_t tmem = bars + 64;
     static constexpr size_t total = tmem + 16 + 1024;                      // + alignment slack
 };
 
@@ -607,6 +607,288 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_big_tc(DetectArgs a) {
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
 }
 
+// ------------------------------------------------------------------------
+// k_big_tc2: warp-specialised, software-pipelined version of k_big_tc.
+// Warps 0-7 (SIMT): y staging (cp.async, 2 stages), B / B_lo construction,
+// y -> y_lo conversion and the epilogue; warp 8 lane 0: the MMA issuer. TMEM
+// holds two accumulator buffers, so the epilogue of unit i-1 runs while the
+// tensor cores do passes 1-2 of unit i. mbarriers: yfull[2] (cp.async), bready,
+// c1 (passes 1-2 committed), ylo, c2 (pass 3 committed), tfree[2].
+constexpr int kTc2Simt = 256;
+__device__ __forceinline__ void simt_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+template <int NR, int NL, int QM, int LT>
+__device__ __forceinline__ void tc2_epilogue(const DetectArgs& a, uint32_t tmem_buf, long long u, const float* slope,
+                                             bool zf, float norm) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);
+    const int wq = warp & 3, lh = warp >> 2;
+    constexpr int KH = NL / 2;
+    constexpr int kRecBytes = NL * QM * LlrTraits<LT>::bytes;
+    constexpr int kHalfBytes = KH * QM * LlrTraits<LT>::bytes;
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+        if (pass == 1 && wq >= 2) break;
+        const uint32_t taddr = tmem_buf + ((uint32_t)(32 * wq) << 16) + (pass ? 32u : 0u) + KH * lh;
+        uint32_t xr[KH], xi[KH];
+        tmem_ld8(taddr, xr);
+        tmem_ld8(taddr + 16u, xi);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const int row = pass ? 32 * wq + lane : 40 + 32 * wq + lane;
+        if (pass == 1 && row >= 40) continue;
+        const int s = row / kSc, f = row % kSc;
+        const size_t re = (size_t)(slot * kSym + s) * a.n_sc + fb * kSc + f;
+        if (a.llr) {
+            float v[KH * QM];
+#pragma unroll
+            for (int q = 0; q < KH; ++q) {
+                const float2 x = make_float2(__uint_as_float(xr[q]), __uint_as_float(xi[q]));
+                if (!zf) demap_layer<QM, false, LT>(x, slope[q], v + q * QM);
+                else demap_layer<QM, true, LT>(x, slope[q], v + q * QM);
+            }
+            uint32_t wd[(kHalfBytes + 3) / 4];
+            if (!zf) pack_llr<LT, KH * QM, false>(v, wd);
+            else pack_llr<LT, KH * QM, true>(v, wd);
+            store_bytes<kHalfBytes>((char*)a.llr + re * kRecBytes + lh * kHalfBytes, wd);
+        }
+        if (a.xhat) {
+            const float ia = rsqrtf(norm);
+#pragma unroll
+            for (int q = 0; q < KH; ++q)
+                a.xhat[re * NL + KH * lh + q] = make_float2(__uint_as_float(xr[q]) * ia, __uint_as_float(xi[q]) * ia);
+        }
+    }
+}
+
+// W~ rows of unit u needed by this thread for B (thread -> row n = t/8, K-tile (t>>1)&3, chunks 4(t&1)..+3)
+template <int NR, int NL>
+__device__ __forceinline__ void tc2_fetch_w(const DetectArgs& a, long long u, float4 (&wv)[4]) {
+    constexpr int WS = BigWs<NR, NL>::stride;
+    const int t = threadIdx.x;
+    const int n = t >> 3, kt = (t >> 1) & 3, c0 = (t & 1) * 4, l = n & 15;
+    const float* wsu = reinterpret_cast<const float*>(a.ws) + u * WS;
+#pragma unroll
+    for (int cq = 0; cq < 4; ++cq) {
+        const int r0 = kt * 16 + 2 * (c0 + cq);
+        const float2 w0 = *reinterpret_cast<const float2*>(wsu + 2 * (r0 * NL + l));
+        const float2 w1 = *reinterpret_cast<const float2*>(wsu + 2 * ((r0 + 1) * NL + l));
+        wv[cq] = make_float4(w0.x, w0.y, w1.x, w1.y);
+    }
+}
+template <int NR, int NL>
+__device__ __forceinline__ void tc2_build_b(float* fB, float* fBlo, const float4 (&wv)[4]) {
+    using SM = TcSmem<NR, NL>;
+    const int t = threadIdx.x;
+    const int n = t >> 3, kt = (t >> 1) & 3, c0 = (t & 1) * 4;
+    const bool im_row = n >= 16;
+#pragma unroll
+    for (int cq = 0; cq < 4; ++cq) {
+        const int c = c0 + cq;
+        const float4 w = wv[cq];  // (Wr_r0, Wi_r0, Wr_r1, Wi_r1)
+        float4 v;
+        if (!im_row) v = make_float4(w.x, -w.y, w.z, -w.w);   // xr += Wr yr - Wi yi
+        else v = make_float4(w.y, w.x, w.w, w.z);             // xi += Wi yr + Wr yi
+        const float4 lo = make_float4(v.x - tf32_trunc(v.x), v.y - tf32_trunc(v.y), v.z - tf32_trunc(v.z),
+                                      v.w - tf32_trunc(v.w));
+        const int off = kt * (int)(SM::btile / 4) + n * 32 + ((c ^ (n & 7)) << 2);
+        *reinterpret_cast<float4*>(fB + off) = v;
+        *reinterpret_cast<float4*>(fBlo + off) = lo;
+    }
+}
+
+template <int NR, int NL, int QM, int LT>
+__global__ void __launch_bounds__(kTc2Simt + 32, 1) k_big_tc2(DetectArgs a) {
+    static_assert(NL == 16 && NR == 64, "k_big_tc2: 64 x 16");
+    using SM = TcSmem<NR, NL>;
+    constexpr int KT = SM::KT;
+    constexpr int WS = BigWs<NR, NL>::stride;
+    extern __shared__ unsigned char smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    unsigned char* gbase = smem_raw + (base - raw);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + SM::bars);
+    uint64_t* yfull = bars;         // [2]
+    uint64_t* bready = bars + 2;
+    uint64_t* c1 = bars + 3;
+    uint64_t* ylo = bars + 4;
+    uint64_t* c2 = bars + 5;
+    uint64_t* tfree = bars + 6;     // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + SM::tmem);
+    float* fB = reinterpret_cast<float*>(gbase + SM::B);
+    float* fBlo = reinterpret_cast<float*>(gbase + SM::Blo);
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    static_assert(SM::tmem - SM::bars >= 64, "barrier space");
+
+    pdl_launch_dependents();
+    if (t == 0) {
+        mbar_init(&yfull[0], kTc2Simt);
+        mbar_init(&yfull[1], kTc2Simt);
+        for (int i = 2; i < 8; ++i) mbar_init(&bars[i], 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const long long u0 = blockIdx.x, du = gridDim.x;
+    const long long n_my = u0 < a.n_units ? (a.n_units - u0 + du - 1) / du : 0;  // units of this CTA
+
+    if (warp == kTc2Simt / 32) {
+        // ===== MMA issuer =====
+        if (lane == 0) {
+            constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+#pragma unroll 1
+            for (long long i = 0; i < n_my; ++i) {
+                const int st = (int)(i & 1);
+                const uint32_t ys = base + SM::y0 + st * (uint32_t)SM::ystage;
+                const uint32_t acc = tmem + 64u * (uint32_t)st;
+                if (i >= 2) mbar_wait_bounded(&tfree[st], (uint32_t)(((i >> 1) + 1) & 1));
+                mbar_wait_bounded(&yfull[st], (uint32_t)((i >> 1) & 1));
+                mbar_wait_bounded(bready, (uint32_t)(i & 1));
+                fence_proxy_async();
+                tc_fence_after();
+#pragma unroll
+                for (int tile = 0; tile < 2; ++tile) {
+                    const uint32_t row0 = tile ? 40u : 0u, dcol = tile ? 0u : 32u;
+#pragma unroll
+                    for (int pass = 0; pass < 2; ++pass) {
+                        const uint32_t bb = base + (pass ? (uint32_t)SM::Blo : (uint32_t)SM::B);
+#pragma unroll
+                        for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+                            for (int ks = 0; ks < 4; ++ks)
+                                umma_tf32(acc + dcol,
+                                          umma_desc_sw128(ys + kt * (uint32_t)SM::ktile + row0 * 128u + ks * 32u),
+                                          umma_desc_sw128(bb + kt * (uint32_t)SM::btile + ks * 32u), idesc,
+                                          (pass | kt | ks) ? 1u : 0u);
+                    }
+                }
+                umma_commit(c1);
+                mbar_wait_bounded(ylo, (uint32_t)(i & 1));
+                fence_proxy_async();
+                tc_fence_after();
+#pragma unroll
+                for (int tile = 0; tile < 2; ++tile) {
+                    const uint32_t row0 = tile ? 40u : 0u, dcol = tile ? 0u : 32u;
+#pragma unroll
+                    for (int kt = 0; kt < KT; ++kt)
+#pragma unroll
+                        for (int ks = 0; ks < 4; ++ks)
+                            umma_tf32(acc + dcol, umma_desc_sw128(ys + kt * (uint32_t)SM::ktile + row0 * 128u + ks * 32u),
+                                      umma_desc_sw128(base + (uint32_t)SM::B + kt * (uint32_t)SM::btile + ks * 32u),
+                                      idesc, 1u);
+                }
+                umma_commit(c2);
+            }
+        }
+    } else {
+        // ===== SIMT warps =====
+        const float norm = (float)qam_norm(QM);
+        const bool zf = !(a.sigma2 > 0.f);
+        if (n_my > 0) tc_issue_y<NR, NL>(a, base + SM::y0, u0, &yfull[0]);
+        if (n_my > 1) tc_issue_y<NR, NL>(a, base + SM::y0 + (uint32_t)SM::ystage, u0 + du, &yfull[1]);
+        pdl_wait();  // W~ of this call's setup kernel is complete
+        float4 wv[4];
+        if (n_my > 0) {
+            tc2_fetch_w<NR, NL>(a, u0, wv);
+            tc2_build_b<NR, NL>(fB, fBlo, wv);
+            fence_proxy_async();
+            simt_bar();
+            if (t == 0) mbar_arrive(bready);
+        }
+        float slope_prev[NL / 2];
+#pragma unroll 1
+        for (long long i = 0; i < n_my; ++i) {
+            const long long u = u0 + i * du;
+            const int st = (int)(i & 1);
+            float slope[NL / 2];
+            {
+                const float* wsu = reinterpret_cast<const float*>(a.ws) + u * WS + NR * NL * 2 + (warp >> 2) * (NL / 2);
+#pragma unroll
+                for (int k = 0; k < NL / 2; ++k) slope[k] = wsu[k];
+            }
+            if (i >= 1) {
+                // unit i-1: pass 3 done -> its y stage is free (refill with unit i+1) and its accumulator is ready
+                mbar_wait_bounded(c2, (uint32_t)((i - 1) & 1));
+                if (i + 1 < n_my) tc_issue_y<NR, NL>(a, base + SM::y0 + (st ^ 1) * (uint32_t)SM::ystage, u + du, &yfull[st ^ 1]);
+                tc_fence_after();
+                tc2_epilogue<NR, NL, QM, LT>(a, tmem + 64u * (uint32_t)(st ^ 1), u - du, slope_prev, zf, norm);
+                tc_fence_before();
+                simt_bar();
+                if (t == 0) mbar_arrive(&tfree[st ^ 1]);
+            }
+            // passes 1-2 of unit i done -> y -> y_lo in place
+            mbar_wait_bounded(c1, (uint32_t)(i & 1));
+            {
+                float4* y4 = reinterpret_cast<float4*>(gbase + SM::y0 + st * SM::ystage);
+                constexpr int n4 = (int)(SM::ystage / 16);
+#pragma unroll 4
+                for (int q = t; q < n4; q += kTc2Simt) {
+                    float4 v = y4[q];
+                    v.x -= tf32_trunc(v.x);
+                    v.y -= tf32_trunc(v.y);
+                    v.z -= tf32_trunc(v.z);
+                    v.w -= tf32_trunc(v.w);
+                    y4[q] = v;
+                }
+            }
+            fence_proxy_async();
+            simt_bar();
+            if (t == 0) mbar_arrive(ylo);
+            if (i + 1 < n_my) {
+                tc2_fetch_w<NR, NL>(a, u + du, wv);   // overlaps pass 3
+                mbar_wait_bounded(c2, (uint32_t)(i & 1));
+                tc2_build_b<NR, NL>(fB, fBlo, wv);
+                fence_proxy_async();
+                simt_bar();
+                if (t == 0) mbar_arrive(bready);
+            }
+#pragma unroll
+            for (int k = 0; k < NL / 2; ++k) slope_prev[k] = slope[k];
+        }
+        if (n_my > 0) {
+            const long long i = n_my - 1;
+            mbar_wait_bounded(c2, (uint32_t)(i & 1));
+            tc_fence_after();
+            tc2_epilogue<NR, NL, QM, LT>(a, tmem + 64u * (uint32_t)(i & 1), u0 + i * du, slope_prev, zf, norm);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+}
+
+template <int NR, int NL, int QM, int LT>
+cudaError_t launch_tc2(const DetectArgs& a, cudaStream_t s) {
+    if (a.n_units <= 0) return cudaSuccess;
+    static int n_sm = 0;
+    if (!n_sm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    constexpr int UPB = 4;
+    cudaError_t e = launch_kernel(k_big_setup<NR, NL, QM, UPB>, dim3((unsigned)((a.n_units + UPB - 1) / UPB)),
+                                  dim3(32 * UPB), UPB * SetupSmem<NR, NL>::per_unit, s, a.overlap, a);
+    if (e != cudaSuccess) return e;
+    const unsigned grid = (unsigned)(a.n_units < n_sm ? a.n_units : n_sm);
+    return launch_kernel(k_big_tc2<NR, NL, QM, LT>, dim3(grid), dim3(kTc2Simt + 32), TcSmem<NR, NL>::total, s,
+                         a.overlap, a);
+}
+
+template <int NR, int NL, int QM, int LT>
+cudaError_t prepare_tc2() {
+    cudaError_t e = cudaFuncSetAttribute(k_big_setup<NR, NL, QM, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(4 * SetupSmem<NR, NL>::per_unit));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_big_tc2<NR, NL, QM, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)TcSmem<NR, NL>::total);
+}
+
 template <int NR, int NL, int QM, int LT>
 cudaError_t launch_tc(const DetectArgs& a, cudaStream_t s) {
     if (a.n_units <= 0) return cudaSuccess;
@@ -668,8 +950,15 @@ cudaError_t prepare() {
             workspace<NR, NL>                                                                             \
     }
 
+#define BIGTC2_ENTRY(NAME, NR, NL, QM, LT)                                                                \
+    KernelEntry {                                                                                         \
+        NAME, NR, NL, QM, kSc, 14, LT, 32, 2, launch_tc2<NR, NL, QM, LT>, prepare_tc2<NR, NL, QM, LT>,   \
+            workspace<NR, NL>                                                                             \
+    }
+
 const KernelEntry kEntries[] = {
-    BIGTC_ENTRY("bigtc_64x16_q6_i8", 64, 16, 6, kLlrI8),  // C5 (tensor cores), selectable by name for now
+    BIGTC2_ENTRY("bigtc2_64x16_q6_i8", 64, 16, 6, kLlrI8),  // C5 (tensor cores, warp-specialised)
+    BIGTC_ENTRY("bigtc_64x16_q6_i8", 64, 16, 6, kLlrI8),
     BIG_ENTRY("big_64x16_q6_i8", 64, 16, 6, kLlrI8),  // C5
     BIG_ENTRY("big_64x16_q6_f16", 64, 16, 6, kLlrF16),
     BIG_ENTRY("big_64x16_q6_f32", 64, 16, 6, kLlrF32),
