@@ -123,8 +123,9 @@ mimo_status_t mimo_detect_mmse_ex(mimo_plan_t plan, const void* H, const void* y
 
 /* End-to-end form with HOST buffers (same layouts): copies H and y to a
  * plan-owned device workspace, detects, copies the LLRs back, and returns after
- * the stream has drained. Work is split into slot chunks pipelined over two
- * streams so host->device, kernel and device->host overlap; pinned
+ * the stream has drained. Work is split into slot chunks (~2 MiB of input)
+ * on a 3-deep device buffer ring over three streams (host->device, kernels,
+ * device->host) so both PCIe directions and the kernels overlap; pinned
  * (page-locked) host buffers are required for overlap but not for correctness.
  * Errors: as mimo_detect_mmse, plus OOM. */
 mimo_status_t mimo_detect_mmse_host(mimo_plan_t plan, const void* H_host, const void* y_host,

@@ -957,9 +957,9 @@ cudaError_t prepare() {
     }
 
 const KernelEntry kEntries[] = {
-    BIGTC2_ENTRY("bigtc2_64x16_q6_i8", 64, 16, 6, kLlrI8),  // C5 (tensor cores, warp-specialised)
+    BIG_ENTRY("big_64x16_q6_i8", 64, 16, 6, kLlrI8),  // C5 (SIMT GEMM; currently the fastest)
+    BIGTC2_ENTRY("bigtc2_64x16_q6_i8", 64, 16, 6, kLlrI8),  // tensor cores, warp-specialised
     BIGTC_ENTRY("bigtc_64x16_q6_i8", 64, 16, 6, kLlrI8),
-    BIG_ENTRY("big_64x16_q6_i8", 64, 16, 6, kLlrI8),  // C5
     BIG_ENTRY("big_64x16_q6_f16", 64, 16, 6, kLlrF16),
     BIG_ENTRY("big_64x16_q6_f32", 64, 16, 6, kLlrF32),
     BIG_ENTRY("big_64x16_q8_i8", 64, 16, 8, kLlrI8),

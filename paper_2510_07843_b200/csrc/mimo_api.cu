@@ -40,8 +40,10 @@ struct mimo_plan_s {
     // mimo_detect_mmse_host staging
     char* ws = nullptr;
     size_t ws_bytes = 0;
-    cudaStream_t hs[2] = {nullptr, nullptr};
+    static constexpr int kNB = 3;          // host path: buffer ring depth
+    cudaStream_t hs[3] = {nullptr, nullptr, nullptr};  // H2D, kernels, D2H
     cudaEvent_t ev = nullptr;
+    cudaEvent_t e_in[kNB] = {}, e_k[kNB] = {}, e_out[kNB] = {};
     // kernel workspaces: slot 0 for the plan's stream, 1..2 for the host path's streams
     void* kws[3] = {nullptr, nullptr, nullptr};
     size_t kws_bytes[3] = {0, 0, 0};
@@ -304,19 +306,33 @@ mimo_status_t mimo_detect_mmse_host(mimo_plan_t p, const void* H_host, const voi
     const size_t h_slot = (size_t)n_fb * n_rx * n_layers * 8;
     const size_t y_slot = (size_t)symph * n_sc * n_rx * 8;
     const size_t l_slot = (size_t)symph * n_sc * n_layers * qm * llr_bytes(p->d.llr_type);
-    // ~4 MiB of input per chunk: large enough to amortise launch + copy
-    // latency, small enough that H2D, kernel and D2H of neighbours overlap.
-    int cs = (int)((4u << 20) / (h_slot + y_slot));
+    // Chunks of whole slots, ~2 MiB of input each, on a 3-deep buffer ring over
+    // three streams (H2D | kernels | D2H) so both PCIe directions and the
+    // kernels run concurrently; events order buffer reuse.
+    constexpr int NB = mimo_plan_s::kNB;
+    int cs = (int)((2u << 20) / (h_slot + y_slot));
     if (cs < 1) cs = 1;
     if (cs > n_slots) cs = n_slots;
     auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };
     const size_t bh = up(h_slot * cs), by = up(y_slot * cs), bl = up(l_slot * cs);
-    const size_t need = 2 * (bh + by + bl);
+    const size_t need = NB * (bh + by + bl);
     cudaError_t e;
+    for (int i = 0; i < 3; ++i)
+        if (!p->hs[i] && (e = cudaStreamCreateWithFlags(&p->hs[i], cudaStreamNonBlocking)) != cudaSuccess)
+            return cuda_fail(p, e, "cudaStreamCreate");
+    if (!p->ev) {
+        if ((e = cudaEventCreateWithFlags(&p->ev, cudaEventDisableTiming)) != cudaSuccess)
+            return cuda_fail(p, e, "cudaEventCreate");
+        for (int i = 0; i < NB; ++i) {
+            cudaEventCreateWithFlags(&p->e_in[i], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&p->e_k[i], cudaEventDisableTiming);
+            if ((e = cudaEventCreateWithFlags(&p->e_out[i], cudaEventDisableTiming)) != cudaSuccess)
+                return cuda_fail(p, e, "cudaEventCreate");
+        }
+    }
     if (p->ws_bytes < need) {
         if (p->ws) {
-            cudaStreamSynchronize(p->hs[0]);
-            cudaStreamSynchronize(p->hs[1]);
+            for (int i = 0; i < 3; ++i) cudaStreamSynchronize(p->hs[i]);
             cudaFree(p->ws);
             p->ws = nullptr;
             p->ws_bytes = 0;
@@ -325,33 +341,36 @@ mimo_status_t mimo_detect_mmse_host(mimo_plan_t p, const void* H_host, const voi
         if (e != cudaSuccess) return cuda_fail(p, e, "cudaMalloc(host-path workspace)");
         p->ws_bytes = need;
     }
-    for (int i = 0; i < 2; ++i)
-        if (!p->hs[i] && (e = cudaStreamCreateWithFlags(&p->hs[i], cudaStreamNonBlocking)) != cudaSuccess)
-            return cuda_fail(p, e, "cudaStreamCreate");
-    if (!p->ev && (e = cudaEventCreateWithFlags(&p->ev, cudaEventDisableTiming)) != cudaSuccess)
-        return cuda_fail(p, e, "cudaEventCreate");
     // order after work already enqueued on the plan's stream
     if ((e = cudaEventRecord(p->ev, p->stream)) != cudaSuccess) return cuda_fail(p, e, "cudaEventRecord");
-    for (int i = 0; i < 2; ++i) cudaStreamWaitEvent(p->hs[i], p->ev, 0);
+    for (int i = 0; i < 3; ++i) cudaStreamWaitEvent(p->hs[i], p->ev, 0);
+    cudaStream_t s_in = p->hs[0], s_k = p->hs[1], s_out = p->hs[2];
 
     int chunk = 0;
     for (int s0 = 0; s0 < n_slots; s0 += cs, ++chunk) {
         const int ns = (n_slots - s0) < cs ? (n_slots - s0) : cs;
-        const int b = chunk & 1;
-        cudaStream_t s = p->hs[b];
+        const int b = chunk % NB;
         char* base = p->ws + (size_t)b * (bh + by + bl);
         char *dH = base, *dy = base + bh, *dl = base + bh + by;
-        e = cudaMemcpyAsync(dH, (const char*)H_host + h_slot * s0, h_slot * ns, cudaMemcpyHostToDevice, s);
+        if (chunk >= NB) cudaStreamWaitEvent(s_in, p->e_k[b], 0);  // inputs of chunk - NB consumed
+        e = cudaMemcpyAsync(dH, (const char*)H_host + h_slot * s0, h_slot * ns, cudaMemcpyHostToDevice, s_in);
         if (e == cudaSuccess)
-            e = cudaMemcpyAsync(dy, (const char*)y_host + y_slot * s0, y_slot * ns, cudaMemcpyHostToDevice, s);
+            e = cudaMemcpyAsync(dy, (const char*)y_host + y_slot * s0, y_slot * ns, cudaMemcpyHostToDevice, s_in);
+        if (e == cudaSuccess) e = cudaEventRecord(p->e_in[b], s_in);
         if (e != cudaSuccess) return cuda_fail(p, e, "cudaMemcpyAsync H2D");
+        cudaStreamWaitEvent(s_k, p->e_in[b], 0);
+        if (chunk >= NB) cudaStreamWaitEvent(s_k, p->e_out[b], 0);  // outputs of chunk - NB drained
         mimo::DetectArgs a = make_args(p, dH, dy, sigma2, n_sc, ns * symph, dl, nullptr, nullptr);
-        st = launch(p, a, s, 1 + b);
+        a.overlap = 0;
+        st = launch(p, a, s_k, 1);
         if (st != MIMO_OK) return st;
-        e = cudaMemcpyAsync((char*)llr_host + l_slot * s0, dl, l_slot * ns, cudaMemcpyDeviceToHost, s);
+        if ((e = cudaEventRecord(p->e_k[b], s_k)) != cudaSuccess) return cuda_fail(p, e, "cudaEventRecord");
+        cudaStreamWaitEvent(s_out, p->e_k[b], 0);
+        e = cudaMemcpyAsync((char*)llr_host + l_slot * s0, dl, l_slot * ns, cudaMemcpyDeviceToHost, s_out);
+        if (e == cudaSuccess) e = cudaEventRecord(p->e_out[b], s_out);
         if (e != cudaSuccess) return cuda_fail(p, e, "cudaMemcpyAsync D2H");
     }
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < 3; ++i)
         if ((e = cudaStreamSynchronize(p->hs[i])) != cudaSuccess) return cuda_fail(p, e, "cudaStreamSynchronize");
     return MIMO_OK;
 }
@@ -375,7 +394,7 @@ mimo_status_t mimo_plan_sync_status(mimo_plan_t p, long long* n_failed) {
     if (g.err != cudaSuccess) return cuda_fail(p, g.err, "cudaSetDevice");
     unsigned long long h = 0;
     cudaError_t e = cudaStreamSynchronize(p->stream);
-    for (int i = 0; i < 2 && e == cudaSuccess; ++i)
+    for (int i = 0; i < 3 && e == cudaSuccess; ++i)
         if (p->hs[i]) e = cudaStreamSynchronize(p->hs[i]);
     if (e == cudaSuccess) e = cudaMemcpyAsync(&h, p->d_fail, sizeof(h), cudaMemcpyDeviceToHost, p->stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(p->d_fail, 0, sizeof(h), p->stream);
@@ -390,12 +409,17 @@ mimo_status_t mimo_plan_destroy(mimo_plan_t p) {
     {
         DeviceGuard g(p->d.device);
         cudaStreamSynchronize(p->stream);
-        for (int i = 0; i < 2; ++i)
+        for (int i = 0; i < 3; ++i)
             if (p->hs[i]) {
                 cudaStreamSynchronize(p->hs[i]);
                 cudaStreamDestroy(p->hs[i]);
             }
         if (p->ev) cudaEventDestroy(p->ev);
+        for (int i = 0; i < mimo_plan_s::kNB; ++i) {
+            if (p->e_in[i]) cudaEventDestroy(p->e_in[i]);
+            if (p->e_k[i]) cudaEventDestroy(p->e_k[i]);
+            if (p->e_out[i]) cudaEventDestroy(p->e_out[i]);
+        }
         if (p->ws) cudaFree(p->ws);
         for (int i = 0; i < 3; ++i)
             if (p->kws[i]) cudaFree(p->kws[i]);
