@@ -310,7 +310,9 @@ mimo_status_t mimo_detect_mmse_host(mimo_plan_t p, const void* H_host, const voi
     // three streams (H2D | kernels | D2H) so both PCIe directions and the
     // kernels run concurrently; events order buffer reuse.
     constexpr int NB = mimo_plan_s::kNB;
-    int cs = (int)((2u << 20) / (h_slot + y_slot));
+    size_t chunk_bytes = 2u << 20;
+    if (const char* cb = getenv("MIMO_HOST_CHUNK_BYTES")) chunk_bytes = (size_t)atoll(cb);  // tuning knob
+    int cs = (int)(chunk_bytes / (h_slot + y_slot));
     if (cs < 1) cs = 1;
     if (cs > n_slots) cs = n_slots;
     auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };
