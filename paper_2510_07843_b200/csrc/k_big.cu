@@ -16,6 +16,9 @@
 //     (RE pair, layer half) accumulates its 2 x 8 complex outputs over r with
 //     128-bit shared loads (register-tiled SIMT GEMM, 12.8 FFMA per load),
 //     then demaps its 16 layer-REs and stores 48 contiguous LLR bytes per RE.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "kernels.h"
 
 namespace mimo {
@@ -696,8 +699,26 @@ __device__ __forceinline__ void tc2_build_b(float* fB, float* fBlo, const float4
     }
 }
 
+// y tile of unit u, K-tile kt via TMA (3-D map over y viewed as [n_sym][n_sc][2*NR floats],
+// box {32 floats, 12 subcarriers, 14 symbols}, SWIZZLE_128B = the UMMA SW128 K-major layout)
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+template <int NR, int NL>
+__device__ __forceinline__ void tc2_issue_y_tma(const DetectArgs& a, const CUtensorMap* map, uint32_t stage,
+                                                long long u, uint64_t* bar) {
+    using SM = TcSmem<NR, NL>;
+    const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);
+    mbar_arrive_expect_tx(bar, (uint32_t)SM::ystage);
+#pragma unroll
+    for (int kt = 0; kt < SM::KT; ++kt) tma_load_3d(stage + kt * (uint32_t)SM::ktile, map, 32 * kt, fb * kSc, slot * kSym, bar);
+}
+
 template <int NR, int NL, int QM, int LT>
-__global__ void __launch_bounds__(kTc2Simt + 32, 1) k_big_tc2(DetectArgs a) {
+__global__ void __launch_bounds__(kTc2Simt + 32, 1) k_big_tc2(DetectArgs a, const __grid_constant__ CUtensorMap ymap) {
     static_assert(NL == 16 && NR == 64, "k_big_tc2: 64 x 16");
     using SM = TcSmem<NR, NL>;
     constexpr int KT = SM::KT;
@@ -721,9 +742,7 @@ __global__ void __launch_bounds__(kTc2Simt + 32, 1) k_big_tc2(DetectArgs a) {
 
     pdl_launch_dependents();
     if (t == 0) {
-        mbar_init(&yfull[0], kTc2Simt);
-        mbar_init(&yfull[1], kTc2Simt);
-        for (int i = 2; i < 8; ++i) mbar_init(&bars[i], 1);
+        for (int i = 0; i < 8; ++i) mbar_init(&bars[i], 1);
         fence_mbar_init();
     }
     if (warp == 0) {
@@ -789,8 +808,10 @@ __global__ void __launch_bounds__(kTc2Simt + 32, 1) k_big_tc2(DetectArgs a) {
         // ===== SIMT warps =====
         const float norm = (float)qam_norm(QM);
         const bool zf = !(a.sigma2 > 0.f);
-        if (n_my > 0) tc_issue_y<NR, NL>(a, base + SM::y0, u0, &yfull[0]);
-        if (n_my > 1) tc_issue_y<NR, NL>(a, base + SM::y0 + (uint32_t)SM::ystage, u0 + du, &yfull[1]);
+        if (t == 0) {
+            if (n_my > 0) tc2_issue_y_tma<NR, NL>(a, &ymap, base + SM::y0, u0, &yfull[0]);
+            if (n_my > 1) tc2_issue_y_tma<NR, NL>(a, &ymap, base + SM::y0 + (uint32_t)SM::ystage, u0 + du, &yfull[1]);
+        }
         pdl_wait();  // W~ of this call's setup kernel is complete
         float4 wv[4];
         if (n_my > 0) {
@@ -814,7 +835,11 @@ __global__ void __launch_bounds__(kTc2Simt + 32, 1) k_big_tc2(DetectArgs a) {
             if (i >= 1) {
                 // unit i-1: pass 3 done -> its y stage is free (refill with unit i+1) and its accumulator is ready
                 mbar_wait_bounded(c2, (uint32_t)((i - 1) & 1));
-                if (i + 1 < n_my) tc_issue_y<NR, NL>(a, base + SM::y0 + (st ^ 1) * (uint32_t)SM::ystage, u + du, &yfull[st ^ 1]);
+                if (t == 0 && i + 1 < n_my) {
+                    fence_proxy_async();  // y_lo writes of unit i-1 (generic) before the TMA overwrite
+                    tc2_issue_y_tma<NR, NL>(a, &ymap, base + SM::y0 + (st ^ 1) * (uint32_t)SM::ystage, u + du,
+                                            &yfull[st ^ 1]);
+                }
                 tc_fence_after();
                 tc2_epilogue<NR, NL, QM, LT>(a, tmem + 64u * (uint32_t)(st ^ 1), u - du, slope_prev, zf, norm);
                 tc_fence_before();
@@ -862,6 +887,19 @@ __global__ void __launch_bounds__(kTc2Simt + 32, 1) k_big_tc2(DetectArgs a) {
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
 }
 
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link)
+inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
 template <int NR, int NL, int QM, int LT>
 cudaError_t launch_tc2(const DetectArgs& a, cudaStream_t s) {
     if (a.n_units <= 0) return cudaSuccess;
@@ -871,13 +909,33 @@ cudaError_t launch_tc2(const DetectArgs& a, cudaStream_t s) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
     }
+    auto enc = tensor_map_encoder();
+    if (!enc) return cudaErrorNotSupported;
+    CUtensorMap ymap;
+    const cuuint64_t gdim[3] = {(cuuint64_t)(2 * NR), (cuuint64_t)a.n_sc, (cuuint64_t)a.n_sym};
+    const cuuint64_t gstride[2] = {(cuuint64_t)NR * 8, (cuuint64_t)a.n_sc * NR * 8};
+    const cuuint32_t box[3] = {32, (cuuint32_t)kSc, (cuuint32_t)kSym};
+    const cuuint32_t estride[3] = {1, 1, 1};
+    if (enc(&ymap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float2*>(a.y), gdim, gstride, box, estride,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
     constexpr int UPB = 4;
     cudaError_t e = launch_kernel(k_big_setup<NR, NL, QM, UPB>, dim3((unsigned)((a.n_units + UPB - 1) / UPB)),
                                   dim3(32 * UPB), UPB * SetupSmem<NR, NL>::per_unit, s, a.overlap, a);
     if (e != cudaSuccess) return e;
     const unsigned grid = (unsigned)(a.n_units < n_sm ? a.n_units : n_sm);
-    return launch_kernel(k_big_tc2<NR, NL, QM, LT>, dim3(grid), dim3(kTc2Simt + 32), TcSmem<NR, NL>::total, s,
-                         a.overlap, a);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kTc2Simt + 32);
+    cfg.dynamicSmemBytes = TcSmem<NR, NL>::total;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = a.overlap ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k_big_tc2<NR, NL, QM, LT>, a, ymap);
 }
 
 template <int NR, int NL, int QM, int LT>
