@@ -974,6 +974,319 @@ cudaError_t prepare_tc() {
                                 (int)TcSmem<NR, NL>::total);
 }
 
+// ------------------------------------------------------------------------
+// k_big_tc3: half-unit software pipeline on the tensor cores.
+// Work item = half a PRB-unit (7 symbols x 12 subcarriers = 84 RE rows), so a
+// y stage is 48 KiB (4 K-tiles x 96 rows x 128 B, TMA box {32, 12, 7}) and three
+// stages plus two B sets fit: B set = [B_hi; B_lo] stacked along N (64 rows),
+// so passes 1+2 are ONE N=64 MMA chain (the tcgen05 issue cost, ~50 cycles per
+// tf32 MMA, does not grow from N=32 to N=64) and pass 3 uses the B_hi rows.
+// The MMA thread keeps two halves in flight: p12(h) then p3(h-1), so the tensor
+// pipe works while the SIMT warps convert y(h) -> y_lo(h) and run epilogues.
+struct Tc3 {
+    static constexpr int ROWS = 96;                                     // 84 valid + pad
+    static constexpr int KT = 4;
+    static constexpr size_t ktile = (size_t)ROWS * 128;                 // 12 KiB
+    static constexpr size_t ystage = KT * ktile;                        // 48 KiB
+    static constexpr size_t bktile = (size_t)64 * 128;                  // 8 KiB: 32 rows B_hi + 32 rows B_lo
+    static constexpr size_t bset = KT * bktile;                         // 32 KiB
+    static constexpr size_t y0 = 0;
+    static constexpr size_t B0 = 3 * ystage;
+    static constexpr size_t bars = B0 + 2 * bset;                       // 13 mbarriers
+    static constexpr size_t tmem = bars + 13 * 8;
+    static constexpr size_t total = tmem + 16 + 1024;
+};
+
+template <int NR, int NL>
+__device__ __forceinline__ void tc3_issue_y(const DetectArgs& a, const CUtensorMap* map, uint32_t stage, long long h,
+                                            uint64_t* bar) {
+    const long long u = h >> 1;
+    const int q = (int)(h & 1);
+    const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);
+    mbar_arrive_expect_tx(bar, (uint32_t)(Tc3::KT * 84 * 128));
+#pragma unroll
+    for (int kt = 0; kt < Tc3::KT; ++kt)
+        tma_load_3d(stage + kt * (uint32_t)Tc3::ktile, map, 32 * kt, fb * kSc, slot * kSym + 7 * q, bar);
+}
+// B set rows: n in [0,32): B_hi (fp32, read as TF32), n + 32: B_lo = B - trunc(B)
+template <int NR, int NL>
+__device__ __forceinline__ void tc3_build_b(float* fset, const float4 (&wv)[4]) {
+    const int t = threadIdx.x;
+    const int n = t >> 3, kt = (t >> 1) & 3, c0 = (t & 1) * 4;
+    const bool im_row = n >= 16;
+#pragma unroll
+    for (int cq = 0; cq < 4; ++cq) {
+        const int c = c0 + cq;
+        const float4 w = wv[cq];
+        float4 v;
+        if (!im_row) v = make_float4(w.x, -w.y, w.z, -w.w);
+        else v = make_float4(w.y, w.x, w.w, w.z);
+        const float4 lo = make_float4(v.x - tf32_trunc(v.x), v.y - tf32_trunc(v.y), v.z - tf32_trunc(v.z),
+                                      v.w - tf32_trunc(v.w));
+        float* kb = fset + kt * (int)(Tc3::bktile / 4);
+        *reinterpret_cast<float4*>(kb + n * 32 + ((c ^ (n & 7)) << 2)) = v;
+        *reinterpret_cast<float4*>(kb + (n + 32) * 32 + ((c ^ (n & 7)) << 2)) = lo;  // (n+32)&7 == n&7
+    }
+}
+
+template <int NR, int NL, int QM, int LT>
+__device__ __forceinline__ void tc3_epilogue(const DetectArgs& a, uint32_t tmem_buf, long long h, const float* slope,
+                                             bool zf, float norm) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wq = warp & 3, lh = warp >> 2;
+    if (wq >= 3) return;
+    const long long u = h >> 1;
+    const int q = (int)(h & 1);
+    const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);
+    constexpr int KH = NL / 2;
+    constexpr int kRecBytes = NL * QM * LlrTraits<LT>::bytes;
+    constexpr int kHalfBytes = KH * QM * LlrTraits<LT>::bytes;
+    const uint32_t taddr = tmem_buf + ((uint32_t)(32 * wq) << 16) + KH * lh;
+    uint32_t xr[KH], xi[KH], xr2[KH], xi2[KH];
+    tmem_ld8(taddr, xr);
+    tmem_ld8(taddr + 16u, xi);
+    tmem_ld8(taddr + 32u, xr2);
+    tmem_ld8(taddr + 48u, xi2);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    const int row = 32 * wq + lane;
+    if (row >= 84) return;
+    const int s = 7 * q + row / kSc, f = row % kSc;
+    const size_t re = (size_t)(slot * kSym + s) * a.n_sc + fb * kSc + f;
+    float2 x[KH];
+#pragma unroll
+    for (int k = 0; k < KH; ++k)
+        x[k] = make_float2(__uint_as_float(xr[k]) + __uint_as_float(xr2[k]), __uint_as_float(xi[k]) + __uint_as_float(xi2[k]));
+    if (a.llr) {
+        float v[KH * QM];
+#pragma unroll
+        for (int k = 0; k < KH; ++k) {
+            if (!zf) demap_layer<QM, false, LT>(x[k], slope[k], v + k * QM);
+            else demap_layer<QM, true, LT>(x[k], slope[k], v + k * QM);
+        }
+        uint32_t wd[(kHalfBytes + 3) / 4];
+        if (!zf) pack_llr<LT, KH * QM, false>(v, wd);
+        else pack_llr<LT, KH * QM, true>(v, wd);
+        store_bytes<kHalfBytes>((char*)a.llr + re * kRecBytes + lh * kHalfBytes, wd);
+    }
+    if (a.xhat) {
+        const float ia = rsqrtf(norm);
+#pragma unroll
+        for (int k = 0; k < KH; ++k) a.xhat[re * NL + KH * lh + k] = make_float2(x[k].x * ia, x[k].y * ia);
+    }
+}
+
+template <int NR, int NL, int QM, int LT>
+__global__ void __launch_bounds__(kTc2Simt + 32, 1) k_big_tc3(DetectArgs a, const __grid_constant__ CUtensorMap ymap) {
+    static_assert(NL == 16 && NR == 64, "k_big_tc3: 64 x 16");
+    constexpr int WS = BigWs<NR, NL>::stride;
+    extern __shared__ unsigned char smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    unsigned char* gbase = smem_raw + (base - raw);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + Tc3::bars);
+    uint64_t* yfull = bars;        // [3]
+    uint64_t* bready = bars + 3;   // [2]
+    uint64_t* c1 = bars + 5;       // [2]
+    uint64_t* ylo = bars + 7;      // [2]
+    uint64_t* c2 = bars + 9;       // [2]
+    uint64_t* tfree = bars + 11;   // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + Tc3::tmem);
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+
+    pdl_launch_dependents();
+    if (t == 0) {
+        for (int i = 0; i < 13; ++i) mbar_init(&bars[i], 1);
+        fence_mbar_init();
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const long long u0 = blockIdx.x, du = gridDim.x;
+    const long long n_units_my = u0 < a.n_units ? (a.n_units - u0 + du - 1) / du : 0;
+    const long long n_half = 2 * n_units_my;
+    auto unit_of = [&](long long h) { return u0 + (h >> 1) * du; };  // global unit of my half h
+    auto ystage = [&](long long h) { return base + (uint32_t)Tc3::y0 + (uint32_t)(h % 3) * (uint32_t)Tc3::ystage; };
+    auto bset = [&](long long h) { return base + (uint32_t)Tc3::B0 + (uint32_t)((h >> 1) & 1) * (uint32_t)Tc3::bset; };
+
+    if (warp == kTc2Simt / 32) {
+        // ===== MMA issuer: p12(h) [N=64, A=y, B=[B_hi;B_lo]] then p3(h-1) [N=32, A=y_lo, B_hi] =====
+        if (lane == 0) {
+            constexpr uint32_t id64 = (1u << 4) | (2u << 7) | (2u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+            constexpr uint32_t id32 = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+            auto p3 = [&](long long hp) {
+                const int b = (int)(hp & 1);
+                mbar_wait_bounded(&ylo[b], (uint32_t)((hp >> 1) & 1));
+                fence_proxy_async();
+                tc_fence_after();
+                const uint32_t ys = ystage(hp), bs = bset(hp), acc = tmem + 64u * (uint32_t)b;
+#pragma unroll
+                for (int kt = 0; kt < Tc3::KT; ++kt)
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks)
+                        umma_tf32(acc, umma_desc_sw128(ys + kt * (uint32_t)Tc3::ktile + ks * 32u),
+                                  umma_desc_sw128(bs + kt * (uint32_t)Tc3::bktile + ks * 32u), id32, 1u);
+                umma_commit(&c2[b]);
+            };
+#pragma unroll 1
+            for (long long h = 0; h < n_half; ++h) {
+                const int b = (int)(h & 1);
+                if (h >= 2) mbar_wait_bounded(&tfree[b], (uint32_t)(((h >> 1) + 1) & 1));
+                mbar_wait_bounded(&yfull[h % 3], (uint32_t)((h / 3) & 1));
+                mbar_wait_bounded(&bready[(h >> 1) & 1], (uint32_t)((h >> 2) & 1));
+                fence_proxy_async();
+                tc_fence_after();
+                const uint32_t ys = ystage(h), bs = bset(h), acc = tmem + 64u * (uint32_t)b;
+#pragma unroll
+                for (int kt = 0; kt < Tc3::KT; ++kt)
+#pragma unroll
+                    for (int ks = 0; ks < 4; ++ks)
+                        umma_tf32(acc, umma_desc_sw128(ys + kt * (uint32_t)Tc3::ktile + ks * 32u),
+                                  umma_desc_sw128(bs + kt * (uint32_t)Tc3::bktile + ks * 32u), id64,
+                                  (kt | ks) ? 1u : 0u);
+                umma_commit(&c1[b]);
+                if (h >= 1) p3(h - 1);
+            }
+            if (n_half > 0) p3(n_half - 1);
+        }
+    } else {
+        // ===== SIMT warps =====
+        const float norm = (float)qam_norm(QM);
+        const bool zf = !(a.sigma2 > 0.f);
+        if (t == 0)
+            for (long long h = 0; h < 3 && h < n_half; ++h) tc3_issue_y<NR, NL>(a, &ymap, ystage(h), h, &yfull[h % 3]);
+        pdl_wait();  // W~ of this call's setup kernel is complete
+        float4 wv[4];
+        for (long long v = 0; v < 2 && v < n_units_my; ++v) {
+            tc2_fetch_w<NR, NL>(a, u0 + v * du, wv);
+            tc3_build_b<NR, NL>(reinterpret_cast<float*>(gbase + Tc3::B0 + v * Tc3::bset), wv);
+        }
+        fence_proxy_async();
+        simt_bar();
+        if (t == 0) {
+            mbar_arrive(&bready[0]);
+            if (n_units_my > 1) mbar_arrive(&bready[1]);
+        }
+        float slope[NL / 2];
+#pragma unroll 1
+        for (long long h = 0; h < n_half; ++h) {
+            const int b = (int)(h & 1);
+            // passes 1+2 of half h done -> y(h) -> y_lo(h) in place
+            mbar_wait_bounded(&c1[b], (uint32_t)((h >> 1) & 1));
+            {
+                float4* y4 = reinterpret_cast<float4*>(gbase + (ystage(h) - base));
+                constexpr int n4 = (int)(Tc3::ystage / 16);
+#pragma unroll 4
+                for (int i = t; i < n4; i += kTc2Simt) {
+                    float4 v = y4[i];
+                    v.x -= tf32_trunc(v.x);
+                    v.y -= tf32_trunc(v.y);
+                    v.z -= tf32_trunc(v.z);
+                    v.w -= tf32_trunc(v.w);
+                    y4[i] = v;
+                }
+            }
+            fence_proxy_async();
+            simt_bar();
+            if (t == 0) mbar_arrive(&ylo[b]);
+            if (h >= 1) {
+                const long long hp = h - 1;
+                const int bp = (int)(hp & 1);
+                mbar_wait_bounded(&c2[bp], (uint32_t)((hp >> 1) & 1));
+                // stage of hp is free: refill with half hp + 3
+                if (t == 0 && hp + 3 < n_half) {
+                    fence_proxy_async();
+                    tc3_issue_y<NR, NL>(a, &ymap, ystage(hp + 3), hp + 3, &yfull[(hp + 3) % 3]);
+                }
+                {
+                    const float* wsu = reinterpret_cast<const float*>(a.ws) + unit_of(hp) * WS + NR * NL * 2 +
+                                       (warp >> 2) * (NL / 2);
+#pragma unroll
+                    for (int k = 0; k < NL / 2; ++k) slope[k] = wsu[k];
+                }
+                tc_fence_after();
+                tc3_epilogue<NR, NL, QM, LT>(a, tmem + 64u * (uint32_t)bp, hp, slope, zf, norm);
+                tc_fence_before();
+                const bool unit_done = (hp & 1) == 1;
+                const long long vn = (hp >> 1) + 2;  // unit that reuses this B set
+                if (unit_done && vn < n_units_my) tc2_fetch_w<NR, NL>(a, u0 + vn * du, wv);
+                simt_bar();
+                if (t == 0) mbar_arrive(&tfree[bp]);
+                if (unit_done && vn < n_units_my) {
+                    tc3_build_b<NR, NL>(reinterpret_cast<float*>(gbase + (bset(hp) - base)), wv);
+                    fence_proxy_async();
+                    simt_bar();
+                    if (t == 0) mbar_arrive(&bready[(hp >> 1) & 1]);
+                }
+            }
+        }
+        if (n_half > 0) {
+            const long long hp = n_half - 1;
+            const int bp = (int)(hp & 1);
+            mbar_wait_bounded(&c2[bp], (uint32_t)((hp >> 1) & 1));
+            const float* wsu = reinterpret_cast<const float*>(a.ws) + unit_of(hp) * WS + NR * NL * 2 + (warp >> 2) * (NL / 2);
+#pragma unroll
+            for (int k = 0; k < NL / 2; ++k) slope[k] = wsu[k];
+            tc_fence_after();
+            tc3_epilogue<NR, NL, QM, LT>(a, tmem + 64u * (uint32_t)bp, hp, slope, zf, norm);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+}
+
+template <int NR, int NL, int QM, int LT>
+cudaError_t launch_tc3(const DetectArgs& a, cudaStream_t s) {
+    if (a.n_units <= 0) return cudaSuccess;
+    static int n_sm = 0;
+    if (!n_sm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    auto enc = tensor_map_encoder();
+    if (!enc) return cudaErrorNotSupported;
+    CUtensorMap ymap;
+    const cuuint64_t gdim[3] = {(cuuint64_t)(2 * NR), (cuuint64_t)a.n_sc, (cuuint64_t)a.n_sym};
+    const cuuint64_t gstride[2] = {(cuuint64_t)NR * 8, (cuuint64_t)a.n_sc * NR * 8};
+    const cuuint32_t box[3] = {32, (cuuint32_t)kSc, 7};
+    const cuuint32_t estride[3] = {1, 1, 1};
+    if (enc(&ymap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float2*>(a.y), gdim, gstride, box, estride,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    constexpr int UPB = 4;
+    cudaError_t e = launch_kernel(k_big_setup<NR, NL, QM, UPB>, dim3((unsigned)((a.n_units + UPB - 1) / UPB)),
+                                  dim3(32 * UPB), UPB * SetupSmem<NR, NL>::per_unit, s, a.overlap, a);
+    if (e != cudaSuccess) return e;
+    const unsigned grid = (unsigned)(a.n_units < n_sm ? a.n_units : n_sm);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kTc2Simt + 32);
+    cfg.dynamicSmemBytes = Tc3::total;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = a.overlap ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k_big_tc3<NR, NL, QM, LT>, a, ymap);
+}
+
+template <int NR, int NL, int QM, int LT>
+cudaError_t prepare_tc3() {
+    cudaError_t e = cudaFuncSetAttribute(k_big_setup<NR, NL, QM, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(4 * SetupSmem<NR, NL>::per_unit));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_big_tc3<NR, NL, QM, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)Tc3::total);
+}
+
 template <int NR, int NL>
 size_t workspace(const DetectArgs& a) {
     return (size_t)a.n_units * BigWs<NR, NL>::stride * 4;
@@ -1014,8 +1327,15 @@ cudaError_t prepare() {
             workspace<NR, NL>                                                                             \
     }
 
+#define BIGTC3_ENTRY(NAME, NR, NL, QM, LT)                                                                \
+    KernelEntry {                                                                                         \
+        NAME, NR, NL, QM, kSc, 14, LT, 32, 2, launch_tc3<NR, NL, QM, LT>, prepare_tc3<NR, NL, QM, LT>,   \
+            workspace<NR, NL>                                                                             \
+    }
+
 const KernelEntry kEntries[] = {
     BIG_ENTRY("big_64x16_q6_i8", 64, 16, 6, kLlrI8),  // C5 (SIMT GEMM; currently the fastest)
+    BIGTC3_ENTRY("bigtc3_64x16_q6_i8", 64, 16, 6, kLlrI8),
     BIGTC2_ENTRY("bigtc2_64x16_q6_i8", 64, 16, 6, kLlrI8),  // tensor cores, warp-specialised
     BIGTC_ENTRY("bigtc_64x16_q6_i8", 64, 16, 6, kLlrI8),
     BIG_ENTRY("big_64x16_q6_f16", 64, 16, 6, kLlrF16),

@@ -26,12 +26,14 @@ __global__ void k(int iters, long long* out) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((N >> 3) << 17) | ((128u >> 4) << 24);
     const uint32_t a = su32(sm), b = su32(sm + 65536);
+    const uint64_t da0 = desc(a), db0 = desc(b);
     long long t0 = clock64();
     if (threadIdx.x == 0) {
         for (int it = 0; it < iters; ++it) {
 #pragma unroll
             for (int kk = 0; kk < 96; ++kk) {
-                uint64_t da = desc(a + (kk & 3) * 32 + (kk >> 2) * 1024), db = desc(b + (kk & 3) * 32);
+                // advance the 14-bit start-address field (16-byte units) of precomputed descriptors
+                const uint64_t da = da0 + (uint64_t)((kk & 3) * 2 + (kk >> 2) * 64), db = db0 + (uint64_t)((kk & 3) * 2);
                 asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
                              ::"r"(tb), "l"(da), "l"(db), "r"(idesc), "r"(kk));
             }
@@ -52,7 +54,7 @@ int main() {
     long long* d;
     cudaMalloc(&d, 8 * 148);
     long long h[148];
-    for (int n : {32, 64, 128}) {
+    for (int n : {32, 64, 128, 32}) {
         auto f = n == 32 ? k<32> : n == 64 ? k<64> : k<128>;
         cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 140 * 1024);
         f<<<148, 128, 140 * 1024>>>(10, d);
