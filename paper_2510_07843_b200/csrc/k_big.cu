@@ -998,10 +998,8 @@ struct Tc3 {
 };
 
 template <int NR, int NL>
-__device__ __forceinline__ void tc3_issue_y(const DetectArgs& a, const CUtensorMap* map, uint32_t stage, long long h,
-                                            uint64_t* bar) {
-    const long long u = h >> 1;
-    const int q = (int)(h & 1);
+__device__ __forceinline__ void tc3_issue_y(const DetectArgs& a, const CUtensorMap* map, uint32_t stage, long long u,
+                                            int q, uint64_t* bar) {
     const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);
     mbar_arrive_expect_tx(bar, (uint32_t)(Tc3::KT * 84 * 128));
 #pragma unroll
@@ -1030,13 +1028,11 @@ __device__ __forceinline__ void tc3_build_b(float* fset, const float4 (&wv)[4]) 
 }
 
 template <int NR, int NL, int QM, int LT>
-__device__ __forceinline__ void tc3_epilogue(const DetectArgs& a, uint32_t tmem_buf, long long h, const float* slope,
-                                             bool zf, float norm) {
+__device__ __forceinline__ void tc3_epilogue(const DetectArgs& a, uint32_t tmem_buf, long long u, int q,
+                                             const float* slope, bool zf, float norm) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int wq = warp & 3, lh = warp >> 2;
     if (wq >= 3) return;
-    const long long u = h >> 1;
-    const int q = (int)(h & 1);
     const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);
     constexpr int KH = NL / 2;
     constexpr int kRecBytes = NL * QM * LlrTraits<LT>::bytes;
@@ -1158,7 +1154,8 @@ __global__ void __launch_bounds__(kTc2Simt + 32, 1) k_big_tc3(DetectArgs a, cons
         const float norm = (float)qam_norm(QM);
         const bool zf = !(a.sigma2 > 0.f);
         if (t == 0)
-            for (long long h = 0; h < 3 && h < n_half; ++h) tc3_issue_y<NR, NL>(a, &ymap, ystage(h), h, &yfull[h % 3]);
+            for (long long h = 0; h < 3 && h < n_half; ++h)
+                tc3_issue_y<NR, NL>(a, &ymap, ystage(h), unit_of(h), (int)(h & 1), &yfull[h % 3]);
         pdl_wait();  // W~ of this call's setup kernel is complete
         float4 wv[4];
         for (long long v = 0; v < 2 && v < n_units_my; ++v) {
@@ -1200,7 +1197,8 @@ __global__ void __launch_bounds__(kTc2Simt + 32, 1) k_big_tc3(DetectArgs a, cons
                 // stage of hp is free: refill with half hp + 3
                 if (t == 0 && hp + 3 < n_half) {
                     fence_proxy_async();
-                    tc3_issue_y<NR, NL>(a, &ymap, ystage(hp + 3), hp + 3, &yfull[(hp + 3) % 3]);
+                    tc3_issue_y<NR, NL>(a, &ymap, ystage(hp + 3), unit_of(hp + 3), (int)((hp + 3) & 1),
+                                        &yfull[(hp + 3) % 3]);
                 }
                 {
                     const float* wsu = reinterpret_cast<const float*>(a.ws) + unit_of(hp) * WS + NR * NL * 2 +
@@ -1209,7 +1207,7 @@ __global__ void __launch_bounds__(kTc2Simt + 32, 1) k_big_tc3(DetectArgs a, cons
                     for (int k = 0; k < NL / 2; ++k) slope[k] = wsu[k];
                 }
                 tc_fence_after();
-                tc3_epilogue<NR, NL, QM, LT>(a, tmem + 64u * (uint32_t)bp, hp, slope, zf, norm);
+                tc3_epilogue<NR, NL, QM, LT>(a, tmem + 64u * (uint32_t)bp, unit_of(hp), (int)(hp & 1), slope, zf, norm);
                 tc_fence_before();
                 const bool unit_done = (hp & 1) == 1;
                 const long long vn = (hp >> 1) + 2;  // unit that reuses this B set
@@ -1232,7 +1230,7 @@ __global__ void __launch_bounds__(kTc2Simt + 32, 1) k_big_tc3(DetectArgs a, cons
 #pragma unroll
             for (int k = 0; k < NL / 2; ++k) slope[k] = wsu[k];
             tc_fence_after();
-            tc3_epilogue<NR, NL, QM, LT>(a, tmem + 64u * (uint32_t)bp, hp, slope, zf, norm);
+            tc3_epilogue<NR, NL, QM, LT>(a, tmem + 64u * (uint32_t)bp, unit_of(hp), (int)(hp & 1), slope, zf, norm);
         }
     }
     tc_fence_before();
