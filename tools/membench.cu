@@ -58,3 +58,52 @@ extern "C" int membench_rw(const void* src, void* dst, long long rd_bytes, long 
                         : cudaLaunchKernelEx(&cfg, rw_kernel<4, false>, a, b, nr, nw, (uint32_t*)sink);
     return (int)e;
 }
+
+// ---- bulk-copy (TMA, non-tensor) read throughput: each CTA streams its slice of src through
+// a ring of S smem stages of `chunk` bytes, one mbarrier per stage, `per` bulk copies per stage.
+__device__ __forceinline__ uint32_t s32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__global__ void bulk_read_kernel(const uint8_t* __restrict__ src, long long bytes, int chunk, int per, uint32_t* sink) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    __shared__ __align__(8) uint64_t bar[4];
+    const int S = 4;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < S; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s32(&bar[i])));
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    __syncthreads();
+    const long long n_chunks = bytes / chunk;
+    long long my = 0;
+    uint32_t acc = 0;
+    if (threadIdx.x == 0) {
+        const int piece = chunk / per;
+        auto issue = [&](long long c, int st) {
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s32(&bar[st])), "r"(chunk));
+            for (int p = 0; p < per; ++p)
+                asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                             ::"r"(s32(sm + st * chunk + p * piece)), "l"(src + c * chunk + p * piece), "r"(piece),
+                             "r"(s32(&bar[st])) : "memory");
+        };
+        long long c = blockIdx.x;
+        int k = 0;
+        for (int st = 0; st < S && c + (long long)st * gridDim.x < n_chunks; ++st) issue(c + (long long)st * gridDim.x, st);
+        for (; c < n_chunks; c += gridDim.x, ++k) {
+            const int st = k % S;
+            uint32_t ok = 0;
+            while (!ok)
+                asm volatile("{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0,1,0,p;\n\t}"
+                             : "=r"(ok) : "r"(s32(&bar[st])), "r"((k / S) & 1));
+            acc ^= sm[st * chunk];
+            const long long cn = c + (long long)S * gridDim.x;
+            if (cn < n_chunks) issue(cn, st);
+            ++my;
+        }
+    }
+    if (acc == 0x12345u) sink[0] = acc + (uint32_t)my;
+}
+
+extern "C" int membench_bulk(const void* src, long long bytes, int chunk, int per, void* sink, int blocks, void* stream) {
+    cudaFuncSetAttribute(bulk_read_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * chunk);
+    bulk_read_kernel<<<blocks, 32, 4 * chunk, (cudaStream_t)stream>>>((const uint8_t*)src, bytes, chunk, per,
+                                                                        (uint32_t*)sink);
+    return (int)cudaGetLastError();
+}

@@ -78,5 +78,33 @@ def main():
         del bufs
 
 
+
+
+def bulk_main():
+    L = build()
+    L.membench_bulk.argtypes = [ctypes.c_void_p, ctypes.c_longlong, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                ctypes.c_int, ctypes.c_void_p]
+    sink = torch.zeros(8, dtype=torch.int32, device="cuda")
+    nbytes = 1 << 30
+    src = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.Stream()
+    for chunk, per in [(16384, 1), (32768, 1), (49152, 1), (16384, 32), (32768, 64), (49152, 96), (49152, 384)]:
+        for bps in (1, 2):
+            blocks = 148 * bps
+            with torch.cuda.stream(s):
+                L.membench_bulk(src.data_ptr(), nbytes, chunk, per, sink.data_ptr(), blocks, s.cuda_stream)
+            s.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(s):
+                e0.record(s)
+                for _ in range(3):
+                    L.membench_bulk(src.data_ptr(), nbytes, chunk, per, sink.data_ptr(), blocks, s.cuda_stream)
+                e1.record(s)
+            s.synchronize()
+            us = e0.elapsed_time(e1) * 1e3 / 3
+            print(f"bulk read: chunk {chunk:6d} B in {per:3d} copies of {chunk // per:5d} B, {blocks} CTAs x 4 stages: "
+                  f"{nbytes / us / 1e3:7.1f} GB/s", flush=True)
+
+
 if __name__ == "__main__":
-    main()
+    bulk_main() if "bulk" in sys.argv else main()
