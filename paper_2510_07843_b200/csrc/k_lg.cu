@@ -27,7 +27,7 @@ struct LgSmem {
     static constexpr int UPW = 32 / NL;
     static constexpr int TU = UPW * NW;
     // per-unit strides padded by 16-32 B so the UPW units of a warp hit distinct banks
-    static constexpr int YS = NR;                                       // float2 per unit in a y row (contiguous row copies)
+    static constexpr int YS = NR + 2;                                   // float2 per unit in a y row
     static constexpr int HS = NR * NL + 4;                              // float2 per unit H
     static constexpr int LS = NL * NL + 4;                              // float2 per unit L / X
     static constexpr size_t bars = 0;                                   // 15 mbarriers
@@ -81,14 +81,12 @@ __global__ void __launch_bounds__(32 * NW) k_lg(DetectArgs a) {
         for (int s = 0; s < kSym; ++s) mbar_arrive_expect_tx(&bars[s], (uint32_t)nvalid * NR * 8u);
     }
     __syncthreads();
-    // group leaders copy their unit's H into a padded slot; the 14 y rows of the tile are one
-    // contiguous copy each (few large bulk copies: the copy engine is request-rate bound)
-    if (k == 0 && active)
+    // the group leader of each unit copies its H and its 14 y vectors into padded slots
+    if (k == 0 && active) {
         bulk_g2s(sH + ul * SM::HS, a.H + ((size_t)slot * a.n_sc + sc) * NR * NL, NR * NL * 8u, &bars[kSym]);
-    if (t == 0) {
 #pragma unroll 1
         for (int s = 0; s < kSym; ++s)
-            bulk_g2s(sy + s * TU * SM::YS, a.y + ((size_t)(slot * kSym + s) * a.n_sc + sc0) * NR, nvalid * NR * 8u,
+            bulk_g2s(sy + (s * TU + ul) * SM::YS, a.y + ((size_t)(slot * kSym + s) * a.n_sc + sc) * NR, NR * 8u,
                      &bars[s]);
     }
     mbar_wait(&bars[kSym], 0);
@@ -208,24 +206,6 @@ __global__ void __launch_bounds__(32 * NW) k_lg(DetectArgs a) {
         w[r] = (fac > 0.f) ? make_float2(sv.x * fac, sv.y * fac) : make_float2(0.f, 0.f);
     }
 
-    // Rotate W~_k by 2j 16-byte chunks (j = unit index within the warp) so that in the apply
-    // the UPW units of a warp read different bank groups of their contiguous y rows.
-    static_assert(NR % 2 == 0 && (NR / 2) % UPW == 0, "rotation");
-    constexpr int NCH = NR / 2;  // 16-byte chunks per y vector
-    const int jrot = (lane / NL) * (NCH / UPW);
-    {
-        __syncwarp();
-        float2* scr = sH + ul * SM::HS + k * NR;  // H is no longer needed
-#pragma unroll
-        for (int r = 0; r < NR; ++r) scr[r] = w[r];
-        __syncwarp();
-#pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-            const int p = (c + jrot) % NCH;
-            w[2 * c] = scr[2 * p];
-            w[2 * c + 1] = scr[2 * p + 1];
-        }
-    }
     pdl_wait();  // global writes only after the previous grid completed
     if (active) {
         const size_t unit = (size_t)slot * a.n_sc + sc;
@@ -240,14 +220,10 @@ __global__ void __launch_bounds__(32 * NW) k_lg(DetectArgs a) {
     for (int s = 0; s < kSym; ++s) {
         mbar_wait(&bars[s], 0);
         if (!active) continue;
-        const float4* ys4 = reinterpret_cast<const float4*>(sy + (s * TU + ul) * SM::YS);
+        const float2* ys = sy + (s * TU + ul) * SM::YS;
         float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int c = 0; c < NCH; ++c) {
-            const float4 yv = ys4[(c + jrot) % NCH];  // chunk (c + jrot): conflict-free across the warp's units
-            acc = cmac(acc, w[2 * c], make_float2(yv.x, yv.y));
-            acc = cmac(acc, w[2 * c + 1], make_float2(yv.z, yv.w));
-        }
+        for (int r = 0; r < NR; ++r) acc = cmac(acc, w[r], ys[r]);
         const size_t re = (size_t)(slot * kSym + s) * a.n_sc + sc;
         if (a.llr) {
             float v[QM];
