@@ -132,6 +132,40 @@ mimo_status_t mimo_detect_mmse_host(mimo_plan_t plan, const void* H_host, const 
                                     float sigma2, int n_rx, int n_layers, int n_sc, int n_sym,
                                     int qam_order, void* llr_host);
 
+/* Paper-literal route: the LMMSE pipeline exactly as
+ * the paper states it -- "LU decomposition, forward/backward substitution, and
+ * matrix inversion" (Fig. 4 caption) of "the
+ * received signal covariance matrix R" -- run as five UNFUSED
+ * stage kernels so that each stage can be timed (the B200 analogue of Fig. 5b,
+ * PAPER.md:108-109):
+ *   stage 0  R = H H^H + sigma2 I                     (n_rx x n_rx)
+ *   stage 1  P R = L U, partial pivoting (largest |a_ik|); a unit fails when a
+ *            pivot |u_kk| <= 16 u max|a_ij| (u = unit roundoff of the working
+ *            precision) or on NaN -- e.g. sigma2 = 0 with n_rx > n_layers
+ *   stage 2  R^-1, column by column: L z = P e_c, U x = z
+ *   stage 3  W = H^H R^-1, mu_k = [W H]_kk, SINR_k = mu_k / (1 - mu_k)
+ *            (+inf at sigma2 = 0), W~ = W / mu_k (readings R3, R4)
+ *   stage 4  x~ = W~ y, exact max-log LLRs, quantise (as mimo_detect_mmse)
+ * Stages 0-3 run in precision_bits = 32 ("PS", fp32) or 64 ("PD", fp64)
+ * arithmetic; W~ is rounded once to fp32 and stage 4 is
+ * fp32. Arguments, layouts and outputs are those of mimo_detect_mmse_ex; the
+ * plan's n_rx must be 1, 2, 4, 8 or 16 (else MIMO_ERR_UNSUPPORTED); the plan's
+ * sc_per_h / sym_per_h / llr_type / llr_scale apply. The intermediate R, L\U,
+ * R^-1 and W~ live in a plan-owned workspace (grown on demand; not during
+ * graph capture). Failed units are erasures (LLR 0, x~ 0, SINR 0) and counted
+ * (mimo_plan_sync_status -> MIMO_ERR_NOT_PD).
+ * stage_us: NULL (asynchronous, like mimo_detect_mmse), or a host array of
+ * MIMO_LU_STAGES floats that receives each stage's device time in
+ * microseconds (CUDA events on the plan's stream; the call then synchronises
+ * that stream before returning).
+ * Errors: INVALID_ARG (as mimo_detect_mmse_ex; precision_bits not 32 or 64),
+ * UNSUPPORTED, CUDA, OOM. */
+#define MIMO_LU_STAGES 5
+mimo_status_t mimo_detect_lmmse_lu(mimo_plan_t plan, const void* H, const void* y, float sigma2,
+                                   int n_rx, int n_layers, int n_sc, int n_sym, int qam_order,
+                                   int precision_bits, void* llr_out, void* xhat_out, float* sinr_out,
+                                   float* stage_us);
+
 /* Pre-allocate the plan's kernel workspace for calls of up to n_sc x n_sym
  * (some kernel families keep per-unit W~ in a plan-owned buffer). Calls grow the
  * workspace on demand, but not while the stream is being captured into a CUDA

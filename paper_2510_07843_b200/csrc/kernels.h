@@ -54,6 +54,14 @@ const KernelEntry* big_entries(int* n);
 // sym_per_h, llr_type; 8-byte alignment.
 cudaError_t launch_generic(const DetectArgs& a, cudaStream_t s);
 constexpr int kGenericMaxRx = 64;
+
+// Paper-literal covariance/LU route (k_lu.cu): five
+// stage kernels over a workspace of lu_route_workspace() bytes (DetectArgs::ws).
+// precision_bits 32 ("PS") or 64 ("PD"); ev (nullable) = 6 events recorded
+// before stage 0 and after each stage.
+bool lu_route_supported(int n_rx);
+size_t lu_route_workspace(int n_rx, long long n_units, int precision_bits);
+cudaError_t launch_lu_route(const DetectArgs& a, int precision_bits, cudaStream_t s, cudaEvent_t* ev);
 constexpr int kGenericMaxLayers = 16;
 
 }  // namespace mimo

@@ -47,6 +47,10 @@ struct mimo_plan_s {
     // kernel workspaces: slot 0 for the plan's stream, 1..2 for the host path's streams
     void* kws[3] = {nullptr, nullptr, nullptr};
     size_t kws_bytes[3] = {0, 0, 0};
+    // paper-literal LU route (mimo_detect_lmmse_lu)
+    void* lu_ws = nullptr;
+    size_t lu_ws_bytes = 0;
+    cudaEvent_t lu_ev[MIMO_LU_STAGES + 1] = {};
 };
 
 namespace {
@@ -377,6 +381,72 @@ mimo_status_t mimo_detect_mmse_host(mimo_plan_t p, const void* H_host, const voi
     return MIMO_OK;
 }
 
+mimo_status_t mimo_detect_lmmse_lu(mimo_plan_t p, const void* H, const void* y, float sigma2, int n_rx,
+                                   int n_layers, int n_sc, int n_sym, int qm, int precision_bits, void* llr_out,
+                                   void* xhat_out, float* sinr_out, float* stage_us) {
+    if (!p) return arg_fail(nullptr, "null plan");
+    if (precision_bits != 32 && precision_bits != 64) return arg_fail(p, "precision_bits must be 32 or 64");
+    mimo_status_t st = check_dims(p, sigma2, n_rx, n_layers, n_sc, n_sym, qm);
+    if (st != MIMO_OK) return st;
+    if (!mimo::lu_route_supported(n_rx)) {
+        snprintf(p->err, sizeof(p->err), "LU route: n_rx must be 1, 2, 4, 8 or 16");
+        return MIMO_ERR_UNSUPPORTED;
+    }
+    if (stage_us)
+        for (int i = 0; i < MIMO_LU_STAGES; ++i) stage_us[i] = 0.f;
+    if ((long long)n_sc * n_sym == 0) return MIMO_OK;
+    if (!H || !y) return arg_fail(p, "null H or y");
+    if (!llr_out && !xhat_out && !sinr_out) return arg_fail(p, "no output requested");
+    if (!aligned(H, 16) || !aligned(y, 16) || !aligned(llr_out, 16) || !aligned(xhat_out, 16) ||
+        !aligned(sinr_out, 4))
+        return arg_fail(p, "pointer not 16-byte aligned");
+    const int dev = p->d.device;
+    if (!is_device_ptr(H, dev) || !is_device_ptr(y, dev) || !is_device_ptr(llr_out, dev) ||
+        !is_device_ptr(xhat_out, dev) || !is_device_ptr(sinr_out, dev))
+        return arg_fail(p, "pointer is not device memory on the plan's device");
+    DeviceGuard g(dev);
+    if (g.err != cudaSuccess) return cuda_fail(p, g.err, "cudaSetDevice");
+    mimo::DetectArgs a = make_args(p, H, y, sigma2, n_sc, n_sym, llr_out, xhat_out, sinr_out);
+    a.overlap = 0;
+    const size_t need = mimo::lu_route_workspace(n_rx, a.n_units, precision_bits);
+    cudaError_t e;
+    if (p->lu_ws_bytes < need) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (p->stream) cudaStreamIsCapturing(p->stream, &cs);
+        if (cs != cudaStreamCaptureStatusNone) return arg_fail(p, "LU workspace must grow while capturing a graph");
+        if (p->lu_ws) {
+            cudaStreamSynchronize(p->stream);
+            cudaFree(p->lu_ws);
+            p->lu_ws = nullptr;
+            p->lu_ws_bytes = 0;
+        }
+        if ((e = cudaMalloc(&p->lu_ws, need)) != cudaSuccess) {
+            p->lu_ws = nullptr;
+            return cuda_fail(p, e, "cudaMalloc(LU workspace)");
+        }
+        p->lu_ws_bytes = need;
+    }
+    a.ws = p->lu_ws;
+    cudaEvent_t* ev = nullptr;
+    if (stage_us) {
+        for (int i = 0; i <= MIMO_LU_STAGES; ++i)
+            if (!p->lu_ev[i] && (e = cudaEventCreate(&p->lu_ev[i])) != cudaSuccess)
+                return cuda_fail(p, e, "cudaEventCreate");
+        ev = p->lu_ev;
+    }
+    if ((e = mimo::launch_lu_route(a, precision_bits, p->stream, ev)) != cudaSuccess)
+        return cuda_fail(p, e, "LU route");
+    if (stage_us) {
+        if ((e = cudaEventSynchronize(ev[MIMO_LU_STAGES])) != cudaSuccess) return cuda_fail(p, e, "LU route sync");
+        for (int i = 0; i < MIMO_LU_STAGES; ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+            stage_us[i] = ms * 1000.f;
+        }
+    }
+    return MIMO_OK;
+}
+
 mimo_status_t mimo_plan_reserve(mimo_plan_t p, int n_sc, int n_sym) {
     if (!p) return arg_fail(nullptr, "null plan");
     if (n_sc < 0 || n_sym < 0 || n_sc % p->d.sc_per_h || n_sym % p->d.sym_per_h)
@@ -423,6 +493,9 @@ mimo_status_t mimo_plan_destroy(mimo_plan_t p) {
             if (p->e_out[i]) cudaEventDestroy(p->e_out[i]);
         }
         if (p->ws) cudaFree(p->ws);
+        if (p->lu_ws) cudaFree(p->lu_ws);
+        for (int i = 0; i <= MIMO_LU_STAGES; ++i)
+            if (p->lu_ev[i]) cudaEventDestroy(p->lu_ev[i]);
         for (int i = 0; i < 3; ++i)
             if (p->kws[i]) cudaFree(p->kws[i]);
         if (p->d_fail) cudaFree(p->d_fail);

@@ -28,6 +28,7 @@ MIMO_ERR_NOT_PD = 4
 MIMO_ERR_OOM = 5
 
 LLR_F32, LLR_F16, LLR_I8 = 0, 1, 2
+LU_STAGES = ("cov", "lu", "inv", "weights", "apply")  # mimo_detect_lmmse_lu stages (MIMO_LU_STAGES)
 PLAN_OVERLAP_CALLS = 1
 SYM_PER_SLOT = 14
 
@@ -76,6 +77,8 @@ def load_library(path: str | None = None):
     L.mimo_detect_mmse_ex.restype = i
     L.mimo_detect_mmse_host.argtypes = [vp, vp, vp, f, i, i, i, i, i, vp]
     L.mimo_detect_mmse_host.restype = i
+    L.mimo_detect_lmmse_lu.argtypes = [vp, vp, vp, f, i, i, i, i, i, i, vp, vp, vp, ctypes.POINTER(f)]
+    L.mimo_detect_lmmse_lu.restype = i
     L.mimo_plan_reserve.argtypes = [vp, i, i]
     L.mimo_plan_reserve.restype = i
     L.mimo_plan_sync_status.argtypes = [vp, ctypes.POINTER(ll)]
@@ -210,6 +213,36 @@ class Plan:
                                                self.n_layers, n_sc, n_sym, self.qm, ptr(out), ptr(xhat),
                                                ptr(sinr))
         self._check(st)
+        return out
+
+    def detect_lu(self, H, y, sigma2: float, *, precision: int = 32, out=None, xhat=None, sinr=None,
+                  timing: bool = False, want_llr: bool = True):
+        """Paper-literal route (covariance R, pivoted LU, substitution inversion, W = H^H R^-1)
+        as five stage kernels; precision 32 ("PS") or 64 ("PD"). Returns the LLR tensor, or
+        (llr, {stage: device microseconds}) when timing=True (the call then synchronises)."""
+        import torch
+        n_sym, n_sc = y.shape[0], y.shape[1]
+        sh = self.shapes(n_sc, n_sym)
+        self._dev_tensor(H, "H", torch.complex64, sh["H"])
+        self._dev_tensor(y, "y", torch.complex64, sh["y"])
+        if want_llr and out is None:
+            out = torch.empty(sh["llr"], dtype=self.llr_dtype, device=self.device)
+        if out is not None:
+            self._dev_tensor(out, "out", self.llr_dtype, sh["llr"])
+        if xhat is not None:
+            self._dev_tensor(xhat, "xhat", torch.complex64, sh["xhat"])
+        if sinr is not None:
+            self._dev_tensor(sinr, "sinr", torch.float32, sh["sinr"])
+        if self._fixed_stream is None:
+            self._lib.mimo_plan_set_stream(self._h, ctypes.c_void_p(self._stream_ptr()))
+        ptr = (lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None)
+        st_us = (ctypes.c_float * len(LU_STAGES))() if timing else None
+        st = self._lib.mimo_detect_lmmse_lu(self._h, ptr(H), ptr(y), ctypes.c_float(sigma2), self.n_rx,
+                                            self.n_layers, n_sc, n_sym, self.qm, int(precision), ptr(out),
+                                            ptr(xhat), ptr(sinr), st_us)
+        self._check(st)
+        if timing:
+            return out, dict(zip(LU_STAGES, (float(v) for v in st_us)))
         return out
 
     def detect_host(self, H, y, sigma2: float, out=None):

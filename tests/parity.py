@@ -49,25 +49,27 @@ def run_gpu(w: synth.Workload, *, xhat=True, sinr=True, llr_scale=1.0, plan=None
     return res
 
 
-def oracle_units(w: synth.Workload, units, threads=None, H=None, y=None):
+def oracle_units(w: synth.Workload, units, threads=None, H=None, y=None, route="chol"):
     units = np.asarray(units, dtype=np.int64)
     Hu = (w.H if H is None else H).reshape(w.n_units, w.n_rx, w.n_layers)[units]
     yy = w.y if y is None else y
     Yu = np.stack([yy[synth.unit_re_index(u, w.n_sc, w.sc_per_h)] for u in units]) if len(units) else \
         np.zeros((0, 14 * w.sc_per_h, w.n_rx), np.complex64)
-    return oracle.detect(Hu, Yu, w.sigma2, w.qm, threads=threads or oracle.max_threads())
+    return oracle.detect(Hu, Yu, w.sigma2, w.qm, threads=threads or oracle.max_threads(), route=route)
 
 
 def gather_units(w: synth.Workload, grid: np.ndarray, units):
     return np.stack([grid[synth.unit_re_index(u, w.n_sc, w.sc_per_h)] for u in units])
 
 
-def compare(w: synth.Workload, gpu: dict, units=None, llr_scale=1.0, threads=None, H=None, y=None) -> dict:
-    """Compare GPU outputs against the oracle on the given units (default: all)."""
+def compare(w: synth.Workload, gpu: dict, units=None, llr_scale=1.0, threads=None, H=None, y=None,
+            route="chol", tol_x=TOL_X, tol_sinr=TOL_SINR, tol_llr=TOL_LLR) -> dict:
+    """Compare GPU outputs against the oracle on the given units (default: all).
+    route="lu" compares with the oracle's paper-literal covariance/LU route."""
     if units is None:
         units = np.arange(w.n_units)
     units = np.asarray(units, dtype=np.int64)
-    ref = oracle_units(w, units, threads=threads, H=H, y=y)
+    ref = oracle_units(w, units, threads=threads, H=H, y=y, route=route)
     rep = dict(units=len(units), n_failed_ref=int((~ref["ok"]).sum()))
     # x~
     if "xhat" in gpu:
@@ -75,7 +77,7 @@ def compare(w: synth.Workload, gpu: dict, units=None, llr_scale=1.0, threads=Non
         rx = ref["xhat"]
         err = np.abs(gx - rx) / np.maximum(np.abs(rx), 1.0)
         rep["xhat_max_err"] = float(err.max()) if err.size else 0.0
-        assert rep["xhat_max_err"] <= TOL_X, rep
+        assert rep["xhat_max_err"] <= tol_x, rep
     # SINR
     if "sinr" in gpu:
         gs = gpu["sinr"][units].astype(np.float64)
@@ -85,15 +87,15 @@ def compare(w: synth.Workload, gpu: dict, units=None, llr_scale=1.0, threads=Non
         # relative 1e-4; below SINR 1e-3 (erased / near-erased layers) absolute 1e-7
         rel = np.abs(gs[fin] - rs[fin]) / np.maximum(np.abs(rs[fin]), 1e-3)
         rep["sinr_max_rel"] = float(rel.max()) if rel.size else 0.0
-        assert rep["sinr_max_rel"] <= TOL_SINR, rep
+        assert rep["sinr_max_rel"] <= tol_sinr, rep
     # LLRs
     gl = gather_units(w, gpu["llr"], units)
     rl = ref["llr"] * llr_scale
-    rep.update(compare_llr(gl, rl, w.llr))
+    rep.update(compare_llr(gl, rl, w.llr, tol_llr))
     return rep
 
 
-def compare_llr(gl: np.ndarray, rl: np.ndarray, llr: str) -> dict:
+def compare_llr(gl: np.ndarray, rl: np.ndarray, llr: str, tol_llr: float = TOL_LLR) -> dict:
     """gl: GPU LLRs (quantised); rl: oracle fp64 LLRs already multiplied by llr_scale."""
     rep = {}
     if llr == "i8":
@@ -101,7 +103,7 @@ def compare_llr(gl: np.ndarray, rl: np.ndarray, llr: str) -> dict:
         g = gl.astype(np.int64)
         d = np.abs(g - q)
         v = np.clip(rl, -127.0, 127.0)
-        near_half = np.abs(np.abs(v - np.floor(v)) - 0.5) <= TOL_LLR * np.maximum(np.abs(v), 1.0)
+        near_half = np.abs(np.abs(v - np.floor(v)) - 0.5) <= tol_llr * np.maximum(np.abs(v), 1.0)
         bad = (d > 1) | ((d == 1) & ~near_half)
         rep["llr_mismatch"] = int((d > 0).sum())
         rep["llr_bad"] = int(bad.sum())
@@ -113,8 +115,8 @@ def compare_llr(gl: np.ndarray, rl: np.ndarray, llr: str) -> dict:
         assert np.all(np.isfinite(g)), "non-finite GPU LLR"
         err = np.abs(g - qref) / np.maximum(np.abs(qref), 1.0)
         rep["llr_max_err"] = float(err.max()) if err.size else 0.0
-        assert rep["llr_max_err"] <= TOL_LLR, rep
-        hard_ok = ((g < 0) == (qref < 0)) | (np.abs(rl) < TOL_LLR)
+        assert rep["llr_max_err"] <= tol_llr, rep
+        hard_ok = ((g < 0) == (qref < 0)) | (np.abs(rl) < tol_llr)
     rep["hard_bit_mismatch"] = int((~hard_ok).sum())
     assert rep["hard_bit_mismatch"] == 0, rep
     rep["n_llr"] = int(gl.size)
