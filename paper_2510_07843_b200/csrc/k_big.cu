@@ -41,7 +41,12 @@ __device__ __forceinline__ float2 shfl2(float2 v, int src) {
 // One warp per PRB-unit (UPB units per CTA), warp-synchronous, no CTA barriers.
 template <int NR, int NL>
 struct SetupSmem {
-    static constexpr size_t per_unit = (size_t)NR * NL * 8 + 3 * NL * NL * 8 + 3 * NL * 4 + 16;
+    // sH [NR][NL] float2 | sX [NL][NL] float2 | sDinv [NL] float | mbarrier
+    static constexpr size_t h = 0;
+    static constexpr size_t x = (size_t)NR * NL * 8;
+    static constexpr size_t dinv = x + (size_t)NL * NL * 8;
+    static constexpr size_t bar = (dinv + NL * 4 + 7) / 8 * 8;
+    static constexpr size_t per_unit = (bar + 8 + 15) / 16 * 16;
 };
 
 template <int NR, int NL, int QM, int UPB>
@@ -50,31 +55,32 @@ __global__ void __launch_bounds__(32 * UPB) k_big_setup(DetectArgs a) {
     constexpr int WS = BigWs<NR, NL>::stride;
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    unsigned char* base = smem + (size_t)warp * SetupSmem<NR, NL>::per_unit;
-    float2* sH = reinterpret_cast<float2*>(base);                 // [r][l]
-    float2* sG = sH + NR * NL;                                    // G
-    float2* sX = sG + NL * NL;                                    // L rows, then X = L^-1 [i][j]
-    float2* sGi = sX + NL * NL;                                   // G^-1
-    float* sDinv = reinterpret_cast<float*>(sGi + NL * NL);
+    using SS = SetupSmem<NR, NL>;
+    unsigned char* base = smem + (size_t)warp * SS::per_unit;
+    float2* sH = reinterpret_cast<float2*>(base + SS::h);         // [r][l]
+    float2* sX = reinterpret_cast<float2*>(base + SS::x);         // L rows, then X = L^-1 [i][j]
+    float* sDinv = reinterpret_cast<float*>(base + SS::dinv);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(base + SS::bar);
 
     pdl_launch_dependents();
     const long long u = (long long)blockIdx.x * UPB + warp;
     const bool valid = u < a.n_units;
     const float s2 = a.sigma2;
     const float norm = (float)qam_norm(QM);
-    if (valid) {
-        const float4* src = reinterpret_cast<const float4*>(a.H + u * NR * NL);
-        float4* dst = reinterpret_cast<float4*>(sH);
-#pragma unroll 4
-        for (int i = lane; i < NR * NL / 2; i += 32) dst[i] = __ldg(src + i);
+    if (valid && lane == 0) {  // a1: the unit's H (8 KiB) by one bulk copy
+        mbar_init(bar, 1);
+        fence_mbar_init();
+        mbar_arrive_expect_tx(bar, (uint32_t)(NR * NL * 8));
+        bulk_g2s(sH, a.H + u * NR * NL, (uint32_t)(NR * NL * 8), bar);
     }
     __syncwarp();
-    // a2: lane -> row i = lane/2, columns 8h .. 8h+7 of G (full rows, broadcast H reads)
+    if (valid) mbar_wait(bar, 0);
+    // a2: lane -> row i = lane/2, columns 8h .. 8h+7 of G (broadcast H reads)
+    float2 gq[8];
     {
         const int i = lane >> 1, h = lane & 1;
-        float2 g[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) g[q] = make_float2(0.f, 0.f);
+        for (int q = 0; q < 8; ++q) gq[q] = make_float2(0.f, 0.f);
 #pragma unroll 4
         for (int r = 0; r < NR; ++r) {
             const float2 hi = sH[r * NL + i];
@@ -82,24 +88,24 @@ __global__ void __launch_bounds__(32 * UPB) k_big_setup(DetectArgs a) {
 #pragma unroll
             for (int q2 = 0; q2 < 4; ++q2) {
                 const float4 v = hr[q2];
-                g[2 * q2].x = fmaf(hi.x, v.x, fmaf(hi.y, v.y, g[2 * q2].x));
-                g[2 * q2].y = fmaf(hi.x, v.y, fmaf(-hi.y, v.x, g[2 * q2].y));
-                g[2 * q2 + 1].x = fmaf(hi.x, v.z, fmaf(hi.y, v.w, g[2 * q2 + 1].x));
-                g[2 * q2 + 1].y = fmaf(hi.x, v.w, fmaf(-hi.y, v.z, g[2 * q2 + 1].y));
+                gq[2 * q2].x = fmaf(hi.x, v.x, fmaf(hi.y, v.y, gq[2 * q2].x));
+                gq[2 * q2].y = fmaf(hi.x, v.y, fmaf(-hi.y, v.x, gq[2 * q2].y));
+                gq[2 * q2 + 1].x = fmaf(hi.x, v.z, fmaf(hi.y, v.w, gq[2 * q2 + 1].x));
+                gq[2 * q2 + 1].y = fmaf(hi.x, v.w, fmaf(-hi.y, v.z, gq[2 * q2 + 1].y));
             }
         }
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int j = 8 * h + q;
-            sG[i * NL + j] = (i == j) ? make_float2(g[q].x + s2, 0.f) : g[q];
-        }
     }
-    __syncwarp();
     // a3: Cholesky, lane k (and its duplicate k+16) holds row k
     const int k = lane & 15;
-    float2 g[NL];
+    float2 g[NL];  // row k of G: columns 0-7 from lane 2k, 8-15 from lane 2k+1
 #pragma unroll
-    for (int j = 0; j < NL; ++j) g[j] = sG[k * NL + j];
+    for (int q = 0; q < 8; ++q) {
+        g[q] = shfl2(gq[q], 2 * k);
+        g[8 + q] = shfl2(gq[q], 2 * k + 1);
+    }
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
+        if (j == k) g[j] = make_float2(g[j].x + s2, 0.f);
     float gmax = 0.f;
 #pragma unroll
     for (int j = 0; j < NL; ++j)
@@ -1238,6 +1244,182 @@ __global__ void __launch_bounds__(kTc2Simt + 32, 1) k_big_tc3(DetectArgs a, cons
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
 }
 
+// ------------------------------------------------------------------------
+// k_big_apply2: rows a6-a7 as a K-streamed SIMT GEMM.
+// One CTA (168 threads) per PRB-unit; X~[16 x 168] = W~[16 x 64] Y[64 x 168]
+// complex, K (= rx) streamed in 4 chunks of 16 antennas: each chunk is one TMA
+// tile of the unit's 168 y rows x 128 B (3-D map {128 floats, n_sc, n_sym}, box
+// {32, 12, 14}, SWIZZLE_128B: the 16-byte chunk c of RE row e sits at c ^ (e & 7),
+// so 8 consecutive REs reading the same antennas hit 8 distinct bank groups).
+// Two chunk stages (2 x 21 KiB) + W~ (8 KiB) keep 4 CTAs (21 warps) per SM.
+// Thread t: layer quad lq = t & 3 (layers 4lq..4lq+3), RE quad q = t >> 2
+// (REs q, q+42, q+84, q+126): a 4 x 4 complex register tile, 16 FFMA per
+// 128-bit shared load. Epilogue: exact max-log demap of the 4 x 4 outputs,
+// 24-byte (int8) LLR pieces per RE (4 threads = one contiguous 96-byte record).
+struct Ap2 {
+    static constexpr int ROWS = kRe;                        // 168
+    static constexpr size_t chunk = (size_t)ROWS * 128;     // 21504 = 21 KiB
+    static constexpr size_t y0 = 0;                         // 2 stages, 1024-aligned
+    static constexpr size_t W = 2 * chunk;                  // [64][16] float2 + 16 slopes
+    static constexpr size_t wbytes = 64 * 16 * 8 + 16 * 4;  // 8256
+    static constexpr size_t bars = W + (wbytes + 127) / 128 * 128;  // 3 mbarriers
+    static constexpr size_t total = bars + 64 + 1024;       // + alignment slack
+    static constexpr int THREADS = 168;
+};
+
+template <int NR, int NL, int QM, int LT>
+__global__ void __launch_bounds__(Ap2::THREADS, 4) k_big_apply2(DetectArgs a, const __grid_constant__ CUtensorMap ymap) {
+    static_assert(NL == 16 && NR == 64, "k_big_apply2: 64 x 16");
+    constexpr int WS = BigWs<NR, NL>::stride;
+    constexpr int NCH = NR / 16;  // K chunks of 16 antennas
+    extern __shared__ unsigned char smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    unsigned char* g = smem_raw + (base - raw);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(g + Ap2::bars);  // [0],[1] y stages, [2] W~
+    const float2* sW = reinterpret_cast<const float2*>(g + Ap2::W);
+    const float* sSlope = reinterpret_cast<const float*>(g + Ap2::W + 64 * 16 * 8);
+
+    pdl_launch_dependents();
+    const int t = threadIdx.x;
+    const long long u = blockIdx.x;
+    const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);
+    if (t == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        mbar_init(&bars[2], 1);
+        fence_mbar_init();
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ymap)) : "memory");
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            mbar_arrive_expect_tx(&bars[c], (uint32_t)Ap2::chunk);
+            tma_load_3d(base + (uint32_t)(Ap2::y0 + c * Ap2::chunk), &ymap, 32 * c, fb * kSc, slot * kSym, &bars[c]);
+        }
+    }
+    __syncthreads();  // barriers initialised before anyone waits on them
+    pdl_wait();       // W~ of this call's setup kernel is complete
+    if (t == 0) {
+        mbar_arrive_expect_tx(&bars[2], (uint32_t)Ap2::wbytes);
+        bulk_g2s(g + Ap2::W, reinterpret_cast<const float*>(a.ws) + u * WS, (uint32_t)Ap2::wbytes, &bars[2]);
+    }
+    const int lq = t & 3, q = t >> 2;
+    float2 acc[4][4];  // [RE e][layer kk]
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) acc[e][kk] = make_float2(0.f, 0.f);
+    mbar_wait(&bars[2], 0);
+#pragma unroll 1
+    for (int c = 0; c < NCH; ++c) {
+        const int st = c & 1;
+        mbar_wait(&bars[st], (uint32_t)((c >> 1) & 1));
+        const unsigned char* ys = g + Ap2::y0 + st * Ap2::chunk;
+#pragma unroll 2
+        for (int j = 0; j < 8; ++j) {  // 16-byte chunk j = antennas 16c + 2j, 16c + 2j + 1
+            float4 yv[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int row = q + 42 * e;
+                yv[e] = *reinterpret_cast<const float4*>(ys + row * 128 + ((j ^ (row & 7)) << 4));
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int r = 16 * c + 2 * j + h;
+                const float4 w01 = *reinterpret_cast<const float4*>(sW + r * NL + 4 * lq);
+                const float4 w23 = *reinterpret_cast<const float4*>(sW + r * NL + 4 * lq + 2);
+                const float2 wk[4] = {make_float2(w01.x, w01.y), make_float2(w01.z, w01.w),
+                                      make_float2(w23.x, w23.y), make_float2(w23.z, w23.w)};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 yr = h ? make_float2(yv[e].z, yv[e].w) : make_float2(yv[e].x, yv[e].y);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) acc[e][kk] = cmac(acc[e][kk], wk[kk], yr);
+                }
+            }
+        }
+        if (c + 2 < NCH) {
+            __syncthreads();  // every thread is done with stage st
+            if (t == 0) {
+                mbar_arrive_expect_tx(&bars[st], (uint32_t)Ap2::chunk);
+                tma_load_3d(base + (uint32_t)(Ap2::y0 + st * Ap2::chunk), &ymap, 32 * (c + 2), fb * kSc, slot * kSym,
+                            &bars[st]);
+            }
+        }
+    }
+    float slope[4];
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) slope[kk] = sSlope[4 * lq + kk];
+    constexpr int kRec = NL * QM * LlrTraits<LT>::bytes;   // one RE record
+    constexpr int kPiece = 4 * QM * LlrTraits<LT>::bytes;  // this thread's 4 layers
+    const bool zf = !(a.sigma2 > 0.f);
+    const float ia = rsqrtf((float)qam_norm(QM));
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const int ri = q + 42 * e;
+        const int s = ri / kSc, f = ri % kSc;
+        const size_t re = (size_t)(slot * kSym + s) * a.n_sc + fb * kSc + f;
+        if (a.llr) {
+            float v[4 * QM];
+            uint32_t wd[(kPiece + 3) / 4];
+            if (!zf) {
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) demap_layer<QM, false, LT>(acc[e][kk], slope[kk], v + kk * QM);
+                pack_llr<LT, 4 * QM, false>(v, wd);
+            } else {
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) demap_layer<QM, true, LT>(acc[e][kk], slope[kk], v + kk * QM);
+                pack_llr<LT, 4 * QM, true>(v, wd);
+            }
+            store_bytes<kPiece>((char*)a.llr + re * kRec + lq * kPiece, wd);
+        }
+        if (a.xhat) {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+                a.xhat[re * NL + 4 * lq + kk] = make_float2(acc[e][kk].x * ia, acc[e][kk].y * ia);
+        }
+    }
+}
+
+template <int NR, int NL, int QM, int LT>
+cudaError_t launch_ap2(const DetectArgs& a, cudaStream_t s) {
+    if (a.n_units <= 0) return cudaSuccess;
+    auto enc = tensor_map_encoder();
+    if (!enc) return cudaErrorNotSupported;
+    CUtensorMap ymap;
+    const cuuint64_t gdim[3] = {(cuuint64_t)(2 * NR), (cuuint64_t)a.n_sc, (cuuint64_t)a.n_sym};
+    const cuuint64_t gstride[2] = {(cuuint64_t)NR * 8, (cuuint64_t)a.n_sc * NR * 8};
+    const cuuint32_t box[3] = {32, (cuuint32_t)kSc, (cuuint32_t)kSym};
+    const cuuint32_t estride[3] = {1, 1, 1};
+    if (enc(&ymap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float2*>(a.y), gdim, gstride, box, estride,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    constexpr int UPB = 4;
+    cudaError_t e = launch_kernel(k_big_setup<NR, NL, QM, UPB>, dim3((unsigned)((a.n_units + UPB - 1) / UPB)),
+                                  dim3(32 * UPB), UPB * SetupSmem<NR, NL>::per_unit, s, a.overlap, a);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)a.n_units);
+    cfg.blockDim = dim3(Ap2::THREADS);
+    cfg.dynamicSmemBytes = Ap2::total;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = a.overlap ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k_big_apply2<NR, NL, QM, LT>, a, ymap);
+}
+
+template <int NR, int NL, int QM, int LT>
+cudaError_t prepare_ap2() {
+    cudaError_t e = cudaFuncSetAttribute(k_big_setup<NR, NL, QM, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(4 * SetupSmem<NR, NL>::per_unit));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_big_apply2<NR, NL, QM, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)Ap2::total);
+}
+
 template <int NR, int NL, int QM, int LT>
 cudaError_t launch_tc3(const DetectArgs& a, cudaStream_t s) {
     if (a.n_units <= 0) return cudaSuccess;
@@ -1331,8 +1513,15 @@ cudaError_t prepare() {
             workspace<NR, NL>                                                                             \
     }
 
+#define BIGAP2_ENTRY(NAME, NR, NL, QM, LT)                                                               \
+    KernelEntry {                                                                                         \
+        NAME, NR, NL, QM, kSc, 14, LT, 32, 2, launch_ap2<NR, NL, QM, LT>, prepare_ap2<NR, NL, QM, LT>,   \
+            workspace<NR, NL>                                                                             \
+    }
+
 const KernelEntry kEntries[] = {
     BIG_ENTRY("big_64x16_q6_i8", 64, 16, 6, kLlrI8),  // C5 (SIMT GEMM; currently the fastest)
+    BIGAP2_ENTRY("big2_64x16_q6_i8", 64, 16, 6, kLlrI8),
     BIGTC3_ENTRY("bigtc3_64x16_q6_i8", 64, 16, 6, kLlrI8),
     BIGTC2_ENTRY("bigtc2_64x16_q6_i8", 64, 16, 6, kLlrI8),  // tensor cores, warp-specialised
     BIGTC_ENTRY("bigtc_64x16_q6_i8", 64, 16, 6, kLlrI8),

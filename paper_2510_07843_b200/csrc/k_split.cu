@@ -276,8 +276,8 @@ __global__ void __launch_bounds__(128) k_apply_units(DetectArgs a) {
 // Streaming apply with a register prefetch ring: thread (g, sc) walks symbols
 // g, g+G, ... of its slot keeping PF y vectors in flight (continuous HBM
 // traffic instead of one burst per thread).
-template <int NR, int NL, int QM, int LT, int G, int PF, int SCPH>
-__global__ void __launch_bounds__(128) k_apply_stream(DetectArgs a) {
+template <int NR, int NL, int QM, int LT, int G, int PF, int SCPH, int MINB>
+__global__ void __launch_bounds__(128, MINB) k_apply_stream(DetectArgs a) {
     constexpr int NS = (kSym + G - 1) / G;
     constexpr int WS = UnitWs<NR, NL>::stride;
     static_assert(PF >= 1 && PF <= NS, "prefetch distance");
@@ -356,14 +356,14 @@ __global__ void __launch_bounds__(128) k_apply_stream(DetectArgs a) {
     }
 }
 
-template <int NR, int NL, int QM, int LT, int UPC, int G, int PF, int SCPH>
+template <int NR, int NL, int QM, int LT, int UPC, int G, int PF, int SCPH, int MINB>
 cudaError_t launch_stream(const DetectArgs& a, cudaStream_t s) {
     if (a.n_units <= 0) return cudaSuccess;
     const unsigned g1 = (unsigned)((a.n_units + UPC - 1) / UPC);
     cudaError_t e = launch_kernel(k_setup_units<NR, NL, QM, UPC>, dim3(g1), dim3(128), 0, s, a.overlap, a);
     if (e != cudaSuccess) return e;
     dim3 g2((a.n_sc + 127) / 128, a.n_slots * G);
-    return launch_kernel(k_apply_stream<NR, NL, QM, LT, G, PF, SCPH>, g2, dim3(128), 0, s, a.overlap, a);
+    return launch_kernel(k_apply_stream<NR, NL, QM, LT, G, PF, SCPH, MINB>, g2, dim3(128), 0, s, a.overlap, a);
 }
 
 template <int NR, int NL>
@@ -387,10 +387,11 @@ cudaError_t launch(const DetectArgs& a, cudaStream_t s) {
             workspace<NR, NL>                                                                        \
     }
 
-#define STREAM_ENTRY(NAME, NR, NL, QM, LT, SCPH, UPC, G, PF)                                        \
+#define STREAM_ENTRY(NAME, NR, NL, QM, LT, SCPH, UPC, G, PF) STREAM_ENTRY_B(NAME, NR, NL, QM, LT, SCPH, UPC, G, PF, 1)
+#define STREAM_ENTRY_B(NAME, NR, NL, QM, LT, SCPH, UPC, G, PF, MINB)                                 \
     KernelEntry {                                                                                    \
-        NAME, NR, NL, QM, SCPH, 14, LT, 32, 2, launch_stream<NR, NL, QM, LT, UPC, G, PF, SCPH>, nullptr, \
-            workspace<NR, NL>                                                                        \
+        NAME, NR, NL, QM, SCPH, 14, LT, 32, 2, launch_stream<NR, NL, QM, LT, UPC, G, PF, SCPH, MINB>,    \
+            nullptr, workspace<NR, NL>                                                               \
     }
 
 const KernelEntry kEntries[] = {
@@ -400,6 +401,10 @@ const KernelEntry kEntries[] = {
     STREAM_ENTRY("stream_8x4_q6_i8_g2pf2", 8, 4, 6, kLlrI8, 12, 16, 2, 2),
     STREAM_ENTRY("stream_8x4_q6_i8_g2pf4", 8, 4, 6, kLlrI8, 12, 16, 2, 4),
     STREAM_ENTRY("stream_8x4_q6_i8_g7pf2", 8, 4, 6, kLlrI8, 12, 16, 7, 2),
+    STREAM_ENTRY_B("stream_8x4_q6_i8_b4", 8, 4, 6, kLlrI8, 12, 16, 2, 2, 4),
+    STREAM_ENTRY_B("stream_8x4_q6_i8_b5", 8, 4, 6, kLlrI8, 12, 16, 2, 2, 5),
+    STREAM_ENTRY_B("stream_8x4_q6_i8_g1b4", 8, 4, 6, kLlrI8, 12, 16, 1, 2, 4),
+    STREAM_ENTRY_B("stream_8x4_q6_i8_g7b6", 8, 4, 6, kLlrI8, 12, 16, 7, 2, 6),
     SPLIT_ENTRY("split_8x4_q6_i8", 8, 4, 6, kLlrI8, 12, 32, 7),
     SPLIT_ENTRY("split_8x4_q6_f32", 8, 4, 6, kLlrF32, 12, 32, 7),
     SPLIT_ENTRY("split_8x4_q6_f16", 8, 4, 6, kLlrF16, 12, 32, 7),
