@@ -1420,6 +1420,238 @@ cudaError_t prepare_ap2() {
                                 (int)Ap2::total);
 }
 
+// ------------------------------------------------------------------------
+// k_big_apply3: rows a6-a7 on the tensor cores, one CTA (4 warps) per PRB-unit,
+// two CTAs per SM. The 168 x 128 real GEMM  X^T = Y^T B  (reading R21: 3-pass
+// TF32 split) is streamed over K in the same 4 TMA chunks as k_big_apply2
+// (16 antennas = 128 B per RE row, SWIZZLE_128B = the canonical K-major UMMA
+// layout). Per chunk c:
+//   MMA1(c): A = y chunk (fp32 read as TF32 = y_hi), B = [B_hi; B_lo] rows of
+//            K-tile c (N = 64): columns 0-31 += y_hi B_hi, 32-63 += y_hi B_lo;
+//   SIMT   : y_lo = y - trunc(y) into a separate chunk buffer (no in-place
+//            rewrite, so the y stage is released as soon as MMA1 has read it);
+//   MMA2(c): A = y_lo chunk, B = B_hi rows (N = 32): columns 0-31 += y_lo B_hi.
+// Two M = 128 tiles cover the 168 RE rows (rows 0-127 and 40-167), 64 TMEM
+// columns each. B is built once per unit from W~ (plan workspace) by the SIMT
+// threads: row n < 16 = Re output k = n (Wr, -Wi pairs), n >= 16 = Im output
+// (Wi, Wr pairs), B_lo = B - trunc(B) at row n + 32. Epilogue: thread = TMEM
+// lane = RE row, 64 columns -> x~_k = hi + lo, exact max-log demap, 96-byte
+// record store. Thread 0 issues the MMAs (single-thread tcgen05.mma) and the
+// TMA refills.
+struct Ap3 {
+    static constexpr int THREADS = 128;
+    static constexpr size_t chunk = (size_t)kRe * 128;      // 21504
+    static constexpr size_t y0 = 0;                         // 2 stages
+    static constexpr size_t ylo = 2 * chunk;                // 1 buffer
+    static constexpr size_t B = 3 * chunk;                  // 4 K-tiles x 64 rows x 128 B (1024-aligned)
+    static constexpr size_t wraw = B + 4 * 64 * 128;        // W~ [64][16] float2 + 16 slopes
+    static constexpr size_t wbytes = 64 * 16 * 8 + 16 * 4;  // 8256
+    static constexpr size_t bars = wraw + 8320;             // 8 mbarriers
+    static constexpr size_t tslot = bars + 64;
+    static constexpr size_t total = tslot + 16 + 1024;
+};
+static_assert(Ap3::B % 1024 == 0, "B set must be 1024-aligned");
+
+template <int NR, int NL, int QM, int LT>
+__global__ void __launch_bounds__(Ap3::THREADS, 2) k_big_apply3(DetectArgs a, const __grid_constant__ CUtensorMap ymap) {
+    static_assert(NL == 16 && NR == 64, "k_big_apply3: 64 x 16");
+    constexpr int WS = BigWs<NR, NL>::stride;
+    constexpr int NCH = 4;
+    extern __shared__ unsigned char smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    unsigned char* g = smem_raw + (base - raw);
+    uint64_t* ybar = reinterpret_cast<uint64_t*>(g + Ap3::bars);  // [2]
+    uint64_t* wbar = ybar + 2;
+    uint64_t* m1bar = ybar + 3;
+    uint64_t* m2bar = ybar + 4;
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(g + Ap3::tslot);
+    const float2* sW = reinterpret_cast<const float2*>(g + Ap3::wraw);
+    const float* sSlope = reinterpret_cast<const float*>(g + Ap3::wraw + 64 * 16 * 8);
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+
+    pdl_launch_dependents();
+    const long long u = blockIdx.x;
+    const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);
+    if (t == 0) {
+        for (int i = 0; i < 5; ++i) mbar_init(&ybar[i], 1);
+        fence_mbar_init();
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ymap)) : "memory");
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            mbar_arrive_expect_tx(&ybar[c], (uint32_t)Ap3::chunk);
+            tma_load_3d(base + (uint32_t)(Ap3::y0 + c * Ap3::chunk), &ymap, 32 * c, fb * kSc, slot * kSym, &ybar[c]);
+        }
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tslot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+    pdl_wait();  // W~ of this call's setup kernel is complete
+    if (t == 0) {
+        mbar_arrive_expect_tx(wbar, (uint32_t)Ap3::wbytes);
+        bulk_g2s(g + Ap3::wraw, reinterpret_cast<const float*>(a.ws) + u * WS, (uint32_t)Ap3::wbytes, wbar);
+    }
+    mbar_wait(wbar, 0);
+    {  // B set: thread -> row n = t >> 2 (output), K-tile kt = t & 3, 8 chunks of 2 antennas
+        const int n = t >> 2, kt = t & 3, kk = n & 15;
+        const bool im_row = n >= 16;
+        float* kb = reinterpret_cast<float*>(g + Ap3::B + (size_t)kt * 64 * 128);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            const int r0 = 16 * kt + 2 * c;
+            const float2 w0 = sW[r0 * NL + kk], w1 = sW[(r0 + 1) * NL + kk];
+            const float4 v = im_row ? make_float4(w0.y, w0.x, w1.y, w1.x) : make_float4(w0.x, -w0.y, w1.x, -w1.y);
+            const float4 lo = make_float4(v.x - tf32_trunc(v.x), v.y - tf32_trunc(v.y), v.z - tf32_trunc(v.z),
+                                          v.w - tf32_trunc(v.w));
+            *reinterpret_cast<float4*>(kb + n * 32 + ((c ^ (n & 7)) << 2)) = v;
+            *reinterpret_cast<float4*>(kb + (n + 32) * 32 + ((c ^ (n & 7)) << 2)) = lo;
+        }
+    }
+    fence_proxy_async();
+    __syncthreads();
+    constexpr uint32_t id64 = (1u << 4) | (2u << 7) | (2u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+    constexpr uint32_t id32 = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+    const uint32_t bbase = base + (uint32_t)Ap3::B;
+    const uint32_t ylob = base + (uint32_t)Ap3::ylo;
+#pragma unroll 1
+    for (int c = 0; c < NCH; ++c) {
+        const int st = c & 1;
+        const uint32_t ys = base + (uint32_t)(Ap3::y0 + st * Ap3::chunk);
+        mbar_wait(&ybar[st], (uint32_t)((c >> 1) & 1));
+        if (t == 0) {
+            tc_fence_after();
+#pragma unroll
+            for (int tile = 0; tile < 2; ++tile)
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks)
+                    umma_tf32(tmem + 64u * tile, umma_desc_sw128(ys + (tile ? 40u * 128u : 0u) + ks * 32u),
+                              umma_desc_sw128(bbase + (uint32_t)c * 8192u + ks * 32u), id64, (c | ks) ? 1u : 0u);
+            umma_commit(m1bar);
+        }
+        if (c >= 1) mbar_wait(m2bar, (uint32_t)((c - 1) & 1));  // y_lo buffer free
+        {
+            const float4* src = reinterpret_cast<const float4*>(g + Ap3::y0 + st * Ap3::chunk);
+            float4* dst = reinterpret_cast<float4*>(g + Ap3::ylo);
+            constexpr int n4 = (int)(Ap3::chunk / 16);
+#pragma unroll 4
+            for (int i = t; i < n4; i += Ap3::THREADS) {
+                float4 v = src[i];
+                v.x -= tf32_trunc(v.x);
+                v.y -= tf32_trunc(v.y);
+                v.z -= tf32_trunc(v.z);
+                v.w -= tf32_trunc(v.w);
+                dst[i] = v;
+            }
+        }
+        fence_proxy_async();
+        __syncthreads();
+        if (t == 0) {
+            tc_fence_after();
+#pragma unroll
+            for (int tile = 0; tile < 2; ++tile)
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks)
+                    umma_tf32(tmem + 64u * tile, umma_desc_sw128(ylob + (tile ? 40u * 128u : 0u) + ks * 32u),
+                              umma_desc_sw128(bbase + (uint32_t)c * 8192u + ks * 32u), id32, 1u);
+            umma_commit(m2bar);
+            if (c + 2 < NCH) {
+                mbar_wait(m1bar, (uint32_t)(c & 1));  // MMA1(c) has read stage st
+                mbar_arrive_expect_tx(&ybar[st], (uint32_t)Ap3::chunk);
+                tma_load_3d(ys, &ymap, 32 * (c + 2), fb * kSc, slot * kSym, &ybar[st]);
+            }
+        }
+    }
+    mbar_wait(m2bar, (uint32_t)((NCH - 1) & 1));
+    tc_fence_after();
+    // epilogue: tile 0 rows 0-127 (all warps), tile 1 rows 128-167 (= TMEM lanes 88-127 of tile 1)
+    constexpr int kRec = NL * QM * LlrTraits<LT>::bytes;
+    const bool zf = !(a.sigma2 > 0.f);
+    const float ia = rsqrtf((float)qam_norm(QM));
+#pragma unroll 1
+    for (int tile = 0; tile < 2; ++tile) {
+        if (tile == 1 && warp < 2) break;
+        uint32_t hv[32], lv[32];
+        const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16) + 64u * tile;
+        tmem_ld32(taddr, hv);
+        tmem_ld32(taddr + 32u, lv);
+        const int row = (tile ? 40 : 0) + 32 * warp + lane;
+        if (tile == 1 && row < 128) continue;
+        const int s = row / kSc, f = row % kSc;
+        const size_t re = (size_t)(slot * kSym + s) * a.n_sc + fb * kSc + f;
+        float2 x[NL];
+#pragma unroll
+        for (int k = 0; k < NL; ++k)
+            x[k] = make_float2(__uint_as_float(hv[k]) + __uint_as_float(lv[k]),
+                               __uint_as_float(hv[16 + k]) + __uint_as_float(lv[16 + k]));
+        if (a.llr) {
+            float v[NL * QM];
+            uint32_t wd[(kRec + 3) / 4];
+            if (!zf) {
+#pragma unroll
+                for (int k = 0; k < NL; ++k) demap_layer<QM, false, LT>(x[k], sSlope[k], v + k * QM);
+                pack_llr<LT, NL * QM, false>(v, wd);
+            } else {
+#pragma unroll
+                for (int k = 0; k < NL; ++k) demap_layer<QM, true, LT>(x[k], sSlope[k], v + k * QM);
+                pack_llr<LT, NL * QM, true>(v, wd);
+            }
+            store_bytes<kRec>((char*)a.llr + re * kRec, wd);
+        }
+        if (a.xhat) {
+#pragma unroll
+            for (int k = 0; k < NL; ++k) a.xhat[re * NL + k] = make_float2(x[k].x * ia, x[k].y * ia);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+}
+
+template <int NR, int NL, int QM, int LT>
+cudaError_t launch_ap3(const DetectArgs& a, cudaStream_t s) {
+    if (a.n_units <= 0) return cudaSuccess;
+    auto enc = tensor_map_encoder();
+    if (!enc) return cudaErrorNotSupported;
+    CUtensorMap ymap;
+    const cuuint64_t gdim[3] = {(cuuint64_t)(2 * NR), (cuuint64_t)a.n_sc, (cuuint64_t)a.n_sym};
+    const cuuint64_t gstride[2] = {(cuuint64_t)NR * 8, (cuuint64_t)a.n_sc * NR * 8};
+    const cuuint32_t box[3] = {32, (cuuint32_t)kSc, (cuuint32_t)kSym};
+    const cuuint32_t estride[3] = {1, 1, 1};
+    if (enc(&ymap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float2*>(a.y), gdim, gstride, box, estride,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    constexpr int UPB = 4;
+    cudaError_t e = launch_kernel(k_big_setup<NR, NL, QM, UPB>, dim3((unsigned)((a.n_units + UPB - 1) / UPB)),
+                                  dim3(32 * UPB), UPB * SetupSmem<NR, NL>::per_unit, s, a.overlap, a);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)a.n_units);
+    cfg.blockDim = dim3(Ap3::THREADS);
+    cfg.dynamicSmemBytes = Ap3::total;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = a.overlap ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k_big_apply3<NR, NL, QM, LT>, a, ymap);
+}
+
+template <int NR, int NL, int QM, int LT>
+cudaError_t prepare_ap3() {
+    cudaError_t e = cudaFuncSetAttribute(k_big_setup<NR, NL, QM, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(4 * SetupSmem<NR, NL>::per_unit));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_big_apply3<NR, NL, QM, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)Ap3::total);
+}
+
 template <int NR, int NL, int QM, int LT>
 cudaError_t launch_tc3(const DetectArgs& a, cudaStream_t s) {
     if (a.n_units <= 0) return cudaSuccess;
@@ -1520,8 +1752,10 @@ cudaError_t prepare() {
     }
 
 const KernelEntry kEntries[] = {
-    BIG_ENTRY("big_64x16_q6_i8", 64, 16, 6, kLlrI8),  // C5 (SIMT GEMM; currently the fastest)
-    BIGAP2_ENTRY("big2_64x16_q6_i8", 64, 16, 6, kLlrI8),
+    BIGAP2_ENTRY("big2_64x16_q6_i8", 64, 16, 6, kLlrI8),  // C5 (K-streamed SIMT GEMM; currently the fastest)
+    BIG_ENTRY("big_64x16_q6_i8", 64, 16, 6, kLlrI8),
+    KernelEntry{"big3_64x16_q6_i8", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap3<64, 16, 6, kLlrI8>,
+                prepare_ap3<64, 16, 6, kLlrI8>, workspace<64, 16>},
     BIGTC3_ENTRY("bigtc3_64x16_q6_i8", 64, 16, 6, kLlrI8),
     BIGTC2_ENTRY("bigtc2_64x16_q6_i8", 64, 16, 6, kLlrI8),  // tensor cores, warp-specialised
     BIGTC_ENTRY("bigtc_64x16_q6_i8", 64, 16, 6, kLlrI8),
