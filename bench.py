@@ -37,6 +37,9 @@ from paper_2510_07843_b200 import shard, synth  # noqa: E402
 
 METRIC = "MIMO-detected REs/s per B200 (LLR Gbit/s alongside) vs roofline"
 FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
+FALLBACK_BF16_TFLOPS = 2250.0  # B200_PROFILING.md nominal dense bf16
+TF32_PER_BF16 = 1.1 / 2.25   # B200_PROFILING.md nominal dense tf32 / bf16
+TC_KERNELS = ("big3_", "big4_")  # kernels whose row a6 runs on tcgen05 (R21)
 
 
 def parse():
@@ -75,8 +78,9 @@ def measured_peaks() -> dict:
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return dict(hbm_gbs=float(d["hbm_gbs"]), src="measured", sm_max_mhz=float(d.get("sm_max_mhz", 1965.0)))
-    return dict(hbm_gbs=FALLBACK_HBM_GBS, src="fallback", sm_max_mhz=1965.0)
+        return dict(hbm_gbs=float(d["hbm_gbs"]), src="measured", sm_max_mhz=float(d.get("sm_max_mhz", 1965.0)),
+                    bf16_tflops=float(d.get("bf16_tflops", FALLBACK_BF16_TFLOPS)))
+    return dict(hbm_gbs=FALLBACK_HBM_GBS, src="fallback", sm_max_mhz=1965.0, bf16_tflops=FALLBACK_BF16_TFLOPS)
 
 
 def ncu_traffic(k) -> float | None:
@@ -350,17 +354,29 @@ def run_ours(args, k):
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
     fp32_tflops = n_sm * 128 * 2 * peaks["sm_max_mhz"] * 1e6 / 1e12
     t_hbm = b["total"] / (peaks["hbm_gbs"] * 1e9)
-    t_alu = fl["total"] / (fp32_tflops * 1e12)
-    if t_alu > t_hbm:
-        roof = {"bound": "alu", "achieved": fl["total"] / step_s / 1e12, "peak": fp32_tflops, "unit": "TFLOP/s",
-                "frac": (fl["total"] / step_s / 1e12) / fp32_tflops, "algorithmic_flops_per_step": fl["total"],
+    # Which pipe runs row a6 (x~ = W~ y): tensor-core kernels (3-pass TF32, R21) move the
+    # apply flops off the FP32 SIMT pipe, so their bound is max(HBM, SIMT setup+demap, TF32 tensor).
+    tensor_apply = plan.kernel_name.startswith(TC_KERNELS)
+    simt_flops = fl["setup"] + fl["demap"] if tensor_apply else fl["total"]
+    t_alu = simt_flops / (fp32_tflops * 1e12)
+    tf32_tflops = peaks["bf16_tflops"] * TF32_PER_BF16
+    t_tc = 3 * fl["apply"] / (tf32_tflops * 1e12) if tensor_apply else 0.0
+    if t_alu > t_hbm and t_alu >= t_tc:
+        roof = {"bound": "alu", "achieved": simt_flops / step_s / 1e12, "peak": fp32_tflops, "unit": "TFLOP/s",
+                "frac": (simt_flops / step_s / 1e12) / fp32_tflops, "algorithmic_flops_per_step": simt_flops,
                 "peak_src": f"derived: {n_sm} SMs x 128 FP32 lanes x 2 x {peaks['sm_max_mhz']:.0f} MHz"}
+    elif t_tc > t_hbm:
+        roof = {"bound": "tensor", "achieved": 3 * fl["apply"] / step_s / 1e12, "peak": tf32_tflops,
+                "unit": "TFLOP/s", "frac": (3 * fl["apply"] / step_s / 1e12) / tf32_tflops,
+                "peak_src": "measured bf16 x nominal TF32/BF16 ratio (B200_PROFILING.md)"}
     else:
         ach = b["total"] / step_s / 1e9
         roof = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": ach / peaks["hbm_gbs"], "peak_src": peaks["src"] + " (MEASURED_PEAKS.json hbm_gbs)"}
     roof.update({"traffic": ncu_traffic(k), "algorithmic_bytes_per_step": b["total"],
-                 "t_roof_us": max(t_hbm, t_alu) * 1e6, "step_us": step_s * 1e6,
+                 "t_roof_us": max(t_hbm, t_alu, t_tc) * 1e6, "step_us": step_s * 1e6,
+                 "apply_pipe": "tcgen05 kind::tf32 x3 (R21)" if tensor_apply else "FP32 SIMT",
+                 "t_hbm_us": t_hbm * 1e6, "t_simt_us": t_alu * 1e6, "t_tensor_us": t_tc * 1e6,
                  "launches_per_step": plan.launches_per_call})
     achieved = b["total"] / per_launch_s / 1e9
     clocks = sampler.result()
@@ -412,7 +428,7 @@ def run_ours(args, k):
         "config": cfg,
         "llr_gbit_s": value * w.n_layers * w.qm / 1e9,
         "roofline": dict(roof, serialised_call_us=single_us,
-                         serialised_frac=max(t_hbm, t_alu) / (single_us * 1e-6)),
+                         serialised_frac=max(t_hbm, t_alu, t_tc) / (single_us * 1e-6)),
         "cpu_baseline": cpu,
         "e2e": e2e,
         "clocks": clocks,

@@ -1652,6 +1652,308 @@ cudaError_t prepare_ap3() {
                                 (int)Ap3::total);
 }
 
+// ------------------------------------------------------------------------
+// k_big_apply4: the k_big_apply3 computation as a persistent, warp-specialised
+// pipeline (one CTA per SM, 288 threads) so that loads, tensor-core passes,
+// y_lo conversion and the demap epilogue of different chunks / units overlap:
+//   warp 8 lane 0  control: TMA producer (y chunks S = 4 stages ahead, W~ of
+//                  unit i+2) and single-thread tcgen05.mma issuer;
+//   warps 0-3      converters: B(i) from W~ (hi/lo, double-buffered), y -> y_lo
+//                  per chunk (2 y_lo buffers);
+//   warps 4-7      epilogue: TMEM (2 accumulator buffers x 128 columns) ->
+//                  x~ -> exact max-log demap -> LLR stores.
+// Chunk g = 4 i + c of the CTA's i-th unit (u = blockIdx.x + i gridDim.x).
+// mbarrier k-th completion is waited with parity k & 1.
+struct Ap4 {
+    static constexpr int S = 4;                              // y stages
+    static constexpr size_t chunk = (size_t)kRe * 128;       // 21504
+    static constexpr size_t y0 = 0;
+    static constexpr size_t ylo = S * chunk;                 // 2 buffers
+    static constexpr size_t B = ylo + 2 * chunk;             // 2 x 32 KiB (1024-aligned)
+    static constexpr size_t bset = 4 * 64 * 128;
+    static constexpr size_t wraw = B + 2 * bset;             // 2 x (W~ + slopes)
+    static constexpr size_t wstride = 8320;
+    static constexpr size_t wbytes = 64 * 16 * 8 + 16 * 4;   // 8256
+    static constexpr size_t slope = wraw + 2 * wstride;      // [2][16] float
+    static constexpr size_t bars = slope + 128;              // mbarriers
+    static constexpr int NBAR = 2 * S + 2 * 2 + 2 * 5;       // yfull, yfree | ylofull, ylofree | wfull, bready, accfull, tfree, spare
+    static constexpr size_t tslot = bars + NBAR * 8;
+    static constexpr size_t total = tslot + 16 + 1024;
+    static constexpr int THREADS = 288;
+};
+static_assert(Ap4::B % 1024 == 0 && Ap4::ylo % 1024 == 0, "UMMA operand alignment");
+
+template <int NR, int NL, int QM, int LT>
+__global__ void __launch_bounds__(Ap4::THREADS, 1) k_big_apply4(DetectArgs a, const __grid_constant__ CUtensorMap ymap) {
+    static_assert(NL == 16 && NR == 64, "k_big_apply4: 64 x 16");
+    constexpr int WS = BigWs<NR, NL>::stride;
+    constexpr int S = Ap4::S;
+    extern __shared__ unsigned char smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    unsigned char* g = smem_raw + (base - raw);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(g + Ap4::bars);
+    uint64_t* yfull = bar;            // [S]  TMA tx
+    uint64_t* yfree = bar + S;        // [S]  MMA1 commit + converters (count 2)
+    uint64_t* ylofull = bar + 2 * S;  // [2]  converters
+    uint64_t* ylofree = ylofull + 2;  // [2]  MMA2 commit
+    uint64_t* wfull = ylofree + 2;    // [2]  W~ bulk copy tx
+    uint64_t* bready = wfull + 2;     // [2]  converters
+    uint64_t* accfull = bready + 2;   // [2]  commit after the unit's last MMA
+    uint64_t* tfree = accfull + 2;    // [2]  epilogue done with the TMEM buffer
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(g + Ap4::tslot);
+    float* sslope = reinterpret_cast<float*>(g + Ap4::slope);
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const long long u0 = blockIdx.x, du = gridDim.x;
+    const long long n_my = u0 < a.n_units ? (a.n_units - u0 + du - 1) / du : 0;
+    const long long G = 4 * n_my;
+
+    pdl_launch_dependents();
+    if (t == 0) {
+        for (int i = 0; i < S; ++i) {
+            mbar_init(&yfull[i], 1);
+            mbar_init(&yfree[i], 2);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&ylofull[i], 1);
+            mbar_init(&ylofree[i], 1);
+            mbar_init(&wfull[i], 1);
+            mbar_init(&bready[i], 1);
+            mbar_init(&accfull[i], 1);
+            mbar_init(&tfree[i], 1);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 8) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tslot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+
+    auto issue_y = [&](long long gg) {
+        const long long uu = u0 + (gg >> 2) * du;
+        const int slot = (int)(uu / a.n_fb), fb = (int)(uu % a.n_fb), st = (int)(gg % S);
+        mbar_arrive_expect_tx(&yfull[st], (uint32_t)Ap4::chunk);
+        tma_load_3d(base + (uint32_t)(Ap4::y0 + st * Ap4::chunk), &ymap, 32 * (int)(gg & 3), fb * kSc, slot * kSym,
+                    &yfull[st]);
+    };
+    auto issue_w = [&](long long i) {
+        const int b = (int)(i & 1);
+        mbar_arrive_expect_tx(&wfull[b], (uint32_t)Ap4::wbytes);
+        bulk_g2s(g + Ap4::wraw + b * Ap4::wstride, reinterpret_cast<const float*>(a.ws) + (u0 + i * du) * WS,
+                 (uint32_t)Ap4::wbytes, &wfull[b]);
+    };
+
+    if (warp == 8) {
+        // ================= control: TMA producer + MMA issuer =================
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ymap)) : "memory");
+            for (long long gg = 0; gg < S && gg < G; ++gg) issue_y(gg);
+            pdl_wait();  // W~ of this call's setup kernel is complete
+            for (long long i = 0; i < 2 && i < n_my; ++i) issue_w(i);
+            constexpr uint32_t id64 = (1u << 4) | (2u << 7) | (2u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+            constexpr uint32_t id32 = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+#pragma unroll 1
+            for (long long i = 0; i < n_my; ++i) {
+                const int b = (int)(i & 1);
+                mbar_wait(&bready[b], (uint32_t)((i >> 1) & 1));
+                if (i + 2 < n_my) issue_w(i + 2);  // W~ buffer b was consumed by B(i)
+                if (i >= 2) mbar_wait(&tfree[b], (uint32_t)(((i >> 1) + 1) & 1));
+                const uint32_t acc = tmem + 128u * (uint32_t)b;
+                const uint32_t bb = base + (uint32_t)(Ap4::B + b * Ap4::bset);
+#pragma unroll 1
+                for (int c = 0; c < 4; ++c) {
+                    const long long gg = 4 * i + c;
+                    const int st = (int)(gg % S), lb = (int)(gg & 1);
+                    const uint32_t ys = base + (uint32_t)(Ap4::y0 + st * Ap4::chunk);
+                    mbar_wait(&yfull[st], (uint32_t)((gg / S) & 1));
+                    tc_fence_after();
+#pragma unroll
+                    for (int tile = 0; tile < 2; ++tile)
+#pragma unroll
+                        for (int ks = 0; ks < 4; ++ks)
+                            umma_tf32(acc + 64u * tile, umma_desc_sw128(ys + (tile ? 40u * 128u : 0u) + ks * 32u),
+                                      umma_desc_sw128(bb + (uint32_t)c * 8192u + ks * 32u), id64, (c | ks) ? 1u : 0u);
+                    umma_commit(&yfree[st]);
+                    mbar_wait(&ylofull[lb], (uint32_t)((gg >> 1) & 1));
+                    tc_fence_after();
+                    const uint32_t yl = base + (uint32_t)(Ap4::ylo + lb * Ap4::chunk);
+#pragma unroll
+                    for (int tile = 0; tile < 2; ++tile)
+#pragma unroll
+                        for (int ks = 0; ks < 4; ++ks)
+                            umma_tf32(acc + 64u * tile, umma_desc_sw128(yl + (tile ? 40u * 128u : 0u) + ks * 32u),
+                                      umma_desc_sw128(bb + (uint32_t)c * 8192u + ks * 32u), id32, 1u);
+                    umma_commit(&ylofree[lb]);
+                    if (c == 3) umma_commit(&accfull[b]);
+                    if (gg + S < G) {  // refill stage st once MMA1(gg) and the conversion of gg are done
+                        mbar_wait(&yfree[st], (uint32_t)((gg / S) & 1));
+                        issue_y(gg + S);
+                    }
+                }
+            }
+        }
+    } else if (warp < 4) {
+        // ================= converters =================
+        const int tc = t;  // 0..127
+#pragma unroll 1
+        for (long long i = 0; i < n_my; ++i) {
+            const int b = (int)(i & 1);
+            mbar_wait(&wfull[b], (uint32_t)((i >> 1) & 1));
+            if (i >= 2) mbar_wait(&tfree[b], (uint32_t)(((i >> 1) + 1) & 1));  // B(i-2) and slopes(i-2) no longer used
+            {
+                const float2* sW = reinterpret_cast<const float2*>(g + Ap4::wraw + b * Ap4::wstride);
+                const int n = tc >> 2, kt = tc & 3, kk = n & 15;
+                const bool im_row = n >= 16;
+                float* kb = reinterpret_cast<float*>(g + Ap4::B + b * Ap4::bset + (size_t)kt * 64 * 128);
+#pragma unroll
+                for (int c = 0; c < 8; ++c) {
+                    const int r0 = 16 * kt + 2 * c;
+                    const float2 w0 = sW[r0 * NL + kk], w1 = sW[(r0 + 1) * NL + kk];
+                    const float4 v = im_row ? make_float4(w0.y, w0.x, w1.y, w1.x) : make_float4(w0.x, -w0.y, w1.x, -w1.y);
+                    const float4 lo = make_float4(v.x - tf32_trunc(v.x), v.y - tf32_trunc(v.y), v.z - tf32_trunc(v.z),
+                                                  v.w - tf32_trunc(v.w));
+                    *reinterpret_cast<float4*>(kb + n * 32 + ((c ^ (n & 7)) << 2)) = v;
+                    *reinterpret_cast<float4*>(kb + (n + 32) * 32 + ((c ^ (n & 7)) << 2)) = lo;
+                }
+                if (tc < NL) sslope[b * 16 + tc] = reinterpret_cast<const float*>(sW + 64 * NL)[tc];
+            }
+            fence_proxy_async();
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (tc == 0) mbar_arrive(&bready[b]);
+#pragma unroll 1
+            for (int c = 0; c < 4; ++c) {
+                const long long gg = 4 * i + c;
+                const int st = (int)(gg % S), lb = (int)(gg & 1);
+                mbar_wait(&yfull[st], (uint32_t)((gg / S) & 1));
+                if (gg >= 2) mbar_wait(&ylofree[lb], (uint32_t)(((gg >> 1) + 1) & 1));
+                const float4* src = reinterpret_cast<const float4*>(g + Ap4::y0 + st * Ap4::chunk);
+                float4* dst = reinterpret_cast<float4*>(g + Ap4::ylo + lb * Ap4::chunk);
+                constexpr int n4 = (int)(Ap4::chunk / 16);
+#pragma unroll 4
+                for (int q = tc; q < n4; q += 128) {
+                    float4 v = src[q];
+                    v.x -= tf32_trunc(v.x);
+                    v.y -= tf32_trunc(v.y);
+                    v.z -= tf32_trunc(v.z);
+                    v.w -= tf32_trunc(v.w);
+                    dst[q] = v;
+                }
+                fence_proxy_async();
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (tc == 0) {
+                    mbar_arrive(&ylofull[lb]);
+                    mbar_arrive(&yfree[st]);
+                }
+            }
+        }
+    } else {
+        // ================= epilogue =================
+        const int we = warp - 4;  // TMEM lane quadrant
+        constexpr int kRec = NL * QM * LlrTraits<LT>::bytes;
+        const bool zf = !(a.sigma2 > 0.f);
+        const float ia = rsqrtf((float)qam_norm(QM));
+#pragma unroll 1
+        for (long long i = 0; i < n_my; ++i) {
+            const int b = (int)(i & 1);
+            const long long u = u0 + i * du;
+            const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);
+            mbar_wait(&accfull[b], (uint32_t)((i >> 1) & 1));
+            tc_fence_after();
+#pragma unroll 1
+            for (int tile = 0; tile < 2; ++tile) {
+                if (tile == 1 && we < 2) break;
+                uint32_t hv[32], lv[32];
+                const uint32_t taddr = tmem + ((uint32_t)(32 * we) << 16) + 128u * (uint32_t)b + 64u * tile;
+                tmem_ld32(taddr, hv);
+                tmem_ld32(taddr + 32u, lv);
+                const int row = (tile ? 40 : 0) + 32 * we + lane;
+                if (tile == 1 && row < 128) continue;
+                const int s = row / kSc, f = row % kSc;
+                const size_t re = (size_t)(slot * kSym + s) * a.n_sc + fb * kSc + f;
+                float2 x[NL];
+#pragma unroll
+                for (int k = 0; k < NL; ++k)
+                    x[k] = make_float2(__uint_as_float(hv[k]) + __uint_as_float(lv[k]),
+                                       __uint_as_float(hv[16 + k]) + __uint_as_float(lv[16 + k]));
+                if (a.llr) {
+                    float v[NL * QM];
+                    uint32_t wd[(kRec + 3) / 4];
+                    if (!zf) {
+#pragma unroll
+                        for (int k = 0; k < NL; ++k) demap_layer<QM, false, LT>(x[k], sslope[b * 16 + k], v + k * QM);
+                        pack_llr<LT, NL * QM, false>(v, wd);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < NL; ++k) demap_layer<QM, true, LT>(x[k], sslope[b * 16 + k], v + k * QM);
+                        pack_llr<LT, NL * QM, true>(v, wd);
+                    }
+                    store_bytes<kRec>((char*)a.llr + re * kRec, wd);
+                }
+                if (a.xhat) {
+#pragma unroll
+                    for (int k = 0; k < NL; ++k) a.xhat[re * NL + k] = make_float2(x[k].x * ia, x[k].y * ia);
+                }
+            }
+            tc_fence_before();
+            asm volatile("bar.sync 2, 128;" ::: "memory");
+            if (t == 128) mbar_arrive(&tfree[b]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+template <int NR, int NL, int QM, int LT>
+cudaError_t launch_ap4(const DetectArgs& a, cudaStream_t s) {
+    if (a.n_units <= 0) return cudaSuccess;
+    static int n_sm = 0;
+    if (!n_sm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    auto enc = tensor_map_encoder();
+    if (!enc) return cudaErrorNotSupported;
+    CUtensorMap ymap;
+    const cuuint64_t gdim[3] = {(cuuint64_t)(2 * NR), (cuuint64_t)a.n_sc, (cuuint64_t)a.n_sym};
+    const cuuint64_t gstride[2] = {(cuuint64_t)NR * 8, (cuuint64_t)a.n_sc * NR * 8};
+    const cuuint32_t box[3] = {32, (cuuint32_t)kSc, (cuuint32_t)kSym};
+    const cuuint32_t estride[3] = {1, 1, 1};
+    if (enc(&ymap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float2*>(a.y), gdim, gstride, box, estride,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    constexpr int UPB = 4;
+    cudaError_t e = launch_kernel(k_big_setup<NR, NL, QM, UPB>, dim3((unsigned)((a.n_units + UPB - 1) / UPB)),
+                                  dim3(32 * UPB), UPB * SetupSmem<NR, NL>::per_unit, s, a.overlap, a);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(a.n_units < n_sm ? a.n_units : n_sm));
+    cfg.blockDim = dim3(Ap4::THREADS);
+    cfg.dynamicSmemBytes = Ap4::total;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = a.overlap ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k_big_apply4<NR, NL, QM, LT>, a, ymap);
+}
+
+template <int NR, int NL, int QM, int LT>
+cudaError_t prepare_ap4() {
+    cudaError_t e = cudaFuncSetAttribute(k_big_setup<NR, NL, QM, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(4 * SetupSmem<NR, NL>::per_unit));
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(k_big_apply4<NR, NL, QM, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)Ap4::total);
+}
+
 template <int NR, int NL, int QM, int LT>
 cudaError_t launch_tc3(const DetectArgs& a, cudaStream_t s) {
     if (a.n_units <= 0) return cudaSuccess;
@@ -1756,6 +2058,8 @@ const KernelEntry kEntries[] = {
     BIG_ENTRY("big_64x16_q6_i8", 64, 16, 6, kLlrI8),
     KernelEntry{"big3_64x16_q6_i8", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap3<64, 16, 6, kLlrI8>,
                 prepare_ap3<64, 16, 6, kLlrI8>, workspace<64, 16>},
+    KernelEntry{"big4_64x16_q6_i8", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8>,
+                prepare_ap4<64, 16, 6, kLlrI8>, workspace<64, 16>},
     BIGTC3_ENTRY("bigtc3_64x16_q6_i8", 64, 16, 6, kLlrI8),
     BIGTC2_ENTRY("bigtc2_64x16_q6_i8", 64, 16, 6, kLlrI8),  // tensor cores, warp-specialised
     BIGTC_ENTRY("bigtc_64x16_q6_i8", 64, 16, 6, kLlrI8),
