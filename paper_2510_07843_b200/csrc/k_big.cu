@@ -1,21 +1,23 @@
 // k_big.cu -- massive-MIMO per-PRB detector (C5: 64 rx x 16 layers, 64-QAM,
 // int8, H per PRB). The per-RE filter x~ = W~ y is a dense complex contraction
-// (16 x 64 per RE, 1024 cMAC): C5 is FP32-bound, not HBM-bound (SURVEY.md
-// §8(d)), so the kernels are organised around the FFMA pipe.
+// (16 x 64 per RE, 1024 cMAC): on the FP32 SIMT pipe C5 is FP32-bound (SURVEY.md
+// §8(d)); on the tensor cores (3-pass TF32, reading R21) it becomes HBM-bound.
 //
 //   k_big_setup (rows a2-a5), one warp per PRB-unit, warp-synchronous, fp32
-//     (reading R18; cond(G) <= ~10 on C5): G = H^H H + s2 I (half a row per
-//     lane, broadcast 128-bit H reads), Cholesky with lane k holding row k
-//     (pivots and columns by __shfl_sync; guard R17), X = L^-1 column per lane,
-//     row k of G^-1 = X^H X per lane, W~ = diag(sqrt(norm)/mu) G^-1 H^H (lane
-//     (k, half) covers half the antennas), written to the plan workspace as
-//     [unit][r][k] plus slopes.
-//   k_big_apply (rows a6-a7), one CTA per PRB-unit: the unit's 168 y vectors
-//     are bulk-copied into shared memory at a padded 528-byte stride
-//     (conflict-free 128-bit reads) and W~ [r][k] next to them; thread
-//     (RE pair, layer half) accumulates its 2 x 8 complex outputs over r with
-//     128-bit shared loads (register-tiled SIMT GEMM, 12.8 FFMA per load),
-//     then demaps its 16 layer-REs and stores 48 contiguous LLR bytes per RE.
+//     (reading R18; cond(G) <= ~10 on C5): H by one bulk copy, G = H^H H + s2 I
+//     (half a row per lane, broadcast 128-bit H reads), rows of G gathered by
+//     shuffles, Cholesky with lane k holding row k (pivots and columns by
+//     __shfl_sync; guard R17), X = L^-1 column per lane, row k of G^-1 = X^H X
+//     per lane, W~ = diag(sqrt(norm)/mu) G^-1 H^H (lane (k, half) covers half the
+//     antennas), written to the plan workspace as [unit][r][k] plus slopes.
+//   Apply kernels (rows a6-a7), all reading W~ from the workspace:
+//   k_big_apply4 (C5 default): persistent, warp-specialised tcgen05 pipeline
+//     (TMA y chunks, single-thread MMA issue, converter and epilogue warps).
+//   k_big_apply3: the same tensor-core computation, one CTA per unit.
+//   k_big_apply2: SIMT, K-streamed TMA chunks, 4 x 4 complex register tile.
+//   k_big_apply (other shapes / LLR types): SIMT, CTA per PRB-unit, the unit's
+//     168 y vectors bulk-copied at a padded 528-byte stride, thread (RE pair,
+//     layer half) accumulates 2 x 8 complex outputs.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -324,41 +326,12 @@ __global__ void __launch_bounds__(kRe) k_big_apply(DetectArgs a) {
 }
 
 // ------------------------------------------------------------------------
-// k_big_tc: the same a6-a7 on the 5th-gen tensor cores (tcgen05, kind::tf32).
-//
-// Per PRB-unit the filter is a real GEMM  X^T[168 x 32] = Y^T[168 x 128] B[128 x 32]
-// with y rows (64 complex = 128 fp32, interleaved re/im) as the K-major A
-// operand and B = [[Wr^T, Wi^T], [-Wi^T, Wr^T]] (rows interleaved re/im, built
-// per unit in shared memory from W~). fp32 accuracy from TF32 units by the
-// 3-pass split A B = A_hi B_hi + A_hi B_lo + A_lo B_hi: the tensor core reads an
+// tcgen05 / TMA building blocks for the tensor-core apply kernels (k_big_apply3/4).
+// fp32-accurate products from TF32 units (reading R21): the tensor core reads an
 // fp32 operand as TF32 (low 13 mantissa bits ignored, i.e. hi = trunc(x)), so
-// pass 1 uses (y, B), pass 2 (y, B_lo) with B_lo = B - trunc(B), and pass 3
-// (y_lo, B) after y is replaced in place by y - trunc(y). Dropped: lo*lo and
-// the truncation of the lo parts, ~2^-20 relative per product (R21).
-//
-// Persistent CTA (128 threads, one per SM). Shared memory holds two y stages
-// (cp.async with a manual 128-byte swizzle = the canonical SWIZZLE_128B
-// K-major UMMA layout, 4 K-tiles x 168 rows x 128 B each), B and B_lo
-// (4 K-tiles x 32 rows x 128 B). The next unit's y streams in while the current
-// one is computed. Two M=128 MMA tiles cover the 168 RE rows (rows 0-127 and
-// 40-167) with N=32 accumulator columns each in TMEM (64 columns allocated).
-// Epilogue: tcgen05.ld 32x32b.x32 gives each thread one RE's 32 outputs
-// (TMEM lane = RE row), exact max-log demap, 96-byte LLR record stores.
-template <int NR, int NL>
-struct TcSmem {
-    static constexpr int ROWS = kRe;                                       // 168
-    static constexpr int KT = NR * 2 / 32;                                 // K-tiles of 32 fp32 (128 B)
-    static constexpr size_t ktile = (size_t)ROWS * 128;                    // 21504 = 21 KiB
-    static constexpr size_t ystage = (size_t)KT * ktile;                   // 86016
-    static constexpr size_t btile = (size_t)2 * NL * 128;                  // 32 rows x 128 B
-    static constexpr size_t y0 = 0;
-    static constexpr size_t B = 2 * ystage;
-    static constexpr size_t Blo = B + (size_t)KT * btile;
-    static constexpr size_t bars = Blo + (size_t)KT * btile;               // up to 8 mbarriers
-    static constexpr size_t tmem = bars + 64;
-    static constexpr size_t total = tmem + 16 + 1024;                      // + alignment slack
-};
-
+// A B = A_hi B_hi + A_hi B_lo + A_lo B_hi with B_lo = B - trunc(B) and
+// A_lo = A - trunc(A); the dropped lo*lo term and the truncation of the lo
+// parts are ~2^-20 relative per product.
 __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
     // start address >> 4 | LBO (unused for swizzled K-major) = 1 | SBO = 1024 B | version 1 | SWIZZLE_128B
     return (uint64_t)((saddr & 0x3FFFFu) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
@@ -377,26 +350,6 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
-}
-__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
-    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-// bounded wait: a descriptor bug must not hang the GPU
-__device__ __forceinline__ void mbar_wait_bounded(uint64_t* bar, uint32_t parity) {
-    uint32_t ok = 0;
-    for (long long it = 0; it < (1ll << 26); ++it) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(ok)
-            : "r"(smem_u32(bar)), "r"(parity)
-            : "memory");
-        if (ok) return;
-    }
-    __trap();
-}
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
@@ -415,484 +368,12 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t* r) {
 }
 __device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
-constexpr int kTcThreads = 256;  // 8 warps: warps w and w+4 share a TMEM lane window
-
-// y rows of unit u -> stage (warp w moves rows w, w+8, ...; lane = 16-byte chunk)
-template <int NR, int NL>
-__device__ __forceinline__ void tc_issue_y(const DetectArgs& a, uint32_t stage, long long u, uint64_t* bar) {
-    using SM = TcSmem<NR, NL>;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);
-    const int kt = lane >> 3, cc = lane & 7;
-#pragma unroll 2
-    for (int i = warp; i < SM::ROWS; i += kTcThreads / 32) {
-        const int s = i / kSc, f = i % kSc;
-        const char* src = reinterpret_cast<const char*>(a.y + ((size_t)(slot * kSym + s) * a.n_sc + fb * kSc + f) * NR) +
-                          lane * 16;
-        cp_async16(stage + kt * (uint32_t)SM::ktile + i * 128u + ((cc ^ (i & 7)) << 4), src);
-    }
-    cp_async_arrive(bar);
-}
-
-template <int NR, int NL, int QM, int LT>
-__global__ void __launch_bounds__(kTcThreads, 1) k_big_tc(DetectArgs a) {
-    static_assert(NL == 16 && NR == 64, "k_big_tc: 64 x 16");
-    using SM = TcSmem<NR, NL>;
-    constexpr int KT = SM::KT;
-    constexpr int WS = BigWs<NR, NL>::stride;
-    extern __shared__ unsigned char smem_raw[];
-    const uint32_t raw = smem_u32(smem_raw);
-    const uint32_t base = (raw + 1023u) & ~1023u;
-    unsigned char* gbase = smem_raw + (base - raw);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + SM::bars);  // [0],[1] y stages, [2] mma
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + SM::tmem);
-    float* fB = reinterpret_cast<float*>(gbase + SM::B);
-    float* fBlo = reinterpret_cast<float*>(gbase + SM::Blo);
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-
-    pdl_launch_dependents();
-    if (t == 0) {
-        mbar_init(&bars[0], kTcThreads);
-        mbar_init(&bars[1], kTcThreads);
-        mbar_init(&bars[2], 1);
-        fence_mbar_init();
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(smem_u32(tmem_slot)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-
-    // instruction descriptor: D f32, A/B tf32, K-major A and B, N = 32, M = 128
-    constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
-    const float norm = (float)qam_norm(QM);
-    const bool zf = !(a.sigma2 > 0.f);
-    long long u = blockIdx.x;
-    if (u < a.n_units) tc_issue_y<NR, NL>(a, base + SM::y0, u, &bars[0]);
-    pdl_wait();  // W~ of this call's setup kernel is complete
-    uint32_t mma_phase = 0;
-#pragma unroll 1
-    for (int it = 0; u < a.n_units; ++it, u += gridDim.x) {
-        const int st = it & 1;
-        const uint32_t ys = base + SM::y0 + st * (uint32_t)SM::ystage;
-        float* fy = reinterpret_cast<float*>(gbase + SM::y0 + st * SM::ystage);
-        const long long un = u + gridDim.x;
-        if (un < a.n_units) tc_issue_y<NR, NL>(a, base + SM::y0 + (st ^ 1) * (uint32_t)SM::ystage, un, &bars[st ^ 1]);
-        // B, B_lo from W~ [r][k]: thread -> row n = t / 8 (xr_l or xi_l), K-tile kt, 4 chunks (8 antennas)
-        const float* wsu = reinterpret_cast<const float*>(a.ws) + u * WS;
-        {
-            const int n = t >> 3, kt = (t >> 1) & 3, c0 = (t & 1) * 4;
-            const int l = n & 15;
-            const bool im_row = n >= 16;
-#pragma unroll
-            for (int cq = 0; cq < 4; ++cq) {  // chunk c = antennas r0, r0+1 (4 floats: yr, yi, yr, yi)
-                const int c = c0 + cq;
-                const int r0 = kt * 16 + 2 * c;
-                const float2 w0 = *reinterpret_cast<const float2*>(wsu + 2 * (r0 * NL + l));
-                const float2 w1 = *reinterpret_cast<const float2*>(wsu + 2 * ((r0 + 1) * NL + l));
-                float4 v;
-                if (!im_row) v = make_float4(w0.x, -w0.y, w1.x, -w1.y);   // xr += Wr yr - Wi yi
-                else v = make_float4(w0.y, w0.x, w1.y, w1.x);             // xi += Wi yr + Wr yi
-                const float4 lo = make_float4(v.x - tf32_trunc(v.x), v.y - tf32_trunc(v.y), v.z - tf32_trunc(v.z),
-                                              v.w - tf32_trunc(v.w));
-                const int off = kt * (int)(SM::btile / 4) + n * 32 + ((c ^ (n & 7)) << 2);
-                *reinterpret_cast<float4*>(fB + off) = v;
-                *reinterpret_cast<float4*>(fBlo + off) = lo;
-            }
-        }
-        float slope[NL / 2];  // this warp's layer half (warps 0-3: layers 0-7, warps 4-7: 8-15)
-#pragma unroll
-        for (int k = 0; k < NL / 2; ++k) slope[k] = wsu[NR * NL * 2 + (warp >> 2) * (NL / 2) + k];
-        mbar_wait_bounded(&bars[st], (it >> 1) & 1);
-        fence_proxy_async();
-        __syncthreads();
-        // passes 1 + 2: (y, B) and (y, B_lo); tile 0 rows 0-127 -> TMEM cols 32..63, tile 1 rows 40-167 -> cols 0..31
-        if (t == 0) {
-            tc_fence_after();
-#pragma unroll
-            for (int tile = 0; tile < 2; ++tile) {
-                const uint32_t row0 = tile ? 40u : 0u;
-                const uint32_t dcol = tile ? 0u : 32u;
-#pragma unroll
-                for (int pass = 0; pass < 2; ++pass) {
-                    const uint32_t bb = base + (pass ? (uint32_t)SM::Blo : (uint32_t)SM::B);
-#pragma unroll
-                    for (int kt = 0; kt < KT; ++kt)
-#pragma unroll
-                        for (int ks = 0; ks < 4; ++ks) {
-                            const uint64_t da = umma_desc_sw128(ys + kt * (uint32_t)SM::ktile + row0 * 128u + ks * 32u);
-                            const uint64_t db = umma_desc_sw128(bb + kt * (uint32_t)SM::btile + ks * 32u);
-                            umma_tf32(tmem + dcol, da, db, idesc, (pass | kt | ks) ? 1u : 0u);
-                        }
-                }
-            }
-            umma_commit(&bars[2]);
-        }
-        mbar_wait_bounded(&bars[2], mma_phase);
-        mma_phase ^= 1;
-        // y -> y_lo in place (passes 1-2 have consumed y)
-        {
-            float4* y4 = reinterpret_cast<float4*>(fy);
-            constexpr int n4 = (int)(SM::ystage / 16);
-#pragma unroll 4
-            for (int i = t; i < n4; i += kTcThreads) {
-                float4 v = y4[i];
-                v.x -= tf32_trunc(v.x);
-                v.y -= tf32_trunc(v.y);
-                v.z -= tf32_trunc(v.z);
-                v.w -= tf32_trunc(v.w);
-                y4[i] = v;
-            }
-        }
-        fence_proxy_async();
-        __syncthreads();
-        if (t == 0) {
-            tc_fence_after();
-#pragma unroll
-            for (int tile = 0; tile < 2; ++tile) {
-                const uint32_t row0 = tile ? 40u : 0u;
-                const uint32_t dcol = tile ? 0u : 32u;
-#pragma unroll
-                for (int kt = 0; kt < KT; ++kt)
-#pragma unroll
-                    for (int ks = 0; ks < 4; ++ks) {
-                        const uint64_t da = umma_desc_sw128(ys + kt * (uint32_t)SM::ktile + row0 * 128u + ks * 32u);
-                        const uint64_t db = umma_desc_sw128(base + (uint32_t)SM::B + kt * (uint32_t)SM::btile + ks * 32u);
-                        umma_tf32(tmem + dcol, da, db, idesc, 1u);
-                    }
-            }
-            umma_commit(&bars[2]);
-        }
-        mbar_wait_bounded(&bars[2], mma_phase);
-        mma_phase ^= 1;
-        tc_fence_after();
-        // epilogue: warp w reads TMEM lanes 32(w%4).. ; warps 0-3 take layers 0-7, warps 4-7 layers 8-15.
-        // tile 1 (cols 0..31): lanes -> rows 40..167; tile 0 (cols 32..63): lanes 0..39 -> rows 0..39.
-        const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);
-        const int wq = warp & 3, lh = warp >> 2;  // lane window, layer half
-        constexpr int KH = NL / 2;
-        constexpr int kRecBytes = NL * QM * LlrTraits<LT>::bytes;
-        constexpr int kHalfBytes = KH * QM * LlrTraits<LT>::bytes;
-#pragma unroll 1
-        for (int pass = 0; pass < 2; ++pass) {
-            if (pass == 1 && wq >= 2) break;
-            const uint32_t taddr = tmem + ((uint32_t)(32 * wq) << 16) + (pass ? 32u : 0u) + KH * lh;
-            uint32_t xr[KH], xi[KH];
-            tmem_ld8(taddr, xr);        // columns KH*lh .. +7      (Re of this half's layers)
-            tmem_ld8(taddr + 16u, xi);  // columns 16 + KH*lh .. +7 (Im)
-            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-            const int row = pass ? 32 * wq + lane : 40 + 32 * wq + lane;
-            if (pass == 1 && row >= 40) continue;
-            const int s = row / kSc, f = row % kSc;
-            const size_t re = (size_t)(slot * kSym + s) * a.n_sc + fb * kSc + f;
-            if (a.llr) {
-                float v[KH * QM];
-#pragma unroll
-                for (int q = 0; q < KH; ++q) {
-                    const float2 x = make_float2(__uint_as_float(xr[q]), __uint_as_float(xi[q]));
-                    if (!zf) demap_layer<QM, false, LT>(x, slope[q], v + q * QM);
-                    else demap_layer<QM, true, LT>(x, slope[q], v + q * QM);
-                }
-                uint32_t wd[(kHalfBytes + 3) / 4];
-                if (!zf) pack_llr<LT, KH * QM, false>(v, wd);
-                else pack_llr<LT, KH * QM, true>(v, wd);
-                store_bytes<kHalfBytes>((char*)a.llr + re * kRecBytes + lh * kHalfBytes, wd);
-            }
-            if (a.xhat) {
-                const float ia = rsqrtf(norm);
-#pragma unroll
-                for (int q = 0; q < KH; ++q)
-                    a.xhat[re * NL + KH * lh + q] =
-                        make_float2(__uint_as_float(xr[q]) * ia, __uint_as_float(xi[q]) * ia);
-            }
-        }
-        tc_fence_before();
-        __syncthreads();  // TMEM, B and this y stage are free
-    }
-    __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem));
-}
-
-// ------------------------------------------------------------------------
-// k_big_tc2: warp-specialised, software-pipelined version of k_big_tc.
-// Warps 0-7 (SIMT): y staging (cp.async, 2 stages), B / B_lo construction,
-// y -> y_lo conversion and the epilogue; warp 8 lane 0: the MMA issuer. TMEM
-// holds two accumulator buffers, so the epilogue of unit i-1 runs while the
-// tensor cores do passes 1-2 of unit i. mbarriers: yfull[2] (cp.async), bready,
-// c1 (passes 1-2 committed), ylo, c2 (pass 3 committed), tfree[2].
-constexpr int kTc2Simt = 256;
-__device__ __forceinline__ void simt_bar() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
-
-template <int NR, int NL, int QM, int LT>
-__device__ __forceinline__ void tc2_epilogue(const DetectArgs& a, uint32_t tmem_buf, long long u, const float* slope,
-                                             bool zf, float norm) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);
-    const int wq = warp & 3, lh = warp >> 2;
-    constexpr int KH = NL / 2;
-    constexpr int kRecBytes = NL * QM * LlrTraits<LT>::bytes;
-    constexpr int kHalfBytes = KH * QM * LlrTraits<LT>::bytes;
-#pragma unroll 1
-    for (int pass = 0; pass < 2; ++pass) {
-        if (pass == 1 && wq >= 2) break;
-        const uint32_t taddr = tmem_buf + ((uint32_t)(32 * wq) << 16) + (pass ? 32u : 0u) + KH * lh;
-        uint32_t xr[KH], xi[KH];
-        tmem_ld8(taddr, xr);
-        tmem_ld8(taddr + 16u, xi);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        const int row = pass ? 32 * wq + lane : 40 + 32 * wq + lane;
-        if (pass == 1 && row >= 40) continue;
-        const int s = row / kSc, f = row % kSc;
-        const size_t re = (size_t)(slot * kSym + s) * a.n_sc + fb * kSc + f;
-        if (a.llr) {
-            float v[KH * QM];
-#pragma unroll
-            for (int q = 0; q < KH; ++q) {
-                const float2 x = make_float2(__uint_as_float(xr[q]), __uint_as_float(xi[q]));
-                if (!zf) demap_layer<QM, false, LT>(x, slope[q], v + q * QM);
-                else demap_layer<QM, true, LT>(x, slope[q], v + q * QM);
-            }
-            uint32_t wd[(kHalfBytes + 3) / 4];
-            if (!zf) pack_llr<LT, KH * QM, false>(v, wd);
-            else pack_llr<LT, KH * QM, true>(v, wd);
-            store_bytes<kHalfBytes>((char*)a.llr + re * kRecBytes + lh * kHalfBytes, wd);
-        }
-        if (a.xhat) {
-            const float ia = rsqrtf(norm);
-#pragma unroll
-            for (int q = 0; q < KH; ++q)
-                a.xhat[re * NL + KH * lh + q] = make_float2(__uint_as_float(xr[q]) * ia, __uint_as_float(xi[q]) * ia);
-        }
-    }
-}
-
-// W~ rows of unit u needed by this thread for B (thread -> row n = t/8, K-tile (t>>1)&3, chunks 4(t&1)..+3)
-template <int NR, int NL>
-__device__ __forceinline__ void tc2_fetch_w(const DetectArgs& a, long long u, float4 (&wv)[4]) {
-    constexpr int WS = BigWs<NR, NL>::stride;
-    const int t = threadIdx.x;
-    const int n = t >> 3, kt = (t >> 1) & 3, c0 = (t & 1) * 4, l = n & 15;
-    const float* wsu = reinterpret_cast<const float*>(a.ws) + u * WS;
-#pragma unroll
-    for (int cq = 0; cq < 4; ++cq) {
-        const int r0 = kt * 16 + 2 * (c0 + cq);
-        const float2 w0 = *reinterpret_cast<const float2*>(wsu + 2 * (r0 * NL + l));
-        const float2 w1 = *reinterpret_cast<const float2*>(wsu + 2 * ((r0 + 1) * NL + l));
-        wv[cq] = make_float4(w0.x, w0.y, w1.x, w1.y);
-    }
-}
-template <int NR, int NL>
-__device__ __forceinline__ void tc2_build_b(float* fB, float* fBlo, const float4 (&wv)[4]) {
-    using SM = TcSmem<NR, NL>;
-    const int t = threadIdx.x;
-    const int n = t >> 3, kt = (t >> 1) & 3, c0 = (t & 1) * 4;
-    const bool im_row = n >= 16;
-#pragma unroll
-    for (int cq = 0; cq < 4; ++cq) {
-        const int c = c0 + cq;
-        const float4 w = wv[cq];  // (Wr_r0, Wi_r0, Wr_r1, Wi_r1)
-        float4 v;
-        if (!im_row) v = make_float4(w.x, -w.y, w.z, -w.w);   // xr += Wr yr - Wi yi
-        else v = make_float4(w.y, w.x, w.w, w.z);             // xi += Wi yr + Wr yi
-        const float4 lo = make_float4(v.x - tf32_trunc(v.x), v.y - tf32_trunc(v.y), v.z - tf32_trunc(v.z),
-                                      v.w - tf32_trunc(v.w));
-        const int off = kt * (int)(SM::btile / 4) + n * 32 + ((c ^ (n & 7)) << 2);
-        *reinterpret_cast<float4*>(fB + off) = v;
-        *reinterpret_cast<float4*>(fBlo + off) = lo;
-    }
-}
-
-// y tile of unit u, K-tile kt via TMA (3-D map over y viewed as [n_sym][n_sc][2*NR floats],
-// box {32 floats, 12 subcarriers, 14 symbols}, SWIZZLE_128B = the UMMA SW128 K-major layout)
 __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
         : "memory");
 }
-template <int NR, int NL>
-__device__ __forceinline__ void tc2_issue_y_tma(const DetectArgs& a, const CUtensorMap* map, uint32_t stage,
-                                                long long u, uint64_t* bar) {
-    using SM = TcSmem<NR, NL>;
-    const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);
-    mbar_arrive_expect_tx(bar, (uint32_t)SM::ystage);
-#pragma unroll
-    for (int kt = 0; kt < SM::KT; ++kt) tma_load_3d(stage + kt * (uint32_t)SM::ktile, map, 32 * kt, fb * kSc, slot * kSym, bar);
-}
-
-template <int NR, int NL, int QM, int LT>
-__global__ void __launch_bounds__(kTc2Simt + 32, 1) k_big_tc2(DetectArgs a, const __grid_constant__ CUtensorMap ymap) {
-    static_assert(NL == 16 && NR == 64, "k_big_tc2: 64 x 16");
-    using SM = TcSmem<NR, NL>;
-    constexpr int KT = SM::KT;
-    constexpr int WS = BigWs<NR, NL>::stride;
-    extern __shared__ unsigned char smem_raw[];
-    const uint32_t raw = smem_u32(smem_raw);
-    const uint32_t base = (raw + 1023u) & ~1023u;
-    unsigned char* gbase = smem_raw + (base - raw);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + SM::bars);
-    uint64_t* yfull = bars;         // [2]
-    uint64_t* bready = bars + 2;
-    uint64_t* c1 = bars + 3;
-    uint64_t* ylo = bars + 4;
-    uint64_t* c2 = bars + 5;
-    uint64_t* tfree = bars + 6;     // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + SM::tmem);
-    float* fB = reinterpret_cast<float*>(gbase + SM::B);
-    float* fBlo = reinterpret_cast<float*>(gbase + SM::Blo);
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    static_assert(SM::tmem - SM::bars >= 64, "barrier space");
-
-    pdl_launch_dependents();
-    if (t == 0) {
-        for (int i = 0; i < 8; ++i) mbar_init(&bars[i], 1);
-        fence_mbar_init();
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tmem_slot)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    const long long u0 = blockIdx.x, du = gridDim.x;
-    const long long n_my = u0 < a.n_units ? (a.n_units - u0 + du - 1) / du : 0;  // units of this CTA
-
-    if (warp == kTc2Simt / 32) {
-        // ===== MMA issuer =====
-        if (lane == 0) {
-            constexpr uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
-#pragma unroll 1
-            for (long long i = 0; i < n_my; ++i) {
-                const int st = (int)(i & 1);
-                const uint32_t ys = base + SM::y0 + st * (uint32_t)SM::ystage;
-                const uint32_t acc = tmem + 64u * (uint32_t)st;
-                if (i >= 2) mbar_wait_bounded(&tfree[st], (uint32_t)(((i >> 1) + 1) & 1));
-                mbar_wait_bounded(&yfull[st], (uint32_t)((i >> 1) & 1));
-                mbar_wait_bounded(bready, (uint32_t)(i & 1));
-                fence_proxy_async();
-                tc_fence_after();
-#pragma unroll
-                for (int tile = 0; tile < 2; ++tile) {
-                    const uint32_t row0 = tile ? 40u : 0u, dcol = tile ? 0u : 32u;
-#pragma unroll
-                    for (int pass = 0; pass < 2; ++pass) {
-                        const uint32_t bb = base + (pass ? (uint32_t)SM::Blo : (uint32_t)SM::B);
-#pragma unroll
-                        for (int kt = 0; kt < KT; ++kt)
-#pragma unroll
-                            for (int ks = 0; ks < 4; ++ks)
-                                umma_tf32(acc + dcol,
-                                          umma_desc_sw128(ys + kt * (uint32_t)SM::ktile + row0 * 128u + ks * 32u),
-                                          umma_desc_sw128(bb + kt * (uint32_t)SM::btile + ks * 32u), idesc,
-                                          (pass | kt | ks) ? 1u : 0u);
-                    }
-                }
-                umma_commit(c1);
-                mbar_wait_bounded(ylo, (uint32_t)(i & 1));
-                fence_proxy_async();
-                tc_fence_after();
-#pragma unroll
-                for (int tile = 0; tile < 2; ++tile) {
-                    const uint32_t row0 = tile ? 40u : 0u, dcol = tile ? 0u : 32u;
-#pragma unroll
-                    for (int kt = 0; kt < KT; ++kt)
-#pragma unroll
-                        for (int ks = 0; ks < 4; ++ks)
-                            umma_tf32(acc + dcol, umma_desc_sw128(ys + kt * (uint32_t)SM::ktile + row0 * 128u + ks * 32u),
-                                      umma_desc_sw128(base + (uint32_t)SM::B + kt * (uint32_t)SM::btile + ks * 32u),
-                                      idesc, 1u);
-                }
-                umma_commit(c2);
-            }
-        }
-    } else {
-        // ===== SIMT warps =====
-        const float norm = (float)qam_norm(QM);
-        const bool zf = !(a.sigma2 > 0.f);
-        if (t == 0) {
-            if (n_my > 0) tc2_issue_y_tma<NR, NL>(a, &ymap, base + SM::y0, u0, &yfull[0]);
-            if (n_my > 1) tc2_issue_y_tma<NR, NL>(a, &ymap, base + SM::y0 + (uint32_t)SM::ystage, u0 + du, &yfull[1]);
-        }
-        pdl_wait();  // W~ of this call's setup kernel is complete
-        float4 wv[4];
-        if (n_my > 0) {
-            tc2_fetch_w<NR, NL>(a, u0, wv);
-            tc2_build_b<NR, NL>(fB, fBlo, wv);
-            fence_proxy_async();
-            simt_bar();
-            if (t == 0) mbar_arrive(bready);
-        }
-        float slope_prev[NL / 2];
-#pragma unroll 1
-        for (long long i = 0; i < n_my; ++i) {
-            const long long u = u0 + i * du;
-            const int st = (int)(i & 1);
-            float slope[NL / 2];
-            {
-                const float* wsu = reinterpret_cast<const float*>(a.ws) + u * WS + NR * NL * 2 + (warp >> 2) * (NL / 2);
-#pragma unroll
-                for (int k = 0; k < NL / 2; ++k) slope[k] = wsu[k];
-            }
-            if (i >= 1) {
-                // unit i-1: pass 3 done -> its y stage is free (refill with unit i+1) and its accumulator is ready
-                mbar_wait_bounded(c2, (uint32_t)((i - 1) & 1));
-                if (t == 0 && i + 1 < n_my) {
-                    fence_proxy_async();  // y_lo writes of unit i-1 (generic) before the TMA overwrite
-                    tc2_issue_y_tma<NR, NL>(a, &ymap, base + SM::y0 + (st ^ 1) * (uint32_t)SM::ystage, u + du,
-                                            &yfull[st ^ 1]);
-                }
-                tc_fence_after();
-                tc2_epilogue<NR, NL, QM, LT>(a, tmem + 64u * (uint32_t)(st ^ 1), u - du, slope_prev, zf, norm);
-                tc_fence_before();
-                simt_bar();
-                if (t == 0) mbar_arrive(&tfree[st ^ 1]);
-            }
-            // passes 1-2 of unit i done -> y -> y_lo in place
-            mbar_wait_bounded(c1, (uint32_t)(i & 1));
-            {
-                float4* y4 = reinterpret_cast<float4*>(gbase + SM::y0 + st * SM::ystage);
-                constexpr int n4 = (int)(SM::ystage / 16);
-#pragma unroll 4
-                for (int q = t; q < n4; q += kTc2Simt) {
-                    float4 v = y4[q];
-                    v.x -= tf32_trunc(v.x);
-                    v.y -= tf32_trunc(v.y);
-                    v.z -= tf32_trunc(v.z);
-                    v.w -= tf32_trunc(v.w);
-                    y4[q] = v;
-                }
-            }
-            fence_proxy_async();
-            simt_bar();
-            if (t == 0) mbar_arrive(ylo);
-            if (i + 1 < n_my) {
-                tc2_fetch_w<NR, NL>(a, u + du, wv);   // overlaps pass 3
-                mbar_wait_bounded(c2, (uint32_t)(i & 1));
-                tc2_build_b<NR, NL>(fB, fBlo, wv);
-                fence_proxy_async();
-                simt_bar();
-                if (t == 0) mbar_arrive(bready);
-            }
-#pragma unroll
-            for (int k = 0; k < NL / 2; ++k) slope_prev[k] = slope[k];
-        }
-        if (n_my > 0) {
-            const long long i = n_my - 1;
-            mbar_wait_bounded(c2, (uint32_t)(i & 1));
-            tc_fence_after();
-            tc2_epilogue<NR, NL, QM, LT>(a, tmem + 64u * (uint32_t)(i & 1), u0 + i * du, slope_prev, zf, norm);
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
-}
-
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda link)
 inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -904,344 +385,6 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
             fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
     }
     return fn;
-}
-
-template <int NR, int NL, int QM, int LT>
-cudaError_t launch_tc2(const DetectArgs& a, cudaStream_t s) {
-    if (a.n_units <= 0) return cudaSuccess;
-    static int n_sm = 0;
-    if (!n_sm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    }
-    auto enc = tensor_map_encoder();
-    if (!enc) return cudaErrorNotSupported;
-    CUtensorMap ymap;
-    const cuuint64_t gdim[3] = {(cuuint64_t)(2 * NR), (cuuint64_t)a.n_sc, (cuuint64_t)a.n_sym};
-    const cuuint64_t gstride[2] = {(cuuint64_t)NR * 8, (cuuint64_t)a.n_sc * NR * 8};
-    const cuuint32_t box[3] = {32, (cuuint32_t)kSc, (cuuint32_t)kSym};
-    const cuuint32_t estride[3] = {1, 1, 1};
-    if (enc(&ymap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float2*>(a.y), gdim, gstride, box, estride,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return cudaErrorInvalidValue;
-    constexpr int UPB = 4;
-    cudaError_t e = launch_kernel(k_big_setup<NR, NL, QM, UPB>, dim3((unsigned)((a.n_units + UPB - 1) / UPB)),
-                                  dim3(32 * UPB), UPB * SetupSmem<NR, NL>::per_unit, s, a.overlap, a);
-    if (e != cudaSuccess) return e;
-    const unsigned grid = (unsigned)(a.n_units < n_sm ? a.n_units : n_sm);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kTc2Simt + 32);
-    cfg.dynamicSmemBytes = TcSmem<NR, NL>::total;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = a.overlap ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, k_big_tc2<NR, NL, QM, LT>, a, ymap);
-}
-
-template <int NR, int NL, int QM, int LT>
-cudaError_t prepare_tc2() {
-    cudaError_t e = cudaFuncSetAttribute(k_big_setup<NR, NL, QM, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(4 * SetupSmem<NR, NL>::per_unit));
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_big_tc2<NR, NL, QM, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)TcSmem<NR, NL>::total);
-}
-
-template <int NR, int NL, int QM, int LT>
-cudaError_t launch_tc(const DetectArgs& a, cudaStream_t s) {
-    if (a.n_units <= 0) return cudaSuccess;
-    static int n_sm = 0;
-    if (!n_sm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    }
-    constexpr int UPB = 4;
-    cudaError_t e = launch_kernel(k_big_setup<NR, NL, QM, UPB>, dim3((unsigned)((a.n_units + UPB - 1) / UPB)),
-                                  dim3(32 * UPB), UPB * SetupSmem<NR, NL>::per_unit, s, a.overlap, a);
-    if (e != cudaSuccess) return e;
-    const unsigned grid = (unsigned)(a.n_units < n_sm ? a.n_units : n_sm);
-    return launch_kernel(k_big_tc<NR, NL, QM, LT>, dim3(grid), dim3(kTcThreads), TcSmem<NR, NL>::total, s, a.overlap,
-                         a);
-}
-
-template <int NR, int NL, int QM, int LT>
-cudaError_t prepare_tc() {
-    cudaError_t e = cudaFuncSetAttribute(k_big_setup<NR, NL, QM, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(4 * SetupSmem<NR, NL>::per_unit));
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_big_tc<NR, NL, QM, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)TcSmem<NR, NL>::total);
-}
-
-// ------------------------------------------------------------------------
-// k_big_tc3: half-unit software pipeline on the tensor cores.
-// Work item = half a PRB-unit (7 symbols x 12 subcarriers = 84 RE rows), so a
-// y stage is 48 KiB (4 K-tiles x 96 rows x 128 B, TMA box {32, 12, 7}) and three
-// stages plus two B sets fit: B set = [B_hi; B_lo] stacked along N (64 rows),
-// so passes 1+2 are ONE N=64 MMA chain (the tcgen05 issue cost, ~50 cycles per
-// tf32 MMA, does not grow from N=32 to N=64) and pass 3 uses the B_hi rows.
-// The MMA thread keeps two halves in flight: p12(h) then p3(h-1), so the tensor
-// pipe works while the SIMT warps convert y(h) -> y_lo(h) and run epilogues.
-struct Tc3 {
-    static constexpr int ROWS = 96;                                     // 84 valid + pad
-    static constexpr int KT = 4;
-    static constexpr size_t ktile = (size_t)ROWS * 128;                 // 12 KiB
-    static constexpr size_t ystage = KT * ktile;                        // 48 KiB
-    static constexpr size_t bktile = (size_t)64 * 128;                  // 8 KiB: 32 rows B_hi + 32 rows B_lo
-    static constexpr size_t bset = KT * bktile;                         // 32 KiB
-    static constexpr size_t y0 = 0;
-    static constexpr size_t B0 = 3 * ystage;
-    static constexpr size_t bars = B0 + 2 * bset;                       // 13 mbarriers
-    static constexpr size_t tmem = bars + 13 * 8;
-    static constexpr size_t total = tmem + 16 + 1024;
-};
-
-template <int NR, int NL>
-__device__ __forceinline__ void tc3_issue_y(const DetectArgs& a, const CUtensorMap* map, uint32_t stage, long long u,
-                                            int q, uint64_t* bar) {
-    const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);
-    mbar_arrive_expect_tx(bar, (uint32_t)(Tc3::KT * 84 * 128));
-#pragma unroll
-    for (int kt = 0; kt < Tc3::KT; ++kt)
-        tma_load_3d(stage + kt * (uint32_t)Tc3::ktile, map, 32 * kt, fb * kSc, slot * kSym + 7 * q, bar);
-}
-// B set rows: n in [0,32): B_hi (fp32, read as TF32), n + 32: B_lo = B - trunc(B)
-template <int NR, int NL>
-__device__ __forceinline__ void tc3_build_b(float* fset, const float4 (&wv)[4]) {
-    const int t = threadIdx.x;
-    const int n = t >> 3, kt = (t >> 1) & 3, c0 = (t & 1) * 4;
-    const bool im_row = n >= 16;
-#pragma unroll
-    for (int cq = 0; cq < 4; ++cq) {
-        const int c = c0 + cq;
-        const float4 w = wv[cq];
-        float4 v;
-        if (!im_row) v = make_float4(w.x, -w.y, w.z, -w.w);
-        else v = make_float4(w.y, w.x, w.w, w.z);
-        const float4 lo = make_float4(v.x - tf32_trunc(v.x), v.y - tf32_trunc(v.y), v.z - tf32_trunc(v.z),
-                                      v.w - tf32_trunc(v.w));
-        float* kb = fset + kt * (int)(Tc3::bktile / 4);
-        *reinterpret_cast<float4*>(kb + n * 32 + ((c ^ (n & 7)) << 2)) = v;
-        *reinterpret_cast<float4*>(kb + (n + 32) * 32 + ((c ^ (n & 7)) << 2)) = lo;  // (n+32)&7 == n&7
-    }
-}
-
-template <int NR, int NL, int QM, int LT>
-__device__ __forceinline__ void tc3_epilogue(const DetectArgs& a, uint32_t tmem_buf, long long u, int q,
-                                             const float* slope, bool zf, float norm) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int wq = warp & 3, lh = warp >> 2;
-    if (wq >= 3) return;
-    const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);
-    constexpr int KH = NL / 2;
-    constexpr int kRecBytes = NL * QM * LlrTraits<LT>::bytes;
-    constexpr int kHalfBytes = KH * QM * LlrTraits<LT>::bytes;
-    const uint32_t taddr = tmem_buf + ((uint32_t)(32 * wq) << 16) + KH * lh;
-    uint32_t xr[KH], xi[KH], xr2[KH], xi2[KH];
-    tmem_ld8(taddr, xr);
-    tmem_ld8(taddr + 16u, xi);
-    tmem_ld8(taddr + 32u, xr2);
-    tmem_ld8(taddr + 48u, xi2);
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    const int row = 32 * wq + lane;
-    if (row >= 84) return;
-    const int s = 7 * q + row / kSc, f = row % kSc;
-    const size_t re = (size_t)(slot * kSym + s) * a.n_sc + fb * kSc + f;
-    float2 x[KH];
-#pragma unroll
-    for (int k = 0; k < KH; ++k)
-        x[k] = make_float2(__uint_as_float(xr[k]) + __uint_as_float(xr2[k]), __uint_as_float(xi[k]) + __uint_as_float(xi2[k]));
-    if (a.llr) {
-        float v[KH * QM];
-#pragma unroll
-        for (int k = 0; k < KH; ++k) {
-            if (!zf) demap_layer<QM, false, LT>(x[k], slope[k], v + k * QM);
-            else demap_layer<QM, true, LT>(x[k], slope[k], v + k * QM);
-        }
-        uint32_t wd[(kHalfBytes + 3) / 4];
-        if (!zf) pack_llr<LT, KH * QM, false>(v, wd);
-        else pack_llr<LT, KH * QM, true>(v, wd);
-        store_bytes<kHalfBytes>((char*)a.llr + re * kRecBytes + lh * kHalfBytes, wd);
-    }
-    if (a.xhat) {
-        const float ia = rsqrtf(norm);
-#pragma unroll
-        for (int k = 0; k < KH; ++k) a.xhat[re * NL + KH * lh + k] = make_float2(x[k].x * ia, x[k].y * ia);
-    }
-}
-
-template <int NR, int NL, int QM, int LT>
-__global__ void __launch_bounds__(kTc2Simt + 32, 1) k_big_tc3(DetectArgs a, const __grid_constant__ CUtensorMap ymap) {
-    static_assert(NL == 16 && NR == 64, "k_big_tc3: 64 x 16");
-    constexpr int WS = BigWs<NR, NL>::stride;
-    extern __shared__ unsigned char smem_raw[];
-    const uint32_t raw = smem_u32(smem_raw);
-    const uint32_t base = (raw + 1023u) & ~1023u;
-    unsigned char* gbase = smem_raw + (base - raw);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(gbase + Tc3::bars);
-    uint64_t* yfull = bars;        // [3]
-    uint64_t* bready = bars + 3;   // [2]
-    uint64_t* c1 = bars + 5;       // [2]
-    uint64_t* ylo = bars + 7;      // [2]
-    uint64_t* c2 = bars + 9;       // [2]
-    uint64_t* tfree = bars + 11;   // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + Tc3::tmem);
-    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-
-    pdl_launch_dependents();
-    if (t == 0) {
-        for (int i = 0; i < 13; ++i) mbar_init(&bars[i], 1);
-        fence_mbar_init();
-    }
-    if (warp == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tmem_slot)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    const long long u0 = blockIdx.x, du = gridDim.x;
-    const long long n_units_my = u0 < a.n_units ? (a.n_units - u0 + du - 1) / du : 0;
-    const long long n_half = 2 * n_units_my;
-    auto unit_of = [&](long long h) { return u0 + (h >> 1) * du; };  // global unit of my half h
-    auto ystage = [&](long long h) { return base + (uint32_t)Tc3::y0 + (uint32_t)(h % 3) * (uint32_t)Tc3::ystage; };
-    auto bset = [&](long long h) { return base + (uint32_t)Tc3::B0 + (uint32_t)((h >> 1) & 1) * (uint32_t)Tc3::bset; };
-
-    if (warp == kTc2Simt / 32) {
-        // ===== MMA issuer: p12(h) [N=64, A=y, B=[B_hi;B_lo]] then p3(h-1) [N=32, A=y_lo, B_hi] =====
-        if (lane == 0) {
-            constexpr uint32_t id64 = (1u << 4) | (2u << 7) | (2u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
-            constexpr uint32_t id32 = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
-            auto p3 = [&](long long hp) {
-                const int b = (int)(hp & 1);
-                mbar_wait_bounded(&ylo[b], (uint32_t)((hp >> 1) & 1));
-                fence_proxy_async();
-                tc_fence_after();
-                const uint32_t ys = ystage(hp), bs = bset(hp), acc = tmem + 64u * (uint32_t)b;
-#pragma unroll
-                for (int kt = 0; kt < Tc3::KT; ++kt)
-#pragma unroll
-                    for (int ks = 0; ks < 4; ++ks)
-                        umma_tf32(acc, umma_desc_sw128(ys + kt * (uint32_t)Tc3::ktile + ks * 32u),
-                                  umma_desc_sw128(bs + kt * (uint32_t)Tc3::bktile + ks * 32u), id32, 1u);
-                umma_commit(&c2[b]);
-            };
-#pragma unroll 1
-            for (long long h = 0; h < n_half; ++h) {
-                const int b = (int)(h & 1);
-                if (h >= 2) mbar_wait_bounded(&tfree[b], (uint32_t)(((h >> 1) + 1) & 1));
-                mbar_wait_bounded(&yfull[h % 3], (uint32_t)((h / 3) & 1));
-                mbar_wait_bounded(&bready[(h >> 1) & 1], (uint32_t)((h >> 2) & 1));
-                fence_proxy_async();
-                tc_fence_after();
-                const uint32_t ys = ystage(h), bs = bset(h), acc = tmem + 64u * (uint32_t)b;
-#pragma unroll
-                for (int kt = 0; kt < Tc3::KT; ++kt)
-#pragma unroll
-                    for (int ks = 0; ks < 4; ++ks)
-                        umma_tf32(acc, umma_desc_sw128(ys + kt * (uint32_t)Tc3::ktile + ks * 32u),
-                                  umma_desc_sw128(bs + kt * (uint32_t)Tc3::bktile + ks * 32u), id64,
-                                  (kt | ks) ? 1u : 0u);
-                umma_commit(&c1[b]);
-                if (h >= 1) p3(h - 1);
-            }
-            if (n_half > 0) p3(n_half - 1);
-        }
-    } else {
-        // ===== SIMT warps =====
-        const float norm = (float)qam_norm(QM);
-        const bool zf = !(a.sigma2 > 0.f);
-        if (t == 0)
-            for (long long h = 0; h < 3 && h < n_half; ++h)
-                tc3_issue_y<NR, NL>(a, &ymap, ystage(h), unit_of(h), (int)(h & 1), &yfull[h % 3]);
-        pdl_wait();  // W~ of this call's setup kernel is complete
-        float4 wv[4];
-        for (long long v = 0; v < 2 && v < n_units_my; ++v) {
-            tc2_fetch_w<NR, NL>(a, u0 + v * du, wv);
-            tc3_build_b<NR, NL>(reinterpret_cast<float*>(gbase + Tc3::B0 + v * Tc3::bset), wv);
-        }
-        fence_proxy_async();
-        simt_bar();
-        if (t == 0) {
-            mbar_arrive(&bready[0]);
-            if (n_units_my > 1) mbar_arrive(&bready[1]);
-        }
-        float slope[NL / 2];
-#pragma unroll 1
-        for (long long h = 0; h < n_half; ++h) {
-            const int b = (int)(h & 1);
-            // passes 1+2 of half h done -> y(h) -> y_lo(h) in place
-            mbar_wait_bounded(&c1[b], (uint32_t)((h >> 1) & 1));
-            {
-                float4* y4 = reinterpret_cast<float4*>(gbase + (ystage(h) - base));
-                constexpr int n4 = (int)(Tc3::ystage / 16);
-#pragma unroll 4
-                for (int i = t; i < n4; i += kTc2Simt) {
-                    float4 v = y4[i];
-                    v.x -= tf32_trunc(v.x);
-                    v.y -= tf32_trunc(v.y);
-                    v.z -= tf32_trunc(v.z);
-                    v.w -= tf32_trunc(v.w);
-                    y4[i] = v;
-                }
-            }
-            fence_proxy_async();
-            simt_bar();
-            if (t == 0) mbar_arrive(&ylo[b]);
-            if (h >= 1) {
-                const long long hp = h - 1;
-                const int bp = (int)(hp & 1);
-                mbar_wait_bounded(&c2[bp], (uint32_t)((hp >> 1) & 1));
-                // stage of hp is free: refill with half hp + 3
-                if (t == 0 && hp + 3 < n_half) {
-                    fence_proxy_async();
-                    tc3_issue_y<NR, NL>(a, &ymap, ystage(hp + 3), unit_of(hp + 3), (int)((hp + 3) & 1),
-                                        &yfull[(hp + 3) % 3]);
-                }
-                {
-                    const float* wsu = reinterpret_cast<const float*>(a.ws) + unit_of(hp) * WS + NR * NL * 2 +
-                                       (warp >> 2) * (NL / 2);
-#pragma unroll
-                    for (int k = 0; k < NL / 2; ++k) slope[k] = wsu[k];
-                }
-                tc_fence_after();
-                tc3_epilogue<NR, NL, QM, LT>(a, tmem + 64u * (uint32_t)bp, unit_of(hp), (int)(hp & 1), slope, zf, norm);
-                tc_fence_before();
-                const bool unit_done = (hp & 1) == 1;
-                const long long vn = (hp >> 1) + 2;  // unit that reuses this B set
-                if (unit_done && vn < n_units_my) tc2_fetch_w<NR, NL>(a, u0 + vn * du, wv);
-                simt_bar();
-                if (t == 0) mbar_arrive(&tfree[bp]);
-                if (unit_done && vn < n_units_my) {
-                    tc3_build_b<NR, NL>(reinterpret_cast<float*>(gbase + (bset(hp) - base)), wv);
-                    fence_proxy_async();
-                    simt_bar();
-                    if (t == 0) mbar_arrive(&bready[(hp >> 1) & 1]);
-                }
-            }
-        }
-        if (n_half > 0) {
-            const long long hp = n_half - 1;
-            const int bp = (int)(hp & 1);
-            mbar_wait_bounded(&c2[bp], (uint32_t)((hp >> 1) & 1));
-            const float* wsu = reinterpret_cast<const float*>(a.ws) + unit_of(hp) * WS + NR * NL * 2 + (warp >> 2) * (NL / 2);
-#pragma unroll
-            for (int k = 0; k < NL / 2; ++k) slope[k] = wsu[k];
-            tc_fence_after();
-            tc3_epilogue<NR, NL, QM, LT>(a, tmem + 64u * (uint32_t)bp, unit_of(hp), (int)(hp & 1), slope, zf, norm);
-        }
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
 }
 
 // ------------------------------------------------------------------------
@@ -1664,45 +807,46 @@ cudaError_t prepare_ap3() {
 //                  x~ -> exact max-log demap -> LLR stores.
 // Chunk g = 4 i + c of the CTA's i-th unit (u = blockIdx.x + i gridDim.x).
 // mbarrier k-th completion is waited with parity k & 1.
+template <int S_, int NLO_>
 struct Ap4 {
-    static constexpr int S = 4;                              // y stages
-    static constexpr size_t chunk = (size_t)kRe * 128;       // 21504
+    static constexpr int S = S_;                             // y stages
+    static constexpr int NLO = NLO_;                         // y_lo buffers
+    static constexpr size_t chunk = (size_t)kRe * 128;       // 21504 = 21 x 1024
     static constexpr size_t y0 = 0;
-    static constexpr size_t ylo = S * chunk;                 // 2 buffers
-    static constexpr size_t B = ylo + 2 * chunk;             // 2 x 32 KiB (1024-aligned)
+    static constexpr size_t ylo = S * chunk;
+    static constexpr size_t B = ylo + NLO * chunk;           // 2 x 32 KiB (1024-aligned)
     static constexpr size_t bset = 4 * 64 * 128;
-    static constexpr size_t wraw = B + 2 * bset;             // 2 x (W~ + slopes)
-    static constexpr size_t wstride = 8320;
-    static constexpr size_t wbytes = 64 * 16 * 8 + 16 * 4;   // 8256
-    static constexpr size_t slope = wraw + 2 * wstride;      // [2][16] float
-    static constexpr size_t bars = slope + 128;              // mbarriers
-    static constexpr int NBAR = 2 * S + 2 * 2 + 2 * 5;       // yfull, yfree | ylofull, ylofree | wfull, bready, accfull, tfree, spare
+    static constexpr size_t slope = B + 2 * bset;            // [4][16] float (unit i -> slot i & 3)
+    static constexpr size_t bars = slope + 256;              // mbarriers
+    static constexpr int NBAR = 2 * S + 2 * NLO + 2 * 3;     // yfull, yfree | ylofull, ylofree | bready, accfull, tfree
     static constexpr size_t tslot = bars + NBAR * 8;
     static constexpr size_t total = tslot + 16 + 1024;
-    static constexpr int THREADS = 288;
+    static_assert(B % 1024 == 0 && ylo % 1024 == 0, "UMMA operand alignment");
+    static_assert(total <= 227 * 1024, "shared memory");
 };
-static_assert(Ap4::B % 1024 == 0 && Ap4::ylo % 1024 == 0, "UMMA operand alignment");
 
-template <int NR, int NL, int QM, int LT>
-__global__ void __launch_bounds__(Ap4::THREADS, 1) k_big_apply4(DetectArgs a, const __grid_constant__ CUtensorMap ymap) {
+template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_>
+__global__ void __launch_bounds__(32 * (5 + EW), 1) k_big_apply4(DetectArgs a, const __grid_constant__ CUtensorMap ymap) {
+    using A4 = Ap4<S_, NLO_>;
+    constexpr int CW = 4 + EW;  // control warp
+    constexpr int NLO = NLO_;
     static_assert(NL == 16 && NR == 64, "k_big_apply4: 64 x 16");
     constexpr int WS = BigWs<NR, NL>::stride;
-    constexpr int S = Ap4::S;
+    constexpr int S = A4::S;
     extern __shared__ unsigned char smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     unsigned char* g = smem_raw + (base - raw);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(g + Ap4::bars);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(g + A4::bars);
     uint64_t* yfull = bar;            // [S]  TMA tx
     uint64_t* yfree = bar + S;        // [S]  MMA1 commit + converters (count 2)
-    uint64_t* ylofull = bar + 2 * S;  // [2]  converters
-    uint64_t* ylofree = ylofull + 2;  // [2]  MMA2 commit
-    uint64_t* wfull = ylofree + 2;    // [2]  W~ bulk copy tx
-    uint64_t* bready = wfull + 2;     // [2]  converters
+    uint64_t* ylofull = bar + 2 * S;  // [NLO]  converters
+    uint64_t* ylofree = ylofull + NLO;  // [NLO]  MMA2 commit
+    uint64_t* bready = ylofree + NLO;  // [2]  converters
     uint64_t* accfull = bready + 2;   // [2]  commit after the unit's last MMA
     uint64_t* tfree = accfull + 2;    // [2]  epilogue done with the TMEM buffer
-    uint32_t* tslot = reinterpret_cast<uint32_t*>(g + Ap4::tslot);
-    float* sslope = reinterpret_cast<float*>(g + Ap4::slope);
+    uint32_t* tslot = reinterpret_cast<uint32_t*>(g + A4::tslot);
+    float* sslope = reinterpret_cast<float*>(g + A4::slope);
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const long long u0 = blockIdx.x, du = gridDim.x;
     const long long n_my = u0 < a.n_units ? (a.n_units - u0 + du - 1) / du : 0;
@@ -1714,17 +858,18 @@ __global__ void __launch_bounds__(Ap4::THREADS, 1) k_big_apply4(DetectArgs a, co
             mbar_init(&yfull[i], 1);
             mbar_init(&yfree[i], 2);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < NLO; ++i) {
             mbar_init(&ylofull[i], 1);
             mbar_init(&ylofree[i], 1);
-            mbar_init(&wfull[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
             mbar_init(&bready[i], 1);
             mbar_init(&accfull[i], 1);
             mbar_init(&tfree[i], 1);
         }
         fence_mbar_init();
     }
-    if (warp == 8) {
+    if (warp == CW) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tslot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
@@ -1736,39 +881,30 @@ __global__ void __launch_bounds__(Ap4::THREADS, 1) k_big_apply4(DetectArgs a, co
     auto issue_y = [&](long long gg) {
         const long long uu = u0 + (gg >> 2) * du;
         const int slot = (int)(uu / a.n_fb), fb = (int)(uu % a.n_fb), st = (int)(gg % S);
-        mbar_arrive_expect_tx(&yfull[st], (uint32_t)Ap4::chunk);
-        tma_load_3d(base + (uint32_t)(Ap4::y0 + st * Ap4::chunk), &ymap, 32 * (int)(gg & 3), fb * kSc, slot * kSym,
+        mbar_arrive_expect_tx(&yfull[st], (uint32_t)A4::chunk);
+        tma_load_3d(base + (uint32_t)(A4::y0 + st * A4::chunk), &ymap, 32 * (int)(gg & 3), fb * kSc, slot * kSym,
                     &yfull[st]);
     };
-    auto issue_w = [&](long long i) {
-        const int b = (int)(i & 1);
-        mbar_arrive_expect_tx(&wfull[b], (uint32_t)Ap4::wbytes);
-        bulk_g2s(g + Ap4::wraw + b * Ap4::wstride, reinterpret_cast<const float*>(a.ws) + (u0 + i * du) * WS,
-                 (uint32_t)Ap4::wbytes, &wfull[b]);
-    };
 
-    if (warp == 8) {
+    if (warp == CW) {
         // ================= control: TMA producer + MMA issuer =================
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ymap)) : "memory");
             for (long long gg = 0; gg < S && gg < G; ++gg) issue_y(gg);
-            pdl_wait();  // W~ of this call's setup kernel is complete
-            for (long long i = 0; i < 2 && i < n_my; ++i) issue_w(i);
             constexpr uint32_t id64 = (1u << 4) | (2u << 7) | (2u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
             constexpr uint32_t id32 = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
 #pragma unroll 1
             for (long long i = 0; i < n_my; ++i) {
                 const int b = (int)(i & 1);
                 mbar_wait(&bready[b], (uint32_t)((i >> 1) & 1));
-                if (i + 2 < n_my) issue_w(i + 2);  // W~ buffer b was consumed by B(i)
                 if (i >= 2) mbar_wait(&tfree[b], (uint32_t)(((i >> 1) + 1) & 1));
                 const uint32_t acc = tmem + 128u * (uint32_t)b;
-                const uint32_t bb = base + (uint32_t)(Ap4::B + b * Ap4::bset);
+                const uint32_t bb = base + (uint32_t)(A4::B + b * A4::bset);
 #pragma unroll 1
                 for (int c = 0; c < 4; ++c) {
                     const long long gg = 4 * i + c;
-                    const int st = (int)(gg % S), lb = (int)(gg & 1);
-                    const uint32_t ys = base + (uint32_t)(Ap4::y0 + st * Ap4::chunk);
+                    const int st = (int)(gg % S), lb = (int)(gg % NLO);
+                    const uint32_t ys = base + (uint32_t)(A4::y0 + st * A4::chunk);
                     mbar_wait(&yfull[st], (uint32_t)((gg / S) & 1));
                     tc_fence_after();
 #pragma unroll
@@ -1778,9 +914,9 @@ __global__ void __launch_bounds__(Ap4::THREADS, 1) k_big_apply4(DetectArgs a, co
                             umma_tf32(acc + 64u * tile, umma_desc_sw128(ys + (tile ? 40u * 128u : 0u) + ks * 32u),
                                       umma_desc_sw128(bb + (uint32_t)c * 8192u + ks * 32u), id64, (c | ks) ? 1u : 0u);
                     umma_commit(&yfree[st]);
-                    mbar_wait(&ylofull[lb], (uint32_t)((gg >> 1) & 1));
+                    mbar_wait(&ylofull[lb], (uint32_t)((gg / NLO) & 1));
                     tc_fence_after();
-                    const uint32_t yl = base + (uint32_t)(Ap4::ylo + lb * Ap4::chunk);
+                    const uint32_t yl = base + (uint32_t)(A4::ylo + lb * A4::chunk);
 #pragma unroll
                     for (int tile = 0; tile < 2; ++tile)
 #pragma unroll
@@ -1798,41 +934,57 @@ __global__ void __launch_bounds__(Ap4::THREADS, 1) k_big_apply4(DetectArgs a, co
         }
     } else if (warp < 4) {
         // ================= converters =================
+        // W~ of the next unit is prefetched into registers (plain coherent loads; the setup kernel wrote it)
+        // while the current unit's chunks are converted.
         const int tc = t;  // 0..127
+        const int n = tc >> 2, kt = tc & 3, kk = n & 15;
+        const bool im_row = n >= 16;
+        pdl_wait();  // W~ of this call's setup kernel is complete and visible
+        float2 wv[16];
+        float slv = 0.f;
+        auto fetch = [&](long long i) {
+            const float2* src = reinterpret_cast<const float2*>(reinterpret_cast<const float*>(a.ws) + (u0 + i * du) * WS);
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                const int r0 = 16 * kt + 2 * c;
+                wv[2 * c] = src[r0 * NL + kk];
+                wv[2 * c + 1] = src[(r0 + 1) * NL + kk];
+            }
+            if (tc < NL) slv = reinterpret_cast<const float*>(src + NR * NL)[tc];
+        };
+        if (n_my > 0) fetch(0);
 #pragma unroll 1
         for (long long i = 0; i < n_my; ++i) {
             const int b = (int)(i & 1);
-            mbar_wait(&wfull[b], (uint32_t)((i >> 1) & 1));
-            if (i >= 2) mbar_wait(&tfree[b], (uint32_t)(((i >> 1) + 1) & 1));  // B(i-2) and slopes(i-2) no longer used
+            // B buffer b is free once unit i-2's MMAs completed; slopes use a 4-deep ring (unit i+4 reuses
+            // slot i & 3 only after accfull(i+2), which the control issues after tfree(i): epilogue(i) done)
+            if (i >= 2) mbar_wait(&accfull[b], (uint32_t)(((i >> 1) + 1) & 1));
             {
-                const float2* sW = reinterpret_cast<const float2*>(g + Ap4::wraw + b * Ap4::wstride);
-                const int n = tc >> 2, kt = tc & 3, kk = n & 15;
-                const bool im_row = n >= 16;
-                float* kb = reinterpret_cast<float*>(g + Ap4::B + b * Ap4::bset + (size_t)kt * 64 * 128);
+                float* kb = reinterpret_cast<float*>(g + A4::B + b * A4::bset + (size_t)kt * 64 * 128);
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
-                    const int r0 = 16 * kt + 2 * c;
-                    const float2 w0 = sW[r0 * NL + kk], w1 = sW[(r0 + 1) * NL + kk];
+                    const float2 w0 = wv[2 * c], w1 = wv[2 * c + 1];
                     const float4 v = im_row ? make_float4(w0.y, w0.x, w1.y, w1.x) : make_float4(w0.x, -w0.y, w1.x, -w1.y);
                     const float4 lo = make_float4(v.x - tf32_trunc(v.x), v.y - tf32_trunc(v.y), v.z - tf32_trunc(v.z),
                                                   v.w - tf32_trunc(v.w));
                     *reinterpret_cast<float4*>(kb + n * 32 + ((c ^ (n & 7)) << 2)) = v;
                     *reinterpret_cast<float4*>(kb + (n + 32) * 32 + ((c ^ (n & 7)) << 2)) = lo;
                 }
-                if (tc < NL) sslope[b * 16 + tc] = reinterpret_cast<const float*>(sW + 64 * NL)[tc];
+                if (tc < NL) sslope[(i & 3) * 16 + tc] = slv;
             }
             fence_proxy_async();
             asm volatile("bar.sync 1, 128;" ::: "memory");
             if (tc == 0) mbar_arrive(&bready[b]);
+            if (i + 1 < n_my) fetch(i + 1);
 #pragma unroll 1
             for (int c = 0; c < 4; ++c) {
                 const long long gg = 4 * i + c;
-                const int st = (int)(gg % S), lb = (int)(gg & 1);
+                const int st = (int)(gg % S), lb = (int)(gg % NLO);
                 mbar_wait(&yfull[st], (uint32_t)((gg / S) & 1));
-                if (gg >= 2) mbar_wait(&ylofree[lb], (uint32_t)(((gg >> 1) + 1) & 1));
-                const float4* src = reinterpret_cast<const float4*>(g + Ap4::y0 + st * Ap4::chunk);
-                float4* dst = reinterpret_cast<float4*>(g + Ap4::ylo + lb * Ap4::chunk);
-                constexpr int n4 = (int)(Ap4::chunk / 16);
+                if (gg >= NLO) mbar_wait(&ylofree[lb], (uint32_t)(((gg / NLO) + 1) & 1));
+                const float4* src = reinterpret_cast<const float4*>(g + A4::y0 + st * A4::chunk);
+                float4* dst = reinterpret_cast<float4*>(g + A4::ylo + lb * A4::chunk);
+                constexpr int n4 = (int)(A4::chunk / 16);
 #pragma unroll 4
                 for (int q = tc; q < n4; q += 128) {
                     float4 v = src[q];
@@ -1852,8 +1004,12 @@ __global__ void __launch_bounds__(Ap4::THREADS, 1) k_big_apply4(DetectArgs a, co
         }
     } else {
         // ================= epilogue =================
-        const int we = warp - 4;  // TMEM lane quadrant
+        // EW = 4: warp 4+q reads TMEM lane quadrant q, all 16 layers of its RE rows;
+        // EW = 8: warps 4+q and 8+q share quadrant q, layers 8h .. 8h+7 each (h = e >> 2).
+        const int e = warp - 4, we = e & 3, h = EW == 8 ? (e >> 2) : 0;
+        constexpr int KL = EW == 8 ? NL / 2 : NL;  // layers per thread
         constexpr int kRec = NL * QM * LlrTraits<LT>::bytes;
+        constexpr int kPiece = KL * QM * LlrTraits<LT>::bytes;
         const bool zf = !(a.sigma2 > 0.f);
         const float ia = rsqrtf((float)qam_norm(QM));
 #pragma unroll 1
@@ -1866,49 +1022,68 @@ __global__ void __launch_bounds__(Ap4::THREADS, 1) k_big_apply4(DetectArgs a, co
 #pragma unroll 1
             for (int tile = 0; tile < 2; ++tile) {
                 if (tile == 1 && we < 2) break;
-                uint32_t hv[32], lv[32];
-                const uint32_t taddr = tmem + ((uint32_t)(32 * we) << 16) + 128u * (uint32_t)b + 64u * tile;
-                tmem_ld32(taddr, hv);
-                tmem_ld32(taddr + 32u, lv);
+                uint32_t hr[KL], hi[KL], lr[KL], li[KL];
+                const uint32_t taddr = tmem + ((uint32_t)(32 * we) << 16) + 128u * (uint32_t)b + 64u * tile + KL * h;
+                if constexpr (KL == 16) {
+                    uint32_t hv[32], lv[32];
+                    tmem_ld32(taddr, hv);
+                    tmem_ld32(taddr + 32u, lv);
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) {
+                        hr[k] = hv[k];
+                        hi[k] = hv[16 + k];
+                        lr[k] = lv[k];
+                        li[k] = lv[16 + k];
+                    }
+                } else {
+                    tmem_ld8(taddr, hr);
+                    tmem_ld8(taddr + 16u, hi);
+                    tmem_ld8(taddr + 32u, lr);
+                    tmem_ld8(taddr + 48u, li);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                }
                 const int row = (tile ? 40 : 0) + 32 * we + lane;
                 if (tile == 1 && row < 128) continue;
                 const int s = row / kSc, f = row % kSc;
                 const size_t re = (size_t)(slot * kSym + s) * a.n_sc + fb * kSc + f;
-                float2 x[NL];
+                float2 x[KL];
 #pragma unroll
-                for (int k = 0; k < NL; ++k)
-                    x[k] = make_float2(__uint_as_float(hv[k]) + __uint_as_float(lv[k]),
-                                       __uint_as_float(hv[16 + k]) + __uint_as_float(lv[16 + k]));
+                for (int k = 0; k < KL; ++k)
+                    x[k] = make_float2(__uint_as_float(hr[k]) + __uint_as_float(lr[k]),
+                                       __uint_as_float(hi[k]) + __uint_as_float(li[k]));
+                const float* sl = sslope + (i & 3) * 16 + KL * h;
                 if (a.llr) {
-                    float v[NL * QM];
-                    uint32_t wd[(kRec + 3) / 4];
+                    float v[KL * QM];
+                    uint32_t wd[(kPiece + 3) / 4];
                     if (!zf) {
 #pragma unroll
-                        for (int k = 0; k < NL; ++k) demap_layer<QM, false, LT>(x[k], sslope[b * 16 + k], v + k * QM);
-                        pack_llr<LT, NL * QM, false>(v, wd);
+                        for (int k = 0; k < KL; ++k) demap_layer<QM, false, LT>(x[k], sl[k], v + k * QM);
+                        pack_llr<LT, KL * QM, false>(v, wd);
                     } else {
 #pragma unroll
-                        for (int k = 0; k < NL; ++k) demap_layer<QM, true, LT>(x[k], sslope[b * 16 + k], v + k * QM);
-                        pack_llr<LT, NL * QM, true>(v, wd);
+                        for (int k = 0; k < KL; ++k) demap_layer<QM, true, LT>(x[k], sl[k], v + k * QM);
+                        pack_llr<LT, KL * QM, true>(v, wd);
                     }
-                    store_bytes<kRec>((char*)a.llr + re * kRec, wd);
+                    store_bytes<kPiece>((char*)a.llr + re * kRec + h * kPiece, wd);
                 }
                 if (a.xhat) {
 #pragma unroll
-                    for (int k = 0; k < NL; ++k) a.xhat[re * NL + k] = make_float2(x[k].x * ia, x[k].y * ia);
+                    for (int k = 0; k < KL; ++k)
+                        a.xhat[re * NL + KL * h + k] = make_float2(x[k].x * ia, x[k].y * ia);
                 }
             }
             tc_fence_before();
-            asm volatile("bar.sync 2, 128;" ::: "memory");
+            if constexpr (EW == 8) asm volatile("bar.sync 2, 256;" ::: "memory");
+            else asm volatile("bar.sync 2, 128;" ::: "memory");
             if (t == 128) mbar_arrive(&tfree[b]);
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 8) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    if (warp == CW) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
 }
 
-template <int NR, int NL, int QM, int LT>
+template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_>
 cudaError_t launch_ap4(const DetectArgs& a, cudaStream_t s) {
     if (a.n_units <= 0) return cudaSuccess;
     static int n_sm = 0;
@@ -1934,71 +1109,24 @@ cudaError_t launch_ap4(const DetectArgs& a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(a.n_units < n_sm ? a.n_units : n_sm));
-    cfg.blockDim = dim3(Ap4::THREADS);
-    cfg.dynamicSmemBytes = Ap4::total;
+    cfg.blockDim = dim3(32 * (5 + EW));
+    cfg.dynamicSmemBytes = Ap4<S_, NLO_>::total;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = a.overlap ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, k_big_apply4<NR, NL, QM, LT>, a, ymap);
+    return cudaLaunchKernelEx(&cfg, k_big_apply4<NR, NL, QM, LT, EW, S_, NLO_>, a, ymap);
 }
 
-template <int NR, int NL, int QM, int LT>
+template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_>
 cudaError_t prepare_ap4() {
     cudaError_t e = cudaFuncSetAttribute(k_big_setup<NR, NL, QM, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(4 * SetupSmem<NR, NL>::per_unit));
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_big_apply4<NR, NL, QM, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)Ap4::total);
-}
-
-template <int NR, int NL, int QM, int LT>
-cudaError_t launch_tc3(const DetectArgs& a, cudaStream_t s) {
-    if (a.n_units <= 0) return cudaSuccess;
-    static int n_sm = 0;
-    if (!n_sm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
-    }
-    auto enc = tensor_map_encoder();
-    if (!enc) return cudaErrorNotSupported;
-    CUtensorMap ymap;
-    const cuuint64_t gdim[3] = {(cuuint64_t)(2 * NR), (cuuint64_t)a.n_sc, (cuuint64_t)a.n_sym};
-    const cuuint64_t gstride[2] = {(cuuint64_t)NR * 8, (cuuint64_t)a.n_sc * NR * 8};
-    const cuuint32_t box[3] = {32, (cuuint32_t)kSc, 7};
-    const cuuint32_t estride[3] = {1, 1, 1};
-    if (enc(&ymap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float2*>(a.y), gdim, gstride, box, estride,
-            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return cudaErrorInvalidValue;
-    constexpr int UPB = 4;
-    cudaError_t e = launch_kernel(k_big_setup<NR, NL, QM, UPB>, dim3((unsigned)((a.n_units + UPB - 1) / UPB)),
-                                  dim3(32 * UPB), UPB * SetupSmem<NR, NL>::per_unit, s, a.overlap, a);
-    if (e != cudaSuccess) return e;
-    const unsigned grid = (unsigned)(a.n_units < n_sm ? a.n_units : n_sm);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kTc2Simt + 32);
-    cfg.dynamicSmemBytes = Tc3::total;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = a.overlap ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, k_big_tc3<NR, NL, QM, LT>, a, ymap);
-}
-
-template <int NR, int NL, int QM, int LT>
-cudaError_t prepare_tc3() {
-    cudaError_t e = cudaFuncSetAttribute(k_big_setup<NR, NL, QM, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(4 * SetupSmem<NR, NL>::per_unit));
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_big_tc3<NR, NL, QM, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)Tc3::total);
+    return cudaFuncSetAttribute(k_big_apply4<NR, NL, QM, LT, EW, S_, NLO_>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ap4<S_, NLO_>::total);
 }
 
 template <int NR, int NL>
@@ -2029,24 +1157,6 @@ cudaError_t prepare() {
 #define BIG_ENTRY(NAME, NR, NL, QM, LT) \
     KernelEntry { NAME, NR, NL, QM, kSc, 14, LT, 32, 2, launch<NR, NL, QM, LT>, prepare<NR, NL, QM, LT>, workspace<NR, NL> }
 
-#define BIGTC_ENTRY(NAME, NR, NL, QM, LT)                                                                 \
-    KernelEntry {                                                                                         \
-        NAME, NR, NL, QM, kSc, 14, LT, 32, 2, launch_tc<NR, NL, QM, LT>, prepare_tc<NR, NL, QM, LT>,     \
-            workspace<NR, NL>                                                                             \
-    }
-
-#define BIGTC2_ENTRY(NAME, NR, NL, QM, LT)                                                                \
-    KernelEntry {                                                                                         \
-        NAME, NR, NL, QM, kSc, 14, LT, 32, 2, launch_tc2<NR, NL, QM, LT>, prepare_tc2<NR, NL, QM, LT>,   \
-            workspace<NR, NL>                                                                             \
-    }
-
-#define BIGTC3_ENTRY(NAME, NR, NL, QM, LT)                                                                \
-    KernelEntry {                                                                                         \
-        NAME, NR, NL, QM, kSc, 14, LT, 32, 2, launch_tc3<NR, NL, QM, LT>, prepare_tc3<NR, NL, QM, LT>,   \
-            workspace<NR, NL>                                                                             \
-    }
-
 #define BIGAP2_ENTRY(NAME, NR, NL, QM, LT)                                                               \
     KernelEntry {                                                                                         \
         NAME, NR, NL, QM, kSc, 14, LT, 32, 2, launch_ap2<NR, NL, QM, LT>, prepare_ap2<NR, NL, QM, LT>,   \
@@ -2054,15 +1164,18 @@ cudaError_t prepare() {
     }
 
 const KernelEntry kEntries[] = {
-    BIGAP2_ENTRY("big2_64x16_q6_i8", 64, 16, 6, kLlrI8),  // C5 (K-streamed SIMT GEMM; currently the fastest)
+#define BIG4_ENTRY(NAME, EW, S, NLO)                                                                       \
+    KernelEntry {                                                                                          \
+        NAME, 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, EW, S, NLO>,                \
+            prepare_ap4<64, 16, 6, kLlrI8, EW, S, NLO>, workspace<64, 16>                                  \
+    }
+    BIG4_ENTRY("big4_64x16_q6_i8", 4, 4, 2),  // C5 default: tcgen05 3-pass TF32 apply (fastest)
+    BIG4_ENTRY("big4e8_64x16_q6_i8", 8, 4, 2),
+    BIG4_ENTRY("big4s5_64x16_q6_i8", 4, 5, 2),
+    BIGAP2_ENTRY("big2_64x16_q6_i8", 64, 16, 6, kLlrI8),  // SIMT K-streamed apply
     BIG_ENTRY("big_64x16_q6_i8", 64, 16, 6, kLlrI8),
     KernelEntry{"big3_64x16_q6_i8", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap3<64, 16, 6, kLlrI8>,
                 prepare_ap3<64, 16, 6, kLlrI8>, workspace<64, 16>},
-    KernelEntry{"big4_64x16_q6_i8", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8>,
-                prepare_ap4<64, 16, 6, kLlrI8>, workspace<64, 16>},
-    BIGTC3_ENTRY("bigtc3_64x16_q6_i8", 64, 16, 6, kLlrI8),
-    BIGTC2_ENTRY("bigtc2_64x16_q6_i8", 64, 16, 6, kLlrI8),  // tensor cores, warp-specialised
-    BIGTC_ENTRY("bigtc_64x16_q6_i8", 64, 16, 6, kLlrI8),
     BIG_ENTRY("big_64x16_q6_f16", 64, 16, 6, kLlrF16),
     BIG_ENTRY("big_64x16_q6_f32", 64, 16, 6, kLlrF32),
     BIG_ENTRY("big_64x16_q8_i8", 64, 16, 8, kLlrI8),
