@@ -534,6 +534,254 @@ cudaError_t prepare2() {
     return cudaSuccess;
 }
 
+// k_lg3: k_lg with the CTA's whole y tile (14 symbols x TU subcarriers x NR
+// antennas) fetched by ONE TMA tensor-box copy (3-D map {2 NR floats, n_sc,
+// n_sym}, box {2 NR, TU, 14}, SWIZZLE_128B) instead of 14 small bulk copies per
+// unit: the copy engine generates the 128-byte rows itself (tools/tmabench.cu:
+// tensor boxes stream at ~7 TB/s, per-row bulk copies are request-rate bound).
+// Row = 14-symbol index x TU + unit; the 16-byte chunk c of a row sits at
+// c ^ (row & 7), so the UPW units of a warp reading the same antennas hit
+// different bank groups (no padding needed). Ragged tails are zero-filled by TMA.
+template <int NR, int NL, int NW>
+struct Lg3Smem {
+    static constexpr int UPW = 32 / NL;
+    static constexpr int TU = UPW * NW;
+    static constexpr int HS = NR * NL + 4;                                  // float2 per unit H (padded)
+    static constexpr int LS = NL * NL + 4;                                  // float2 per unit L / X
+    static constexpr size_t y = 0;                                          // [14][TU][NR] float2, SW128
+    static constexpr size_t H = (size_t)kSym * TU * NR * 8;                 // [TU][HS]
+    static constexpr size_t LX = H + (size_t)TU * HS * 8;                   // [TU][LS]
+    static constexpr size_t dinv = LX + (size_t)TU * LS * 8;                // [TU][NL]
+    static constexpr size_t bars = (dinv + (size_t)TU * NL * 4 + 7) / 8 * 8;  // y, H
+    static constexpr size_t total = bars + 16 + 1024;                       // + 1024-alignment slack
+};
+
+template <int NR, int NL, int QM, int LT, int NW>
+__global__ void __launch_bounds__(32 * NW) k_lg3(DetectArgs a, const __grid_constant__ CUtensorMap ymap) {
+    using SM = Lg3Smem<NR, NL, NW>;
+    constexpr int UPW = SM::UPW;
+    constexpr int TU = SM::TU;
+    static_assert(32 % NL == 0 && NR * 8 == 128, "k_lg3: one 128-byte row per (symbol, unit)");
+    extern __shared__ unsigned char smem_raw[];
+    const uint32_t raw = smem_u32(smem_raw);
+    const uint32_t base = (raw + 1023u) & ~1023u;
+    unsigned char* smem = smem_raw + (base - raw);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SM::bars);
+    float2* sH = reinterpret_cast<float2*>(smem + SM::H);
+    float2* sLX = reinterpret_cast<float2*>(smem + SM::LX);
+    float* sDinv = reinterpret_cast<float*>(smem + SM::dinv);
+
+    pdl_launch_dependents();
+    const int slot = blockIdx.y;
+    const int sc0 = blockIdx.x * TU;
+    const int nvalid = min(TU, a.n_sc - sc0);
+    const int t = threadIdx.x;
+    const int lane = t & 31, warp = t >> 5;
+    const int k = lane % NL;                     // this lane's layer
+    const int gbase = lane - k;                  // first lane of the group
+    const int ul = warp * UPW + lane / NL;       // unit within the tile
+    const bool active = ul < nvalid;
+    const int sc = sc0 + ul;
+    const float s2 = a.sigma2;
+    const float norm = (float)qam_norm(QM);
+
+    if (t == 0) {
+        mbar_init(&bars[0], 1);
+        mbar_init(&bars[1], 1);
+        fence_mbar_init();
+        mbar_arrive_expect_tx(&bars[0], (uint32_t)(kSym * TU * NR * 8));
+        tma_load_3d(base + (uint32_t)SM::y, &ymap, 0, sc0, slot * kSym, &bars[0]);
+        mbar_arrive_expect_tx(&bars[1], (uint32_t)nvalid * NR * NL * 8u);
+    }
+    __syncthreads();
+    if (k == 0 && active)
+        bulk_g2s(sH + ul * SM::HS, a.H + ((size_t)slot * a.n_sc + sc) * NR * NL, NR * NL * 8u, &bars[1]);
+    mbar_wait(&bars[1], 0);
+
+    const float2* hU = sH + ul * SM::HS;
+    float2 g[NL];
+#pragma unroll
+    for (int j = 0; j < NL; ++j) g[j] = make_float2(0.f, 0.f);
+#pragma unroll 4
+    for (int r = 0; r < NR; ++r) {
+        const float2 hk = hU[r * NL + k];
+#pragma unroll
+        for (int j = 0; j < NL; ++j) {
+            const float2 hj = hU[r * NL + j];
+            g[j].x = fmaf(hk.x, hj.x, fmaf(hk.y, hj.y, g[j].x));
+            g[j].y = fmaf(hk.x, hj.y, fmaf(-hk.y, hj.x, g[j].y));
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
+        if (j == k) g[j] = make_float2(g[j].x + s2, 0.f);
+    float gmax = 0.f;
+#pragma unroll
+    for (int j = 0; j < NL; ++j)
+        if (j == k) gmax = g[j].x;
+#pragma unroll
+    for (int off = 1; off < NL; off <<= 1) gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, off));
+
+    bool fail = !(gmax == gmax);
+    float my_dinv = 0.f;
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+        float p = __shfl_sync(0xffffffffu, g[j].x, gbase + j);
+        if (!(p > (float)kPivotTau * gmax)) {
+            fail = true;
+            p = 1.f;
+        }
+        const float dinv = rsqrtf(p);
+        if (k == j) my_dinv = dinv;
+        if (k > j) g[j] = make_float2(g[j].x * dinv, g[j].y * dinv);
+#pragma unroll
+        for (int m = j + 1; m < NL; ++m) {
+            const float2 lmj = shfl2(g[j], gbase + m);
+            if (k >= m) {
+                g[m].x = fmaf(-g[j].x, lmj.x, fmaf(-g[j].y, lmj.y, g[m].x));
+                g[m].y = fmaf(-g[j].y, lmj.x, fmaf(g[j].x, lmj.y, g[m].y));
+            }
+        }
+    }
+    float2* lU = sLX + ul * SM::LS;
+#pragma unroll
+    for (int j = 0; j < NL; ++j) lU[k * NL + j] = (j < k) ? g[j] : make_float2(0.f, 0.f);
+    sDinv[ul * NL + k] = my_dinv;
+    __syncwarp();
+    float2 x[NL];
+#pragma unroll
+    for (int i = 0; i < NL; ++i) {
+        float2 sv = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int m = 0; m < i; ++m) sv = cmac(sv, lU[i * NL + m], x[m]);
+        const float di = sDinv[ul * NL + i];
+        x[i] = (i == k) ? make_float2(my_dinv, 0.f)
+                        : (i < k ? make_float2(0.f, 0.f) : make_float2(-sv.x * di, -sv.y * di));
+    }
+    float A = 0.f;
+#pragma unroll
+    for (int i = 0; i < NL; ++i) A = fmaf(x[i].x, x[i].x, fmaf(x[i].y, x[i].y, A));
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < NL; ++i) lU[i * NL + k] = x[i];
+    __syncwarp();
+    float2 gi[NL];
+#pragma unroll
+    for (int j = 0; j < NL; ++j) {
+        float2 sv = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int m = j; m < NL; ++m) {
+            const float2 xm = x[m], xmj = lU[m * NL + j];
+            sv.x = fmaf(xm.x, xmj.x, fmaf(xm.y, xmj.y, sv.x));
+            sv.y = fmaf(xm.x, xmj.y, fmaf(-xm.y, xmj.x, sv.y));
+        }
+        gi[j] = sv;
+    }
+    float sinr, fac;
+    const float mu = fmaf(-s2, A, 1.f);
+    if (s2 == 0.f) {
+        sinr = __int_as_float(0x7f800000);
+        fac = sqrtf(norm);
+    } else {
+        sinr = __fdividef(mu, s2 * A);
+        fac = __fdividef(sqrtf(norm), mu);
+    }
+    if (!(mu > 0.f) || fail) {
+        sinr = 0.f;
+        fac = 0.f;
+    }
+    const float slope = sinr / norm * a.llr_scale;
+    float2 w[NR];
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+        float2 sv = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int j = 0; j < NL; ++j) {
+            const float2 h = hU[r * NL + j];
+            sv.x = fmaf(gi[j].x, h.x, fmaf(gi[j].y, h.y, sv.x));
+            sv.y = fmaf(gi[j].y, h.x, fmaf(-gi[j].x, h.y, sv.y));
+        }
+        w[r] = (fac > 0.f) ? make_float2(sv.x * fac, sv.y * fac) : make_float2(0.f, 0.f);
+    }
+
+    pdl_wait();  // global writes only after the previous grid completed
+    if (active) {
+        const size_t unit = (size_t)slot * a.n_sc + sc;
+        if (k == 0 && fail) atomicAdd(a.fail_count, 1ull);
+        if (a.sinr) a.sinr[unit * NL + k] = sinr;
+    }
+    constexpr int kLlrBytes = QM * LlrTraits<LT>::bytes;
+    constexpr int kWords = (kLlrBytes + 3) / 4;
+    const float ia = rsqrtf(norm);
+    const bool zf = !(s2 > 0.f);
+    mbar_wait(&bars[0], 0);
+    if (!active) return;
+    const unsigned char* ybase = smem + SM::y;
+#pragma unroll 1
+    for (int s = 0; s < kSym; ++s) {
+        const int row = s * TU + ul;
+        const unsigned char* yr = ybase + row * 128;
+        const int sw = row & 7;
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int c = 0; c < NR / 2; ++c) {
+            const float4 v = *reinterpret_cast<const float4*>(yr + ((c ^ sw) << 4));
+            acc = cmac(acc, w[2 * c], make_float2(v.x, v.y));
+            acc = cmac(acc, w[2 * c + 1], make_float2(v.z, v.w));
+        }
+        const size_t re = (size_t)(slot * kSym + s) * a.n_sc + sc;
+        if (a.llr) {
+            float v[QM];
+            uint32_t wd[kWords];
+            if (!zf) {
+                demap_layer<QM, false, LT>(acc, slope, v);
+                pack_llr<LT, QM, false>(v, wd);
+            } else {
+                demap_layer<QM, true, LT>(acc, slope, v);
+                pack_llr<LT, QM, true>(v, wd);
+            }
+            store_bytes<kLlrBytes>((char*)a.llr + (re * NL + k) * kLlrBytes, wd);
+        }
+        if (a.xhat) a.xhat[re * NL + k] = make_float2(acc.x * ia, acc.y * ia);
+    }
+}
+
+template <int NR, int NL, int QM, int LT, int NW>
+cudaError_t launch3(const DetectArgs& a, cudaStream_t s) {
+    if (a.n_sc <= 0 || a.n_slots <= 0) return cudaSuccess;
+    constexpr int TU = Lg3Smem<NR, NL, NW>::TU;
+    auto enc = tensor_map_encoder();
+    if (!enc) return cudaErrorNotSupported;
+    CUtensorMap ymap;
+    const cuuint64_t gdim[3] = {(cuuint64_t)(2 * NR), (cuuint64_t)a.n_sc, (cuuint64_t)a.n_sym};
+    const cuuint64_t gstride[2] = {(cuuint64_t)NR * 8, (cuuint64_t)a.n_sc * NR * 8};
+    const cuuint32_t box[3] = {(cuuint32_t)(2 * NR), (cuuint32_t)TU, (cuuint32_t)kSym};
+    const cuuint32_t estride[3] = {1, 1, 1};
+    if (enc(&ymap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float2*>(a.y), gdim, gstride, box, estride,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return cudaErrorInvalidValue;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((a.n_sc + TU - 1) / TU, a.n_slots);
+    cfg.blockDim = dim3(32 * NW);
+    cfg.dynamicSmemBytes = Lg3Smem<NR, NL, NW>::total;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = a.overlap ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k_lg3<NR, NL, QM, LT, NW>, a, ymap);
+}
+
+template <int NR, int NL, int QM, int LT, int NW>
+cudaError_t prepare3() {
+    constexpr size_t smem = Lg3Smem<NR, NL, NW>::total;
+    if (smem > 48 * 1024)
+        return cudaFuncSetAttribute(k_lg3<NR, NL, QM, LT, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return cudaSuccess;
+}
+
 template <int NR, int NL, int QM, int LT, int NW>
 cudaError_t launch(const DetectArgs& a, cudaStream_t s) {
     if (a.n_sc <= 0 || a.n_slots <= 0) return cudaSuccess;
@@ -560,8 +808,14 @@ cudaError_t prepare() {
             prepare2<NR, NL, QM, LT, NW, R, SU>                                                        \
     }
 
+#define LG3_ENTRY(NAME, NR, NL, QM, LT, NW)                                                              \
+    KernelEntry { NAME, NR, NL, QM, 1, 14, LT, 32, 1, launch3<NR, NL, QM, LT, NW>, prepare3<NR, NL, QM, LT, NW> }
+
 const KernelEntry kEntries[] = {
-    LG_ENTRY("lg_16x8_q8_f16", 16, 8, 8, kLlrF16, 2),  // C4
+    LG3_ENTRY("lg3_16x8_q8_f16", 16, 8, 8, kLlrF16, 2),  // C4 (one TMA tensor box per CTA for y)
+    LG_ENTRY("lg_16x8_q8_f16", 16, 8, 8, kLlrF16, 2),
+    LG3_ENTRY("lg3_16x8_q8_f16_w1", 16, 8, 8, kLlrF16, 1),
+    LG3_ENTRY("lg3_16x8_q8_f16_w4", 16, 8, 8, kLlrF16, 4),
     LG2_ENTRY("lg2_16x8_q8_f16", 16, 8, 8, kLlrF16, 2, 4),
     LG2_ENTRY("lg2_16x8_q8_f16_r14", 16, 8, 8, kLlrF16, 2, 14),
     LG2S_ENTRY("lg2_16x8_q8_f16_r14s2", 16, 8, 8, kLlrF16, 2, 14, 2),
