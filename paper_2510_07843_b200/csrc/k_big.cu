@@ -804,10 +804,10 @@ struct Ap4 {
     static_assert(total <= 227 * 1024, "shared memory");
 };
 
-template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_>
-__global__ void __launch_bounds__(32 * (5 + EW), 1) k_big_apply4(DetectArgs a, const __grid_constant__ CUtensorMap ymap) {
+template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_, int ABL>
+__global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, const __grid_constant__ CUtensorMap ymap) {
     using A4 = Ap4<S_, NLO_>;
-    constexpr int CW = 4 + EW;  // control warp
+    constexpr int CW = 4 + EW;  // control warp (MMA issuer); CW + 1: TMA producer
     constexpr int NLO = NLO_;
     static_assert(NL == 16 && NR == 64, "k_big_apply4: 64 x 16");
     constexpr int WS = BigWs<NR, NL>::stride;
@@ -865,11 +865,20 @@ __global__ void __launch_bounds__(32 * (5 + EW), 1) k_big_apply4(DetectArgs a, c
                     &yfull[st]);
     };
 
-    if (warp == CW) {
-        // ================= control: TMA producer + MMA issuer =================
+    if (warp == CW + 1) {
+        // ================= TMA producer: y chunks, S stages ahead =================
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ymap)) : "memory");
-            for (long long gg = 0; gg < S && gg < G; ++gg) issue_y(gg);
+#pragma unroll 1
+            for (long long gg = 0; gg < G; ++gg) {
+                const int st = (int)(gg % S);
+                if (gg >= S) mbar_wait(&yfree[st], (uint32_t)(((gg / S) + 1) & 1));  // MMA1 + conversion of gg - S
+                issue_y(gg);
+            }
+        }
+    } else if (warp == CW) {
+        // ================= control: MMA issuer =================
+        if (lane == 0) {
             constexpr uint32_t id64 = (1u << 4) | (2u << 7) | (2u << 10) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
             constexpr uint32_t id32 = (1u << 4) | (2u << 7) | (2u << 10) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
 #pragma unroll 1
@@ -904,10 +913,6 @@ __global__ void __launch_bounds__(32 * (5 + EW), 1) k_big_apply4(DetectArgs a, c
                                       umma_desc_sw128(bb + (uint32_t)c * 8192u + ks * 32u), id32, 1u);
                     umma_commit(&ylofree[lb]);
                     if (c == 3) umma_commit(&accfull[b]);
-                    if (gg + S < G) {  // refill stage st once MMA1(gg) and the conversion of gg are done
-                        mbar_wait(&yfree[st], (uint32_t)((gg / S) & 1));
-                        issue_y(gg + S);
-                    }
                 }
             }
         }
@@ -964,14 +969,16 @@ __global__ void __launch_bounds__(32 * (5 + EW), 1) k_big_apply4(DetectArgs a, c
                 const float4* src = reinterpret_cast<const float4*>(g + A4::y0 + st * A4::chunk);
                 float4* dst = reinterpret_cast<float4*>(g + A4::ylo + lb * A4::chunk);
                 constexpr int n4 = (int)(A4::chunk / 16);
+                if constexpr (!(ABL & 1)) {  // ABL: timing ablations (wrong results), never selected by default
 #pragma unroll 4
-                for (int q = tc; q < n4; q += 128) {
-                    float4 v = src[q];
-                    v.x -= tf32_trunc(v.x);
-                    v.y -= tf32_trunc(v.y);
-                    v.z -= tf32_trunc(v.z);
-                    v.w -= tf32_trunc(v.w);
-                    dst[q] = v;
+                    for (int q = tc; q < n4; q += 128) {
+                        float4 v = src[q];
+                        v.x -= tf32_trunc(v.x);
+                        v.y -= tf32_trunc(v.y);
+                        v.z -= tf32_trunc(v.z);
+                        v.w -= tf32_trunc(v.w);
+                        dst[q] = v;
+                    }
                 }
                 fence_proxy_async();
                 asm volatile("bar.sync 1, 128;" ::: "memory");
@@ -1031,7 +1038,7 @@ __global__ void __launch_bounds__(32 * (5 + EW), 1) k_big_apply4(DetectArgs a, c
                     x[k] = make_float2(__uint_as_float(hr[k]) + __uint_as_float(lr[k]),
                                        __uint_as_float(hi[k]) + __uint_as_float(li[k]));
                 const float* sl = sslope + (i & 3) * 16 + KL * h;
-                if (a.llr) {
+                if (a.llr && !(ABL & 2)) {
                     float v[KL * QM];
                     uint32_t wd[(kPiece + 3) / 4];
                     if (!zf) {
@@ -1062,7 +1069,7 @@ __global__ void __launch_bounds__(32 * (5 + EW), 1) k_big_apply4(DetectArgs a, c
     if (warp == CW) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
 }
 
-template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_>
+template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_, int ABL = 0>
 cudaError_t launch_ap4(const DetectArgs& a, cudaStream_t s) {
     if (a.n_units <= 0) return cudaSuccess;
     static int n_sm = 0;
@@ -1088,7 +1095,7 @@ cudaError_t launch_ap4(const DetectArgs& a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(a.n_units < n_sm ? a.n_units : n_sm));
-    cfg.blockDim = dim3(32 * (5 + EW));
+    cfg.blockDim = dim3(32 * (6 + EW));
     cfg.dynamicSmemBytes = Ap4<S_, NLO_>::total;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -1096,15 +1103,15 @@ cudaError_t launch_ap4(const DetectArgs& a, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = a.overlap ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, k_big_apply4<NR, NL, QM, LT, EW, S_, NLO_>, a, ymap);
+    return cudaLaunchKernelEx(&cfg, k_big_apply4<NR, NL, QM, LT, EW, S_, NLO_, ABL>, a, ymap);
 }
 
-template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_>
+template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_, int ABL = 0>
 cudaError_t prepare_ap4() {
     cudaError_t e = cudaFuncSetAttribute(k_big_setup<NR, NL, QM, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(4 * SetupSmem<NR, NL>::per_unit));
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_big_apply4<NR, NL, QM, LT, EW, S_, NLO_>,
+    return cudaFuncSetAttribute(k_big_apply4<NR, NL, QM, LT, EW, S_, NLO_, ABL>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ap4<S_, NLO_>::total);
 }
 
@@ -1151,6 +1158,13 @@ const KernelEntry kEntries[] = {
     BIG4_ENTRY("big4_64x16_q6_i8", 4, 4, 2),  // C5 default: tcgen05 3-pass TF32 apply (fastest)
     BIG4_ENTRY("big4e8_64x16_q6_i8", 8, 4, 2),
     BIG4_ENTRY("big4s5_64x16_q6_i8", 4, 5, 2),
+    // timing ablations (results are wrong on purpose; only reachable through MIMO_FORCE_KERNEL)
+    KernelEntry{"ablation_big4_noconv", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 1>,
+                prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 1>, workspace<64, 16>},
+    KernelEntry{"ablation_big4_noepi", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 2>,
+                prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 2>, workspace<64, 16>},
+    KernelEntry{"ablation_big4_none", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 3>,
+                prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 3>, workspace<64, 16>},
     BIGAP2_ENTRY("big2_64x16_q6_i8", 64, 16, 6, kLlrI8),  // SIMT K-streamed apply
     BIG_ENTRY("big_64x16_q6_i8", 64, 16, 6, kLlrI8),
     KernelEntry{"big3_64x16_q6_i8", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap3<64, 16, 6, kLlrI8>,
