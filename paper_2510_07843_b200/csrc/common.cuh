@@ -52,6 +52,49 @@ __device__ __forceinline__ float2 cmac(float2 acc, float2 a, float2 b) {   // ac
     acc.y = fmaf(a.y, b.x, acc.y);
     return acc;
 }
+// ---- packed fp32x2 (FFMA2, sm_100): two fp32 FMAs per instruction. A plain 3-register
+// FFMA issues at half the FMA pipe's rate on Blackwell, so complex MACs written as two
+// FFMA2 (with broadcast / half-swapped operands, which the ISA encodes for free) halve
+// the FMA-pipe instruction count of the SIMT GEMM-like loops.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {  // (a.x b.x + c.x, a.y b.y + c.y)
+    unsigned long long ua, ub, uc, d;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(ua) : "f"(a.x), "f"(a.y));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(ub) : "f"(b.x), "f"(b.y));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(uc) : "f"(c.x), "f"(c.y));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(ua), "l"(ub), "l"(uc));
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(d));
+    return r;
+}
+// A complex coefficient w pre-packed for acc += w * y:  (w.x, w.x) * y + (-w.y, w.y) * swap(y)
+struct CPack {
+    float2 xx, ny;
+};
+__device__ __forceinline__ CPack cpack(float2 w) { return CPack{make_float2(w.x, w.x), make_float2(-w.y, w.y)}; }
+// ... and for acc += conj(w) * y:  (w.x, w.x) * y + (w.y, -w.y) * swap(y)
+__device__ __forceinline__ CPack cpack_conj(float2 w) { return CPack{make_float2(w.x, w.x), make_float2(w.y, -w.y)}; }
+__device__ __forceinline__ float2 cmac_p(float2 acc, const CPack& w, float2 y) {
+    acc = ffma2(w.xx, y, acc);
+    return ffma2(w.ny, make_float2(y.y, y.x), acc);
+}
+// acc + w * conj(y):  (w.x, w.y) * y.x + (w.y, -w.x) * y.y  ==  (w.x, w.x)... written for a fixed w:
+// acc.x += w.x y.x + w.y y.y ; acc.y += w.y y.x - w.x y.y
+struct CPackC {
+    float2 a, b;  // a = (w.x, w.y) * y.x ; b = (w.y, -w.x) * y.y
+};
+__device__ __forceinline__ CPackC cpackc(float2 w) { return CPackC{w, make_float2(w.y, -w.x)}; }
+__device__ __forceinline__ float2 cmacc_p(float2 acc, const CPackC& w, float2 y) {  // acc + w * conj(y)
+    acc = ffma2(w.a, make_float2(y.x, y.x), acc);
+    return ffma2(w.b, make_float2(y.y, y.y), acc);
+}
+
+// acc + w * y with y shared by several w: ny = (-y.y, y.x) computed once per y,
+// w's halves used as broadcast scalars (free operand forms of FFMA2).
+__device__ __forceinline__ float2 cmac_y(float2 acc, float2 w, float2 y, float2 ny) {
+    acc = ffma2(make_float2(w.x, w.x), y, acc);
+    return ffma2(make_float2(w.y, w.y), ny, acc);
+}
+
 __device__ __forceinline__ double2 dmul(double2 a, double2 b) {
     return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }

@@ -82,16 +82,14 @@ __global__ void __launch_bounds__(32 * UPB) k_big_setup(DetectArgs a) {
 #pragma unroll
         for (int q = 0; q < 8; ++q) gq[q] = make_float2(0.f, 0.f);
 #pragma unroll 4
-        for (int r = 0; r < NR; ++r) {
-            const float2 hi = sH[r * NL + i];
+        for (int r = 0; r < NR; ++r) {  // packed FFMA2: gq[q] += conj(H_ri) H_r,8h+q
+            const CPack hi = cpack_conj(sH[r * NL + i]);
             const float4* hr = reinterpret_cast<const float4*>(sH + r * NL + 8 * h);
 #pragma unroll
             for (int q2 = 0; q2 < 4; ++q2) {
                 const float4 v = hr[q2];
-                gq[2 * q2].x = fmaf(hi.x, v.x, fmaf(hi.y, v.y, gq[2 * q2].x));
-                gq[2 * q2].y = fmaf(hi.x, v.y, fmaf(-hi.y, v.x, gq[2 * q2].y));
-                gq[2 * q2 + 1].x = fmaf(hi.x, v.z, fmaf(hi.y, v.w, gq[2 * q2 + 1].x));
-                gq[2 * q2 + 1].y = fmaf(hi.x, v.w, fmaf(-hi.y, v.z, gq[2 * q2 + 1].y));
+                gq[2 * q2] = cmac_p(gq[2 * q2], hi, make_float2(v.x, v.y));
+                gq[2 * q2 + 1] = cmac_p(gq[2 * q2 + 1], hi, make_float2(v.z, v.w));
             }
         }
     }
@@ -190,6 +188,9 @@ __global__ void __launch_bounds__(32 * UPB) k_big_setup(DetectArgs a) {
     pdl_wait();  // the previous call may still read the workspace
     if (valid) {
         float2* ws = reinterpret_cast<float2*>(reinterpret_cast<float*>(a.ws) + u * WS);
+        CPackC gp[NL];  // packed FFMA2: sv += G^-1_kj conj(H_rj)
+#pragma unroll
+        for (int j = 0; j < NL; ++j) gp[j] = cpackc(gi[j]);
 #pragma unroll 2
         for (int rr = 0; rr < NR / 2; ++rr) {
             const int r = half * (NR / 2) + rr;
@@ -198,10 +199,8 @@ __global__ void __launch_bounds__(32 * UPB) k_big_setup(DetectArgs a) {
 #pragma unroll
             for (int j2 = 0; j2 < NL / 2; ++j2) {
                 const float4 v = hr[j2];
-                sv.x = fmaf(gi[2 * j2].x, v.x, fmaf(gi[2 * j2].y, v.y, sv.x));
-                sv.y = fmaf(gi[2 * j2].y, v.x, fmaf(-gi[2 * j2].x, v.y, sv.y));
-                sv.x = fmaf(gi[2 * j2 + 1].x, v.z, fmaf(gi[2 * j2 + 1].y, v.w, sv.x));
-                sv.y = fmaf(gi[2 * j2 + 1].y, v.z, fmaf(-gi[2 * j2 + 1].x, v.w, sv.y));
+                sv = cmacc_p(sv, gp[2 * j2], make_float2(v.x, v.y));
+                sv = cmacc_p(sv, gp[2 * j2 + 1], make_float2(v.z, v.w));
             }
             ws[r * NL + k] = fac > 0.f ? make_float2(sv.x * fac, sv.y * fac) : make_float2(0.f, 0.f);
         }
@@ -1158,6 +1157,8 @@ const KernelEntry kEntries[] = {
     BIG4_ENTRY("big4_64x16_q6_i8", 4, 4, 2),  // C5 default: tcgen05 3-pass TF32 apply (fastest)
     BIG4_ENTRY("big4e8_64x16_q6_i8", 8, 4, 2),
     BIG4_ENTRY("big4s5_64x16_q6_i8", 4, 5, 2),
+    BIG4_ENTRY("big4s6_64x16_q6_i8", 4, 6, 1),
+    BIG4_ENTRY("big4s3_64x16_q6_i8", 4, 3, 2),
     // timing ablations (results are wrong on purpose; only reachable through MIMO_FORCE_KERNEL)
     KernelEntry{"ablation_big4_noconv", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 1>,
                 prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 1>, workspace<64, 16>},

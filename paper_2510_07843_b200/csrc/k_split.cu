@@ -322,11 +322,12 @@ __global__ void __launch_bounds__(128, MINB) k_apply_stream(DetectArgs a) {
                                reinterpret_cast<uint32_t*>(&ring[i % PF][0]));
         float2 x[NL];
 #pragma unroll
-        for (int k = 0; k < NL; ++k) {
-            float2 acc = make_float2(0.f, 0.f);
+        for (int k = 0; k < NL; ++k) x[k] = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int r = 0; r < NR; ++r) acc = cmac(acc, w[k][r], yv[r]);
-            x[k] = acc;
+        for (int r = 0; r < NR; ++r) {  // packed FFMA2, y_r shared by the NL layers
+            const float2 ny = make_float2(-yv[r].y, yv[r].x);
+#pragma unroll
+            for (int k = 0; k < NL; ++k) x[k] = cmac_y(x[k], w[k][r], yv[r], ny);
         }
         const size_t re = (size_t)(slot * kSym + s) * a.n_sc + sc;
         if (a.llr) {
