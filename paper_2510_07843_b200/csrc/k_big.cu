@@ -904,12 +904,14 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
                     mbar_wait(&ylofull[lb], (uint32_t)((gg / NLO) & 1));
                     tc_fence_after();
                     const uint32_t yl = base + (uint32_t)(A4::ylo + lb * A4::chunk);
+                    if constexpr (!(ABL & 4)) {
 #pragma unroll
-                    for (int tile = 0; tile < 2; ++tile)
+                        for (int tile = 0; tile < 2; ++tile)
 #pragma unroll
-                        for (int ks = 0; ks < 4; ++ks)
-                            umma_tf32(acc + 64u * tile, umma_desc_sw128(yl + (tile ? 40u * 128u : 0u) + ks * 32u),
-                                      umma_desc_sw128(bb + (uint32_t)c * 8192u + ks * 32u), id32, 1u);
+                            for (int ks = 0; ks < 4; ++ks)
+                                umma_tf32(acc + 64u * tile, umma_desc_sw128(yl + (tile ? 40u * 128u : 0u) + ks * 32u),
+                                          umma_desc_sw128(bb + (uint32_t)c * 8192u + ks * 32u), id32, 1u);
+                    }
                     umma_commit(&ylofree[lb]);
                     if (c == 3) umma_commit(&accfull[b]);
                 }
@@ -1166,6 +1168,8 @@ const KernelEntry kEntries[] = {
                 prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 2>, workspace<64, 16>},
     KernelEntry{"ablation_big4_none", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 3>,
                 prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 3>, workspace<64, 16>},
+    KernelEntry{"ablation_big4_mma1", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 7>,
+                prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 7>, workspace<64, 16>},
     BIGAP2_ENTRY("big2_64x16_q6_i8", 64, 16, 6, kLlrI8),  // SIMT K-streamed apply
     BIG_ENTRY("big_64x16_q6_i8", 64, 16, 6, kLlrI8),
     KernelEntry{"big3_64x16_q6_i8", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap3<64, 16, 6, kLlrI8>,
