@@ -785,9 +785,11 @@ cudaError_t prepare_ap3() {
 //                  x~ -> exact max-log demap -> LLR stores.
 // Chunk g = 4 i + c of the CTA's i-th unit (u = blockIdx.x + i gridDim.x).
 // mbarrier k-th completion is waited with parity k & 1.
-template <int S_, int NLO_>
+template <int S_, int NLO_, int TR_ = 0>
 struct Ap4 {
     static constexpr int S = S_;                             // y stages
+    static constexpr int TRW = 96;                           // TR: transpose-buffer width (REs)
+    static constexpr int TRS = TRW + 4;                      // TR: floats per accumulator row in the stage (pad: banks)
     static constexpr int NLO = NLO_;                         // y_lo buffers
     static constexpr size_t chunk = (size_t)kRe * 128;       // 21504 = 21 x 1024
     static constexpr size_t y0 = 0;
@@ -795,7 +797,8 @@ struct Ap4 {
     static constexpr size_t B = ylo + NLO * chunk;           // 2 x 32 KiB (1024-aligned)
     static constexpr size_t bset = 4 * 64 * 128;
     static constexpr size_t slope = B + 2 * bset;            // [4][16] float (unit i -> slot i & 3)
-    static constexpr size_t bars = slope + 256;              // mbarriers
+    static constexpr size_t tb = slope + 256;                // TR: [TRW][TRS] float
+    static constexpr size_t bars = tb + (TR_ ? (size_t)64 * TRS * 4 : 0);  // mbarriers
     static constexpr int NBAR = 2 * S + 2 * NLO + 2 * 3;     // yfull, yfree | ylofull, ylofree | bready, accfull, tfree
     static constexpr size_t tslot = bars + NBAR * 8;
     static constexpr size_t total = tslot + 16 + 1024;
@@ -803,9 +806,17 @@ struct Ap4 {
     static_assert(total <= 227 * 1024, "shared memory");
 };
 
-template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_, int ABL>
+// TR = 1 ("big5"): the transposed product  X[64 x 168] = [B_hi; B_lo][64 x 128] Y^T[128 x 168]
+// with the W~ set as the M = 64 A operand and the unit's 168 y rows as one N = 168 B operand:
+// 4 + 4 tcgen05.mma per chunk instead of 16 (two M = 128 tiles x hi|lo and lo passes), no
+// duplicated rows. The M = 64 accumulator puts row m in TMEM lane (m % 16) + 32 (m / 16),
+// column n = RE, so the epilogue transposes through shared memory (96 REs at a time).
+template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_, int ABL, int TR>
 __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, const __grid_constant__ CUtensorMap ymap) {
-    using A4 = Ap4<S_, NLO_>;
+    using A4 = Ap4<S_, NLO_, TR>;
+    static_assert(!TR || EW == 4, "transposed epilogue uses 4 warps");
+    constexpr uint32_t kTmemCols = TR ? 512u : 256u;
+    constexpr uint32_t kAccStride = TR ? 256u : 128u;
     constexpr int CW = 4 + EW;  // control warp (MMA issuer); CW + 1: TMA producer
     constexpr int NLO = NLO_;
     static_assert(NL == 16 && NR == 64, "k_big_apply4: 64 x 16");
@@ -848,7 +859,8 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
         fence_mbar_init();
     }
     if (warp == CW) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tslot)));
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tslot)),
+                     "r"(kTmemCols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
@@ -885,7 +897,8 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
                 const int b = (int)(i & 1);
                 mbar_wait(&bready[b], (uint32_t)((i >> 1) & 1));
                 if (i >= 2) mbar_wait(&tfree[b], (uint32_t)(((i >> 1) + 1) & 1));
-                const uint32_t acc = tmem + 128u * (uint32_t)b;
+                constexpr uint32_t idT = (1u << 4) | (2u << 7) | (2u << 10) | (((uint32_t)kRe >> 3) << 17) | ((64u >> 4) << 24);
+                const uint32_t acc = tmem + kAccStride * (uint32_t)b;
                 const uint32_t bb = base + (uint32_t)(A4::B + b * A4::bset);
 #pragma unroll 1
                 for (int c = 0; c < 4; ++c) {
@@ -894,17 +907,30 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
                     const uint32_t ys = base + (uint32_t)(A4::y0 + st * A4::chunk);
                     mbar_wait(&yfull[st], (uint32_t)((gg / S) & 1));
                     tc_fence_after();
-#pragma unroll
-                    for (int tile = 0; tile < 2; ++tile)
+                    if constexpr (TR) {
 #pragma unroll
                         for (int ks = 0; ks < 4; ++ks)
-                            umma_tf32(acc + 64u * tile, umma_desc_sw128(ys + (tile ? 40u * 128u : 0u) + ks * 32u),
-                                      umma_desc_sw128(bb + (uint32_t)c * 8192u + ks * 32u), id64, (c | ks) ? 1u : 0u);
+                            umma_tf32(acc, umma_desc_sw128(bb + (uint32_t)c * 8192u + ks * 32u),
+                                      umma_desc_sw128(ys + ks * 32u), idT, (c | ks) ? 1u : 0u);
+                    } else {
+#pragma unroll
+                        for (int tile = 0; tile < 2; ++tile)
+#pragma unroll
+                            for (int ks = 0; ks < 4; ++ks)
+                                umma_tf32(acc + 64u * tile, umma_desc_sw128(ys + (tile ? 40u * 128u : 0u) + ks * 32u),
+                                          umma_desc_sw128(bb + (uint32_t)c * 8192u + ks * 32u), id64,
+                                          (c | ks) ? 1u : 0u);
+                    }
                     umma_commit(&yfree[st]);
                     mbar_wait(&ylofull[lb], (uint32_t)((gg / NLO) & 1));
                     tc_fence_after();
                     const uint32_t yl = base + (uint32_t)(A4::ylo + lb * A4::chunk);
-                    if constexpr (!(ABL & 4)) {
+                    if constexpr (TR) {  // A = [B_hi; B_lo]: also adds the (tiny) lo*lo term
+#pragma unroll
+                        for (int ks = 0; ks < 4; ++ks)
+                            umma_tf32(acc, umma_desc_sw128(bb + (uint32_t)c * 8192u + ks * 32u),
+                                      umma_desc_sw128(yl + ks * 32u), idT, 1u);
+                    } else if constexpr (!(ABL & 4)) {
 #pragma unroll
                         for (int tile = 0; tile < 2; ++tile)
 #pragma unroll
@@ -1006,11 +1032,73 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
             const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);
             mbar_wait(&accfull[b], (uint32_t)((i >> 1) & 1));
             tc_fence_after();
+            if constexpr (TR) {
+                // rows 16q..16q+15 of quadrant q = (Re hi | Im hi | Re lo | Im lo) x 16 layers, column = RE
+                float* T = reinterpret_cast<float*>(g + A4::tb);
+                const int tid = t - 128;
+                const uint32_t tq = tmem + ((uint32_t)(32 * we) << 16) + kAccStride * (uint32_t)b;
 #pragma unroll 1
-            for (int tile = 0; tile < 2; ++tile) {
+                for (int p = 0; p < 2; ++p) {
+                    const int n0 = p * A4::TRW, wcol = p ? kRe - A4::TRW : A4::TRW;
+#pragma unroll 1
+                    for (int c0 = 0; c0 < wcol; c0 += 32) {
+                        uint32_t v[32];
+                        if (wcol - c0 >= 32) {
+                            tmem_ld32(tq + (uint32_t)(n0 + c0), v);
+                        } else {
+                            tmem_ld8(tq + (uint32_t)(n0 + c0), v);
+                            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                        }
+                        if (lane < 16) {  // accumulator row m = 16 we + lane, 128-bit stores along the REs
+                            const int nc = wcol - c0 >= 32 ? 32 : 8;
+                            float* trow = T + (16 * we + lane) * A4::TRS + c0;
+#pragma unroll
+                            for (int j4 = 0; j4 < 8; ++j4)
+                                if (4 * j4 < nc)
+                                    *reinterpret_cast<float4*>(trow + 4 * j4) =
+                                        make_float4(__uint_as_float(v[4 * j4]), __uint_as_float(v[4 * j4 + 1]),
+                                                    __uint_as_float(v[4 * j4 + 2]), __uint_as_float(v[4 * j4 + 3]));
+                        }
+                    }
+                    asm volatile("bar.sync 2, 128;" ::: "memory");
+                    if (tid < wcol) {
+                        const int row = n0 + tid;
+                        const int s = row / kSc, f = row % kSc;
+                        const size_t re = (size_t)(slot * kSym + s) * a.n_sc + fb * kSc + f;
+                        float q[64];  // column tid of the 64 accumulator rows (consecutive threads: conflict-free)
+#pragma unroll
+                        for (int m = 0; m < 64; ++m) q[m] = T[m * A4::TRS + tid];
+                        float2 x[NL];
+#pragma unroll
+                        for (int k = 0; k < NL; ++k) x[k] = make_float2(q[k] + q[32 + k], q[16 + k] + q[48 + k]);
+                        const float* sl = sslope + (i & 3) * 16;
+                        if (a.llr && !(ABL & 2)) {
+                            float vv[NL * QM];
+                            uint32_t wd[(kRec + 3) / 4];
+                            if (!zf) {
+#pragma unroll
+                                for (int k = 0; k < NL; ++k) demap_layer<QM, false, LT>(x[k], sl[k], vv + k * QM);
+                                pack_llr<LT, NL * QM, false>(vv, wd);
+                            } else {
+#pragma unroll
+                                for (int k = 0; k < NL; ++k) demap_layer<QM, true, LT>(x[k], sl[k], vv + k * QM);
+                                pack_llr<LT, NL * QM, true>(vv, wd);
+                            }
+                            store_bytes<kRec>((char*)a.llr + re * kRec, wd);
+                        }
+                        if (a.xhat) {
+#pragma unroll
+                            for (int k = 0; k < NL; ++k) a.xhat[re * NL + k] = make_float2(x[k].x * ia, x[k].y * ia);
+                        }
+                    }
+                    asm volatile("bar.sync 2, 128;" ::: "memory");
+                }
+            }
+#pragma unroll 1
+            for (int tile = 0; tile < (TR ? 0 : 2); ++tile) {
                 if (tile == 1 && we < 2) break;
                 uint32_t hr[KL], hi[KL], lr[KL], li[KL];
-                const uint32_t taddr = tmem + ((uint32_t)(32 * we) << 16) + 128u * (uint32_t)b + 64u * tile + KL * h;
+                const uint32_t taddr = tmem + ((uint32_t)(32 * we) << 16) + kAccStride * (uint32_t)b + 64u * tile + KL * h;
                 if constexpr (KL == 16) {
                     uint32_t hv[32], lv[32];
                     tmem_ld32(taddr, hv);
@@ -1067,10 +1155,10 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == CW) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    if (warp == CW) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
 }
 
-template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_, int ABL = 0>
+template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_, int ABL = 0, int TR = 0>
 cudaError_t launch_ap4(const DetectArgs& a, cudaStream_t s) {
     if (a.n_units <= 0) return cudaSuccess;
     static int n_sm = 0;
@@ -1097,23 +1185,23 @@ cudaError_t launch_ap4(const DetectArgs& a, cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(a.n_units < n_sm ? a.n_units : n_sm));
     cfg.blockDim = dim3(32 * (6 + EW));
-    cfg.dynamicSmemBytes = Ap4<S_, NLO_>::total;
+    cfg.dynamicSmemBytes = Ap4<S_, NLO_, TR>::total;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = a.overlap ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, k_big_apply4<NR, NL, QM, LT, EW, S_, NLO_, ABL>, a, ymap);
+    return cudaLaunchKernelEx(&cfg, k_big_apply4<NR, NL, QM, LT, EW, S_, NLO_, ABL, TR>, a, ymap);
 }
 
-template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_, int ABL = 0>
+template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_, int ABL = 0, int TR = 0>
 cudaError_t prepare_ap4() {
     cudaError_t e = cudaFuncSetAttribute(k_big_setup<NR, NL, QM, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(4 * SetupSmem<NR, NL>::per_unit));
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_big_apply4<NR, NL, QM, LT, EW, S_, NLO_, ABL>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ap4<S_, NLO_>::total);
+    return cudaFuncSetAttribute(k_big_apply4<NR, NL, QM, LT, EW, S_, NLO_, ABL, TR>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ap4<S_, NLO_, TR>::total);
 }
 
 template <int NR, int NL>
@@ -1159,8 +1247,12 @@ const KernelEntry kEntries[] = {
     BIG4_ENTRY("big4_64x16_q6_i8", 4, 4, 2),  // C5 default: tcgen05 3-pass TF32 apply (fastest)
     BIG4_ENTRY("big4e8_64x16_q6_i8", 8, 4, 2),
     BIG4_ENTRY("big4s5_64x16_q6_i8", 4, 5, 2),
-    BIG4_ENTRY("big4s6_64x16_q6_i8", 4, 6, 1),
-    BIG4_ENTRY("big4s3_64x16_q6_i8", 4, 3, 2),
+    KernelEntry{"big5_64x16_q6_i8", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 0, 1>,
+                prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 0, 1>, workspace<64, 16>},
+    KernelEntry{"big5s3_64x16_q6_i8", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 3, 2, 0, 1>,
+                prepare_ap4<64, 16, 6, kLlrI8, 4, 3, 2, 0, 1>, workspace<64, 16>},
+    KernelEntry{"ablation_big5_none", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 3, 1>,
+                prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 3, 1>, workspace<64, 16>},
     // timing ablations (results are wrong on purpose; only reachable through MIMO_FORCE_KERNEL)
     KernelEntry{"ablation_big4_noconv", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 1>,
                 prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 1>, workspace<64, 16>},

@@ -556,7 +556,7 @@ struct Lg3Smem {
     static constexpr size_t total = bars + 16 + 1024;                       // + 1024-alignment slack
 };
 
-template <int NR, int NL, int QM, int LT, int NW>
+template <int NR, int NL, int QM, int LT, int NW, int PFD>
 __global__ void __launch_bounds__(32 * NW) k_lg3(DetectArgs a, const __grid_constant__ CUtensorMap ymap) {
     using SM = Lg3Smem<NR, NL, NW>;
     constexpr int UPW = SM::UPW;
@@ -592,6 +592,20 @@ __global__ void __launch_bounds__(32 * NW) k_lg3(DetectArgs a, const __grid_cons
         mbar_arrive_expect_tx(&bars[0], (uint32_t)(kSym * TU * NR * 8));
         tma_load_3d(base + (uint32_t)SM::y, &ymap, 0, sc0, slot * kSym, &bars[0]);
         mbar_arrive_expect_tx(&bars[1], (uint32_t)nvalid * NR * NL * 8u);
+        if constexpr (PFD > 0) {
+            // warm L2 with the H and y tiles of the CTA PFD launches ahead (about one wave later),
+            // so its start-up loads hit L2 instead of exposing DRAM latency
+            const long long lin = (long long)blockIdx.y * gridDim.x + blockIdx.x + PFD;
+            if (lin < (long long)gridDim.x * gridDim.y) {
+                const int ps = (int)(lin / gridDim.x), psc0 = (int)(lin % gridDim.x) * TU;
+                const int pn = min(TU, a.n_sc - psc0);
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.H + ((size_t)ps * a.n_sc + psc0) * NR * NL),
+                             "r"((uint32_t)pn * NR * NL * 8u) : "memory");
+                asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                                 reinterpret_cast<uint64_t>(&ymap)),
+                             "r"(0), "r"(psc0), "r"(ps * kSym) : "memory");
+            }
+        }
     }
     __syncthreads();
     if (k == 0 && active)
@@ -746,7 +760,7 @@ __global__ void __launch_bounds__(32 * NW) k_lg3(DetectArgs a, const __grid_cons
     }
 }
 
-template <int NR, int NL, int QM, int LT, int NW>
+template <int NR, int NL, int QM, int LT, int NW, int PFD>
 cudaError_t launch3(const DetectArgs& a, cudaStream_t s) {
     if (a.n_sc <= 0 || a.n_slots <= 0) return cudaSuccess;
     constexpr int TU = Lg3Smem<NR, NL, NW>::TU;
@@ -771,14 +785,15 @@ cudaError_t launch3(const DetectArgs& a, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = a.overlap ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, k_lg3<NR, NL, QM, LT, NW>, a, ymap);
+    return cudaLaunchKernelEx(&cfg, k_lg3<NR, NL, QM, LT, NW, PFD>, a, ymap);
 }
 
-template <int NR, int NL, int QM, int LT, int NW>
+template <int NR, int NL, int QM, int LT, int NW, int PFD>
 cudaError_t prepare3() {
     constexpr size_t smem = Lg3Smem<NR, NL, NW>::total;
     if (smem > 48 * 1024)
-        return cudaFuncSetAttribute(k_lg3<NR, NL, QM, LT, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        return cudaFuncSetAttribute(k_lg3<NR, NL, QM, LT, NW, PFD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem);
     return cudaSuccess;
 }
 
@@ -808,13 +823,19 @@ cudaError_t prepare() {
             prepare2<NR, NL, QM, LT, NW, R, SU>                                                        \
     }
 
-#define LG3_ENTRY(NAME, NR, NL, QM, LT, NW)                                                              \
-    KernelEntry { NAME, NR, NL, QM, 1, 14, LT, 32, 1, launch3<NR, NL, QM, LT, NW>, prepare3<NR, NL, QM, LT, NW> }
+#define LG3_ENTRY(NAME, NR, NL, QM, LT, NW) LG3P_ENTRY(NAME, NR, NL, QM, LT, NW, 0)
+#define LG3P_ENTRY(NAME, NR, NL, QM, LT, NW, PFD)                                                      \
+    KernelEntry {                                                                                      \
+        NAME, NR, NL, QM, 1, 14, LT, 32, 1, launch3<NR, NL, QM, LT, NW, PFD>, prepare3<NR, NL, QM, LT, NW, PFD> \
+    }
 
 const KernelEntry kEntries[] = {
     LG3_ENTRY("lg3_16x8_q8_f16", 16, 8, 8, kLlrF16, 2),  // C4 (one TMA tensor box per CTA for y)
     LG_ENTRY("lg_16x8_q8_f16", 16, 8, 8, kLlrF16, 2),
     LG3_ENTRY("lg3_16x8_q8_f16_w1", 16, 8, 8, kLlrF16, 1),
+    LG3P_ENTRY("lg3_16x8_q8_f16_pf1036", 16, 8, 8, kLlrF16, 2, 1036),
+    LG3P_ENTRY("lg3_16x8_q8_f16_pf2072", 16, 8, 8, kLlrF16, 2, 2072),
+    LG3P_ENTRY("lg3_16x8_q8_f16_pf518", 16, 8, 8, kLlrF16, 2, 518),
     LG3_ENTRY("lg3_16x8_q8_f16_w4", 16, 8, 8, kLlrF16, 4),
     LG2_ENTRY("lg2_16x8_q8_f16", 16, 8, 8, kLlrF16, 2, 4),
     LG2_ENTRY("lg2_16x8_q8_f16_r14", 16, 8, 8, kLlrF16, 2, 14),
