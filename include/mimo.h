@@ -166,6 +166,26 @@ mimo_status_t mimo_detect_lmmse_lu(mimo_plan_t plan, const void* H, const void* 
                                    int precision_bits, void* llr_out, void* xhat_out, float* sinr_out,
                                    float* stage_us);
 
+/* Coloured-noise detection / interference-rejection combining (SURVEY.md §8(f)
+ * NEXT-3; reading R24): y = H x + n with n ~ CN(0, R_nn) and a Hermitian
+ * positive-definite R_nn per H-unit (e.g. the covariance of known interferers
+ * plus noise, or sigma2_u I for a per-unit noise level). Computes the LMMSE filter
+ *   W = H^H (H H^H + R_nn)^-1
+ * (for R_nn = sigma2 I this is the paper's R of PAPER.md:117 and equals
+ * mimo_detect_mmse), by whitening: R_nn = L_R L_R^H, H~ = L_R^-1 H, the white
+ * Gram/Cholesky route with sigma2 = 1 on H~, and W = G^-1 H~^H L_R^-1 applied to
+ * the un-whitened y. mu_k = 1 - [G^-1]_kk, SINR_k = 1/[G^-1]_kk - 1, x~ = (W y)/mu
+ * and the LLRs as in mimo_detect_mmse. Setup in fp64, per-RE apply in fp32.
+ *   Rnn: DEVICE complex64 [n_units][n_rx][n_rx], full Hermitian matrix (the lower
+ *        triangle is read), 8-byte aligned.
+ * Other arguments, layouts and outputs as mimo_detect_mmse_ex; n_rx <= 16 (else
+ * MIMO_ERR_UNSUPPORTED). Units whose R_nn or G fails the Cholesky guard (R17) or
+ * contain NaN are erasures and counted (MIMO_ERR_NOT_PD from sync_status).
+ * Asynchronous. Errors: INVALID_ARG, UNSUPPORTED, CUDA. */
+mimo_status_t mimo_detect_irc(mimo_plan_t plan, const void* H, const void* y, const void* Rnn,
+                              int n_rx, int n_layers, int n_sc, int n_sym, int qam_order,
+                              void* llr_out, void* xhat_out, float* sinr_out);
+
 /* Pre-allocate the plan's kernel workspace for calls of up to n_sc x n_sym
  * (some kernel families keep per-unit W~ in a plan-owned buffer). Calls grow the
  * workspace on demand, but not while the stream is being captured into a CUDA

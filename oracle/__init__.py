@@ -66,6 +66,8 @@ def lib():
             L.oracle_detect.argtypes = [i, i, i, i, l, i, p, p, ctypes.c_float, p, p, p, p, i]
             L.oracle_detect.restype = l
             L.oracle_quantize.argtypes = [i, l, p, d, p]
+            L.oracle_detect_irc.argtypes = [i, i, i, l, i, p, p, p, p, p, p, p, i]
+            L.oracle_detect_irc.restype = l
             L.oracle_max_threads.restype = i
             _lib = L
     return _lib
@@ -191,6 +193,28 @@ def detect(H_units, Y_units, sigma2, qm: int, *, route: str = "chol", threads: i
     nb = lib().oracle_detect(1 if route == "lu" else 0, nr, nl, qm, nu, ne, _ptr(H), _ptr(Y),
                              ctypes.c_float(np.float32(sigma2)), _ptr(xt), _ptr(sinr), _ptr(llr),
                              _ptr(ok), int(threads))
+    if nb < 0:
+        raise ValueError("unsupported qm")
+    return dict(xhat=xt, sinr=sinr, llr=llr, ok=ok.astype(bool), n_failed=int(nb))
+
+
+def detect_irc(H_units, Y_units, R_units, qm: int, *, threads: int = 1):
+    """Coloured-noise (interference-rejection) detector, W = H^H (H H^H + R_nn)^-1 per unit.
+
+    R_units complex64 [n_units][nr][nr] (Hermitian positive definite noise + interference covariance).
+    Same outputs as detect()."""
+    H = np.ascontiguousarray(H_units, dtype=np.complex64)
+    Y = np.ascontiguousarray(Y_units, dtype=np.complex64)
+    R = np.ascontiguousarray(R_units, dtype=np.complex64)
+    nu, nr, nl = H.shape
+    ne = Y.shape[1]
+    assert Y.shape == (nu, ne, nr) and R.shape == (nu, nr, nr), (Y.shape, R.shape)
+    xt = np.zeros((nu, ne, nl), np.complex128)
+    sinr = np.zeros((nu, nl))
+    llr = np.zeros((nu, ne, nl, qm))
+    ok = np.zeros(nu, np.int8)
+    nb = lib().oracle_detect_irc(nr, nl, qm, nu, ne, _ptr(H), _ptr(Y), _ptr(R), _ptr(xt), _ptr(sinr), _ptr(llr),
+                                 _ptr(ok), int(threads))
     if nb < 0:
         raise ValueError("unsupported qm")
     return dict(xhat=xt, sinr=sinr, llr=llr, ok=ok.astype(bool), n_failed=int(nb))

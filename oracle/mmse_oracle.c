@@ -24,6 +24,7 @@
  *   - oracle_weights_chol    W = G^-1 H^H             (Gram form, reading R1)
  *   - oracle_weights_lu      W = H^H R^-1             (paper-literal covariance form)
  *   - oracle_detect          per-unit detector, Gram/Cholesky route
+ *   - oracle_detect_irc      coloured-noise (interference-rejection) detector, W = H^H (H H^H + R_nn)^-1
  *   - oracle_detect_cov_lu   per-unit detector, covariance/LU route (paper-literal)
  *   - oracle_constellation   38.211 5.1 Gray QAM (reading R6)
  *   - oracle_maxlog          brute-force max-log over all 2^qm points (reading R5)
@@ -480,6 +481,93 @@ done:
     free(W);
     free(mu);
     return ok;
+}
+
+/* Detect one H-unit with a coloured-noise covariance R_nn (SURVEY.md §8(f)
+ * NEXT-3, interference-rejection combining; reading R24). The LMMSE filter for
+ * y = H x + n, n ~ CN(0, R_nn), E[x x^H] = I, written out as its definition:
+ *   W = H^H (H H^H + R_nn)^-1           (R_nn = s2 I gives the paper's R)
+ * with the inverse formed by the LU + substitution inversion above; then, as in
+ * the white case, mu_k = [W H]_kk, SINR_k = mu_k / (1 - mu_k), x~ = (W y)_k / mu_k,
+ * brute-force max-log. Rf: complex64 [nr][nr] (full Hermitian matrix). */
+static int detect_unit_irc(int nr, int nl, int qm, int n_re, const float* Hf, const float* Yf, const float* Rf,
+                           const double* cre, const double* cim, cplx* xt, double* sinr, double* llr)
+{
+    cplx* H = malloc(sizeof(cplx) * (size_t)nr * nl);
+    cplx* Rt = malloc(sizeof(cplx) * (size_t)nr * nr);
+    cplx* Ri = malloc(sizeof(cplx) * (size_t)nr * nr);
+    cplx* W = malloc(sizeof(cplx) * (size_t)nl * nr);
+    double* mu = malloc(sizeof(double) * (size_t)nl);
+    for (int i = 0; i < nr * nl; i++) H[i] = (double)Hf[2 * i] + I * (double)Hf[2 * i + 1];
+    /* R_total = H H^H + R_nn */
+    for (int i = 0; i < nr; i++)
+        for (int j = 0; j < nr; j++) {
+            cplx s = (double)Rf[2 * (i * nr + j)] + I * (double)Rf[2 * (i * nr + j) + 1];
+            for (int l = 0; l < nl; l++) s += H[i * nl + l] * conj(H[j * nl + l]);
+            Rt[i * nr + j] = s;
+        }
+    int ok = oracle_lu_invert(nr, (const double*)Rt, (double*)Ri);
+    if (!ok) {
+        memset(xt, 0, sizeof(cplx) * (size_t)n_re * nl);
+        memset(sinr, 0, sizeof(double) * (size_t)nl);
+        memset(llr, 0, sizeof(double) * (size_t)n_re * nl * qm);
+        goto done;
+    }
+    for (int l = 0; l < nl; l++)
+        for (int c = 0; c < nr; c++) {
+            cplx s = 0;
+            for (int r = 0; r < nr; r++) s += conj(H[r * nl + l]) * Ri[r * nr + c];
+            W[l * nr + c] = s;
+        }
+    for (int k = 0; k < nl; k++) {
+        cplx s = 0;
+        for (int r = 0; r < nr; r++) s += W[k * nr + r] * H[r * nl + k];
+        mu[k] = creal(s);
+        sinr[k] = mu[k] / (1.0 - mu[k]);
+        if (!(mu[k] > 0.0)) sinr[k] = 0.0;
+    }
+    for (int e = 0; e < n_re; e++) {
+        for (int k = 0; k < nl; k++) {
+            cplx* out = xt + (size_t)e * nl + k;
+            double* lo = llr + ((size_t)e * nl + k) * qm;
+            if (!(mu[k] > 0.0)) {
+                *out = 0;
+                for (int j = 0; j < qm; j++) lo[j] = 0.0;
+                continue;
+            }
+            cplx s = 0;
+            for (int r = 0; r < nr; r++)
+                s += W[k * nr + r] * ((double)Yf[((size_t)e * nr + r) * 2] + I * (double)Yf[((size_t)e * nr + r) * 2 + 1]);
+            *out = s / mu[k];
+            maxlog_with(qm, cre, cim, creal(*out), cimag(*out), sinr[k], lo);
+        }
+    }
+done:
+    free(H);
+    free(Rt);
+    free(Ri);
+    free(W);
+    free(mu);
+    return ok;
+}
+
+/* Batch driver of the coloured-noise route: R complex64 [n_units][nr][nr]. */
+long oracle_detect_irc(int nr, int nl, int qm, long n_units, int n_re, const float* H, const float* Y,
+                       const float* R, double* xt, double* sinr, double* llr, signed char* ok, int n_threads)
+{
+    double cre[256], cim[256];
+    if (oracle_constellation(qm, cre, cim) == 0) return -1;
+    long n_bad = 0;
+    if (n_threads < 1) n_threads = 1;
+#pragma omp parallel for schedule(dynamic, 4) num_threads(n_threads) reduction(+ : n_bad)
+    for (long u = 0; u < n_units; u++) {
+        int r = detect_unit_irc(nr, nl, qm, n_re, H + (size_t)u * nr * nl * 2, Y + (size_t)u * n_re * nr * 2,
+                                R + (size_t)u * nr * nr * 2, cre, cim, (cplx*)xt + (size_t)u * n_re * nl,
+                                sinr + (size_t)u * nl, llr + (size_t)u * n_re * nl * qm);
+        ok[u] = (signed char)r;
+        if (!r) n_bad++;
+    }
+    return n_bad;
 }
 
 /* Batch driver over H-units (units are independent: SPEC.md:470-471).

@@ -60,6 +60,9 @@ constexpr int kGenericMaxRx = 64;
 // precision_bits 32 ("PS") or 64 ("PD"); ev (nullable) = 6 events recorded
 // before stage 0 and after each stage.
 bool lu_route_supported(int n_rx);
+// Coloured-noise (interference-rejection) detector (k_irc.cu): Rnn device complex64 [n_units][n_rx][n_rx].
+bool irc_supported(int n_rx, int n_layers);
+cudaError_t launch_irc(const DetectArgs& a, const float2* Rnn, cudaStream_t s);
 size_t lu_route_workspace(int n_rx, long long n_units, int precision_bits);
 cudaError_t launch_lu_route(const DetectArgs& a, int precision_bits, cudaStream_t s, cudaEvent_t* ev);
 constexpr int kGenericMaxLayers = 16;

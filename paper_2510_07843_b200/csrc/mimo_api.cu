@@ -447,6 +447,34 @@ mimo_status_t mimo_detect_lmmse_lu(mimo_plan_t p, const void* H, const void* y, 
     return MIMO_OK;
 }
 
+mimo_status_t mimo_detect_irc(mimo_plan_t p, const void* H, const void* y, const void* Rnn, int n_rx, int n_layers,
+                              int n_sc, int n_sym, int qm, void* llr_out, void* xhat_out, float* sinr_out) {
+    if (!p) return arg_fail(nullptr, "null plan");
+    mimo_status_t st = check_dims(p, 1.0f, n_rx, n_layers, n_sc, n_sym, qm);
+    if (st != MIMO_OK) return st;
+    if (!mimo::irc_supported(n_rx, n_layers)) {
+        snprintf(p->err, sizeof(p->err), "IRC route: n_rx must be <= 16");
+        return MIMO_ERR_UNSUPPORTED;
+    }
+    if ((long long)n_sc * n_sym == 0) return MIMO_OK;
+    if (!H || !y || !Rnn) return arg_fail(p, "null H, y or Rnn");
+    if (!llr_out && !xhat_out && !sinr_out) return arg_fail(p, "no output requested");
+    if (!aligned(H, 8) || !aligned(y, 8) || !aligned(Rnn, 8) || !aligned(llr_out, 8) || !aligned(xhat_out, 8) ||
+        !aligned(sinr_out, 4))
+        return arg_fail(p, "pointer not 8-byte aligned");
+    const int dev = p->d.device;
+    if (!is_device_ptr(H, dev) || !is_device_ptr(y, dev) || !is_device_ptr(Rnn, dev) ||
+        !is_device_ptr(llr_out, dev) || !is_device_ptr(xhat_out, dev) || !is_device_ptr(sinr_out, dev))
+        return arg_fail(p, "pointer is not device memory on the plan's device");
+    DeviceGuard g(dev);
+    if (g.err != cudaSuccess) return cuda_fail(p, g.err, "cudaSetDevice");
+    mimo::DetectArgs a = make_args(p, H, y, 1.0f, n_sc, n_sym, llr_out, xhat_out, sinr_out);
+    a.overlap = 0;
+    cudaError_t e = mimo::launch_irc(a, static_cast<const float2*>(Rnn), p->stream);
+    if (e != cudaSuccess) return cuda_fail(p, e, "IRC route");
+    return MIMO_OK;
+}
+
 mimo_status_t mimo_plan_reserve(mimo_plan_t p, int n_sc, int n_sym) {
     if (!p) return arg_fail(nullptr, "null plan");
     if (n_sc < 0 || n_sym < 0 || n_sc % p->d.sc_per_h || n_sym % p->d.sym_per_h)

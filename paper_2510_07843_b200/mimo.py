@@ -79,6 +79,8 @@ def load_library(path: str | None = None):
     L.mimo_detect_mmse_host.restype = i
     L.mimo_detect_lmmse_lu.argtypes = [vp, vp, vp, f, i, i, i, i, i, i, vp, vp, vp, ctypes.POINTER(f)]
     L.mimo_detect_lmmse_lu.restype = i
+    L.mimo_detect_irc.argtypes = [vp, vp, vp, vp, i, i, i, i, i, vp, vp, vp]
+    L.mimo_detect_irc.restype = i
     L.mimo_plan_reserve.argtypes = [vp, i, i]
     L.mimo_plan_reserve.restype = i
     L.mimo_plan_sync_status.argtypes = [vp, ctypes.POINTER(ll)]
@@ -243,6 +245,30 @@ class Plan:
         self._check(st)
         if timing:
             return out, dict(zip(LU_STAGES, (float(v) for v in st_us)))
+        return out
+
+    def detect_irc(self, H, y, Rnn, *, out=None, xhat=None, sinr=None, want_llr: bool = True):
+        """Coloured-noise / interference-rejection detection: Rnn complex64 [n_units][n_rx][n_rx] on the device."""
+        import torch
+        n_sym, n_sc = y.shape[0], y.shape[1]
+        sh = self.shapes(n_sc, n_sym)
+        self._dev_tensor(H, "H", torch.complex64, sh["H"])
+        self._dev_tensor(y, "y", torch.complex64, sh["y"])
+        n_units = sh["sinr"][0]
+        self._dev_tensor(Rnn, "Rnn", torch.complex64, (n_units, self.n_rx, self.n_rx))
+        if want_llr and out is None:
+            out = torch.empty(sh["llr"], dtype=self.llr_dtype, device=self.device)
+        if out is not None:
+            self._dev_tensor(out, "out", self.llr_dtype, sh["llr"])
+        if xhat is not None:
+            self._dev_tensor(xhat, "xhat", torch.complex64, sh["xhat"])
+        if sinr is not None:
+            self._dev_tensor(sinr, "sinr", torch.float32, sh["sinr"])
+        if self._fixed_stream is None:
+            self._lib.mimo_plan_set_stream(self._h, ctypes.c_void_p(self._stream_ptr()))
+        ptr = (lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None)
+        self._check(self._lib.mimo_detect_irc(self._h, ptr(H), ptr(y), ptr(Rnn), self.n_rx, self.n_layers, n_sc,
+                                              n_sym, self.qm, ptr(out), ptr(xhat), ptr(sinr)))
         return out
 
     def detect_host(self, H, y, sigma2: float, out=None):

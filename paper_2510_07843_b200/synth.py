@@ -129,6 +129,7 @@ class Workload:
     y: np.ndarray      # complex64 [n_sym][n_sc][nr]
     bits: np.ndarray   # uint8 [n_sym][n_sc][nl][qm]
     seed: int
+    Rnn: np.ndarray | None = None  # complex64 [n_units][nr][nr] noise + interference covariance (IRC workloads)
 
     @property
     def n_sym(self) -> int:
@@ -228,6 +229,32 @@ def generate(cfg, *, n_sc: int | None = None, n_slots: int | None = None,
     return Workload(name=c.get("name", str(key)), n_rx=nr, n_layers=nl, qm=qm, n_sc=nsc,
                     n_slots=nslots, sc_per_h=scph, llr=c["llr"], sigma2=s2,
                     H=H64.reshape(nslots, n_fb, nr, nl), y=y, bits=bits, seed=seed)
+
+
+def generate_irc(cfg, *, n_interf: int = 2, inr_db: float = 10.0, **kw) -> Workload:
+    """A workload with coloured interference for the interference-rejection detector (NEXT-3).
+
+    Draws the white workload of generate(cfg, **kw), then with Generator(PCG64(seed + 1)):
+    (4) per H-unit an interferer channel G_I ~ CN(0, sigma2 * 10^(INR/10)) of shape
+    [nr][n_interf], (5) unit-power QPSK interferer symbols per RE; y += G_I x_I (fp64, then
+    complex64). The receiver knows R_nn = G_I G_I^H + sigma2 I per unit (complex64)."""
+    w = generate(cfg, **kw)
+    rng = np.random.Generator(np.random.PCG64(w.seed + 1))
+    nr, scph = w.n_rx, w.sc_per_h
+    p_i = float(w.sigma2) * 10.0 ** (inr_db / 10.0)
+    GI = _cn(rng, (w.n_units, nr, n_interf), p_i)
+    xi = (rng.integers(0, 2, size=(w.n_sym, w.n_sc, n_interf, 2)) * 2 - 1) / np.sqrt(2.0)
+    xi = xi[..., 0] + 1j * xi[..., 1]
+    GI_grid = GI.reshape(w.n_slots, w.n_fb, nr, n_interf)
+    y = w.y.astype(np.complex128)
+    for t in range(w.n_slots):
+        xs = xi[t * SYM_PER_SLOT:(t + 1) * SYM_PER_SLOT].reshape(SYM_PER_SLOT, w.n_fb, scph, n_interf)
+        ys = np.einsum("fri,sfci->sfcr", GI_grid[t], xs, optimize=True).reshape(SYM_PER_SLOT, w.n_sc, nr)
+        y[t * SYM_PER_SLOT:(t + 1) * SYM_PER_SLOT] += ys
+    w.y = y.astype(np.complex64)
+    R = GI @ np.conj(np.swapaxes(GI, 1, 2)) + float(w.sigma2) * np.eye(nr)[None]
+    w.Rnn = R.astype(np.complex64)
+    return w
 
 
 def config_algorithmic_bytes(cfg_key, llr_bytes: int | None = None) -> dict:
