@@ -87,30 +87,32 @@ def _cn(rng: np.random.Generator, shape, var: float) -> np.ndarray:
     return (g[..., 0] + 1j * g[..., 1]) * np.sqrt(var / 2.0)
 
 
-def unit_gather(grid: np.ndarray, n_slots: int, n_sc: int, sc_per_h: int) -> np.ndarray:
-    """[n_sym][n_sc][...] -> [n_units][14*sc_per_h][...] (symbol-major inside a unit). Indexing only."""
+def unit_gather(grid: np.ndarray, n_slots: int, n_sc: int, sc_per_h: int, sym_per_h: int = SYM_PER_SLOT) -> np.ndarray:
+    """[n_sym][n_sc][...] -> [n_units][sym_per_h*sc_per_h][...] (symbol-major inside a unit). Indexing only."""
     n_fb = n_sc // sc_per_h
+    n_tb = grid.shape[0] // sym_per_h
     tail = grid.shape[2:]
-    g = grid.reshape((n_slots, SYM_PER_SLOT, n_fb, sc_per_h) + tail)
-    g = np.moveaxis(g, 2, 1)  # [slot][fb][sym][f]...
-    return g.reshape((n_slots * n_fb, SYM_PER_SLOT * sc_per_h) + tail)
+    g = grid.reshape((n_tb, sym_per_h, n_fb, sc_per_h) + tail)
+    g = np.moveaxis(g, 2, 1)  # [time block][fb][sym][f]...
+    return g.reshape((n_tb * n_fb, sym_per_h * sc_per_h) + tail)
 
 
-def unit_scatter(units: np.ndarray, n_slots: int, n_sc: int, sc_per_h: int) -> np.ndarray:
+def unit_scatter(units: np.ndarray, n_slots: int, n_sc: int, sc_per_h: int, sym_per_h: int = SYM_PER_SLOT) -> np.ndarray:
     """Inverse of unit_gather. Indexing only."""
     n_fb = n_sc // sc_per_h
+    n_tb = units.shape[0] // n_fb
     tail = units.shape[2:]
-    g = units.reshape((n_slots, n_fb, SYM_PER_SLOT, sc_per_h) + tail)
+    g = units.reshape((n_tb, n_fb, sym_per_h, sc_per_h) + tail)
     g = np.moveaxis(g, 1, 2)
-    return np.ascontiguousarray(g.reshape((n_slots * SYM_PER_SLOT, n_sc) + tail))
+    return np.ascontiguousarray(g.reshape((n_tb * sym_per_h, n_sc) + tail))
 
 
-def unit_re_index(u: int, n_sc: int, sc_per_h: int):
+def unit_re_index(u: int, n_sc: int, sc_per_h: int, sym_per_h: int = SYM_PER_SLOT):
     """(sym, sc) index arrays of the REs of unit u, in unit (symbol-major) order."""
     n_fb = n_sc // sc_per_h
-    slot, fb = divmod(int(u), n_fb)
-    s = np.repeat(np.arange(SYM_PER_SLOT), sc_per_h) + slot * SYM_PER_SLOT
-    f = np.tile(np.arange(sc_per_h), SYM_PER_SLOT) + fb * sc_per_h
+    tb, fb = divmod(int(u), n_fb)
+    s = np.repeat(np.arange(sym_per_h), sc_per_h) + tb * sym_per_h
+    f = np.tile(np.arange(sc_per_h), sym_per_h) + fb * sc_per_h
     return s, f
 
 
@@ -129,6 +131,7 @@ class Workload:
     y: np.ndarray      # complex64 [n_sym][n_sc][nr]
     bits: np.ndarray   # uint8 [n_sym][n_sc][nl][qm]
     seed: int
+    sym_per_h: int = SYM_PER_SLOT  # symbols sharing one H (14 = one H per slot; NEXT-3: time-varying H)
     Rnn: np.ndarray | None = None  # complex64 [n_units][nr][nr] noise + interference covariance (IRC workloads)
 
     @property
@@ -141,7 +144,7 @@ class Workload:
 
     @property
     def n_units(self) -> int:
-        return self.n_slots * self.n_fb
+        return (self.n_sym // self.sym_per_h) * self.n_fb
 
     @property
     def n_re(self) -> int:
@@ -151,7 +154,7 @@ class Workload:
         return self.H.reshape(self.n_units, self.n_rx, self.n_layers)
 
     def y_units(self) -> np.ndarray:
-        return unit_gather(self.y, self.n_slots, self.n_sc, self.sc_per_h)
+        return unit_gather(self.y, self.n_slots, self.n_sc, self.sc_per_h, self.sym_per_h)
 
     def sha256(self) -> str:
         h = hashlib.sha256()
@@ -170,7 +173,8 @@ def generate(cfg, *, n_sc: int | None = None, n_slots: int | None = None,
     Recipe (SURVEY.md §8(d)): Generator(PCG64(seed)), seed = 1000 + k by default;
     draws in fp64 in this order: (1) H_w for all units (slot-major, then
     frequency block), (2) bits for all REs in [n_sym][n_sc][nl][qm] order,
-    (3) noise slot by slot in [n_sym][n_sc][nr] order. Channel: iid CN(0, v),
+    (3) noise slot by slot (time block by time block when sym_per_h != 14) in
+    [n_sym][n_sc][nr] order. Channel: iid CN(0, v),
     or Kronecker H = C_r H_w C_t^T with C = chol(rho^|i-j|). y = H x + n in fp64,
     then H and y are cast to complex64.
     """
@@ -187,14 +191,18 @@ def generate(cfg, *, n_sc: int | None = None, n_slots: int | None = None,
     if seed is None:
         seed = 1000 + (key if isinstance(key, int) else 0)
     nr, nl, qm, scph = c["n_rx"], c["n_layers"], c["qm"], c["sc_per_h"]
+    sph = c.get("sym_per_h", SYM_PER_SLOT)  # NEXT-3: H constant over sph symbols (14 = per slot)
     nsc, nslots = c["n_sc"], c["n_slots"]
     if nsc % scph:
         raise ValueError("n_sc must be a multiple of sc_per_h")
+    if (nslots * SYM_PER_SLOT) % sph:
+        raise ValueError("n_sym must be a multiple of sym_per_h")
     s2 = sigma2_of(snr_db if snr_db is not None else c["snr_db"]) if sigma2 is None else np.float32(sigma2)
     rng = np.random.Generator(np.random.PCG64(seed))
     n_fb = nsc // scph
-    n_units = nslots * n_fb
     n_sym = nslots * SYM_PER_SLOT
+    n_tb = n_sym // sph
+    n_units = n_tb * n_fb
 
     # (1) channel per H-unit
     Hw = _cn(rng, (n_units, nr, nl), 1.0)
@@ -215,20 +223,20 @@ def generate(cfg, *, n_sc: int | None = None, n_slots: int | None = None,
     # (3) y = H x + n, fp64, per slot (bounded memory), then complex64.
     # The noiseless product uses the complex64-rounded H so that H is exactly
     # the channel the detector sees (noiseless pins compare against x exactly).
-    Hq = H64.astype(np.complex128).reshape(nslots, n_fb, nr, nl)
+    Hq = H64.astype(np.complex128).reshape(n_tb, n_fb, nr, nl)
     y = np.empty((n_sym, nsc, nr), dtype=np.complex64)
-    for t in range(nslots):
-        xs = x[t * SYM_PER_SLOT:(t + 1) * SYM_PER_SLOT]          # [14][nsc][nl]
-        xs = xs.reshape(SYM_PER_SLOT, n_fb, scph, nl)
-        ys = np.einsum("frl,sfcl->sfcr", Hq[t], xs, optimize=True)  # [14][n_fb][scph][nr]
-        ys = ys.reshape(SYM_PER_SLOT, nsc, nr)
+    for t in range(n_tb):  # per time block of sph symbols (= per slot when sph = 14)
+        xs = x[t * sph:(t + 1) * sph]                            # [sph][nsc][nl]
+        xs = xs.reshape(sph, n_fb, scph, nl)
+        ys = np.einsum("frl,sfcl->sfcr", Hq[t], xs, optimize=True)  # [sph][n_fb][scph][nr]
+        ys = ys.reshape(sph, nsc, nr)
         if not noiseless:
-            ys = ys + _cn(rng, (SYM_PER_SLOT, nsc, nr), float(s2))
-        y[t * SYM_PER_SLOT:(t + 1) * SYM_PER_SLOT] = ys.astype(np.complex64)
+            ys = ys + _cn(rng, (sph, nsc, nr), float(s2))
+        y[t * sph:(t + 1) * sph] = ys.astype(np.complex64)
 
     return Workload(name=c.get("name", str(key)), n_rx=nr, n_layers=nl, qm=qm, n_sc=nsc,
                     n_slots=nslots, sc_per_h=scph, llr=c["llr"], sigma2=s2,
-                    H=H64.reshape(nslots, n_fb, nr, nl), y=y, bits=bits, seed=seed)
+                    H=H64.reshape(n_tb, n_fb, nr, nl), y=y, bits=bits, seed=seed, sym_per_h=sph)
 
 
 def generate_irc(cfg, *, n_interf: int = 2, inr_db: float = 10.0, **kw) -> Workload:

@@ -31,7 +31,8 @@ def run_gpu(w: synth.Workload, *, xhat=True, sinr=True, llr_scale=1.0, plan=None
     from paper_2510_07843_b200 import mimo
     own = plan is None
     if own:
-        plan = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, llr_dtype=w.llr, llr_scale=llr_scale)
+        plan = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, sym_per_h=w.sym_per_h, llr_dtype=w.llr,
+                         llr_scale=llr_scale)
     Hd = torch.from_numpy(w.H if H is None else H).cuda()
     yd = torch.from_numpy(w.y if y is None else y).cuda()
     sh = plan.shapes(w.n_sc, w.n_sym)
@@ -53,13 +54,13 @@ def oracle_units(w: synth.Workload, units, threads=None, H=None, y=None, route="
     units = np.asarray(units, dtype=np.int64)
     Hu = (w.H if H is None else H).reshape(w.n_units, w.n_rx, w.n_layers)[units]
     yy = w.y if y is None else y
-    Yu = np.stack([yy[synth.unit_re_index(u, w.n_sc, w.sc_per_h)] for u in units]) if len(units) else \
-        np.zeros((0, 14 * w.sc_per_h, w.n_rx), np.complex64)
+    Yu = np.stack([yy[synth.unit_re_index(u, w.n_sc, w.sc_per_h, w.sym_per_h)] for u in units]) if len(units) else \
+        np.zeros((0, w.sym_per_h * w.sc_per_h, w.n_rx), np.complex64)
     return oracle.detect(Hu, Yu, w.sigma2, w.qm, threads=threads or oracle.max_threads(), route=route)
 
 
 def gather_units(w: synth.Workload, grid: np.ndarray, units):
-    return np.stack([grid[synth.unit_re_index(u, w.n_sc, w.sc_per_h)] for u in units])
+    return np.stack([grid[synth.unit_re_index(u, w.n_sc, w.sc_per_h, w.sym_per_h)] for u in units])
 
 
 def compare(w: synth.Workload, gpu: dict, units=None, llr_scale=1.0, threads=None, H=None, y=None,

@@ -190,3 +190,15 @@ def test_host_path_c5_chunked():
     plan = mimo.Plan(64, 16, 6, sc_per_h=12, llr_dtype="i8")
     out = plan.detect_host(w.H, w.y, float(w.sigma2))
     assert np.array_equal(out, g["llr"])
+
+
+@pytest.mark.parametrize("k,sph", [(2, 1), (2, 7), (3, 2), (4, 7), (1, 1)])
+def test_time_varying_channel(k, sph):
+    """NEXT-3: H changes every sph symbols (sym_per_h < 14; the generic kernel serves it)."""
+    cfg = dict(synth.CONFIGS[k], sym_per_h=sph)
+    kw = dict(n_sc=48, n_slots=1) if k != 1 else {}
+    w = synth.generate(cfg, **kw)
+    assert w.n_units == (w.n_sym // sph) * w.n_fb
+    g = parity.run_gpu(w)
+    assert g["n_failed"] == 0
+    print(k, sph, g["kernel"], parity.compare(w, g))
