@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU budget of the oracle baseline")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no graphs, no e2e/cpu legs)")
+    ap.add_argument("--bfp", type=int, default=0,
+                    help="NEXT-4: feed y as W-bit block-floating-point (mimo_detect_mmse_bfp; C3 shape only)")
     ap.add_argument("--overlap", type=int, default=1,
                     help="1: back-to-back calls overlap via PDL (MIMO_PLAN_OVERLAP_CALLS); 0: serialised")
     return ap.parse_args()
@@ -253,6 +255,10 @@ def run_ours(args, k):
     s0, s1 = shard.weak_slots(c["n_slots"], rank)
     w = synth.generate(k, seed=shard.shard_seed(base_seed, rank))
     b = synth.config_algorithmic_bytes(k)
+    ybfp = None
+    if args.bfp:  # NEXT-4: y crosses HBM as BFP blocks (reading R25); algorithmic y bytes shrink accordingly
+        ybfp = synth.bfp_compress(w.y, args.bfp)
+        b = dict(b, y=int(ybfp.nbytes), total=b["H"] + int(ybfp.nbytes) + b["llr"])
     plan = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, llr_dtype=w.llr, device=local,
                      overlap_calls=bool(args.overlap))
     plan1 = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, llr_dtype=w.llr, device=local)
@@ -263,7 +269,7 @@ def run_ours(args, k):
     free = torch.cuda.mem_get_info(dev)[0]
     n_sets = int(min(n_sets, max(2, (free * 0.5) // b["total"])))
     H0 = torch.from_numpy(w.H).to(dev)
-    y0 = torch.from_numpy(w.y).to(dev)
+    y0 = torch.from_numpy(w.y if ybfp is None else ybfp).to(dev)
     sets = []
     for i in range(n_sets):
         sets.append((H0.clone(), y0.clone(),
@@ -274,7 +280,10 @@ def run_ours(args, k):
 
     def step(i):
         H, y, out = sets[i % n_sets]
-        plan.detect(H, y, s2, out=out)
+        if ybfp is None:
+            plan.detect(H, y, s2, out=out)
+        else:
+            plan.detect_bfp(H, y, s2, n_sym=w.n_sym, n_sc=w.n_sc, iq_width=args.bfp, out=out)
 
     if args.profile:
         with torch.cuda.stream(stream):
@@ -329,7 +338,10 @@ def run_ours(args, k):
     # context: the same steps with calls serialised (no PDL overlap) -> single-call device time
     def step1(i):
         H, y, out = sets[i % n_sets]
-        plan1.detect(H, y, s2, out=out)
+        if ybfp is None:
+            plan1.detect(H, y, s2, out=out)
+        else:
+            plan1.detect_bfp(H, y, s2, n_sym=w.n_sym, n_sc=w.n_sc, iq_width=args.bfp, out=out)
     g1 = torch.cuda.CUDAGraph()
     with torch.cuda.stream(stream):
         step1(0)
@@ -383,7 +395,7 @@ def run_ours(args, k):
 
     # e2e: host buffers through mimo_detect_mmse_host (H2D + kernel + D2H per step)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and ybfp is None:
         Hh = torch.from_numpy(w.H).pin_memory()
         yh = torch.from_numpy(w.y).pin_memory()
         lh = torch.empty(plan.shapes(w.n_sc, w.n_sym)["llr"], dtype=plan.llr_dtype).pin_memory()
@@ -402,7 +414,7 @@ def run_ours(args, k):
                "path": "mimo_detect_mmse_host (pinned host buffers, 2-stream slot-chunk pipeline)"}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and ybfp is None:
         import oracle
         cpu = oracle_rate(w, args.cpu_seconds, oracle.max_threads())
 
@@ -415,7 +427,9 @@ def run_ours(args, k):
     cfg.update({"global_slots": c["n_slots"] * world, "slots_per_gpu": c["n_slots"],
                 "l2_flush": f"{n_sets} rotating buffer sets x {b['total'] / 1e6:.1f} MB = "
                             f"{n_sets * b['total'] / 1e6:.0f} MB > 3x L2 ({l2 / 1e6:.0f} MB)",
-                "graph_steps": S, "kernel": plan.kernel_name,
+                "graph_steps": S, "kernel": plan.kernel_name + (f" + BFP{args.bfp} y (k_apply_bfp)" if ybfp is not None else ""),
+                "y_format": f"BFP {args.bfp}-bit mantissas, block per (symbol, PRB, antenna) (reading R25)"
+                            if ybfp is not None else "complex64",
                 "call_overlap": "PDL (MIMO_PLAN_OVERLAP_CALLS): call i+1 loads/sets up while call i stores"
                                 if args.overlap else "none (serialised calls)",
                 "parallelism": f"slot-sharded x{world}, no collective" if world > 1 else "single GPU"})

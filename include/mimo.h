@@ -186,6 +186,22 @@ mimo_status_t mimo_detect_irc(mimo_plan_t plan, const void* H, const void* y, co
                               int n_rx, int n_layers, int n_sc, int n_sym, int qam_order,
                               void* llr_out, void* xhat_out, float* sinr_out);
 
+/* Detection from BLOCK-FLOATING-POINT compressed y (fronthaul format; SURVEY.md
+ * §8(f) NEXT-4, reading R25), decompressed inside the detector's y loads so the
+ * fp32 y never exists in HBM. One block per (symbol, PRB, antenna):
+ *   block_bytes = roundup4(1 + 3 * iq_width); byte 0 = exponent e (bits 0..3);
+ *   then the 24 two's-complement iq_width-bit mantissas I0,Q0,...,I11,Q11 of the
+ *   PRB's 12 subcarriers, packed MSB-first; value = m * 2^e * bfp_scale.
+ *   y_bfp: DEVICE bytes [n_sym][n_sc/12][n_rx][block_bytes], 4-byte aligned.
+ * iq_width in 8..16; bfp_scale finite > 0. Everything else as mimo_detect_mmse_ex.
+ * Supported for n_rx = 8, n_layers = 4, sc_per_h = 12, sym_per_h = 14 (the C3
+ * family; else MIMO_ERR_UNSUPPORTED). Asynchronous. Errors: INVALID_ARG,
+ * UNSUPPORTED, CUDA, OOM (workspace). */
+mimo_status_t mimo_detect_mmse_bfp(mimo_plan_t plan, const void* H, const void* y_bfp, float sigma2,
+                                   int n_rx, int n_layers, int n_sc, int n_sym, int qam_order,
+                                   int iq_width, float bfp_scale,
+                                   void* llr_out, void* xhat_out, float* sinr_out);
+
 /* Pre-allocate the plan's kernel workspace for calls of up to n_sc x n_sym
  * (some kernel families keep per-unit W~ in a plan-owned buffer). Calls grow the
  * workspace on demand, but not while the stream is being captured into a CUDA

@@ -68,6 +68,8 @@ def lib():
             L.oracle_quantize.argtypes = [i, l, p, d, p]
             L.oracle_detect_irc.argtypes = [i, i, i, l, i, p, p, p, p, p, p, p, i]
             L.oracle_detect_irc.restype = l
+            L.oracle_bfp_decode.argtypes = [l, i, d, p, p]
+            L.oracle_bfp_decode.restype = None
             L.oracle_max_threads.restype = i
             _lib = L
     return _lib
@@ -218,6 +220,17 @@ def detect_irc(H_units, Y_units, R_units, qm: int, *, threads: int = 1):
     if nb < 0:
         raise ValueError("unsupported qm")
     return dict(xhat=xt, sinr=sinr, llr=llr, ok=ok.astype(bool), n_failed=int(nb))
+
+
+def bfp_decode(blocks, iq_width: int, scale: float) -> np.ndarray:
+    """BFP blocks uint8 [..., block_bytes] -> complex64 [..., 12] (reading R25)."""
+    b = np.ascontiguousarray(blocks, dtype=np.uint8)
+    bb = ((1 + 3 * iq_width) + 3) & ~3
+    assert b.shape[-1] == bb, (b.shape, bb)
+    n = b.size // bb
+    out = np.zeros(n * 24, np.float32)
+    lib().oracle_bfp_decode(n, int(iq_width), float(scale), _ptr(b), _ptr(out))
+    return out.view(np.complex64).reshape(b.shape[:-1] + (12,))
 
 
 def quantize(llr, llr_type: str, scale: float = 1.0) -> np.ndarray:

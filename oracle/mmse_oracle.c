@@ -25,6 +25,7 @@
  *   - oracle_weights_lu      W = H^H R^-1             (paper-literal covariance form)
  *   - oracle_detect          per-unit detector, Gram/Cholesky route
  *   - oracle_detect_irc      coloured-noise (interference-rejection) detector, W = H^H (H H^H + R_nn)^-1
+ *   - oracle_bfp_decode      block-floating-point fronthaul decompression (reading R25)
  *   - oracle_detect_cov_lu   per-unit detector, covariance/LU route (paper-literal)
  *   - oracle_constellation   38.211 5.1 Gray QAM (reading R6)
  *   - oracle_maxlog          brute-force max-log over all 2^qm points (reading R5)
@@ -600,6 +601,35 @@ long oracle_detect(int route, int nr, int nl, int qm, long n_units, int n_re,
         if (!r) n_bad++;
     }
     return n_bad;
+}
+
+/* ------------------------------------------------------- BFP fronthaul -- */
+
+/* Block-floating-point decompression (the O-RAN format
+ * is not in the container, reading R25 fixes it): one block = one PRB (12
+ * subcarriers) of one antenna in one OFDM symbol, block_bytes = roundup4(1 + 3 W):
+ *   byte 0        exponent e in bits 0..3
+ *   bytes 1..     24 two's-complement W-bit mantissas m_j, j = 2 f + {0: I, 1: Q},
+ *                 packed MSB-first (stream bit 0 = bit 7 of byte 1)
+ *   value_j = m_j * 2^e * scale.
+ * Decoded bit by bit, in fp64, rounded once to fp32: out complex64 [n_blocks][12]. */
+void oracle_bfp_decode(long n_blocks, int W, double scale, const unsigned char* blocks, float* out)
+{
+    const int bb = ((1 + 3 * W) + 3) & ~3;
+    for (long b = 0; b < n_blocks; b++) {
+        const unsigned char* blk = blocks + (size_t)b * bb;
+        const int e = blk[0] & 0xF;
+        for (int j = 0; j < 24; j++) {
+            long m = 0;
+            for (int t = 0; t < W; t++) {
+                const int bit = j * W + t; /* stream bit index, MSB-first */
+                const int v = (blk[1 + bit / 8] >> (7 - bit % 8)) & 1;
+                m = (m << 1) | v;
+            }
+            if (m >= (1L << (W - 1))) m -= (1L << W); /* two's complement */
+            out[(size_t)b * 24 + j] = (float)((double)m * ldexp(1.0, e) * scale);
+        }
+    }
 }
 
 /* ----------------------------------------------------------- quantisers -- */

@@ -357,6 +357,131 @@ __global__ void __launch_bounds__(128, MINB) k_apply_stream(DetectArgs a) {
     }
 }
 
+// k_apply_bfp: the k_apply_units apply with the y loads replaced by fused
+// block-floating-point decompression (reading R25): per
+// (symbol, PRB, antenna) one block of roundup4(1 + 3W) bytes (exponent byte,
+// then 24 W-bit two's-complement mantissas MSB-first); thread (subcarrier f of
+// its PRB) reads the exponent word and the one or two 32-bit words holding its
+// 2W bits (I then Q), byte-swaps them into a big-endian 64-bit window, and
+// extracts the signed mantissas with arithmetic shifts: y = m * 2^e * scale.
+// The raw fp32 y never exists in HBM: y traffic drops from 64 B to
+// 8 * roundup4(1 + 3W) / 12 B per RE (18.7 B at W = 9).
+template <int NR, int NL, int QM, int LT, int G>
+__global__ void __launch_bounds__(128, 4) k_apply_bfp(DetectArgs a, const uint32_t* __restrict__ yb, int W, float scale) {
+    constexpr int NS = (kSym + G - 1) / G;
+    constexpr int WS = UnitWs<NR, NL>::stride;
+    pdl_launch_dependents();
+    const int sc = blockIdx.x * blockDim.x + threadIdx.x;
+    const int slot = blockIdx.y / G, g = blockIdx.y % G;
+    const bool active = sc < a.n_sc;
+    const int bw = ((1 + 3 * W) + 3) >> 2;  // 32-bit words per block
+    const int n_prb = a.n_sc / 12;
+    const int prb = sc / 12, f = sc % 12;
+    const int bit0 = 8 + 2 * f * W;         // stream position of this subcarrier's I mantissa
+    const int wi = bit0 >> 5, sh = bit0 & 31;
+    const bool two = sh + 2 * W > 32;
+    pdl_wait();  // W~ of this call's setup kernel is complete
+    if (!active) return;
+    const size_t unit = (size_t)slot * n_prb + prb;
+    const float* wsu = reinterpret_cast<const float*>(a.ws) + unit * WS;
+    float2 w[NL][NR];
+    static_assert((NL * NR * 8) % 32 == 0, "W~ rows in 32-byte chunks");
+#pragma unroll
+    for (int i = 0; i < NL * NR * 8 / 32; ++i)
+        ld_v8_coherent(wsu + 8 * i, reinterpret_cast<uint32_t*>(&w[0][0]) + 8 * i);
+    float slope[NL];
+#pragma unroll
+    for (int k = 0; k < NL; ++k) slope[k] = wsu[NL * NR * 2 + k];
+    constexpr int kLlrBytes = NL * QM * LlrTraits<LT>::bytes;
+    constexpr int kWords = (kLlrBytes + 3) / 4;
+    const bool zf = !(a.sigma2 > 0.f);
+    const float ia = rsqrtf((float)qam_norm(QM));
+#pragma unroll 1
+    for (int i = 0; i < NS; ++i) {
+        const int s = g + i * G;
+        if (s >= kSym) break;
+        const uint32_t* rowb = yb + ((size_t)(slot * kSym + s) * n_prb + prb) * NR * bw;
+        uint32_t ew[NR], a0[NR], a1[NR];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {  // issue all loads first
+            const uint32_t* blk = rowb + r * bw;
+            ew[r] = __ldg(blk);
+            a0[r] = __ldg(blk + wi);
+            a1[r] = two ? __ldg(blk + wi + 1) : 0u;
+        }
+        float2 yv[NR];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            const unsigned long long win =
+                (((unsigned long long)__byte_perm(a0[r], 0, 0x0123) << 32) | __byte_perm(a1[r], 0, 0x0123)) << sh;
+            const long long sv = (long long)win;
+            const int mi = (int)(sv >> (64 - W));
+            const int mq = (int)(((long long)(win << W)) >> (64 - W));
+            const float step = scale * __int_as_float((127 + (int)(ew[r] & 0xFu)) << 23);  // scale * 2^e
+            yv[r] = make_float2((float)mi * step, (float)mq * step);
+        }
+        float2 x[NL];
+#pragma unroll
+        for (int k = 0; k < NL; ++k) {
+            float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int r = 0; r < NR; ++r) acc = cmac(acc, w[k][r], yv[r]);
+            x[k] = acc;
+        }
+        const size_t re = (size_t)(slot * kSym + s) * a.n_sc + sc;
+        if (a.llr) {
+            float v[NL * QM];
+            uint32_t wd[kWords];
+            if (!zf) {
+#pragma unroll
+                for (int k = 0; k < NL; ++k) demap_layer<QM, false, LT>(x[k], slope[k], v + k * QM);
+                pack_llr<LT, NL * QM, false>(v, wd);
+            } else {
+#pragma unroll
+                for (int k = 0; k < NL; ++k) demap_layer<QM, true, LT>(x[k], slope[k], v + k * QM);
+                pack_llr<LT, NL * QM, true>(v, wd);
+            }
+            store_bytes<kLlrBytes>((char*)a.llr + re * kLlrBytes, wd);
+        }
+        if (a.xhat) {
+            uint32_t wd[2 * NL];
+#pragma unroll
+            for (int k = 0; k < NL; ++k) {
+                wd[2 * k] = __float_as_uint(x[k].x * ia);
+                wd[2 * k + 1] = __float_as_uint(x[k].y * ia);
+            }
+            store_bytes<NL * 8>(a.xhat + re * NL, wd);
+        }
+    }
+}
+
+template <int QM, int LT>
+cudaError_t launch_bfp_t(const DetectArgs& a, const uint32_t* yb, int W, float scale, cudaStream_t s) {
+    constexpr int G = 2;
+    const unsigned g1 = (unsigned)((a.n_units + 15) / 16);
+    cudaError_t e = launch_kernel(k_setup_units<8, 4, QM, 16>, dim3(g1), dim3(128), 0, s, a.overlap, a);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((a.n_sc + 127) / 128, a.n_slots * G);
+    cfg.blockDim = dim3(128);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = a.overlap ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k_apply_bfp<8, 4, QM, LT, G>, a, yb, W, scale);
+}
+
+template <int QM>
+cudaError_t launch_bfp_q(const DetectArgs& a, const uint32_t* yb, int W, float scale, cudaStream_t s) {
+    switch (a.llr_type) {
+    case kLlrF32: return launch_bfp_t<QM, kLlrF32>(a, yb, W, scale, s);
+    case kLlrF16: return launch_bfp_t<QM, kLlrF16>(a, yb, W, scale, s);
+    default: return launch_bfp_t<QM, kLlrI8>(a, yb, W, scale, s);
+    }
+}
+
 template <int NR, int NL, int QM, int LT, int UPC, int G, int PF, int SCPH, int MINB>
 cudaError_t launch_stream(const DetectArgs& a, cudaStream_t s) {
     if (a.n_units <= 0) return cudaSuccess;
@@ -415,6 +540,23 @@ const KernelEntry kEntries[] = {
 };
 
 }  // namespace
+
+bool bfp_supported(int n_rx, int n_layers, int sc_per_h, int sym_per_h) {
+    return n_rx == 8 && n_layers == 4 && sc_per_h == 12 && sym_per_h == kSym;
+}
+
+size_t bfp_workspace(const DetectArgs& a) { return (size_t)a.n_units * UnitWs<8, 4>::stride * 4; }
+
+cudaError_t launch_bfp(const DetectArgs& a, const void* y_bfp, int W, float scale, cudaStream_t s) {
+    if (a.n_units <= 0) return cudaSuccess;
+    const uint32_t* yb = static_cast<const uint32_t*>(y_bfp);
+    switch (a.qm) {
+    case 2: return launch_bfp_q<2>(a, yb, W, scale, s);
+    case 4: return launch_bfp_q<4>(a, yb, W, scale, s);
+    case 6: return launch_bfp_q<6>(a, yb, W, scale, s);
+    default: return launch_bfp_q<8>(a, yb, W, scale, s);
+    }
+}
 
 const KernelEntry* split_entries(int* n) {
     *n = (int)(sizeof(kEntries) / sizeof(kEntries[0]));

@@ -62,6 +62,10 @@ constexpr int kGenericMaxRx = 64;
 bool lu_route_supported(int n_rx);
 // Coloured-noise (interference-rejection) detector (k_irc.cu): Rnn device complex64 [n_units][n_rx][n_rx].
 bool irc_supported(int n_rx, int n_layers);
+// BFP-compressed y, fused decompression (k_split.cu; C3 family: 8 x 4, H per PRB).
+bool bfp_supported(int n_rx, int n_layers, int sc_per_h, int sym_per_h);
+size_t bfp_workspace(const DetectArgs& a);
+cudaError_t launch_bfp(const DetectArgs& a, const void* y_bfp, int iq_width, float scale, cudaStream_t s);
 cudaError_t launch_irc(const DetectArgs& a, const float2* Rnn, cudaStream_t s);
 size_t lu_route_workspace(int n_rx, long long n_units, int precision_bits);
 cudaError_t launch_lu_route(const DetectArgs& a, int precision_bits, cudaStream_t s, cudaEvent_t* ev);

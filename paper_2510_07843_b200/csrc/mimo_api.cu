@@ -475,6 +475,39 @@ mimo_status_t mimo_detect_irc(mimo_plan_t p, const void* H, const void* y, const
     return MIMO_OK;
 }
 
+mimo_status_t mimo_detect_mmse_bfp(mimo_plan_t p, const void* H, const void* y_bfp, float sigma2, int n_rx,
+                                   int n_layers, int n_sc, int n_sym, int qm, int iq_width, float bfp_scale,
+                                   void* llr_out, void* xhat_out, float* sinr_out) {
+    if (!p) return arg_fail(nullptr, "null plan");
+    mimo_status_t st = check_dims(p, sigma2, n_rx, n_layers, n_sc, n_sym, qm);
+    if (st != MIMO_OK) return st;
+    if (iq_width < 8 || iq_width > 16) return arg_fail(p, "iq_width must be in 8..16");
+    if (!(bfp_scale > 0.f) || !std::isfinite(bfp_scale)) return arg_fail(p, "bfp_scale must be finite > 0");
+    if (!mimo::bfp_supported(n_rx, n_layers, p->d.sc_per_h, p->d.sym_per_h)) {
+        snprintf(p->err, sizeof(p->err), "BFP route: supported for 8 rx x 4 layers, H per PRB, 14 symbols");
+        return MIMO_ERR_UNSUPPORTED;
+    }
+    if ((long long)n_sc * n_sym == 0) return MIMO_OK;
+    if (!H || !y_bfp) return arg_fail(p, "null H or y_bfp");
+    if (!llr_out && !xhat_out && !sinr_out) return arg_fail(p, "no output requested");
+    if (!aligned(H, 32) || !aligned(y_bfp, 4) || !aligned(llr_out, 16) || !aligned(xhat_out, 16) ||
+        !aligned(sinr_out, 4))
+        return arg_fail(p, "pointer misaligned (H 32 B, y_bfp 4 B, outputs 16 B)");
+    const int dev = p->d.device;
+    if (!is_device_ptr(H, dev) || !is_device_ptr(y_bfp, dev) || !is_device_ptr(llr_out, dev) ||
+        !is_device_ptr(xhat_out, dev) || !is_device_ptr(sinr_out, dev))
+        return arg_fail(p, "pointer is not device memory on the plan's device");
+    DeviceGuard g(dev);
+    if (g.err != cudaSuccess) return cuda_fail(p, g.err, "cudaSetDevice");
+    mimo::DetectArgs a = make_args(p, H, nullptr, sigma2, n_sc, n_sym, llr_out, xhat_out, sinr_out);
+    st = ensure_ws(p, 0, mimo::bfp_workspace(a), p->stream);
+    if (st != MIMO_OK) return st;
+    a.ws = p->kws[0];
+    cudaError_t e = mimo::launch_bfp(a, y_bfp, iq_width, bfp_scale, p->stream);
+    if (e != cudaSuccess) return cuda_fail(p, e, "BFP route");
+    return MIMO_OK;
+}
+
 mimo_status_t mimo_plan_reserve(mimo_plan_t p, int n_sc, int n_sym) {
     if (!p) return arg_fail(nullptr, "null plan");
     if (n_sc < 0 || n_sym < 0 || n_sc % p->d.sc_per_h || n_sym % p->d.sym_per_h)

@@ -81,6 +81,8 @@ def load_library(path: str | None = None):
     L.mimo_detect_lmmse_lu.restype = i
     L.mimo_detect_irc.argtypes = [vp, vp, vp, vp, i, i, i, i, i, vp, vp, vp]
     L.mimo_detect_irc.restype = i
+    L.mimo_detect_mmse_bfp.argtypes = [vp, vp, vp, f, i, i, i, i, i, i, f, vp, vp, vp]
+    L.mimo_detect_mmse_bfp.restype = i
     L.mimo_plan_reserve.argtypes = [vp, i, i]
     L.mimo_plan_reserve.restype = i
     L.mimo_plan_sync_status.argtypes = [vp, ctypes.POINTER(ll)]
@@ -269,6 +271,30 @@ class Plan:
         ptr = (lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None)
         self._check(self._lib.mimo_detect_irc(self._h, ptr(H), ptr(y), ptr(Rnn), self.n_rx, self.n_layers, n_sc,
                                               n_sym, self.qm, ptr(out), ptr(xhat), ptr(sinr)))
+        return out
+
+    def detect_bfp(self, H, y_bfp, sigma2: float, *, n_sym: int, n_sc: int, iq_width: int = 9,
+                   bfp_scale: float = 2.0 ** -8, out=None, xhat=None, sinr=None, want_llr: bool = True):
+        """Detect from BFP-compressed y (uint8 device tensor [n_sym][n_sc/12][n_rx][block_bytes])."""
+        import torch
+        sh = self.shapes(n_sc, n_sym)
+        self._dev_tensor(H, "H", torch.complex64, sh["H"])
+        bb = ((1 + 3 * iq_width) + 3) & ~3
+        self._dev_tensor(y_bfp, "y_bfp", torch.uint8, (n_sym, n_sc // 12, self.n_rx, bb))
+        if want_llr and out is None:
+            out = torch.empty(sh["llr"], dtype=self.llr_dtype, device=self.device)
+        if out is not None:
+            self._dev_tensor(out, "out", self.llr_dtype, sh["llr"])
+        if xhat is not None:
+            self._dev_tensor(xhat, "xhat", torch.complex64, sh["xhat"])
+        if sinr is not None:
+            self._dev_tensor(sinr, "sinr", torch.float32, sh["sinr"])
+        if self._fixed_stream is None:
+            self._lib.mimo_plan_set_stream(self._h, ctypes.c_void_p(self._stream_ptr()))
+        ptr = (lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None)
+        self._check(self._lib.mimo_detect_mmse_bfp(self._h, ptr(H), ptr(y_bfp), ctypes.c_float(sigma2), self.n_rx,
+                                                   self.n_layers, n_sc, n_sym, self.qm, int(iq_width),
+                                                   ctypes.c_float(bfp_scale), ptr(out), ptr(xhat), ptr(sinr)))
         return out
 
     def detect_host(self, H, y, sigma2: float, out=None):

@@ -265,6 +265,39 @@ def generate_irc(cfg, *, n_interf: int = 2, inr_db: float = 10.0, **kw) -> Workl
     return w
 
 
+def bfp_block_bytes(iq_width: int) -> int:
+    """Bytes of one BFP block (reading R25): exponent byte + 24 W-bit mantissas, rounded up to 4."""
+    return ((1 + 3 * iq_width) + 3) & ~3
+
+
+def bfp_compress(y: np.ndarray, iq_width: int = 9, scale: float = 2.0 ** -8) -> np.ndarray:
+    """RU-side block-floating-point compression of y (NEXT-4, reading R25).
+
+    y complex64 [n_sym][n_sc][n_rx] (n_sc a multiple of 12) -> uint8
+    [n_sym][n_sc/12][n_rx][bfp_block_bytes(W)]: per (symbol, PRB, antenna) the smallest
+    exponent e in 0..15 with every |I|, |Q| / (scale 2^e) rounding into the W-bit range,
+    mantissas round(v / (scale 2^e)) clipped to [-2^(W-1), 2^(W-1) - 1], packed MSB-first
+    after the exponent byte. The detector only ever sees what this encodes."""
+    W = int(iq_width)
+    n_sym, n_sc, nr = y.shape
+    n_prb = n_sc // 12
+    v = y.reshape(n_sym, n_prb, 12, nr).transpose(0, 1, 3, 2)            # [sym][prb][r][f]
+    iq = np.stack([v.real, v.imag], axis=-1).reshape(n_sym, n_prb, nr, 24).astype(np.float64)
+    mmax = 2 ** (W - 1) - 1
+    amax = np.max(np.abs(iq), axis=-1) / scale                          # [sym][prb][r]
+    e = np.zeros(amax.shape, np.int64)
+    for _ in range(16):                                                  # smallest e that fits
+        over = np.rint(amax / (2.0 ** e)) > mmax
+        e = np.where(over & (e < 15), e + 1, e)
+    m = np.clip(np.rint(iq / (scale * (2.0 ** e))[..., None]), -mmax - 1, mmax).astype(np.int64)
+    bits = ((m[..., None] & (1 << np.arange(W - 1, -1, -1))) != 0).astype(np.uint8)  # MSB-first
+    stream = bits.reshape(n_sym, n_prb, nr, 24 * W)
+    pad = 8 * (bfp_block_bytes(W) - 1) - 24 * W
+    stream = np.concatenate([stream, np.zeros(stream.shape[:-1] + (pad,), np.uint8)], axis=-1)
+    payload = np.packbits(stream, axis=-1, bitorder="big")
+    return np.concatenate([e.astype(np.uint8)[..., None], payload], axis=-1)
+
+
 def config_algorithmic_bytes(cfg_key, llr_bytes: int | None = None) -> dict:
     """Algorithmic bytes of one full pass (H read once, y read once, LLRs written once), SURVEY.md §8(d)."""
     c = CONFIGS[cfg_key]

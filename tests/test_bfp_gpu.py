@@ -1,0 +1,59 @@
+"""GPU parity of detection from BFP-compressed y (mimo_detect_mmse_bfp, SURVEY.md
+§8(f) NEXT-4, reading R25) against the oracle run on the oracle's own decode of
+the same bytes, at the north_star tolerances."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import parity
+from paper_2510_07843_b200 import mimo, synth
+
+pytestmark = pytest.mark.gpu
+SCALE = 2.0 ** -8
+
+
+def run_bfp(w, W, *, xhat=True):
+    p = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, llr_dtype=w.llr)
+    yb = torch.from_numpy(synth.bfp_compress(w.y, W, SCALE)).cuda()
+    sh = p.shapes(w.n_sc, w.n_sym)
+    x = torch.empty(sh["xhat"], dtype=torch.complex64, device="cuda") if xhat else None
+    s = torch.empty(sh["sinr"], dtype=torch.float32, device="cuda")
+    out = p.detect_bfp(torch.from_numpy(w.H).cuda(), yb, float(w.sigma2), n_sym=w.n_sym, n_sc=w.n_sc,
+                       iq_width=W, bfp_scale=SCALE, xhat=x, sinr=s)
+    nf = p.sync_status()
+    p.close()
+    r = dict(llr=out.cpu().numpy(), sinr=s.cpu().numpy(), n_failed=nf)
+    if xhat:
+        r["xhat"] = x.cpu().numpy()
+    return r
+
+
+def decoded_y(w, W):
+    d = oracle.bfp_decode(synth.bfp_compress(w.y, W, SCALE), W, SCALE)  # [sym][prb][r][f]
+    return np.ascontiguousarray(d.transpose(0, 1, 3, 2).reshape(w.y.shape))
+
+
+@pytest.mark.parametrize("W", [8, 9, 12, 16])
+def test_bfp_matches_oracle_on_decoded_y(W):
+    w = synth.generate(3, n_sc=300, n_slots=2)
+    g = run_bfp(w, W)
+    assert g["n_failed"] == 0
+    print(W, parity.compare(w, g, y=decoded_y(w, W)))
+
+
+def test_bfp_full_size_sampled():
+    w = synth.generate(3)
+    g = run_bfp(w, 9, xhat=False)
+    rng = np.random.default_rng(7)
+    units = np.unique(np.concatenate([[0, w.n_units - 1], rng.choice(w.n_units, 200, replace=False)]))
+    print(parity.compare(w, g, units, y=decoded_y(w, 9)))
+
+
+def test_bfp_unsupported_shape():
+    p = mimo.Plan(4, 4, 4)
+    w = synth.generate(2, n_sc=24, n_slots=1)
+    yb = torch.zeros((w.n_sym, 2, 4, 28), dtype=torch.uint8, device="cuda")
+    with pytest.raises(mimo.MimoError) as e:
+        p.detect_bfp(torch.from_numpy(w.H).cuda(), yb, float(w.sigma2), n_sym=w.n_sym, n_sc=24)
+    assert e.value.status == mimo.MIMO_ERR_UNSUPPORTED
