@@ -192,7 +192,7 @@ mimo_status_t mimo_detect_irc(mimo_plan_t plan, const void* H, const void* y, co
  *   block_bytes = roundup4(1 + 3 * iq_width); byte 0 = exponent e (bits 0..3);
  *   then the 24 two's-complement iq_width-bit mantissas I0,Q0,...,I11,Q11 of the
  *   PRB's 12 subcarriers, packed MSB-first; value = m * 2^e * bfp_scale.
- *   y_bfp: DEVICE bytes [n_sym][n_sc/12][n_rx][block_bytes], 4-byte aligned.
+ *   y_bfp: DEVICE bytes [n_sym][n_sc/12][n_rx][block_bytes], 16-byte aligned.
  * iq_width in 8..16; bfp_scale finite > 0. Everything else as mimo_detect_mmse_ex.
  * Supported for n_rx = 8, n_layers = 4, sc_per_h = 12, sym_per_h = 14 (the C3
  * family; else MIMO_ERR_UNSUPPORTED). Asynchronous. Errors: INVALID_ARG,

@@ -15,6 +15,8 @@
 // With MIMO_PLAN_OVERLAP_CALLS (PDL) the setup of call i+1 overlaps the apply
 // tail of call i, and the y loads of each apply overlap its setup's tail;
 // writes always follow griddepcontrol.wait.
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace mimo {
@@ -360,29 +362,47 @@ __global__ void __launch_bounds__(128, MINB) k_apply_stream(DetectArgs a) {
 // k_apply_bfp: the k_apply_units apply with the y loads replaced by fused
 // block-floating-point decompression (reading R25): per
 // (symbol, PRB, antenna) one block of roundup4(1 + 3W) bytes (exponent byte,
-// then 24 W-bit two's-complement mantissas MSB-first); thread (subcarrier f of
-// its PRB) reads the exponent word and the one or two 32-bit words holding its
-// 2W bits (I then Q), byte-swaps them into a big-endian 64-bit window, and
-// extracts the signed mantissas with arithmetic shifts: y = m * 2^e * scale.
+// then 24 W-bit two's-complement mantissas MSB-first). Per symbol the CTA's
+// blocks (<= 12 PRBs x 8 antennas, contiguous) are copied into shared memory with
+// coalesced 16-byte cp.async (double-buffered, next symbol in flight); thread
+// (subcarrier f of its PRB) reads the exponent and the one or two 32-bit words
+// holding its 2W bits (I then Q), byte-swaps them into a big-endian 64-bit window
+// and extracts the signed mantissas with arithmetic shifts: y = m * 2^e * scale.
 // The raw fp32 y never exists in HBM: y traffic drops from 64 B to
 // 8 * roundup4(1 + 3W) / 12 B per RE (18.7 B at W = 9).
 template <int NR, int NL, int QM, int LT, int G>
 __global__ void __launch_bounds__(128, 4) k_apply_bfp(DetectArgs a, const uint32_t* __restrict__ yb, int W, float scale) {
     constexpr int NS = (kSym + G - 1) / G;
     constexpr int WS = UnitWs<NR, NL>::stride;
+    constexpr int kMaxPrb = 12;                     // a 128-subcarrier CTA touches at most 12 PRBs
+    __shared__ __align__(16) uint32_t sb[2][kMaxPrb * NR * 13];  // 2 symbols x (PRBs x antennas x <= 52-byte blocks)
     pdl_launch_dependents();
-    const int sc = blockIdx.x * blockDim.x + threadIdx.x;
+    const int sc0 = blockIdx.x * blockDim.x;
+    const int sc = sc0 + threadIdx.x;
     const int slot = blockIdx.y / G, g = blockIdx.y % G;
     const bool active = sc < a.n_sc;
-    const int bw = ((1 + 3 * W) + 3) >> 2;  // 32-bit words per block
+    const int bw = ((1 + 3 * W) + 3) >> 2;         // 32-bit words per block
     const int n_prb = a.n_sc / 12;
+    const int p0 = sc0 / 12, p1 = min(n_prb, (sc0 + (int)blockDim.x + 11) / 12);
+    const int span16 = (p1 - p0) * NR * bw / 4;     // 16-byte chunks of the CTA's blocks in one symbol
     const int prb = sc / 12, f = sc % 12;
-    const int bit0 = 8 + 2 * f * W;         // stream position of this subcarrier's I mantissa
+    const int bit0 = 8 + 2 * f * W;                 // stream position of this subcarrier's I mantissa
     const int wi = bit0 >> 5, sh = bit0 & 31;
     const bool two = sh + 2 * W > 32;
+    // cooperative, coalesced 16-byte async copies of one symbol's blocks into a shared buffer
+    auto fetch = [&](int i, int buf) {
+        const int s = g + i * G;
+        if (s < kSym) {
+            const uint32_t* src = yb + ((size_t)(slot * kSym + s) * n_prb + p0) * NR * bw;
+            for (int q = threadIdx.x; q < span16; q += blockDim.x)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(&sb[buf][4 * q])),
+                             "l"(src + 4 * q) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    fetch(0, 0);
     pdl_wait();  // W~ of this call's setup kernel is complete
-    if (!active) return;
-    const size_t unit = (size_t)slot * n_prb + prb;
+    const size_t unit = (size_t)slot * n_prb + (active ? prb : p0);
     const float* wsu = reinterpret_cast<const float*>(a.ws) + unit * WS;
     float2 w[NL][NR];
     static_assert((NL * NR * 8) % 32 == 0, "W~ rows in 32-byte chunks");
@@ -400,26 +420,24 @@ __global__ void __launch_bounds__(128, 4) k_apply_bfp(DetectArgs a, const uint32
     for (int i = 0; i < NS; ++i) {
         const int s = g + i * G;
         if (s >= kSym) break;
-        const uint32_t* rowb = yb + ((size_t)(slot * kSym + s) * n_prb + prb) * NR * bw;
-        uint32_t ew[NR], a0[NR], a1[NR];
-#pragma unroll
-        for (int r = 0; r < NR; ++r) {  // issue all loads first
-            const uint32_t* blk = rowb + r * bw;
-            ew[r] = __ldg(blk);
-            a0[r] = __ldg(blk + wi);
-            a1[r] = two ? __ldg(blk + wi + 1) : 0u;
-        }
+        fetch(i + 1, (i + 1) & 1);                   // next symbol streams in while this one is decoded
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncthreads();
+        const uint32_t* rowb = &sb[i & 1][(prb - p0) * NR * bw];
         float2 yv[NR];
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
+            const uint32_t* blk = rowb + r * bw;
+            const uint32_t e = blk[0] & 0xFu, a0 = blk[wi], a1 = two ? blk[wi + 1] : 0u;
             const unsigned long long win =
-                (((unsigned long long)__byte_perm(a0[r], 0, 0x0123) << 32) | __byte_perm(a1[r], 0, 0x0123)) << sh;
-            const long long sv = (long long)win;
-            const int mi = (int)(sv >> (64 - W));
+                (((unsigned long long)__byte_perm(a0, 0, 0x0123) << 32) | __byte_perm(a1, 0, 0x0123)) << sh;
+            const int mi = (int)(((long long)win) >> (64 - W));
             const int mq = (int)(((long long)(win << W)) >> (64 - W));
-            const float step = scale * __int_as_float((127 + (int)(ew[r] & 0xFu)) << 23);  // scale * 2^e
+            const float step = scale * __int_as_float((127 + (int)e) << 23);  // scale * 2^e
             yv[r] = make_float2((float)mi * step, (float)mq * step);
         }
+        __syncthreads();                              // buffer i & 1 is refilled two iterations later
+        if (!active) continue;
         float2 x[NL];
 #pragma unroll
         for (int k = 0; k < NL; ++k) {
@@ -455,9 +473,8 @@ __global__ void __launch_bounds__(128, 4) k_apply_bfp(DetectArgs a, const uint32
     }
 }
 
-template <int QM, int LT>
-cudaError_t launch_bfp_t(const DetectArgs& a, const uint32_t* yb, int W, float scale, cudaStream_t s) {
-    constexpr int G = 2;
+template <int QM, int LT, int G>
+cudaError_t launch_bfp_g(const DetectArgs& a, const uint32_t* yb, int W, float scale, cudaStream_t s) {
     const unsigned g1 = (unsigned)((a.n_units + 15) / 16);
     cudaError_t e = launch_kernel(k_setup_units<8, 4, QM, 16>, dim3(g1), dim3(128), 0, s, a.overlap, a);
     if (e != cudaSuccess) return e;
@@ -471,6 +488,22 @@ cudaError_t launch_bfp_t(const DetectArgs& a, const uint32_t* yb, int W, float s
     cfg.attrs = attr;
     cfg.numAttrs = a.overlap ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, k_apply_bfp<8, 4, QM, LT, G>, a, yb, W, scale);
+}
+
+// symbols per thread = 14 / G; MIMO_BFP_G (tuning knob) overrides the default G = 2
+template <int QM, int LT>
+cudaError_t launch_bfp_t(const DetectArgs& a, const uint32_t* yb, int W, float scale, cudaStream_t s) {
+    static int g = 0;
+    if (!g) {
+        const char* e = getenv("MIMO_BFP_G");
+        g = e ? atoi(e) : 2;
+    }
+    switch (g) {
+    case 1: return launch_bfp_g<QM, LT, 1>(a, yb, W, scale, s);
+    case 2: return launch_bfp_g<QM, LT, 2>(a, yb, W, scale, s);
+    case 14: return launch_bfp_g<QM, LT, 14>(a, yb, W, scale, s);
+    default: return launch_bfp_g<QM, LT, 7>(a, yb, W, scale, s);
+    }
 }
 
 template <int QM>

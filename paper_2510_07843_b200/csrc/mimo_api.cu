@@ -490,9 +490,9 @@ mimo_status_t mimo_detect_mmse_bfp(mimo_plan_t p, const void* H, const void* y_b
     if ((long long)n_sc * n_sym == 0) return MIMO_OK;
     if (!H || !y_bfp) return arg_fail(p, "null H or y_bfp");
     if (!llr_out && !xhat_out && !sinr_out) return arg_fail(p, "no output requested");
-    if (!aligned(H, 32) || !aligned(y_bfp, 4) || !aligned(llr_out, 16) || !aligned(xhat_out, 16) ||
+    if (!aligned(H, 32) || !aligned(y_bfp, 16) || !aligned(llr_out, 16) || !aligned(xhat_out, 16) ||
         !aligned(sinr_out, 4))
-        return arg_fail(p, "pointer misaligned (H 32 B, y_bfp 4 B, outputs 16 B)");
+        return arg_fail(p, "pointer misaligned (H 32 B, y_bfp 16 B, outputs 16 B)");
     const int dev = p->d.device;
     if (!is_device_ptr(H, dev) || !is_device_ptr(y_bfp, dev) || !is_device_ptr(llr_out, dev) ||
         !is_device_ptr(xhat_out, dev) || !is_device_ptr(sinr_out, dev))
