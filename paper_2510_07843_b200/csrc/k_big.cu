@@ -1246,11 +1246,8 @@ const KernelEntry kEntries[] = {
     }
     BIG4_ENTRY("big4_64x16_q6_i8", 4, 4, 2),  // C5 default: tcgen05 3-pass TF32 apply (fastest)
     BIG4_ENTRY("big4e8_64x16_q6_i8", 8, 4, 2),
-    BIG4_ENTRY("big4s5_64x16_q6_i8", 4, 5, 2),
     KernelEntry{"big5_64x16_q6_i8", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 0, 1>,
                 prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 0, 1>, workspace<64, 16>},
-    KernelEntry{"big5s3_64x16_q6_i8", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 3, 2, 0, 1>,
-                prepare_ap4<64, 16, 6, kLlrI8, 4, 3, 2, 0, 1>, workspace<64, 16>},
     KernelEntry{"ablation_big5_none", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 3, 1>,
                 prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 3, 1>, workspace<64, 16>},
     // timing ablations (results are wrong on purpose; only reachable through MIMO_FORCE_KERNEL)

@@ -241,299 +241,6 @@ __global__ void __launch_bounds__(32 * NW) k_lg(DetectArgs a) {
     }
 }
 
-// k_lg2: the same per-unit computation with (i) a ring of R y slots per unit
-// instead of all 14 symbols (each unit's group leader refills its own slot
-// with a 16-byte-aligned bulk copy once the group has consumed it; one
-// mbarrier per (unit, slot)), which cuts shared memory per CTA to raise the
-// resident warps, and (ii) 128-bit shared loads of H and y rows.
-template <int NR, int NL, int NW, int R>
-struct Lg2Smem {
-    static constexpr int UPW = 32 / NL;
-    static constexpr int TU = UPW * NW;
-    static constexpr int YS = NR + 2;                                       // float2 per unit y slot
-    static constexpr int HS = NR * NL + 4;                                  // float2 per unit H
-    static constexpr int LS = NL * NL + 4;                                  // float2 per unit L / X
-    static constexpr size_t y = 0;                                          // [R][TU][YS]
-    static constexpr size_t H = y + (size_t)R * TU * YS * 8;                // [TU][HS]
-    static constexpr size_t LX = H + (size_t)TU * HS * 8;                   // [TU][LS]
-    static constexpr size_t dinv = LX + (size_t)TU * LS * 8;                // [TU][NL]
-    static constexpr size_t bars = (dinv + (size_t)TU * NL * 4 + 7) / 8 * 8;  // [TU][R + 1]
-    static constexpr size_t total = bars + (size_t)TU * (R + 1) * 8;
-};
-
-template <int NR, int NL, int QM, int LT, int NW, int R, int SU>
-__global__ void __launch_bounds__(32 * NW) k_lg2(DetectArgs a) {
-    using SM = Lg2Smem<NR, NL, NW, R>;
-    constexpr int UPW = SM::UPW;
-    constexpr int TU = SM::TU;
-    static_assert(32 % NL == 0 && NL % 2 == 0 && NR % 2 == 0, "k_lg2 shape");
-    static_assert(R >= 1 && R <= kSym, "ring depth");
-    extern __shared__ __align__(128) unsigned char smem[];
-    float2* sy = reinterpret_cast<float2*>(smem + SM::y);
-    float2* sH = reinterpret_cast<float2*>(smem + SM::H);
-    float2* sLX = reinterpret_cast<float2*>(smem + SM::LX);
-    float* sDinv = reinterpret_cast<float*>(smem + SM::dinv);
-
-    pdl_launch_dependents();
-    const int slot = blockIdx.y;
-    const int sc0 = blockIdx.x * TU;
-    const int nvalid = min(TU, a.n_sc - sc0);
-    const int t = threadIdx.x;
-    const int lane = t & 31, warp = t >> 5;
-    const int k = lane % NL;                     // this lane's layer
-    const int gbase = lane - k;                  // first lane of the group
-    const int ul = warp * UPW + lane / NL;       // unit within the tile
-    const bool active = ul < nvalid;
-    const bool leader = active && k == 0;
-    const int sc = sc0 + ul;
-    const float s2 = a.sigma2;
-    const float norm = (float)qam_norm(QM);
-    uint64_t* ubar = reinterpret_cast<uint64_t*>(smem + SM::bars) + ul * (R + 1);  // [0, R) y slots, [R] H
-    const float2* ysrc = a.y + ((size_t)slot * kSym * a.n_sc + sc) * NR;           // symbol 0 of this unit
-    const size_t ystride = (size_t)a.n_sc * NR;                                     // one symbol row
-    if (leader) {
-#pragma unroll
-        for (int i = 0; i <= R; ++i) mbar_init(&ubar[i], 1);
-        fence_mbar_init();
-        mbar_arrive_expect_tx(&ubar[R], (uint32_t)(NR * NL * 8));
-        bulk_g2s(sH + ul * SM::HS, a.H + ((size_t)slot * a.n_sc + sc) * NR * NL, NR * NL * 8u, &ubar[R]);
-#pragma unroll
-        for (int s = 0; s < R; ++s) {
-            mbar_arrive_expect_tx(&ubar[s], (uint32_t)(NR * 8));
-            bulk_g2s(sy + (s * TU + ul) * SM::YS, ysrc + s * ystride, NR * 8u, &ubar[s]);
-        }
-    }
-    __syncwarp();
-    if (active) mbar_wait(&ubar[R], 0);
-
-    const float2* hU = sH + ul * SM::HS;  // H[r][l] of this lane's unit (garbage but in-bounds if !active)
-    // a2: row k of G, 128-bit row reads
-    float2 g[NL];
-#pragma unroll
-    for (int j = 0; j < NL; ++j) g[j] = make_float2(0.f, 0.f);
-#pragma unroll 4
-    for (int r = 0; r < NR; ++r) {
-        const float2 hk = hU[r * NL + k];
-        const float4* hr = reinterpret_cast<const float4*>(hU + r * NL);
-#pragma unroll
-        for (int j2 = 0; j2 < NL / 2; ++j2) {  // conj(H_rk) H_rj
-            const float4 v = hr[j2];
-            g[2 * j2].x = fmaf(hk.x, v.x, fmaf(hk.y, v.y, g[2 * j2].x));
-            g[2 * j2].y = fmaf(hk.x, v.y, fmaf(-hk.y, v.x, g[2 * j2].y));
-            g[2 * j2 + 1].x = fmaf(hk.x, v.z, fmaf(hk.y, v.w, g[2 * j2 + 1].x));
-            g[2 * j2 + 1].y = fmaf(hk.x, v.w, fmaf(-hk.y, v.z, g[2 * j2 + 1].y));
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < NL; ++j)
-        if (j == k) g[j] = make_float2(g[j].x + s2, 0.f);
-    float gmax = 0.f;
-#pragma unroll
-    for (int j = 0; j < NL; ++j)
-        if (j == k) gmax = g[j].x;
-#pragma unroll
-    for (int off = 1; off < NL; off <<= 1) gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, off));
-
-    // a3: right-looking Cholesky, lane k holds row k (guard R17)
-    bool fail = !(gmax == gmax);
-    float my_dinv = 0.f;
-#pragma unroll
-    for (int j = 0; j < NL; ++j) {
-        float p = __shfl_sync(0xffffffffu, g[j].x, gbase + j);
-        if (!(p > (float)kPivotTau * gmax)) {
-            fail = true;
-            p = 1.f;
-        }
-        const float dinv = rsqrtf(p);
-        if (k == j) my_dinv = dinv;
-        if (k > j) g[j] = make_float2(g[j].x * dinv, g[j].y * dinv);
-#pragma unroll
-        for (int m = j + 1; m < NL; ++m) {
-            const float2 lmj = shfl2(g[j], gbase + m);
-            if (k >= m) {
-                g[m].x = fmaf(-g[j].x, lmj.x, fmaf(-g[j].y, lmj.y, g[m].x));
-                g[m].y = fmaf(-g[j].y, lmj.x, fmaf(g[j].x, lmj.y, g[m].y));
-            }
-        }
-    }
-    float2* lU = sLX + ul * SM::LS;
-#pragma unroll
-    for (int j = 0; j < NL; ++j) lU[k * NL + j] = (j < k) ? g[j] : make_float2(0.f, 0.f);
-    sDinv[ul * NL + k] = my_dinv;
-    __syncwarp();
-    // a4: column k of X = L^-1
-    float2 x[NL];
-#pragma unroll
-    for (int i = 0; i < NL; ++i) {
-        float2 sv = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int m = 0; m < i; ++m) sv = cmac(sv, lU[i * NL + m], x[m]);
-        const float di = sDinv[ul * NL + i];
-        x[i] = (i == k) ? make_float2(my_dinv, 0.f)
-                        : (i < k ? make_float2(0.f, 0.f) : make_float2(-sv.x * di, -sv.y * di));
-    }
-    float A = 0.f;
-#pragma unroll
-    for (int i = 0; i < NL; ++i) A = fmaf(x[i].x, x[i].x, fmaf(x[i].y, x[i].y, A));
-    __syncwarp();
-#pragma unroll
-    for (int i = 0; i < NL; ++i) lU[i * NL + k] = x[i];
-    __syncwarp();
-    // row k of G^-1 = X^H X
-    float2 gi[NL];
-#pragma unroll
-    for (int j = 0; j < NL; ++j) {
-        float2 sv = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int m = j; m < NL; ++m) {
-            const float2 xm = x[m], xmj = lU[m * NL + j];
-            sv.x = fmaf(xm.x, xmj.x, fmaf(xm.y, xmj.y, sv.x));
-            sv.y = fmaf(xm.x, xmj.y, fmaf(-xm.y, xmj.x, sv.y));
-        }
-        gi[j] = sv;
-    }
-    // a5
-    float sinr, fac;
-    const float mu = fmaf(-s2, A, 1.f);
-    if (s2 == 0.f) {
-        sinr = __int_as_float(0x7f800000);
-        fac = sqrtf(norm);
-    } else {
-        sinr = __fdividef(mu, s2 * A);
-        fac = __fdividef(sqrtf(norm), mu);
-    }
-    if (!(mu > 0.f) || fail) {
-        sinr = 0.f;
-        fac = 0.f;
-    }
-    const float slope = sinr / norm * a.llr_scale;
-    // row k of W~ = fac_k G^-1 H^H (level units)
-    float2 w[NR];
-#pragma unroll
-    for (int r = 0; r < NR; ++r) {
-        const float4* hr = reinterpret_cast<const float4*>(hU + r * NL);
-        float2 sv = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int j2 = 0; j2 < NL / 2; ++j2) {
-            const float4 h = hr[j2];
-            sv.x = fmaf(gi[2 * j2].x, h.x, fmaf(gi[2 * j2].y, h.y, sv.x));
-            sv.y = fmaf(gi[2 * j2].y, h.x, fmaf(-gi[2 * j2].x, h.y, sv.y));
-            sv.x = fmaf(gi[2 * j2 + 1].x, h.z, fmaf(gi[2 * j2 + 1].y, h.w, sv.x));
-            sv.y = fmaf(gi[2 * j2 + 1].y, h.z, fmaf(-gi[2 * j2 + 1].x, h.w, sv.y));
-        }
-        w[r] = (fac > 0.f) ? make_float2(sv.x * fac, sv.y * fac) : make_float2(0.f, 0.f);
-    }
-
-    pdl_wait();  // global writes only after the previous grid completed
-    if (active) {
-        const size_t unit = (size_t)slot * a.n_sc + sc;
-        if (k == 0 && fail) atomicAdd(a.fail_count, 1ull);
-        if (a.sinr) a.sinr[unit * NL + k] = sinr;
-    }
-    constexpr int kLlrBytes = QM * LlrTraits<LT>::bytes;  // this lane's layer
-    constexpr int kWords = (kLlrBytes + 3) / 4;
-    const float ia = rsqrtf(norm);
-    const bool zf = !(s2 > 0.f);
-    if constexpr (SU == 2) {
-        // all 14 symbols staged (R == 14): two symbols per iteration, even/odd-antenna
-        // partial sums -> 8 independent FMA chains per lane
-        static_assert(R == kSym, "SU = 2 needs the full y tile");
-#pragma unroll 1
-        for (int s = 0; s < kSym; s += 2) {
-            float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-            if (active) {
-                mbar_wait(&ubar[s], 0);
-                mbar_wait(&ubar[s + 1], 0);
-                const float4* y0 = reinterpret_cast<const float4*>(sy + (s * TU + ul) * SM::YS);
-                const float4* y1 = reinterpret_cast<const float4*>(sy + ((s + 1) * TU + ul) * SM::YS);
-                float2 b0 = make_float2(0.f, 0.f), b1 = make_float2(0.f, 0.f);
-#pragma unroll
-                for (int r2 = 0; r2 < NR / 2; ++r2) {
-                    const float4 v0 = y0[r2], v1 = y1[r2];
-                    acc[0] = cmac(acc[0], w[2 * r2], make_float2(v0.x, v0.y));
-                    b0 = cmac(b0, w[2 * r2 + 1], make_float2(v0.z, v0.w));
-                    acc[1] = cmac(acc[1], w[2 * r2], make_float2(v1.x, v1.y));
-                    b1 = cmac(b1, w[2 * r2 + 1], make_float2(v1.z, v1.w));
-                }
-                acc[0] = make_float2(acc[0].x + b0.x, acc[0].y + b0.y);
-                acc[1] = make_float2(acc[1].x + b1.x, acc[1].y + b1.y);
-            }
-            if (!active) continue;
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const size_t re = (size_t)(slot * kSym + s + e) * a.n_sc + sc;
-                if (a.llr) {
-                    float v[QM];
-                    uint32_t wd[kWords];
-                    if (!zf) {
-                        demap_layer<QM, false, LT>(acc[e], slope, v);
-                        pack_llr<LT, QM, false>(v, wd);
-                    } else {
-                        demap_layer<QM, true, LT>(acc[e], slope, v);
-                        pack_llr<LT, QM, true>(v, wd);
-                    }
-                    store_bytes<kLlrBytes>((char*)a.llr + (re * NL + k) * kLlrBytes, wd);
-                }
-                if (a.xhat) a.xhat[re * NL + k] = make_float2(acc[e].x * ia, acc[e].y * ia);
-            }
-        }
-        return;
-    }
-#pragma unroll 1
-    for (int s = 0; s < kSym; ++s) {
-        const int rs = s % R;
-        float2 acc = make_float2(0.f, 0.f);
-        if (active) {
-            mbar_wait(&ubar[rs], (uint32_t)((s / R) & 1));
-            const float4* ys = reinterpret_cast<const float4*>(sy + (rs * TU + ul) * SM::YS);
-#pragma unroll
-            for (int r2 = 0; r2 < NR / 2; ++r2) {
-                const float4 v = ys[r2];
-                acc = cmac(acc, w[2 * r2], make_float2(v.x, v.y));
-                acc = cmac(acc, w[2 * r2 + 1], make_float2(v.z, v.w));
-            }
-        }
-        uint32_t wd[kWords];
-        if (a.llr) {
-            float v[QM];
-            if (!zf) {
-                demap_layer<QM, false, LT>(acc, slope, v);
-                pack_llr<LT, QM, false>(v, wd);
-            } else {
-                demap_layer<QM, true, LT>(acc, slope, v);
-                pack_llr<LT, QM, true>(v, wd);
-            }
-        }
-        __syncwarp();  // the group has consumed slot rs (its values are in acc)
-        if (leader && s + R < kSym) {
-            mbar_arrive_expect_tx(&ubar[rs], (uint32_t)(NR * 8));
-            bulk_g2s(sy + (rs * TU + ul) * SM::YS, ysrc + (s + R) * ystride, NR * 8u, &ubar[rs]);
-        }
-        if (!active) continue;
-        const size_t re = (size_t)(slot * kSym + s) * a.n_sc + sc;
-        if (a.llr) store_bytes<kLlrBytes>((char*)a.llr + (re * NL + k) * kLlrBytes, wd);
-        if (a.xhat) a.xhat[re * NL + k] = make_float2(acc.x * ia, acc.y * ia);
-    }
-}
-
-template <int NR, int NL, int QM, int LT, int NW, int R, int SU>
-cudaError_t launch2(const DetectArgs& a, cudaStream_t s) {
-    if (a.n_sc <= 0 || a.n_slots <= 0) return cudaSuccess;
-    constexpr int TU = Lg2Smem<NR, NL, NW, R>::TU;
-    dim3 grid((a.n_sc + TU - 1) / TU, a.n_slots);
-    return launch_kernel(k_lg2<NR, NL, QM, LT, NW, R, SU>, grid, dim3(32 * NW), Lg2Smem<NR, NL, NW, R>::total, s,
-                         a.overlap, a);
-}
-
-template <int NR, int NL, int QM, int LT, int NW, int R, int SU>
-cudaError_t prepare2() {
-    constexpr size_t smem = Lg2Smem<NR, NL, NW, R>::total;
-    if (smem > 48 * 1024)
-        return cudaFuncSetAttribute(k_lg2<NR, NL, QM, LT, NW, R, SU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem);
-    return cudaSuccess;
-}
-
 // k_lg3: k_lg with the CTA's whole y tile (14 symbols x TU subcarriers x NR
 // antennas) fetched by ONE TMA tensor-box copy (3-D map {2 NR floats, n_sc,
 // n_sym}, box {2 NR, TU, 14}, SWIZZLE_128B) instead of 14 small bulk copies per
@@ -816,13 +523,6 @@ cudaError_t prepare() {
 #define LG_ENTRY(NAME, NR, NL, QM, LT, NW) \
     KernelEntry { NAME, NR, NL, QM, 1, 14, LT, 32, 1, launch<NR, NL, QM, LT, NW>, prepare<NR, NL, QM, LT, NW> }
 
-#define LG2_ENTRY(NAME, NR, NL, QM, LT, NW, R) LG2S_ENTRY(NAME, NR, NL, QM, LT, NW, R, 1)
-#define LG2S_ENTRY(NAME, NR, NL, QM, LT, NW, R, SU)                                                    \
-    KernelEntry {                                                                                      \
-        NAME, NR, NL, QM, 1, 14, LT, 32, 1, launch2<NR, NL, QM, LT, NW, R, SU>,                        \
-            prepare2<NR, NL, QM, LT, NW, R, SU>                                                        \
-    }
-
 #define LG3_ENTRY(NAME, NR, NL, QM, LT, NW) LG3P_ENTRY(NAME, NR, NL, QM, LT, NW, 0)
 #define LG3P_ENTRY(NAME, NR, NL, QM, LT, NW, PFD)                                                      \
     KernelEntry {                                                                                      \
@@ -833,17 +533,7 @@ const KernelEntry kEntries[] = {
     LG3_ENTRY("lg3_16x8_q8_f16", 16, 8, 8, kLlrF16, 2),  // C4 (one TMA tensor box per CTA for y)
     LG_ENTRY("lg_16x8_q8_f16", 16, 8, 8, kLlrF16, 2),
     LG3_ENTRY("lg3_16x8_q8_f16_w1", 16, 8, 8, kLlrF16, 1),
-    LG3P_ENTRY("lg3_16x8_q8_f16_pf1036", 16, 8, 8, kLlrF16, 2, 1036),
-    LG3P_ENTRY("lg3_16x8_q8_f16_pf2072", 16, 8, 8, kLlrF16, 2, 2072),
-    LG3P_ENTRY("lg3_16x8_q8_f16_pf518", 16, 8, 8, kLlrF16, 2, 518),
     LG3_ENTRY("lg3_16x8_q8_f16_w4", 16, 8, 8, kLlrF16, 4),
-    LG2_ENTRY("lg2_16x8_q8_f16", 16, 8, 8, kLlrF16, 2, 4),
-    LG2_ENTRY("lg2_16x8_q8_f16_r14", 16, 8, 8, kLlrF16, 2, 14),
-    LG2S_ENTRY("lg2_16x8_q8_f16_r14s2", 16, 8, 8, kLlrF16, 2, 14, 2),
-    LG2S_ENTRY("lg2_16x8_q8_f16_r14s2w1", 16, 8, 8, kLlrF16, 1, 14, 2),
-    LG2_ENTRY("lg2_16x8_q8_f16_r6", 16, 8, 8, kLlrF16, 2, 6),
-    LG2_ENTRY("lg2_16x8_q8_f16_w1", 16, 8, 8, kLlrF16, 1, 4),
-    LG2_ENTRY("lg2_16x8_q8_f16_w4", 16, 8, 8, kLlrF16, 4, 4),
     LG_ENTRY("lg_16x8_q8_f32", 16, 8, 8, kLlrF32, 2),
     LG_ENTRY("lg_16x8_q8_i8", 16, 8, 8, kLlrI8, 2),
     LG_ENTRY("lg_16x8_q6_f16", 16, 8, 6, kLlrF16, 2),

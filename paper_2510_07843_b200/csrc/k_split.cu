@@ -556,20 +556,9 @@ cudaError_t launch(const DetectArgs& a, cudaStream_t s) {
 const KernelEntry kEntries[] = {
     STREAM_ENTRY_B("stream_8x4_q6_i8", 8, 4, 6, kLlrI8, 12, 16, 2, 2, 4),  // C3: <= 128 regs -> 4 CTAs/SM
     STREAM_ENTRY("stream_8x4_q6_i8_pf3", 8, 4, 6, kLlrI8, 12, 16, 2, 3),
-    STREAM_ENTRY("stream_8x4_q6_i8_g1pf4", 8, 4, 6, kLlrI8, 12, 16, 1, 4),
-    STREAM_ENTRY("stream_8x4_q6_i8_g1pf3", 8, 4, 6, kLlrI8, 12, 16, 1, 3),
-    STREAM_ENTRY("stream_8x4_q6_i8_g2pf2", 8, 4, 6, kLlrI8, 12, 16, 2, 2),
-    STREAM_ENTRY("stream_8x4_q6_i8_g2pf4", 8, 4, 6, kLlrI8, 12, 16, 2, 4),
-    STREAM_ENTRY("stream_8x4_q6_i8_g7pf2", 8, 4, 6, kLlrI8, 12, 16, 7, 2),
-    STREAM_ENTRY_B("stream_8x4_q6_i8_b5", 8, 4, 6, kLlrI8, 12, 16, 2, 2, 5),
-    STREAM_ENTRY_B("stream_8x4_q6_i8_g1b4", 8, 4, 6, kLlrI8, 12, 16, 1, 2, 4),
-    STREAM_ENTRY_B("stream_8x4_q6_i8_g7b6", 8, 4, 6, kLlrI8, 12, 16, 7, 2, 6),
     SPLIT_ENTRY("split_8x4_q6_i8", 8, 4, 6, kLlrI8, 12, 32, 7),
     SPLIT_ENTRY("split_8x4_q6_f32", 8, 4, 6, kLlrF32, 12, 32, 7),
     SPLIT_ENTRY("split_8x4_q6_f16", 8, 4, 6, kLlrF16, 12, 32, 7),
-    SPLIT_ENTRY("split_8x4_q6_i8_g2", 8, 4, 6, kLlrI8, 12, 32, 2),
-    SPLIT_ENTRY("split_8x4_q6_i8_g14", 8, 4, 6, kLlrI8, 12, 32, 14),
-    SPLIT_ENTRY("split_8x4_q6_i8_u16", 8, 4, 6, kLlrI8, 12, 16, 7),
 };
 
 }  // namespace

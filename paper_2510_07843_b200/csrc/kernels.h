@@ -45,7 +45,6 @@ struct KernelEntry {
 // Tables provided by each kernel family (k_*.cu).
 const KernelEntry* tpu_entries(int* n);
 const KernelEntry* prb_entries(int* n);
-const KernelEntry* prbp_entries(int* n);
 const KernelEntry* split_entries(int* n);
 const KernelEntry* lg_entries(int* n);
 const KernelEntry* big_entries(int* n);

@@ -72,8 +72,8 @@ mimo_status_t arg_fail(mimo_plan_t p, const char* what) {
 // (a tuning/debug knob) picks a named variant instead, or "generic".
 const mimo::KernelEntry* select_fast(const mimo_plan_desc_t& d) {
     using LF = const mimo::KernelEntry* (*)(int*);
-    const LF tables[] = {mimo::tpu_entries, mimo::split_entries, mimo::lg_entries, mimo::big_entries, mimo::prb_entries,
-                         mimo::prbp_entries};
+    const LF tables[] = {mimo::tpu_entries, mimo::split_entries, mimo::lg_entries, mimo::big_entries,
+                         mimo::prb_entries};
     const char* force = getenv("MIMO_FORCE_KERNEL");
     if (force && strcmp(force, "generic") == 0) return nullptr;
     for (LF f : tables) {
