@@ -249,23 +249,27 @@ __global__ void __launch_bounds__(32 * NW) k_lg(DetectArgs a) {
 // Row = 14-symbol index x TU + unit; the 16-byte chunk c of a row sits at
 // c ^ (row & 7), so the UPW units of a warp reading the same antennas hit
 // different bank groups (no padding needed). Ragged tails are zero-filled by TMA.
-template <int NR, int NL, int NW>
+template <int NR, int NL, int NW, int HT = 0>
 struct Lg3Smem {
     static constexpr int UPW = 32 / NL;
     static constexpr int TU = UPW * NW;
     static constexpr int HS = NR * NL + 4;                                  // float2 per unit H (padded)
     static constexpr int LS = NL * NL + 4;                                  // float2 per unit L / X
     static constexpr size_t y = 0;                                          // [14][TU][NR] float2, SW128
-    static constexpr size_t H = (size_t)kSym * TU * NR * 8;                 // [TU][HS]
-    static constexpr size_t LX = H + (size_t)TU * HS * 8;                   // [TU][LS]
+    static constexpr size_t H = (size_t)kSym * TU * NR * 8;                 // [TU][HS], or HT: [NR*NL/16][TU][128 B] SW128
+    static constexpr size_t LX = H + (HT ? (size_t)TU * NR * NL * 8 : (size_t)TU * HS * 8);  // [TU][LS]
     static constexpr size_t dinv = LX + (size_t)TU * LS * 8;                // [TU][NL]
     static constexpr size_t bars = (dinv + (size_t)TU * NL * 4 + 7) / 8 * 8;  // y, H
     static constexpr size_t total = bars + 16 + 1024;                       // + 1024-alignment slack
 };
 
-template <int NR, int NL, int QM, int LT, int NW, int PFD>
-__global__ void __launch_bounds__(32 * NW) k_lg3(DetectArgs a, const __grid_constant__ CUtensorMap ymap) {
-    using SM = Lg3Smem<NR, NL, NW>;
+// HT = 1: H also by one TMA tensor box per CTA: H viewed as (32 floats = one 128-byte row of
+// 2 rx x 8 layers, unit, row-within-unit) -- unit as the middle dimension -- so the box lands
+// as [row][unit][128 B] and SWIZZLE_128B spreads the UPW units of a warp over distinct banks.
+template <int NR, int NL, int QM, int LT, int NW, int PFD, int HT = 0>
+__global__ void __launch_bounds__(32 * NW) k_lg3(DetectArgs a, const __grid_constant__ CUtensorMap ymap,
+                                                 const __grid_constant__ CUtensorMap hmap) {
+    using SM = Lg3Smem<NR, NL, NW, HT>;
     constexpr int UPW = SM::UPW;
     constexpr int TU = SM::TU;
     static_assert(32 % NL == 0 && NR * 8 == 128, "k_lg3: one 128-byte row per (symbol, unit)");
@@ -298,7 +302,12 @@ __global__ void __launch_bounds__(32 * NW) k_lg3(DetectArgs a, const __grid_cons
         fence_mbar_init();
         mbar_arrive_expect_tx(&bars[0], (uint32_t)(kSym * TU * NR * 8));
         tma_load_3d(base + (uint32_t)SM::y, &ymap, 0, sc0, slot * kSym, &bars[0]);
-        mbar_arrive_expect_tx(&bars[1], (uint32_t)nvalid * NR * NL * 8u);
+        if constexpr (HT) {
+            mbar_arrive_expect_tx(&bars[1], (uint32_t)(TU * NR * NL * 8));
+            tma_load_3d(base + (uint32_t)SM::H, &hmap, 0, slot * a.n_sc + sc0, 0, &bars[1]);
+        } else {
+            mbar_arrive_expect_tx(&bars[1], (uint32_t)nvalid * NR * NL * 8u);
+        }
         if constexpr (PFD > 0) {
             // warm L2 with the H and y tiles of the CTA PFD launches ahead (about one wave later),
             // so its start-up loads hit L2 instead of exposing DRAM latency
@@ -315,20 +324,31 @@ __global__ void __launch_bounds__(32 * NW) k_lg3(DetectArgs a, const __grid_cons
         }
     }
     __syncthreads();
-    if (k == 0 && active)
+    if (!HT && k == 0 && active)
         bulk_g2s(sH + ul * SM::HS, a.H + ((size_t)slot * a.n_sc + sc) * NR * NL, NR * NL * 8u, &bars[1]);
     mbar_wait(&bars[1], 0);
 
     const float2* hU = sH + ul * SM::HS;
+    const unsigned char* hT = smem + SM::H;
+    auto hat = [&](int r, int j) -> float2 {  // H[r][j] of this lane's unit
+        if constexpr (HT) {
+            constexpr int RPR = 128 / (NL * 8);  // rx rows per 128-byte row
+            const int row = (r / RPR) * TU + ul;
+            const int byte = (r % RPR) * NL * 8 + j * 8;
+            return *reinterpret_cast<const float2*>(hT + row * 128 + (((byte >> 4) ^ (row & 7)) << 4) + (byte & 15));
+        } else {
+            return hU[r * NL + j];
+        }
+    };
     float2 g[NL];
 #pragma unroll
     for (int j = 0; j < NL; ++j) g[j] = make_float2(0.f, 0.f);
 #pragma unroll 4
     for (int r = 0; r < NR; ++r) {
-        const float2 hk = hU[r * NL + k];
+        const float2 hk = hat(r, k);
 #pragma unroll
         for (int j = 0; j < NL; ++j) {
-            const float2 hj = hU[r * NL + j];
+            const float2 hj = hat(r, j);
             g[j].x = fmaf(hk.x, hj.x, fmaf(hk.y, hj.y, g[j].x));
             g[j].y = fmaf(hk.x, hj.y, fmaf(-hk.y, hj.x, g[j].y));
         }
@@ -418,7 +438,7 @@ __global__ void __launch_bounds__(32 * NW) k_lg3(DetectArgs a, const __grid_cons
         float2 sv = make_float2(0.f, 0.f);
 #pragma unroll
         for (int j = 0; j < NL; ++j) {
-            const float2 h = hU[r * NL + j];
+            const float2 h = hat(r, j);
             sv.x = fmaf(gi[j].x, h.x, fmaf(gi[j].y, h.y, sv.x));
             sv.y = fmaf(gi[j].y, h.x, fmaf(-gi[j].x, h.y, sv.y));
         }
@@ -467,7 +487,7 @@ __global__ void __launch_bounds__(32 * NW) k_lg3(DetectArgs a, const __grid_cons
     }
 }
 
-template <int NR, int NL, int QM, int LT, int NW, int PFD>
+template <int NR, int NL, int QM, int LT, int NW, int PFD, int HT = 0>
 cudaError_t launch3(const DetectArgs& a, cudaStream_t s) {
     if (a.n_sc <= 0 || a.n_slots <= 0) return cudaSuccess;
     constexpr int TU = Lg3Smem<NR, NL, NW>::TU;
@@ -482,24 +502,34 @@ cudaError_t launch3(const DetectArgs& a, cudaStream_t s) {
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return cudaErrorInvalidValue;
+    CUtensorMap hmap = ymap;  // unused unless HT
+    if (HT) {
+        const cuuint64_t hdim[3] = {32, (cuuint64_t)a.n_slots * a.n_sc, (cuuint64_t)(NR * NL * 8 / 128)};
+        const cuuint64_t hstride[2] = {(cuuint64_t)NR * NL * 8, 128};
+        const cuuint32_t hbox[3] = {32, (cuuint32_t)TU, (cuuint32_t)(NR * NL * 8 / 128)};
+        if (enc(&hmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float2*>(a.H), hdim, hstride, hbox, estride,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((a.n_sc + TU - 1) / TU, a.n_slots);
     cfg.blockDim = dim3(32 * NW);
-    cfg.dynamicSmemBytes = Lg3Smem<NR, NL, NW>::total;
+    cfg.dynamicSmemBytes = Lg3Smem<NR, NL, NW, HT>::total;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = a.overlap ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, k_lg3<NR, NL, QM, LT, NW, PFD>, a, ymap);
+    return cudaLaunchKernelEx(&cfg, k_lg3<NR, NL, QM, LT, NW, PFD, HT>, a, ymap, hmap);
 }
 
-template <int NR, int NL, int QM, int LT, int NW, int PFD>
+template <int NR, int NL, int QM, int LT, int NW, int PFD, int HT = 0>
 cudaError_t prepare3() {
-    constexpr size_t smem = Lg3Smem<NR, NL, NW>::total;
+    constexpr size_t smem = Lg3Smem<NR, NL, NW, HT>::total;
     if (smem > 48 * 1024)
-        return cudaFuncSetAttribute(k_lg3<NR, NL, QM, LT, NW, PFD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        return cudaFuncSetAttribute(k_lg3<NR, NL, QM, LT, NW, PFD, HT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem);
     return cudaSuccess;
 }
@@ -533,6 +563,8 @@ const KernelEntry kEntries[] = {
     LG3_ENTRY("lg3_16x8_q8_f16", 16, 8, 8, kLlrF16, 2),  // C4 (one TMA tensor box per CTA for y)
     LG_ENTRY("lg_16x8_q8_f16", 16, 8, 8, kLlrF16, 2),
     LG3_ENTRY("lg3_16x8_q8_f16_w1", 16, 8, 8, kLlrF16, 1),
+    KernelEntry{"lg3h_16x8_q8_f16", 16, 8, 8, 1, 14, kLlrF16, 32, 1, launch3<16, 8, 8, kLlrF16, 2, 0, 1>,
+                prepare3<16, 8, 8, kLlrF16, 2, 0, 1>},
     LG3_ENTRY("lg3_16x8_q8_f16_w4", 16, 8, 8, kLlrF16, 4),
     LG_ENTRY("lg_16x8_q8_f32", 16, 8, 8, kLlrF32, 2),
     LG_ENTRY("lg_16x8_q8_i8", 16, 8, 8, kLlrI8, 2),
