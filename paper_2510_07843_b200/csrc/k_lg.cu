@@ -560,11 +560,12 @@ cudaError_t prepare() {
     }
 
 const KernelEntry kEntries[] = {
-    LG3_ENTRY("lg3_16x8_q8_f16", 16, 8, 8, kLlrF16, 2),  // C4 (one TMA tensor box per CTA for y)
-    LG_ENTRY("lg_16x8_q8_f16", 16, 8, 8, kLlrF16, 2),
-    LG3_ENTRY("lg3_16x8_q8_f16_w1", 16, 8, 8, kLlrF16, 1),
+    // C4: y and H of the CTA's 8 units as one TMA tensor box each
     KernelEntry{"lg3h_16x8_q8_f16", 16, 8, 8, 1, 14, kLlrF16, 32, 1, launch3<16, 8, 8, kLlrF16, 2, 0, 1>,
                 prepare3<16, 8, 8, kLlrF16, 2, 0, 1>},
+    LG3_ENTRY("lg3_16x8_q8_f16", 16, 8, 8, kLlrF16, 2),  // y by TMA, H by per-unit bulk copies
+    LG_ENTRY("lg_16x8_q8_f16", 16, 8, 8, kLlrF16, 2),
+    LG3_ENTRY("lg3_16x8_q8_f16_w1", 16, 8, 8, kLlrF16, 1),
     LG3_ENTRY("lg3_16x8_q8_f16_w4", 16, 8, 8, kLlrF16, 4),
     LG_ENTRY("lg_16x8_q8_f32", 16, 8, 8, kLlrF32, 2),
     LG_ENTRY("lg_16x8_q8_i8", 16, 8, 8, kLlrI8, 2),
