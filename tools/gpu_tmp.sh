@@ -1,2 +1,6 @@
-MIMO_FORCE_KERNEL=lg3h_16x8_q8_f16 timeout 300 python -m pytest tests/test_parity_gpu.py -x -q -k "config and 4" 2>&1 | tail -1
-bash tools/bench_variants.sh 4 lg3_16x8_q8_f16 lg3h_16x8_q8_f16 2>&1
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 60 python tools/dbg_time.py big4_64x16_q6_i8 5 2>&1 | tail -4
+timeout 60 python tools/dbg_time.py big6_64x16_q6_i8 5 4 0 2>&1 | tail -4
+timeout 60 python tools/dbg_time.py big6_64x16_q6_i8 5 40 0 2>&1 | tail -4
+timeout 60 python tools/dbg_time.py big6_64x16_q6_i8 5 40 1 2>&1 | tail -4
