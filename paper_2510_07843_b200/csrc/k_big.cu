@@ -5,11 +5,12 @@
 //
 //   k_big_setup (rows a2-a5), one warp per PRB-unit, warp-synchronous, fp32
 //     (reading R18; cond(G) <= ~10 on C5): H by one bulk copy, G = H^H H + s2 I
-//     (half a row per lane, broadcast 128-bit H reads), rows of G gathered by
-//     shuffles, Cholesky with lane k holding row k (pivots and columns by
-//     __shfl_sync; guard R17), X = L^-1 column per lane, row k of G^-1 = X^H X
-//     per lane, W~ = diag(sqrt(norm)/mu) G^-1 H^H (lane (k, half) covers half the
-//     antennas), written to the plan workspace as [unit][r][k] plus slopes.
+//     (half a row per lane, broadcast 128-bit H reads), then G^-1 by in-place
+//     Gauss-Jordan on the same lane layout (ALG = 1, default, reading R26; pivots
+//     and rows by __shfl_sync, guard R17) -- or, ALG = 0, rows gathered to lane k,
+//     Cholesky, X = L^-1 column per lane and row k of G^-1 = X^H X --, then
+//     W~ = diag(sqrt(norm)/mu) G^-1 H^H (lane (k, half) covers half the antennas),
+//     written to the plan workspace as [unit][r][k] plus slopes.
 //   Apply kernels (rows a6-a7), all reading W~ from the workspace:
 //   k_big_apply4 (C5 default): persistent, warp-specialised tcgen05 pipeline
 //     (TMA y chunks, single-thread MMA issue, converter and epilogue warps).
@@ -39,23 +40,23 @@ __device__ __forceinline__ float2 shfl2(float2 v, int src) {
 }
 
 // One warp per PRB-unit (UPB units per CTA), warp-synchronous, no CTA barriers.
-template <int NR, int NL>
+template <int NR, int NL, int ALG = 1>
 struct SetupSmem {
-    // sH [NR][NL] float2 | sX [NL][NL] float2 | sDinv [NL] float | mbarrier
+    // sH [NR][NL] float2 | sX [NL][NL] float2 | sDinv [NL] float (Cholesky route only) | mbarrier
     static constexpr size_t h = 0;
     static constexpr size_t x = (size_t)NR * NL * 8;
-    static constexpr size_t dinv = x + (size_t)NL * NL * 8;
-    static constexpr size_t bar = (dinv + NL * 4 + 7) / 8 * 8;
+    static constexpr size_t dinv = x + (ALG == 0 ? (size_t)NL * NL * 8 : 0);
+    static constexpr size_t bar = (dinv + (ALG == 0 ? NL * 4 : 0) + 7) / 8 * 8;
     static constexpr size_t per_unit = (bar + 8 + 15) / 16 * 16;
 };
 
-template <int NR, int NL, int QM, int UPB>
+template <int NR, int NL, int QM, int UPB, int ALG = 1>
 __global__ void __launch_bounds__(32 * UPB) k_big_setup(DetectArgs a) {
     static_assert(NL == 16 && NR % 32 == 0, "k_big_setup: 16 layers, NR multiple of 32");
     constexpr int WS = BigWs<NR, NL>::stride;
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    using SS = SetupSmem<NR, NL>;
+    using SS = SetupSmem<NR, NL, ALG>;
     unsigned char* base = smem + (size_t)warp * SS::per_unit;
     float2* sH = reinterpret_cast<float2*>(base + SS::h);         // [r][l]
     float2* sX = reinterpret_cast<float2*>(base + SS::x);         // L rows, then X = L^-1 [i][j]
@@ -93,98 +94,167 @@ __global__ void __launch_bounds__(32 * UPB) k_big_setup(DetectArgs a) {
             }
         }
     }
-    // a3: Cholesky, lane k (and its duplicate k+16) holds row k
-    const int k = lane & 15;
-    float2 g[NL];  // row k of G: columns 0-7 from lane 2k, 8-15 from lane 2k+1
+    int k, half;         // W~ lanes: row k of G^-1, antenna half
+    float2 gi[NL];       // row k of G^-1
+    float sinr, fac;
+    bool fail;
+    if constexpr (ALG == 1) {
+        // a3-a4 (reading R26): in-place Gauss-Jordan inversion of G (Hermitian PD: no pivoting),
+        // lane (k, h) = (lane / 2, lane % 2) keeps G[k][8h .. 8h+7] from the Gram. Step j: pivot
+        // p_j = G[j][j] (the LDL^H pivot = square of Cholesky's d_jj, guard R17), row j scaled by
+        // 1/p_j and broadcast by shuffles, every other row k updated with f = G[k][j].
+        k = lane >> 1;
+        half = lane & 1;
+        const int h = half;
+        float gd = 0.f;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-        g[q] = shfl2(gq[q], 2 * k);
-        g[8 + q] = shfl2(gq[q], 2 * k + 1);
-    }
+        for (int q = 0; q < 8; ++q)
+            if (8 * h + q == k) {
+                gq[q] = make_float2(gq[q].x + s2, 0.f);
+                gd = gq[q].x;
+            }
+        float gmax = gd;
 #pragma unroll
-    for (int j = 0; j < NL; ++j)
-        if (j == k) g[j] = make_float2(g[j].x + s2, 0.f);
-    float gmax = 0.f;
+        for (int off = 1; off < 32; off <<= 1) gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, off));
+        fail = !(gmax == gmax);
+        const float tau = (float)kPivotTau * gmax;
 #pragma unroll
-    for (int j = 0; j < NL; ++j)
-        if (j == k) gmax = g[j].x;
+        for (int j = 0; j < NL; ++j) {
+            const int hj = j >> 3, qj = j & 7;
+            const float2 f = shfl2(gq[qj], (lane & ~1) | hj);    // G[k][j]
+            float p = __shfl_sync(0xffffffffu, gq[qj].x, 2 * j + hj);  // G[j][j]
+            if (!(p > tau)) {
+                fail = true;
+                p = 1.f;
+            }
+            const float pinv = 1.f / p;
+            const bool prow = k == j;
 #pragma unroll
-    for (int off = 1; off < NL; off <<= 1) gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, off));
-    bool fail = !(gmax == gmax);
-    float my_dinv = 0.f;
-#pragma unroll
-    for (int j = 0; j < NL; ++j) {
-        float p = __shfl_sync(0xffffffffu, g[j].x, j);
-        if (!(p > (float)kPivotTau * gmax)) {
-            fail = true;
-            p = 1.f;
-        }
-        const float dinv = rsqrtf(p);
-        if (k == j) my_dinv = dinv;
-        if (k > j) g[j] = make_float2(g[j].x * dinv, g[j].y * dinv);
-#pragma unroll
-        for (int m = j + 1; m < NL; ++m) {
-            const float2 lmj = shfl2(g[j], m);
-            if (k >= m) {
-                g[m].x = fmaf(-g[j].x, lmj.x, fmaf(-g[j].y, lmj.y, g[m].x));
-                g[m].y = fmaf(-g[j].y, lmj.x, fmaf(g[j].x, lmj.y, g[m].y));
+            for (int q = 0; q < 8; ++q) {
+                float2 rj = shfl2(gq[q], 2 * j + h);                 // G[j][8h+q]
+                if (8 * h + q == j) rj = make_float2(1.f, 0.f);
+                rj = make_float2(rj.x * pinv, rj.y * pinv);
+                float2 b = (8 * h + q == j) ? make_float2(0.f, 0.f) : gq[q];
+                b.x = fmaf(-f.x, rj.x, fmaf(f.y, rj.y, b.x));
+                b.y = fmaf(-f.x, rj.y, fmaf(-f.y, rj.x, b.y));
+                gq[q] = prow ? rj : b;
             }
         }
-    }
-    if (lane < NL) {
+        // row k of G^-1: own half + the partner lane's half
+        float A = 0.f;
 #pragma unroll
-        for (int j = 0; j < NL; ++j) sX[k * NL + j] = (j < k) ? g[j] : make_float2(0.f, 0.f);
-        sDinv[k] = my_dinv;
-    }
-    __syncwarp();
-    // a4: X = L^-1, column k per lane (lanes 16..31 duplicate)
-    float2 x[NL];
-#pragma unroll
-    for (int i = 0; i < NL; ++i) {
-        float2 sv = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int m = 0; m < i; ++m) sv = cmac(sv, sX[i * NL + m], x[m]);
-        const float di = sDinv[i];
-        x[i] = (i == k) ? make_float2(di, 0.f) : (i < k ? make_float2(0.f, 0.f) : make_float2(-sv.x * di, -sv.y * di));
-    }
-    __syncwarp();
-    if (lane < NL) {
-#pragma unroll
-        for (int i = 0; i < NL; ++i) sX[i * NL + k] = x[i];
-    }
-    __syncwarp();
-    // row k of G^-1 = X^H X (lane k; x = column k of X), A_kk
-    float2 gi[NL];
-#pragma unroll
-    for (int j = 0; j < NL; ++j) {
-        float2 sv = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int m = j; m < NL; ++m) {
-            const float2 xm = x[m], xmj = sX[m * NL + j];
-            sv.x = fmaf(xm.x, xmj.x, fmaf(xm.y, xmj.y, sv.x));
-            sv.y = fmaf(xm.x, xmj.y, fmaf(-xm.y, xmj.x, sv.y));
+        for (int q = 0; q < 8; ++q) {
+            const float2 o = shfl2(gq[q], lane ^ 1);
+            gi[q] = h ? o : gq[q];
+            gi[8 + q] = h ? gq[q] : o;
         }
-        gi[j] = sv;
-    }
-    float A = 0.f;
 #pragma unroll
-    for (int j = 0; j < NL; ++j)
-        if (j == k) A = gi[j].x;
-    const float mu = fmaf(-s2, A, 1.f);
-    float sinr, fac;
-    if (s2 == 0.f) {
-        sinr = __int_as_float(0x7f800000);
-        fac = sqrtf(norm);
+        for (int j = 0; j < NL; ++j)
+            if (j == k) A = gi[j].x;
+        const float mu = fmaf(-s2, A, 1.f);
+        if (s2 == 0.f) {
+            sinr = __int_as_float(0x7f800000);
+            fac = sqrtf(norm);
+        } else {
+            sinr = __fdividef(mu, s2 * A);
+            fac = __fdividef(sqrtf(norm), mu);
+        }
+        if (!(mu > 0.f) || fail) {
+            sinr = 0.f;
+            fac = 0.f;
+        }
     } else {
-        sinr = __fdividef(mu, s2 * A);
-        fac = __fdividef(sqrtf(norm), mu);
-    }
-    if (!(mu > 0.f) || fail) {
-        sinr = 0.f;
-        fac = 0.f;
+        // a3: Cholesky, lane k (and its duplicate k+16) holds row k
+        k = lane & 15;
+        half = lane >> 4;
+        float2 g[NL];  // row k of G: columns 0-7 from lane 2k, 8-15 from lane 2k+1
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            g[q] = shfl2(gq[q], 2 * k);
+            g[8 + q] = shfl2(gq[q], 2 * k + 1);
+        }
+#pragma unroll
+        for (int j = 0; j < NL; ++j)
+            if (j == k) g[j] = make_float2(g[j].x + s2, 0.f);
+        float gmax = 0.f;
+#pragma unroll
+        for (int j = 0; j < NL; ++j)
+            if (j == k) gmax = g[j].x;
+#pragma unroll
+        for (int off = 1; off < NL; off <<= 1) gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, off));
+        fail = !(gmax == gmax);
+        float my_dinv = 0.f;
+#pragma unroll
+        for (int j = 0; j < NL; ++j) {
+            float p = __shfl_sync(0xffffffffu, g[j].x, j);
+            if (!(p > (float)kPivotTau * gmax)) {
+                fail = true;
+                p = 1.f;
+            }
+            const float dinv = rsqrtf(p);
+            if (k == j) my_dinv = dinv;
+            if (k > j) g[j] = make_float2(g[j].x * dinv, g[j].y * dinv);
+#pragma unroll
+            for (int m = j + 1; m < NL; ++m) {
+                const float2 lmj = shfl2(g[j], m);
+                if (k >= m) {
+                    g[m].x = fmaf(-g[j].x, lmj.x, fmaf(-g[j].y, lmj.y, g[m].x));
+                    g[m].y = fmaf(-g[j].y, lmj.x, fmaf(g[j].x, lmj.y, g[m].y));
+                }
+            }
+        }
+        if (lane < NL) {
+#pragma unroll
+            for (int j = 0; j < NL; ++j) sX[k * NL + j] = (j < k) ? g[j] : make_float2(0.f, 0.f);
+            sDinv[k] = my_dinv;
+        }
+        __syncwarp();
+        // a4: X = L^-1, column k per lane (lanes 16..31 duplicate)
+        float2 x[NL];
+#pragma unroll
+        for (int i = 0; i < NL; ++i) {
+            float2 sv = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int m = 0; m < i; ++m) sv = cmac(sv, sX[i * NL + m], x[m]);
+            const float di = sDinv[i];
+            x[i] = (i == k) ? make_float2(di, 0.f) : (i < k ? make_float2(0.f, 0.f) : make_float2(-sv.x * di, -sv.y * di));
+        }
+        __syncwarp();
+        if (lane < NL) {
+#pragma unroll
+            for (int i = 0; i < NL; ++i) sX[i * NL + k] = x[i];
+        }
+        __syncwarp();
+        // row k of G^-1 = X^H X (lane k; x = column k of X), A_kk
+#pragma unroll
+        for (int j = 0; j < NL; ++j) {
+            float2 sv = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int m = j; m < NL; ++m) {
+                const float2 xm = x[m], xmj = sX[m * NL + j];
+                sv.x = fmaf(xm.x, xmj.x, fmaf(xm.y, xmj.y, sv.x));
+                sv.y = fmaf(xm.x, xmj.y, fmaf(-xm.y, xmj.x, sv.y));
+            }
+            gi[j] = sv;
+        }
+        float A = 0.f;
+#pragma unroll
+        for (int j = 0; j < NL; ++j)
+            if (j == k) A = gi[j].x;
+        const float mu = fmaf(-s2, A, 1.f);
+        if (s2 == 0.f) {
+            sinr = __int_as_float(0x7f800000);
+            fac = sqrtf(norm);
+        } else {
+            sinr = __fdividef(mu, s2 * A);
+            fac = __fdividef(sqrtf(norm), mu);
+        }
+        if (!(mu > 0.f) || fail) {
+            sinr = 0.f;
+            fac = 0.f;
+        }
     }
     // W~[r][k] = fac_k sum_j G^-1_kj conj(H_rj): lane (k, half) covers r in [half*NR/2, (half+1)*NR/2)
-    const int half = lane >> 4;
     pdl_wait();  // the previous call may still read the workspace
     if (valid) {
         float2* ws = reinterpret_cast<float2*>(reinterpret_cast<float*>(a.ws) + u * WS);
@@ -204,7 +274,7 @@ __global__ void __launch_bounds__(32 * UPB) k_big_setup(DetectArgs a) {
             }
             ws[r * NL + k] = fac > 0.f ? make_float2(sv.x * fac, sv.y * fac) : make_float2(0.f, 0.f);
         }
-        if (lane < NL) {
+        if (half == 0) {
             reinterpret_cast<float*>(ws)[NR * NL * 2 + k] = sinr / norm * a.llr_scale;
             if (a.sinr) a.sinr[u * NL + k] = sinr;
         }
@@ -1158,7 +1228,7 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
     if (warp == CW) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
 }
 
-template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_, int ABL = 0, int TR = 0>
+template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_, int ABL = 0, int TR = 0, int SALG = 1>
 cudaError_t launch_ap4(const DetectArgs& a, cudaStream_t s) {
     if (a.n_units <= 0) return cudaSuccess;
     static int n_sm = 0;
@@ -1179,8 +1249,8 @@ cudaError_t launch_ap4(const DetectArgs& a, cudaStream_t s) {
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return cudaErrorInvalidValue;
     constexpr int UPB = 4;
-    cudaError_t e = launch_kernel(k_big_setup<NR, NL, QM, UPB>, dim3((unsigned)((a.n_units + UPB - 1) / UPB)),
-                                  dim3(32 * UPB), UPB * SetupSmem<NR, NL>::per_unit, s, a.overlap, a);
+    cudaError_t e = launch_kernel(k_big_setup<NR, NL, QM, UPB, SALG>, dim3((unsigned)((a.n_units + UPB - 1) / UPB)),
+                                  dim3(32 * UPB), UPB * SetupSmem<NR, NL, SALG>::per_unit, s, a.overlap, a);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(a.n_units < n_sm ? a.n_units : n_sm));
@@ -1195,10 +1265,10 @@ cudaError_t launch_ap4(const DetectArgs& a, cudaStream_t s) {
     return cudaLaunchKernelEx(&cfg, k_big_apply4<NR, NL, QM, LT, EW, S_, NLO_, ABL, TR>, a, ymap);
 }
 
-template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_, int ABL = 0, int TR = 0>
+template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_, int ABL = 0, int TR = 0, int SALG = 1>
 cudaError_t prepare_ap4() {
-    cudaError_t e = cudaFuncSetAttribute(k_big_setup<NR, NL, QM, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)(4 * SetupSmem<NR, NL>::per_unit));
+    cudaError_t e = cudaFuncSetAttribute(k_big_setup<NR, NL, QM, 4, SALG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)(4 * SetupSmem<NR, NL, SALG>::per_unit));
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(k_big_apply4<NR, NL, QM, LT, EW, S_, NLO_, ABL, TR>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ap4<S_, NLO_, TR>::total);
@@ -1246,6 +1316,9 @@ const KernelEntry kEntries[] = {
     }
     BIG4_ENTRY("big4_64x16_q6_i8", 4, 4, 2),  // C5 default: tcgen05 3-pass TF32 apply (fastest)
     BIG4_ENTRY("big4e8_64x16_q6_i8", 8, 4, 2),
+    // big4 with the Cholesky / L^-1 / X^H X setup route instead of Gauss-Jordan (reading R26)
+    KernelEntry{"big4c_64x16_q6_i8", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 0, 0, 0>,
+                prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 0, 0, 0>, workspace<64, 16>},
     KernelEntry{"big5_64x16_q6_i8", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 0, 1>,
                 prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 0, 1>, workspace<64, 16>},
     KernelEntry{"ablation_big5_none", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 3, 1>,
