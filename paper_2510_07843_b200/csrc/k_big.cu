@@ -410,6 +410,23 @@ __device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t da, uint64_t
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(da), "l"(db), "r"(idesc), "r"(acc));
 }
+// A operand in TMEM (lane = row m, one 32-bit column per K element), B by smem descriptor.
+__device__ __forceinline__ void umma_tf32_ta(uint32_t d_tmem, uint32_t a_tmem, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+        "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+        "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]), "f"(v[9]),
+        "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]), "f"(v[17]), "f"(v[18]),
+        "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]), "f"(v[25]), "f"(v[26]), "f"(v[27]),
+        "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+        : "memory");
+}
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
@@ -855,16 +872,16 @@ cudaError_t prepare_ap3() {
 //                  x~ -> exact max-log demap -> LLR stores.
 // Chunk g = 4 i + c of the CTA's i-th unit (u = blockIdx.x + i gridDim.x).
 // mbarrier k-th completion is waited with parity k & 1.
-template <int S_, int NLO_, int TR_ = 0>
+template <int S_, int NLO_, int TR_ = 0, int TRW_ = 96, int TA_ = 0>
 struct Ap4 {
     static constexpr int S = S_;                             // y stages
-    static constexpr int TRW = 96;                           // TR: transpose-buffer width (REs)
+    static constexpr int TRW = TRW_;                         // TR: transpose-buffer width (REs)
     static constexpr int TRS = TRW + 4;                      // TR: floats per accumulator row in the stage (pad: banks)
     static constexpr int NLO = NLO_;                         // y_lo buffers
     static constexpr size_t chunk = (size_t)kRe * 128;       // 21504 = 21 x 1024
     static constexpr size_t y0 = 0;
     static constexpr size_t ylo = S * chunk;
-    static constexpr size_t B = ylo + NLO * chunk;           // 2 x 32 KiB (1024-aligned)
+    static constexpr size_t B = ylo + (TA_ ? 0 : NLO * chunk);  // 2 x 32 KiB (1024-aligned)
     static constexpr size_t bset = 4 * 64 * 128;
     static constexpr size_t slope = B + 2 * bset;            // [4][16] float (unit i -> slot i & 3)
     static constexpr size_t tb = slope + 256;                // TR: [TRW][TRS] float
@@ -880,13 +897,27 @@ struct Ap4 {
 // with the W~ set as the M = 64 A operand and the unit's 168 y rows as one N = 168 B operand:
 // 4 + 4 tcgen05.mma per chunk instead of 16 (two M = 128 tiles x hi|lo and lo passes), no
 // duplicated rows. The M = 64 accumulator puts row m in TMEM lane (m % 16) + 32 (m / 16),
-// column n = RE, so the epilogue transposes through shared memory (96 REs at a time).
-template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_, int ABL, int TR>
+// column n = RE, so the epilogue transposes through shared memory (96 REs at a time; with
+// EW = 8 all 168 at once, two warps per TMEM lane quadrant).
+// TA = 1 ("big8"): the A operand (y rows, hi and lo) lives in TMEM instead of shared memory.
+// The converter warps read each y row once from the TMA stage (warp w serves TMEM lane quadrant
+// w: rows 32w + lane of tile 0 and 40 + 32w + lane of tile 1; a compact tile 1 -- REs 128-167
+// in lanes 0-39 only -- measured slower, 383 vs 352 us: it piles converter and epilogue work on
+// the same two SM sub-partitions), store it raw (the tensor core reads
+// its TF32 truncation = y_hi) and as y_lo = y - trunc(y) with tcgen05.st, so the MMAs read only
+// the small W~ operand from shared memory; the TMA stage is released as soon as it is read.
+// TMEM: columns 0-255 accumulators (2 x 128), 256-511 the A ring (NLO = 2 chunks x 2 tiles x hi|lo
+// x 32 columns). Measured per step (C5): 352 us against big4's 402 us. Not better: a hybrid that keeps
+// the y_hi pass in shared memory (only y_lo in TMEM, 4-deep ring) 372 us; three N = 32 passes into
+// one 32-column accumulator (3-deep ring) 430 us -- an A-in-TMEM tf32 MMA costs ~81 cycles against
+// ~50 for an SS one (tools/tcbench.cu), so the MMA count matters more than the ring depth.
+template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_, int ABL, int TR, int TA = 0>
 __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, const __grid_constant__ CUtensorMap ymap) {
-    using A4 = Ap4<S_, NLO_, TR>;
-    static_assert(!TR || EW == 4, "transposed epilogue uses 4 warps");
-    constexpr uint32_t kTmemCols = TR ? 512u : 256u;
+    using A4 = Ap4<S_, NLO_, TR, (TR && EW == 8) ? kRe : 96, TA>;
+    static_assert(!TA || (!TR && NLO_ == 2), "TA: untransposed, two A buffers");
+    constexpr uint32_t kTmemCols = (TR || TA) ? 512u : 256u;
     constexpr uint32_t kAccStride = TR ? 256u : 128u;
+    constexpr uint32_t kAring = 256u;  // TA: first TMEM column of the A ring
     constexpr int CW = 4 + EW;  // control warp (MMA issuer); CW + 1: TMA producer
     constexpr int NLO = NLO_;
     static_assert(NL == 16 && NR == 64, "k_big_apply4: 64 x 16");
@@ -915,7 +946,7 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
     if (t == 0) {
         for (int i = 0; i < S; ++i) {
             mbar_init(&yfull[i], 1);
-            mbar_init(&yfree[i], 2);
+            mbar_init(&yfree[i], TA ? 1 : 2);
         }
         for (int i = 0; i < NLO; ++i) {
             mbar_init(&ylofull[i], 1);
@@ -974,6 +1005,26 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
                 for (int c = 0; c < 4; ++c) {
                     const long long gg = 4 * i + c;
                     const int st = (int)(gg % S), lb = (int)(gg % NLO);
+                    if constexpr (TA) {
+                        const uint32_t ab = tmem + kAring + 128u * (uint32_t)lb;  // A ring buffer lb
+                        mbar_wait(&ylofull[lb], (uint32_t)((gg / NLO) & 1));
+                        tc_fence_after();
+#pragma unroll
+                        for (int tile = 0; tile < 2; ++tile)
+#pragma unroll
+                            for (int ks = 0; ks < 4; ++ks)
+                                umma_tf32_ta(acc + 64u * tile, ab + 64u * tile + 8u * ks,
+                                             umma_desc_sw128(bb + (uint32_t)c * 8192u + ks * 32u), id64, (c | ks) ? 1u : 0u);
+#pragma unroll
+                        for (int tile = 0; tile < (ABL & 4 ? 0 : 2); ++tile)
+#pragma unroll
+                            for (int ks = 0; ks < 4; ++ks)
+                                umma_tf32_ta(acc + 64u * tile, ab + 64u * tile + 32u + 8u * ks,
+                                             umma_desc_sw128(bb + (uint32_t)c * 8192u + ks * 32u), id32, 1u);
+                        umma_commit(&ylofree[lb]);
+                        if (c == 3) umma_commit(&accfull[b]);
+                        continue;
+                    }
                     const uint32_t ys = base + (uint32_t)(A4::y0 + st * A4::chunk);
                     mbar_wait(&yfull[st], (uint32_t)((gg / S) & 1));
                     tc_fence_after();
@@ -1063,6 +1114,38 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
                 const int st = (int)(gg % S), lb = (int)(gg % NLO);
                 mbar_wait(&yfull[st], (uint32_t)((gg / S) & 1));
                 if (gg >= NLO) mbar_wait(&ylofree[lb], (uint32_t)(((gg / NLO) + 1) & 1));
+                if constexpr (TA) {
+                    // tile 0: REs 32 w + lane; tile 1: REs 40 + 32 w + lane -> TMEM lane quadrant w
+                    tc_fence_after();
+                    const unsigned char* ysm = g + A4::y0 + st * A4::chunk;
+#pragma unroll
+                    for (int tile = 0; tile < 2; ++tile) {
+                        const int r = (tile ? 40 : 0) + 32 * warp + lane;
+                        const float4* row = reinterpret_cast<const float4*>(ysm + (size_t)r * 128);
+                        float v[32], lo[32];
+#pragma unroll
+                        for (int cc = 0; cc < 8; ++cc) {
+                            const float4 q = row[cc ^ (r & 7)];  // SWIZZLE_128B: 16-byte chunk cc of row r
+                            v[4 * cc] = q.x;
+                            v[4 * cc + 1] = q.y;
+                            v[4 * cc + 2] = q.z;
+                            v[4 * cc + 3] = q.w;
+                        }
+#pragma unroll
+                        for (int k = 0; k < 32; ++k) lo[k] = v[k] - tf32_trunc(v[k]);
+                        const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16) + kAring + 128u * (uint32_t)lb + 64u * tile;
+                        tmem_st32(ta, v);
+                        tmem_st32(ta + 32u, lo);
+                    }
+                    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+                    tc_fence_before();
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (tc == 0) {
+                        mbar_arrive(&ylofull[lb]);
+                        mbar_arrive(&yfree[st]);
+                    }
+                    continue;
+                }
                 const float4* src = reinterpret_cast<const float4*>(g + A4::y0 + st * A4::chunk);
                 float4* dst = reinterpret_cast<float4*>(g + A4::ylo + lb * A4::chunk);
                 constexpr int n4 = (int)(A4::chunk / 16);
@@ -1104,14 +1187,17 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
             tc_fence_after();
             if constexpr (TR) {
                 // rows 16q..16q+15 of quadrant q = (Re hi | Im hi | Re lo | Im lo) x 16 layers, column = RE
+                // (EW = 8: the two warps of a quadrant take alternate 32-column blocks, and TRW = 168
+                // so one pass covers the unit with one RE per epilogue thread)
                 float* T = reinterpret_cast<float*>(g + A4::tb);
                 const int tid = t - 128;
                 const uint32_t tq = tmem + ((uint32_t)(32 * we) << 16) + kAccStride * (uint32_t)b;
+                constexpr int NPASS = (kRe + A4::TRW - 1) / A4::TRW;
 #pragma unroll 1
-                for (int p = 0; p < 2; ++p) {
-                    const int n0 = p * A4::TRW, wcol = p ? kRe - A4::TRW : A4::TRW;
+                for (int p = 0; p < NPASS; ++p) {
+                    const int n0 = p * A4::TRW, wcol = (kRe - n0 < A4::TRW) ? kRe - n0 : A4::TRW;
 #pragma unroll 1
-                    for (int c0 = 0; c0 < wcol; c0 += 32) {
+                    for (int c0 = 32 * h; c0 < wcol; c0 += 32 * (EW / 4)) {
                         uint32_t v[32];
                         if (wcol - c0 >= 32) {
                             tmem_ld32(tq + (uint32_t)(n0 + c0), v);
@@ -1130,7 +1216,7 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
                                                     __uint_as_float(v[4 * j4 + 2]), __uint_as_float(v[4 * j4 + 3]));
                         }
                     }
-                    asm volatile("bar.sync 2, 128;" ::: "memory");
+                    asm volatile("bar.sync 2, %0;" ::"r"(32 * EW) : "memory");
                     if (tid < wcol) {
                         const int row = n0 + tid;
                         const int s = row / kSc, f = row % kSc;
@@ -1161,7 +1247,7 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
                             for (int k = 0; k < NL; ++k) a.xhat[re * NL + k] = make_float2(x[k].x * ia, x[k].y * ia);
                         }
                     }
-                    asm volatile("bar.sync 2, 128;" ::: "memory");
+                    asm volatile("bar.sync 2, %0;" ::"r"(32 * EW) : "memory");
                 }
             }
 #pragma unroll 1
@@ -1228,7 +1314,7 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
     if (warp == CW) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
 }
 
-template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_, int ABL = 0, int TR = 0, int SALG = 1>
+template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_, int ABL = 0, int TR = 0, int SALG = 1, int TA = 0>
 cudaError_t launch_ap4(const DetectArgs& a, cudaStream_t s) {
     if (a.n_units <= 0) return cudaSuccess;
     static int n_sm = 0;
@@ -1255,23 +1341,24 @@ cudaError_t launch_ap4(const DetectArgs& a, cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(a.n_units < n_sm ? a.n_units : n_sm));
     cfg.blockDim = dim3(32 * (6 + EW));
-    cfg.dynamicSmemBytes = Ap4<S_, NLO_, TR>::total;
+    cfg.dynamicSmemBytes = Ap4<S_, NLO_, TR, (TR && EW == 8) ? kRe : 96, TA>::total;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = a.overlap ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, k_big_apply4<NR, NL, QM, LT, EW, S_, NLO_, ABL, TR>, a, ymap);
+    return cudaLaunchKernelEx(&cfg, k_big_apply4<NR, NL, QM, LT, EW, S_, NLO_, ABL, TR, TA>, a, ymap);
 }
 
-template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_, int ABL = 0, int TR = 0, int SALG = 1>
+template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_, int ABL = 0, int TR = 0, int SALG = 1, int TA = 0>
 cudaError_t prepare_ap4() {
     cudaError_t e = cudaFuncSetAttribute(k_big_setup<NR, NL, QM, 4, SALG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(4 * SetupSmem<NR, NL, SALG>::per_unit));
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_big_apply4<NR, NL, QM, LT, EW, S_, NLO_, ABL, TR>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Ap4<S_, NLO_, TR>::total);
+    return cudaFuncSetAttribute(k_big_apply4<NR, NL, QM, LT, EW, S_, NLO_, ABL, TR, TA>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)Ap4<S_, NLO_, TR, (TR && EW == 8) ? kRe : 96, TA>::total);
 }
 
 template <int NR, int NL>
@@ -1314,13 +1401,22 @@ const KernelEntry kEntries[] = {
         NAME, 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, EW, S, NLO>,                \
             prepare_ap4<64, 16, 6, kLlrI8, EW, S, NLO>, workspace<64, 16>                                  \
     }
-    BIG4_ENTRY("big4_64x16_q6_i8", 4, 4, 2),  // C5 default: tcgen05 3-pass TF32 apply (fastest)
+    // C5 default: big4's tcgen05 3-pass TF32 pipeline with the y operand (hi, lo) in TMEM (fastest)
+    KernelEntry{"big8_64x16_q6_i8", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 0, 0, 1, 1>,
+                prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 0, 0, 1, 1>, workspace<64, 16>},
+    BIG4_ENTRY("big4_64x16_q6_i8", 4, 4, 2),  // y_lo through a shared-memory ring
     BIG4_ENTRY("big4e8_64x16_q6_i8", 8, 4, 2),
     // big4 with the Cholesky / L^-1 / X^H X setup route instead of Gauss-Jordan (reading R26)
     KernelEntry{"big4c_64x16_q6_i8", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 0, 0, 0>,
                 prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 0, 0, 0>, workspace<64, 16>},
     KernelEntry{"big5_64x16_q6_i8", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 0, 1>,
                 prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 0, 1>, workspace<64, 16>},
+    KernelEntry{"ablation_big8_noepi", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 2, 0, 1, 1>,
+                prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 2, 0, 1, 1>, workspace<64, 16>},
+    KernelEntry{"ablation_big8_mma1", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 4, 0, 1, 1>,
+                prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 4, 0, 1, 1>, workspace<64, 16>},
+    KernelEntry{"big5e8_64x16_q6_i8", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 8, 3, 2, 0, 1>,
+                prepare_ap4<64, 16, 6, kLlrI8, 8, 3, 2, 0, 1>, workspace<64, 16>},
     KernelEntry{"ablation_big5_none", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 3, 1>,
                 prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 3, 1>, workspace<64, 16>},
     // timing ablations (results are wrong on purpose; only reachable through MIMO_FORCE_KERNEL)
