@@ -32,7 +32,7 @@ constexpr int kRe = kSym * kSc;  // 168 REs per PRB-unit
 template <int NR, int NL>
 struct BigWs {
     static constexpr int w_floats = NR * NL * 2;                 // W~ [r][k] float2
-    static constexpr int stride = (w_floats + NL + 31) / 32 * 32; // floats per unit (128-byte multiple)
+    static constexpr int stride = (w_floats + NL + 3 + 31) / 32 * 32; // + slopes, 3 fp16-apply scales (128-B multiple)
 };
 
 __device__ __forceinline__ float2 shfl2(float2 v, int src) {
@@ -93,6 +93,17 @@ __global__ void __launch_bounds__(32 * UPB) k_big_setup(DetectArgs a) {
                 gq[2 * q2 + 1] = cmac_p(gq[2 * q2 + 1], hi, make_float2(v.z, v.w));
             }
         }
+    }
+    // ||H||_F^2 = trace(H^H H): the mean receive power per antenna is ||H||^2 / NR + s2 (unit-power
+    // symbols); the fp16 apply (big11) scales y by a power of two derived from it
+    float trH = 0.f;
+    {
+        const int i = lane >> 1, h = lane & 1;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            if (8 * h + q == i) trH = gq[q].x;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) trH += __shfl_xor_sync(0xffffffffu, trH, off);
     }
     int k, half;         // W~ lanes: row k of G^-1, antenna half
     float2 gi[NL];       // row k of G^-1
@@ -258,6 +269,7 @@ __global__ void __launch_bounds__(32 * UPB) k_big_setup(DetectArgs a) {
     pdl_wait();  // the previous call may still read the workspace
     if (valid) {
         float2* ws = reinterpret_cast<float2*>(reinterpret_cast<float*>(a.ws) + u * WS);
+        float wmax = 0.f;
         CPackC gp[NL];  // packed FFMA2: sv += G^-1_kj conj(H_rj)
 #pragma unroll
         for (int j = 0; j < NL; ++j) gp[j] = cpackc(gi[j]);
@@ -272,11 +284,25 @@ __global__ void __launch_bounds__(32 * UPB) k_big_setup(DetectArgs a) {
                 sv = cmacc_p(sv, gp[2 * j2], make_float2(v.x, v.y));
                 sv = cmacc_p(sv, gp[2 * j2 + 1], make_float2(v.z, v.w));
             }
-            ws[r * NL + k] = fac > 0.f ? make_float2(sv.x * fac, sv.y * fac) : make_float2(0.f, 0.f);
+            const float2 w = fac > 0.f ? make_float2(sv.x * fac, sv.y * fac) : make_float2(0.f, 0.f);
+            ws[r * NL + k] = w;
+            wmax = fmaxf(wmax, fmaxf(fabsf(w.x), fabsf(w.y)));
         }
         if (half == 0) {
             reinterpret_cast<float*>(ws)[NR * NL * 2 + k] = sinr / norm * a.llr_scale;
             if (a.sinr) a.sinr[u * NL + k] = sinr;
+        }
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) wmax = fmaxf(wmax, __shfl_xor_sync(0xffffffffu, wmax, off));
+        if (lane == 0) {  // reading R27: sy = 2^-ey, sw = 2^-ew bring y and W~ to O(1); inv = 2^(ey + ew)
+            const float py = sqrtf(trH / (float)NR + s2);
+            int ey = 0, ew = 0;
+            if (py > 0.f && py < 3.0e38f) frexpf(py, &ey);
+            if (wmax > 0.f && wmax < 3.0e38f) frexpf(wmax, &ew);
+            float* sc = reinterpret_cast<float*>(ws) + NR * NL * 2 + NL;
+            sc[0] = ldexpf(1.f, -ey);
+            sc[1] = ldexpf(1.f, -ew);
+            sc[2] = ldexpf(1.f, ey + ew);
         }
         if (lane == 0 && fail) atomicAdd(a.fail_count, 1ull);
     }
@@ -416,6 +442,21 @@ __device__ __forceinline__ void umma_tf32_ta(uint32_t d_tmem, uint32_t a_tmem, u
         "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
         "r"(a_tmem), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void umma_f16_ta(uint32_t d_tmem, uint32_t a_tmem, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(db), "r"(idesc), "r"(acc));
+}
+// fp16 hi/lo split of a pair (reading R27): hi = rn(a), lo = rn(a - hi); packed as one 32-bit word
+// (low half = the even K element).
+__device__ __forceinline__ void split_h2(float a0, float a1, uint32_t& hi, uint32_t& lo) {
+    const __half2 h = __floats2half2_rn(a0, a1);
+    const float2 f = __half22float2(h);
+    const __half2 l = __floats2half2_rn(a0 - f.x, a1 - f.y);
+    hi = *reinterpret_cast<const uint32_t*>(&h);
+    lo = *reinterpret_cast<const uint32_t*>(&l);
 }
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
     asm volatile(
@@ -884,7 +925,7 @@ struct Ap4 {
     static constexpr size_t B = ylo + (TA_ ? 0 : NLO * chunk);  // 2 x 32 KiB (1024-aligned)
     static constexpr size_t bset = 4 * 64 * 128;
     static constexpr size_t slope = B + 2 * bset;            // [4][16] float (unit i -> slot i & 3)
-    static constexpr size_t tb = slope + 256;                // TR: [TRW][TRS] float
+    static constexpr size_t tb = slope + 512;                // TR: [TRW][TRS] float (slope area: [4][16] + [4] inv)
     static constexpr size_t bars = tb + (TR_ ? (size_t)64 * TRS * 4 : 0);  // mbarriers
     static constexpr int NBAR = 2 * S + 2 * NLO + 2 * 3;     // yfull, yfree | ylofull, ylofree | bready, accfull, tfree
     static constexpr size_t tslot = bars + NBAR * 8;
@@ -1005,6 +1046,26 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
                 for (int c = 0; c < 4; ++c) {
                     const long long gg = 4 * i + c;
                     const int st = (int)(gg % S), lb = (int)(gg % NLO);
+                    if constexpr (TA == 2) {  // fp16 hi/lo (R27): 2 K-steps of 16 per chunk, 8 MMAs
+                        constexpr uint32_t h64 = (1u << 4) | ((64u >> 3) << 17) | ((128u >> 4) << 24);
+                        constexpr uint32_t h32 = (1u << 4) | ((32u >> 3) << 17) | ((128u >> 4) << 24);
+                        const uint32_t ab = tmem + kAring + 64u * (uint32_t)lb;  // A ring buffer lb
+                        mbar_wait(&ylofull[lb], (uint32_t)((gg / NLO) & 1));
+                        tc_fence_after();
+                        const uint32_t wb = bb + (uint32_t)(c >> 1) * 8192u + (uint32_t)(c & 1) * 64u;
+#pragma unroll
+                        for (int tile = 0; tile < 2; ++tile)
+#pragma unroll
+                            for (int ks = 0; ks < 2; ++ks) {
+                                umma_f16_ta(acc + 64u * tile, ab + 32u * tile + 8u * ks, umma_desc_sw128(wb + ks * 32u),
+                                            h64, (c | ks) ? 1u : 0u);
+                                umma_f16_ta(acc + 64u * tile, ab + 32u * tile + 16u + 8u * ks,
+                                            umma_desc_sw128(wb + ks * 32u), h32, 1u);
+                            }
+                        umma_commit(&ylofree[lb]);
+                        if (c == 3) umma_commit(&accfull[b]);
+                        continue;
+                    }
                     if constexpr (TA) {
                         const uint32_t ab = tmem + kAring + 128u * (uint32_t)lb;  // A ring buffer lb
                         mbar_wait(&ylofull[lb], (uint32_t)((gg / NLO) & 1));
@@ -1074,6 +1135,7 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
         pdl_wait();  // W~ of this call's setup kernel is complete and visible
         float2 wv[16];
         float slv = 0.f;
+        float3 scl = make_float3(1.f, 1.f, 1.f);  // TA 2: (sy, sw, inv) of the prefetched unit
         auto fetch = [&](long long i) {
             const float2* src = reinterpret_cast<const float2*>(reinterpret_cast<const float*>(a.ws) + (u0 + i * du) * WS);
 #pragma unroll
@@ -1083,6 +1145,10 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
                 wv[2 * c + 1] = src[(r0 + 1) * NL + kk];
             }
             if (tc < NL) slv = reinterpret_cast<const float*>(src + NR * NL)[tc];
+            if constexpr (TA == 2) {
+                const float* sc = reinterpret_cast<const float*>(src + NR * NL) + NL;
+                scl = make_float3(sc[0], sc[1], sc[2]);
+            }
         };
         if (n_my > 0) fetch(0);
 #pragma unroll 1
@@ -1091,7 +1157,28 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
             // B buffer b is free once unit i-2's MMAs completed; slopes use a 4-deep ring (unit i+4 reuses
             // slot i & 3 only after accfull(i+2), which the control issues after tfree(i): epilogue(i) done)
             if (i >= 2) mbar_wait(&accfull[b], (uint32_t)(((i >> 1) + 1) & 1));
-            {
+            const float sy = scl.x;  // this unit's y scale (scl is overwritten by the prefetch below)
+            if constexpr (TA == 2) {
+                // B (fp16, SW128 K-major): K-tile kt2 = kt / 2 holds chunks 2 kt2, 2 kt2 + 1 (64 fp16 per row);
+                // this thread's 16 antennas are 16-byte chunks 4 (kt & 1) + j, j = 0..3, of rows n and n + 32
+                unsigned char* kb = g + A4::B + b * A4::bset + (size_t)(kt >> 1) * 8192;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    uint32_t hv[4], lv[4];
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) {
+                        const float2 w = make_float2(wv[4 * j + m].x * scl.y, wv[4 * j + m].y * scl.y);
+                        if (im_row) split_h2(w.y, w.x, hv[m], lv[m]);
+                        else split_h2(w.x, -w.y, hv[m], lv[m]);
+                    }
+                    const int q = 4 * (kt & 1) + j;
+                    *reinterpret_cast<uint4*>(kb + n * 128 + ((q ^ (n & 7)) << 4)) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+                    *reinterpret_cast<uint4*>(kb + (n + 32) * 128 + ((q ^ (n & 7)) << 4)) =
+                        make_uint4(lv[0], lv[1], lv[2], lv[3]);
+                }
+                if (tc < NL) sslope[(i & 3) * 16 + tc] = slv;
+                if (tc == 0) sslope[64 + (i & 3)] = scl.z;
+            } else {
                 float* kb = reinterpret_cast<float*>(g + A4::B + b * A4::bset + (size_t)kt * 64 * 128);
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
@@ -1119,7 +1206,7 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
                     tc_fence_after();
                     const unsigned char* ysm = g + A4::y0 + st * A4::chunk;
 #pragma unroll
-                    for (int tile = 0; tile < 2; ++tile) {
+                    for (int tile = 0; tile < (ABL & 1 ? 0 : 2); ++tile) {
                         const int r = (tile ? 40 : 0) + 32 * warp + lane;
                         const float4* row = reinterpret_cast<const float4*>(ysm + (size_t)r * 128);
                         float v[32], lo[32];
@@ -1131,11 +1218,20 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
                             v[4 * cc + 2] = q.z;
                             v[4 * cc + 3] = q.w;
                         }
+                        if constexpr (TA == 2) {  // fp16 pairs: columns 0-15 y_hi, 16-31 y_lo (scaled by sy)
+                            uint32_t pk[32];
 #pragma unroll
-                        for (int k = 0; k < 32; ++k) lo[k] = v[k] - tf32_trunc(v[k]);
-                        const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16) + kAring + 128u * (uint32_t)lb + 64u * tile;
-                        tmem_st32(ta, v);
-                        tmem_st32(ta + 32u, lo);
+                            for (int k2 = 0; k2 < 16; ++k2) split_h2(v[2 * k2] * sy, v[2 * k2 + 1] * sy, pk[k2], pk[16 + k2]);
+                            tmem_st32(tmem + ((uint32_t)(32 * warp) << 16) + kAring + 64u * (uint32_t)lb + 32u * tile,
+                                      reinterpret_cast<const float*>(pk));
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < 32; ++k) lo[k] = v[k] - tf32_trunc(v[k]);
+                            const uint32_t ta =
+                                tmem + ((uint32_t)(32 * warp) << 16) + kAring + 128u * (uint32_t)lb + 64u * tile;
+                            tmem_st32(ta, v);
+                            tmem_st32(ta + 32u, lo);
+                        }
                     }
                     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
                     tc_fence_before();
@@ -1278,10 +1374,11 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
                 const int s = row / kSc, f = row % kSc;
                 const size_t re = (size_t)(slot * kSym + s) * a.n_sc + fb * kSc + f;
                 float2 x[KL];
+                const float xs = TA == 2 ? sslope[64 + (i & 3)] : 1.f;  // undo the fp16 path's scales (exact)
 #pragma unroll
                 for (int k = 0; k < KL; ++k)
-                    x[k] = make_float2(__uint_as_float(hr[k]) + __uint_as_float(lr[k]),
-                                       __uint_as_float(hi[k]) + __uint_as_float(li[k]));
+                    x[k] = make_float2((__uint_as_float(hr[k]) + __uint_as_float(lr[k])) * xs,
+                                       (__uint_as_float(hi[k]) + __uint_as_float(li[k])) * xs);
                 const float* sl = sslope + (i & 3) * 16 + KL * h;
                 if (a.llr && !(ABL & 2)) {
                     float v[KL * QM];
@@ -1405,12 +1502,21 @@ const KernelEntry kEntries[] = {
     KernelEntry{"big8_64x16_q6_i8", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 0, 0, 1, 1>,
                 prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 0, 0, 1, 1>, workspace<64, 16>},
     BIG4_ENTRY("big4_64x16_q6_i8", 4, 4, 2),  // y_lo through a shared-memory ring
+    // big11: big8 with fp16 hi/lo operands (reading R27): K = 16 per MMA, 8 MMAs per chunk instead of 16
+    KernelEntry{"big11_64x16_q6_i8", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 0, 0, 1, 2>,
+                prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 0, 0, 1, 2>, workspace<64, 16>},
     BIG4_ENTRY("big4e8_64x16_q6_i8", 8, 4, 2),
     // big4 with the Cholesky / L^-1 / X^H X setup route instead of Gauss-Jordan (reading R26)
     KernelEntry{"big4c_64x16_q6_i8", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 0, 0, 0>,
                 prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 0, 0, 0>, workspace<64, 16>},
     KernelEntry{"big5_64x16_q6_i8", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 0, 1>,
                 prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 0, 1>, workspace<64, 16>},
+    KernelEntry{"ablation_big8_noconv", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 1, 0, 1, 1>,
+                prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 1, 0, 1, 1>, workspace<64, 16>},
+    KernelEntry{"ablation_big8_none", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 3, 0, 1, 1>,
+                prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 3, 0, 1, 1>, workspace<64, 16>},
+    KernelEntry{"ablation_big11_noconv", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 1, 0, 1, 2>,
+                prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 1, 0, 1, 2>, workspace<64, 16>},
     KernelEntry{"ablation_big8_noepi", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 2, 0, 1, 1>,
                 prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 2, 0, 1, 1>, workspace<64, 16>},
     KernelEntry{"ablation_big8_mma1", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 4, 0, 1, 1>,

@@ -1,4 +1,6 @@
 #!/bin/bash
-timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu.log
-timeout 300 python bench.py --config 5 --no-e2e --no-cpu-baseline > gpurun_out/bench_c5.json 2>gpurun_out/bench_c5.err; echo "bench rc=$?"
-python -c "import json; d=json.loads(open('gpurun_out/bench_c5.json').read().strip().splitlines()[-1]); print(d['config']['kernel'], d['ms_per_step']*1000, d['roofline']['frac'], d['roofline']['bound'], d['clocks'])"
+for k in big8_64x16_q6_i8 ablation_big8_noconv ablation_big8_noepi ablation_big8_none ablation_big8_mma1 big11_64x16_q6_i8 ablation_big11_noconv; do echo $k; timeout 60 python tools/dbg_time.py $k 5 40 1 2>&1 | tail -1; done
+python bench.py --config 5 --profile --steps 3 --warmup 2 > /dev/null 2>&1
+for k in big8_64x16_q6_i8 ablation_big8_noconv ablation_big8_none; do
+MIMO_FORCE_KERNEL=$k ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_big_apply --csv python bench.py --config 5 --profile --steps 3 --warmup 2 2>/dev/null | grep k_big_apply | tail -1 | awk -F'","' '{print $NF}'
+done
