@@ -12,8 +12,9 @@
 //     W~ = diag(sqrt(norm)/mu) G^-1 H^H (lane (k, half) covers half the antennas),
 //     written to the plan workspace as [unit][r][k] plus slopes.
 //   Apply kernels (rows a6-a7), all reading W~ from the workspace:
-//   k_big_apply4 (C5 default): persistent, warp-specialised tcgen05 pipeline
-//     (TMA y chunks, single-thread MMA issue, converter and epilogue warps).
+//   k_big_apply4: persistent, warp-specialised tcgen05 pipeline (TMA y chunks,
+//     single-thread MMA issue, converter and epilogue warps); TA = 1 ("big8",
+//     the C5 default) keeps the y operand in TMEM, TA = 2 ("big11") in fp16.
 //   k_big_apply3: the same tensor-core computation, one CTA per unit.
 //   k_big_apply2: SIMT, K-streamed TMA chunks, 4 x 4 complex register tile.
 //   k_big_apply (other shapes / LLR types): SIMT, CTA per PRB-unit, the unit's
