@@ -121,6 +121,21 @@ mimo_status_t mimo_detect_mmse_ex(mimo_plan_t plan, const void* H, const void* y
                                   int n_rx, int n_layers, int n_sc, int n_sym, int qam_order,
                                   void* llr_out, void* xhat_out, float* sinr_out);
 
+/* Per-slot noise variance (SURVEY.md 8(f) NEXT-3 "per-slot sigma2 arrays"; the
+ * paper uses one sigma2 per configuration). Same computation as
+ * mimo_detect_mmse_ex with sigma2 replaced, for every H-unit of H time block t
+ * (units t * (n_sc / sc_per_h) ... ; t = slot when sym_per_h = 14), by
+ * sigma2_v[t]. sigma2_v: DEVICE float32 [n_sym / sym_per_h], 4-byte aligned,
+ * owned by the caller, read on the plan's stream. Each entry must be finite
+ * and > 0 (no zero-forcing on this path): a bad entry makes that block's units
+ * fail the pivot guard -- outputs zeroed and counted, mimo_plan_sync_status ->
+ * MIMO_ERR_NOT_PD. Served by the same kernels as mimo_detect_mmse_ex.
+ * Errors: as mimo_detect_mmse_ex (sigma2 checks replaced by: null, misaligned
+ * or non-device sigma2_v -> INVALID_ARG). */
+mimo_status_t mimo_detect_mmse_sv(mimo_plan_t plan, const void* H, const void* y, const float* sigma2_v,
+                                  int n_rx, int n_layers, int n_sc, int n_sym, int qam_order,
+                                  void* llr_out, void* xhat_out, float* sinr_out);
+
 /* End-to-end form with HOST buffers (same layouts): copies H and y to a
  * plan-owned device workspace, detects, copies the LLRs back, and returns after
  * the stream has drained. Work is split into slot chunks (~2 MiB of input)

@@ -39,7 +39,18 @@ struct DetectArgs {
     int llr_type;
     int overlap;          // launch with programmatic dependent launch (MIMO_PLAN_OVERLAP_CALLS)
     void* ws;             // plan-owned workspace (kernel families that need one)
+    const float* sigma2_v;  // mimo_detect_mmse_sv: one noise variance per H time block [n_slots] (else null)
 };
+
+// Noise variance of H time block `blk` (= slot for sym_per_h = 14): the scalar sigma2, or the
+// per-block array entry, which must be finite and > 0 -- anything else becomes NaN so that the
+// unit fails the pivot guard (R17) and is counted / zeroed like a non-PD unit.
+__device__ __forceinline__ float block_sigma2(const DetectArgs& a, long long blk) {
+    if (!a.sigma2_v) return a.sigma2;
+    const float v = __ldg(a.sigma2_v + blk);
+    return (v > 0.f && v <= 3.4e38f) ? v : __int_as_float(0x7fc00000);
+}
+__device__ __forceinline__ float unit_sigma2(const DetectArgs& a, long long u) { return block_sigma2(a, u / a.n_fb); }
 
 // Per-axis PAM normalisation of the 38.211 constellations: a = 1/sqrt(norm).
 __host__ __device__ constexpr int qam_norm(int qm) { return qm == 2 ? 2 : qm == 4 ? 10 : qm == 6 ? 42 : 170; }

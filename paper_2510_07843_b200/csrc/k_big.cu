@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(32 * UPB) k_big_setup(DetectArgs a) {
     pdl_launch_dependents();
     const long long u = (long long)blockIdx.x * UPB + warp;
     const bool valid = u < a.n_units;
-    const float s2 = a.sigma2;
+    const float s2 = unit_sigma2(a, valid ? u : 0);
     const float norm = (float)qam_norm(QM);
     if (valid && lane == 0) {  // a1: the unit's H (8 KiB) by one bulk copy
         mbar_init(bar, 1);

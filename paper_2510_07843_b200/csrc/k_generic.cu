@@ -94,13 +94,13 @@ __global__ void __launch_bounds__(kThreads) k_generic(DetectArgs a) {
     pdl_launch_dependents();
     pdl_wait();
     const int nr = a.n_rx, nl = a.n_layers, tid = threadIdx.x;
-    const double s2 = (double)a.sigma2;
     const double norm = (double)qam_norm(QM);
     const double sq_norm = sqrt(norm);
 
     for (long long u = blockIdx.x; u < a.n_units; u += gridDim.x) {
         const int slot = (int)(u / a.n_fb);
         const int fb = (int)(u % a.n_fb);
+        const double s2 = (double)block_sigma2(a, slot);
         // a1: stage H_u
         for (int i = tid; i < nr * nl; i += blockDim.x) {
             const float2 h = __ldg(a.H + (size_t)u * nr * nl + i);

@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(32 * NW) k_lg(DetectArgs a) {
     const int ul = warp * UPW + lane / NL;       // unit within the tile
     const bool active = ul < nvalid;
     const int sc = sc0 + ul;
-    const float s2 = a.sigma2;
+    const float s2 = block_sigma2(a, slot);
     const float norm = (float)qam_norm(QM);
 
     if (t == 0) {
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(32 * NW) k_lg3(DetectArgs a, const __grid_cons
     const int ul = warp * UPW + lane / NL;       // unit within the tile
     const bool active = ul < nvalid;
     const int sc = sc0 + ul;
-    const float s2 = a.sigma2;
+    const float s2 = block_sigma2(a, slot);
     const float norm = (float)qam_norm(QM);
 
     if (t == 0) {

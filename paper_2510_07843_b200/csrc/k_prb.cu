@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(kSc* P* G) k_prb(DetectArgs a) {
     const int p = f / kSc;
     const bool active = f < np * kSc;
     const float norm = (float)qam_norm(QM);
-    const float s2 = a.sigma2;
+    const float s2 = block_sigma2(a, slot);
 
     if (t == 0) {
 #pragma unroll

@@ -50,7 +50,6 @@ __global__ void __launch_bounds__(128) k_setup_units(DetectArgs a) {
     const int t = threadIdx.x;
     const long long u0 = (long long)blockIdx.x * UPC;
     const int nu = (int)min((long long)UPC, a.n_units - u0);
-    const float s2 = a.sigma2;
     const float norm = (float)qam_norm(QM);
     const float sqn = sqrtf(norm);
     float* ws = reinterpret_cast<float*>(a.ws);
@@ -79,12 +78,13 @@ __global__ void __launch_bounds__(128) k_setup_units(DetectArgs a) {
             acc.x += c.x;
             acc.y += c.y;
         }
-        if (i == j) acc = make_float2(acc.x + s2, 0.f);
+        if (i == j) acc = make_float2(acc.x + unit_sigma2(a, u0 + pu), 0.f);
         sGi[(pu * NL + i) * NL + j] = acc;
     }
     __syncthreads();
     // a3-a5: one thread per unit
     if (t < nu) {
+        const float s2 = unit_sigma2(a, u0 + t);
         float2 L[NL][NL];
         float gmax = 0.f;
 #pragma unroll

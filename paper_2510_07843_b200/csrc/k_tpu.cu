@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(TU* G) k_tpu(DetectArgs a) {
     }
 
     SetupOut<NR, NL> o;
-    if (does_setup) setup_unit<ST, NR, NL>(hf, a.sigma2, (float)qam_norm(QM), a.llr_scale, o);
+    if (does_setup) setup_unit<ST, NR, NL>(hf, block_sigma2(a, slot), (float)qam_norm(QM), a.llr_scale, o);
     if constexpr (SHARE) {
         if (does_setup) {
 #pragma unroll

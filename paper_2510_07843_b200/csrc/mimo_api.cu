@@ -288,6 +288,34 @@ mimo_status_t mimo_detect_mmse_ex(mimo_plan_t p, const void* H, const void* y, f
     return launch(p, a, p->stream);
 }
 
+mimo_status_t mimo_detect_mmse_sv(mimo_plan_t p, const void* H, const void* y, const float* sigma2_v, int n_rx,
+                                  int n_layers, int n_sc, int n_sym, int qm, void* llr_out, void* xhat_out,
+                                  float* sinr_out) {
+    if (!p) return arg_fail(nullptr, "null plan");
+    mimo_status_t st = check_dims(p, 1.0f, n_rx, n_layers, n_sc, n_sym, qm);
+    if (st != MIMO_OK) return st;
+    if ((long long)n_sc * n_sym == 0) return MIMO_OK;
+    if (!sigma2_v) return arg_fail(p, "null sigma2_v");
+    if (!aligned(sigma2_v, 4)) return arg_fail(p, "sigma2_v not 4-byte aligned");
+    if (!is_device_ptr(sigma2_v, p->d.device)) return arg_fail(p, "sigma2_v is not device memory on the plan's device");
+    if (!H || !y) return arg_fail(p, "null H or y");
+    if (!llr_out && !xhat_out && !sinr_out) return arg_fail(p, "no output requested");
+    if (!aligned(H, 16) || !aligned(y, 16) || !aligned(llr_out, 16) || !aligned(xhat_out, 16) ||
+        !aligned(sinr_out, 4))
+        return arg_fail(p, "pointer not 16-byte aligned");
+    const int dev = p->d.device;
+    if (!is_device_ptr(H, dev) || !is_device_ptr(y, dev) || !is_device_ptr(llr_out, dev) ||
+        !is_device_ptr(xhat_out, dev) || !is_device_ptr(sinr_out, dev))
+        return arg_fail(p, "pointer is not device memory on the plan's device");
+    DeviceGuard g(dev);
+    if (g.err != cudaSuccess) return cuda_fail(p, g.err, "cudaSetDevice");
+    // the scalar sigma2 = 1 keeps every apply kernel on its sigma2 > 0 (non zero-forcing) path; the
+    // setups read each unit's variance from sigma2_v (block_sigma2 in common.cuh)
+    mimo::DetectArgs a = make_args(p, H, y, 1.0f, n_sc, n_sym, llr_out, xhat_out, sinr_out);
+    a.sigma2_v = sigma2_v;
+    return launch(p, a, p->stream);
+}
+
 mimo_status_t mimo_detect_mmse(mimo_plan_t p, const void* H, const void* y, float sigma2, int n_rx, int n_layers,
                                int n_sc, int n_sym, int qm, void* llr_out) {
     if (p && (long long)n_sc * n_sym > 0 && !llr_out) return arg_fail(p, "null llr_out");

@@ -75,6 +75,8 @@ def load_library(path: str | None = None):
     L.mimo_detect_mmse.restype = i
     L.mimo_detect_mmse_ex.argtypes = [vp, vp, vp, f, i, i, i, i, i, vp, vp, vp]
     L.mimo_detect_mmse_ex.restype = i
+    L.mimo_detect_mmse_sv.argtypes = [vp, vp, vp, vp, i, i, i, i, i, vp, vp, vp]
+    L.mimo_detect_mmse_sv.restype = i
     L.mimo_detect_mmse_host.argtypes = [vp, vp, vp, f, i, i, i, i, i, vp]
     L.mimo_detect_mmse_host.restype = i
     L.mimo_detect_lmmse_lu.argtypes = [vp, vp, vp, f, i, i, i, i, i, i, vp, vp, vp, ctypes.POINTER(f)]
@@ -189,9 +191,11 @@ class Plan:
         return t
 
     # -- API ---------------------------------------------------------------
-    def detect(self, H, y, sigma2: float, out=None, xhat=None, sinr=None, *, n_sc=None, n_sym=None,
+    def detect(self, H, y, sigma2, out=None, xhat=None, sinr=None, *, n_sc=None, n_sym=None,
                want_llr: bool = True):
-        """Detect all REs of y (device tensors). Returns the LLR tensor (or None)."""
+        """Detect all REs of y (device tensors). Returns the LLR tensor (or None).
+        sigma2: a float, or a device float32 tensor [n_sym / sym_per_h] of per-slot (per H time
+        block) noise variances, each finite and > 0 (mimo_detect_mmse_sv)."""
         import torch
         n_sym = y.shape[0] if n_sym is None else n_sym
         n_sc = y.shape[1] if n_sc is None else n_sc
@@ -209,7 +213,11 @@ class Plan:
         if self._fixed_stream is None:
             self._lib.mimo_plan_set_stream(self._h, ctypes.c_void_p(self._stream_ptr()))
         ptr = (lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None)
-        if xhat is None and sinr is None:
+        if isinstance(sigma2, torch.Tensor):
+            self._dev_tensor(sigma2, "sigma2", torch.float32, (n_sym // self.sym_per_h,))
+            st = self._lib.mimo_detect_mmse_sv(self._h, ptr(H), ptr(y), ptr(sigma2), self.n_rx, self.n_layers,
+                                               n_sc, n_sym, self.qm, ptr(out), ptr(xhat), ptr(sinr))
+        elif xhat is None and sinr is None:
             st = self._lib.mimo_detect_mmse(self._h, ptr(H), ptr(y), ctypes.c_float(sigma2), self.n_rx,
                                             self.n_layers, n_sc, n_sym, self.qm, ptr(out))
         else:
