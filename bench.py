@@ -39,7 +39,7 @@ METRIC = "MIMO-detected REs/s per B200 (LLR Gbit/s alongside) vs roofline"
 FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
 FALLBACK_BF16_TFLOPS = 2250.0  # B200_PROFILING.md nominal dense bf16
 TF32_PER_BF16 = 1.1 / 2.25   # B200_PROFILING.md nominal dense tf32 / bf16
-TC_KERNELS = ("big3", "big4", "big5", "big8")  # kernels whose row a6 runs on tcgen05 (R21)
+TC_KERNELS = ("big3", "big4", "big5", "big8", "big11")  # kernels whose row a6 runs on tcgen05 (R21)
 
 
 def parse():

@@ -13,8 +13,9 @@
 //     written to the plan workspace as [unit][r][k] plus slopes.
 //   Apply kernels (rows a6-a7), all reading W~ from the workspace:
 //   k_big_apply4: persistent, warp-specialised tcgen05 pipeline (TMA y chunks,
-//     single-thread MMA issue, converter and epilogue warps); TA = 1 ("big8",
-//     the C5 default) keeps the y operand in TMEM, TA = 2 ("big11") in fp16.
+//     single-thread MMA issue, converter and epilogue warps); TA = 1 ("big8";
+//     "big8e6" with six epilogue warps is the C5 default) keeps the y operand in
+//     TMEM, TA = 2 ("big11") in fp16.
 //   k_big_apply3: the same tensor-core computation, one CTA per unit.
 //   k_big_apply2: SIMT, K-streamed TMA chunks, 4 x 4 complex register tile.
 //   k_big_apply (other shapes / LLR types): SIMT, CTA per PRB-unit, the unit's
@@ -455,7 +456,13 @@ __device__ __forceinline__ void umma_f16_ta(uint32_t d_tmem, uint32_t a_tmem, ui
 __device__ __forceinline__ void split_h2(float a0, float a1, uint32_t& hi, uint32_t& lo) {
     const __half2 h = __floats2half2_rn(a0, a1);
     const float2 f = __half22float2(h);
-    const __half2 l = __floats2half2_rn(a0 - f.x, a1 - f.y);
+    unsigned long long ua, uf, ud;  // packed (a - f): one sub.f32x2
+    asm("mov.b64 %0, {%1, %2};" : "=l"(ua) : "f"(a0), "f"(a1));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(uf) : "f"(f.x), "f"(f.y));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(ud) : "l"(ua), "l"(uf));
+    float2 d;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(ud));
+    const __half2 l = __floats2half2_rn(d.x, d.y);
     hi = *reinterpret_cast<const uint32_t*>(&h);
     lo = *reinterpret_cast<const uint32_t*>(&l);
 }
@@ -957,6 +964,10 @@ template <int NR, int NL, int QM, int LT, int EW, int S_, int NLO_, int ABL, int
 __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, const __grid_constant__ CUtensorMap ymap) {
     using A4 = Ap4<S_, NLO_, TR, (TR && EW == 8) ? kRe : 96, TA>;
     static_assert(!TA || (!TR && NLO_ == 2), "TA: untransposed, two A buffers");
+    // EW = 6 (TA only): warps 4-7 take tile 0 of their lane quadrant, warps 8-9 tile 1, which is
+    // compact (REs 128-167 in lanes 0-39 of quadrants 0, 1): one epilogue pass per warp per unit
+    constexpr bool CT = EW == 6;
+    static_assert(!CT || TA, "EW 6: TMEM A operand only");
     constexpr uint32_t kTmemCols = (TR || TA) ? 512u : 256u;
     constexpr uint32_t kAccStride = TR ? 256u : 128u;
     constexpr uint32_t kAring = 256u;  // TA: first TMEM column of the A ring
@@ -1208,7 +1219,9 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
                     const unsigned char* ysm = g + A4::y0 + st * A4::chunk;
 #pragma unroll
                     for (int tile = 0; tile < (ABL & 1 ? 0 : 2); ++tile) {
-                        const int r = (tile ? 40 : 0) + 32 * warp + lane;
+                        if (CT && tile == 1 && warp >= 2) break;  // compact tile 1: REs 128-167 in lanes 0-39
+                        const int r = tile ? (CT ? min(128 + 32 * warp + lane, kRe - 1) : 40 + 32 * warp + lane)
+                                           : 32 * warp + lane;
                         const float4* row = reinterpret_cast<const float4*>(ysm + (size_t)r * 128);
                         float v[32], lo[32];
 #pragma unroll
@@ -1221,8 +1234,12 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
                         }
                         if constexpr (TA == 2) {  // fp16 pairs: columns 0-15 y_hi, 16-31 y_lo (scaled by sy)
                             uint32_t pk[32];
+                            if (sy != 1.f) {  // uniform per unit; 1 for O(1)-scaled inputs
 #pragma unroll
-                            for (int k2 = 0; k2 < 16; ++k2) split_h2(v[2 * k2] * sy, v[2 * k2 + 1] * sy, pk[k2], pk[16 + k2]);
+                                for (int k = 0; k < 32; ++k) v[k] *= sy;
+                            }
+#pragma unroll
+                            for (int k2 = 0; k2 < 16; ++k2) split_h2(v[2 * k2], v[2 * k2 + 1], pk[k2], pk[16 + k2]);
                             tmem_st32(tmem + ((uint32_t)(32 * warp) << 16) + kAring + 64u * (uint32_t)lb + 32u * tile,
                                       reinterpret_cast<const float*>(pk));
                         } else {
@@ -1348,8 +1365,8 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
                 }
             }
 #pragma unroll 1
-            for (int tile = 0; tile < (TR ? 0 : 2); ++tile) {
-                if (tile == 1 && we < 2) break;
+            for (int tile = CT ? (e >> 2) : 0; tile < (TR ? 0 : (CT ? (e >> 2) + 1 : 2)); ++tile) {
+                if (!CT && tile == 1 && we < 2) break;
                 uint32_t hr[KL], hi[KL], lr[KL], li[KL];
                 const uint32_t taddr = tmem + ((uint32_t)(32 * we) << 16) + kAccStride * (uint32_t)b + 64u * tile + KL * h;
                 if constexpr (KL == 16) {
@@ -1370,16 +1387,22 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
                     tmem_ld8(taddr + 48u, li);
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
                 }
-                const int row = (tile ? 40 : 0) + 32 * we + lane;
-                if (tile == 1 && row < 128) continue;
+                const int row = (tile ? (CT ? 128 : 40) : 0) + 32 * we + lane;
+                if (tile == 1 && (CT ? row >= kRe : row < 128)) continue;
                 const int s = row / kSc, f = row % kSc;
                 const size_t re = (size_t)(slot * kSym + s) * a.n_sc + fb * kSc + f;
                 float2 x[KL];
-                const float xs = TA == 2 ? sslope[64 + (i & 3)] : 1.f;  // undo the fp16 path's scales (exact)
 #pragma unroll
                 for (int k = 0; k < KL; ++k)
-                    x[k] = make_float2((__uint_as_float(hr[k]) + __uint_as_float(lr[k])) * xs,
-                                       (__uint_as_float(hi[k]) + __uint_as_float(li[k])) * xs);
+                    x[k] = make_float2(__uint_as_float(hr[k]) + __uint_as_float(lr[k]),
+                                       __uint_as_float(hi[k]) + __uint_as_float(li[k]));
+                if constexpr (TA == 2) {  // undo the fp16 path's scales (exact; 1 for O(1)-scaled units)
+                    const float xs = sslope[64 + (i & 3)];
+                    if (xs != 1.f) {
+#pragma unroll
+                        for (int k = 0; k < KL; ++k) x[k] = make_float2(x[k].x * xs, x[k].y * xs);
+                    }
+                }
                 const float* sl = sslope + (i & 3) * 16 + KL * h;
                 if (a.llr && !(ABL & 2)) {
                     float v[KL * QM];
@@ -1402,8 +1425,7 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_big_apply4(DetectArgs a, c
                 }
             }
             tc_fence_before();
-            if constexpr (EW == 8) asm volatile("bar.sync 2, 256;" ::: "memory");
-            else asm volatile("bar.sync 2, 128;" ::: "memory");
+            asm volatile("bar.sync 2, %0;" ::"r"(32 * EW) : "memory");
             if (t == 128) mbar_arrive(&tfree[b]);
         }
     }
@@ -1499,7 +1521,10 @@ const KernelEntry kEntries[] = {
         NAME, 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, EW, S, NLO>,                \
             prepare_ap4<64, 16, 6, kLlrI8, EW, S, NLO>, workspace<64, 16>                                  \
     }
-    // C5 default: big4's tcgen05 3-pass TF32 pipeline with the y operand (hi, lo) in TMEM (fastest)
+    // C5 default: big4's tcgen05 3-pass TF32 pipeline with the y operand (hi, lo) in TMEM and six epilogue
+    // warps (tile 0 on warps 4-7, compact tile 1 on warps 8-9)
+    KernelEntry{"big8e6_64x16_q6_i8", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 6, 4, 2, 0, 0, 1, 1>,
+                prepare_ap4<64, 16, 6, kLlrI8, 6, 4, 2, 0, 0, 1, 1>, workspace<64, 16>},
     KernelEntry{"big8_64x16_q6_i8", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 0, 0, 1, 1>,
                 prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 0, 0, 1, 1>, workspace<64, 16>},
     BIG4_ENTRY("big4_64x16_q6_i8", 4, 4, 2),  // y_lo through a shared-memory ring
@@ -1516,6 +1541,12 @@ const KernelEntry kEntries[] = {
                 prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 1, 0, 1, 1>, workspace<64, 16>},
     KernelEntry{"ablation_big8_none", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 3, 0, 1, 1>,
                 prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 3, 0, 1, 1>, workspace<64, 16>},
+    KernelEntry{"big11e6_64x16_q6_i8", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 6, 4, 2, 0, 0, 1, 2>,
+                prepare_ap4<64, 16, 6, kLlrI8, 6, 4, 2, 0, 0, 1, 2>, workspace<64, 16>},
+    KernelEntry{"ablation_big11_noepi", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 2, 0, 1, 2>,
+                prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 2, 0, 1, 2>, workspace<64, 16>},
+    KernelEntry{"ablation_big11_none", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 3, 0, 1, 2>,
+                prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 3, 0, 1, 2>, workspace<64, 16>},
     KernelEntry{"ablation_big11_noconv", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 1, 0, 1, 2>,
                 prepare_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 1, 0, 1, 2>, workspace<64, 16>},
     KernelEntry{"ablation_big8_noepi", 64, 16, 6, kSc, 14, kLlrI8, 32, 2, launch_ap4<64, 16, 6, kLlrI8, 4, 4, 2, 2, 0, 1, 1>,

@@ -10,7 +10,7 @@ from paper_2510_07843_b200 import synth
 
 pytestmark = pytest.mark.gpu
 
-C5_VARIANTS = ["big4_64x16_q6_i8", "big4c_64x16_q6_i8", "big4e8_64x16_q6_i8", "big5_64x16_q6_i8", "big5e8_64x16_q6_i8", "big8_64x16_q6_i8", "big11_64x16_q6_i8",
+C5_VARIANTS = ["big4_64x16_q6_i8", "big4c_64x16_q6_i8", "big4e8_64x16_q6_i8", "big5_64x16_q6_i8", "big5e8_64x16_q6_i8", "big8_64x16_q6_i8", "big11_64x16_q6_i8", "big8e6_64x16_q6_i8", "big11e6_64x16_q6_i8",
                "big3_64x16_q6_i8", "big2_64x16_q6_i8",
                "big_64x16_q6_i8"]
 C4_VARIANTS = ["lg3h_16x8_q8_f16", "lg3_16x8_q8_f16", "lg3_16x8_q8_f16_w1", "lg_16x8_q8_f16"]
