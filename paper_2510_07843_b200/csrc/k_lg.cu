@@ -263,6 +263,9 @@ struct Lg3Smem {
     static constexpr size_t total = bars + 16 + 1024;                       // + 1024-alignment slack
 };
 
+// HT = 2: as HT = 1 with the per-RE apply as packed FFMA2, acc += (w.x, w.y) y.x + (-w.y, w.x) y.y
+// (y components broadcast; 80.3 vs 80.9 us per C4 step -- the same packing in the Gram and W~
+// loops of the setup made the step slower, 82.4 us, so they stay scalar).
 // HT = 1: H also by one TMA tensor box per CTA: H viewed as (32 floats = one 128-byte row of
 // 2 rx x 8 layers, unit, row-within-unit) -- unit as the middle dimension -- so the box lands
 // as [row][unit][128 B] and SWIZZLE_128B spreads the UPW units of a warp over distinct banks.
@@ -445,6 +448,11 @@ __global__ void __launch_bounds__(32 * NW) k_lg3(DetectArgs a, const __grid_cons
         w[r] = (fac > 0.f) ? make_float2(sv.x * fac, sv.y * fac) : make_float2(0.f, 0.f);
     }
 
+    float2 wq[HT == 2 ? NR : 1];  // HT 2: (-w.y, w.x) for the packed apply
+    if constexpr (HT == 2) {
+#pragma unroll
+        for (int r = 0; r < NR; ++r) wq[r] = make_float2(-w[r].y, w[r].x);
+    }
     pdl_wait();  // global writes only after the previous grid completed
     if (active) {
         const size_t unit = (size_t)slot * a.n_sc + sc;
@@ -464,11 +472,22 @@ __global__ void __launch_bounds__(32 * NW) k_lg3(DetectArgs a, const __grid_cons
         const unsigned char* yr = ybase + row * 128;
         const int sw = row & 7;
         float2 acc = make_float2(0.f, 0.f);
+        if constexpr (HT == 2) {  // packed FFMA2: acc += w y as (w.x, w.y) y.x + (-w.y, w.x) y.y
 #pragma unroll
-        for (int c = 0; c < NR / 2; ++c) {
-            const float4 v = *reinterpret_cast<const float4*>(yr + ((c ^ sw) << 4));
-            acc = cmac(acc, w[2 * c], make_float2(v.x, v.y));
-            acc = cmac(acc, w[2 * c + 1], make_float2(v.z, v.w));
+            for (int c = 0; c < NR / 2; ++c) {
+                const float4 v = *reinterpret_cast<const float4*>(yr + ((c ^ sw) << 4));
+                acc = ffma2(w[2 * c], make_float2(v.x, v.x), acc);
+                acc = ffma2(wq[2 * c], make_float2(v.y, v.y), acc);
+                acc = ffma2(w[2 * c + 1], make_float2(v.z, v.z), acc);
+                acc = ffma2(wq[2 * c + 1], make_float2(v.w, v.w), acc);
+            }
+        } else {
+#pragma unroll
+            for (int c = 0; c < NR / 2; ++c) {
+                const float4 v = *reinterpret_cast<const float4*>(yr + ((c ^ sw) << 4));
+                acc = cmac(acc, w[2 * c], make_float2(v.x, v.y));
+                acc = cmac(acc, w[2 * c + 1], make_float2(v.z, v.w));
+            }
         }
         const size_t re = (size_t)(slot * kSym + s) * a.n_sc + sc;
         if (a.llr) {
@@ -560,7 +579,10 @@ cudaError_t prepare() {
     }
 
 const KernelEntry kEntries[] = {
-    // C4: y and H of the CTA's 8 units as one TMA tensor box each
+    // C4 default: y and H of the CTA's 8 units as one TMA tensor box each (lg3h), per-RE apply as
+    // packed FFMA2 (HT = 2)
+    KernelEntry{"lg3hp_16x8_q8_f16", 16, 8, 8, 1, 14, kLlrF16, 32, 1, launch3<16, 8, 8, kLlrF16, 2, 0, 2>,
+                prepare3<16, 8, 8, kLlrF16, 2, 0, 2>},
     KernelEntry{"lg3h_16x8_q8_f16", 16, 8, 8, 1, 14, kLlrF16, 32, 1, launch3<16, 8, 8, kLlrF16, 2, 0, 1>,
                 prepare3<16, 8, 8, kLlrF16, 2, 0, 1>},
     LG3_ENTRY("lg3_16x8_q8_f16", 16, 8, 8, kLlrF16, 2),  // y by TMA, H by per-unit bulk copies

@@ -1,6 +1,2 @@
 #!/bin/bash
-timeout 60 python tools/dbg_size.py big8e6_64x16_q6_i8 3276 40 big4c_64x16_q6_i8 2>&1 | tail -1
-for k in big8e6_64x16_q6_i8; do echo $k; timeout 60 python tools/dbg_time.py $k 5 40 1 2>&1 | tail -1; done
-timeout 600 python -m pytest tests/test_variants_gpu.py tests/test_parity_gpu.py tests/test_sigma2v_gpu.py -q -x -k "c5 or 5" 2>&1 | tail -2
-python bench.py --config 5 --profile --steps 3 --warmup 2 > /dev/null 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_big_setup --csv python bench.py --config 5 --profile --steps 3 --warmup 2 2>/dev/null | grep k_big_setup | tail -2 | awk -F'","' '{print $NF}'
+timeout 1500 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu.log
