@@ -1,6 +1,2 @@
 #!/bin/bash
-timeout 60 python tools/dbg_size.py big8e6g_64x16_q6_i8 3276 40 big8e6_64x16_q6_i8 2>&1 | tail -1
-for k in big8e6_64x16_q6_i8 big8e6g_64x16_q6_i8 big8e6_64x16_q6_i8 big8e6g_64x16_q6_i8; do echo $k; timeout 60 python tools/dbg_time.py $k 5 40 1 2>&1 | tail -1; done
-python bench.py --config 5 --profile --steps 3 --warmup 2 > /dev/null 2>&1
-MIMO_FORCE_KERNEL=big8e6g_64x16_q6_i8 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:k_big --csv python bench.py --config 5 --profile --steps 3 --warmup 2 2>/dev/null | grep "k_big" | tail -2 | awk -F'","' '{print $5, $NF}'
-timeout 600 python -m pytest tests/test_variants_gpu.py -q -x -k "big8e6g" 2>&1 | tail -2
+timeout 600 python -m pytest tests/test_edge_gpu.py -q -x 2>&1 | tail -25
