@@ -122,7 +122,7 @@ def test_nan_input_flagged():
     assert np.all(g["llr"][s, f] == 0)
 
 
-@pytest.mark.parametrize("k", [2, 3, 4])
+@pytest.mark.parametrize("k", [2, 3, 4, 5])
 def test_power_of_two_scaling_bit_identical(k):
     w = synth.generate(k, n_sc=96, n_slots=1)
     g1 = parity.run_gpu(w)

@@ -1,2 +1,2 @@
 #!/bin/bash
-timeout 600 python -m pytest tests/test_edge_gpu.py -q -x 2>&1 | tail -25
+timeout 600 python -m pytest tests/test_parity_gpu.py -q -x -k "power_of_two" 2>&1 | tail -5
