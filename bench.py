@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--config", default="2",
                     help="BASELINE config 1..5 (default 2 = configs[1], the headline), P (paper shape) or all")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=60)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU budget of the oracle baseline")
@@ -401,17 +401,30 @@ def run_ours(args, k):
         lh = torch.empty(plan.shapes(w.n_sc, w.n_sym)["llr"], dtype=plan.llr_dtype).pin_memory()
         for _ in range(2):
             plan.detect_host(Hh, yh, s2, out=lh)
+        # context: one synchronous call per step (each call fills and drains its own pipeline)
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
             plan.detect_host(Hh, yh, s2, out=lh)
+        dt_sync = shard.max_over_ranks(time.perf_counter() - t0, device=dev)
+        # the e2e number: a stream of TTIs through the asynchronous call -- every step still copies its
+        # inputs from pinned host memory and its LLRs back; the plan is synchronised inside the timed
+        # region, so all copies of all steps are included
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            plan.detect_host(Hh, yh, s2, out=lh, wait=False)
+        plan.sync_status()
         dt = time.perf_counter() - t0
         dt = shard.max_over_ranks(dt, device=dev)
         e2e = {"value": b["n_re"] * args.e2e_steps * world / dt, "unit": "RE/s",
                "h2d_bytes_per_step": b["H"] + b["y"], "d2h_bytes_per_step": b["llr"],
                "ms_per_step": dt * 1e3 / args.e2e_steps,
-               "path": "mimo_detect_mmse_host (pinned host buffers, 2-stream slot-chunk pipeline)"}
+               "path": "mimo_detect_mmse_host_async per step + one plan sync (pinned host buffers, "
+                       "3-stream slot-chunk pipeline; consecutive steps overlap their transfers)",
+               "sync_call_ms_per_step": dt_sync * 1e3 / args.e2e_steps}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and ybfp is None:

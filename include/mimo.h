@@ -138,7 +138,7 @@ mimo_status_t mimo_detect_mmse_sv(mimo_plan_t plan, const void* H, const void* y
 
 /* End-to-end form with HOST buffers (same layouts): copies H and y to a
  * plan-owned device workspace, detects, copies the LLRs back, and returns after
- * the stream has drained. Work is split into slot chunks (~2 MiB of input)
+ * the stream has drained. Work is split into slot chunks (~4 MiB of input)
  * on a 3-deep device buffer ring over three streams (host->device, kernels,
  * device->host) so both PCIe directions and the kernels overlap; pinned
  * (page-locked) host buffers are required for overlap but not for correctness.
@@ -146,6 +146,18 @@ mimo_status_t mimo_detect_mmse_sv(mimo_plan_t plan, const void* H, const void* y
 mimo_status_t mimo_detect_mmse_host(mimo_plan_t plan, const void* H_host, const void* y_host,
                                     float sigma2, int n_rx, int n_layers, int n_sc, int n_sym,
                                     int qam_order, void* llr_host);
+
+/* Asynchronous form of mimo_detect_mmse_host: the same copies and kernels are
+ * enqueued (ordered after the work already on the plan's stream) and the call
+ * returns at once; mimo_plan_sync_status and mimo_plan_destroy wait for it. Consecutive calls overlap -- the next call's host->device copies run
+ * while the previous call's results drain -- so a stream of TTIs is bound by
+ * the busier PCIe direction, not by each call's fill and drain. The host
+ * buffers must stay valid and unmodified (inputs) / unread (llr_host) until
+ * then. Errors: as mimo_detect_mmse_host (enqueue errors only; execution
+ * errors surface at the sync). */
+mimo_status_t mimo_detect_mmse_host_async(mimo_plan_t plan, const void* H_host, const void* y_host,
+                                          float sigma2, int n_rx, int n_layers, int n_sc, int n_sym,
+                                          int qam_order, void* llr_host);
 
 /* Paper-literal route: the LMMSE pipeline exactly as
  * the paper states it -- "LU decomposition, forward/backward substitution, and

@@ -43,6 +43,7 @@ struct mimo_plan_s {
     static constexpr int kNB = 3;          // host path: buffer ring depth
     cudaStream_t hs[3] = {nullptr, nullptr, nullptr};  // H2D, kernels, D2H
     cudaEvent_t ev = nullptr;
+    unsigned long long host_chunk = 0;  // host-path buffer ring position
     cudaEvent_t e_in[kNB] = {}, e_k[kNB] = {}, e_out[kNB] = {};
     // kernel workspaces: slot 0 for the plan's stream, 1..2 for the host path's streams
     void* kws[3] = {nullptr, nullptr, nullptr};
@@ -322,8 +323,8 @@ mimo_status_t mimo_detect_mmse(mimo_plan_t p, const void* H, const void* y, floa
     return mimo_detect_mmse_ex(p, H, y, sigma2, n_rx, n_layers, n_sc, n_sym, qm, llr_out, nullptr, nullptr);
 }
 
-mimo_status_t mimo_detect_mmse_host(mimo_plan_t p, const void* H_host, const void* y_host, float sigma2, int n_rx,
-                                    int n_layers, int n_sc, int n_sym, int qm, void* llr_host) {
+static mimo_status_t host_path(mimo_plan_t p, const void* H_host, const void* y_host, float sigma2, int n_rx, int n_layers,
+                        int n_sc, int n_sym, int qm, void* llr_host, bool wait) {
     if (!p) return arg_fail(nullptr, "null plan");
     mimo_status_t st = check_dims(p, sigma2, n_rx, n_layers, n_sc, n_sym, qm);
     if (st != MIMO_OK) return st;
@@ -338,11 +339,13 @@ mimo_status_t mimo_detect_mmse_host(mimo_plan_t p, const void* H_host, const voi
     const size_t h_slot = (size_t)n_fb * n_rx * n_layers * 8;
     const size_t y_slot = (size_t)symph * n_sc * n_rx * 8;
     const size_t l_slot = (size_t)symph * n_sc * n_layers * qm * llr_bytes(p->d.llr_type);
-    // Chunks of whole slots, ~2 MiB of input each, on a 3-deep buffer ring over
+    // Chunks of whole slots, ~4 MiB of input each, on a 3-deep buffer ring over
     // three streams (H2D | kernels | D2H) so both PCIe directions and the
     // kernels run concurrently; events order buffer reuse.
     constexpr int NB = mimo_plan_s::kNB;
-    size_t chunk_bytes = 2u << 20;
+    // measured best on the B200 box for C2 (tools/e2e_chunks.py): 4 MiB for a synchronous call (its
+    // own fill and drain are exposed), 16 MiB for a stream of asynchronous calls (they overlap)
+    size_t chunk_bytes = wait ? (4u << 20) : (16u << 20);
     if (const char* cb = getenv("MIMO_HOST_CHUNK_BYTES")) chunk_bytes = (size_t)atoll(cb);  // tuning knob
     int cs = (int)(chunk_bytes / (h_slot + y_slot));
     if (cs < 1) cs = 1;
@@ -383,17 +386,19 @@ mimo_status_t mimo_detect_mmse_host(mimo_plan_t p, const void* H_host, const voi
     int chunk = 0;
     for (int s0 = 0; s0 < n_slots; s0 += cs, ++chunk) {
         const int ns = (n_slots - s0) < cs ? (n_slots - s0) : cs;
-        const int b = chunk % NB;
+        const int b = (int)(p->host_chunk++ % NB);  // the ring continues across (asynchronous) calls
         char* base = p->ws + (size_t)b * (bh + by + bl);
         char *dH = base, *dy = base + bh, *dl = base + bh + by;
-        if (chunk >= NB) cudaStreamWaitEvent(s_in, p->e_k[b], 0);  // inputs of chunk - NB consumed
+        // buffer b's previous use (this call's chunk - NB, or a previous asynchronous call's chunk) is
+        // over: its inputs consumed / its outputs drained (waiting on a never-recorded event is a no-op)
+        cudaStreamWaitEvent(s_in, p->e_k[b], 0);
         e = cudaMemcpyAsync(dH, (const char*)H_host + h_slot * s0, h_slot * ns, cudaMemcpyHostToDevice, s_in);
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(dy, (const char*)y_host + y_slot * s0, y_slot * ns, cudaMemcpyHostToDevice, s_in);
         if (e == cudaSuccess) e = cudaEventRecord(p->e_in[b], s_in);
         if (e != cudaSuccess) return cuda_fail(p, e, "cudaMemcpyAsync H2D");
         cudaStreamWaitEvent(s_k, p->e_in[b], 0);
-        if (chunk >= NB) cudaStreamWaitEvent(s_k, p->e_out[b], 0);  // outputs of chunk - NB drained
+        cudaStreamWaitEvent(s_k, p->e_out[b], 0);
         mimo::DetectArgs a = make_args(p, dH, dy, sigma2, n_sc, ns * symph, dl, nullptr, nullptr);
         a.overlap = 0;
         st = launch(p, a, s_k, 1);
@@ -404,9 +409,23 @@ mimo_status_t mimo_detect_mmse_host(mimo_plan_t p, const void* H_host, const voi
         if (e == cudaSuccess) e = cudaEventRecord(p->e_out[b], s_out);
         if (e != cudaSuccess) return cuda_fail(p, e, "cudaMemcpyAsync D2H");
     }
+    // asynchronous form: mimo_plan_sync_status synchronises the host-path streams. No join into the
+    // plan's stream -- the next call orders after that stream's tail, and a join there would
+    // serialise consecutive calls (no H2D of call i+1 under the D2H of call i)
+    if (!wait) return MIMO_OK;
     for (int i = 0; i < 3; ++i)
         if ((e = cudaStreamSynchronize(p->hs[i])) != cudaSuccess) return cuda_fail(p, e, "cudaStreamSynchronize");
     return MIMO_OK;
+}
+
+mimo_status_t mimo_detect_mmse_host(mimo_plan_t p, const void* H_host, const void* y_host, float sigma2, int n_rx,
+                                    int n_layers, int n_sc, int n_sym, int qm, void* llr_host) {
+    return host_path(p, H_host, y_host, sigma2, n_rx, n_layers, n_sc, n_sym, qm, llr_host, true);
+}
+
+mimo_status_t mimo_detect_mmse_host_async(mimo_plan_t p, const void* H_host, const void* y_host, float sigma2,
+                                          int n_rx, int n_layers, int n_sc, int n_sym, int qm, void* llr_host) {
+    return host_path(p, H_host, y_host, sigma2, n_rx, n_layers, n_sc, n_sym, qm, llr_host, false);
 }
 
 mimo_status_t mimo_detect_lmmse_lu(mimo_plan_t p, const void* H, const void* y, float sigma2, int n_rx,

@@ -78,6 +78,8 @@ def load_library(path: str | None = None):
     L.mimo_detect_mmse_sv.argtypes = [vp, vp, vp, vp, i, i, i, i, i, vp, vp, vp]
     L.mimo_detect_mmse_sv.restype = i
     L.mimo_detect_mmse_host.argtypes = [vp, vp, vp, f, i, i, i, i, i, vp]
+    L.mimo_detect_mmse_host_async.argtypes = [vp, vp, vp, f, i, i, i, i, i, vp]
+    L.mimo_detect_mmse_host_async.restype = i
     L.mimo_detect_mmse_host.restype = i
     L.mimo_detect_lmmse_lu.argtypes = [vp, vp, vp, f, i, i, i, i, i, i, vp, vp, vp, ctypes.POINTER(f)]
     L.mimo_detect_lmmse_lu.restype = i
@@ -305,8 +307,10 @@ class Plan:
                                                    ctypes.c_float(bfp_scale), ptr(out), ptr(xhat), ptr(sinr)))
         return out
 
-    def detect_host(self, H, y, sigma2: float, out=None):
-        """End-to-end detect with HOST buffers (numpy or CPU tensors; pin them for overlap)."""
+    def detect_host(self, H, y, sigma2: float, out=None, wait: bool = True):
+        """End-to-end detect with HOST buffers (numpy or CPU tensors; pin them for overlap).
+        wait=False: mimo_detect_mmse_host_async -- returns at once; call sync_status() before
+        reading `out` or reusing H / y (consecutive calls overlap their transfers)."""
         import torch
         to_np = (lambda t: t.numpy() if isinstance(t, torch.Tensor) else t)
         Hn, yn = to_np(H), to_np(y)
@@ -325,10 +329,10 @@ class Plan:
             raise ValueError("out has the wrong size or is not contiguous")
         if self._fixed_stream is None:
             self._lib.mimo_plan_set_stream(self._h, ctypes.c_void_p(self._stream_ptr()))
-        st = self._lib.mimo_detect_mmse_host(self._h, Hn.ctypes.data_as(ctypes.c_void_p),
-                                             yn.ctypes.data_as(ctypes.c_void_p), ctypes.c_float(sigma2),
-                                             self.n_rx, self.n_layers, n_sc, n_sym, self.qm,
-                                             on.ctypes.data_as(ctypes.c_void_p))
+        fn = self._lib.mimo_detect_mmse_host if wait else self._lib.mimo_detect_mmse_host_async
+        st = fn(self._h, Hn.ctypes.data_as(ctypes.c_void_p), yn.ctypes.data_as(ctypes.c_void_p),
+                ctypes.c_float(sigma2), self.n_rx, self.n_layers, n_sc, n_sym, self.qm,
+                on.ctypes.data_as(ctypes.c_void_p))
         self._check(st)
         return out
 

@@ -183,6 +183,25 @@ def test_host_path_matches_device_path():
     assert np.array_equal(out, g["llr"])
 
 
+@pytest.mark.parametrize("k", [2, 3, 5])
+def test_host_path_async_stream_of_calls(k):
+    """mimo_detect_mmse_host_async: three back-to-back calls on different TTIs (own pinned buffers),
+    one plan sync, every result equal to the device path's."""
+    import torch
+    from paper_2510_07843_b200 import mimo
+    ws = [synth.generate(k, n_slots=3 if k == 5 else 4, seed=50 + i) for i in range(3)]
+    w0 = ws[0]
+    plan = mimo.Plan(w0.n_rx, w0.n_layers, w0.qm, sc_per_h=w0.sc_per_h, llr_dtype=w0.llr)
+    pinned = [(torch.from_numpy(w.H).pin_memory(), torch.from_numpy(w.y).pin_memory()) for w in ws]
+    outs = [torch.empty(plan.shapes(w.n_sc, w.n_sym)["llr"], dtype=plan.llr_dtype).pin_memory() for w in ws]
+    for (H, y), w, o in zip(pinned, ws, outs):
+        plan.detect_host(H, y, float(w.sigma2), out=o, wait=False)
+    assert plan.sync_status() == 0
+    for w, o in zip(ws, outs):
+        g = parity.run_gpu(w, xhat=False, sinr=False)
+        assert np.array_equal(o.numpy(), g["llr"])
+
+
 def test_host_path_c5_chunked():
     w = synth.generate(5, n_slots=6)
     g = parity.run_gpu(w, xhat=False, sinr=False)
