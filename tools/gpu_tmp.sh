@@ -1,3 +1,4 @@
 #!/bin/bash
-timeout 600 python -m pytest tests/test_parity_gpu.py tests/test_api_gpu.py -q -x 2>&1 | tail -2
-timeout 400 python bench.py --config 2 2>/dev/null | tail -1 > gpurun_out/bench_c2.json; python -c "import json; d=json.loads(open('gpurun_out/bench_c2.json').read()); print(d['ms_per_step'], d['e2e'], d['cpu_baseline'])"
+for i in 1 2 3 4; do
+BENCH_DEBUG_E2E=1 timeout 400 python bench.py 2>gpurun_out/err.txt | tail -1 > gpurun_out/b.json; grep "e2e async" gpurun_out/err.txt; python -c "import json; d=json.loads(open('gpurun_out/b.json').read()); print(d['ms_per_step']*1e3, d['e2e']['ms_per_step'], d['e2e']['sync_call_ms_per_step'])"
+done
