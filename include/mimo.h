@@ -235,7 +235,8 @@ mimo_status_t mimo_detect_mmse_bfp(mimo_plan_t plan, const void* H, const void* 
  * graph: reserve before capturing. Errors: INVALID_ARG, CUDA, OOM. */
 mimo_status_t mimo_plan_reserve(mimo_plan_t plan, int n_sc, int n_sym);
 
-/* Synchronise the plan's stream, return the number of units flagged by the
+/* Synchronise the plan's stream (and the host-buffer path's streams, which
+ * mimo_detect_mmse_host_async leaves running), return the number of units flagged by the
  * Cholesky guard since the previous call (and reset the count). Returns
  * MIMO_ERR_NOT_PD if that number is > 0, MIMO_ERR_CUDA on a sticky CUDA
  * error. n_failed_units may be NULL. */
