@@ -444,6 +444,8 @@ def run_ours(args, k):
     if rank == 0 and world == 1 and not args.no_cpu_baseline and ybfp is None:
         import oracle
         cpu = oracle_rate(w, args.cpu_seconds, oracle.max_threads())
+        one = oracle_rate(w, min(2.0, args.cpu_seconds), 1)  # also on one thread
+        cpu["single_thread"] = {"value": one["value"], "unit": "RE/s", "sample": one["sample"]}
 
     if world > 1:
         dist.barrier()

@@ -1,2 +1,2 @@
 #!/bin/bash
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -6
+timeout 400 python bench.py 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['cpu_baseline'])"
