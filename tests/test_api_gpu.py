@@ -153,3 +153,40 @@ def test_overlap_mode_parity(k):
     plan = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, llr_dtype=w.llr, overlap_calls=True)
     g = parity.run_gpu(w, plan=plan)
     parity.compare(w, g)
+
+
+def _call_sv(plan, H, y, s2v, out, nr=4, nl=4, nsc=32, nsym=14, qm=4):
+    p = lambda t: ctypes.c_void_p(t if isinstance(t, int) else t.data_ptr()) if t is not None else None
+    return plan._lib.mimo_detect_mmse_sv(plan._h, p(H), p(y), p(s2v), nr, nl, nsc, nsym, qm, p(out), None, None)
+
+
+def test_sigma2_array_errors(setup):
+    """mimo_detect_mmse_sv: null / host / misaligned sigma2_v and bad dims are INVALID_ARG."""
+    import torch
+    plan, H, y, out, _ = setup
+    s2v = torch.full((1,), 0.1, device="cuda")
+    assert _call_sv(plan, H, y, s2v, out) == mimo.MIMO_OK
+    assert plan.sync_status() == 0
+    assert _call_sv(plan, H, y, None, out) == mimo.MIMO_ERR_INVALID_ARG
+    host = np.full(1, 0.1, np.float32)
+    assert _call_sv(plan, H, y, host.ctypes.data, out) == mimo.MIMO_ERR_INVALID_ARG
+    assert _call_sv(plan, H, y, s2v.data_ptr() + 2, out) == mimo.MIMO_ERR_INVALID_ARG
+    assert _call_sv(plan, H, y, s2v, out, nsym=13) == mimo.MIMO_ERR_INVALID_ARG
+    with pytest.raises(ValueError):  # binding: one variance per H time block
+        plan.detect(H, y, torch.full((2,), 0.1, device="cuda"))
+
+
+def test_host_async_errors_and_empty(setup):
+    """mimo_detect_mmse_host_async validates like the synchronous call; an empty grid is a no-op."""
+    plan, H, y, out, w = setup
+    f = plan._lib.mimo_detect_mmse_host_async
+    llr = np.empty((14, 32, 4, 4), np.float32)
+    args = lambda s2, nsym: (plan._h, w.H.ctypes.data_as(ctypes.c_void_p), w.y.ctypes.data_as(ctypes.c_void_p),
+                             ctypes.c_float(s2), 4, 4, 32, nsym, 4, llr.ctypes.data_as(ctypes.c_void_p))
+    assert f(*args(-1.0, 14)) == mimo.MIMO_ERR_INVALID_ARG
+    assert f(*args(0.1, 13)) == mimo.MIMO_ERR_INVALID_ARG
+    assert f(*args(0.1, 0)) == mimo.MIMO_OK
+    assert f(*args(float(w.sigma2), 14)) == mimo.MIMO_OK
+    assert plan.sync_status() == 0
+    ref = plan.detect_host(w.H, w.y, float(w.sigma2))
+    assert np.array_equal(llr, ref)
