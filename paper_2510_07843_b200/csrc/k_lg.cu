@@ -579,9 +579,11 @@ cudaError_t prepare() {
     }
 
 const KernelEntry kEntries[] = {
-    // C4 default: y and H of the CTA's 8 units as one TMA tensor box each (lg3h), per-RE apply as
-    // packed FFMA2 (HT = 2)
-    KernelEntry{"lg3hp_16x8_q8_f16", 16, 8, 8, 1, 14, kLlrF16, 32, 1, launch3<16, 8, 8, kLlrF16, 2, 0, 2>,
+    // C4 default: y and H of the CTA's units as one TMA tensor box each (lg3h), per-RE apply as
+    // packed FFMA2 (HT = 2), 4 warps = 16 units per CTA (78.4 us; 2 warps 79.8, 1: 84.1, 6: 94.2, 8: 81.4)
+    KernelEntry{"lg3hp_16x8_q8_f16", 16, 8, 8, 1, 14, kLlrF16, 32, 1, launch3<16, 8, 8, kLlrF16, 4, 0, 2>,
+                prepare3<16, 8, 8, kLlrF16, 4, 0, 2>},
+    KernelEntry{"lg3hp_w2", 16, 8, 8, 1, 14, kLlrF16, 32, 1, launch3<16, 8, 8, kLlrF16, 2, 0, 2>,
                 prepare3<16, 8, 8, kLlrF16, 2, 0, 2>},
     KernelEntry{"lg3h_16x8_q8_f16", 16, 8, 8, 1, 14, kLlrF16, 32, 1, launch3<16, 8, 8, kLlrF16, 2, 0, 1>,
                 prepare3<16, 8, 8, kLlrF16, 2, 0, 1>},

@@ -13,7 +13,7 @@ pytestmark = pytest.mark.gpu
 C5_VARIANTS = ["big4_64x16_q6_i8", "big4c_64x16_q6_i8", "big4e8_64x16_q6_i8", "big5_64x16_q6_i8", "big5e8_64x16_q6_i8", "big8_64x16_q6_i8", "big11_64x16_q6_i8", "big8e6_64x16_q6_i8", "big11e6_64x16_q6_i8",
                "big3_64x16_q6_i8", "big2_64x16_q6_i8",
                "big_64x16_q6_i8"]
-C4_VARIANTS = ["lg3h_16x8_q8_f16", "lg3hp_16x8_q8_f16", "lg3_16x8_q8_f16", "lg3_16x8_q8_f16_w1", "lg_16x8_q8_f16"]
+C4_VARIANTS = ["lg3h_16x8_q8_f16", "lg3hp_16x8_q8_f16", "lg3hp_w2", "lg3_16x8_q8_f16", "lg3_16x8_q8_f16_w1", "lg_16x8_q8_f16"]
 C3_VARIANTS = ["stream_8x4_q6_i8_pf3", "split_8x4_q6_i8", "prb_8x4_q6_i8"]
 
 
