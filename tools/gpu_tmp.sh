@@ -1,3 +1,3 @@
 #!/bin/bash
-timeout 900 python -m pytest tests -m gpu -q -x -k "4 or c4 or lg" 2>&1 | tail -2
-timeout 300 bash tools/bench_variants.sh 4 lg3hp_16x8_q8_f16 lg3hp_w2
+for k in stream_8x4_q6_i8 stream_u32 stream_u64 stream_8x4_q6_i8 stream_u32 stream_u64; do echo $k; timeout 60 python tools/dbg_time.py $k 3 20 1 2>&1 | tail -1; done
+timeout 300 bash tools/bench_variants.sh 3 stream_8x4_q6_i8 stream_u32
