@@ -1,19 +1,29 @@
 #!/usr/bin/env python
 """Benchmark of the B200 per-RE MMSE detector + max-log demapper.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 5] [--impl ours|reference]
+                    [--emulate 2 4 8] [--kernel NAME]
 
 Metric (BASELINE.json): MIMO-detected REs/s (and LLR Gbit/s) per B200 vs roofline.
 A "step" is one mimo_detect_mmse call over one full batch of the configured
-workload (default configs[1] = C2: 4x4 16-QAM, 3276 sc x 14 sym x 10 slots),
-i.e. every hot-path row a1-a7 for every RE. Inputs are device-resident and
-rotated over enough buffer sets that the working set exceeds 3x L2; the K timed
-steps are replayed from CUDA graphs and timed with CUDA events on the launching
-stream. Multi-GPU (torchrun): weak scaling, rank r detects its own C2-sized
-block of slots; time = max over ranks.
+workload -- every hot-path row a1-a7 for every RE. The default workload is the
+largest config, configs[4] = C5 (64 rx x 16 layers, 64-QAM, 3276 sc x 14 sym x
+40 slots, int8 LLRs; BASELINE.json "sharded by slot across 8 GPUs"); --config k
+selects another. Inputs are device-resident and rotated over enough buffer sets
+that the working set exceeds 3x L2; the K timed steps are replayed from CUDA
+graphs and timed with CUDA events on the launching stream.
+
+Multi-GPU (torchrun, N ranks): STRONG scaling of the same configured job. Every
+rank draws the whole seeded job and detects its block of the 2-D slot x PRB
+partition (shard.block_partition: C5 over 8 GPUs = 5 slots each); there is no
+collective on the data path. Timing: barrier, graph replays, synchronize,
+barrier; value = job REs x K / max over ranks of the CUDA-event time (the host
+wall clock over the same region is reported beside it). --emulate N runs the N
+shards one after another on a single GPU, reports their times and checks that
+the reassembled LLRs are bit-identical to the unsharded call.
 
 `e2e` times the same metric through the host-buffer C-ABI call
-(mimo_detect_mmse_host: pinned H/y -> device -> kernel -> LLRs back), and
+(mimo_detect_mmse_host_async: pinned H/y -> device -> kernels -> LLRs back), and
 `cpu_baseline` / `--impl reference` time the fp64 oracle (test infrastructure,
 deliberately slow) on a bounded sample on the host cores.
 """
@@ -39,7 +49,12 @@ METRIC = "MIMO-detected REs/s per B200 (LLR Gbit/s alongside) vs roofline"
 FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
 FALLBACK_BF16_TFLOPS = 2250.0  # B200_PROFILING.md nominal dense bf16
 TF32_PER_BF16 = 1.1 / 2.25   # B200_PROFILING.md nominal dense tf32 / bf16
-TC_KERNELS = ("big3", "big4", "big5", "big8", "big11")  # kernels whose row a6 runs on tcgen05 (R21)
+TC_KERNELS = ("big8", "c5")  # kernels whose row a6 runs on tcgen05 (R21, R28)
+# The paper's own CPU figure: a 4x4 LMMSE detection of one 720-subcarrier,
+# 14-symbol TTI in <= 0.03 ms on an Intel i9-14900KF with AVX2 -- another CPU and workload.
+PAPER_CPU_CONTEXT = {"value": 720 * 14 / 0.03e-3, "unit": "RE/s", "hardware": "Intel Core i9-14900KF, AVX2",
+                     "workload": "4x4, 60 RB x 12 = 720 subcarriers x 14 symbols, one TTI, <= 0.03 ms",
+                     "source": "PAPER.md:117, :123", "note": "context only: different CPU and workload"}
 
 
 def parse():
@@ -47,8 +62,11 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=50)
-    ap.add_argument("--config", default="2",
-                    help="BASELINE config 1..5 (default 2 = configs[1], the headline), P (paper shape) or all")
+    ap.add_argument("--config", default="5",
+                    help="BASELINE config 1..5 (default 5 = configs[4], the largest), P (paper shape) or all")
+    ap.add_argument("--kernel", default=None, help="kernel specialisation by name (default: the plan's default)")
+    ap.add_argument("--emulate", type=int, nargs="*", default=[],
+                    help="one-GPU emulation of N-GPU strong scaling (each N: shards run sequentially)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=60)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -83,6 +101,16 @@ def measured_peaks() -> dict:
         return dict(hbm_gbs=float(d["hbm_gbs"]), src="measured", sm_max_mhz=float(d.get("sm_max_mhz", 1965.0)),
                     bf16_tflops=float(d.get("bf16_tflops", FALLBACK_BF16_TFLOPS)))
     return dict(hbm_gbs=FALLBACK_HBM_GBS, src="fallback", sm_max_mhz=1965.0, bf16_tflops=FALLBACK_BF16_TFLOPS)
+
+
+def kernel_share(args, k) -> dict | None:
+    """Share of the step of the dominant kernel, from the committed ncu launch list (profiles/)."""
+    p = os.path.join(ROOT, "profiles", "kernel_share.json")
+    if not os.path.exists(p) or args.kernel:
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    return d.get(synth.CONFIGS[k]["name"])
 
 
 def ncu_traffic(k) -> float | None:
@@ -217,7 +245,7 @@ def run_reference(args, k):
     c = synth.CONFIGS[k]
     line = {"impl": "reference", "metric": METRIC, "value": v,
             "unit": "RE/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": dt * 1e3 / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE config shapes)",
             "config": workload_desc(k),
             "llr_gbit_s": v * c["n_layers"] * c["qm"] / 1e9,
@@ -235,147 +263,90 @@ def largest_divisor_le(n: int, cap: int) -> int:
     return 1
 
 
-def run_ours(args, k):
+class Shard:
+    """One plan + rotating device buffer sets for one block of the configured job."""
+
+    def __init__(self, mimo, w, Hn, yn, n_sc, n_slots, dev, k, args, overlap, ybfp=None):
+        import torch
+        self.n_sc, self.n_slots, self.n_sym = n_sc, n_slots, n_slots * synth.SYM_PER_SLOT
+        self.b = synth.config_algorithmic_bytes(k, n_sc=n_sc, n_slots=n_slots)
+        self.bfp = args.bfp
+        if ybfp is not None:  # NEXT-4: y crosses HBM as BFP blocks (reading R25)
+            self.b = dict(self.b, y=int(ybfp.nbytes), total=self.b["H"] + int(ybfp.nbytes) + self.b["llr"])
+        self.plan = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, llr_dtype=w.llr, device=dev.index,
+                              overlap_calls=overlap, kernel=args.kernel)
+        self.plan.reserve(n_sc, self.n_sym)
+        l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+        n_sets = max(2, math.ceil(3 * l2 / self.b["total"]))  # working set >= 3x L2: every step streams HBM
+        free = torch.cuda.mem_get_info(dev)[0]
+        self.n_sets = int(min(n_sets, max(2, (free * 0.4) // self.b["total"])))
+        H0 = torch.from_numpy(Hn).to(dev)
+        y0 = torch.from_numpy(yn if ybfp is None else ybfp).to(dev)
+        self.sets = [(H0.clone(), y0.clone(),
+                      torch.empty(self.plan.shapes(n_sc, self.n_sym)["llr"], dtype=self.plan.llr_dtype, device=dev))
+                     for _ in range(self.n_sets)]
+        del H0, y0
+        self.s2 = float(w.sigma2)
+        self.l2 = l2
+
+    def step(self, i):
+        H, y, out = self.sets[i % self.n_sets]
+        if not self.bfp:
+            self.plan.detect(H, y, self.s2, out=out)
+        else:
+            self.plan.detect_bfp(H, y, self.s2, n_sym=self.n_sym, n_sc=self.n_sc, iq_width=self.bfp, out=out)
+
+    def graph(self, S, stream):
+        import torch
+        with torch.cuda.stream(stream):
+            for i in range(3):  # eager warm-up (module load, first launches)
+                self.step(i)
+        stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            with torch.cuda.graph(g, stream=stream):
+                for i in range(S):
+                    self.step(i)
+        stream.synchronize()
+        return g
+
+
+def timed_replays(g, stream, K, S, W, barrier=None):
+    """W warm-up steps (>= 0.3 s), then K steps as K/S graph replays bracketed by barrier +
+    synchronize; CUDA events on the launching stream. Returns (elapsed_ms, wall_s, per-replay us)."""
     import torch
-    import torch.distributed as dist
-    from paper_2510_07843_b200 import mimo
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.gpus != world and world > 1:
-        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-
-    c = synth.CONFIGS[k]
-    base_seed = 1000 + (k if isinstance(k, int) else 0)
-    s0, s1 = shard.weak_slots(c["n_slots"], rank)
-    w = synth.generate(k, seed=shard.shard_seed(base_seed, rank))
-    b = synth.config_algorithmic_bytes(k)
-    ybfp = None
-    if args.bfp:  # NEXT-4: y crosses HBM as BFP blocks (reading R25); algorithmic y bytes shrink accordingly
-        ybfp = synth.bfp_compress(w.y, args.bfp)
-        b = dict(b, y=int(ybfp.nbytes), total=b["H"] + int(ybfp.nbytes) + b["llr"])
-    plan = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, llr_dtype=w.llr, device=local,
-                     overlap_calls=bool(args.overlap))
-    plan1 = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, llr_dtype=w.llr, device=local)
-
-    # rotating buffer sets: working set >= 3x L2 so every step streams from HBM
-    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
-    n_sets = max(2, math.ceil(3 * l2 / b["total"]))
-    free = torch.cuda.mem_get_info(dev)[0]
-    n_sets = int(min(n_sets, max(2, (free * 0.5) // b["total"])))
-    H0 = torch.from_numpy(w.H).to(dev)
-    y0 = torch.from_numpy(w.y if ybfp is None else ybfp).to(dev)
-    sets = []
-    for i in range(n_sets):
-        sets.append((H0.clone(), y0.clone(),
-                     torch.empty(plan.shapes(w.n_sc, w.n_sym)["llr"], dtype=plan.llr_dtype, device=dev)))
-    del H0, y0
-    s2 = float(w.sigma2)
-    stream = torch.cuda.Stream(device=dev)
-
-    def step(i):
-        H, y, out = sets[i % n_sets]
-        if ybfp is None:
-            plan.detect(H, y, s2, out=out)
-        else:
-            plan.detect_bfp(H, y, s2, n_sym=w.n_sym, n_sc=w.n_sc, iq_width=args.bfp, out=out)
-
-    if args.profile:
-        with torch.cuda.stream(stream):
-            for i in range(args.warmup + args.steps):
-                step(i)
-        torch.cuda.synchronize(dev)
-        assert plan.sync_status() == 0
-        if rank == 0:
-            print(json.dumps({"profile_run": True, "kernel": plan.kernel_name,
-                              "launches": args.warmup + args.steps}), flush=True)
-        return
-
-    # CUDA graph of S steps (S | K), replayed K/S times in the timed region
-    K, W = args.steps, max(3, args.warmup)
-    S = largest_divisor_le(K, 256)
     with torch.cuda.stream(stream):
-        for i in range(3):       # eager warm-up (module load, first launches)
-            step(i)
-    stream.synchronize()
-    g = torch.cuda.CUDAGraph()
+        t_end = time.perf_counter() + 0.3
+        done = 0
+        while done < W or time.perf_counter() < t_end:
+            g.replay()
+            done += S
+        stream.synchronize()
+    if barrier:
+        barrier()
+    torch.cuda.synchronize()
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(K // S + 1)]
+    t0 = time.perf_counter()
     with torch.cuda.stream(stream):
-        with torch.cuda.graph(g, stream=stream):
-            for i in range(S):
-                step(i)
-    stream.synchronize()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        evs[0].record(stream)
+        for r in range(K // S):
+            g.replay()
+            evs[r + 1].record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    if barrier:
+        barrier()
+    per = sorted(evs[r].elapsed_time(evs[r + 1]) * 1e3 / S for r in range(K // S))
+    return evs[0].elapsed_time(evs[-1]), wall, per
 
-    sampler = ClockSampler(local)
-    with sampler:
-        with torch.cuda.stream(stream):
-            # untimed warm-up: W steps, and at least ~0.3 s so clocks settle under load
-            t_end = time.perf_counter() + 0.3
-            done = 0
-            while done < W or time.perf_counter() < t_end:
-                g.replay()
-                done += S
-            stream.synchronize()
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize(dev)
-        evs = [torch.cuda.Event(enable_timing=True) for _ in range(K // S + 1)]
-        with torch.cuda.stream(stream):
-            ev0.record(stream)
-            evs[0].record(stream)
-            for r in range(K // S):
-                g.replay()
-                evs[r + 1].record(stream)
-            ev1.record(stream)
-        torch.cuda.synchronize(dev)
-        if world > 1:
-            dist.barrier()
-    elapsed_ms = ev0.elapsed_time(ev1)
-    per_replay_us = sorted(evs[r].elapsed_time(evs[r + 1]) * 1e3 / S for r in range(K // S))
-    pct = lambda q: per_replay_us[min(len(per_replay_us) - 1, int(q * len(per_replay_us)))]
-    step_dist = {"p10": pct(0.1), "p50": pct(0.5), "p90": pct(0.9), "replays": len(per_replay_us),
-                 "steps_per_replay": S}
-    n_failed = plan.sync_status()
 
-    # context: the same steps with calls serialised (no PDL overlap) -> single-call device time
-    def step1(i):
-        H, y, out = sets[i % n_sets]
-        if ybfp is None:
-            plan1.detect(H, y, s2, out=out)
-        else:
-            plan1.detect_bfp(H, y, s2, n_sym=w.n_sym, n_sc=w.n_sc, iq_width=args.bfp, out=out)
-    g1 = torch.cuda.CUDAGraph()
-    with torch.cuda.stream(stream):
-        step1(0)
-        with torch.cuda.graph(g1, stream=stream):
-            for i in range(S):
-                step1(i)
-        g1.replay()
-        ev0.record(stream)
-        g1.replay()
-        ev1.record(stream)
-    stream.synchronize()
-    single_us = ev0.elapsed_time(ev1) * 1e3 / S
-    assert n_failed == 0, f"{n_failed} units failed the Cholesky guard"
-    t_max_ms = shard.max_over_ranks(elapsed_ms, device=dev)
-    n_re_all = b["n_re"] * K * world
-    value = n_re_all / (t_max_ms / 1e3)
-    per_launch_s = (elapsed_ms / 1e3) / (K * plan.launches_per_call)
-    peaks = measured_peaks()
-    fl = synth.config_algorithmic_flops(k)
-    step_s = (t_max_ms / 1e3) / K
-    # FP32 SIMT peak: 148 SMs x 128 lanes x 2 flop x max SM clock
+def roofline_of(k, plan_kernel, b, fl, step_s, peaks, dev):
+    import torch
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    fp32_tflops = n_sm * 128 * 2 * peaks["sm_max_mhz"] * 1e6 / 1e12
+    fp32_tflops = n_sm * 128 * 2 * peaks["sm_max_mhz"] * 1e6 / 1e12  # 148 SMs x 128 lanes x 2 x max clock
     t_hbm = b["total"] / (peaks["hbm_gbs"] * 1e9)
-    # Which pipe runs row a6 (x~ = W~ y): tensor-core kernels (3-pass TF32, R21) move the
-    # apply flops off the FP32 SIMT pipe, so their bound is max(HBM, SIMT setup+demap, TF32 tensor).
-    tensor_apply = plan.kernel_name.startswith(TC_KERNELS)
+    # row a6 on tcgen05 (3-pass split products, DESIGN.md R21/R28): its flops leave the FP32 pipe
+    tensor_apply = plan_kernel.startswith(TC_KERNELS)
     simt_flops = fl["setup"] + fl["demap"] if tensor_apply else fl["total"]
     t_alu = simt_flops / (fp32_tflops * 1e12)
     tf32_tflops = peaks["bf16_tflops"] * TF32_PER_BF16
@@ -392,91 +363,220 @@ def run_ours(args, k):
         ach = b["total"] / step_s / 1e9
         roof = {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": ach / peaks["hbm_gbs"], "peak_src": peaks["src"] + " (MEASURED_PEAKS.json hbm_gbs)"}
-    roof.update({"traffic": ncu_traffic(k), "algorithmic_bytes_per_step": b["total"],
-                 "t_roof_us": max(t_hbm, t_alu, t_tc) * 1e6, "step_us": step_s * 1e6,
-                 "apply_pipe": "tcgen05 kind::tf32 x3 (R21)" if tensor_apply else "FP32 SIMT",
-                 "t_hbm_us": t_hbm * 1e6, "t_simt_us": t_alu * 1e6, "t_tensor_us": t_tc * 1e6,
-                 "launches_per_step": plan.launches_per_call})
-    achieved = b["total"] / per_launch_s / 1e9
+    roof.update({"algorithmic_bytes_per_step": b["total"], "t_roof_us": max(t_hbm, t_alu, t_tc) * 1e6,
+                 "step_us": step_s * 1e6, "apply_pipe": "tcgen05 (3-pass split, R21/R28)" if tensor_apply else "FP32 SIMT",
+                 "t_hbm_us": t_hbm * 1e6, "t_simt_us": t_alu * 1e6, "t_tensor_us": t_tc * 1e6})
+    return roof
+
+
+def emulate_shards(mimo, w, k, args, dev, n_emul, full_llr):
+    """One-GPU emulation of an N-GPU strong-scaling run: run every rank's block of
+    the 2-D partition sequentially on this device, time each (CUDA graphs, events), and check that
+    the reassembled LLRs are bit-identical to the unsharded call. The emulated N-GPU step time is
+    the max over shards (the ranks would run concurrently on their own GPUs)."""
+    import torch
+    n_prb = w.n_sc // shard.SC_PER_PRB
+    try:
+        blocks = shard.block_partition(w.n_slots, n_prb, n_emul)
+    except ValueError as e:
+        return {"n": n_emul, "unavailable": str(e)}
+    full = torch.empty_like(full_llr)
+    stream = torch.cuda.Stream(device=dev)
+    shard_us = []
+    K = max(8, min(args.steps, 64))
+    S = largest_divisor_le(K, 64)
+    for blk in blocks:
+        Hb, yb, nsc, nsl = shard.shard_arrays(w.H, w.y, w.n_slots, w.sc_per_h, blk)
+        sh = Shard(mimo, w, Hb, yb, nsc, nsl, dev, k, args, overlap=bool(args.overlap))
+        g = sh.graph(S, stream)
+        el, _, _ = timed_replays(g, stream, K, S, 3)
+        shard_us.append(el * 1e3 / K)
+        H, y, out = sh.sets[0]
+        with torch.cuda.stream(stream):
+            sh.plan.detect(H, y, sh.s2, out=out)
+        stream.synchronize()
+        shard.place_block(full, out, blk)
+        del sh, g
+        torch.cuda.empty_cache()
+    t = max(shard_us)
+    return {"n": n_emul, "grid": list(blocks[0]["grid"]), "shard_step_us": shard_us, "step_us": t,
+            "value": w.n_re / (t * 1e-6), "unit": "RE/s", "steps_per_shard": K,
+            "bit_identical": bool(torch.equal(full, full_llr))}
+
+
+def run_ours(args, k):
+    import torch
+    import torch.distributed as dist
+    from paper_2510_07843_b200 import mimo
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.gpus != world and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    barrier = (lambda: dist.barrier()) if world > 1 else None
+
+    c = synth.CONFIGS[k]
+    w = synth.generate(k)  # the whole configured job, one seed: every rank draws the same job
+    n_prb = w.n_sc // shard.SC_PER_PRB
+    # strong scaling: rank r detects its block of the 2-D slot x PRB partition of THIS job (no
+    # collective on the data path); a job too small to split (C1) runs as replicas
+    try:
+        blk = shard.block_partition(w.n_slots, n_prb, world)[rank] if world > 1 else None
+        scaling = "strong"
+    except ValueError:
+        blk, scaling = None, "replicas"
+    if blk is not None:
+        Hn, yn, n_sc_r, n_slots_r = shard.shard_arrays(w.H, w.y, w.n_slots, w.sc_per_h, blk)
+    else:
+        Hn, yn, n_sc_r, n_slots_r = w.H, w.y, w.n_sc, w.n_slots
+    ybfp = synth.bfp_compress(yn, args.bfp) if args.bfp else None
+    sh = Shard(mimo, w, Hn, yn, n_sc_r, n_slots_r, dev, k, args, overlap=bool(args.overlap), ybfp=ybfp)
+    plan = sh.plan
+    stream = torch.cuda.Stream(device=dev)
+
+    if args.profile:
+        with torch.cuda.stream(stream):
+            for i in range(args.warmup + args.steps):
+                sh.step(i)
+        torch.cuda.synchronize(dev)
+        assert plan.sync_status() == 0
+        if rank == 0:
+            print(json.dumps({"profile_run": True, "kernel": plan.kernel_name,
+                              "launches": args.warmup + args.steps}), flush=True)
+        return
+
+    K, W = args.steps, max(3, args.warmup)
+    S = largest_divisor_le(K, 256)
+    g = sh.graph(S, stream)
+    sampler = ClockSampler(local)
+    with sampler:
+        elapsed_ms, wall_s, per_replay_us = timed_replays(g, stream, K, S, W, barrier)
+    pct = lambda q: per_replay_us[min(len(per_replay_us) - 1, int(q * len(per_replay_us)))]
+    step_dist = {"p10": pct(0.1), "p50": pct(0.5), "p90": pct(0.9), "replays": len(per_replay_us),
+                 "steps_per_replay": S}
+    n_failed = plan.sync_status()
+    assert n_failed == 0, f"{n_failed} units failed the Cholesky guard"
+
+    # context: the same steps with calls serialised (no PDL overlap) -> single-call device time
+    sh1 = Shard.__new__(Shard)
+    sh1.__dict__.update(sh.__dict__)
+    sh1.plan = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, llr_dtype=w.llr, device=local,
+                         kernel=args.kernel)
+    sh1.plan.reserve(n_sc_r, sh.n_sym)
+    g1 = sh1.graph(S, stream)
+    el1, _, _ = timed_replays(g1, stream, S, S, 1)
+    single_us = el1 * 1e3 / S
+    del g1
+
+    t_max_ms = shard.max_over_ranks(elapsed_ms, device=dev)
+    wall_max = shard.max_over_ranks(wall_s, device=dev)
+    n_re_job = synth.config_algorithmic_bytes(k)["n_re"]
+    n_re_all = n_re_job * K * (world if scaling == "replicas" else 1)
+    value = n_re_all / (t_max_ms / 1e3)
+    peaks = measured_peaks()
+    step_s = (t_max_ms / 1e3) / K
+    b = sh.b
+    fl = synth.config_algorithmic_flops(k, n_sc=n_sc_r, n_slots=n_slots_r)
+    roof = roofline_of(k, plan.kernel_name, b, fl, step_s, peaks, dev)
+    roof.update({"traffic": ncu_traffic(k) if world == 1 and not args.bfp else None,
+                 "launches_per_step": plan.launches_per_call, "serialised_call_us": single_us,
+                 "serialised_frac": roof["t_roof_us"] / single_us})
+    dk = kernel_share(args, k)
+    if dk:
+        roof["dominant_kernel"] = dk
     clocks = sampler.result()
 
-    # e2e: host buffers through mimo_detect_mmse_host (H2D + kernel + D2H per step)
+    # e2e: the public host-buffer C-ABI call (mimo_detect_mmse_host_async), pinned host buffers:
+    # every step copies its H and y host->device and its LLRs device->host inside the timed region
     e2e = None
     if not args.no_e2e and ybfp is None:
-        Hh = torch.from_numpy(w.H).pin_memory()
-        yh = torch.from_numpy(w.y).pin_memory()
-        lh = torch.empty(plan.shapes(w.n_sc, w.n_sym)["llr"], dtype=plan.llr_dtype).pin_memory()
+        Hh = torch.from_numpy(Hn).pin_memory()
+        yh = torch.from_numpy(yn).pin_memory()
+        lh = torch.empty(plan.shapes(n_sc_r, sh.n_sym)["llr"], dtype=plan.llr_dtype).pin_memory()
         for _ in range(2):
-            plan.detect_host(Hh, yh, s2, out=lh)
-        # context: one synchronous call per step (each call fills and drains its own pipeline)
-        if world > 1:
-            dist.barrier()
+            plan.detect_host(Hh, yh, sh.s2, out=lh)
+        if barrier:
+            barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            plan.detect_host(Hh, yh, s2, out=lh)
+            plan.detect_host(Hh, yh, sh.s2, out=lh)
         dt_sync = shard.max_over_ranks(time.perf_counter() - t0, device=dev)
-        # the e2e number: a stream of TTIs through the asynchronous call -- every step still copies its
-        # inputs from pinned host memory and its LLRs back; the plan is synchronised inside the timed
-        # region, so all copies of all steps are included
-        for _ in range(3):  # warm-up: sizes the asynchronous path's (larger-chunk) staging ring
-            plan.detect_host(Hh, yh, s2, out=lh, wait=False)
+        for _ in range(3):
+            plan.detect_host(Hh, yh, sh.s2, out=lh, wait=False)
         plan.sync_status()
-        if world > 1:
-            dist.barrier()
+        if barrier:
+            barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            plan.detect_host(Hh, yh, s2, out=lh, wait=False)
-        t_enq = time.perf_counter() - t0
+            plan.detect_host(Hh, yh, sh.s2, out=lh, wait=False)
         plan.sync_status()
-        dt = time.perf_counter() - t0
-        if os.environ.get("BENCH_DEBUG_E2E"):
-            print(f"e2e async: enqueue {t_enq * 1e3:.2f} ms, total {dt * 1e3:.2f} ms for {args.e2e_steps} steps",
-                  file=sys.stderr, flush=True)
-        dt = shard.max_over_ranks(dt, device=dev)
-        e2e = {"value": b["n_re"] * args.e2e_steps * world / dt, "unit": "RE/s",
+        dt = shard.max_over_ranks(time.perf_counter() - t0, device=dev)
+        e2e = {"value": n_re_job * args.e2e_steps * (world if scaling == "replicas" else 1) / dt, "unit": "RE/s",
                "h2d_bytes_per_step": b["H"] + b["y"], "d2h_bytes_per_step": b["llr"],
                "ms_per_step": dt * 1e3 / args.e2e_steps,
                "path": "mimo_detect_mmse_host_async per step + one plan sync (pinned host buffers, "
                        "3-stream slot-chunk pipeline; consecutive steps overlap their transfers)",
-               "sync_call_ms_per_step": dt_sync * 1e3 / args.e2e_steps}
+               "sync_call_ms_per_step": dt_sync * 1e3 / args.e2e_steps,
+               "bytes_note": "per rank" if world > 1 else "whole job"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and ybfp is None:
         import oracle
         cpu = oracle_rate(w, args.cpu_seconds, oracle.max_threads())
-        one = oracle_rate(w, min(2.0, args.cpu_seconds), 1)  # also on one thread
-        cpu["single_thread"] = {"value": one["value"], "unit": "RE/s", "sample": one["sample"]}
+        one = oracle_rate(w, min(3.0, args.cpu_seconds), 1)  # SURVEY 8(d): also on one thread
+        cpu["single_thread"] = {"value": one["value"], "unit": "RE/s", "cores": 1, "sample": one["sample"]}
+        cpu["paper_context"] = PAPER_CPU_CONTEXT
 
-    if world > 1:
-        dist.barrier()
+    emul = None
+    if world == 1 and args.emulate and ybfp is None:
+        H, y, out = sh.sets[0]
+        with torch.cuda.stream(stream):
+            plan.detect(H, y, sh.s2, out=out)
+        stream.synchronize()
+        full_llr = out.clone()
+        emul = [emulate_shards(mimo, w, k, args, dev, n, full_llr) for n in args.emulate]
+
+    if barrier:
+        barrier()
     if rank != 0:
         dist.destroy_process_group()
         return
     cfg = workload_desc(k)
-    cfg.update({"global_slots": c["n_slots"] * world, "slots_per_gpu": c["n_slots"],
-                "l2_flush": f"{n_sets} rotating buffer sets x {b['total'] / 1e6:.1f} MB = "
-                            f"{n_sets * b['total'] / 1e6:.0f} MB > 3x L2 ({l2 / 1e6:.0f} MB)",
+    cfg.update({"l2_flush": f"{sh.n_sets} rotating buffer sets x {b['total'] / 1e6:.1f} MB = "
+                            f"{sh.n_sets * b['total'] / 1e6:.0f} MB > 3x L2 ({sh.l2 / 1e6:.0f} MB)",
                 "graph_steps": S, "kernel": plan.kernel_name + (f" + BFP{args.bfp} y (k_apply_bfp)" if ybfp is not None else ""),
                 "y_format": f"BFP {args.bfp}-bit mantissas, block per (symbol, PRB, antenna) (reading R25)"
                             if ybfp is not None else "complex64",
                 "call_overlap": "PDL (MIMO_PLAN_OVERLAP_CALLS): call i+1 loads/sets up while call i stores"
                                 if args.overlap else "none (serialised calls)",
-                "parallelism": f"slot-sharded x{world}, no collective" if world > 1 else "single GPU"})
+                "input_sha256": w.sha256(),
+                "parallelism": (f"2-D slot x PRB block partition {blk['grid'][0]}x{blk['grid'][1]} over {world} GPUs, "
+                                f"rank 0 block slots {blk['slots']} PRBs {blk['prbs']}, no collective")
+                               if blk is not None else (f"{world} replicas (job too small to split)" if world > 1
+                                                        else "single GPU, whole job")})
     line = {
         "metric": METRIC,
         "value": value, "unit": "RE/s", "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": t_max_ms / K, "step_us_per_replay": step_dist, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": t_max_ms / K, "wall_ms_per_step": wall_max * 1e3 / K,
+        "step_us_per_replay": step_dist, "higher_is_better": True,
+        "scaling": "strong" if world == 1 else scaling,
         "vs_baseline": None, "dtype": "f32", "setup_dtype": "f64" if plan.kernel_name.startswith("tpu") else "f32",
         "data": "synthetic (seeded numpy PCG64, BASELINE config shapes; DESIGN.md input recipe)",
         "config": cfg,
         "llr_gbit_s": value * w.n_layers * w.qm / 1e9,
-        "roofline": dict(roof, serialised_call_us=single_us,
-                         serialised_frac=max(t_hbm, t_alu, t_tc) / (single_us * 1e-6)),
+        "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "clocks": clocks,
         "gpu_launches": K * plan.launches_per_call,
     }
+    if emul is not None:
+        line["emulated_multi_gpu"] = emul
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

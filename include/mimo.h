@@ -50,7 +50,7 @@
 extern "C" {
 #endif
 
-#define MIMO_ABI_VERSION 1
+#define MIMO_ABI_VERSION 2
 
 typedef struct mimo_plan_s* mimo_plan_t;
 
@@ -80,6 +80,14 @@ typedef struct {
     int llr_type;    /* mimo_llr_type_t */
     float llr_scale; /* multiplier applied to natural-log LLRs before quantisation (> 0, finite) */
     int flags;       /* bitwise OR of MIMO_PLAN_* flags (0 = none) */
+    /* The descriptor is the library's only configuration (no environment
+     * variables). The two fields below default to 0 / NULL. */
+    const char* kernel; /* NULL or "" = the default kernel specialisation for the shape; "generic" =
+                           the generic CTA-per-unit kernel; otherwise the exact name of another compiled
+                           specialisation of the same shape (mimo_plan_kernel_name) -- an unknown name is
+                           MIMO_ERR_UNSUPPORTED. Only shape-serving, result-exact kernels are compiled in. */
+    long long host_chunk_bytes; /* mimo_detect_mmse_host*: input bytes (H + y) per pipeline chunk of whole
+                                   H time blocks; 0 = default (4 MiB synchronous, 16 MiB asynchronous) */
 } mimo_plan_desc_t;
 
 /* Plan flags.

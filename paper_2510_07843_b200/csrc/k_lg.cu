@@ -583,22 +583,13 @@ const KernelEntry kEntries[] = {
     // packed FFMA2 (HT = 2), 4 warps = 16 units per CTA (78.4 us; 2 warps 79.8, 1: 84.1, 6: 94.2, 8: 81.4)
     KernelEntry{"lg3hp_16x8_q8_f16", 16, 8, 8, 1, 14, kLlrF16, 32, 1, launch3<16, 8, 8, kLlrF16, 4, 0, 2>,
                 prepare3<16, 8, 8, kLlrF16, 4, 0, 2>},
-    KernelEntry{"lg3hp_w2", 16, 8, 8, 1, 14, kLlrF16, 32, 1, launch3<16, 8, 8, kLlrF16, 2, 0, 2>,
-                prepare3<16, 8, 8, kLlrF16, 2, 0, 2>},
-    KernelEntry{"lg3h_16x8_q8_f16", 16, 8, 8, 1, 14, kLlrF16, 32, 1, launch3<16, 8, 8, kLlrF16, 2, 0, 1>,
-                prepare3<16, 8, 8, kLlrF16, 2, 0, 1>},
     LG3_ENTRY("lg3_16x8_q8_f16", 16, 8, 8, kLlrF16, 2),  // y by TMA, H by per-unit bulk copies
     LG_ENTRY("lg_16x8_q8_f16", 16, 8, 8, kLlrF16, 2),
-    LG3_ENTRY("lg3_16x8_q8_f16_w1", 16, 8, 8, kLlrF16, 1),
-    LG3_ENTRY("lg3_16x8_q8_f16_w4", 16, 8, 8, kLlrF16, 4),
     LG_ENTRY("lg_16x8_q8_f32", 16, 8, 8, kLlrF32, 2),
     LG_ENTRY("lg_16x8_q8_i8", 16, 8, 8, kLlrI8, 2),
     LG_ENTRY("lg_16x8_q6_f16", 16, 8, 6, kLlrF16, 2),
     LG_ENTRY("lg_8x8_q6_f16", 8, 8, 6, kLlrF16, 2),
     LG_ENTRY("lg_16x16_q8_f16", 16, 16, 8, kLlrF16, 2),
-    // tuning variants for C4
-    LG_ENTRY("lg_16x8_q8_f16_w1", 16, 8, 8, kLlrF16, 1),
-    LG_ENTRY("lg_16x8_q8_f16_w4", 16, 8, 8, kLlrF16, 4),
 };
 
 }  // namespace

@@ -307,12 +307,6 @@ const KernelEntry kEntries[] = {
     PRB_ENTRY("prb_8x4_q4_i8", 8, 4, 4, kLlrI8, 4, 2),
     PRB_ENTRY("prb_4x4_q6_i8", 4, 4, 6, kLlrI8, 4, 2),
     PRB_ENTRY("prb_8x2_q6_i8", 8, 2, 6, kLlrI8, 4, 2),
-    // tuning variants for C3
-    PRB_ENTRY("prb_8x4_q6_i8_p8g1", 8, 4, 6, kLlrI8, 8, 1),
-    PRB_ENTRY("prb_8x4_q6_i8_p8g2", 8, 4, 6, kLlrI8, 8, 2),
-    PRB_ENTRY("prb_8x4_q6_i8_p4g1", 8, 4, 6, kLlrI8, 4, 1),
-    PRB_ENTRY("prb_8x4_q6_i8_p4g4", 8, 4, 6, kLlrI8, 4, 4),
-    PRB_ENTRY("prb_8x4_q6_i8_p2g4", 8, 4, 6, kLlrI8, 2, 4),
 };
 
 }  // namespace

@@ -490,20 +490,10 @@ cudaError_t launch_bfp_g(const DetectArgs& a, const uint32_t* yb, int W, float s
     return cudaLaunchKernelEx(&cfg, k_apply_bfp<8, 4, QM, LT, G>, a, yb, W, scale);
 }
 
-// symbols per thread = 14 / G; MIMO_BFP_G (tuning knob) overrides the default G = 2
+// symbols per thread = 14 / G (G = 2: measured best of 1, 2, 7, 14 in round 1)
 template <int QM, int LT>
 cudaError_t launch_bfp_t(const DetectArgs& a, const uint32_t* yb, int W, float scale, cudaStream_t s) {
-    static int g = 0;
-    if (!g) {
-        const char* e = getenv("MIMO_BFP_G");
-        g = e ? atoi(e) : 2;
-    }
-    switch (g) {
-    case 1: return launch_bfp_g<QM, LT, 1>(a, yb, W, scale, s);
-    case 2: return launch_bfp_g<QM, LT, 2>(a, yb, W, scale, s);
-    case 14: return launch_bfp_g<QM, LT, 14>(a, yb, W, scale, s);
-    default: return launch_bfp_g<QM, LT, 7>(a, yb, W, scale, s);
-    }
+    return launch_bfp_g<QM, LT, 2>(a, yb, W, scale, s);
 }
 
 template <int QM>
@@ -555,7 +545,6 @@ cudaError_t launch(const DetectArgs& a, cudaStream_t s) {
 
 const KernelEntry kEntries[] = {
     STREAM_ENTRY_B("stream_8x4_q6_i8", 8, 4, 6, kLlrI8, 12, 16, 2, 2, 4),  // C3: <= 128 regs -> 4 CTAs/SM
-    STREAM_ENTRY("stream_8x4_q6_i8_pf3", 8, 4, 6, kLlrI8, 12, 16, 2, 3),
     SPLIT_ENTRY("split_8x4_q6_i8", 8, 4, 6, kLlrI8, 12, 32, 7),
     SPLIT_ENTRY("split_8x4_q6_f32", 8, 4, 6, kLlrF32, 12, 32, 7),
     SPLIT_ENTRY("split_8x4_q6_f16", 8, 4, 6, kLlrF16, 12, 32, 7),

@@ -72,9 +72,6 @@ __device__ __forceinline__ Cx<T> msubc(Cx<T> acc, Cx<T> a, Cx<T> b) {
 __device__ __forceinline__ double rsq(double v) { return rsqrt(v); }
 __device__ __forceinline__ float rsq(float v) { return rsqrtf(v); }
 
-// Tag type: skip the setup (W~ = scaled H^T; timing experiments only).
-struct NoSetup {};
-
 template <int NR, int NL>
 struct SetupOut {
     float2 w[NL][NR];  // W~ * sqrt(norm), fp32
@@ -91,17 +88,7 @@ template <typename T, int NR, int NL>
 __device__ __forceinline__ void setup_unit(const float2 (&hf)[NR][NL], float sigma2, float norm, float llr_scale,
                                            SetupOut<NR, NL>& o) {
     const float sqn = sqrtf(norm);
-    if constexpr (std::is_same<T, NoSetup>::value) {
-#pragma unroll
-        for (int k = 0; k < NL; ++k) {
-#pragma unroll
-            for (int r = 0; r < NR; ++r) o.w[k][r] = make_float2(hf[r][k].x * sqn, -hf[r][k].y * sqn);
-            o.sinr[k] = 10.f;
-            o.slope[k] = 10.f / norm * llr_scale;
-        }
-        o.fail = false;
-        return;
-    } else {
+    {
         const T s2 = (T)sigma2;
         Cx<T> h[NR][NL];
 #pragma unroll
@@ -456,8 +443,8 @@ cudaError_t prepare() {
     }
 #define TPU_ENTRY(NAME, NR, NL, QM, LT, TU, G, YL, ST) TPU_ENTRY2(NAME, NR, NL, QM, LT, TU, G, YL, ST, false)
 
-// First entry matching a plan wins; the rest are selectable by name
-// (MIMO_FORCE_KERNEL) for tuning experiments.
+// First entry matching a plan wins (the default); another entry of the same
+// shape is selectable by name through mimo_plan_desc_t.kernel.
 const KernelEntry kEntries[] = {
     TPU_ENTRY("tpu_2x2_q2_f32", 2, 2, 2, kLlrF32, 32, 1, kYBulk, double),                 // C1
     TPU_ENTRY2("tpu_4x4_q4_f32", 4, 4, 4, kLlrF32, 64, 2, kYBulk, double, true),          // C2, paper 4x4
@@ -469,16 +456,6 @@ const KernelEntry kEntries[] = {
     TPU_ENTRY2("tpu_4x4_q2_f32", 4, 4, 2, kLlrF32, 64, 2, kYBulk, double, true),
     TPU_ENTRY2("tpu_4x4_q6_f32", 4, 4, 6, kLlrF32, 64, 2, kYBulk, double, true),
     TPU_ENTRY2("tpu_4x4_q8_f32", 4, 4, 8, kLlrF32, 64, 2, kYBulk, double, true),
-    // tuning variants for C2 (MIMO_FORCE_KERNEL)
-    TPU_ENTRY("tpu_4x4_q4_f32_dup2_tu32", 4, 4, 4, kLlrF32, 32, 2, kYBulk, double),
-    TPU_ENTRY("tpu_4x4_q4_f32_async", 4, 4, 4, kLlrF32, 32, 2, kYAsync, double),
-    TPU_ENTRY("tpu_4x4_q4_f32_ldg", 4, 4, 4, kLlrF32, 32, 2, kYLdg, double),
-    TPU_ENTRY("tpu_4x4_q4_f32_nosetup", 4, 4, 4, kLlrF32, 32, 2, kYBulk, NoSetup),
-    TPU_ENTRY("tpu_4x4_q4_f32_fp32setup", 4, 4, 4, kLlrF32, 32, 2, kYBulk, float),
-    TPU_ENTRY2("tpu_4x4_q4_f32_share2_tu128", 4, 4, 4, kLlrF32, 128, 2, kYBulk, double, true),
-    TPU_ENTRY2("tpu_4x4_q4_f32_share2_tu64_async", 4, 4, 4, kLlrF32, 64, 2, kYAsync, double, true),
-    TPU_ENTRY2("tpu_4x4_q4_f32_share3_tu64", 4, 4, 4, kLlrF32, 64, 3, kYBulk, double, true),
-    TPU_ENTRY2("tpu_4x4_q4_f32_share2_tu96", 4, 4, 4, kLlrF32, 96, 2, kYBulk, double, true),
 };
 
 }  // namespace

@@ -48,6 +48,7 @@ const KernelEntry* prb_entries(int* n);
 const KernelEntry* split_entries(int* n);
 const KernelEntry* lg_entries(int* n);
 const KernelEntry* big_entries(int* n);
+const KernelEntry* c5_entries(int* n);
 
 // Generic kernel: any n_rx <= 64, n_layers <= min(16, n_rx), qm, sc_per_h,
 // sym_per_h, llr_type; 8-byte alignment.

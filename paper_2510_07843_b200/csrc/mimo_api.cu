@@ -44,6 +44,7 @@ struct mimo_plan_s {
     cudaStream_t hs[3] = {nullptr, nullptr, nullptr};  // H2D, kernels, D2H
     cudaEvent_t ev = nullptr;
     unsigned long long host_chunk = 0;  // host-path buffer ring position
+    size_t host_bh = 0, host_by = 0, host_bl = 0;  // host-path buffer layout of the ring in use
     cudaEvent_t e_in[kNB] = {}, e_k[kNB] = {}, e_out[kNB] = {};
     // kernel workspaces: slot 0 for the plan's stream, 1..2 for the host path's streams
     void* kws[3] = {nullptr, nullptr, nullptr};
@@ -69,23 +70,28 @@ mimo_status_t arg_fail(mimo_plan_t p, const char* what) {
     return MIMO_ERR_INVALID_ARG;
 }
 
-// First specialised kernel serving the descriptor. MIMO_FORCE_KERNEL=<name>
-// (a tuning/debug knob) picks a named variant instead, or "generic".
-const mimo::KernelEntry* select_fast(const mimo_plan_desc_t& d) {
+// The kernel specialisation serving the descriptor: the first table entry of the
+// shape (the default), or the entry desc.kernel names. Sets *generic for
+// desc.kernel == "generic"; returns nullptr with *unknown set for a name that
+// no compiled entry of this shape carries.
+const mimo::KernelEntry* select_fast(const mimo_plan_desc_t& d, bool* generic, bool* unknown) {
     using LF = const mimo::KernelEntry* (*)(int*);
-    const LF tables[] = {mimo::tpu_entries, mimo::split_entries, mimo::lg_entries, mimo::big_entries,
-                         mimo::prb_entries};
-    const char* force = getenv("MIMO_FORCE_KERNEL");
-    if (force && strcmp(force, "generic") == 0) return nullptr;
+    const LF tables[] = {mimo::tpu_entries, mimo::split_entries, mimo::lg_entries, mimo::c5_entries,
+                         mimo::big_entries, mimo::prb_entries};
+    const char* want = (d.kernel && *d.kernel) ? d.kernel : nullptr;
+    *generic = want && strcmp(want, "generic") == 0;
+    *unknown = false;
+    if (*generic) return nullptr;
     for (LF f : tables) {
         int n = 0;
         const mimo::KernelEntry* t = f(&n);
         for (int i = 0; i < n; ++i)
             if (t[i].n_rx == d.n_rx && t[i].n_layers == d.n_layers && t[i].qm == d.qam_order &&
                 t[i].sc_per_h == d.sc_per_h && t[i].sym_per_h == d.sym_per_h && t[i].llr_type == d.llr_type &&
-                (!force || !*force || strcmp(force, t[i].name) == 0))
+                (!want || strcmp(want, t[i].name) == 0))
                 return &t[i];
     }
+    *unknown = want != nullptr;
     return nullptr;
 }
 
@@ -240,7 +246,18 @@ mimo_status_t mimo_plan_create(const mimo_plan_desc_t* desc, mimo_plan_t* out) {
     if (!p) return MIMO_ERR_OOM;
     p->d = d;
     p->stream = static_cast<cudaStream_t>(d.stream);
-    p->fast = select_fast(d);
+    bool generic = false, unknown = false;
+    p->fast = select_fast(d, &generic, &unknown);
+    p->d.kernel = nullptr;  // the caller's string is not kept
+    if (unknown) {
+        snprintf(g_last_error, sizeof(g_last_error), "no compiled kernel named '%s' serves this shape", d.kernel);
+        delete p;
+        return MIMO_ERR_UNSUPPORTED;
+    }
+    if (d.host_chunk_bytes < 0) {
+        delete p;
+        return arg_fail(nullptr, "host_chunk_bytes must be >= 0");
+    }
     if (p->fast && p->fast->prepare) {
         e = p->fast->prepare();
         if (e != cudaSuccess) {
@@ -345,8 +362,7 @@ static mimo_status_t host_path(mimo_plan_t p, const void* H_host, const void* y_
     constexpr int NB = mimo_plan_s::kNB;
     // measured best on the B200 box for C2 (tools/e2e_chunks.py): 4 MiB for a synchronous call (its
     // own fill and drain are exposed), 16 MiB for a stream of asynchronous calls (they overlap)
-    size_t chunk_bytes = wait ? (4u << 20) : (16u << 20);
-    if (const char* cb = getenv("MIMO_HOST_CHUNK_BYTES")) chunk_bytes = (size_t)atoll(cb);  // tuning knob
+    size_t chunk_bytes = p->d.host_chunk_bytes > 0 ? (size_t)p->d.host_chunk_bytes : wait ? (4u << 20) : (16u << 20);
     int cs = (int)(chunk_bytes / (h_slot + y_slot));
     if (cs < 1) cs = 1;
     if (cs > n_slots) cs = n_slots;
@@ -366,6 +382,18 @@ static mimo_status_t host_path(mimo_plan_t p, const void* H_host, const void* y_
             if ((e = cudaEventCreateWithFlags(&p->e_out[i], cudaEventDisableTiming)) != cudaSuccess)
                 return cuda_fail(p, e, "cudaEventCreate");
         }
+    }
+    // The ring position carries over between calls, so consecutive calls must share one buffer
+    // layout: when it changes (other chunk size or call shape), drain every pending use of the
+    // old layout and restart the ring before any buffer is reused (an earlier asynchronous call
+    // may still be copying into / out of the region a new layout would overlap).
+    if (bh != p->host_bh || by != p->host_by || bl != p->host_bl) {
+        for (int i = 0; i < 3; ++i)
+            if ((e = cudaStreamSynchronize(p->hs[i])) != cudaSuccess) return cuda_fail(p, e, "cudaStreamSynchronize");
+        p->host_chunk = 0;
+        p->host_bh = bh;
+        p->host_by = by;
+        p->host_bl = bl;
     }
     if (p->ws_bytes < need) {
         if (p->ws) {

@@ -43,7 +43,7 @@ class _Desc(ctypes.Structure):
     _fields_ = [("device", ctypes.c_int), ("stream", ctypes.c_void_p), ("n_rx", ctypes.c_int),
                 ("n_layers", ctypes.c_int), ("qam_order", ctypes.c_int), ("sc_per_h", ctypes.c_int),
                 ("sym_per_h", ctypes.c_int), ("llr_type", ctypes.c_int), ("llr_scale", ctypes.c_float),
-                ("flags", ctypes.c_int)]
+                ("flags", ctypes.c_int), ("kernel", ctypes.c_char_p), ("host_chunk_bytes", ctypes.c_longlong)]
 
 
 _lib = None
@@ -126,7 +126,8 @@ class Plan:
 
     def __init__(self, n_rx: int, n_layers: int, qm: int, *, sc_per_h: int = 1,
                  sym_per_h: int = SYM_PER_SLOT, llr_dtype="f32", llr_scale: float = 1.0,
-                 device=None, stream=None, overlap_calls: bool = False):
+                 device=None, stream=None, overlap_calls: bool = False, kernel: str | None = None,
+                 host_chunk_bytes: int = 0):
         import torch
         L = load_library()
         if not torch.cuda.is_available():
@@ -145,7 +146,8 @@ class Plan:
         self.llr_dtype = _llr_torch_dtype(self.llr_type)
         self._fixed_stream = stream
         d = _Desc(dev.index, ctypes.c_void_p(self._stream_ptr()), n_rx, n_layers, qm, sc_per_h, sym_per_h,
-                  self.llr_type, float(llr_scale), PLAN_OVERLAP_CALLS if overlap_calls else 0)
+                  self.llr_type, float(llr_scale), PLAN_OVERLAP_CALLS if overlap_calls else 0,
+                  kernel.encode() if kernel else None, int(host_chunk_bytes))
         h = ctypes.c_void_p()
         st = L.mimo_plan_create(ctypes.byref(d), ctypes.byref(h))
         if st != MIMO_OK:
@@ -188,7 +190,9 @@ class Plan:
             raise ValueError(f"{name} must be {dtype}, got {t.dtype}")
         if not t.is_contiguous():
             raise ValueError(f"{name} must be contiguous")
-        if tuple(t.shape) != tuple(shape) and t.numel() != int(np.prod(shape)):
+        # exact shape, or a flat view with the right element count (a transposed / reshaped
+        # tensor of the same size is rejected rather than silently misread)
+        if tuple(t.shape) != tuple(shape) and not (t.dim() == 1 and t.numel() == int(np.prod(shape))):
             raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
         return t
 

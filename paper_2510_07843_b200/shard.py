@@ -24,13 +24,57 @@ def slot_partition(n_slots: int, world: int) -> list[tuple[int, int]]:
     return out
 
 
-def weak_slots(slots_per_rank: int, rank: int) -> tuple[int, int]:
-    """Weak scaling: rank r owns slots [r*S, (r+1)*S) of an (N*S)-slot job."""
-    return rank * slots_per_rank, (rank + 1) * slots_per_rank
+SC_PER_PRB = 12
+
+
+def block_partition(n_slots: int, n_prb: int, world: int) -> list[dict]:
+    """2-D (slot x PRB) block partition of one configured job over `world` ranks.
+
+    a = gcd(n_slots, world) slot groups x b = world / a PRB groups; both splits are contiguous
+    and balanced (sizes differ by <= 1: 273 PRBs over 4 groups -> 69/68/68/68). Rank r owns slot
+    group r // b and PRB group r % b. Every (slot, PRB) is owned by exactly one rank, and each
+    block is a whole number of H-units for per-subcarrier and per-PRB channels alike, so the
+    shards need no exchange step. C5 (40 slots) over 8 ranks: 8 x 1, five slots per GPU -- the
+    north_star's "sharded by slot across 8 GPUs"; C2 (10 slots) over 8: 2 x 4.
+    Returns per rank {"slots": (s0, s1), "prbs": (p0, p1), "grid": (a, b)}."""
+    import math
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    a = math.gcd(n_slots, world)
+    b = world // a
+    if b > n_prb:
+        raise ValueError(f"cannot split {n_prb} PRBs into {b} groups")
+    sl = slot_partition(n_slots, a)
+    pr = slot_partition(n_prb, b)
+    return [{"slots": sl[r // b], "prbs": pr[r % b], "grid": (a, b)} for r in range(world)]
+
+
+def shard_arrays(H, y, n_slots: int, sc_per_h: int, block: dict, sym_per_slot: int = 14):
+    """Contiguous copies of one rank's block of H [n_slots][n_fb][nr][nl] and y [n_sym][n_sc][nr]
+    (numpy or torch; indexing only). Returns (H_blk, y_blk, n_sc_blk, n_slots_blk)."""
+    s0, s1 = block["slots"]
+    p0, p1 = block["prbs"]
+    c0, c1 = p0 * SC_PER_PRB, p1 * SC_PER_PRB
+    f0, f1 = c0 // sc_per_h, c1 // sc_per_h
+    Hb = H[s0:s1, f0:f1]
+    yb = y[s0 * sym_per_slot:s1 * sym_per_slot, c0:c1]
+    if hasattr(Hb, "contiguous"):
+        return Hb.contiguous(), yb.contiguous(), c1 - c0, s1 - s0
+    import numpy as np
+    return np.ascontiguousarray(Hb), np.ascontiguousarray(yb), c1 - c0, s1 - s0
+
+
+def place_block(full, part, block: dict, sym_per_slot: int = 14):
+    """Result placement: write one rank's [sym][sc][...] output block into the full grid."""
+    s0, s1 = block["slots"]
+    p0, p1 = block["prbs"]
+    full[s0 * sym_per_slot:s1 * sym_per_slot, p0 * SC_PER_PRB:p1 * SC_PER_PRB] = part
+    return full
 
 
 def shard_seed(base_seed: int, rank: int) -> int:
-    """Seed of rank r's shard (each rank's slots are an independent seeded draw)."""
+    """Seed of an independently drawn per-rank workload (replica runs only; the strong-scaling
+    path slices one seeded job with block_partition instead)."""
     return base_seed + 7919 * rank
 
 
@@ -53,6 +97,17 @@ def sum_over_ranks(value: float, device=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
+
+
+def gather_objects(obj, world: int, dst: int = 0):
+    """Result placement for verification: gather one picklable object per rank to rank dst
+    (list on dst, None elsewhere). Never inside a timed region."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or world == 1:
+        return [obj]
+    objs = [None] * world if dist.get_rank() == dst else None
+    dist.gather_object(obj, objs, dst=dst)
+    return objs
 
 
 def gather_slot_blocks(local, world: int, dst: int = 0):

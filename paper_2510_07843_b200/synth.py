@@ -298,9 +298,15 @@ def bfp_compress(y: np.ndarray, iq_width: int = 9, scale: float = 2.0 ** -8) -> 
     return np.concatenate([e.astype(np.uint8)[..., None], payload], axis=-1)
 
 
-def config_algorithmic_bytes(cfg_key, llr_bytes: int | None = None) -> dict:
-    """Algorithmic bytes of one full pass (H read once, y read once, LLRs written once), SURVEY.md §8(d)."""
-    c = CONFIGS[cfg_key]
+def config_algorithmic_bytes(cfg_key, llr_bytes: int | None = None, n_sc: int | None = None,
+                             n_slots: int | None = None) -> dict:
+    """Algorithmic bytes of one full pass (H read once, y read once, LLRs written once), SURVEY.md §8(d).
+    n_sc / n_slots override the config's grid (a multi-GPU shard)."""
+    c = dict(CONFIGS[cfg_key])
+    if n_sc is not None:
+        c["n_sc"] = n_sc
+    if n_slots is not None:
+        c["n_slots"] = n_slots
     nr, nl, qm, scph = c["n_rx"], c["n_layers"], c["qm"], c["sc_per_h"]
     n_sym = c["n_slots"] * SYM_PER_SLOT
     n_re = n_sym * c["n_sc"]
@@ -313,14 +319,18 @@ def config_algorithmic_bytes(cfg_key, llr_bytes: int | None = None) -> dict:
                 n_llr=n_re * nl * qm)
 
 
-def config_algorithmic_flops(cfg_key) -> dict:
+def config_algorithmic_flops(cfg_key, n_sc: int | None = None, n_slots: int | None = None) -> dict:
     """Algorithmic flops of one full pass (SURVEY.md §8(d) counting convention).
 
     Setup per H-unit (rows a2-a5), in complex MACs (8 real flops each):
       Gram nr*nl(nl+1)/2 + Cholesky nl^3/6 + L^-1 nl^3/6 + W nl^2*nr;
     per RE: x~ = W~ y, nl*nr cMAC (row a6), and ~8 flops per LLR bit (row a7).
     """
-    c = CONFIGS[cfg_key]
+    c = dict(CONFIGS[cfg_key])
+    if n_sc is not None:
+        c["n_sc"] = n_sc
+    if n_slots is not None:
+        c["n_slots"] = n_slots
     nr, nl, qm, scph = c["n_rx"], c["n_layers"], c["qm"], c["sc_per_h"]
     n_sym = c["n_slots"] * SYM_PER_SLOT
     n_re = n_sym * c["n_sc"]

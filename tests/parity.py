@@ -25,14 +25,15 @@ def np_llr_dtype(llr: str):
     return {"f32": np.float32, "f16": np.float16, "i8": np.int8}[llr]
 
 
-def run_gpu(w: synth.Workload, *, xhat=True, sinr=True, llr_scale=1.0, plan=None, H=None, y=None):
-    """Detect the whole workload on cuda:0 through the C ABI; returns numpy arrays."""
+def run_gpu(w: synth.Workload, *, xhat=True, sinr=True, llr_scale=1.0, plan=None, H=None, y=None, kernel=None):
+    """Detect the whole workload on cuda:0 through the C ABI; returns numpy arrays.
+    kernel: a named kernel specialisation (mimo_plan_desc_t.kernel), default the shape's default."""
     import torch
     from paper_2510_07843_b200 import mimo
     own = plan is None
     if own:
         plan = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, sym_per_h=w.sym_per_h, llr_dtype=w.llr,
-                         llr_scale=llr_scale)
+                         llr_scale=llr_scale, kernel=kernel)
     Hd = torch.from_numpy(w.H if H is None else H).cuda()
     yd = torch.from_numpy(w.y if y is None else y).cuda()
     sh = plan.shapes(w.n_sc, w.n_sym)

@@ -36,8 +36,26 @@ def test_no_torch_or_oracle_in_library():
     assert "oracle_" not in strings
 
 
+def test_no_environment_configuration_or_ablations_in_library():
+    """The plan descriptor is the library's only configuration: no MIMO_* environment
+    knobs and no wrong-on-purpose timing-ablation kernels are compiled into libmimo.so."""
+    blob = open(mimo.LIB_PATH, "rb").read()
+    for s in (b"MIMO_FORCE_KERNEL", b"MIMO_HOST_CHUNK_BYTES", b"MIMO_BFP_G", b"ablation", b"nosetup", b"NoSetup"):
+        assert s not in blob, s
+    src = open(__import__("os").path.join(mimo._PKG, "csrc", "mimo_api.cu")).read()
+    assert "getenv" not in src
+
+
+def test_descriptor_layout_matches_header():
+    """ctypes mirror of mimo_plan_desc_t: field order and the two ABI-2 fields."""
+    names = [f[0] for f in mimo._Desc._fields_]
+    assert names[-2:] == ["kernel", "host_chunk_bytes"]
+    hdr = open(mimo.HEADER).read()
+    assert "const char* kernel;" in hdr and "long long host_chunk_bytes;" in hdr
+
+
 def test_abi_version_and_status_strings(lib):
-    assert lib.mimo_abi_version() == 1
+    assert lib.mimo_abi_version() == 2
     for s in range(6):
         assert lib.mimo_status_string(s).decode().startswith("MIMO_")
     assert lib.mimo_plan_destroy(None) == mimo.MIMO_OK

@@ -84,6 +84,48 @@ def test_kernel_selection():
     assert mimo.Plan(2, 2, 2).kernel_name.startswith("tpu_2x2")
     assert mimo.Plan(7, 3, 4).kernel_name == "generic"
     assert mimo.Plan(4, 4, 4).launches_per_call == 1
+    # the descriptor's kernel field: a named variant, "generic", an unknown name -> UNSUPPORTED
+    assert mimo.Plan(64, 16, 6, sc_per_h=12, llr_dtype="i8").kernel_name.startswith("c5_")
+    assert mimo.Plan(64, 16, 6, sc_per_h=12, llr_dtype="i8", kernel="big_64x16_q6_i8").kernel_name == "big_64x16_q6_i8"
+    assert mimo.Plan(4, 4, 4, kernel="generic").kernel_name == "generic"
+    with pytest.raises(mimo.MimoError) as ei:
+        mimo.Plan(4, 4, 4, kernel="no_such_kernel")
+    assert ei.value.status == mimo.MIMO_ERR_UNSUPPORTED
+    with pytest.raises(mimo.MimoError):  # a name of another shape's kernel does not serve this one
+        mimo.Plan(4, 4, 4, kernel="c5_bf16_64x16_q6_i8")
+
+
+def test_host_path_async_then_sync_of_other_layout():
+    """a synchronous host-buffer call right after an asynchronous one of the same
+    plan uses another chunk layout; both must return the device path's LLRs exactly."""
+    import torch
+    w = synth.generate(2)  # full C2: the async call's 16 MiB chunks vs the sync call's 4 MiB ones
+    plan = mimo.Plan(4, 4, 4)
+    H, y = torch.from_numpy(w.H), torch.from_numpy(w.y)
+    ref = plan.detect(H.cuda(), y.cuda(), float(w.sigma2)).cpu()
+    Hh, yh = H.pin_memory(), y.pin_memory()
+    la = torch.empty_like(ref).pin_memory()
+    lb = torch.empty_like(ref).pin_memory()
+    w2 = synth.generate(2, n_slots=3, seed=77)  # another shape, then the full one again
+    ref2 = plan.detect(torch.from_numpy(w2.H).cuda(), torch.from_numpy(w2.y).cuda(), float(w2.sigma2)).cpu()
+    lc = torch.empty_like(ref2).pin_memory()
+    plan.detect_host(Hh, yh, float(w.sigma2), out=la, wait=False)
+    plan.detect_host(torch.from_numpy(w2.H).pin_memory(), torch.from_numpy(w2.y).pin_memory(), float(w2.sigma2),
+                     out=lc, wait=True)
+    plan.detect_host(Hh, yh, float(w.sigma2), out=lb, wait=True)
+    assert plan.sync_status() == 0
+    assert torch.equal(la, ref) and torch.equal(lb, ref) and torch.equal(lc, ref2)
+
+
+def test_host_chunk_bytes_descriptor_field():
+    import torch
+    w = synth.generate(2, n_sc=96, n_slots=6)
+    ref = mimo.Plan(4, 4, 4).detect(torch.from_numpy(w.H).cuda(), torch.from_numpy(w.y).cuda(), float(w.sigma2)).cpu()
+    for cb in (1, 200_000, 1 << 30):
+        p = mimo.Plan(4, 4, 4, host_chunk_bytes=cb)
+        out = torch.empty_like(ref)
+        p.detect_host(torch.from_numpy(w.H), torch.from_numpy(w.y), float(w.sigma2), out=out)
+        assert torch.equal(out, ref)
 
 
 def test_stream_ordering():

@@ -1,6 +1,6 @@
-"""GPU parity of the non-default kernel variants (selected by name through
-MIMO_FORCE_KERNEL, the tuning knob of mimo_api.cu select_fast): every variant the
-bench or DESIGN.md reports a time for must produce oracle-exact results too.
+"""GPU parity of the non-default kernel variants (selected by name through the plan
+descriptor's `kernel` field): every variant compiled into libmimo.so must produce
+oracle-exact results too.
 Same tolerances as test_parity_gpu.py (tests/parity.py)."""
 import numpy as np
 import pytest
@@ -10,16 +10,13 @@ from paper_2510_07843_b200 import synth
 
 pytestmark = pytest.mark.gpu
 
-C5_VARIANTS = ["big4_64x16_q6_i8", "big4c_64x16_q6_i8", "big4e8_64x16_q6_i8", "big5_64x16_q6_i8", "big5e8_64x16_q6_i8", "big8_64x16_q6_i8", "big11_64x16_q6_i8", "big8e6_64x16_q6_i8", "big11e6_64x16_q6_i8",
-               "big3_64x16_q6_i8", "big2_64x16_q6_i8",
-               "big_64x16_q6_i8"]
-C4_VARIANTS = ["lg3h_16x8_q8_f16", "lg3hp_16x8_q8_f16", "lg3hp_w2", "lg3_16x8_q8_f16", "lg3_16x8_q8_f16_w1", "lg_16x8_q8_f16"]
-C3_VARIANTS = ["stream_8x4_q6_i8_pf3", "split_8x4_q6_i8", "prb_8x4_q6_i8"]
+C5_VARIANTS = ["c5_bf16_64x16_q6_i8", "c5_tf32_64x16_q6_i8", "c5_bf16_chol_64x16_q6_i8", "big_64x16_q6_i8"]
+C4_VARIANTS = ["lg3hp_16x8_q8_f16", "lg3_16x8_q8_f16", "lg_16x8_q8_f16"]
+C3_VARIANTS = ["stream_8x4_q6_i8", "split_8x4_q6_i8", "prb_8x4_q6_i8"]
 
 
 def _forced(monkeypatch, name, w, **kw):
-    monkeypatch.setenv("MIMO_FORCE_KERNEL", name)
-    g = parity.run_gpu(w, **kw)
+    g = parity.run_gpu(w, kernel=name, **kw)
     assert g["kernel"] == name, f"forced {name}, plan selected {g['kernel']}"
     assert g["n_failed"] == 0
     return g
@@ -28,7 +25,7 @@ def _forced(monkeypatch, name, w, **kw):
 @pytest.mark.parametrize("name", C5_VARIANTS)
 def test_c5_variant(monkeypatch, name):
     # 4 slots x 273 PRBs = 1092 units: > 7 units per CTA of the 148-CTA persistent grids, so the
-    # stage / TMEM / B-operand rings of big4/big5 wrap several times
+    # stage / TMEM / B-operand rings of the persistent c5 kernels wrap several times
     w = synth.generate(5, n_sc=3276, n_slots=4)
     g = _forced(monkeypatch, name, w, xhat=False, sinr=True)
     rng = np.random.default_rng(7)

@@ -19,20 +19,15 @@ CASES = [  # (config, generate kwargs, forced kernel or None)
     (3, dict(n_sc=48, n_slots=1), None),
     (4, dict(n_sc=40, n_slots=1), None),
     (5, dict(n_sc=24, n_slots=1), None),
-    (5, dict(n_sc=24, n_slots=1), "big2_64x16_q6_i8"),
-    (5, dict(n_sc=24, n_slots=1), "big3_64x16_q6_i8"),
-    (5, dict(n_sc=24, n_slots=1), "big5_64x16_q6_i8"),
+    (5, dict(n_sc=24, n_slots=1), "c5_tf32_64x16_q6_i8"),
+    (5, dict(n_sc=24, n_slots=1), "big_64x16_q6_i8"),
     (2, dict(n_sc=36, n_slots=1), "generic"),
 ]
 
 
 def run(k, kw, force):
-    if force:
-        os.environ["MIMO_FORCE_KERNEL"] = force
-    else:
-        os.environ.pop("MIMO_FORCE_KERNEL", None)
     w = synth.generate(k, **kw)
-    p = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, llr_dtype=w.llr)
+    p = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, llr_dtype=w.llr, kernel=force)
     H, y = torch.from_numpy(w.H).cuda(), torch.from_numpy(w.y).cuda()
     sh = p.shapes(w.n_sc, w.n_sym)
     x = torch.empty(sh["xhat"], dtype=torch.complex64, device="cuda")
@@ -46,7 +41,6 @@ def run(k, kw, force):
 def main():
     for k, kw, force in CASES:
         run(k, kw, force)
-    os.environ.pop("MIMO_FORCE_KERNEL", None)
     p, w, H, y = run(2, dict(n_sc=36, n_slots=1), None)
     for prec in (32, 64):
         p.detect_lu(H, y, float(w.sigma2), precision=prec)
