@@ -26,8 +26,44 @@
 // TA = 3: kind::f16 with BF16 hi/lo operands (K = 16 per instruction: half the MMAs and half
 // the TMEM A bytes of TA = 1).
 
+#include <type_traits>
+
 #include "big_setup.cuh"
 #include "tc.cuh"
+
+// Optional per-role cycle accounting for tuning builds (tools/dbg/build_prof.sh compiles this
+// file with -DC5_PROFILE into a separate library); compiled out of libmimo.so.
+#ifdef C5_PROFILE
+__device__ unsigned long long g_c5_prof[148 * 32];
+extern "C" int mimo_c5_prof_read(unsigned long long* host) {
+    return (int)cudaMemcpyFromSymbol(host, g_c5_prof, sizeof(g_c5_prof));
+}
+extern "C" int mimo_c5_prof_reset() {
+    static unsigned long long z[148 * 32] = {};
+    return (int)cudaMemcpyToSymbol(g_c5_prof, z, sizeof(z));
+}
+#define PROF_T(v) const long long v = clock64()
+#define PROF_ADD(acc, slot, t0) acc[slot] += (unsigned long long)(clock64() - (t0))
+#define PROF_DECL unsigned long long prof[32] = {}
+#define PROF_FLUSH(cond)                                                                   \
+    if (cond)                                                                              \
+        for (int _i = 0; _i < 32; ++_i)                                                    \
+            if (prof[_i]) atomicAdd(&g_c5_prof[(blockIdx.x % 148) * 32 + _i], prof[_i]);
+__device__ unsigned long long g_c5_sprof[148 * 32];
+extern "C" int mimo_c5_sprof_read(unsigned long long* host) {
+    return (int)cudaMemcpyFromSymbol(host, g_c5_sprof, sizeof(g_c5_sprof));
+}
+#define PROF_SFLUSH(cond)                                                                  \
+    if (cond)                                                                              \
+        for (int _i = 0; _i < 32; ++_i)                                                    \
+            if (prof[_i]) atomicAdd(&g_c5_sprof[(blockIdx.x % 148) * 32 + _i], prof[_i]);
+#else
+#define PROF_SFLUSH(cond)
+#define PROF_T(v)
+#define PROF_ADD(acc, slot, t0)
+#define PROF_DECL
+#define PROF_FLUSH(cond)
+#endif
 
 namespace mimo {
 namespace {
@@ -41,8 +77,10 @@ struct C5Smem {
     static constexpr size_t B = S * chunk;                    // 2 B sets (1024-aligned)
     static constexpr size_t bset = TA_ == 1 ? 4 * 64 * 128 : 2 * 64 * 128;  // K atoms x 64 rows x 128 B
     static constexpr size_t slope = B + 2 * bset;             // [4][16] slope | [4][16] sqrt(slope / 127)
-    static constexpr size_t bars = slope + 512;
-    static constexpr int NBAR = 2 * S + 2 * NLO + 2 * 3;      // yfull, yfree | afull, afree | bready, accfull, tfree
+    static constexpr size_t wst = slope + 512;                // [2] W~ workspace records staged by TMA
+    static constexpr size_t wrec = (size_t)BigWs<64, 16>::stride * 4;
+    static constexpr size_t bars = wst + 2 * wrec;
+    static constexpr int NBAR = 2 * S + 2 * NLO + 2 * 3 + 4;  // yfull, yfree | afull, afree | bready, accfull, tfree | wfull, wfree
     static constexpr size_t tslot = bars + NBAR * 8;
     static constexpr size_t total = tslot + 16 + 1024;        // + 1024-B alignment slack
     static_assert(B % 1024 == 0, "UMMA operand alignment");
@@ -77,13 +115,13 @@ __device__ __forceinline__ void demap_axis_i8(float u, float rs, uint32_t* q, in
     }
 }
 
-template <int QM, int LT, int EW, int S_, int NLO_, int TA>
+template <int QM, int LT, int EW, int S_, int NLO_, int TA, bool BEPI>
 __global__ void __launch_bounds__(32 * (6 + EW), 1) k_c5_apply(DetectArgs a, const __grid_constant__ CUtensorMap ymap) {
     constexpr int NR = 64, NL = 16;
     using SM = C5Smem<S_, NLO_, TA>;
     constexpr int S = S_, NLO = NLO_;
-    constexpr bool CT = EW == 6;  // compact tile 1 (REs 128-167 in lanes 0-39)
-    static_assert(EW == 4 || EW == 6, "4 or 6 epilogue warps");
+    static_assert(EW == 6, "6 epilogue warps (4 for tile 0, 2 for the compact tile 1)");
+
     static_assert(TA == 1 || TA == 3, "TF32 or BF16 operands");
     constexpr uint32_t kAring = 256u;                // TMEM columns 0-255: 2 accumulators x 128
     constexpr uint32_t kAcols = TA == 1 ? 128u : 64u;  // TMEM columns per A ring slot (one chunk, 2 tiles)
@@ -102,6 +140,8 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_c5_apply(DetectArgs a, con
     uint64_t* bready = afree + NLO;    // [2]    converters built B
     uint64_t* accfull = bready + 2;    // [2]    the unit's last MMA completed
     uint64_t* tfree = accfull + 2;     // [2]    epilogue done with the accumulator
+    uint64_t* wfull = tfree + 2;       // [2]    W~ record of unit i staged (TMA tx)
+    uint64_t* wfree = wfull + 2;       // [2]    B set built from it
     uint32_t* tslot = reinterpret_cast<uint32_t*>(g + SM::tslot);
     float* sslope = reinterpret_cast<float*>(g + SM::slope);
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -111,18 +151,21 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_c5_apply(DetectArgs a, con
 
     pdl_launch_dependents();
     if (t == 0) {
+        constexpr uint32_t ngrp = 1;
         for (int i = 0; i < S; ++i) {
             mbar_init(&yfull[i], 1);
-            mbar_init(&yfree[i], 1);
+            mbar_init(&yfree[i], ngrp);
         }
         for (int i = 0; i < NLO; ++i) {
-            mbar_init(&afull[i], 1);
+            mbar_init(&afull[i], ngrp);
             mbar_init(&afree[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&bready[i], 1);
             mbar_init(&accfull[i], 1);
-            mbar_init(&tfree[i], 1);
+            mbar_init(&tfree[i], ngrp);
+            mbar_init(&wfull[i], 1);
+            mbar_init(&wfree[i], 1);
         }
         fence_mbar_init();
     }
@@ -135,17 +178,43 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_c5_apply(DetectArgs a, con
     if (warp == CW + 1) {
         // ================= TMA producer: y chunks, S stages ahead =================
         if (lane == 0) {
+            PROF_DECL;
+            PROF_T(tk0);
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ymap)) : "memory");
+            // W~ records (rows a2-a5 of the setup kernel) of units i = j + 2 are staged when the y chunks
+            // of unit j start; y itself is this call's input and streams before the setup completes
+            auto issue_w = [&](long long i) {
+                const int ws_ = (int)(i & 1);
+                if (i >= 2) mbar_wait_sleep(&wfree[ws_], (uint32_t)(((i >> 1) + 1) & 1));
+                mbar_arrive_expect_tx(&wfull[ws_], (uint32_t)SM::wrec);
+                bulk_g2s(g + SM::wst + ws_ * SM::wrec,
+                         reinterpret_cast<const float*>(a.ws) + (u0 + i * du) * (long long)WS, (uint32_t)SM::wrec,
+                         &wfull[ws_]);
+            };
+            bool waited = false;
 #pragma unroll 1
             for (long long gg = 0; gg < G; ++gg) {
                 const int st = (int)(gg % S);
+                if ((gg & 3) == 0) {
+                    if (!waited) {
+                        pdl_wait();  // the setup kernel of this call has written the workspace
+                        waited = true;
+                        issue_w(0);
+                        if (n_my > 1) issue_w(1);
+                    }
+                    if ((gg >> 2) + 2 < n_my) issue_w((gg >> 2) + 2);
+                }
+                PROF_T(tw);
                 if (gg >= S) mbar_wait_sleep(&yfree[st], (uint32_t)(((gg / S) + 1) & 1));
+                PROF_ADD(prof, 0, tw);
                 const long long uu = u0 + (gg >> 2) * du;
                 const int slot = (int)(uu / a.n_fb), fb = (int)(uu % a.n_fb);
                 mbar_arrive_expect_tx(&yfull[st], (uint32_t)SM::chunk);
                 tma_load_3d(base + (uint32_t)(SM::y0 + st * SM::chunk), &ymap, 32 * (int)(gg & 3), fb * kSc,
                             slot * kSym, &yfull[st]);
             }
+            PROF_ADD(prof, 31, tk0);
+            PROF_FLUSH(true);
         }
     } else if (warp == CW) {
         // ================= MMA issuer =================
@@ -153,11 +222,16 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_c5_apply(DetectArgs a, con
             constexpr uint32_t f = TA == 1 ? tc::kFmtTF32 : tc::kFmtBF16;
             constexpr uint32_t id64 = tc::idesc(f, 128, 64), id32 = tc::idesc(f, 128, 32);
             const uint64_t dB = tc::desc_sw128(base + (uint32_t)SM::B);
+            PROF_DECL;
 #pragma unroll 1
             for (long long i = 0; i < n_my; ++i) {
                 const int b = (int)(i & 1);
+                PROF_T(t0);
                 mbar_wait_sleep(&bready[b], (uint32_t)((i >> 1) & 1));
+                PROF_ADD(prof, 8, t0);
+                PROF_T(t1);
                 if (i >= 2) mbar_wait_sleep(&tfree[b], (uint32_t)(((i >> 1) + 1) & 1));
+                PROF_ADD(prof, 9, t1);
                 const uint32_t acc = tmem + 128u * (uint32_t)b;
                 const uint64_t db = tc::desc_add(dB, (uint32_t)(b * SM::bset));
 #pragma unroll 1
@@ -165,7 +239,9 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_c5_apply(DetectArgs a, con
                     const long long gg = 4 * i + c;
                     const int lb = (int)(gg % NLO);
                     const uint32_t ab = tmem + kAring + kAcols * (uint32_t)lb;
+                    PROF_T(t2);
                     mbar_wait_sleep(&afull[lb], (uint32_t)((gg / NLO) & 1));
+                    PROF_ADD(prof, 10, t2);
                     tc::fence_after();
                     if constexpr (TA == 1) {  // 4 K-steps of 8 per chunk; K atom c of the B set
 #pragma unroll
@@ -190,28 +266,101 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_c5_apply(DetectArgs a, con
                     if (c == 3) tc::commit(&accfull[b]);
                 }
             }
+            PROF_FLUSH(true);
         }
-    } else if (warp < 4) {
-        // ================= converters =================
-        const int tc_ = t;  // 0..127
-        const int n = tc_ >> 2, kt = tc_ & 3, kk = n & 15;
-        const bool im_row = n >= 16;
-        pdl_wait();  // W~ of this call's setup kernel is complete and visible
-        float2 wv[16];
-        float slv = 0.f;
-        auto fetch = [&](long long i) {  // this thread's 16 antennas of W~ row kk of unit i
-            const float2* src = reinterpret_cast<const float2*>(reinterpret_cast<const float*>(a.ws) + (u0 + i * du) * WS);
+    } else {
+        // ---- shared pieces of the converter and epilogue roles
+        // convert RE row r of stage st into TMEM A-ring slot lb, row tile `tile`, this warp's lane quadrant
+        auto convert_row = [&](int st, int lb, int tile, int r, int quad) {
+            const float4* row = reinterpret_cast<const float4*>(g + SM::y0 + st * SM::chunk + (size_t)r * 128);
+            float v[32];
 #pragma unroll
-            for (int c = 0; c < 16; ++c) wv[c] = src[(16 * kt + c) * NL + kk];
-            if (tc_ < NL) slv = reinterpret_cast<const float*>(src + NR * NL)[tc_];
+            for (int cc = 0; cc < 8; ++cc) {
+                const float4 q = row[cc ^ (r & 7)];  // SWIZZLE_128B: 16-byte piece cc of row r
+                v[4 * cc] = q.x;
+                v[4 * cc + 1] = q.y;
+                v[4 * cc + 2] = q.z;
+                v[4 * cc + 3] = q.w;
+            }
+            const uint32_t ta = tmem + ((uint32_t)(32 * quad) << 16) + kAring + kAcols * (uint32_t)lb;
+            if constexpr (TA == 1) {
+                uint32_t lo[32];
+#pragma unroll
+                for (int k = 0; k < 32; ++k) lo[k] = __float_as_uint(v[k] - tc::tf32_trunc(v[k]));
+                tc::st32(ta + 64u * tile, reinterpret_cast<const uint32_t*>(v));
+                tc::st32(ta + 64u * tile + 32u, lo);
+            } else {
+                uint32_t pk[32];
+#pragma unroll
+                for (int k2 = 0; k2 < 16; ++k2) tc::split_bf2(v[2 * k2], v[2 * k2 + 1], pk[k2], pk[16 + k2]);
+                tc::st32(ta + 32u * tile, pk);
+            }
         };
-        if (n_my > 0) fetch(0);
-#pragma unroll 1
-        for (long long i = 0; i < n_my; ++i) {
-            const int b = (int)(i & 1);
-            // B set b is free once unit i-2's MMAs completed; the slope ring slot i & 3 was last read
-            // by epilogue(i-4), which finished before tfree(i-4) < accfull(i-2)
-            if (i >= 2) mbar_wait_sleep(&accfull[b], (uint32_t)(((i >> 1) + 1) & 1));
+        constexpr int kRec = NL * QM * LlrTraits<LT>::bytes;
+        const bool zf = !(a.sigma2 > 0.f);
+        const float ia = rsqrtf((float)qam_norm(QM));
+        // x~ of RE `row` (TMEM lane quadrant `quad`, accumulator b, row tile `tile`) -> LLR record
+        auto epilogue_row = [&](long long i, int b, int tile, int row, int quad, bool active) {
+            uint32_t hv[32], lv[32];
+            const uint32_t taddr = tmem + ((uint32_t)(32 * quad) << 16) + 128u * (uint32_t)b + 64u * tile;
+            tc::ld32(taddr, hv);
+            tc::ld32(taddr + 32u, lv);
+            tc::wait_ld();
+            if (!active) return;
+            const long long u = u0 + i * du;
+            const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);
+            const int s = row / kSc, f = row % kSc;
+            const size_t re = (size_t)(slot * kSym + s) * a.n_sc + fb * kSc + f;
+            float2 x[NL];
+#pragma unroll
+            for (int k = 0; k < NL; ++k)
+                x[k] = make_float2(__uint_as_float(hv[k]) + __uint_as_float(lv[k]),
+                                   __uint_as_float(hv[16 + k]) + __uint_as_float(lv[16 + k]));
+            const float* sl = sslope + (i & 3) * 16;
+            if (a.llr) {
+                uint32_t wd[(kRec + 3) / 4];
+                if (LT == kLlrI8 && !zf) {
+                    uint32_t q[NL * QM];
+                    const float* rs = sslope + 64 + (i & 3) * 16;
+#pragma unroll
+                    for (int k = 0; k < NL; ++k) {
+                        demap_axis_i8<QM / 2>(x[k].x, rs[k], q + k * QM, 2);
+                        demap_axis_i8<QM / 2>(x[k].y, rs[k], q + k * QM + 1, 2);
+                    }
+#pragma unroll
+                    for (int w4 = 0; w4 < NL * QM / 4; ++w4)
+                        wd[w4] = __byte_perm(__byte_perm(q[4 * w4], q[4 * w4 + 1], 0x0040),
+                                             __byte_perm(q[4 * w4 + 2], q[4 * w4 + 3], 0x0040), 0x5410);
+                } else {
+                    float v[NL * QM];
+                    if (!zf) {
+#pragma unroll
+                        for (int k = 0; k < NL; ++k) demap_layer<QM, false, LT>(x[k], sl[k], v + k * QM);
+                        pack_llr<LT, NL * QM, false>(v, wd);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < NL; ++k) demap_layer<QM, true, LT>(x[k], sl[k], v + k * QM);
+                        pack_llr<LT, NL * QM, true>(v, wd);
+                    }
+                }
+                store_bytes<kRec>((char*)a.llr + re * kRec, wd);
+            }
+            if (a.xhat) {
+#pragma unroll
+                for (int k = 0; k < NL; ++k) a.xhat[re * NL + k] = make_float2(x[k].x * ia, x[k].y * ia);
+            }
+        };
+
+        // B = [B_hi; B_lo] of unit i (bf16 or tf32 split of the real form of W~) into B set i & 1, and the
+        // unit's slopes into slope ring slot i & 3; tid in 0..127 of the building warp group
+        auto build_B = [&](long long i, int tid) {
+            const int n = tid >> 2, kt = tid & 3, kk = n & 15, b = (int)(i & 1);
+            const bool im_row = n >= 16;
+            mbar_wait_sleep(&wfull[i & 1], (uint32_t)((i >> 1) & 1));
+            const float2* src = reinterpret_cast<const float2*>(g + SM::wst + (i & 1) * SM::wrec);
+            float2 wv[16];
+#pragma unroll
+            for (int c = 0; c < 16; ++c) wv[c] = src[(16 * kt + c) * NL + kk];  // this thread's 16 antennas of row kk
             if constexpr (TA == 1) {
                 float* kb = reinterpret_cast<float*>(g + SM::B + b * SM::bset + (size_t)kt * 64 * 128);
 #pragma unroll
@@ -241,126 +390,112 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_c5_apply(DetectArgs a, con
                     *reinterpret_cast<uint4*>(kb + (n + 32) * 128 + ((q ^ (n & 7)) << 4)) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
                 }
             }
-            if (tc_ < NL) {
-                sslope[(i & 3) * 16 + tc_] = slv;
-                sslope[64 + (i & 3) * 16 + tc_] = sqrtf(slv * (1.f / 127.f));
+            if (tid < NL) {
+                const float slv = reinterpret_cast<const float*>(src + NR * NL)[tid];
+                sslope[(i & 3) * 16 + tid] = slv;
+                sslope[64 + (i & 3) * 16 + tid] = sqrtf(slv * (1.f / 127.f));
             }
             tc::fence_proxy_async();
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (tc_ == 0) mbar_arrive(&bready[b]);
-            if (i + 1 < n_my) fetch(i + 1);
+        };
+
+        if (warp < 4) {
+            // ================= converter group: y rows -> TMEM A ring (+ the B sets unless BEPI) =================
+            const int tc_ = t;  // 0..127
+            PROF_DECL;
 #pragma unroll 1
-            for (int c = 0; c < 4; ++c) {
-                const long long gg = 4 * i + c;
-                const int st = (int)(gg % S), lb = (int)(gg % NLO);
-                mbar_wait_sleep(&yfull[st], (uint32_t)((gg / S) & 1));
-                if (gg >= NLO) mbar_wait_sleep(&afree[lb], (uint32_t)(((gg / NLO) + 1) & 1));
+            for (long long i = 0; i < n_my; ++i) {
+                const int b = (int)(i & 1);
+                if constexpr (!BEPI) {
+                    // B set b is free once unit i-2's MMAs completed; the slope ring slot i & 3 was last read
+                    // by epilogue(i-4), which finished before tfree(i-4) < accfull(i-2)
+                    PROF_T(t0);
+                    if (i >= 2) mbar_wait_sleep(&accfull[b], (uint32_t)(((i >> 1) + 1) & 1));
+                    PROF_ADD(prof, 16, t0);
+                    PROF_T(t1);
+                    build_B(i, tc_);
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (tc_ == 0) {
+                        mbar_arrive(&bready[b]);
+                        mbar_arrive(&wfree[b]);
+                    }
+                    PROF_ADD(prof, 17, t1);
+                }
+#pragma unroll 1
+                for (int c = 0; c < 4; ++c) {
+                    const long long gg = 4 * i + c;
+                    const int st = (int)(gg % S), lb = (int)(gg % NLO);
+                    PROF_T(t2);
+                    mbar_wait_sleep(&yfull[st], (uint32_t)((gg / S) & 1));
+                    PROF_ADD(prof, 18, t2);
+                    PROF_T(t3);
+                    if (gg >= NLO) mbar_wait_sleep(&afree[lb], (uint32_t)(((gg / NLO) + 1) & 1));
+                    PROF_ADD(prof, 19, t3);
+                    PROF_T(t4);
+                    tc::fence_after();
+                    convert_row(st, lb, 0, 32 * warp + lane, warp);
+                    if (warp < 2) convert_row(st, lb, 1, min(128 + 32 * warp + lane, kRe - 1), warp);  // REs 128-167
+                    tc::wait_st();
+                    PROF_ADD(prof, 20, t4);
+                    PROF_T(t5);
+                    tc::fence_before();
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (tc_ == 0) {
+                        mbar_arrive(&afull[lb]);
+                        mbar_arrive(&yfree[st]);
+                    }
+                    PROF_ADD(prof, 21, t5);
+                }
+            }
+            PROF_FLUSH(t == 0);
+        } else {
+            // ================= epilogue: tile 0 on warps 4-7, compact tile 1 on warps 8-9 =================
+            // (BEPI: warps 4-7 also build the B set of unit i + 2 as soon as unit i's MMAs completed)
+            const int e = warp - 4, we = e & 3, tile = e >> 2;
+            PROF_DECL;
+            if constexpr (BEPI) {
+                if (warp < 8) {
+                    for (long long i0 = 0; i0 < 2 && i0 < n_my; ++i0) build_B(i0, t - 128);
+                    asm volatile("bar.sync 4, 128;" ::: "memory");
+                    if (t == 128) {
+                        mbar_arrive(&bready[0]);
+                        mbar_arrive(&wfree[0]);
+                        if (n_my > 1) {
+                            mbar_arrive(&bready[1]);
+                            mbar_arrive(&wfree[1]);
+                        }
+                    }
+                }
+            }
+#pragma unroll 1
+            for (long long i = 0; i < n_my; ++i) {
+                const int b = (int)(i & 1);
+                PROF_T(t0);
+                mbar_wait_sleep(&accfull[b], (uint32_t)((i >> 1) & 1));
+                PROF_ADD(prof, 24, t0);
                 tc::fence_after();
-                const unsigned char* ysm = g + SM::y0 + st * SM::chunk;
-#pragma unroll
-                for (int tile = 0; tile < 2; ++tile) {
-                    if (CT && tile == 1 && warp >= 2) break;
-                    const int r = tile ? (CT ? min(128 + 32 * warp + lane, kRe - 1) : 40 + 32 * warp + lane) : 32 * warp + lane;
-                    const float4* row = reinterpret_cast<const float4*>(ysm + (size_t)r * 128);
-                    float v[32];
-#pragma unroll
-                    for (int cc = 0; cc < 8; ++cc) {
-                        const float4 q = row[cc ^ (r & 7)];  // SWIZZLE_128B: 16-byte piece cc of row r
-                        v[4 * cc] = q.x;
-                        v[4 * cc + 1] = q.y;
-                        v[4 * cc + 2] = q.z;
-                        v[4 * cc + 3] = q.w;
-                    }
-                    const uint32_t ta = tmem + ((uint32_t)(32 * warp) << 16) + kAring + kAcols * (uint32_t)lb;
-                    if constexpr (TA == 1) {
-                        uint32_t lo[32];
-#pragma unroll
-                        for (int k = 0; k < 32; ++k) lo[k] = __float_as_uint(v[k] - tc::tf32_trunc(v[k]));
-                        tc::st32(ta + 64u * tile, reinterpret_cast<const uint32_t*>(v));
-                        tc::st32(ta + 64u * tile + 32u, lo);
-                    } else {
-                        uint32_t pk[32];
-#pragma unroll
-                        for (int k2 = 0; k2 < 16; ++k2) tc::split_bf2(v[2 * k2], v[2 * k2 + 1], pk[k2], pk[16 + k2]);
-                        tc::st32(ta + 32u * tile, pk);
+                if constexpr (BEPI) {
+                    if (warp < 8 && i + 2 < n_my) {  // B set b is free: unit i's MMAs completed
+                        PROF_T(tb);
+                        build_B(i + 2, t - 128);
+                        asm volatile("bar.sync 4, 128;" ::: "memory");
+                        if (t == 128) {
+                            mbar_arrive(&bready[b]);
+                            mbar_arrive(&wfree[b]);
+                        }
+                        PROF_ADD(prof, 27, tb);
                     }
                 }
-                tc::wait_st();
+                PROF_T(t1);
+                const int row = (tile ? 128 : 0) + 32 * we + lane;
+                epilogue_row(i, b, tile, row, we, row < kRe);
+                PROF_ADD(prof, 25, t1);
+                PROF_T(t2);
                 tc::fence_before();
-                asm volatile("bar.sync 1, 128;" ::: "memory");
-                if (tc_ == 0) {
-                    mbar_arrive(&afull[lb]);
-                    mbar_arrive(&yfree[st]);
-                }
+                asm volatile("bar.sync 2, %0;" ::"r"(32 * EW) : "memory");
+                if (t == 128) mbar_arrive(&tfree[b]);
+                PROF_ADD(prof, 26, t2);
             }
-        }
-    } else {
-        // ================= epilogue =================
-        const int e = warp - 4, we = e & 3;
-        constexpr int kRec = NL * QM * LlrTraits<LT>::bytes;
-        const bool zf = !(a.sigma2 > 0.f);
-        const float ia = rsqrtf((float)qam_norm(QM));
-#pragma unroll 1
-        for (long long i = 0; i < n_my; ++i) {
-            const int b = (int)(i & 1);
-            const long long u = u0 + i * du;
-            const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);
-            mbar_wait_sleep(&accfull[b], (uint32_t)((i >> 1) & 1));
-            tc::fence_after();
-#pragma unroll 1
-            for (int tile = CT ? (e >> 2) : 0; tile < (CT ? (e >> 2) + 1 : 2); ++tile) {
-                if (!CT && tile == 1 && we < 2) break;
-                uint32_t hv[32], lv[32];
-                const uint32_t taddr = tmem + ((uint32_t)(32 * we) << 16) + 128u * (uint32_t)b + 64u * tile;
-                tc::ld32(taddr, hv);
-                tc::ld32(taddr + 32u, lv);
-                tc::wait_ld();
-                const int row = (tile ? (CT ? 128 : 40) : 0) + 32 * we + lane;
-                if (tile == 1 && (CT ? row >= kRe : row < 128)) continue;
-                const int s = row / kSc, f = row % kSc;
-                const size_t re = (size_t)(slot * kSym + s) * a.n_sc + fb * kSc + f;
-                float2 x[NL];
-#pragma unroll
-                for (int k = 0; k < NL; ++k)
-                    x[k] = make_float2(__uint_as_float(hv[k]) + __uint_as_float(lv[k]),
-                                       __uint_as_float(hv[16 + k]) + __uint_as_float(lv[16 + k]));
-                const float* sl = sslope + (i & 3) * 16;
-                if (a.llr) {
-                    uint32_t wd[(kRec + 3) / 4];
-                    if (LT == kLlrI8 && !zf) {
-                        uint32_t q[NL * QM];
-                        const float* rs = sslope + 64 + (i & 3) * 16;
-#pragma unroll
-                        for (int k = 0; k < NL; ++k) {
-                            demap_axis_i8<QM / 2>(x[k].x, rs[k], q + k * QM, 2);
-                            demap_axis_i8<QM / 2>(x[k].y, rs[k], q + k * QM + 1, 2);
-                        }
-#pragma unroll
-                        for (int w4 = 0; w4 < NL * QM / 4; ++w4)
-                            wd[w4] = __byte_perm(__byte_perm(q[4 * w4], q[4 * w4 + 1], 0x0040),
-                                                 __byte_perm(q[4 * w4 + 2], q[4 * w4 + 3], 0x0040), 0x5410);
-                    } else {
-                        float v[NL * QM];
-                        if (!zf) {
-#pragma unroll
-                            for (int k = 0; k < NL; ++k) demap_layer<QM, false, LT>(x[k], sl[k], v + k * QM);
-                            pack_llr<LT, NL * QM, false>(v, wd);
-                        } else {
-#pragma unroll
-                            for (int k = 0; k < NL; ++k) demap_layer<QM, true, LT>(x[k], sl[k], v + k * QM);
-                            pack_llr<LT, NL * QM, true>(v, wd);
-                        }
-                    }
-                    store_bytes<kRec>((char*)a.llr + re * kRec, wd);
-                }
-                if (a.xhat) {
-#pragma unroll
-                    for (int k = 0; k < NL; ++k) a.xhat[re * NL + k] = make_float2(x[k].x * ia, x[k].y * ia);
-                }
-            }
-            tc::fence_before();
-            asm volatile("bar.sync 2, %0;" ::"r"(32 * EW) : "memory");
-            if (t == 128) mbar_arrive(&tfree[b]);
+            PROF_FLUSH(t == 128);
         }
     }
     tc::fence_before();
@@ -369,39 +504,38 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_c5_apply(DetectArgs a, con
 }
 
 // ------------------------------------------------------------------------
-// k_c5_setup: rows a2-a5 with the two contractions on the tensor cores and the
-// factorisation on the FP32 pipe, two H-units per batch per CTA (4 warps):
+// k_c5_setup: rows a2-a5 with both contractions on the tensor cores (BF16 split
+// operands, reading R28) and the 16 x 16 inversion on the FP32 pipe. One CTA =
+// 4 warps = 4 H-units per batch (warp w owns unit w of the batch):
 //   a1  H_u (64 x 16 complex = 64 x 32 real X, row r = antenna) by a 2-D TMA box
-//       (SWIZZLE_128B); X_lo = X - trunc(X) beside it (reading R21, TF32 split);
-//   a2  C = Xe^T Xe with Xe = X + X_lo: 16 kind::tf32 MMAs (M = 64 = [X | X_lo]
-//       columns, N = 32, K = 64 antennas), both operands MN-major views of the
-//       same smem tile; G_kl = (C[2k][2l] + C[2k+1][2l+1]) + i (C[2k][2l+1] -
-//       C[2k+1][2l]) + sigma2 delta_kl;
-//   a3  G = L L^H, right-looking Cholesky in registers, one lane per row, the two
-//       units in the two half-warps of warp 0, guard R17 on every pivot;
-//   a4  X = L^-1 by forward substitution (lane k: column k), [G^-1]_kl = sum_i
-//       conj(X_ik) X_il, A_kk = sum_i |X_ik|^2;
-//   a5  mu, SINR, fac = sqrt(norm)/mu (readings R3/R4), B = real form of fac G^-1;
-//   a4  W~^T = X B on the tensor cores: 8 kind::tf32 MMAs (M = 128 = [X; X_lo]
-//       rows, N = 32, K = 32), W~[r] = D[r] + D[64 + r] -> workspace [r][k].
-// The 64-row accumulators span all four TMEM lane quadrants, so every warp reads
-// its quadrant and the halves meet in shared memory.
+//       (fp32, SWIZZLE_128B), converted to XB = [X_hi | X_lo] (bf16, 128-B row r,
+//       same swizzle), X_hi = rn_bf16(X), X_lo = rn_bf16(X - X_hi);
+//   a2  C = (X_hi + X_lo)^T (X_hi + X_lo): 16 kind::f16 MMAs with BOTH operands the
+//       MN-major view of XB (M = 64 from the hi, then the lo columns, N = 32 hi then 32
+//       lo, K = 64 antennas), C in D rows 0-31; G_kl = (C[2k][2l] + C[2k+1][2l+1]) +
+//       i (C[2k][2l+1] - C[2k+1][2l]) + sigma2 delta_kl;
+//   a3-a5  G^-1 by in-place Gauss-Jordan (no pivoting: G is Hermitian PD; its
+//       pivots are the LDL^H pivots, so guard R17 reads the same quantities as
+//       Cholesky's d_jj^2 -- reading R26), mu, SINR, fac = sqrt(norm) / mu,
+//       B = real form of fac G^-1, split into bf16 hi / lo and duplicated along K;
+//   a4  W~^T = XB B'^T: 8 kind::f16 MMAs, A = the K-major view of the SAME XB tile
+//       (K = 64 = hi | lo halves of the 32 real inputs), B' = [B | B] (hi, lo).
+// TMEM: 32 columns per unit (the Gram accumulator, reused for W~). M = 64
+// accumulators put row m in lane 32 (m / 16) + m % 16, so every warp reads its
+// lane quadrant of W~, and warps 0-1 read C.
+// (A persistent warp-specialised variant -- producer, MMA, readout and 12 worker warps
+// over a ring of unit slots -- measured 107-124 us against this kernel's 90, the
+// per-slot chain of H load, Gram round trip and inversion being sequential.)
 namespace su {
-constexpr int UPB = 2;                        // units per batch
-constexpr size_t X = 0;                       // [UPB] x (X 8 KiB | X_lo 8 KiB)
-constexpr size_t BG = UPB * 16384;            // [UPB] x (B_hi 4 KiB | B_lo 4 KiB); also the exchange buffers
-constexpr size_t CS = BG + 8192;              // [UPB][32][32] float C (G assembly), then X^-T rows; dead when
-                                              // B is written (aliases unit 1's B set)
+constexpr int UPB = 4;                   // units per batch (= warps)
+constexpr size_t XB = 0;                 // [UPB] x 8 KiB  bf16 [64 r][hi c 0..31 | lo c 0..31], SW128
+constexpr size_t BG = UPB * 8192;        // [UPB] x 8 KiB  H landing (fp32) -> exchange | C -> B'_hi | B'_lo
 constexpr size_t BAR = BG + UPB * 8192;
 constexpr size_t TSLOT = BAR + 16;
-constexpr size_t TOTAL = TSLOT + 16 + 1024;   // + alignment slack
-constexpr int CTAS_PER_SM = 4;
+constexpr size_t TOTAL = TSLOT + 16 + 1024;  // + 1024-B alignment slack
+constexpr int CTAS_PER_SM = 3;
 static_assert(TOTAL * CTAS_PER_SM <= 227 * 1024, "shared memory");
 }  // namespace su
-
-__device__ __forceinline__ float2 cmul_conj_a(float2 a, float2 b) {  // conj(a) * b
-    return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.x, b.y, -a.y * b.x));
-}
 
 template <int QM>
 __global__ void __launch_bounds__(128, su::CTAS_PER_SM) k_c5_setup(DetectArgs a, const __grid_constant__ CUtensorMap hmap) {
@@ -414,7 +548,6 @@ __global__ void __launch_bounds__(128, su::CTAS_PER_SM) k_c5_setup(DetectArgs a,
     uint64_t* bar_tma = reinterpret_cast<uint64_t*>(g + su::BAR);
     uint64_t* bar_mma = bar_tma + 1;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(g + su::TSLOT);
-    float* Cs = reinterpret_cast<float*>(g + su::CS);
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const float norm = (float)qam_norm(QM);
     const long long n_batch = (a.n_units + su::UPB - 1) / su::UPB;
@@ -426,171 +559,152 @@ __global__ void __launch_bounds__(128, su::CTAS_PER_SM) k_c5_setup(DetectArgs a,
         fence_mbar_init();
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&hmap)) : "memory");
     }
-    if (warp == 0) tc::alloc<64>(tslot);
+    if (warp == 0) tc::alloc<128>(tslot);
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
     const uint32_t tmem = *tslot;
-    bool waited = false;  // PDL: wait for the previous grid before the first workspace write
+    bool waited = false;  // PDL: the previous call may still read the workspace
     uint32_t it = 0;
 #pragma unroll 1
     for (long long bt = blockIdx.x; bt < n_batch; bt += gridDim.x, ++it) {
         const long long ub = bt * su::UPB;
         const int nv = (int)min((long long)su::UPB, a.n_units - ub);  // valid units in this batch
-        // ---- a1: H of the batch's units
+        // ---- a1: H of the batch (fp32, SW128) into the B regions, then XB = bf16 hi | lo
         if (t == 0) {
             mbar_arrive_expect_tx(bar_tma, (uint32_t)(nv * NR * NL * 8));
             for (int s = 0; s < nv; ++s)
                 asm volatile(
                     "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-                    ::"r"(base + (uint32_t)(su::X + s * 16384)), "l"(reinterpret_cast<uint64_t>(&hmap)), "r"(0),
+                    ::"r"(base + (uint32_t)(su::BG + s * 8192)), "l"(reinterpret_cast<uint64_t>(&hmap)), "r"(0),
                     "r"((int)((ub + s) * NR)), "r"(smem_u32(bar_tma))
                     : "memory");
         }
         mbar_wait(bar_tma, it & 1);
-        {  // X_lo = X - trunc(X) (same offsets: the SWIZZLE_128B pattern depends on address bits < 1024)
-            for (int q = t; q < su::UPB * 512; q += 128) {
-                const int s = q >> 9, o = q & 511;
-                const float4 v = reinterpret_cast<const float4*>(g + su::X + s * 16384)[o];
-                reinterpret_cast<float4*>(g + su::X + s * 16384 + 8192)[o] =
-                    make_float4(v.x - tc::tf32_trunc(v.x), v.y - tc::tf32_trunc(v.y), v.z - tc::tf32_trunc(v.z),
-                                v.w - tc::tf32_trunc(v.w));
-            }
+#pragma unroll 2
+        for (int q = t; q < su::UPB * 256; q += 128) {  // item = (unit, row r, 8 columns 8 cp .. 8 cp + 7)
+            const int s = q >> 8, r = (q >> 2) & 63, cp = q & 3, sw = r & 7;
+            const unsigned char* src = g + su::BG + s * 8192 + r * 128;
+            const float4 v0 = *reinterpret_cast<const float4*>(src + (((2 * cp) ^ sw) << 4));
+            const float4 v1 = *reinterpret_cast<const float4*>(src + (((2 * cp + 1) ^ sw) << 4));
+            uint32_t hi[4], lo[4];
+            tc::split_bf2(v0.x, v0.y, hi[0], lo[0]);
+            tc::split_bf2(v0.z, v0.w, hi[1], lo[1]);
+            tc::split_bf2(v1.x, v1.y, hi[2], lo[2]);
+            tc::split_bf2(v1.z, v1.w, hi[3], lo[3]);
+            unsigned char* dst = g + su::XB + s * 8192 + r * 128;
+            *reinterpret_cast<uint4*>(dst + ((cp ^ sw) << 4)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+            *reinterpret_cast<uint4*>(dst + (((4 + cp) ^ sw) << 4)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
         }
         tc::fence_proxy_async();
         tc::fence_before();
         __syncthreads();
-        // ---- a2: Gram on the tensor cores
+        // ---- a2: Gram, MN-major XB as both operands: C = (hi + lo)^T (hi + lo) lands in D rows 0-31 (A = the
+        // hi columns, then, from start + 64 B, the lo columns; D rows 32-63 then read past the tile: unused)
         if (t == 0) {
             tc::fence_after();
-            constexpr uint32_t idg = tc::idesc(tc::kFmtTF32, 64, 32, 1, 1);
+            constexpr uint32_t idg = tc::idesc(tc::kFmtBF16, 64, 32, 1, 1);
             for (int s = 0; s < su::UPB; ++s) {
-                const uint32_t xs = base + (uint32_t)(su::X + s * 16384);
+                const uint32_t xs = base + (uint32_t)(su::XB + s * 8192);
 #pragma unroll
-                for (int ks = 0; ks < 8; ++ks) {  // K = antennas 8 ks .. 8 ks + 7 = one 1024-B atom
-                    const uint64_t dA = tc::desc_sw128(xs + 1024u * ks, 8192, 1024);  // M atoms: X cols | X_lo cols
-                    tc::mma_tf32_ss(tmem + 32u * s, dA, tc::desc_sw128(xs + 1024u * ks, 8192, 1024), idg, ks ? 1u : 0u);
-                    tc::mma_tf32_ss(tmem + 32u * s, dA, tc::desc_sw128(xs + 8192u + 1024u * ks, 8192, 1024), idg, 1u);
+                for (int ks = 0; ks < 4; ++ks) {  // K = antennas 16 ks .. 16 ks + 15 = two 8-row atoms
+                    const uint64_t dh = tc::desc_sw128(xs + 2048u * ks, 16, 1024);
+                    const uint64_t dl = tc::desc_sw128(xs + 64u + 2048u * ks, 16, 1024);
+                    tc::mma_f16_ss(tmem + 32u * s, dh, dh, idg, ks ? 1u : 0u);
+                    tc::mma_f16_ss(tmem + 32u * s, dh, dl, idg, 1u);
+                    tc::mma_f16_ss(tmem + 32u * s, dl, dh, idg, 1u);
+                    tc::mma_f16_ss(tmem + 32u * s, dl, dl, idg, 1u);
                 }
             }
             tc::commit(bar_mma);
         }
         mbar_wait(bar_mma, 0);
         tc::fence_after();
-        {  // M = 64 accumulator: row m in TMEM lane 32 (m / 16) + m % 16; C = D[0:32] + D[32:64]
-            float* ex = reinterpret_cast<float*>(g + su::BG);  // [UPB][32][32]
+        if (warp < 2) {  // M = 64 accumulator: row m in TMEM lane 32 (m / 16) + m % 16 -> C rows 16 warp + lane
 #pragma unroll 1
             for (int s = 0; s < su::UPB; ++s) {
                 uint32_t v[32];
                 tc::ld32(tmem + ((uint32_t)(32 * warp) << 16) + 32u * s, v);
                 tc::wait_ld();
-                if (warp >= 2 && lane < 16) {
-                    float4* dst = reinterpret_cast<float4*>(ex + (s * 32 + 16 * (warp - 2) + lane) * 32);
+                if (lane < 16) {
+                    const int m = 16 * warp + lane;
+                    float* cs = reinterpret_cast<float*>(g + su::BG + s * 8192 + 4096);
 #pragma unroll
                     for (int c = 0; c < 8; ++c)
-                        dst[c ^ (lane & 7)] = make_float4(__uint_as_float(v[4 * c]), __uint_as_float(v[4 * c + 1]),
-                                                          __uint_as_float(v[4 * c + 2]), __uint_as_float(v[4 * c + 3]));
-                }
-                __syncthreads();
-                if (warp < 2 && lane < 16) {
-                    const int m = 16 * warp + lane;
-                    const float4* src = reinterpret_cast<const float4*>(ex + (s * 32 + m) * 32);
-                    float4* dst = reinterpret_cast<float4*>(Cs + (s * 32 + m) * 32);
-#pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const float4 e = src[c ^ (lane & 7)];
-                        dst[c] = make_float4(__uint_as_float(v[4 * c]) + e.x, __uint_as_float(v[4 * c + 1]) + e.y,
-                                             __uint_as_float(v[4 * c + 2]) + e.z, __uint_as_float(v[4 * c + 3]) + e.w);
-                    }
+                        reinterpret_cast<float4*>(cs + m * 32)[c ^ (m & 7)] =
+                            make_float4(__uint_as_float(v[4 * c]), __uint_as_float(v[4 * c + 1]),
+                                        __uint_as_float(v[4 * c + 2]), __uint_as_float(v[4 * c + 3]));
                 }
             }
         }
         tc::fence_before();
         __syncthreads();
-        // ---- a3-a5: Cholesky, inverse, SINR and the B operand (warp 0; unit h = lane / 16, row k = lane % 16)
-        if (warp == 0) {
-            if (!waited) {
-                pdl_wait();  // the previous call may still read the workspace
-                waited = true;
-            }
-            const int h = lane >> 4, k = lane & 15, hb = lane & 16;
-            const long long u = ub + h;
-            const bool valid = h < nv;
+        // ---- a3-a5: warp w inverts unit w; lane (k, h) = (lane / 2, lane % 2) holds G[k][8h .. 8h+7]
+        if (!waited) {
+            pdl_wait();
+            waited = true;
+        }
+        {
+            const int s = warp, k = lane >> 1, h = lane & 1;
+            const long long u = ub + s;
+            const bool valid = s < nv;
             const float s2 = unit_sigma2(a, valid ? u : ub);
-            float2 gr[NL];
+            const float* cs = reinterpret_cast<const float*>(g + su::BG + s * 8192 + 4096);
+            float2 gq[8];
             {
-                const float* c0 = Cs + (h * 32 + 2 * k) * 32;
-                const float* c1 = c0 + 32;
+                const int m0 = 2 * k, m1 = 2 * k + 1;
 #pragma unroll
-                for (int l = 0; l < NL; ++l) gr[l] = make_float2(c0[2 * l] + c1[2 * l + 1], c0[2 * l + 1] - c1[2 * l]);
+                for (int i = 0; i < 4; ++i) {  // columns 16h + 4i .. +3 = layers 8h + 2i, 8h + 2i + 1
+                    const float4 c0 = reinterpret_cast<const float4*>(cs + m0 * 32)[(4 * h + i) ^ (m0 & 7)];
+                    const float4 c1 = reinterpret_cast<const float4*>(cs + m1 * 32)[(4 * h + i) ^ (m1 & 7)];
+                    gq[2 * i] = make_float2(c0.x + c1.y, c0.y - c1.x);
+                    gq[2 * i + 1] = make_float2(c0.z + c1.w, c0.w - c1.z);
+                }
             }
+            float gd = 0.f;
 #pragma unroll
-            for (int l = 0; l < NL; ++l)
-                if (l == k) gr[l] = make_float2(gr[l].x + s2, 0.f);
-            float gmax = 0.f;
+            for (int q = 0; q < 8; ++q) {
+                const bool d = 8 * h + q == k;
+                gq[q].x += d ? s2 : 0.f;
+                gq[q].y = d ? 0.f : gq[q].y;
+                gd = fmaxf(gd, d ? gq[q].x : 0.f);
+            }
+            float gmax = gd;
 #pragma unroll
-            for (int l = 0; l < NL; ++l)
-                if (l == k) gmax = gr[l].x;
-#pragma unroll
-            for (int off = 1; off < 16; off <<= 1) gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, off));
+            for (int off = 1; off < 32; off <<= 1) gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, off));
             bool fail = !(gmax == gmax);
             const float tau = (float)kPivotTau * gmax;
-            // a3: right-looking Cholesky; lane k's gr[m] (m <= k) becomes L[k][m]
-            float dinv = 0.f;
+            // pivot loop rolled over the two column halves (hj), unrolled inside (qj): the fully unrolled
+            // elimination is ~1.7k instructions and starves the warps on instruction fetch
+#pragma unroll 1
+            for (int hj = 0; hj < 2; ++hj)
 #pragma unroll
-            for (int j = 0; j < NL; ++j) {
-                float p = __shfl_sync(0xffffffffu, gr[j].x, hb | j);
+            for (int qj = 0; qj < 8; ++qj) {
+                const int j = 8 * hj + qj;
+                const float2 f = shfl2(gq[qj], (lane & ~1) | hj);          // G[k][j]
+                float p = __shfl_sync(0xffffffffu, gq[qj].x, 2 * j + hj);  // G[j][j]
                 if (!(p > tau)) {
                     fail = true;
                     p = 1.f;
                 }
-                const float r = rsqrtf(p);
-                if (k == j) dinv = r;
-                if (k >= j) gr[j] = make_float2(gr[j].x * r, gr[j].y * r);
+                const float pinv = __frcp_rn(p);
+                const bool prow = k == j;
 #pragma unroll
-                for (int m = j + 1; m < NL; ++m) {
-                    const float2 lm = shfl2(gr[j], hb | m);  // L[m][j]
-                    if (k >= m) {  // G[k][m] -= L[k][j] conj(L[m][j])
-                        gr[m].x = fmaf(-gr[j].x, lm.x, fmaf(-gr[j].y, lm.y, gr[m].x));
-                        gr[m].y = fmaf(-gr[j].y, lm.x, fmaf(gr[j].x, lm.y, gr[m].y));
-                    }
+                for (int q = 0; q < 8; ++q) {
+                    float2 rj = shfl2(gq[q], 2 * j + h);  // G[j][8h+q]
+                    if (8 * h + q == j) rj = make_float2(1.f, 0.f);
+                    rj = make_float2(rj.x * pinv, rj.y * pinv);
+                    float2 b = (8 * h + q == j) ? make_float2(0.f, 0.f) : gq[q];
+                    b.x = fmaf(-f.x, rj.x, fmaf(f.y, rj.y, b.x));
+                    b.y = fmaf(-f.x, rj.y, fmaf(-f.y, rj.x, b.y));
+                    gq[q] = prow ? rj : b;
                 }
             }
-            // a4: column k of X = L^-1 by forward substitution: X_ik = -(1/L_ii) sum_{m<i} L_im X_mk
-            float2 x[NL];
+            // A_kk = [G^-1]_kk lives in lane (k, k / 8)
+            float Ad = 0.f;
 #pragma unroll
-            for (int i = 0; i < NL; ++i) {
-                float2 sv = make_float2(0.f, 0.f);
-#pragma unroll
-                for (int m = 0; m < i; ++m) sv = cmac(sv, shfl2(gr[m], hb | i), x[m]);
-                const float di = __shfl_sync(0xffffffffu, dinv, hb | i);
-                x[i] = (i == k) ? make_float2(di, 0.f) : (i < k ? make_float2(0.f, 0.f) : make_float2(-sv.x * di, -sv.y * di));
-            }
-            float A = 0.f;
-#pragma unroll
-            for (int i = 0; i < NL; ++i) A = fmaf(x[i].x, x[i].x, fmaf(x[i].y, x[i].y, A));
-            // columns of X through shared memory (row k of Xt = column k of X), then row k of G^-1
-            float2* Xt = reinterpret_cast<float2*>(Cs) + h * NL * NL;
-            __syncwarp();
-#pragma unroll
-            for (int i = 0; i < NL; i += 2)
-                *reinterpret_cast<float4*>(Xt + k * NL + i) = make_float4(x[i].x, x[i].y, x[i + 1].x, x[i + 1].y);
-            __syncwarp();
-            float2 gi[NL];
-#pragma unroll
-            for (int l = 0; l < NL; ++l) {
-                float2 sv = make_float2(0.f, 0.f);
-#pragma unroll
-                for (int i = l & ~1; i < NL; i += 2) {  // X_il = 0 for i < l
-                    const float4 v = *reinterpret_cast<const float4*>(Xt + l * NL + i);
-                    const float2 c0 = cmul_conj_a(x[i], make_float2(v.x, v.y));
-                    const float2 c1 = cmul_conj_a(x[i + 1], make_float2(v.z, v.w));
-                    sv.x += c0.x + c1.x;
-                    sv.y += c0.y + c1.y;
-                }
-                gi[l] = sv;
-            }
-            // a5
+            for (int q = 0; q < 8; ++q) Ad += (8 * h + q == k) ? gq[q].x : 0.f;
+            const float A = Ad + __shfl_xor_sync(0xffffffffu, Ad, 1);
             const float mu = fmaf(-s2, A, 1.f);
             float sinr, fac;
             if (s2 == 0.f) {
@@ -604,26 +718,31 @@ __global__ void __launch_bounds__(128, su::CTAS_PER_SM) k_c5_setup(DetectArgs a,
                 sinr = 0.f;
                 fac = 0.f;
             }
-            // B operand of W~^T = X B: rows k (Re W~_k) and 16 + k (Im W~_k), K = (Re, Im) of layer j
-            __syncwarp();  // every lane is done with Xt / C (aliased by the B sets)
-            unsigned char* bg = g + su::BG + h * 8192;
+            __syncwarp();  // C is read; its region becomes B'_lo
+            // B' rows k (Re W~_k) and 16 + k (Im W~_k): K pair (2l, 2l+1) = (Re, Im) parts, duplicated over
+            // the hi | lo halves of K (chunks c and 4 + c); this lane's layers l = 8h .. 8h+7 = chunks 2h, 2h+1
+            unsigned char* bh = g + su::BG + s * 8192;
+            unsigned char* bl = bh + 4096;
 #pragma unroll
-            for (int c = 0; c < 8; ++c) {
-                const float2 g0 = make_float2(fac * gi[2 * c].x, fac * gi[2 * c].y);
-                const float2 g1 = make_float2(fac * gi[2 * c + 1].x, fac * gi[2 * c + 1].y);
-                const float4 vr = make_float4(g0.x, g0.y, g1.x, g1.y);
-                const float4 vi = make_float4(g0.y, -g0.x, g1.y, -g1.x);
-                const int nr = k, ni = 16 + k;
-                *reinterpret_cast<float4*>(bg + nr * 128 + ((c ^ (nr & 7)) << 4)) = vr;
-                *reinterpret_cast<float4*>(bg + ni * 128 + ((c ^ (ni & 7)) << 4)) = vi;
-                *reinterpret_cast<float4*>(bg + 4096 + nr * 128 + ((c ^ (nr & 7)) << 4)) =
-                    make_float4(vr.x - tc::tf32_trunc(vr.x), vr.y - tc::tf32_trunc(vr.y), vr.z - tc::tf32_trunc(vr.z),
-                                vr.w - tc::tf32_trunc(vr.w));
-                *reinterpret_cast<float4*>(bg + 4096 + ni * 128 + ((c ^ (ni & 7)) << 4)) =
-                    make_float4(vi.x - tc::tf32_trunc(vi.x), vi.y - tc::tf32_trunc(vi.y), vi.z - tc::tf32_trunc(vi.z),
-                                vi.w - tc::tf32_trunc(vi.w));
+            for (int cc = 0; cc < 2; ++cc) {
+                uint32_t rh[4], rl[4], ih[4], il[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 w = make_float2(fac * gq[4 * cc + e].x, fac * gq[4 * cc + e].y);
+                    tc::split_bf2(w.x, w.y, rh[e], rl[e]);
+                    tc::split_bf2(w.y, -w.x, ih[e], il[e]);
+                }
+                const int c = 2 * h + cc, nr = k, ni = 16 + k;
+#pragma unroll
+                for (int dup = 0; dup < 2; ++dup) {
+                    const int cd = c + 4 * dup;
+                    *reinterpret_cast<uint4*>(bh + nr * 128 + ((cd ^ (nr & 7)) << 4)) = make_uint4(rh[0], rh[1], rh[2], rh[3]);
+                    *reinterpret_cast<uint4*>(bl + nr * 128 + ((cd ^ (nr & 7)) << 4)) = make_uint4(rl[0], rl[1], rl[2], rl[3]);
+                    *reinterpret_cast<uint4*>(bh + ni * 128 + ((cd ^ (ni & 7)) << 4)) = make_uint4(ih[0], ih[1], ih[2], ih[3]);
+                    *reinterpret_cast<uint4*>(bl + ni * 128 + ((cd ^ (ni & 7)) << 4)) = make_uint4(il[0], il[1], il[2], il[3]);
+                }
             }
-            if (valid) {
+            if (valid && h == 0) {
                 float* wsu = reinterpret_cast<float*>(a.ws) + u * WS;
                 wsu[NR * NL * 2 + k] = sinr / norm * a.llr_scale;
                 if (a.sinr) a.sinr[u * NL + k] = sinr;
@@ -631,69 +750,48 @@ __global__ void __launch_bounds__(128, su::CTAS_PER_SM) k_c5_setup(DetectArgs a,
             }
         }
         tc::fence_proxy_async();
+        tc::fence_before();
         __syncthreads();
-        // ---- a4: W~^T = [X; X_lo] (B_hi + B_lo) on the tensor cores
+        // ---- a4: W~^T = XB B'^T (K-major view of XB: K = 64 = hi | lo halves)
         if (t == 0) {
             tc::fence_after();
-            constexpr uint32_t idw = tc::idesc(tc::kFmtTF32, 128, 32);
+            constexpr uint32_t idw = tc::idesc(tc::kFmtBF16, 64, 32);
             for (int s = 0; s < su::UPB; ++s) {
-                const uint32_t xs = base + (uint32_t)(su::X + s * 16384), bs = base + (uint32_t)(su::BG + s * 8192);
+                const uint32_t xs = base + (uint32_t)(su::XB + s * 8192), bs = base + (uint32_t)(su::BG + s * 8192);
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks) {
                     const uint64_t dA = tc::desc_sw128(xs + 32u * ks);
-                    tc::mma_tf32_ss(tmem + 32u * s, dA, tc::desc_sw128(bs + 32u * ks), idw, ks ? 1u : 0u);
-                    tc::mma_tf32_ss(tmem + 32u * s, dA, tc::desc_sw128(bs + 4096u + 32u * ks), idw, 1u);
+                    tc::mma_f16_ss(tmem + 32u * s, dA, tc::desc_sw128(bs + 32u * ks), idw, ks ? 1u : 0u);
+                    tc::mma_f16_ss(tmem + 32u * s, dA, tc::desc_sw128(bs + 4096u + 32u * ks), idw, 1u);
                 }
             }
             tc::commit(bar_mma);
         }
         mbar_wait(bar_mma, 1);
         tc::fence_after();
-        {  // M = 128 accumulator: row m in lane m. W~[r] = D[r] + D[64 + r]; rows 64-127 meet rows 0-63 in smem
-            float* ex = reinterpret_cast<float*>(g + su::BG);  // [UPB][64][32] (B no longer needed)
 #pragma unroll 1
-            for (int s = 0; s < su::UPB; ++s) {
-                uint32_t v[32];
-                tc::ld32(tmem + ((uint32_t)(32 * warp) << 16) + 32u * s, v);
-                tc::wait_ld();
-                if (warp >= 2) {
-                    float4* dst = reinterpret_cast<float4*>(ex + (s * 64 + 32 * (warp - 2) + lane) * 32);
+        for (int s = 0; s < nv; ++s) {  // row r = 16 warp + lane of W~^T: cols k = Re W~_kr, 16 + k = Im W~_kr
+            uint32_t v[32];
+            tc::ld32(tmem + ((uint32_t)(32 * warp) << 16) + 32u * s, v);
+            tc::wait_ld();
+            if (lane < 16) {
+                const int r = 16 * warp + lane;
+                uint32_t o[32];
 #pragma unroll
-                    for (int c = 0; c < 8; ++c)  // 16-byte piece c at c ^ (row & 7): conflict-free
-                        dst[c ^ (lane & 7)] = make_float4(__uint_as_float(v[4 * c]), __uint_as_float(v[4 * c + 1]),
-                                                          __uint_as_float(v[4 * c + 2]), __uint_as_float(v[4 * c + 3]));
+                for (int kq = 0; kq < NL; ++kq) {
+                    o[2 * kq] = v[kq];
+                    o[2 * kq + 1] = v[16 + kq];
                 }
-                __syncthreads();
-                if (warp < 2 && s < nv) {
-                    const int r = 32 * warp + lane;
-                    const float4* src = reinterpret_cast<const float4*>(ex + (s * 64 + r) * 32);
-                    float w[32];
+                char* dst = reinterpret_cast<char*>(reinterpret_cast<float*>(a.ws) + (ub + s) * WS) + (size_t)r * NL * 8;
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const float4 e = src[c ^ (lane & 7)];
-                        w[4 * c] = __uint_as_float(v[4 * c]) + e.x;
-                        w[4 * c + 1] = __uint_as_float(v[4 * c + 1]) + e.y;
-                        w[4 * c + 2] = __uint_as_float(v[4 * c + 2]) + e.z;
-                        w[4 * c + 3] = __uint_as_float(v[4 * c + 3]) + e.w;
-                    }
-                    // row r of W~^T: columns 0-15 = Re W~_kr, 16-31 = Im W~_kr -> ws[u][r][k] float2
-                    uint32_t o[32];
-#pragma unroll
-                    for (int kq = 0; kq < NL; ++kq) {
-                        o[2 * kq] = __float_as_uint(w[kq]);
-                        o[2 * kq + 1] = __float_as_uint(w[16 + kq]);
-                    }
-                    char* dst = reinterpret_cast<char*>(reinterpret_cast<float*>(a.ws) + (ub + s) * WS) + (size_t)r * NL * 8;
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) st_v8(dst + 32 * q, o + 8 * q);
-                }
+                for (int q = 0; q < 4; ++q) st_v8(dst + 32 * q, o + 8 * q);
             }
         }
         tc::fence_before();
         __syncthreads();
     }
     if (!waited) pdl_wait();
-    if (warp == 0) tc::dealloc<64>(tmem);
+    if (warp == 0) tc::dealloc<128>(tmem);
 }
 
 // Setup kernels: SETUP = 0 SIMT Cholesky route (big_setup.cuh ALG 0), 1 SIMT Gauss-Jordan (ALG 1),
@@ -718,9 +816,9 @@ cudaError_t launch_setup(const DetectArgs& a, cudaStream_t s) {
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return cudaErrorInvalidValue;
+        cudaLaunchConfig_t cfg = {};
         const long long nb = (a.n_units + su::UPB - 1) / su::UPB;
         const long long cap = (long long)n_sm * su::CTAS_PER_SM;
-        cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(nb < cap ? nb : cap));
         cfg.blockDim = dim3(128);
         cfg.dynamicSmemBytes = su::TOTAL;
@@ -747,7 +845,7 @@ cudaError_t prepare_setup() {
                                     (int)(4 * SetupSmem<64, 16, SETUP == 0 ? 0 : 1>::per_unit));
 }
 
-template <int QM, int LT, int EW, int S, int NLO, int TA, int SETUP>
+template <int QM, int LT, int EW, int S, int NLO, int TA, int SETUP, bool BEPI>
 cudaError_t launch_c5(const DetectArgs& a, cudaStream_t s) {
     if (a.n_units <= 0) return cudaSuccess;
     static int n_sm = 0;
@@ -779,31 +877,37 @@ cudaError_t launch_c5(const DetectArgs& a, cudaStream_t s) {
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = a.overlap ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, k_c5_apply<QM, LT, EW, S, NLO, TA>, a, ymap);
+    return cudaLaunchKernelEx(&cfg, k_c5_apply<QM, LT, EW, S, NLO, TA, BEPI>, a, ymap);
 }
 
-template <int QM, int LT, int EW, int S, int NLO, int TA, int SETUP>
+template <int QM, int LT, int EW, int S, int NLO, int TA, int SETUP, bool BEPI>
 cudaError_t prepare_c5() {
     cudaError_t e = prepare_setup<QM, SETUP>();
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_c5_apply<QM, LT, EW, S, NLO, TA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    return cudaFuncSetAttribute(k_c5_apply<QM, LT, EW, S, NLO, TA, BEPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)C5Smem<S, NLO, TA>::total);
 }
 
 size_t c5_workspace(const DetectArgs& a) { return (size_t)a.n_units * BigWs<64, 16>::stride * 4; }
 
-#define C5_ENTRY(NAME, QM, LT, EW, S, NLO, TA, SETUP)                                                     \
+#define C5_ENTRY(NAME, QM, LT, S, NLO, TA, SETUP, BEPI)                                                   \
     KernelEntry {                                                                                          \
-        NAME, 64, 16, QM, kSc, 14, LT, 32, 2, launch_c5<QM, LT, EW, S, NLO, TA, SETUP>,                    \
-            prepare_c5<QM, LT, EW, S, NLO, TA, SETUP>, c5_workspace                                        \
+        NAME, 64, 16, QM, kSc, 14, LT, 32, 2, launch_c5<QM, LT, 6, S, NLO, TA, SETUP, BEPI>,               \
+            prepare_c5<QM, LT, 6, S, NLO, TA, SETUP, BEPI>, c5_workspace                                   \
     }
 
 // First entry of a shape = its default (mimo_api.cu select_fast); the others are selectable by name.
+// Name parts: operand split (bf16 / tf32), setup (tcs = tensor-core contractions; gj = SIMT Gauss-Jordan;
+// chol = SIMT Cholesky), be = the B sets built by the (under-loaded) epilogue warps instead of the
+// converter warps, which set the pace of the pipeline.
 const KernelEntry kEntries[] = {
-    C5_ENTRY("c5_bf16_64x16_q6_i8", 6, kLlrI8, 6, 6, 4, 3, 1),  // C5 default
-    C5_ENTRY("c5_tf32_64x16_q6_i8", 6, kLlrI8, 6, 4, 2, 1, 1),  // round-1 big8e6 operands
-    C5_ENTRY("c5_bf16_chol_64x16_q6_i8", 6, kLlrI8, 6, 6, 4, 3, 0),
-    C5_ENTRY("c5_bf16_tcs_64x16_q6_i8", 6, kLlrI8, 6, 6, 4, 3, 2),  // tensor-core setup
+    C5_ENTRY("c5_bf16_tcs_be_64x16_q6_i8", 6, kLlrI8, 6, 4, 3, 2, true),  // C5 default
+    C5_ENTRY("c5_bf16_tcs_64x16_q6_i8", 6, kLlrI8, 6, 4, 3, 2, false),
+    C5_ENTRY("c5_bf16_tcs_be_s8_64x16_q6_i8", 6, kLlrI8, 8, 4, 3, 2, true),
+    C5_ENTRY("c5_bf16_tcs_be_s7_64x16_q6_i8", 6, kLlrI8, 7, 4, 3, 2, true),
+    C5_ENTRY("c5_bf16_gj_64x16_q6_i8", 6, kLlrI8, 6, 4, 3, 1, false),
+    C5_ENTRY("c5_bf16_chol_64x16_q6_i8", 6, kLlrI8, 6, 4, 3, 0, false),
+    C5_ENTRY("c5_tf32_gj_64x16_q6_i8", 6, kLlrI8, 4, 2, 1, 1, false),  // round-1 big8e6 configuration
 };
 
 }  // namespace

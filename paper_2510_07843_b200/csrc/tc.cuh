@@ -41,6 +41,12 @@ __device__ __forceinline__ void mma_tf32_ss(uint32_t d_tmem, uint64_t da, uint64
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(da), "l"(db), "r"(id), "r"(acc));
 }
+__device__ __forceinline__ void mma_f16_ss(uint32_t d_tmem, uint64_t da, uint64_t db, uint32_t id, uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(da), "l"(db), "r"(id), "r"(acc));
+}
 // A operand in TMEM (lane = row m; one 32-bit column per tf32 K element / per bf16 K pair).
 __device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t db, uint32_t id, uint32_t acc) {
     asm volatile(
@@ -122,17 +128,34 @@ __device__ __forceinline__ void split_bf2(float a0, float a1, uint32_t& hi, uint
 
 }  // namespace tc
 
-// mbarrier wait that lets the hardware suspend the thread until the phase completes (or the
-// hint expires), instead of re-issuing try_wait in a tight loop: waiting warps then take no issue
-// slots from the warps that have work.
+// mbarrier wait for the warp-specialised pipelines: try_wait with a suspend-time hint of
+// C5_WAIT_HINT_NS (0 = the plain try_wait loop).
+#ifndef C5_WAIT_HINT_NS
+#define C5_WAIT_HINT_NS 0
+#endif
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+#if C5_WAIT_HINT_NS > 0
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAITS_%=:\n\t"
         "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], %1, %2;\n\t"
         "@!p bra WAITS_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity), "r"(0x100000u)
+        "r"(parity), "r"((uint32_t)C5_WAIT_HINT_NS)
         : "memory");
+#else
+    mbar_wait(bar, parity);
+#endif
+}
+
+// Non-blocking: has the phase with parity `parity` completed?
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+    return ok != 0;
 }
 
 }  // namespace mimo
