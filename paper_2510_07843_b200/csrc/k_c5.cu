@@ -567,7 +567,9 @@ __global__ void __launch_bounds__(128, su::CTAS_PER_SM) k_c5_setup(DetectArgs a,
     bool waited = false;  // PDL: the previous call may still read the workspace
     uint32_t it = 0;
 #pragma unroll 1
+    PROF_DECL;
     for (long long bt = blockIdx.x; bt < n_batch; bt += gridDim.x, ++it) {
+        PROF_T(p0);
         const long long ub = bt * su::UPB;
         const int nv = (int)min((long long)su::UPB, a.n_units - ub);  // valid units in this batch
         // ---- a1: H of the batch (fp32, SW128) into the B regions, then XB = bf16 hi | lo
@@ -581,6 +583,8 @@ __global__ void __launch_bounds__(128, su::CTAS_PER_SM) k_c5_setup(DetectArgs a,
                     : "memory");
         }
         mbar_wait(bar_tma, it & 1);
+        PROF_ADD(prof, 0, p0);
+        PROF_T(p1);
 #pragma unroll 2
         for (int q = t; q < su::UPB * 256; q += 128) {  // item = (unit, row r, 8 columns 8 cp .. 8 cp + 7)
             const int s = q >> 8, r = (q >> 2) & 63, cp = q & 3, sw = r & 7;
@@ -599,6 +603,8 @@ __global__ void __launch_bounds__(128, su::CTAS_PER_SM) k_c5_setup(DetectArgs a,
         tc::fence_proxy_async();
         tc::fence_before();
         __syncthreads();
+        PROF_ADD(prof, 1, p1);
+        PROF_T(p2);
         // ---- a2: Gram, MN-major XB as both operands: C = (hi + lo)^T (hi + lo) lands in D rows 0-31 (A = the
         // hi columns, then, from start + 64 B, the lo columns; D rows 32-63 then read past the tile: unused)
         if (t == 0) {
@@ -619,6 +625,8 @@ __global__ void __launch_bounds__(128, su::CTAS_PER_SM) k_c5_setup(DetectArgs a,
             tc::commit(bar_mma);
         }
         mbar_wait(bar_mma, 0);
+        PROF_ADD(prof, 2, p2);
+        PROF_T(p3);
         tc::fence_after();
         if (warp < 2) {  // M = 64 accumulator: row m in TMEM lane 32 (m / 16) + m % 16 -> C rows 16 warp + lane
 #pragma unroll 1
@@ -639,6 +647,8 @@ __global__ void __launch_bounds__(128, su::CTAS_PER_SM) k_c5_setup(DetectArgs a,
         }
         tc::fence_before();
         __syncthreads();
+        PROF_ADD(prof, 3, p3);
+        PROF_T(p4);
         // ---- a3-a5: warp w inverts unit w; lane (k, h) = (lane / 2, lane % 2) holds G[k][8h .. 8h+7]
         if (!waited) {
             pdl_wait();
@@ -752,6 +762,8 @@ __global__ void __launch_bounds__(128, su::CTAS_PER_SM) k_c5_setup(DetectArgs a,
         tc::fence_proxy_async();
         tc::fence_before();
         __syncthreads();
+        PROF_ADD(prof, 4, p4);
+        PROF_T(p5);
         // ---- a4: W~^T = XB B'^T (K-major view of XB: K = 64 = hi | lo halves)
         if (t == 0) {
             tc::fence_after();
@@ -768,6 +780,8 @@ __global__ void __launch_bounds__(128, su::CTAS_PER_SM) k_c5_setup(DetectArgs a,
             tc::commit(bar_mma);
         }
         mbar_wait(bar_mma, 1);
+        PROF_ADD(prof, 5, p5);
+        PROF_T(p6);
         tc::fence_after();
 #pragma unroll 1
         for (int s = 0; s < nv; ++s) {  // row r = 16 warp + lane of W~^T: cols k = Re W~_kr, 16 + k = Im W~_kr
@@ -789,7 +803,9 @@ __global__ void __launch_bounds__(128, su::CTAS_PER_SM) k_c5_setup(DetectArgs a,
         }
         tc::fence_before();
         __syncthreads();
+        PROF_ADD(prof, 6, p6);
     }
+    PROF_SFLUSH(t == 0);
     if (!waited) pdl_wait();
     if (warp == 0) tc::dealloc<128>(tmem);
 }
