@@ -114,14 +114,16 @@ def kernel_share(args, k) -> dict | None:
 
 
 def ncu_traffic(k) -> float | None:
-    """dram read+write bytes per launch from the committed ncu --set full capture (profiles/)."""
+    """DRAM read + write bytes per STEP from the committed ncu range capture (profiles/traffic.json:
+    8 back-to-back calls over rotating buffers, so the LLR write-back is counted), comparable with
+    the algorithmic bytes per step that `achieved` uses."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         d = json.load(f)
     v = d.get(synth.CONFIGS[k]["name"])
-    return float(v["dram_bytes_per_launch"]) if v else None
+    return float(v["dram_bytes_per_step"]) if v and "dram_bytes_per_step" in v else None
 
 
 # ----------------------------------------------------------------- clocks --
@@ -494,33 +496,39 @@ def run_ours(args, k):
     # e2e: the public host-buffer C-ABI call (mimo_detect_mmse_host_async), pinned host buffers:
     # every step copies its H and y host->device and its LLRs device->host inside the timed region
     e2e = None
-    if not args.no_e2e and ybfp is None:
+    if not args.no_e2e:
         Hh = torch.from_numpy(Hn).pin_memory()
-        yh = torch.from_numpy(yn).pin_memory()
+        yh = torch.from_numpy(yn if ybfp is None else ybfp).pin_memory()
         lh = torch.empty(plan.shapes(n_sc_r, sh.n_sym)["llr"], dtype=plan.llr_dtype).pin_memory()
+        if ybfp is None:
+            host_call = lambda wait: plan.detect_host(Hh, yh, sh.s2, out=lh, wait=wait)
+        else:  # NEXT-4: the BFP fronthaul bytes cross PCIe, decompressed inside the apply kernel
+            host_call = lambda wait: plan.detect_bfp_host(Hh, yh, sh.s2, n_sym=sh.n_sym, n_sc=n_sc_r,
+                                                          iq_width=args.bfp, out=lh, wait=wait)
         for _ in range(2):
-            plan.detect_host(Hh, yh, sh.s2, out=lh)
+            host_call(True)
         if barrier:
             barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            plan.detect_host(Hh, yh, sh.s2, out=lh)
+            host_call(True)
         dt_sync = shard.max_over_ranks(time.perf_counter() - t0, device=dev)
         for _ in range(3):
-            plan.detect_host(Hh, yh, sh.s2, out=lh, wait=False)
+            host_call(False)
         plan.sync_status()
         if barrier:
             barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            plan.detect_host(Hh, yh, sh.s2, out=lh, wait=False)
+            host_call(False)
         plan.sync_status()
         dt = shard.max_over_ranks(time.perf_counter() - t0, device=dev)
         e2e = {"value": n_re_job * args.e2e_steps * (world if scaling == "replicas" else 1) / dt, "unit": "RE/s",
                "h2d_bytes_per_step": b["H"] + b["y"], "d2h_bytes_per_step": b["llr"],
                "ms_per_step": dt * 1e3 / args.e2e_steps,
-               "path": "mimo_detect_mmse_host_async per step + one plan sync (pinned host buffers, "
-                       "3-stream slot-chunk pipeline; consecutive steps overlap their transfers)",
+               "path": ("mimo_detect_mmse_host_async" if ybfp is None else f"mimo_detect_mmse_bfp_host_async (BFP{args.bfp} y)")
+                       + " per step + one plan sync (pinned host buffers, 3-stream slot-chunk pipeline; consecutive "
+                         "steps overlap their transfers)",
                "sync_call_ms_per_step": dt_sync * 1e3 / args.e2e_steps,
                "bytes_note": "per rank" if world > 1 else "whole job"}
 

@@ -237,6 +237,21 @@ mimo_status_t mimo_detect_mmse_bfp(mimo_plan_t plan, const void* H, const void* 
                                    int iq_width, float bfp_scale,
                                    void* llr_out, void* xhat_out, float* sinr_out);
 
+/* Host-buffer (end-to-end) forms of mimo_detect_mmse_bfp: H_host complex64 and y_bfp_host BFP
+ * bytes [n_sym][n_sc/12][n_rx][block_bytes] in (pinned) host memory, llr_host host memory; the same
+ * slot-chunk pipeline as mimo_detect_mmse_host / _host_async (H and the compressed y cross PCIe,
+ * are decompressed inside the apply kernel's loads, LLRs come back). This is where the fronthaul
+ * format pays: y crosses the host link at 28 B instead of 96 B per (symbol, PRB, antenna) at
+ * iq_width 9 (D-MIMO fronthaul). Same support and errors as mimo_detect_mmse_bfp
+ * plus those of mimo_detect_mmse_host; the _async form returns after enqueuing (synchronise with
+ * mimo_plan_sync_status). */
+mimo_status_t mimo_detect_mmse_bfp_host(mimo_plan_t plan, const void* H_host, const void* y_bfp_host, float sigma2,
+                                        int n_rx, int n_layers, int n_sc, int n_sym, int qam_order, int iq_width,
+                                        float bfp_scale, void* llr_host);
+mimo_status_t mimo_detect_mmse_bfp_host_async(mimo_plan_t plan, const void* H_host, const void* y_bfp_host,
+                                              float sigma2, int n_rx, int n_layers, int n_sc, int n_sym,
+                                              int qam_order, int iq_width, float bfp_scale, void* llr_host);
+
 /* Pre-allocate the plan's kernel workspace for calls of up to n_sc x n_sym
  * (some kernel families keep per-unit W~ in a plan-owned buffer). Calls grow the
  * workspace on demand, but not while the stream is being captured into a CUDA

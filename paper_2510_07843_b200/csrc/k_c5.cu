@@ -122,8 +122,13 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_c5_apply(DetectArgs a, con
     constexpr int S = S_, NLO = NLO_;
     static_assert(EW == 6, "6 epilogue warps (4 for tile 0, 2 for the compact tile 1)");
 
-    static_assert(TA == 1 || TA == 3, "TF32 or BF16 operands");
-    constexpr uint32_t kAring = 256u;                // TMEM columns 0-255: 2 accumulators x 128
+    static_assert(TA == 1 || TA == 3 || TA == 4, "TF32 or BF16 operands");
+    // TA = 4: BF16 with the three split products accumulated into ONE 32-column accumulator per tile
+    // (A = y_hi with B_hi and B_lo, then y_lo with B_hi, all N = 32): x~ needs no hi + lo sum, and the
+    // two accumulators take 128 TMEM columns instead of 256
+    constexpr bool KC = TA == 4;
+    constexpr uint32_t kAccCols = KC ? 64u : 128u;   // TMEM columns per accumulator (2 row tiles)
+    constexpr uint32_t kAring = 2u * kAccCols;       // TMEM columns 0 .. kAring-1: 2 accumulators
     constexpr uint32_t kAcols = TA == 1 ? 128u : 64u;  // TMEM columns per A ring slot (one chunk, 2 tiles)
     static_assert(kAring + NLO * kAcols <= 512u, "TMEM");
     constexpr int CW = 4 + EW;                       // MMA warp; CW + 1: TMA producer
@@ -232,7 +237,7 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_c5_apply(DetectArgs a, con
                 PROF_T(t1);
                 if (i >= 2) mbar_wait_sleep(&tfree[b], (uint32_t)(((i >> 1) + 1) & 1));
                 PROF_ADD(prof, 9, t1);
-                const uint32_t acc = tmem + 128u * (uint32_t)b;
+                const uint32_t acc = tmem + kAccCols * (uint32_t)b;
                 const uint64_t db = tc::desc_add(dB, (uint32_t)(b * SM::bset));
 #pragma unroll 1
                 for (int c = 0; c < 4; ++c) {
@@ -251,6 +256,17 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_c5_apply(DetectArgs a, con
                                 const uint64_t dk = tc::desc_add(db, (uint32_t)(c * 8192 + ks * 32));
                                 tc::mma_tf32_ts(acc + 64u * tile, ab + 64u * tile + 8u * ks, dk, id64, (c | ks) ? 1u : 0u);
                                 tc::mma_tf32_ts(acc + 64u * tile, ab + 64u * tile + 32u + 8u * ks, dk, id32, 1u);
+                            }
+                    } else if constexpr (KC) {  // 2 K-steps of 16, three N = 32 products into one accumulator
+#pragma unroll
+                        for (int tile = 0; tile < 2; ++tile)
+#pragma unroll
+                            for (int ks = 0; ks < 2; ++ks) {
+                                const uint64_t dk = tc::desc_add(db, (uint32_t)((c >> 1) * 8192 + (c & 1) * 64 + ks * 32));
+                                const uint64_t dkl = tc::desc_add(dk, 4096u);  // B_lo rows 32-63
+                                tc::mma_f16_ts(acc + 32u * tile, ab + 32u * tile + 8u * ks, dk, id32, (c | ks) ? 1u : 0u);
+                                tc::mma_f16_ts(acc + 32u * tile, ab + 32u * tile + 8u * ks, dkl, id32, 1u);
+                                tc::mma_f16_ts(acc + 32u * tile, ab + 32u * tile + 16u + 8u * ks, dk, id32, 1u);
                             }
                     } else {  // 2 K-steps of 16; chunk c = half (c & 1) of K atom c >> 1
 #pragma unroll
@@ -301,10 +317,10 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_c5_apply(DetectArgs a, con
         const float ia = rsqrtf((float)qam_norm(QM));
         // x~ of RE `row` (TMEM lane quadrant `quad`, accumulator b, row tile `tile`) -> LLR record
         auto epilogue_row = [&](long long i, int b, int tile, int row, int quad, bool active) {
-            uint32_t hv[32], lv[32];
-            const uint32_t taddr = tmem + ((uint32_t)(32 * quad) << 16) + 128u * (uint32_t)b + 64u * tile;
+            uint32_t hv[32], lv[KC ? 1 : 32];
+            const uint32_t taddr = tmem + ((uint32_t)(32 * quad) << 16) + kAccCols * (uint32_t)b + (kAccCols / 2) * tile;
             tc::ld32(taddr, hv);
-            tc::ld32(taddr + 32u, lv);
+            if constexpr (!KC) tc::ld32(taddr + 32u, lv);
             tc::wait_ld();
             if (!active) return;
             const long long u = u0 + i * du;
@@ -313,9 +329,11 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_c5_apply(DetectArgs a, con
             const size_t re = (size_t)(slot * kSym + s) * a.n_sc + fb * kSc + f;
             float2 x[NL];
 #pragma unroll
-            for (int k = 0; k < NL; ++k)
-                x[k] = make_float2(__uint_as_float(hv[k]) + __uint_as_float(lv[k]),
-                                   __uint_as_float(hv[16 + k]) + __uint_as_float(lv[16 + k]));
+            for (int k = 0; k < NL; ++k) {
+                if constexpr (KC) x[k] = make_float2(__uint_as_float(hv[k]), __uint_as_float(hv[16 + k]));
+                else x[k] = make_float2(__uint_as_float(hv[k]) + __uint_as_float(lv[k]),
+                                        __uint_as_float(hv[16 + k]) + __uint_as_float(lv[16 + k]));
+            }
             const float* sl = sslope + (i & 3) * 16;
             if (a.llr) {
                 uint32_t wd[(kRec + 3) / 4];
@@ -919,8 +937,8 @@ size_t c5_workspace(const DetectArgs& a) { return (size_t)a.n_units * BigWs<64, 
 const KernelEntry kEntries[] = {
     C5_ENTRY("c5_bf16_tcs_be_64x16_q6_i8", 6, kLlrI8, 6, 4, 3, 2, true),  // C5 default
     C5_ENTRY("c5_bf16_tcs_64x16_q6_i8", 6, kLlrI8, 6, 4, 3, 2, false),
-    C5_ENTRY("c5_bf16_tcs_be_s8_64x16_q6_i8", 6, kLlrI8, 8, 4, 3, 2, true),
-    C5_ENTRY("c5_bf16_tcs_be_s7_64x16_q6_i8", 6, kLlrI8, 7, 4, 3, 2, true),
+    C5_ENTRY("c5_bf16kc_tcs_be_64x16_q6_i8", 6, kLlrI8, 6, 4, 4, 2, true),
+    C5_ENTRY("c5_bf16kc6_tcs_be_64x16_q6_i8", 6, kLlrI8, 6, 6, 4, 2, true),
     C5_ENTRY("c5_bf16_gj_64x16_q6_i8", 6, kLlrI8, 6, 4, 3, 1, false),
     C5_ENTRY("c5_bf16_chol_64x16_q6_i8", 6, kLlrI8, 6, 4, 3, 0, false),
     C5_ENTRY("c5_tf32_gj_64x16_q6_i8", 6, kLlrI8, 4, 2, 1, 1, false),  // round-1 big8e6 configuration

@@ -340,11 +340,25 @@ mimo_status_t mimo_detect_mmse(mimo_plan_t p, const void* H, const void* y, floa
     return mimo_detect_mmse_ex(p, H, y, sigma2, n_rx, n_layers, n_sc, n_sym, qm, llr_out, nullptr, nullptr);
 }
 
+// y as block floating point (mimo_detect_mmse_bfp_host*): iq_width = 0 means complex64 y.
+struct BfpY {
+    int iq_width = 0;
+    float scale = 1.f;
+};
+
 static mimo_status_t host_path(mimo_plan_t p, const void* H_host, const void* y_host, float sigma2, int n_rx, int n_layers,
-                        int n_sc, int n_sym, int qm, void* llr_host, bool wait) {
+                        int n_sc, int n_sym, int qm, void* llr_host, bool wait, BfpY bfp = BfpY{}) {
     if (!p) return arg_fail(nullptr, "null plan");
     mimo_status_t st = check_dims(p, sigma2, n_rx, n_layers, n_sc, n_sym, qm);
     if (st != MIMO_OK) return st;
+    if (bfp.iq_width) {
+        if (bfp.iq_width < 8 || bfp.iq_width > 16) return arg_fail(p, "iq_width must be in 8..16");
+        if (!(bfp.scale > 0.f) || !std::isfinite(bfp.scale)) return arg_fail(p, "bfp_scale must be finite > 0");
+        if (!mimo::bfp_supported(n_rx, n_layers, p->d.sc_per_h, p->d.sym_per_h)) {
+            snprintf(p->err, sizeof(p->err), "BFP route: supported for 8 rx x 4 layers, H per PRB, 14 symbols");
+            return MIMO_ERR_UNSUPPORTED;
+        }
+    }
     if ((long long)n_sc * n_sym == 0) return MIMO_OK;
     if (!H_host || !y_host || !llr_host) return arg_fail(p, "null host buffer");
     DeviceGuard g(p->d.device);
@@ -354,7 +368,9 @@ static mimo_status_t host_path(mimo_plan_t p, const void* H_host, const void* y_
     const int n_slots = n_sym / symph;
     const int n_fb = n_sc / p->d.sc_per_h;
     const size_t h_slot = (size_t)n_fb * n_rx * n_layers * 8;
-    const size_t y_slot = (size_t)symph * n_sc * n_rx * 8;
+    const size_t bfp_block = bfp.iq_width ? (size_t)((1 + 3 * bfp.iq_width + 3) & ~3) : 0;
+    const size_t y_slot = bfp.iq_width ? (size_t)symph * (n_sc / 12) * n_rx * bfp_block
+                                       : (size_t)symph * n_sc * n_rx * 8;
     const size_t l_slot = (size_t)symph * n_sc * n_layers * qm * llr_bytes(p->d.llr_type);
     // Chunks of whole slots, ~4 MiB of input each, on a 3-deep buffer ring over
     // three streams (H2D | kernels | D2H) so both PCIe directions and the
@@ -427,10 +443,17 @@ static mimo_status_t host_path(mimo_plan_t p, const void* H_host, const void* y_
         if (e != cudaSuccess) return cuda_fail(p, e, "cudaMemcpyAsync H2D");
         cudaStreamWaitEvent(s_k, p->e_in[b], 0);
         cudaStreamWaitEvent(s_k, p->e_out[b], 0);
-        mimo::DetectArgs a = make_args(p, dH, dy, sigma2, n_sc, ns * symph, dl, nullptr, nullptr);
+        mimo::DetectArgs a = make_args(p, dH, bfp.iq_width ? nullptr : dy, sigma2, n_sc, ns * symph, dl, nullptr, nullptr);
         a.overlap = 0;
-        st = launch(p, a, s_k, 1);
-        if (st != MIMO_OK) return st;
+        if (bfp.iq_width) {
+            st = ensure_ws(p, 1, mimo::bfp_workspace(a), s_k);
+            if (st != MIMO_OK) return st;
+            a.ws = p->kws[1];
+            if ((e = mimo::launch_bfp(a, dy, bfp.iq_width, bfp.scale, s_k)) != cudaSuccess) return cuda_fail(p, e, "BFP route");
+        } else {
+            st = launch(p, a, s_k, 1);
+            if (st != MIMO_OK) return st;
+        }
         if ((e = cudaEventRecord(p->e_k[b], s_k)) != cudaSuccess) return cuda_fail(p, e, "cudaEventRecord");
         cudaStreamWaitEvent(s_out, p->e_k[b], 0);
         e = cudaMemcpyAsync((char*)llr_host + l_slot * s0, dl, l_slot * ns, cudaMemcpyDeviceToHost, s_out);
@@ -454,6 +477,20 @@ mimo_status_t mimo_detect_mmse_host(mimo_plan_t p, const void* H_host, const voi
 mimo_status_t mimo_detect_mmse_host_async(mimo_plan_t p, const void* H_host, const void* y_host, float sigma2,
                                           int n_rx, int n_layers, int n_sc, int n_sym, int qm, void* llr_host) {
     return host_path(p, H_host, y_host, sigma2, n_rx, n_layers, n_sc, n_sym, qm, llr_host, false);
+}
+
+mimo_status_t mimo_detect_mmse_bfp_host(mimo_plan_t p, const void* H_host, const void* y_bfp_host, float sigma2,
+                                        int n_rx, int n_layers, int n_sc, int n_sym, int qm, int iq_width,
+                                        float bfp_scale, void* llr_host) {
+    return host_path(p, H_host, y_bfp_host, sigma2, n_rx, n_layers, n_sc, n_sym, qm, llr_host, true,
+                     BfpY{iq_width, bfp_scale});
+}
+
+mimo_status_t mimo_detect_mmse_bfp_host_async(mimo_plan_t p, const void* H_host, const void* y_bfp_host, float sigma2,
+                                              int n_rx, int n_layers, int n_sc, int n_sym, int qm, int iq_width,
+                                              float bfp_scale, void* llr_host) {
+    return host_path(p, H_host, y_bfp_host, sigma2, n_rx, n_layers, n_sc, n_sym, qm, llr_host, false,
+                     BfpY{iq_width, bfp_scale});
 }
 
 mimo_status_t mimo_detect_lmmse_lu(mimo_plan_t p, const void* H, const void* y, float sigma2, int n_rx,

@@ -80,6 +80,9 @@ def load_library(path: str | None = None):
     L.mimo_detect_mmse_host.argtypes = [vp, vp, vp, f, i, i, i, i, i, vp]
     L.mimo_detect_mmse_host_async.argtypes = [vp, vp, vp, f, i, i, i, i, i, vp]
     L.mimo_detect_mmse_host_async.restype = i
+    for nm in ("mimo_detect_mmse_bfp_host", "mimo_detect_mmse_bfp_host_async"):
+        getattr(L, nm).argtypes = [vp, vp, vp, f, i, i, i, i, i, i, f, vp]
+        getattr(L, nm).restype = i
     L.mimo_detect_mmse_host.restype = i
     L.mimo_detect_lmmse_lu.argtypes = [vp, vp, vp, f, i, i, i, i, i, i, vp, vp, vp, ctypes.POINTER(f)]
     L.mimo_detect_lmmse_lu.restype = i
@@ -336,6 +339,35 @@ class Plan:
         fn = self._lib.mimo_detect_mmse_host if wait else self._lib.mimo_detect_mmse_host_async
         st = fn(self._h, Hn.ctypes.data_as(ctypes.c_void_p), yn.ctypes.data_as(ctypes.c_void_p),
                 ctypes.c_float(sigma2), self.n_rx, self.n_layers, n_sc, n_sym, self.qm,
+                on.ctypes.data_as(ctypes.c_void_p))
+        self._check(st)
+        return out
+
+    def detect_bfp_host(self, H, y_bfp, sigma2: float, *, n_sym: int, n_sc: int, iq_width: int = 9,
+                        bfp_scale: float = 2.0 ** -8, out=None, wait: bool = True):
+        """End-to-end detect with HOST buffers and block-floating-point y (mimo_detect_mmse_bfp_host[_async]):
+        H complex64, y_bfp uint8 [n_sym][n_sc/12][n_rx][block_bytes] (numpy or CPU tensors; pin them)."""
+        import torch
+        to_np = (lambda t: t.numpy() if isinstance(t, torch.Tensor) else t)
+        Hn, yn = to_np(H), to_np(y_bfp)
+        if Hn.dtype != np.complex64 or yn.dtype != np.uint8:
+            raise ValueError("H must be complex64 and y_bfp uint8")
+        if not (Hn.flags.c_contiguous and yn.flags.c_contiguous):
+            raise ValueError("H and y_bfp must be C-contiguous")
+        bb = ((1 + 3 * iq_width) + 3) & ~3
+        sh = self.shapes(n_sc, n_sym)
+        if Hn.size != int(np.prod(sh["H"])) or yn.size != n_sym * (n_sc // 12) * self.n_rx * bb:
+            raise ValueError("H / y_bfp sizes do not match the plan")
+        if out is None:
+            out = np.empty(sh["llr"], dtype={LLR_F32: np.float32, LLR_F16: np.float16, LLR_I8: np.int8}[self.llr_type])
+        on = to_np(out)
+        if on.size != int(np.prod(sh["llr"])) or not on.flags.c_contiguous:
+            raise ValueError("out has the wrong size or is not contiguous")
+        if self._fixed_stream is None:
+            self._lib.mimo_plan_set_stream(self._h, ctypes.c_void_p(self._stream_ptr()))
+        fn = self._lib.mimo_detect_mmse_bfp_host if wait else self._lib.mimo_detect_mmse_bfp_host_async
+        st = fn(self._h, Hn.ctypes.data_as(ctypes.c_void_p), yn.ctypes.data_as(ctypes.c_void_p), ctypes.c_float(sigma2),
+                self.n_rx, self.n_layers, n_sc, n_sym, self.qm, int(iq_width), ctypes.c_float(bfp_scale),
                 on.ctypes.data_as(ctypes.c_void_p))
         self._check(st)
         return out

@@ -57,3 +57,18 @@ def test_bfp_unsupported_shape():
     with pytest.raises(mimo.MimoError) as e:
         p.detect_bfp(torch.from_numpy(w.H).cuda(), yb, float(w.sigma2), n_sym=w.n_sym, n_sc=24)
     assert e.value.status == mimo.MIMO_ERR_UNSUPPORTED
+
+
+@pytest.mark.parametrize("wait", [True, False])
+def test_bfp_host_path_bit_identical_to_device_path(wait):
+    """mimo_detect_mmse_bfp_host[_async]: the compressed y crosses the host link; results are
+    bit-identical to the device-buffer BFP call (same kernels, slot chunks are independent)."""
+    w = synth.generate(3, n_sc=300, n_slots=6)
+    ref = run_bfp(w, 9, xhat=False)["llr"]
+    p = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, llr_dtype=w.llr, host_chunk_bytes=100_000)
+    yb = torch.from_numpy(synth.bfp_compress(w.y, 9, SCALE)).pin_memory()
+    out = torch.empty(ref.shape, dtype=torch.int8).pin_memory()
+    p.detect_bfp_host(torch.from_numpy(w.H).pin_memory(), yb, float(w.sigma2), n_sym=w.n_sym, n_sc=w.n_sc,
+                      iq_width=9, bfp_scale=SCALE, out=out, wait=wait)
+    assert p.sync_status() == 0
+    assert np.array_equal(out.numpy(), ref)
