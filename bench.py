@@ -49,7 +49,7 @@ METRIC = "MIMO-detected REs/s per B200 (LLR Gbit/s alongside) vs roofline"
 FALLBACK_HBM_GBS = 6650.0   # B200_PROFILING.md fallback, used only if MEASURED_PEAKS.json is absent
 FALLBACK_BF16_TFLOPS = 2250.0  # B200_PROFILING.md nominal dense bf16
 TF32_PER_BF16 = 1.1 / 2.25   # B200_PROFILING.md nominal dense tf32 / bf16
-TC_KERNELS = ("big8", "c5")  # kernels whose row a6 runs on tcgen05 (R21, R28)
+TC_KERNELS = ("c5",)  # kernels whose row a6 runs on tcgen05 (R21, R28)
 # The paper's own CPU figure: a 4x4 LMMSE detection of one 720-subcarrier,
 # 14-symbol TTI in <= 0.03 ms on an Intel i9-14900KF with AVX2 -- another CPU and workload.
 PAPER_CPU_CONTEXT = {"value": 720 * 14 / 0.03e-3, "unit": "RE/s", "hardware": "Intel Core i9-14900KF, AVX2",

@@ -68,7 +68,7 @@ extern "C" int mimo_c5_sprof_read(unsigned long long* host) {
 namespace mimo {
 namespace {
 
-template <int S_, int NLO_, int TA_>
+template <int S_, int NLO_, int TA_, bool FUSED_ = false>
 struct C5Smem {
     static constexpr int S = S_;                              // y stages
     static constexpr int NLO = NLO_;                          // TMEM A ring slots (chunks)
@@ -79,9 +79,11 @@ struct C5Smem {
     static constexpr size_t slope = B + 2 * bset;             // [4][16] slope | [4][16] sqrt(slope / 127)
     static constexpr size_t wst = slope + 512;                // [2] W~ workspace records staged by TMA
     static constexpr size_t wrec = (size_t)BigWs<64, 16>::stride * 4;
-    static constexpr size_t bars = wst + 2 * wrec;
-    static constexpr int NBAR = 2 * S + 2 * NLO + 2 * 3 + 4;  // yfull, yfree | afull, afree | bready, accfull, tfree | wfull, wfree
-    static constexpr size_t tslot = bars + NBAR * 8;
+    static constexpr size_t setup = (wst + 2 * wrec + 1023) / 1024 * 1024;  // FUSED: the setup group's 64 KiB
+    static constexpr size_t bars = setup + (FUSED_ ? 65536 : 0);
+    static constexpr int NBAR = 2 * S + 2 * NLO + 2 * 3 + 4 + 2;  // yfull, yfree | afull, afree | bready, accfull, tfree | wfull, wfree | setup tma, mma
+    static constexpr size_t ready = bars + NBAR * 8;           // FUSED: units whose W~ records are written
+    static constexpr size_t tslot = ready + 8;
     static constexpr size_t total = tslot + 16 + 1024;        // + 1024-B alignment slack
     static_assert(B % 1024 == 0, "UMMA operand alignment");
     static_assert(total <= 227 * 1024, "shared memory");
@@ -115,10 +117,307 @@ __device__ __forceinline__ void demap_axis_i8(float u, float rs, uint32_t* q, in
     }
 }
 
-template <int QM, int LT, int EW, int S_, int NLO_, int TA, bool BEPI>
-__global__ void __launch_bounds__(32 * (6 + EW), 1) k_c5_apply(DetectArgs a, const __grid_constant__ CUtensorMap ymap) {
+// ------------------------------------------------------------------------
+// k_c5_setup: rows a2-a5 with both contractions on the tensor cores (BF16 split
+// operands, reading R28) and the 16 x 16 inversion on the FP32 pipe. One CTA =
+// 4 warps = 4 H-units per batch (warp w owns unit w of the batch):
+//   a1  H_u (64 x 16 complex = 64 x 32 real X, row r = antenna) by a 2-D TMA box
+//       (fp32, SWIZZLE_128B), converted to XB = [X_hi | X_lo] (bf16, 128-B row r,
+//       same swizzle), X_hi = rn_bf16(X), X_lo = rn_bf16(X - X_hi);
+//   a2  C = (X_hi + X_lo)^T (X_hi + X_lo): 16 kind::f16 MMAs with BOTH operands the
+//       MN-major view of XB (M = 64 from the hi, then the lo columns, N = 32 hi then 32
+//       lo, K = 64 antennas), C in D rows 0-31; G_kl = (C[2k][2l] + C[2k+1][2l+1]) +
+//       i (C[2k][2l+1] - C[2k+1][2l]) + sigma2 delta_kl;
+//   a3-a5  G^-1 by in-place Gauss-Jordan (no pivoting: G is Hermitian PD; its
+//       pivots are the LDL^H pivots, so guard R17 reads the same quantities as
+//       Cholesky's d_jj^2 -- reading R26), mu, SINR, fac = sqrt(norm) / mu,
+//       B = real form of fac G^-1, split into bf16 hi / lo and duplicated along K;
+//   a4  W~^T = XB B'^T: 8 kind::f16 MMAs, A = the K-major view of the SAME XB tile
+//       (K = 64 = hi | lo halves of the 32 real inputs), B' = [B | B] (hi, lo).
+// TMEM: 32 columns per unit (the Gram accumulator, reused for W~). M = 64
+// accumulators put row m in lane 32 (m / 16) + m % 16, so every warp reads its
+// lane quadrant of W~, and warps 0-1 read C.
+// (A persistent warp-specialised variant -- producer, MMA, readout and 12 worker warps
+// over a ring of unit slots -- measured 107-124 us against this kernel's 90, the
+// per-slot chain of H load, Gram round trip and inversion being sequential.)
+namespace su {
+constexpr int UPB = 4;                   // units per batch (= warps)
+constexpr size_t XB = 0;                 // [UPB] x 8 KiB  bf16 [64 r][hi c 0..31 | lo c 0..31], SW128
+constexpr size_t BG = UPB * 8192;        // [UPB] x 8 KiB  H landing (fp32) -> exchange | C -> B'_hi | B'_lo
+constexpr size_t BAR = BG + UPB * 8192;
+constexpr size_t TSLOT = BAR + 16;
+constexpr size_t TOTAL = TSLOT + 16 + 1024;  // + 1024-B alignment slack
+constexpr int CTAS_PER_SM = 3;
+static_assert(TOTAL * CTAS_PER_SM <= 227 * 1024, "shared memory");
+}  // namespace su
+
+// TMA of the H tiles of one setup batch (fp32, SWIZZLE_128B) into the group's B regions.
+template <typename UnitF>
+__device__ __forceinline__ void setup_issue_h(const CUtensorMap* hmapp, uint32_t gaddr, uint64_t* bar_tma, int nv,
+                                              UnitF unit_of) {
+    mbar_arrive_expect_tx(bar_tma, (uint32_t)(nv * 64 * 16 * 8));
+    for (int s = 0; s < nv; ++s)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+            ::"r"(gaddr + (uint32_t)(su::BG + s * 8192)), "l"(reinterpret_cast<uint64_t>(hmapp)), "r"(0),
+            "r"((int)(unit_of(s) * 64)), "r"(smem_u32(bar_tma))
+            : "memory");
+}
+
+// One batch of up to su::UPB = 4 H-units through rows a2-a5 (a1-a5 steps documented at k_c5_setup),
+// run by a 4-warp group: gt = thread 0..127 of the group, gw = its warp 0..3 (= TMEM lane quadrant
+// of the group's warps), g / gaddr = generic / shared address of the group's 64-KiB region (XB at
+// su::XB, B sets at su::BG), tmem = the group's 128 TMEM columns, it = the group's batch count (TMA
+// barrier parity), unit_of(s) = global H-unit of batch slot s < nv, sync() = the group's barrier.
+// The batch's H tiles were issued by the previous batch (or the caller, for the first one);
+// issue_next() issues the next batch's as soon as this batch's W~ MMAs have released the B regions,
+// so that the H load overlaps the W~ readout.
+template <int QM, typename UnitF, typename SyncF, typename NextF>
+__device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorMap* hmapp, unsigned char* g,
+                                            uint32_t gaddr, uint64_t* bar_tma, uint64_t* bar_mma, uint32_t tmem,
+                                            uint32_t it, int nv, int gt, int gw, int lane, bool& waited,
+                                            UnitF unit_of, SyncF sync, NextF issue_next) {
     constexpr int NR = 64, NL = 16;
-    using SM = C5Smem<S_, NLO_, TA>;
+    constexpr int WS = BigWs<NR, NL>::stride;
+    const float norm = (float)qam_norm(QM);
+    PROF_DECL;
+        PROF_T(p0);
+        // ---- a1: H of the batch (fp32, SW128) in the B regions -> XB = bf16 hi | lo
+        mbar_wait(bar_tma, it & 1);
+        PROF_ADD(prof, 0, p0);
+        PROF_T(p1);
+#pragma unroll 2
+        for (int q = gt; q < su::UPB * 256; q += 128) {  // item = (unit, row r, 8 columns 8 cp .. 8 cp + 7)
+            const int s = q >> 8, r = (q >> 2) & 63, cp = q & 3, sw = r & 7;
+            const unsigned char* src = g + su::BG + s * 8192 + r * 128;
+            const float4 v0 = *reinterpret_cast<const float4*>(src + (((2 * cp) ^ sw) << 4));
+            const float4 v1 = *reinterpret_cast<const float4*>(src + (((2 * cp + 1) ^ sw) << 4));
+            uint32_t hi[4], lo[4];
+            tc::split_bf2(v0.x, v0.y, hi[0], lo[0]);
+            tc::split_bf2(v0.z, v0.w, hi[1], lo[1]);
+            tc::split_bf2(v1.x, v1.y, hi[2], lo[2]);
+            tc::split_bf2(v1.z, v1.w, hi[3], lo[3]);
+            unsigned char* dst = g + su::XB + s * 8192 + r * 128;
+            *reinterpret_cast<uint4*>(dst + ((cp ^ sw) << 4)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+            *reinterpret_cast<uint4*>(dst + (((4 + cp) ^ sw) << 4)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        }
+        tc::fence_proxy_async();
+        tc::fence_before();
+        sync();
+        PROF_ADD(prof, 1, p1);
+        PROF_T(p2);
+        // ---- a2: Gram, MN-major XB as both operands: C = (hi + lo)^T (hi + lo) lands in D rows 0-31 (A = the
+        // hi columns, then, from start + 64 B, the lo columns; D rows 32-63 then read past the tile: unused)
+        if (gt == 0) {
+            tc::fence_after();
+            constexpr uint32_t idg = tc::idesc(tc::kFmtBF16, 64, 32, 1, 1);
+            for (int s = 0; s < su::UPB; ++s) {
+                const uint32_t xs = gaddr + (uint32_t)(su::XB + s * 8192);
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) {  // K = antennas 16 ks .. 16 ks + 15 = two 8-row atoms
+                    const uint64_t dh = tc::desc_sw128(xs + 2048u * ks, 16, 1024);
+                    const uint64_t dl = tc::desc_sw128(xs + 64u + 2048u * ks, 16, 1024);
+                    tc::mma_f16_ss(tmem + 32u * s, dh, dh, idg, ks ? 1u : 0u);
+                    tc::mma_f16_ss(tmem + 32u * s, dh, dl, idg, 1u);
+                    tc::mma_f16_ss(tmem + 32u * s, dl, dh, idg, 1u);
+                    tc::mma_f16_ss(tmem + 32u * s, dl, dl, idg, 1u);
+                }
+            }
+            tc::commit(bar_mma);
+        }
+        mbar_wait(bar_mma, 0);
+        PROF_ADD(prof, 2, p2);
+        PROF_T(p3);
+        tc::fence_after();
+        if (gw < 2) {  // M = 64 accumulator: row m in TMEM lane 32 (m / 16) + m % 16 -> C rows 16 warp + lane
+#pragma unroll 1
+            for (int s = 0; s < su::UPB; ++s) {
+                uint32_t v[32];
+                tc::ld32(tmem + ((uint32_t)(32 * gw) << 16) + 32u * s, v);
+                tc::wait_ld();
+                if (lane < 16) {
+                    const int m = 16 * gw + lane;
+                    float* cs = reinterpret_cast<float*>(g + su::BG + s * 8192 + 4096);
+#pragma unroll
+                    for (int c = 0; c < 8; ++c)
+                        reinterpret_cast<float4*>(cs + m * 32)[c ^ (m & 7)] =
+                            make_float4(__uint_as_float(v[4 * c]), __uint_as_float(v[4 * c + 1]),
+                                        __uint_as_float(v[4 * c + 2]), __uint_as_float(v[4 * c + 3]));
+                }
+            }
+        }
+        tc::fence_before();
+        sync();
+        PROF_ADD(prof, 3, p3);
+        PROF_T(p4);
+        // ---- a3-a5: warp w inverts unit w; lane (k, h) = (lane / 2, lane % 2) holds G[k][8h .. 8h+7]
+        if (!waited) {
+            pdl_wait();
+            waited = true;
+        }
+        {
+            const int s = gw, k = lane >> 1, h = lane & 1;
+            const bool valid = s < nv;
+            const long long u = valid ? unit_of(s) : unit_of(0);
+            const float s2 = unit_sigma2(a, u);
+            const float* cs = reinterpret_cast<const float*>(g + su::BG + s * 8192 + 4096);
+            float2 gq[8];
+            {
+                const int m0 = 2 * k, m1 = 2 * k + 1;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {  // columns 16h + 4i .. +3 = layers 8h + 2i, 8h + 2i + 1
+                    const float4 c0 = reinterpret_cast<const float4*>(cs + m0 * 32)[(4 * h + i) ^ (m0 & 7)];
+                    const float4 c1 = reinterpret_cast<const float4*>(cs + m1 * 32)[(4 * h + i) ^ (m1 & 7)];
+                    gq[2 * i] = make_float2(c0.x + c1.y, c0.y - c1.x);
+                    gq[2 * i + 1] = make_float2(c0.z + c1.w, c0.w - c1.z);
+                }
+            }
+            float gd = 0.f;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const bool d = 8 * h + q == k;
+                gq[q].x += d ? s2 : 0.f;
+                gq[q].y = d ? 0.f : gq[q].y;
+                gd = fmaxf(gd, d ? gq[q].x : 0.f);
+            }
+            float gmax = gd;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, off));
+            bool fail = !(gmax == gmax);
+            const float tau = (float)kPivotTau * gmax;
+            // pivot loop rolled over the two column halves (hj), unrolled inside (qj): the fully unrolled
+            // elimination is ~1.7k instructions and starves the warps on instruction fetch
+#pragma unroll 1
+            for (int hj = 0; hj < 2; ++hj)
+#pragma unroll
+            for (int qj = 0; qj < 8; ++qj) {
+                const int j = 8 * hj + qj;
+                const float2 f = shfl2(gq[qj], (lane & ~1) | hj);          // G[k][j]
+                float p = __shfl_sync(0xffffffffu, gq[qj].x, 2 * j + hj);  // G[j][j]
+                if (!(p > tau)) {
+                    fail = true;
+                    p = 1.f;
+                }
+                const float pinv = __frcp_rn(p);
+                const bool prow = k == j;
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    float2 rj = shfl2(gq[q], 2 * j + h);  // G[j][8h+q]
+                    if (8 * h + q == j) rj = make_float2(1.f, 0.f);
+                    rj = make_float2(rj.x * pinv, rj.y * pinv);
+                    float2 b = (8 * h + q == j) ? make_float2(0.f, 0.f) : gq[q];
+                    b.x = fmaf(-f.x, rj.x, fmaf(f.y, rj.y, b.x));
+                    b.y = fmaf(-f.x, rj.y, fmaf(-f.y, rj.x, b.y));
+                    gq[q] = prow ? rj : b;
+                }
+            }
+            // A_kk = [G^-1]_kk lives in lane (k, k / 8)
+            float Ad = 0.f;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) Ad += (8 * h + q == k) ? gq[q].x : 0.f;
+            const float A = Ad + __shfl_xor_sync(0xffffffffu, Ad, 1);
+            const float mu = fmaf(-s2, A, 1.f);
+            float sinr, fac;
+            if (s2 == 0.f) {
+                sinr = __int_as_float(0x7f800000);
+                fac = sqrtf(norm);
+            } else {
+                sinr = __fdividef(mu, s2 * A);
+                fac = __fdividef(sqrtf(norm), mu);
+            }
+            if (!(mu > 0.f) || fail) {
+                sinr = 0.f;
+                fac = 0.f;
+            }
+            __syncwarp();  // C is read; its region becomes B'_lo
+            // B' rows k (Re W~_k) and 16 + k (Im W~_k): K pair (2l, 2l+1) = (Re, Im) parts, duplicated over
+            // the hi | lo halves of K (chunks c and 4 + c); this lane's layers l = 8h .. 8h+7 = chunks 2h, 2h+1
+            unsigned char* bh = g + su::BG + s * 8192;
+            unsigned char* bl = bh + 4096;
+#pragma unroll
+            for (int cc = 0; cc < 2; ++cc) {
+                uint32_t rh[4], rl[4], ih[4], il[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 w = make_float2(fac * gq[4 * cc + e].x, fac * gq[4 * cc + e].y);
+                    tc::split_bf2(w.x, w.y, rh[e], rl[e]);
+                    tc::split_bf2(w.y, -w.x, ih[e], il[e]);
+                }
+                const int c = 2 * h + cc, nr = k, ni = 16 + k;
+#pragma unroll
+                for (int dup = 0; dup < 2; ++dup) {
+                    const int cd = c + 4 * dup;
+                    *reinterpret_cast<uint4*>(bh + nr * 128 + ((cd ^ (nr & 7)) << 4)) = make_uint4(rh[0], rh[1], rh[2], rh[3]);
+                    *reinterpret_cast<uint4*>(bl + nr * 128 + ((cd ^ (nr & 7)) << 4)) = make_uint4(rl[0], rl[1], rl[2], rl[3]);
+                    *reinterpret_cast<uint4*>(bh + ni * 128 + ((cd ^ (ni & 7)) << 4)) = make_uint4(ih[0], ih[1], ih[2], ih[3]);
+                    *reinterpret_cast<uint4*>(bl + ni * 128 + ((cd ^ (ni & 7)) << 4)) = make_uint4(il[0], il[1], il[2], il[3]);
+                }
+            }
+            if (valid && h == 0) {
+                float* wsu = reinterpret_cast<float*>(a.ws) + u * WS;
+                wsu[NR * NL * 2 + k] = sinr / norm * a.llr_scale;
+                if (a.sinr) a.sinr[u * NL + k] = sinr;
+                if (k == 0 && fail) atomicAdd(a.fail_count, 1ull);
+            }
+        }
+        tc::fence_proxy_async();
+        tc::fence_before();
+        sync();
+        PROF_ADD(prof, 4, p4);
+        PROF_T(p5);
+        // ---- a4: W~^T = XB B'^T (K-major view of XB: K = 64 = hi | lo halves)
+        if (gt == 0) {
+            tc::fence_after();
+            constexpr uint32_t idw = tc::idesc(tc::kFmtBF16, 64, 32);
+            for (int s = 0; s < su::UPB; ++s) {
+                const uint32_t xs = gaddr + (uint32_t)(su::XB + s * 8192), bs = gaddr + (uint32_t)(su::BG + s * 8192);
+#pragma unroll
+                for (int ks = 0; ks < 4; ++ks) {
+                    const uint64_t dA = tc::desc_sw128(xs + 32u * ks);
+                    tc::mma_f16_ss(tmem + 32u * s, dA, tc::desc_sw128(bs + 32u * ks), idw, ks ? 1u : 0u);
+                    tc::mma_f16_ss(tmem + 32u * s, dA, tc::desc_sw128(bs + 4096u + 32u * ks), idw, 1u);
+                }
+            }
+            tc::commit(bar_mma);
+        }
+        mbar_wait(bar_mma, 1);
+        if (gt == 0) issue_next();  // the B regions are free: the next batch's H loads under the W~ readout
+        PROF_ADD(prof, 5, p5);
+        PROF_T(p6);
+        tc::fence_after();
+#pragma unroll 1
+        for (int s = 0; s < nv; ++s) {  // row r = 16 warp + lane of W~^T: cols k = Re W~_kr, 16 + k = Im W~_kr
+            uint32_t v[32];
+            tc::ld32(tmem + ((uint32_t)(32 * gw) << 16) + 32u * s, v);
+            tc::wait_ld();
+            if (lane < 16) {
+                const int r = 16 * gw + lane;
+                uint32_t o[32];
+#pragma unroll
+                for (int kq = 0; kq < NL; ++kq) {
+                    o[2 * kq] = v[kq];
+                    o[2 * kq + 1] = v[16 + kq];
+                }
+                char* dst = reinterpret_cast<char*>(reinterpret_cast<float*>(a.ws) + unit_of(s) * WS) + (size_t)r * NL * 8;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) st_v8(dst + 32 * q, o + 8 * q);
+            }
+        }
+        // the W~ records (and the slopes written above) are read next by TMA (async proxy) in the fused kernel:
+        // make them visible at GPU scope and to the async proxy before the group barrier publishes them
+        __threadfence();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        tc::fence_before();
+        sync();
+        PROF_ADD(prof, 6, p6);
+    PROF_SFLUSH(gt == 0);
+}
+
+template <int QM, int LT, int EW, int S_, int NLO_, int TA, bool BEPI, bool FUSED>
+__global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
+    k_c5_apply(DetectArgs a, const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap hmap) {
+    constexpr int NR = 64, NL = 16;
+    using SM = C5Smem<S_, NLO_, TA, FUSED>;
     constexpr int S = S_, NLO = NLO_;
     static_assert(EW == 6, "6 epilogue warps (4 for tile 0, 2 for the compact tile 1)");
 
@@ -130,7 +429,9 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_c5_apply(DetectArgs a, con
     constexpr uint32_t kAccCols = KC ? 64u : 128u;   // TMEM columns per accumulator (2 row tiles)
     constexpr uint32_t kAring = 2u * kAccCols;       // TMEM columns 0 .. kAring-1: 2 accumulators
     constexpr uint32_t kAcols = TA == 1 ? 128u : 64u;  // TMEM columns per A ring slot (one chunk, 2 tiles)
-    static_assert(kAring + NLO * kAcols <= 512u, "TMEM");
+    static_assert(kAring + NLO * kAcols + (FUSED ? 128u : 0u) <= 512u, "TMEM");
+    static_assert(!FUSED || BEPI, "fused setup: the epilogue warps build the B sets");
+    constexpr uint32_t kSetupCols = kAring + NLO * kAcols;  // FUSED: the setup group's 128 TMEM columns
     constexpr int CW = 4 + EW;                       // MMA warp; CW + 1: TMA producer
     constexpr int WS = BigWs<NR, NL>::stride;
     extern __shared__ unsigned char smem_raw[];
@@ -147,6 +448,9 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_c5_apply(DetectArgs a, con
     uint64_t* tfree = accfull + 2;     // [2]    epilogue done with the accumulator
     uint64_t* wfull = tfree + 2;       // [2]    W~ record of unit i staged (TMA tx)
     uint64_t* wfree = wfull + 2;       // [2]    B set built from it
+    uint64_t* stma = wfree + 2;        //        FUSED: setup group's H TMA
+    uint64_t* smma = stma + 1;         //        FUSED: setup group's MMAs
+    volatile int* units_ready = reinterpret_cast<volatile int*>(g + SM::ready);  // FUSED
     uint32_t* tslot = reinterpret_cast<uint32_t*>(g + SM::tslot);
     float* sslope = reinterpret_cast<float*>(g + SM::slope);
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -172,6 +476,9 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_c5_apply(DetectArgs a, con
             mbar_init(&wfull[i], 1);
             mbar_init(&wfree[i], 1);
         }
+        mbar_init(stma, 1);
+        mbar_init(smma, 1);
+        *units_ready = 0;
         fence_mbar_init();
     }
     if (warp == CW) tc::alloc<512>(tslot);
@@ -191,6 +498,12 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_c5_apply(DetectArgs a, con
             auto issue_w = [&](long long i) {
                 const int ws_ = (int)(i & 1);
                 if (i >= 2) mbar_wait_sleep(&wfree[ws_], (uint32_t)(((i >> 1) + 1) & 1));
+                if constexpr (FUSED) {  // the setup group of this CTA has written unit i's W~ record
+                    PROF_T(tsw);
+                    while (*units_ready <= i) __nanosleep(64);
+                    PROF_ADD(prof, 1, tsw);
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                }
                 mbar_arrive_expect_tx(&wfull[ws_], (uint32_t)SM::wrec);
                 bulk_g2s(g + SM::wst + ws_ * SM::wrec,
                          reinterpret_cast<const float*>(a.ws) + (u0 + i * du) * (long long)WS, (uint32_t)SM::wrec,
@@ -221,6 +534,35 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_c5_apply(DetectArgs a, con
             PROF_ADD(prof, 31, tk0);
             PROF_FLUSH(true);
         }
+    } else if (FUSED && warp >= CW + 2) {
+        // ================= fused setup group (warps 12-15 = lane quadrants 0-3): rows a2-a5 of this CTA's
+        // units, four at a time, ahead of the apply pipeline; W~ records to the workspace (L2-resident
+        // by the time the producer stages them), progress published through units_ready =================
+        const int gw = warp - (CW + 2), gt = t - 32 * (CW + 2);
+        bool waited = false;
+        uint32_t it = 0;
+        if (gt == 0) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&hmap)) : "memory");
+        auto nv_of = [&](long long j0) { return (int)min((long long)su::UPB, n_my - j0); };
+        if (gt == 0 && n_my > 0)
+            setup_issue_h(&hmap, base + (uint32_t)SM::setup, stma, nv_of(0), [&](int s_) { return u0 + s_ * du; });
+#pragma unroll 1
+        for (long long j0 = 0; j0 < n_my; j0 += su::UPB, ++it) {
+            const int nv = nv_of(j0);
+            const long long jn = j0 + su::UPB;
+            setup_batch<QM>(a, &hmap, g + SM::setup, base + (uint32_t)SM::setup, stma, smma, tmem + kSetupCols, it, nv,
+                            gt, gw, lane, waited, [&](int s_) { return u0 + (j0 + s_) * du; },
+                            [] { asm volatile("bar.sync 5, 128;" ::: "memory"); },
+                            [&] {
+                                if (jn < n_my)
+                                    setup_issue_h(&hmap, base + (uint32_t)SM::setup, stma, nv_of(jn),
+                                                  [&](int s_) { return u0 + (jn + s_) * du; });
+                            });
+            if (gt == 0) {
+                __threadfence_block();
+                *units_ready = (int)(j0 + nv);
+            }
+        }
+        if (!waited) pdl_wait();
     } else if (warp == CW) {
         // ================= MMA issuer =================
         if (lane == 0) {
@@ -521,44 +863,8 @@ __global__ void __launch_bounds__(32 * (6 + EW), 1) k_c5_apply(DetectArgs a, con
     if (warp == CW) tc::dealloc<512>(tmem);
 }
 
-// ------------------------------------------------------------------------
-// k_c5_setup: rows a2-a5 with both contractions on the tensor cores (BF16 split
-// operands, reading R28) and the 16 x 16 inversion on the FP32 pipe. One CTA =
-// 4 warps = 4 H-units per batch (warp w owns unit w of the batch):
-//   a1  H_u (64 x 16 complex = 64 x 32 real X, row r = antenna) by a 2-D TMA box
-//       (fp32, SWIZZLE_128B), converted to XB = [X_hi | X_lo] (bf16, 128-B row r,
-//       same swizzle), X_hi = rn_bf16(X), X_lo = rn_bf16(X - X_hi);
-//   a2  C = (X_hi + X_lo)^T (X_hi + X_lo): 16 kind::f16 MMAs with BOTH operands the
-//       MN-major view of XB (M = 64 from the hi, then the lo columns, N = 32 hi then 32
-//       lo, K = 64 antennas), C in D rows 0-31; G_kl = (C[2k][2l] + C[2k+1][2l+1]) +
-//       i (C[2k][2l+1] - C[2k+1][2l]) + sigma2 delta_kl;
-//   a3-a5  G^-1 by in-place Gauss-Jordan (no pivoting: G is Hermitian PD; its
-//       pivots are the LDL^H pivots, so guard R17 reads the same quantities as
-//       Cholesky's d_jj^2 -- reading R26), mu, SINR, fac = sqrt(norm) / mu,
-//       B = real form of fac G^-1, split into bf16 hi / lo and duplicated along K;
-//   a4  W~^T = XB B'^T: 8 kind::f16 MMAs, A = the K-major view of the SAME XB tile
-//       (K = 64 = hi | lo halves of the 32 real inputs), B' = [B | B] (hi, lo).
-// TMEM: 32 columns per unit (the Gram accumulator, reused for W~). M = 64
-// accumulators put row m in lane 32 (m / 16) + m % 16, so every warp reads its
-// lane quadrant of W~, and warps 0-1 read C.
-// (A persistent warp-specialised variant -- producer, MMA, readout and 12 worker warps
-// over a ring of unit slots -- measured 107-124 us against this kernel's 90, the
-// per-slot chain of H load, Gram round trip and inversion being sequential.)
-namespace su {
-constexpr int UPB = 4;                   // units per batch (= warps)
-constexpr size_t XB = 0;                 // [UPB] x 8 KiB  bf16 [64 r][hi c 0..31 | lo c 0..31], SW128
-constexpr size_t BG = UPB * 8192;        // [UPB] x 8 KiB  H landing (fp32) -> exchange | C -> B'_hi | B'_lo
-constexpr size_t BAR = BG + UPB * 8192;
-constexpr size_t TSLOT = BAR + 16;
-constexpr size_t TOTAL = TSLOT + 16 + 1024;  // + 1024-B alignment slack
-constexpr int CTAS_PER_SM = 3;
-static_assert(TOTAL * CTAS_PER_SM <= 227 * 1024, "shared memory");
-}  // namespace su
-
 template <int QM>
 __global__ void __launch_bounds__(128, su::CTAS_PER_SM) k_c5_setup(DetectArgs a, const __grid_constant__ CUtensorMap hmap) {
-    constexpr int NR = 64, NL = 16;
-    constexpr int WS = BigWs<NR, NL>::stride;
     extern __shared__ unsigned char smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
@@ -567,7 +873,6 @@ __global__ void __launch_bounds__(128, su::CTAS_PER_SM) k_c5_setup(DetectArgs a,
     uint64_t* bar_mma = bar_tma + 1;
     uint32_t* tslot = reinterpret_cast<uint32_t*>(g + su::TSLOT);
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const float norm = (float)qam_norm(QM);
     const long long n_batch = (a.n_units + su::UPB - 1) / su::UPB;
 
     pdl_launch_dependents();
@@ -584,246 +889,18 @@ __global__ void __launch_bounds__(128, su::CTAS_PER_SM) k_c5_setup(DetectArgs a,
     const uint32_t tmem = *tslot;
     bool waited = false;  // PDL: the previous call may still read the workspace
     uint32_t it = 0;
+    auto nv_of = [&](long long bt) { return (int)min((long long)su::UPB, a.n_units - bt * su::UPB); };
+    if (t == 0 && blockIdx.x < n_batch)
+        setup_issue_h(&hmap, base, bar_tma, nv_of(blockIdx.x), [&](int s) { return (long long)blockIdx.x * su::UPB + s; });
 #pragma unroll 1
-    PROF_DECL;
     for (long long bt = blockIdx.x; bt < n_batch; bt += gridDim.x, ++it) {
-        PROF_T(p0);
-        const long long ub = bt * su::UPB;
-        const int nv = (int)min((long long)su::UPB, a.n_units - ub);  // valid units in this batch
-        // ---- a1: H of the batch (fp32, SW128) into the B regions, then XB = bf16 hi | lo
-        if (t == 0) {
-            mbar_arrive_expect_tx(bar_tma, (uint32_t)(nv * NR * NL * 8));
-            for (int s = 0; s < nv; ++s)
-                asm volatile(
-                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-                    ::"r"(base + (uint32_t)(su::BG + s * 8192)), "l"(reinterpret_cast<uint64_t>(&hmap)), "r"(0),
-                    "r"((int)((ub + s) * NR)), "r"(smem_u32(bar_tma))
-                    : "memory");
-        }
-        mbar_wait(bar_tma, it & 1);
-        PROF_ADD(prof, 0, p0);
-        PROF_T(p1);
-#pragma unroll 2
-        for (int q = t; q < su::UPB * 256; q += 128) {  // item = (unit, row r, 8 columns 8 cp .. 8 cp + 7)
-            const int s = q >> 8, r = (q >> 2) & 63, cp = q & 3, sw = r & 7;
-            const unsigned char* src = g + su::BG + s * 8192 + r * 128;
-            const float4 v0 = *reinterpret_cast<const float4*>(src + (((2 * cp) ^ sw) << 4));
-            const float4 v1 = *reinterpret_cast<const float4*>(src + (((2 * cp + 1) ^ sw) << 4));
-            uint32_t hi[4], lo[4];
-            tc::split_bf2(v0.x, v0.y, hi[0], lo[0]);
-            tc::split_bf2(v0.z, v0.w, hi[1], lo[1]);
-            tc::split_bf2(v1.x, v1.y, hi[2], lo[2]);
-            tc::split_bf2(v1.z, v1.w, hi[3], lo[3]);
-            unsigned char* dst = g + su::XB + s * 8192 + r * 128;
-            *reinterpret_cast<uint4*>(dst + ((cp ^ sw) << 4)) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-            *reinterpret_cast<uint4*>(dst + (((4 + cp) ^ sw) << 4)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
-        }
-        tc::fence_proxy_async();
-        tc::fence_before();
-        __syncthreads();
-        PROF_ADD(prof, 1, p1);
-        PROF_T(p2);
-        // ---- a2: Gram, MN-major XB as both operands: C = (hi + lo)^T (hi + lo) lands in D rows 0-31 (A = the
-        // hi columns, then, from start + 64 B, the lo columns; D rows 32-63 then read past the tile: unused)
-        if (t == 0) {
-            tc::fence_after();
-            constexpr uint32_t idg = tc::idesc(tc::kFmtBF16, 64, 32, 1, 1);
-            for (int s = 0; s < su::UPB; ++s) {
-                const uint32_t xs = base + (uint32_t)(su::XB + s * 8192);
-#pragma unroll
-                for (int ks = 0; ks < 4; ++ks) {  // K = antennas 16 ks .. 16 ks + 15 = two 8-row atoms
-                    const uint64_t dh = tc::desc_sw128(xs + 2048u * ks, 16, 1024);
-                    const uint64_t dl = tc::desc_sw128(xs + 64u + 2048u * ks, 16, 1024);
-                    tc::mma_f16_ss(tmem + 32u * s, dh, dh, idg, ks ? 1u : 0u);
-                    tc::mma_f16_ss(tmem + 32u * s, dh, dl, idg, 1u);
-                    tc::mma_f16_ss(tmem + 32u * s, dl, dh, idg, 1u);
-                    tc::mma_f16_ss(tmem + 32u * s, dl, dl, idg, 1u);
-                }
-            }
-            tc::commit(bar_mma);
-        }
-        mbar_wait(bar_mma, 0);
-        PROF_ADD(prof, 2, p2);
-        PROF_T(p3);
-        tc::fence_after();
-        if (warp < 2) {  // M = 64 accumulator: row m in TMEM lane 32 (m / 16) + m % 16 -> C rows 16 warp + lane
-#pragma unroll 1
-            for (int s = 0; s < su::UPB; ++s) {
-                uint32_t v[32];
-                tc::ld32(tmem + ((uint32_t)(32 * warp) << 16) + 32u * s, v);
-                tc::wait_ld();
-                if (lane < 16) {
-                    const int m = 16 * warp + lane;
-                    float* cs = reinterpret_cast<float*>(g + su::BG + s * 8192 + 4096);
-#pragma unroll
-                    for (int c = 0; c < 8; ++c)
-                        reinterpret_cast<float4*>(cs + m * 32)[c ^ (m & 7)] =
-                            make_float4(__uint_as_float(v[4 * c]), __uint_as_float(v[4 * c + 1]),
-                                        __uint_as_float(v[4 * c + 2]), __uint_as_float(v[4 * c + 3]));
-                }
-            }
-        }
-        tc::fence_before();
-        __syncthreads();
-        PROF_ADD(prof, 3, p3);
-        PROF_T(p4);
-        // ---- a3-a5: warp w inverts unit w; lane (k, h) = (lane / 2, lane % 2) holds G[k][8h .. 8h+7]
-        if (!waited) {
-            pdl_wait();
-            waited = true;
-        }
-        {
-            const int s = warp, k = lane >> 1, h = lane & 1;
-            const long long u = ub + s;
-            const bool valid = s < nv;
-            const float s2 = unit_sigma2(a, valid ? u : ub);
-            const float* cs = reinterpret_cast<const float*>(g + su::BG + s * 8192 + 4096);
-            float2 gq[8];
-            {
-                const int m0 = 2 * k, m1 = 2 * k + 1;
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {  // columns 16h + 4i .. +3 = layers 8h + 2i, 8h + 2i + 1
-                    const float4 c0 = reinterpret_cast<const float4*>(cs + m0 * 32)[(4 * h + i) ^ (m0 & 7)];
-                    const float4 c1 = reinterpret_cast<const float4*>(cs + m1 * 32)[(4 * h + i) ^ (m1 & 7)];
-                    gq[2 * i] = make_float2(c0.x + c1.y, c0.y - c1.x);
-                    gq[2 * i + 1] = make_float2(c0.z + c1.w, c0.w - c1.z);
-                }
-            }
-            float gd = 0.f;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) {
-                const bool d = 8 * h + q == k;
-                gq[q].x += d ? s2 : 0.f;
-                gq[q].y = d ? 0.f : gq[q].y;
-                gd = fmaxf(gd, d ? gq[q].x : 0.f);
-            }
-            float gmax = gd;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, off));
-            bool fail = !(gmax == gmax);
-            const float tau = (float)kPivotTau * gmax;
-            // pivot loop rolled over the two column halves (hj), unrolled inside (qj): the fully unrolled
-            // elimination is ~1.7k instructions and starves the warps on instruction fetch
-#pragma unroll 1
-            for (int hj = 0; hj < 2; ++hj)
-#pragma unroll
-            for (int qj = 0; qj < 8; ++qj) {
-                const int j = 8 * hj + qj;
-                const float2 f = shfl2(gq[qj], (lane & ~1) | hj);          // G[k][j]
-                float p = __shfl_sync(0xffffffffu, gq[qj].x, 2 * j + hj);  // G[j][j]
-                if (!(p > tau)) {
-                    fail = true;
-                    p = 1.f;
-                }
-                const float pinv = __frcp_rn(p);
-                const bool prow = k == j;
-#pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    float2 rj = shfl2(gq[q], 2 * j + h);  // G[j][8h+q]
-                    if (8 * h + q == j) rj = make_float2(1.f, 0.f);
-                    rj = make_float2(rj.x * pinv, rj.y * pinv);
-                    float2 b = (8 * h + q == j) ? make_float2(0.f, 0.f) : gq[q];
-                    b.x = fmaf(-f.x, rj.x, fmaf(f.y, rj.y, b.x));
-                    b.y = fmaf(-f.x, rj.y, fmaf(-f.y, rj.x, b.y));
-                    gq[q] = prow ? rj : b;
-                }
-            }
-            // A_kk = [G^-1]_kk lives in lane (k, k / 8)
-            float Ad = 0.f;
-#pragma unroll
-            for (int q = 0; q < 8; ++q) Ad += (8 * h + q == k) ? gq[q].x : 0.f;
-            const float A = Ad + __shfl_xor_sync(0xffffffffu, Ad, 1);
-            const float mu = fmaf(-s2, A, 1.f);
-            float sinr, fac;
-            if (s2 == 0.f) {
-                sinr = __int_as_float(0x7f800000);
-                fac = sqrtf(norm);
-            } else {
-                sinr = __fdividef(mu, s2 * A);
-                fac = __fdividef(sqrtf(norm), mu);
-            }
-            if (!(mu > 0.f) || fail) {
-                sinr = 0.f;
-                fac = 0.f;
-            }
-            __syncwarp();  // C is read; its region becomes B'_lo
-            // B' rows k (Re W~_k) and 16 + k (Im W~_k): K pair (2l, 2l+1) = (Re, Im) parts, duplicated over
-            // the hi | lo halves of K (chunks c and 4 + c); this lane's layers l = 8h .. 8h+7 = chunks 2h, 2h+1
-            unsigned char* bh = g + su::BG + s * 8192;
-            unsigned char* bl = bh + 4096;
-#pragma unroll
-            for (int cc = 0; cc < 2; ++cc) {
-                uint32_t rh[4], rl[4], ih[4], il[4];
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float2 w = make_float2(fac * gq[4 * cc + e].x, fac * gq[4 * cc + e].y);
-                    tc::split_bf2(w.x, w.y, rh[e], rl[e]);
-                    tc::split_bf2(w.y, -w.x, ih[e], il[e]);
-                }
-                const int c = 2 * h + cc, nr = k, ni = 16 + k;
-#pragma unroll
-                for (int dup = 0; dup < 2; ++dup) {
-                    const int cd = c + 4 * dup;
-                    *reinterpret_cast<uint4*>(bh + nr * 128 + ((cd ^ (nr & 7)) << 4)) = make_uint4(rh[0], rh[1], rh[2], rh[3]);
-                    *reinterpret_cast<uint4*>(bl + nr * 128 + ((cd ^ (nr & 7)) << 4)) = make_uint4(rl[0], rl[1], rl[2], rl[3]);
-                    *reinterpret_cast<uint4*>(bh + ni * 128 + ((cd ^ (ni & 7)) << 4)) = make_uint4(ih[0], ih[1], ih[2], ih[3]);
-                    *reinterpret_cast<uint4*>(bl + ni * 128 + ((cd ^ (ni & 7)) << 4)) = make_uint4(il[0], il[1], il[2], il[3]);
-                }
-            }
-            if (valid && h == 0) {
-                float* wsu = reinterpret_cast<float*>(a.ws) + u * WS;
-                wsu[NR * NL * 2 + k] = sinr / norm * a.llr_scale;
-                if (a.sinr) a.sinr[u * NL + k] = sinr;
-                if (k == 0 && fail) atomicAdd(a.fail_count, 1ull);
-            }
-        }
-        tc::fence_proxy_async();
-        tc::fence_before();
-        __syncthreads();
-        PROF_ADD(prof, 4, p4);
-        PROF_T(p5);
-        // ---- a4: W~^T = XB B'^T (K-major view of XB: K = 64 = hi | lo halves)
-        if (t == 0) {
-            tc::fence_after();
-            constexpr uint32_t idw = tc::idesc(tc::kFmtBF16, 64, 32);
-            for (int s = 0; s < su::UPB; ++s) {
-                const uint32_t xs = base + (uint32_t)(su::XB + s * 8192), bs = base + (uint32_t)(su::BG + s * 8192);
-#pragma unroll
-                for (int ks = 0; ks < 4; ++ks) {
-                    const uint64_t dA = tc::desc_sw128(xs + 32u * ks);
-                    tc::mma_f16_ss(tmem + 32u * s, dA, tc::desc_sw128(bs + 32u * ks), idw, ks ? 1u : 0u);
-                    tc::mma_f16_ss(tmem + 32u * s, dA, tc::desc_sw128(bs + 4096u + 32u * ks), idw, 1u);
-                }
-            }
-            tc::commit(bar_mma);
-        }
-        mbar_wait(bar_mma, 1);
-        PROF_ADD(prof, 5, p5);
-        PROF_T(p6);
-        tc::fence_after();
-#pragma unroll 1
-        for (int s = 0; s < nv; ++s) {  // row r = 16 warp + lane of W~^T: cols k = Re W~_kr, 16 + k = Im W~_kr
-            uint32_t v[32];
-            tc::ld32(tmem + ((uint32_t)(32 * warp) << 16) + 32u * s, v);
-            tc::wait_ld();
-            if (lane < 16) {
-                const int r = 16 * warp + lane;
-                uint32_t o[32];
-#pragma unroll
-                for (int kq = 0; kq < NL; ++kq) {
-                    o[2 * kq] = v[kq];
-                    o[2 * kq + 1] = v[16 + kq];
-                }
-                char* dst = reinterpret_cast<char*>(reinterpret_cast<float*>(a.ws) + (ub + s) * WS) + (size_t)r * NL * 8;
-#pragma unroll
-                for (int q = 0; q < 4; ++q) st_v8(dst + 32 * q, o + 8 * q);
-            }
-        }
-        tc::fence_before();
-        __syncthreads();
-        PROF_ADD(prof, 6, p6);
+        const long long ub = bt * su::UPB, bn = bt + gridDim.x;
+        setup_batch<QM>(a, &hmap, g, base, bar_tma, bar_mma, tmem, it, nv_of(bt), t, warp, lane, waited,
+                        [&](int s) { return ub + s; }, [] { __syncthreads(); },
+                        [&] {
+                            if (bn < n_batch) setup_issue_h(&hmap, base, bar_tma, nv_of(bn), [&](int s) { return bn * su::UPB + s; });
+                        });
     }
-    PROF_SFLUSH(t == 0);
     if (!waited) pdl_wait();
     if (warp == 0) tc::dealloc<128>(tmem);
 }
@@ -879,7 +956,7 @@ cudaError_t prepare_setup() {
                                     (int)(4 * SetupSmem<64, 16, SETUP == 0 ? 0 : 1>::per_unit));
 }
 
-template <int QM, int LT, int EW, int S, int NLO, int TA, int SETUP, bool BEPI>
+template <int QM, int LT, int EW, int S, int NLO, int TA, int SETUP, bool BEPI, bool FUSED = false>
 cudaError_t launch_c5(const DetectArgs& a, cudaStream_t s) {
     if (a.n_units <= 0) return cudaSuccess;
     static int n_sm = 0;
@@ -899,27 +976,40 @@ cudaError_t launch_c5(const DetectArgs& a, cudaStream_t s) {
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return cudaErrorInvalidValue;
-    cudaError_t e = launch_setup<QM, SETUP>(a, s);
-    if (e != cudaSuccess) return e;
+    CUtensorMap hmap = ymap;  // FUSED: H as {32 floats (16 layers re/im), n_units * 64 rows}; box = one unit
+    if constexpr (FUSED) {
+        const cuuint64_t hdim[2] = {32, (cuuint64_t)a.n_units * 64};
+        const cuuint64_t hstride[1] = {128};
+        const cuuint32_t hbox[2] = {32, 64};
+        if (enc(&hmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float2*>(a.H), hdim, hstride, hbox, estride,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    } else {
+        cudaError_t e = launch_setup<QM, SETUP>(a, s);
+        if (e != cudaSuccess) return e;
+    }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(a.n_units < n_sm ? a.n_units : n_sm));
-    cfg.blockDim = dim3(32 * (6 + EW));
-    cfg.dynamicSmemBytes = C5Smem<S, NLO, TA>::total;
+    cfg.blockDim = dim3(32 * (6 + EW) + (FUSED ? 128 : 0));
+    cfg.dynamicSmemBytes = C5Smem<S, NLO, TA, FUSED>::total;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = a.overlap ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, k_c5_apply<QM, LT, EW, S, NLO, TA, BEPI>, a, ymap);
+    return cudaLaunchKernelEx(&cfg, k_c5_apply<QM, LT, EW, S, NLO, TA, BEPI, FUSED>, a, ymap, hmap);
 }
 
-template <int QM, int LT, int EW, int S, int NLO, int TA, int SETUP, bool BEPI>
+template <int QM, int LT, int EW, int S, int NLO, int TA, int SETUP, bool BEPI, bool FUSED = false>
 cudaError_t prepare_c5() {
-    cudaError_t e = prepare_setup<QM, SETUP>();
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_c5_apply<QM, LT, EW, S, NLO, TA, BEPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)C5Smem<S, NLO, TA>::total);
+    if constexpr (!FUSED) {
+        cudaError_t e = prepare_setup<QM, SETUP>();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaFuncSetAttribute(k_c5_apply<QM, LT, EW, S, NLO, TA, BEPI, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)C5Smem<S, NLO, TA, FUSED>::total);
 }
 
 size_t c5_workspace(const DetectArgs& a) { return (size_t)a.n_units * BigWs<64, 16>::stride * 4; }
@@ -929,16 +1019,22 @@ size_t c5_workspace(const DetectArgs& a) { return (size_t)a.n_units * BigWs<64, 
         NAME, 64, 16, QM, kSc, 14, LT, 32, 2, launch_c5<QM, LT, 6, S, NLO, TA, SETUP, BEPI>,               \
             prepare_c5<QM, LT, 6, S, NLO, TA, SETUP, BEPI>, c5_workspace                                   \
     }
+#define C5F_ENTRY(NAME, QM, LT, S)                                                                          \
+    KernelEntry {                                                                                          \
+        NAME, 64, 16, QM, kSc, 14, LT, 32, 1, launch_c5<QM, LT, 6, S, 4, 4, 2, true, true>,                \
+            prepare_c5<QM, LT, 6, S, 4, 4, 2, true, true>, c5_workspace                                    \
+    }
 
 // First entry of a shape = its default (mimo_api.cu select_fast); the others are selectable by name.
-// Name parts: operand split (bf16 / tf32), setup (tcs = tensor-core contractions; gj = SIMT Gauss-Jordan;
-// chol = SIMT Cholesky), be = the B sets built by the (under-loaded) epilogue warps instead of the
-// converter warps, which set the pace of the pipeline.
+// Name parts: fused = one kernel (setup warp group inside the apply); otherwise a setup kernel + the
+// apply: operand split (bf16 / bf16kc = one accumulator per tile / tf32), setup (tcs = tensor-core
+// contractions; gj = SIMT Gauss-Jordan; chol = SIMT Cholesky), be = the B sets built by the
+// (under-loaded) epilogue warps instead of the converter warps, which set the pace of the pipeline.
 const KernelEntry kEntries[] = {
-    C5_ENTRY("c5_bf16_tcs_be_64x16_q6_i8", 6, kLlrI8, 6, 4, 3, 2, true),  // C5 default
-    C5_ENTRY("c5_bf16_tcs_64x16_q6_i8", 6, kLlrI8, 6, 4, 3, 2, false),
+    C5F_ENTRY("c5_fused_64x16_q6_i8", 6, kLlrI8, 5),  // C5 default: setup warp group inside the apply kernel
+    C5_ENTRY("c5_bf16_tcs_be_64x16_q6_i8", 6, kLlrI8, 6, 4, 3, 2, true),  // two kernels: tensor-core setup + apply
     C5_ENTRY("c5_bf16kc_tcs_be_64x16_q6_i8", 6, kLlrI8, 6, 4, 4, 2, true),
-    C5_ENTRY("c5_bf16kc6_tcs_be_64x16_q6_i8", 6, kLlrI8, 6, 6, 4, 2, true),
+    C5_ENTRY("c5_bf16_tcs_64x16_q6_i8", 6, kLlrI8, 6, 4, 3, 2, false),
     C5_ENTRY("c5_bf16_gj_64x16_q6_i8", 6, kLlrI8, 6, 4, 3, 1, false),
     C5_ENTRY("c5_bf16_chol_64x16_q6_i8", 6, kLlrI8, 6, 4, 3, 0, false),
     C5_ENTRY("c5_tf32_gj_64x16_q6_i8", 6, kLlrI8, 4, 2, 1, 1, false),  // round-1 big8e6 configuration

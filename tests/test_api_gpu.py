@@ -85,14 +85,14 @@ def test_kernel_selection():
     assert mimo.Plan(7, 3, 4).kernel_name == "generic"
     assert mimo.Plan(4, 4, 4).launches_per_call == 1
     # the descriptor's kernel field: a named variant, "generic", an unknown name -> UNSUPPORTED
-    assert mimo.Plan(64, 16, 6, sc_per_h=12, llr_dtype="i8").kernel_name.startswith("c5_")
+    assert mimo.Plan(64, 16, 6, sc_per_h=12, llr_dtype="i8").kernel_name.startswith("c5_fused")
     assert mimo.Plan(64, 16, 6, sc_per_h=12, llr_dtype="i8", kernel="big_64x16_q6_i8").kernel_name == "big_64x16_q6_i8"
     assert mimo.Plan(4, 4, 4, kernel="generic").kernel_name == "generic"
     with pytest.raises(mimo.MimoError) as ei:
         mimo.Plan(4, 4, 4, kernel="no_such_kernel")
     assert ei.value.status == mimo.MIMO_ERR_UNSUPPORTED
     with pytest.raises(mimo.MimoError):  # a name of another shape's kernel does not serve this one
-        mimo.Plan(4, 4, 4, kernel="c5_bf16_64x16_q6_i8")
+        mimo.Plan(4, 4, 4, kernel="c5_fused_64x16_q6_i8")
 
 
 def test_host_path_async_then_sync_of_other_layout():

@@ -10,9 +10,9 @@ from paper_2510_07843_b200 import synth
 
 pytestmark = pytest.mark.gpu
 
-C5_VARIANTS = ["c5_bf16_tcs_be_64x16_q6_i8", "c5_bf16_tcs_64x16_q6_i8", "c5_bf16_gj_64x16_q6_i8",
-               "c5_bf16kc_tcs_be_64x16_q6_i8", "c5_bf16kc6_tcs_be_64x16_q6_i8",
-               "c5_bf16_chol_64x16_q6_i8", "c5_tf32_gj_64x16_q6_i8", "big_64x16_q6_i8"]
+C5_VARIANTS = ["c5_fused_64x16_q6_i8", "c5_bf16_tcs_be_64x16_q6_i8", "c5_bf16kc_tcs_be_64x16_q6_i8",
+               "c5_bf16_tcs_64x16_q6_i8", "c5_bf16_gj_64x16_q6_i8", "c5_bf16_chol_64x16_q6_i8", "c5_tf32_gj_64x16_q6_i8",
+               "big_64x16_q6_i8"]
 C4_VARIANTS = ["lg3hp_16x8_q8_f16", "lg3_16x8_q8_f16", "lg_16x8_q8_f16"]
 C3_VARIANTS = ["stream_8x4_q6_i8", "split_8x4_q6_i8", "prb_8x4_q6_i8"]
 

@@ -14,5 +14,5 @@ for _ in range(n): p.detect(H, y, float(w.sigma2), out=out)
 torch.cuda.synchronize()
 b1 = np.zeros(148 * 32, np.uint64); L.mimo_c5_sprof_read(ctypes.c_void_p(b1.ctypes.data))
 b = (b1 - b0).reshape(148, 32).astype(np.float64)
-nb = (w.n_units + 3) // 4 / 444 * 3  # batches per SM (3 CTAs each)
+nb = (w.n_units + 3) // 4 / 444 * 3 if 'fused' not in sys.argv[1] else w.n_units / 148 / 4  # batches per SM
 for s_, nm in names.items(): print(f"  {nm:18s} {b[:, s_].mean() / (n * nb):8.0f} cycles/batch (per CTA)")

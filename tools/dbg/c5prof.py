@@ -7,7 +7,7 @@ L = mimo.load_library(os.environ.get('PROFLIB', 'tools/dbg/libmimo_prof.so'))
 L.mimo_c5_prof_read.argtypes = [ctypes.c_void_p]
 w = synth.generate(5)
 H, y = torch.from_numpy(w.H).cuda(), torch.from_numpy(w.y).cuda()
-names = {0: "prod.wait_yfree", 31: "prod.total", 8: "mma.wait_bready", 9: "mma.wait_tfree", 10: "mma.wait_afull",
+names = {0: "prod.wait_yfree", 1: "prod.wait_setup(fused)", 31: "prod.total", 8: "mma.wait_bready", 9: "mma.wait_tfree", 10: "mma.wait_afull",
          16: "conv.wait_accfull(B)", 17: "conv.Bbuild", 18: "conv.wait_yfull", 19: "conv.wait_afree",
          20: "conv.convert", 21: "conv.bar+arrive", 24: "epi.wait_accfull", 25: "epi.work", 26: "epi.bar", 27: "epi.Bbuild"}
 for kn in sys.argv[1:]:

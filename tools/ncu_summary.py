@@ -112,8 +112,8 @@ def main():
           "Launch lists: `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
           "--clock-control none` over `python bench.py --config k --profile --steps 3 --warmup 2` "
           "(serialised, cold-cache launches: compare shares, not absolutes). Step traffic: "
-          "`ncu --replay-mode range` over 8 back-to-back calls of `tools/traffic_range.py` (rotating buffer sets "
-          "> 3x L2), so the LLR write-back is counted.", ""]
+          "`ncu --cache-control none` over 8 back-to-back calls of `tools/traffic_range.py` (rotating buffer sets "
+          "> 3x L2, no cache flush between kernels), so the LLR write-back is counted.", ""]
     for k in (1, 2, 3, 4, 5):
         name = synth.CONFIGS[k]["name"]
         b = synth.config_algorithmic_bytes(k)
@@ -139,21 +139,19 @@ def main():
         rp = os.path.join(src, f"range_c{k}.csv")
         if os.path.exists(rp):
             shutil.copy(rp, os.path.join(dst, f"range_c{k}.csv"))
-            rows = _csv(rp)
-            if len(rows) > 1:
-                h = rows[0]
-                met = {}
-                for r in rows[1:]:
-                    d = dict(zip(h, r))
-                    met[d["Metric Name"]] = (float(d["Metric Value"].replace(",", "")), d["Metric Unit"])
-                rd, wr = _val(met, "dram__bytes_read.sum") / 8, _val(met, "dram__bytes_write.sum") / 8
+            L = read_launches(rp)  # every kernel of 8 back-to-back steps, caches not flushed in between
+            if L:
+                rd = sum(_val(m, "dram__bytes_read.sum") for _, _, m in L) / 8
+                wr = sum(_val(m, "dram__bytes_write.sum") for _, _, m in L) / 8
                 traffic[name] = {"dram_bytes_per_step": rd + wr, "dram_read_per_step": rd, "dram_write_per_step": wr,
                                  "algorithmic_bytes_per_step": b["total"], "ratio": (rd + wr) / b["total"],
-                                 "source": f"profiles/{tag}/range_c{k}.csv",
-                                 "note": "ncu range replay over 8 back-to-back calls (rotating buffers), per step; "
-                                         "includes the setup kernel's W~ workspace round trip where there is one"}
-                md += [f"Step traffic (range of 8 calls): read {rd / 1e6:.1f} MB + write {wr / 1e6:.1f} MB = "
-                       f"{(rd + wr) / 1e6:.1f} MB per step = {(rd + wr) / b['total']:.3f} x algorithmic.", ""]
+                                 "launches": len(L), "source": f"profiles/{tag}/range_c{k}.csv",
+                                 "note": "ncu --cache-control none over 8 back-to-back calls (rotating buffers): L2 "
+                                         "write-back of one kernel's LLRs lands in the next; per step, includes the "
+                                         "setup kernel's W~ workspace traffic where there is one"}
+                md += [f"Step traffic (8 calls, no cache flush between kernels): read {rd / 1e6:.1f} MB + write "
+                       f"{wr / 1e6:.1f} MB = {(rd + wr) / 1e6:.1f} MB per step = {(rd + wr) / b['total']:.3f} x "
+                       f"the algorithmic {b['total'] / 1e6:.1f} MB.", ""]
     for nm, k, _ in FULL:
         rep = os.path.join(src, f"full_{nm}.ncu-rep")
         if not os.path.exists(rep):

@@ -15,7 +15,7 @@ done
 # DRAM traffic of whole steps over a range of back-to-back calls (counts the LLR write-back)
 for k in 2 3 4 5; do
   python tools/traffic_range.py --config $k --steps 8 > $out/range_plain_c$k.log 2>&1 && \
-  timeout 600 ncu --replay-mode range --clock-control none --csv \
+  timeout 600 ncu --profile-from-start off --cache-control none --clock-control none --csv \
       --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
       --log-file $out/range_c$k.csv python tools/traffic_range.py --config $k --steps 8 > $out/ncu_range_c$k.log 2>&1
 done

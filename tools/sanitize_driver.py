@@ -19,7 +19,7 @@ CASES = [  # (config, generate kwargs, forced kernel or None)
     (3, dict(n_sc=48, n_slots=1), None),
     (4, dict(n_sc=40, n_slots=1), None),
     (5, dict(n_sc=24, n_slots=1), None),
-    (5, dict(n_sc=24, n_slots=1), "c5_tf32_64x16_q6_i8"),
+    (5, dict(n_sc=24, n_slots=1), "c5_bf16_tcs_be_64x16_q6_i8"),
     (5, dict(n_sc=24, n_slots=1), "big_64x16_q6_i8"),
     (2, dict(n_sc=36, n_slots=1), "generic"),
 ]

@@ -1,11 +1,12 @@
 """K back-to-back detect calls of one config over rotating buffer sets (as bench.py), bracketed by
-cudaProfilerStart/Stop, for an ncu range capture of the DRAM traffic of whole steps -- so the LLR
-write-back that a single cold kernel capture leaves in L2 is counted (the last step's L2-resident
-tail, <= 126 MB, is the only undercount):
+cudaProfilerStart/Stop, for an ncu capture of the DRAM traffic of whole steps WITHOUT cache flushes
+between the kernels -- so the LLR write-back that a single cold kernel capture leaves in L2 is
+counted in the next kernel (the last step's L2-resident tail, <= 126 MB, is the only undercount):
 
-    ncu --replay-mode range \\
+    ncu --profile-from-start off --cache-control none \\
         --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \\
         python tools/traffic_range.py --config 5 --steps 8
+(ncu's --replay-mode range cannot be used: it rejects cuTensorMapEncodeTiled inside the range.)
 """
 import argparse
 import math
