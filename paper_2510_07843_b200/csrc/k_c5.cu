@@ -172,11 +172,17 @@ __device__ __forceinline__ void setup_issue_h(const CUtensorMap* hmapp, uint32_t
 // The batch's H tiles were issued by the previous batch (or the caller, for the first one);
 // issue_next() issues the next batch's as soon as this batch's W~ MMAs have released the B regions,
 // so that the H load overlaps the W~ readout.
-template <int QM, typename UnitF, typename SyncF, typename NextF>
+//
+// PUB (the fused kernel): the W~ records are read back by TMA inside the same kernel, so every writer
+// thread makes its record stores visible at GPU scope and to the async proxy before they are published.
+// That fence is deferred to the NEXT batch, after its conversion (the stores have drained by then and
+// the fence costs nothing), and publish_prev() (after the group barrier) announces the previous batch;
+// the caller fences and publishes the last batch itself.
+template <int QM, bool PUB, typename UnitF, typename SyncF, typename NextF, typename PubF>
 __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorMap* hmapp, unsigned char* g,
                                             uint32_t gaddr, uint64_t* bar_tma, uint64_t* bar_mma, uint32_t tmem,
                                             uint32_t it, int nv, int gt, int gw, int lane, bool& waited,
-                                            UnitF unit_of, SyncF sync, NextF issue_next) {
+                                            UnitF unit_of, SyncF sync, NextF issue_next, PubF publish_prev) {
     constexpr int NR = 64, NL = 16;
     constexpr int WS = BigWs<NR, NL>::stride;
     const float norm = (float)qam_norm(QM);
@@ -202,12 +208,21 @@ __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorM
             *reinterpret_cast<uint4*>(dst + (((4 + cp) ^ sw) << 4)) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
         }
         tc::fence_proxy_async();
+        if constexpr (PUB) {
+            if (it > 0) {  // the previous batch's W~ records (deferred, see above)
+                __threadfence();
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+            }
+        }
         tc::fence_before();
         sync();
+        if constexpr (PUB) publish_prev();
         PROF_ADD(prof, 1, p1);
         PROF_T(p2);
-        // ---- a2: Gram, MN-major XB as both operands: C = (hi + lo)^T (hi + lo) lands in D rows 0-31 (A = the
-        // hi columns, then, from start + 64 B, the lo columns; D rows 32-63 then read past the tile: unused)
+        // ---- a2: Gram, MN-major XB as both operands. A (M = 64) spans the whole 128-byte XB row = the hi
+        // columns (D rows 0-31) and the lo columns (D rows 32-63); B (N = 32) is the hi, then (start + 64 B)
+        // the lo columns: D = [hi | lo]^T (hi + lo), and C = (hi + lo)^T (hi + lo) = D[0:32] + D[32:64]
+        // (two MMAs per K step instead of four N = 32, M = 32-useful ones)
         if (gt == 0) {
             tc::fence_after();
             constexpr uint32_t idg = tc::idesc(tc::kFmtBF16, 64, 32, 1, 1);
@@ -219,8 +234,6 @@ __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorM
                     const uint64_t dl = tc::desc_sw128(xs + 64u + 2048u * ks, 16, 1024);
                     tc::mma_f16_ss(tmem + 32u * s, dh, dh, idg, ks ? 1u : 0u);
                     tc::mma_f16_ss(tmem + 32u * s, dh, dl, idg, 1u);
-                    tc::mma_f16_ss(tmem + 32u * s, dl, dh, idg, 1u);
-                    tc::mma_f16_ss(tmem + 32u * s, dl, dl, idg, 1u);
                 }
             }
             tc::commit(bar_mma);
@@ -229,21 +242,22 @@ __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorM
         PROF_ADD(prof, 2, p2);
         PROF_T(p3);
         tc::fence_after();
-        if (gw < 2) {  // M = 64 accumulator: row m in TMEM lane 32 (m / 16) + m % 16 -> C rows 16 warp + lane
+        // M = 64 accumulator: D row m in TMEM lane 32 (m / 16) + m % 16, so warp w < 2 holds D rows 16 w + lane
+        // (-> C_hi at BG + 4 KiB) and warp w >= 2 D rows 32 + 16 (w - 2) + lane (-> C_lo at BG); the inversion
+        // sums the two
 #pragma unroll 1
-            for (int s = 0; s < su::UPB; ++s) {
-                uint32_t v[32];
-                tc::ld32(tmem + ((uint32_t)(32 * gw) << 16) + 32u * s, v);
-                tc::wait_ld();
-                if (lane < 16) {
-                    const int m = 16 * gw + lane;
-                    float* cs = reinterpret_cast<float*>(g + su::BG + s * 8192 + 4096);
+        for (int s = 0; s < su::UPB; ++s) {
+            uint32_t v[32];
+            tc::ld32(tmem + ((uint32_t)(32 * gw) << 16) + 32u * s, v);
+            tc::wait_ld();
+            if (lane < 16) {
+                const int m = 16 * (gw & 1) + lane;
+                float* cs = reinterpret_cast<float*>(g + su::BG + s * 8192 + (gw < 2 ? 4096 : 0));
 #pragma unroll
-                    for (int c = 0; c < 8; ++c)
-                        reinterpret_cast<float4*>(cs + m * 32)[c ^ (m & 7)] =
-                            make_float4(__uint_as_float(v[4 * c]), __uint_as_float(v[4 * c + 1]),
-                                        __uint_as_float(v[4 * c + 2]), __uint_as_float(v[4 * c + 3]));
-                }
+                for (int c = 0; c < 8; ++c)
+                    reinterpret_cast<float4*>(cs + m * 32)[c ^ (m & 7)] =
+                        make_float4(__uint_as_float(v[4 * c]), __uint_as_float(v[4 * c + 1]),
+                                    __uint_as_float(v[4 * c + 2]), __uint_as_float(v[4 * c + 3]));
             }
         }
         tc::fence_before();
@@ -266,8 +280,12 @@ __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorM
                 const int m0 = 2 * k, m1 = 2 * k + 1;
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {  // columns 16h + 4i .. +3 = layers 8h + 2i, 8h + 2i + 1
-                    const float4 c0 = reinterpret_cast<const float4*>(cs + m0 * 32)[(4 * h + i) ^ (m0 & 7)];
-                    const float4 c1 = reinterpret_cast<const float4*>(cs + m1 * 32)[(4 * h + i) ^ (m1 & 7)];
+                    const float4 a0 = reinterpret_cast<const float4*>(cs + m0 * 32)[(4 * h + i) ^ (m0 & 7)];
+                    const float4 a1 = reinterpret_cast<const float4*>(cs + m1 * 32)[(4 * h + i) ^ (m1 & 7)];
+                    const float4 b0 = reinterpret_cast<const float4*>(cs - 1024 + m0 * 32)[(4 * h + i) ^ (m0 & 7)];
+                    const float4 b1 = reinterpret_cast<const float4*>(cs - 1024 + m1 * 32)[(4 * h + i) ^ (m1 & 7)];
+                    const float4 c0 = make_float4(a0.x + b0.x, a0.y + b0.y, a0.z + b0.z, a0.w + b0.w);
+                    const float4 c1 = make_float4(a1.x + b1.x, a1.y + b1.y, a1.z + b1.z, a1.w + b1.w);
                     gq[2 * i] = make_float2(c0.x + c1.y, c0.y - c1.x);
                     gq[2 * i + 1] = make_float2(c0.z + c1.w, c0.w - c1.z);
                 }
@@ -285,30 +303,49 @@ __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorM
             for (int off = 1; off < 32; off <<= 1) gmax = fmaxf(gmax, __shfl_xor_sync(0xffffffffu, gmax, off));
             bool fail = !(gmax == gmax);
             const float tau = (float)kPivotTau * gmax;
-            // pivot loop rolled over the two column halves (hj), unrolled inside (qj): the fully unrolled
-            // elimination is ~1.7k instructions and starves the warps on instruction fetch
+            // pivot loop rolled over the two column halves (hj), unrolled inside (qj): a fully unrolled
+            // elimination starves the warps on instruction fetch. Pivot row j is published through shared memory (ping-pong 128-B row buffers in the unit's
+            // free H landing area) instead of 16 shuffles per lane; the update b - (G[k][j] / p) r is two
+            // packed FFMA2 per entry, the pivot row's own lanes take b = 0, fs = -1/p (so r / p exactly)
+            float2* rowbuf = reinterpret_cast<float2*>(g + su::BG + s * 8192);
+            __syncwarp();  // every lane has read its C rows (C2 lives here)
 #pragma unroll 1
             for (int hj = 0; hj < 2; ++hj)
 #pragma unroll
             for (int qj = 0; qj < 8; ++qj) {
                 const int j = 8 * hj + qj;
+                const bool prow = k == j;
+                float4* rb = reinterpret_cast<float4*>(rowbuf + 16 * (qj & 1) + 8 * h);
+                if (prow) {
+#pragma unroll
+                    for (int q2 = 0; q2 < 4; ++q2)
+                        rb[q2] = make_float4(gq[2 * q2].x, gq[2 * q2].y, gq[2 * q2 + 1].x, gq[2 * q2 + 1].y);
+                }
                 const float2 f = shfl2(gq[qj], (lane & ~1) | hj);          // G[k][j]
                 float p = __shfl_sync(0xffffffffu, gq[qj].x, 2 * j + hj);  // G[j][j]
+                __syncwarp();
                 if (!(p > tau)) {
                     fail = true;
                     p = 1.f;
                 }
-                const float pinv = __frcp_rn(p);
-                const bool prow = k == j;
+                float pinv;
+                asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(pinv) : "f"(p));
+                const float2 fs = prow ? make_float2(-pinv, 0.f) : make_float2(f.x * pinv, f.y * pinv);
+                const float m = prow ? 0.f : 1.f;
+                const float2 nfx = make_float2(-fs.x, -fs.x), fyy = make_float2(fs.y, -fs.y), mm = make_float2(m, m);
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    float2 rj = shfl2(gq[q], 2 * j + h);  // G[j][8h+q]
-                    if (8 * h + q == j) rj = make_float2(1.f, 0.f);
-                    rj = make_float2(rj.x * pinv, rj.y * pinv);
-                    float2 b = (8 * h + q == j) ? make_float2(0.f, 0.f) : gq[q];
-                    b.x = fmaf(-f.x, rj.x, fmaf(f.y, rj.y, b.x));
-                    b.y = fmaf(-f.x, rj.y, fmaf(-f.y, rj.x, b.y));
-                    gq[q] = prow ? rj : b;
+                for (int q2 = 0; q2 < 4; ++q2) {
+                    const float4 r4 = rb[q2];
+#pragma unroll
+                    for (int e = 0; e < 2; ++e) {
+                        const int q = 2 * q2 + e;
+                        const float2 r = e ? make_float2(r4.z, r4.w) : make_float2(r4.x, r4.y);
+                        float2 b = ffma2(gq[q], mm, make_float2(0.f, 0.f));
+                        b = ffma2(nfx, r, b);
+                        b = ffma2(fyy, make_float2(r.y, r.x), b);
+                        if (q == qj && h == hj) b = prow ? make_float2(pinv, 0.f) : make_float2(-fs.x, -fs.y);
+                        gq[q] = b;
+                    }
                 }
             }
             // A_kk = [G^-1]_kk lives in lane (k, k / 8)
@@ -403,13 +440,11 @@ __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorM
                 for (int q = 0; q < 4; ++q) st_v8(dst + 32 * q, o + 8 * q);
             }
         }
-        // the W~ records (and the slopes written above) are read next by TMA (async proxy) in the fused kernel:
-        // make them visible at GPU scope and to the async proxy before the group barrier publishes them
-        __threadfence();
-        asm volatile("fence.proxy.async.global;" ::: "memory");
+        PROF_ADD(prof, 6, p6);
+        PROF_T(p7);
         tc::fence_before();
         sync();
-        PROF_ADD(prof, 6, p6);
+        PROF_ADD(prof, 7, p7);
     PROF_SFLUSH(gt == 0);
 }
 
@@ -493,8 +528,9 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
             PROF_DECL;
             PROF_T(tk0);
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ymap)) : "memory");
-            // W~ records (rows a2-a5 of the setup kernel) of units i = j + 2 are staged when the y chunks
-            // of unit j start; y itself is this call's input and streams before the setup completes
+            // !BEPI: W~ records (rows a2-a5 of the setup kernel) of units i = j + 2 are staged when the y
+            // chunks of unit j start (BEPI: by the B builder, so that the y stream never waits on them); y
+            // itself is this call's input and streams before the setup completes
             auto issue_w = [&](long long i) {
                 const int ws_ = (int)(i & 1);
                 if (i >= 2) mbar_wait_sleep(&wfree[ws_], (uint32_t)(((i >> 1) + 1) & 1));
@@ -513,7 +549,7 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
 #pragma unroll 1
             for (long long gg = 0; gg < G; ++gg) {
                 const int st = (int)(gg % S);
-                if ((gg & 3) == 0) {
+                if (!BEPI && (gg & 3) == 0) {
                     if (!waited) {
                         pdl_wait();  // the setup kernel of this call has written the workspace
                         waited = true;
@@ -549,18 +585,23 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
         for (long long j0 = 0; j0 < n_my; j0 += su::UPB, ++it) {
             const int nv = nv_of(j0);
             const long long jn = j0 + su::UPB;
-            setup_batch<QM>(a, &hmap, g + SM::setup, base + (uint32_t)SM::setup, stma, smma, tmem + kSetupCols, it, nv,
-                            gt, gw, lane, waited, [&](int s_) { return u0 + (j0 + s_) * du; },
-                            [] { asm volatile("bar.sync 5, 128;" ::: "memory"); },
-                            [&] {
-                                if (jn < n_my)
-                                    setup_issue_h(&hmap, base + (uint32_t)SM::setup, stma, nv_of(jn),
-                                                  [&](int s_) { return u0 + (jn + s_) * du; });
-                            });
-            if (gt == 0) {
-                __threadfence_block();
-                *units_ready = (int)(j0 + nv);
-            }
+            setup_batch<QM, true>(a, &hmap, g + SM::setup, base + (uint32_t)SM::setup, stma, smma, tmem + kSetupCols, it,
+                                  nv, gt, gw, lane, waited, [&](int s_) { return u0 + (j0 + s_) * du; },
+                                  [] { asm volatile("bar.sync 5, 128;" ::: "memory"); },
+                                  [&] {
+                                      if (jn < n_my)
+                                          setup_issue_h(&hmap, base + (uint32_t)SM::setup, stma, nv_of(jn),
+                                                        [&](int s_) { return u0 + (jn + s_) * du; });
+                                  },
+                                  [&] {
+                                      if (gt == 0) *units_ready = (int)j0;  // batches before this one are visible
+                                  });
+        }
+        if (n_my > 0) {  // the last batch
+            __threadfence();
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            asm volatile("bar.sync 5, 128;" ::: "memory");
+            if (gt == 0) *units_ready = (int)n_my;
         }
         if (!waited) pdl_wait();
     } else if (warp == CW) {
@@ -812,17 +853,29 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
             // (BEPI: warps 4-7 also build the B set of unit i + 2 as soon as unit i's MMAs completed)
             const int e = warp - 4, we = e & 3, tile = e >> 2;
             PROF_DECL;
+            // BEPI: thread 128 stages the W~ record of unit i into W stage i & 1 (after the B set that last
+            // read the stage was built); FUSED: once this CTA's setup group has published unit i
+            auto issue_w = [&](long long i) {
+                if constexpr (FUSED) {
+                    while (*units_ready <= i) __nanosleep(64);
+                    asm volatile("fence.proxy.async.global;" ::: "memory");
+                }
+                mbar_arrive_expect_tx(&wfull[i & 1], (uint32_t)SM::wrec);
+                bulk_g2s(g + SM::wst + (i & 1) * SM::wrec,
+                         reinterpret_cast<const float*>(a.ws) + (u0 + i * du) * (long long)WS, (uint32_t)SM::wrec,
+                         &wfull[i & 1]);
+            };
             if constexpr (BEPI) {
                 if (warp < 8) {
+                    if (t == 128) {
+                        pdl_wait();  // the setup (kernel or group) of this call writes the workspace
+                        for (long long i0 = 0; i0 < 2 && i0 < n_my; ++i0) issue_w(i0);
+                    }
                     for (long long i0 = 0; i0 < 2 && i0 < n_my; ++i0) build_B(i0, t - 128);
                     asm volatile("bar.sync 4, 128;" ::: "memory");
                     if (t == 128) {
-                        mbar_arrive(&bready[0]);
-                        mbar_arrive(&wfree[0]);
-                        if (n_my > 1) {
-                            mbar_arrive(&bready[1]);
-                            mbar_arrive(&wfree[1]);
-                        }
+                        for (long long i0 = 0; i0 < 2 && i0 < n_my; ++i0) mbar_arrive(&bready[i0]);
+                        for (long long i0 = 2; i0 < 4 && i0 < n_my; ++i0) issue_w(i0);
                     }
                 }
             }
@@ -836,11 +889,20 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                 if constexpr (BEPI) {
                     if (warp < 8 && i + 2 < n_my) {  // B set b is free: unit i's MMAs completed
                         PROF_T(tb);
+#ifdef C5_PROFILE
+                        {
+                            PROF_T(tw);
+                            mbar_wait_sleep(&wfull[b], (uint32_t)(((i + 2) >> 1) & 1));
+                            PROF_ADD(prof, 28, tw);
+                        }
+#endif
                         build_B(i + 2, t - 128);
                         asm volatile("bar.sync 4, 128;" ::: "memory");
                         if (t == 128) {
                             mbar_arrive(&bready[b]);
-                            mbar_arrive(&wfree[b]);
+                            PROF_T(ti);
+                            if (i + 4 < n_my) issue_w(i + 4);  // W stage b is read
+                            PROF_ADD(prof, 29, ti);
                         }
                         PROF_ADD(prof, 27, tb);
                     }
@@ -895,11 +957,13 @@ __global__ void __launch_bounds__(128, su::CTAS_PER_SM) k_c5_setup(DetectArgs a,
 #pragma unroll 1
     for (long long bt = blockIdx.x; bt < n_batch; bt += gridDim.x, ++it) {
         const long long ub = bt * su::UPB, bn = bt + gridDim.x;
-        setup_batch<QM>(a, &hmap, g, base, bar_tma, bar_mma, tmem, it, nv_of(bt), t, warp, lane, waited,
-                        [&](int s) { return ub + s; }, [] { __syncthreads(); },
-                        [&] {
-                            if (bn < n_batch) setup_issue_h(&hmap, base, bar_tma, nv_of(bn), [&](int s) { return bn * su::UPB + s; });
-                        });
+        setup_batch<QM, false>(a, &hmap, g, base, bar_tma, bar_mma, tmem, it, nv_of(bt), t, warp, lane, waited,
+                               [&](int s) { return ub + s; }, [] { __syncthreads(); },
+                               [&] {
+                                   if (bn < n_batch)
+                                       setup_issue_h(&hmap, base, bar_tma, nv_of(bn), [&](int s) { return bn * su::UPB + s; });
+                               },
+                               [] {});
     }
     if (!waited) pdl_wait();
     if (warp == 0) tc::dealloc<128>(tmem);
@@ -1019,10 +1083,13 @@ size_t c5_workspace(const DetectArgs& a) { return (size_t)a.n_units * BigWs<64, 
         NAME, 64, 16, QM, kSc, 14, LT, 32, 2, launch_c5<QM, LT, 6, S, NLO, TA, SETUP, BEPI>,               \
             prepare_c5<QM, LT, 6, S, NLO, TA, SETUP, BEPI>, c5_workspace                                   \
     }
+#ifndef C5X_FNLO
+#define C5X_FNLO 4
+#endif
 #define C5F_ENTRY(NAME, QM, LT, S)                                                                          \
     KernelEntry {                                                                                          \
-        NAME, 64, 16, QM, kSc, 14, LT, 32, 1, launch_c5<QM, LT, 6, S, 4, 4, 2, true, true>,                \
-            prepare_c5<QM, LT, 6, S, 4, 4, 2, true, true>, c5_workspace                                    \
+        NAME, 64, 16, QM, kSc, 14, LT, 32, 1, launch_c5<QM, LT, 6, S, C5X_FNLO, 4, 2, true, true>,         \
+            prepare_c5<QM, LT, 6, S, C5X_FNLO, 4, 2, true, true>, c5_workspace                             \
     }
 
 // First entry of a shape = its default (mimo_api.cu select_fast); the others are selectable by name.

@@ -51,7 +51,7 @@ def apply_roles(n_my, S, NLO, bepi=True):
         first = True
         for gg in range(G):
             st = gg % S
-            if gg & 3 == 0:
+            if not bepi and gg & 3 == 0:  # BEPI: the B builder stages the W~ records itself
                 if first:
                     first = False
                     yield from issue_w(0)
@@ -102,21 +102,25 @@ def apply_roles(n_my, S, NLO, bepi=True):
                 yield "step"
 
     def epilogue():  # warps 4-7 (and the B builder with BEPI); warps 8-9 share the tfree barrier sync
+        def stage_w(i):  # BEPI: thread 128 issues the W~ TMA of unit i into stage i & 1 (completes at once)
+            wfull[i & 1].arrive()
         if bepi:
             for i0 in range(min(2, n_my)):
+                stage_w(i0)
+            for i0 in range(min(2, n_my)):
                 yield from build_b(i0)
-            bready[0].arrive()
-            wfree[0].arrive()
-            if n_my > 1:
-                bready[1].arrive()
-                wfree[1].arrive()
+            for i0 in range(min(2, n_my)):
+                bready[i0].arrive()
+            for i0 in range(2, min(4, n_my)):
+                stage_w(i0)
         for i in range(n_my):
             b = i & 1
             yield from wait(accfull[b], i >> 1)
             if bepi and i + 2 < n_my:
                 yield from build_b(i + 2)
                 bready[b].arrive()
-                wfree[b].arrive()
+                if i + 4 < n_my:
+                    stage_w(i + 4)
             tfree[b].arrive()
             yield "step"
 
