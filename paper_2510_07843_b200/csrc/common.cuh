@@ -207,6 +207,55 @@ __device__ __forceinline__ uint32_t pack_f16x2_sat(float lo, float hi) {
 // v in [-127, 127] -> float whose low byte is rint(v) as int8 (1.5 * 2^23 magic)
 __device__ __forceinline__ uint32_t i8_magic(float v) { return __float_as_uint(v + 12582912.f); }
 
+// demap_layer for sigma2 > 0 with the I and Q axes as one packed pair (FADD2 / FFMA2 / FMUL2, the |.|
+// and immediate operand forms are free): the same per-axis arithmetic as demap_axis for M >= 3, in the
+// same order, two axes per instruction. Writes the QM LLRs as QM / 2 (I, Q) pairs: f16 -> one binary16x2
+// word per pair, f32 -> two words.
+__device__ __forceinline__ float2 fadd2_(float2 a, float2 b) {
+    unsigned long long ua, ub, d;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(ua) : "f"(a.x), "f"(a.y));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(ub) : "f"(b.x), "f"(b.y));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(ua), "l"(ub));
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(d));
+    return r;
+}
+__device__ __forceinline__ float2 fmul2_(float2 a, float2 b) {
+    unsigned long long ua, ub, d;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(ua) : "f"(a.x), "f"(a.y));
+    asm("mov.b64 %0, {%1, %2};" : "=l"(ub) : "f"(b.x), "f"(b.y));
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(ua), "l"(ub));
+    float2 r;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(r.x), "=f"(r.y) : "l"(d));
+    return r;
+}
+template <int QM, int LT>
+__device__ __forceinline__ void demap_layer_x2(float2 x, float slope, uint32_t* w) {
+    constexpr int M = QM / 2;
+    static_assert(M >= 3 && (LT == kLlrF16 || LT == kLlrF32), "packed demap: 64/256-QAM, float LLRs");
+    float2 t[M];
+    t[0] = x;
+#pragma unroll
+    for (int i = 1; i < M; ++i)
+        t[i] = fadd2_(make_float2(float(1 << (M - i)), float(1 << (M - i))),
+                      make_float2(-fabsf(t[i - 1].x), -fabsf(t[i - 1].y)));
+    const float2 e = fadd2_(make_float2(fabsf(t[M - 1].x), fabsf(t[M - 1].y)), make_float2(-1.f, -1.f));
+    const float2 D = fmul2_(e, e);
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        const float2 at = fadd2_(make_float2(fabsf(t[i].x), fabsf(t[i].y)), make_float2(1.f, 1.f));
+        const float2 mag = ffma2(at, at, make_float2(-D.x, -D.y));
+        const float2 v = fmul2_(make_float2(slope, slope), mag);
+        const float vi = copysignf(v.x, t[i].x), vq = copysignf(v.y, t[i].y);
+        if constexpr (LT == kLlrF16) {
+            w[i] = pack_f16x2_sat(vi, vq);
+        } else {
+            w[2 * i] = __float_as_uint(vi);
+            w[2 * i + 1] = __float_as_uint(vq);
+        }
+    }
+}
+
 template <int LT> struct LlrTraits;
 template <> struct LlrTraits<kLlrF32> { static constexpr int bytes = 4; };
 template <> struct LlrTraits<kLlrF16> { static constexpr int bytes = 2; };

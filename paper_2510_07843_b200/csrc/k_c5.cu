@@ -82,7 +82,8 @@ struct C5Smem {
     static constexpr size_t setup = (wst + 2 * wrec + 1023) / 1024 * 1024;  // FUSED: the setup group's 64 KiB
     static constexpr size_t bars = setup + (FUSED_ ? 65536 : 0);
     static constexpr int NBAR = 2 * S + 2 * NLO + 2 * 3 + 4 + 2;  // yfull, yfree | afull, afree | bready, accfull, tfree | wfull, wfree | setup tma, mma
-    static constexpr size_t ready = bars + NBAR * 8;           // FUSED: units whose W~ records are written
+    static constexpr size_t ready = bars + NBAR * 8;           // FUSED: [0] units whose W~ records are written,
+                                                               //        [1] units whose B sets are built
     static constexpr size_t tslot = ready + 8;
     static constexpr size_t total = tslot + 16 + 1024;        // + 1024-B alignment slack
     static_assert(B % 1024 == 0, "UMMA operand alignment");
@@ -140,6 +141,16 @@ __device__ __forceinline__ void demap_axis_i8(float u, float rs, uint32_t* q, in
 // (A persistent warp-specialised variant -- producer, MMA, readout and 12 worker warps
 // over a ring of unit slots -- measured 107-124 us against this kernel's 90, the
 // per-slot chain of H load, Gram round trip and inversion being sequential.)
+// Fused kernel: W~ records per CTA in the workspace ring (2 setup batches: the setup group runs at most
+// one batch ahead of the B builder, which consumes the records in order)
+#ifndef C5X_RING
+#define C5X_RING 16
+#endif
+#ifndef C5X_HINT
+#define C5X_HINT 0
+#endif
+constexpr int kC5Ring = C5X_RING;
+
 namespace su {
 constexpr int UPB = 4;                   // units per batch (= warps)
 constexpr size_t XB = 0;                 // [UPB] x 8 KiB  bf16 [64 r][hi c 0..31 | lo c 0..31], SW128
@@ -156,12 +167,17 @@ template <typename UnitF>
 __device__ __forceinline__ void setup_issue_h(const CUtensorMap* hmapp, uint32_t gaddr, uint64_t* bar_tma, int nv,
                                               UnitF unit_of) {
     mbar_arrive_expect_tx(bar_tma, (uint32_t)(nv * 64 * 16 * 8));
-    for (int s = 0; s < nv; ++s)
-        asm volatile(
-            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-            ::"r"(gaddr + (uint32_t)(su::BG + s * 8192)), "l"(reinterpret_cast<uint64_t>(hmapp)), "r"(0),
-            "r"((int)(unit_of(s) * 64)), "r"(smem_u32(bar_tma))
-            : "memory");
+    for (int s = 0; s < nv; ++s) {
+        if (C5X_HINT)  // H is read once
+            tc::tma_load_2d_hint(gaddr + (uint32_t)(su::BG + s * 8192), hmapp, 0, (int)(unit_of(s) * 64), bar_tma,
+                                 tc::policy_evict_first());
+        else
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+                ::"r"(gaddr + (uint32_t)(su::BG + s * 8192)), "l"(reinterpret_cast<uint64_t>(hmapp)), "r"(0),
+                "r"((int)(unit_of(s) * 64)), "r"(smem_u32(bar_tma))
+                : "memory");
+    }
 }
 
 // One batch of up to su::UPB = 4 H-units through rows a2-a5 (a1-a5 steps documented at k_c5_setup),
@@ -178,11 +194,19 @@ __device__ __forceinline__ void setup_issue_h(const CUtensorMap* hmapp, uint32_t
 // That fence is deferred to the NEXT batch, after its conversion (the stores have drained by then and
 // the fence costs nothing), and publish_prev() (after the group barrier) announces the previous batch;
 // the caller fences and publishes the last batch itself.
-template <int QM, bool PUB, typename UnitF, typename SyncF, typename NextF, typename PubF>
+// WIDE (the fused kernel, 256 TMEM columns): the Gram and W~ products as N = 64 MMAs (hi | lo halves side
+// by side, summed at readout): 4 + 4 instead of 8 + 8 MMAs per unit; otherwise 128 columns.
+//
+// rec_of(s) = the workspace record (W~ + slopes) of batch slot s: the unit itself, or (fused) a slot of
+// the CTA's ring of records, which ring_wait() (called by every thread before the batch's first record
+// write) makes sure the apply has finished reading.
+template <int QM, bool PUB, bool WIDE, typename UnitF, typename SyncF, typename NextF, typename PubF, typename RecF,
+          typename RingF>
 __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorMap* hmapp, unsigned char* g,
                                             uint32_t gaddr, uint64_t* bar_tma, uint64_t* bar_mma, uint32_t tmem,
                                             uint32_t it, int nv, int gt, int gw, int lane, bool& waited,
-                                            UnitF unit_of, SyncF sync, NextF issue_next, PubF publish_prev) {
+                                            UnitF unit_of, SyncF sync, NextF issue_next, PubF publish_prev,
+                                            RecF rec_of, RingF ring_wait) {
     constexpr int NR = 64, NL = 16;
     constexpr int WS = BigWs<NR, NL>::stride;
     const float norm = (float)qam_norm(QM);
@@ -225,15 +249,19 @@ __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorM
         // (two MMAs per K step instead of four N = 32, M = 32-useful ones)
         if (gt == 0) {
             tc::fence_after();
-            constexpr uint32_t idg = tc::idesc(tc::kFmtBF16, 64, 32, 1, 1);
+            constexpr uint32_t idg = tc::idesc(tc::kFmtBF16, 64, WIDE ? 64 : 32, 1, 1);
             for (int s = 0; s < su::UPB; ++s) {
                 const uint32_t xs = gaddr + (uint32_t)(su::XB + s * 8192);
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks) {  // K = antennas 16 ks .. 16 ks + 15 = two 8-row atoms
                     const uint64_t dh = tc::desc_sw128(xs + 2048u * ks, 16, 1024);
-                    const uint64_t dl = tc::desc_sw128(xs + 64u + 2048u * ks, 16, 1024);
-                    tc::mma_f16_ss(tmem + 32u * s, dh, dh, idg, ks ? 1u : 0u);
-                    tc::mma_f16_ss(tmem + 32u * s, dh, dl, idg, 1u);
+                    if constexpr (WIDE) {  // B = [hi | lo] (N = 64): D = [hi | lo]^T [hi | lo]
+                        tc::mma_f16_ss(tmem + 64u * s, dh, dh, idg, ks ? 1u : 0u);
+                    } else {
+                        const uint64_t dl = tc::desc_sw128(xs + 64u + 2048u * ks, 16, 1024);
+                        tc::mma_f16_ss(tmem + 32u * s, dh, dh, idg, ks ? 1u : 0u);
+                        tc::mma_f16_ss(tmem + 32u * s, dh, dl, idg, 1u);
+                    }
                 }
             }
             tc::commit(bar_mma);
@@ -248,8 +276,17 @@ __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorM
 #pragma unroll 1
         for (int s = 0; s < su::UPB; ++s) {
             uint32_t v[32];
-            tc::ld32(tmem + ((uint32_t)(32 * gw) << 16) + 32u * s, v);
-            tc::wait_ld();
+            if constexpr (WIDE) {  // columns n (B = hi) + n + 32 (B = lo)
+                uint32_t v2[32];
+                tc::ld32(tmem + ((uint32_t)(32 * gw) << 16) + 64u * s, v);
+                tc::ld32(tmem + ((uint32_t)(32 * gw) << 16) + 64u * s + 32u, v2);
+                tc::wait_ld();
+#pragma unroll
+                for (int c = 0; c < 32; ++c) v[c] = __float_as_uint(__uint_as_float(v[c]) + __uint_as_float(v2[c]));
+            } else {
+                tc::ld32(tmem + ((uint32_t)(32 * gw) << 16) + 32u * s, v);
+                tc::wait_ld();
+            }
             if (lane < 16) {
                 const int m = 16 * (gw & 1) + lane;
                 float* cs = reinterpret_cast<float*>(g + su::BG + s * 8192 + (gw < 2 ? 4096 : 0));
@@ -269,6 +306,7 @@ __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorM
             pdl_wait();
             waited = true;
         }
+        ring_wait();
         {
             const int s = gw, k = lane >> 1, h = lane & 1;
             const bool valid = s < nv;
@@ -391,7 +429,7 @@ __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorM
                 }
             }
             if (valid && h == 0) {
-                float* wsu = reinterpret_cast<float*>(a.ws) + u * WS;
+                float* wsu = reinterpret_cast<float*>(a.ws) + rec_of(s) * WS;
                 wsu[NR * NL * 2 + k] = sinr / norm * a.llr_scale;
                 if (a.sinr) a.sinr[u * NL + k] = sinr;
                 if (k == 0 && fail) atomicAdd(a.fail_count, 1ull);
@@ -405,14 +443,18 @@ __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorM
         // ---- a4: W~^T = XB B'^T (K-major view of XB: K = 64 = hi | lo halves)
         if (gt == 0) {
             tc::fence_after();
-            constexpr uint32_t idw = tc::idesc(tc::kFmtBF16, 64, 32);
+            constexpr uint32_t idw = tc::idesc(tc::kFmtBF16, 64, WIDE ? 64 : 32);
             for (int s = 0; s < su::UPB; ++s) {
                 const uint32_t xs = gaddr + (uint32_t)(su::XB + s * 8192), bs = gaddr + (uint32_t)(su::BG + s * 8192);
 #pragma unroll
                 for (int ks = 0; ks < 4; ++ks) {
                     const uint64_t dA = tc::desc_sw128(xs + 32u * ks);
-                    tc::mma_f16_ss(tmem + 32u * s, dA, tc::desc_sw128(bs + 32u * ks), idw, ks ? 1u : 0u);
-                    tc::mma_f16_ss(tmem + 32u * s, dA, tc::desc_sw128(bs + 4096u + 32u * ks), idw, 1u);
+                    if constexpr (WIDE) {  // B = [B'_hi rows; B'_lo rows] (N = 64, contiguous): D = [W_hi | W_lo]
+                        tc::mma_f16_ss(tmem + 64u * s, dA, tc::desc_sw128(bs + 32u * ks), idw, ks ? 1u : 0u);
+                    } else {
+                        tc::mma_f16_ss(tmem + 32u * s, dA, tc::desc_sw128(bs + 32u * ks), idw, ks ? 1u : 0u);
+                        tc::mma_f16_ss(tmem + 32u * s, dA, tc::desc_sw128(bs + 4096u + 32u * ks), idw, 1u);
+                    }
                 }
             }
             tc::commit(bar_mma);
@@ -425,8 +467,17 @@ __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorM
 #pragma unroll 1
         for (int s = 0; s < nv; ++s) {  // row r = 16 warp + lane of W~^T: cols k = Re W~_kr, 16 + k = Im W~_kr
             uint32_t v[32];
-            tc::ld32(tmem + ((uint32_t)(32 * gw) << 16) + 32u * s, v);
-            tc::wait_ld();
+            if constexpr (WIDE) {
+                uint32_t v2[32];
+                tc::ld32(tmem + ((uint32_t)(32 * gw) << 16) + 64u * s, v);
+                tc::ld32(tmem + ((uint32_t)(32 * gw) << 16) + 64u * s + 32u, v2);
+                tc::wait_ld();
+#pragma unroll
+                for (int c = 0; c < 32; ++c) v[c] = __float_as_uint(__uint_as_float(v[c]) + __uint_as_float(v2[c]));
+            } else {
+                tc::ld32(tmem + ((uint32_t)(32 * gw) << 16) + 32u * s, v);
+                tc::wait_ld();
+            }
             if (lane < 16) {
                 const int r = 16 * gw + lane;
                 uint32_t o[32];
@@ -435,9 +486,15 @@ __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorM
                     o[2 * kq] = v[kq];
                     o[2 * kq + 1] = v[16 + kq];
                 }
-                char* dst = reinterpret_cast<char*>(reinterpret_cast<float*>(a.ws) + unit_of(s) * WS) + (size_t)r * NL * 8;
+                char* dst = reinterpret_cast<char*>(reinterpret_cast<float*>(a.ws) + rec_of(s) * WS) + (size_t)r * NL * 8;
+                if constexpr (PUB && C5X_HINT) {  // the fused kernel's ring records stay in L2
+                    const uint64_t pol = tc::policy_evict_last();
 #pragma unroll
-                for (int q = 0; q < 4; ++q) st_v8(dst + 32 * q, o + 8 * q);
+                    for (int q = 0; q < 4; ++q) tc::st_v8_hint(dst + 32 * q, o + 8 * q, pol);
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) st_v8(dst + 32 * q, o + 8 * q);
+                }
             }
         }
         PROF_ADD(prof, 6, p6);
@@ -464,15 +521,22 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
     constexpr uint32_t kAccCols = KC ? 64u : 128u;   // TMEM columns per accumulator (2 row tiles)
     constexpr uint32_t kAring = 2u * kAccCols;       // TMEM columns 0 .. kAring-1: 2 accumulators
     constexpr uint32_t kAcols = TA == 1 ? 128u : 64u;  // TMEM columns per A ring slot (one chunk, 2 tiles)
+    constexpr bool kWide = kAring + NLO * kAcols + 256u <= 512u;  // FUSED: room for the wide setup products
     static_assert(kAring + NLO * kAcols + (FUSED ? 128u : 0u) <= 512u, "TMEM");
     static_assert(!FUSED || BEPI, "fused setup: the epilogue warps build the B sets");
-    constexpr uint32_t kSetupCols = kAring + NLO * kAcols;  // FUSED: the setup group's 128 TMEM columns
+    constexpr uint32_t kSetupCols = kAring + NLO * kAcols;  // FUSED: the setup group's 128 / 256 TMEM columns
     constexpr int CW = 4 + EW;                       // MMA warp; CW + 1: TMA producer
     constexpr int WS = BigWs<NR, NL>::stride;
     extern __shared__ unsigned char smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     unsigned char* g = smem_raw + (base - raw);
+    // workspace record of local unit i: FUSED = slot i % kC5Ring of this CTA's ring (L2-resident, reused),
+    // otherwise the unit's own record (written by the setup kernel)
+    auto rec_of = [&](long long i) -> long long {
+        if constexpr (FUSED) return (long long)blockIdx.x * kC5Ring + i % kC5Ring;
+        else return (long long)blockIdx.x + i * (long long)gridDim.x;
+    };
     uint64_t* bar = reinterpret_cast<uint64_t*>(g + SM::bars);
     uint64_t* yfull = bar;             // [S]    TMA tx
     uint64_t* yfree = bar + S;         // [S]    converters done with the stage
@@ -486,6 +550,7 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
     uint64_t* stma = wfree + 2;        //        FUSED: setup group's H TMA
     uint64_t* smma = stma + 1;         //        FUSED: setup group's MMAs
     volatile int* units_ready = reinterpret_cast<volatile int*>(g + SM::ready);  // FUSED
+    volatile int* units_built = units_ready + 1;                                 // FUSED
     uint32_t* tslot = reinterpret_cast<uint32_t*>(g + SM::tslot);
     float* sslope = reinterpret_cast<float*>(g + SM::slope);
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -514,6 +579,7 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
         mbar_init(stma, 1);
         mbar_init(smma, 1);
         *units_ready = 0;
+        *units_built = 0;
         fence_mbar_init();
     }
     if (warp == CW) tc::alloc<512>(tslot);
@@ -528,6 +594,7 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
             PROF_DECL;
             PROF_T(tk0);
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ymap)) : "memory");
+            const uint64_t ypol = C5X_HINT ? tc::policy_evict_first() : 0;  // y is streamed once
             // !BEPI: W~ records (rows a2-a5 of the setup kernel) of units i = j + 2 are staged when the y
             // chunks of unit j start (BEPI: by the B builder, so that the y stream never waits on them); y
             // itself is this call's input and streams before the setup completes
@@ -541,9 +608,8 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                     asm volatile("fence.proxy.async.global;" ::: "memory");
                 }
                 mbar_arrive_expect_tx(&wfull[ws_], (uint32_t)SM::wrec);
-                bulk_g2s(g + SM::wst + ws_ * SM::wrec,
-                         reinterpret_cast<const float*>(a.ws) + (u0 + i * du) * (long long)WS, (uint32_t)SM::wrec,
-                         &wfull[ws_]);
+                bulk_g2s(g + SM::wst + ws_ * SM::wrec, reinterpret_cast<const float*>(a.ws) + rec_of(i) * WS,
+                         (uint32_t)SM::wrec, &wfull[ws_]);
             };
             bool waited = false;
 #pragma unroll 1
@@ -564,8 +630,12 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                 const long long uu = u0 + (gg >> 2) * du;
                 const int slot = (int)(uu / a.n_fb), fb = (int)(uu % a.n_fb);
                 mbar_arrive_expect_tx(&yfull[st], (uint32_t)SM::chunk);
-                tma_load_3d(base + (uint32_t)(SM::y0 + st * SM::chunk), &ymap, 32 * (int)(gg & 3), fb * kSc,
-                            slot * kSym, &yfull[st]);
+                if (C5X_HINT)
+                    tc::tma_load_3d_hint(base + (uint32_t)(SM::y0 + st * SM::chunk), &ymap, 32 * (int)(gg & 3),
+                                         fb * kSc, slot * kSym, &yfull[st], ypol);
+                else
+                    tma_load_3d(base + (uint32_t)(SM::y0 + st * SM::chunk), &ymap, 32 * (int)(gg & 3), fb * kSc,
+                                slot * kSym, &yfull[st]);
             }
             PROF_ADD(prof, 31, tk0);
             PROF_FLUSH(true);
@@ -585,7 +655,7 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
         for (long long j0 = 0; j0 < n_my; j0 += su::UPB, ++it) {
             const int nv = nv_of(j0);
             const long long jn = j0 + su::UPB;
-            setup_batch<QM, true>(a, &hmap, g + SM::setup, base + (uint32_t)SM::setup, stma, smma, tmem + kSetupCols, it,
+            setup_batch<QM, true, kWide>(a, &hmap, g + SM::setup, base + (uint32_t)SM::setup, stma, smma, tmem + kSetupCols, it,
                                   nv, gt, gw, lane, waited, [&](int s_) { return u0 + (j0 + s_) * du; },
                                   [] { asm volatile("bar.sync 5, 128;" ::: "memory"); },
                                   [&] {
@@ -595,6 +665,10 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                                   },
                                   [&] {
                                       if (gt == 0) *units_ready = (int)j0;  // batches before this one are visible
+                                  },
+                                  [&](int s_) { return rec_of(j0 + s_); },
+                                  [&] {  // ring slots of units j0 .. j0 + nv - 1 held units j0 - kC5Ring ..: built?
+                                      while (*units_built < (int)(j0 + nv - kC5Ring)) __nanosleep(32);
                                   });
         }
         if (n_my > 0) {  // the last batch
@@ -755,7 +829,13 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
         // B = [B_hi; B_lo] of unit i (bf16 or tf32 split of the real form of W~) into B set i & 1, and the
         // unit's slopes into slope ring slot i & 3; tid in 0..127 of the building warp group
         auto build_B = [&](long long i, int tid) {
+            // thread = (B row n = lane, K quarter kt = warp): the 32 lanes of a warp read 16 distinct W~ entries
+            // of one antenna row (no bank conflicts; n and n + 16 share theirs) and store one 16-byte piece each
+#ifdef C5X_OLDMAP
             const int n = tid >> 2, kt = tid & 3, kk = n & 15, b = (int)(i & 1);
+#else
+            const int n = tid & 31, kt = tid >> 5, kk = n & 15, b = (int)(i & 1);
+#endif
             const bool im_row = n >= 16;
             mbar_wait_sleep(&wfull[i & 1], (uint32_t)((i >> 1) & 1));
             const float2* src = reinterpret_cast<const float2*>(g + SM::wst + (i & 1) * SM::wrec);
@@ -861,9 +941,12 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                     asm volatile("fence.proxy.async.global;" ::: "memory");
                 }
                 mbar_arrive_expect_tx(&wfull[i & 1], (uint32_t)SM::wrec);
-                bulk_g2s(g + SM::wst + (i & 1) * SM::wrec,
-                         reinterpret_cast<const float*>(a.ws) + (u0 + i * du) * (long long)WS, (uint32_t)SM::wrec,
-                         &wfull[i & 1]);
+                const float* src = reinterpret_cast<const float*>(a.ws) + rec_of(i) * WS;
+                if constexpr (FUSED && C5X_HINT)
+                    tc::bulk_g2s_hint(g + SM::wst + (i & 1) * SM::wrec, src, (uint32_t)SM::wrec, &wfull[i & 1],
+                                      tc::policy_evict_last());
+                else
+                    bulk_g2s(g + SM::wst + (i & 1) * SM::wrec, src, (uint32_t)SM::wrec, &wfull[i & 1]);
             };
             if constexpr (BEPI) {
                 if (warp < 8) {
@@ -875,6 +958,7 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                     asm volatile("bar.sync 4, 128;" ::: "memory");
                     if (t == 128) {
                         for (long long i0 = 0; i0 < 2 && i0 < n_my; ++i0) mbar_arrive(&bready[i0]);
+                        if constexpr (FUSED) *units_built = (int)min(2ll, n_my);
                         for (long long i0 = 2; i0 < 4 && i0 < n_my; ++i0) issue_w(i0);
                     }
                 }
@@ -900,6 +984,7 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                         asm volatile("bar.sync 4, 128;" ::: "memory");
                         if (t == 128) {
                             mbar_arrive(&bready[b]);
+                            if constexpr (FUSED) *units_built = (int)(i + 3);
                             PROF_T(ti);
                             if (i + 4 < n_my) issue_w(i + 4);  // W stage b is read
                             PROF_ADD(prof, 29, ti);
@@ -923,6 +1008,14 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
     tc::fence_before();
     __syncthreads();
     if (warp == CW) tc::dealloc<512>(tmem);
+#ifdef C5X_NODISCARD
+    if constexpr (false) {
+#else
+    if constexpr (FUSED) {  // the ring records are dead: drop their L2 lines instead of writing them back
+#endif
+        const char* r0 = reinterpret_cast<const char*>(reinterpret_cast<const float*>(a.ws) + rec_of(0) * WS);
+        for (int l = t; l < kC5Ring * WS * 4 / 128; l += blockDim.x) tc::discard_l2(r0 + 128 * l);
+    }
 }
 
 template <int QM>
@@ -957,13 +1050,13 @@ __global__ void __launch_bounds__(128, su::CTAS_PER_SM) k_c5_setup(DetectArgs a,
 #pragma unroll 1
     for (long long bt = blockIdx.x; bt < n_batch; bt += gridDim.x, ++it) {
         const long long ub = bt * su::UPB, bn = bt + gridDim.x;
-        setup_batch<QM, false>(a, &hmap, g, base, bar_tma, bar_mma, tmem, it, nv_of(bt), t, warp, lane, waited,
+        setup_batch<QM, false, false>(a, &hmap, g, base, bar_tma, bar_mma, tmem, it, nv_of(bt), t, warp, lane, waited,
                                [&](int s) { return ub + s; }, [] { __syncthreads(); },
                                [&] {
                                    if (bn < n_batch)
                                        setup_issue_h(&hmap, base, bar_tma, nv_of(bn), [&](int s) { return bn * su::UPB + s; });
                                },
-                               [] {});
+                               [] {}, [&](int s) { return (long long)(ub + s); }, [] {});
     }
     if (!waited) pdl_wait();
     if (warp == 0) tc::dealloc<128>(tmem);
@@ -1077,6 +1170,17 @@ cudaError_t prepare_c5() {
 }
 
 size_t c5_workspace(const DetectArgs& a) { return (size_t)a.n_units * BigWs<64, 16>::stride * 4; }
+// fused kernel: a ring of kC5Ring records per CTA
+size_t c5f_workspace(const DetectArgs& a) {
+    static int n_sm = 0;
+    if (!n_sm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const long long ctas = a.n_units < n_sm ? a.n_units : n_sm;
+    return (size_t)ctas * kC5Ring * BigWs<64, 16>::stride * 4;
+}
 
 #define C5_ENTRY(NAME, QM, LT, S, NLO, TA, SETUP, BEPI)                                                   \
     KernelEntry {                                                                                          \
@@ -1084,12 +1188,12 @@ size_t c5_workspace(const DetectArgs& a) { return (size_t)a.n_units * BigWs<64, 
             prepare_c5<QM, LT, 6, S, NLO, TA, SETUP, BEPI>, c5_workspace                                   \
     }
 #ifndef C5X_FNLO
-#define C5X_FNLO 4
+#define C5X_FNLO 2
 #endif
 #define C5F_ENTRY(NAME, QM, LT, S)                                                                          \
     KernelEntry {                                                                                          \
         NAME, 64, 16, QM, kSc, 14, LT, 32, 1, launch_c5<QM, LT, 6, S, C5X_FNLO, 4, 2, true, true>,         \
-            prepare_c5<QM, LT, 6, S, C5X_FNLO, 4, 2, true, true>, c5_workspace                             \
+            prepare_c5<QM, LT, 6, S, C5X_FNLO, 4, 2, true, true>, c5f_workspace                            \
     }
 
 // First entry of a shape = its default (mimo_api.cu select_fast); the others are selectable by name.

@@ -256,10 +256,13 @@ struct Lg3Smem {
     static constexpr int HS = NR * NL + 4;                                  // float2 per unit H (padded)
     static constexpr int LS = NL * NL + 4;                                  // float2 per unit L / X
     static constexpr size_t y = 0;                                          // [14][TU][NR] float2, SW128
-    static constexpr size_t H = (size_t)kSym * TU * NR * 8;                 // [TU][HS], or HT: [NR*NL/16][TU][128 B] SW128
+    // HT 4: y lands after the setup, over the H / L / X area (which is dead by then)
+    static constexpr size_t ybytes = (size_t)kSym * TU * NR * 8;
+    static constexpr size_t H = HT == 4 ? 0 : ybytes;                       // [TU][HS], or HT: [NR*NL/16][TU][128 B] SW128
     static constexpr size_t LX = H + (HT ? (size_t)TU * NR * NL * 8 : (size_t)TU * HS * 8);  // [TU][LS]
     static constexpr size_t dinv = LX + (size_t)TU * LS * 8;                // [TU][NL]
-    static constexpr size_t bars = (dinv + (size_t)TU * NL * 4 + 7) / 8 * 8;  // y, H
+    static constexpr size_t setup_end = dinv + (size_t)TU * NL * 4;
+    static constexpr size_t bars = ((setup_end > ybytes ? setup_end : ybytes) + 7) / 8 * 8;  // y, H
     static constexpr size_t total = bars + 16 + 1024;                       // + 1024-alignment slack
 };
 
@@ -303,8 +306,14 @@ __global__ void __launch_bounds__(32 * NW) k_lg3(DetectArgs a, const __grid_cons
         mbar_init(&bars[0], 1);
         mbar_init(&bars[1], 1);
         fence_mbar_init();
-        mbar_arrive_expect_tx(&bars[0], (uint32_t)(kSym * TU * NR * 8));
-        tma_load_3d(base + (uint32_t)SM::y, &ymap, 0, sc0, slot * kSym, &bars[0]);
+        if constexpr (HT == 4) {  // y is copied after the setup; warm L2 with it now
+            asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];" ::"l"(
+                             reinterpret_cast<uint64_t>(&ymap)),
+                         "r"(0), "r"(sc0), "r"(slot * kSym) : "memory");
+        } else {
+            mbar_arrive_expect_tx(&bars[0], (uint32_t)(kSym * TU * NR * 8));
+            tma_load_3d(base + (uint32_t)SM::y, &ymap, 0, sc0, slot * kSym, &bars[0]);
+        }
         if constexpr (HT) {
             mbar_arrive_expect_tx(&bars[1], (uint32_t)(TU * NR * NL * 8));
             tma_load_3d(base + (uint32_t)SM::H, &hmap, 0, slot * a.n_sc + sc0, 0, &bars[1]);
@@ -343,17 +352,50 @@ __global__ void __launch_bounds__(32 * NW) k_lg3(DetectArgs a, const __grid_cons
             return hU[r * NL + j];
         }
     };
+    // HT 3: the NL entries H[r][0 .. NL-1] of one antenna as NL / 2 16-byte loads (one swizzled half row)
+    auto hrow = [&](int r, float2* hr) {
+        constexpr int RPR = 128 / (NL * 8);
+        const int row = (r / RPR) * TU + ul;
+#pragma unroll
+        for (int q = 0; q < NL / 2; ++q) {
+            const int c = (r % RPR) * (NL / 2) + q;
+            const float4 v = *reinterpret_cast<const float4*>(hT + row * 128 + ((c ^ (row & 7)) << 4));
+            hr[2 * q] = make_float2(v.x, v.y);
+            hr[2 * q + 1] = make_float2(v.z, v.w);
+        }
+    };
     float2 g[NL];
+    if constexpr (HT >= 3) {
+        // G_kj = sum_r conj(H_rk) H_rj as two packed accumulators with free operand forms (broadcast,
+        // swapped pair): a += H_rk.x (H_rj.x, H_rj.y), b += H_rk.y (H_rj.y, H_rj.x), G = (a.x + b.x, a.y - b.y)
+        float2 ga[NL], gb[NL];
 #pragma unroll
-    for (int j = 0; j < NL; ++j) g[j] = make_float2(0.f, 0.f);
+        for (int j = 0; j < NL; ++j) ga[j] = gb[j] = make_float2(0.f, 0.f);
 #pragma unroll 4
-    for (int r = 0; r < NR; ++r) {
-        const float2 hk = hat(r, k);
+        for (int r = 0; r < NR; ++r) {
+            const float2 hk = hat(r, k);
+            float2 hr[NL];
+            hrow(r, hr);
 #pragma unroll
-        for (int j = 0; j < NL; ++j) {
-            const float2 hj = hat(r, j);
-            g[j].x = fmaf(hk.x, hj.x, fmaf(hk.y, hj.y, g[j].x));
-            g[j].y = fmaf(hk.x, hj.y, fmaf(-hk.y, hj.x, g[j].y));
+            for (int j = 0; j < NL; ++j) {
+                ga[j] = ffma2(make_float2(hk.x, hk.x), hr[j], ga[j]);
+                gb[j] = ffma2(make_float2(hk.y, hk.y), make_float2(hr[j].y, hr[j].x), gb[j]);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < NL; ++j) g[j] = make_float2(ga[j].x + gb[j].x, ga[j].y - gb[j].y);
+    } else {
+#pragma unroll
+        for (int j = 0; j < NL; ++j) g[j] = make_float2(0.f, 0.f);
+#pragma unroll 4
+        for (int r = 0; r < NR; ++r) {
+            const float2 hk = hat(r, k);
+#pragma unroll
+            for (int j = 0; j < NL; ++j) {
+                const float2 hj = hat(r, j);
+                g[j].x = fmaf(hk.x, hj.x, fmaf(hk.y, hj.y, g[j].x));
+                g[j].y = fmaf(hk.x, hj.y, fmaf(-hk.y, hj.x, g[j].y));
+            }
         }
     }
 #pragma unroll
@@ -378,12 +420,24 @@ __global__ void __launch_bounds__(32 * NW) k_lg3(DetectArgs a, const __grid_cons
         const float dinv = rsqrtf(p);
         if (k == j) my_dinv = dinv;
         if (k > j) g[j] = make_float2(g[j].x * dinv, g[j].y * dinv);
+        if constexpr (HT >= 3) {  // G_km -= L_kj conj(L_mj) = L_mj.x (-L_kj) + L_mj.y (-L_kj.y, L_kj.x)
+            const float2 na = make_float2(-g[j].x, -g[j].y), ra = make_float2(-g[j].y, g[j].x);
 #pragma unroll
-        for (int m = j + 1; m < NL; ++m) {
-            const float2 lmj = shfl2(g[j], gbase + m);
-            if (k >= m) {
-                g[m].x = fmaf(-g[j].x, lmj.x, fmaf(-g[j].y, lmj.y, g[m].x));
-                g[m].y = fmaf(-g[j].y, lmj.x, fmaf(g[j].x, lmj.y, g[m].y));
+            for (int m = j + 1; m < NL; ++m) {
+                const float2 lmj = shfl2(g[j], gbase + m);
+                if (k >= m) {
+                    g[m] = ffma2(make_float2(lmj.x, lmj.x), na, g[m]);
+                    g[m] = ffma2(make_float2(lmj.y, lmj.y), ra, g[m]);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int m = j + 1; m < NL; ++m) {
+                const float2 lmj = shfl2(g[j], gbase + m);
+                if (k >= m) {
+                    g[m].x = fmaf(-g[j].x, lmj.x, fmaf(-g[j].y, lmj.y, g[m].x));
+                    g[m].y = fmaf(-g[j].y, lmj.x, fmaf(g[j].x, lmj.y, g[m].y));
+                }
             }
         }
     }
@@ -410,16 +464,33 @@ __global__ void __launch_bounds__(32 * NW) k_lg3(DetectArgs a, const __grid_cons
     for (int i = 0; i < NL; ++i) lU[i * NL + k] = x[i];
     __syncwarp();
     float2 gi[NL];
+    if constexpr (HT >= 3) {  // Gi_kj += conj(X_mk) X_mj = X_mj.x (x.x, -x.y) + X_mj.y (x.y, x.x), x = X_mk
+        float2 cx[NL];
 #pragma unroll
-    for (int j = 0; j < NL; ++j) {
-        float2 sv = make_float2(0.f, 0.f);
+        for (int m = 0; m < NL; ++m) cx[m] = make_float2(x[m].x, -x[m].y);
 #pragma unroll
-        for (int m = j; m < NL; ++m) {
-            const float2 xm = x[m], xmj = lU[m * NL + j];
-            sv.x = fmaf(xm.x, xmj.x, fmaf(xm.y, xmj.y, sv.x));
-            sv.y = fmaf(xm.x, xmj.y, fmaf(-xm.y, xmj.x, sv.y));
+        for (int j = 0; j < NL; ++j) {
+            float2 sv = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int m = j; m < NL; ++m) {
+                const float2 xmj = lU[m * NL + j];
+                sv = ffma2(make_float2(xmj.x, xmj.x), cx[m], sv);
+                sv = ffma2(make_float2(xmj.y, xmj.y), make_float2(x[m].y, x[m].x), sv);
+            }
+            gi[j] = sv;
         }
-        gi[j] = sv;
+    } else {
+#pragma unroll
+        for (int j = 0; j < NL; ++j) {
+            float2 sv = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int m = j; m < NL; ++m) {
+                const float2 xm = x[m], xmj = lU[m * NL + j];
+                sv.x = fmaf(xm.x, xmj.x, fmaf(xm.y, xmj.y, sv.x));
+                sv.y = fmaf(xm.x, xmj.y, fmaf(-xm.y, xmj.x, sv.y));
+            }
+            gi[j] = sv;
+        }
     }
     float sinr, fac;
     const float mu = fmaf(-s2, A, 1.f);
@@ -436,22 +507,48 @@ __global__ void __launch_bounds__(32 * NW) k_lg3(DetectArgs a, const __grid_cons
     }
     const float slope = sinr / norm * a.llr_scale;
     float2 w[NR];
+    if constexpr (HT >= 3) {  // W_kr = sum_j h.x (Gi.x, Gi.y) + h.y (Gi.y, -Gi.x), h = H_rj (broadcast halves)
+        float2 gs[NL];
 #pragma unroll
-    for (int r = 0; r < NR; ++r) {
-        float2 sv = make_float2(0.f, 0.f);
+        for (int j = 0; j < NL; ++j) gs[j] = make_float2(gi[j].y, -gi[j].x);
 #pragma unroll
-        for (int j = 0; j < NL; ++j) {
-            const float2 h = hat(r, j);
-            sv.x = fmaf(gi[j].x, h.x, fmaf(gi[j].y, h.y, sv.x));
-            sv.y = fmaf(gi[j].y, h.x, fmaf(-gi[j].x, h.y, sv.y));
+        for (int r = 0; r < NR; ++r) {
+            float2 hr[NL];
+            hrow(r, hr);
+            float2 sv = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int j = 0; j < NL; ++j) {
+                sv = ffma2(make_float2(hr[j].x, hr[j].x), gi[j], sv);
+                sv = ffma2(make_float2(hr[j].y, hr[j].y), gs[j], sv);
+            }
+            w[r] = (fac > 0.f) ? make_float2(sv.x * fac, sv.y * fac) : make_float2(0.f, 0.f);
         }
-        w[r] = (fac > 0.f) ? make_float2(sv.x * fac, sv.y * fac) : make_float2(0.f, 0.f);
+    } else {
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            float2 sv = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int j = 0; j < NL; ++j) {
+                const float2 h = hat(r, j);
+                sv.x = fmaf(gi[j].x, h.x, fmaf(gi[j].y, h.y, sv.x));
+                sv.y = fmaf(gi[j].y, h.x, fmaf(-gi[j].x, h.y, sv.y));
+            }
+            w[r] = (fac > 0.f) ? make_float2(sv.x * fac, sv.y * fac) : make_float2(0.f, 0.f);
+        }
     }
 
-    float2 wq[HT == 2 ? NR : 1];  // HT 2: (-w.y, w.x) for the packed apply
-    if constexpr (HT == 2) {
+    float2 wq[HT >= 2 ? NR : 1];  // HT 2-4: (-w.y, w.x) for the packed apply
+    if constexpr (HT >= 2) {
 #pragma unroll
         for (int r = 0; r < NR; ++r) wq[r] = make_float2(-w[r].y, w[r].x);
+    }
+    if constexpr (HT == 4) {  // H, L, X are dead in every warp: y over them (the L2-warm tile)
+        __syncthreads();
+        if (t == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive_expect_tx(&bars[0], (uint32_t)(kSym * TU * NR * 8));
+            tma_load_3d(base + (uint32_t)SM::y, &ymap, 0, sc0, slot * kSym, &bars[0]);
+        }
     }
     pdl_wait();  // global writes only after the previous grid completed
     if (active) {
@@ -472,7 +569,7 @@ __global__ void __launch_bounds__(32 * NW) k_lg3(DetectArgs a, const __grid_cons
         const unsigned char* yr = ybase + row * 128;
         const int sw = row & 7;
         float2 acc = make_float2(0.f, 0.f);
-        if constexpr (HT == 2) {  // packed FFMA2: acc += w y as (w.x, w.y) y.x + (-w.y, w.x) y.y
+        if constexpr (HT >= 2) {  // packed FFMA2: acc += w y as (w.x, w.y) y.x + (-w.y, w.x) y.y
 #pragma unroll
             for (int c = 0; c < NR / 2; ++c) {
                 const float4 v = *reinterpret_cast<const float4*>(yr + ((c ^ sw) << 4));
@@ -494,8 +591,12 @@ __global__ void __launch_bounds__(32 * NW) k_lg3(DetectArgs a, const __grid_cons
             float v[QM];
             uint32_t wd[kWords];
             if (!zf) {
-                demap_layer<QM, false, LT>(acc, slope, v);
-                pack_llr<LT, QM, false>(v, wd);
+                if constexpr (HT >= 3 && QM >= 6 && LT != kLlrI8) {
+                    demap_layer_x2<QM, LT>(acc, slope, wd);  // I and Q axes as packed pairs
+                } else {
+                    demap_layer<QM, false, LT>(acc, slope, v);
+                    pack_llr<LT, QM, false>(v, wd);
+                }
             } else {
                 demap_layer<QM, true, LT>(acc, slope, v);
                 pack_llr<LT, QM, true>(v, wd);
@@ -579,8 +680,19 @@ cudaError_t prepare() {
     }
 
 const KernelEntry kEntries[] = {
-    // C4 default: y and H of the CTA's units as one TMA tensor box each (lg3h), per-RE apply as
-    // packed FFMA2 (HT = 2), 4 warps = 16 units per CTA (78.4 us; 2 warps 79.8, 1: 84.1, 6: 94.2, 8: 81.4)
+    // C4 default (lg3hl, HT = 4): H by one TMA box, the Gram, Cholesky update, G^-1 and W~ products and
+    // the max-log demap as packed FFMA2 / FADD2 pairs with free operand forms (HT >= 3), and the y tile
+    // copied only after the setup, over the dead H / L / X area (L2-warm by a prefetch at CTA start):
+    // 29.7 instead of 54 KiB of shared memory lifts residency from 4 to 5 CTAs of 4 warps per SM.
+    // Measured per C4 step (bench, power-capped clocks): lg3hl 78.6 us at 1.78 GHz (139.7k cycles),
+    // lg3hq (HT 3, y early) 80.7 at 1.82 (147k), lg3hp (HT 2) 82.4 at 1.85 (152.6k), lg3hl2 (2 warps) 79.8.
+    KernelEntry{"lg3hl_16x8_q8_f16", 16, 8, 8, 1, 14, kLlrF16, 32, 1, launch3<16, 8, 8, kLlrF16, 4, 0, 4>,
+                prepare3<16, 8, 8, kLlrF16, 4, 0, 4>},
+    KernelEntry{"lg3hl2_16x8_q8_f16", 16, 8, 8, 1, 14, kLlrF16, 32, 1, launch3<16, 8, 8, kLlrF16, 2, 0, 4>,
+                prepare3<16, 8, 8, kLlrF16, 2, 0, 4>},
+    KernelEntry{"lg3hq_16x8_q8_f16", 16, 8, 8, 1, 14, kLlrF16, 32, 1, launch3<16, 8, 8, kLlrF16, 4, 0, 3>,
+                prepare3<16, 8, 8, kLlrF16, 4, 0, 3>},
+    // HT = 2: y and H as TMA boxes, the per-RE apply as packed FFMA2 (round 1 default)
     KernelEntry{"lg3hp_16x8_q8_f16", 16, 8, 8, 1, 14, kLlrF16, 32, 1, launch3<16, 8, 8, kLlrF16, 4, 0, 2>,
                 prepare3<16, 8, 8, kLlrF16, 4, 0, 2>},
     LG3_ENTRY("lg3_16x8_q8_f16", 16, 8, 8, kLlrF16, 2),  // y by TMA, H by per-unit bulk copies

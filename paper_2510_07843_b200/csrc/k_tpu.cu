@@ -254,34 +254,34 @@ __device__ __forceinline__ void apply_re(const DetectArgs& a, const SetupOut<NR,
     }
 }
 
-template <int NR, int NL, int QM, int LT, int TU, int G, int YL, bool ZF>
+template <int NR, int NL, int QM, int LT, int TU, int G, int YL, bool ZF, int SPH>
 __device__ __forceinline__ void apply_symbols(const DetectArgs& a, const SetupOut<NR, NL>& o, const float2* sy,
                                               uint64_t* bars, int slot, int sc, int ul, int g, bool active,
                                               float2 (*pf)[NR]) {
-    constexpr int NS = (kSym + G - 1) / G;  // symbols per thread (upper bound)
+    constexpr int NS = (SPH + G - 1) / G;  // symbols per thread (upper bound)
     if constexpr (YL == kYBulk) {
 #pragma unroll 1
-        for (int s = g; s < kSym; s += G) {
+        for (int s = g; s < SPH; s += G) {
             mbar_wait(&bars[s], 0);
             if (!active) continue;
             float2 yv[NR];
             const float2* ys = sy + (s * TU + ul) * NR;
 #pragma unroll
             for (int r = 0; r < NR; ++r) yv[r] = ys[r];
-            apply_re<NR, NL, QM, LT, ZF>(a, o, yv, (size_t)(slot * kSym + s) * a.n_sc + sc);
+            apply_re<NR, NL, QM, LT, ZF>(a, o, yv, (size_t)(slot * SPH + s) * a.n_sc + sc);
         }
     } else if constexpr (YL == kYAsync) {
         if (!active) return;
 #pragma unroll
         for (int i = 0; i < NS; ++i) {
             const int s = g + i * G;
-            if (s < kSym) {
+            if (s < SPH) {
                 cp_async_wait_dyn<NS>(NS - 1 - i);
                 float2 yv[NR];
                 const float2* ys = sy + (s * TU + ul) * NR;
 #pragma unroll
                 for (int r = 0; r < NR; ++r) yv[r] = ys[r];
-                apply_re<NR, NL, QM, LT, ZF>(a, o, yv, (size_t)(slot * kSym + s) * a.n_sc + sc);
+                apply_re<NR, NL, QM, LT, ZF>(a, o, yv, (size_t)(slot * SPH + s) * a.n_sc + sc);
             }
         }
     } else {
@@ -290,38 +290,38 @@ __device__ __forceinline__ void apply_symbols(const DetectArgs& a, const SetupOu
 #pragma unroll
         for (int i = 0; i < NS; ++i) {
             const int s = g + i * G;
-            if (s < kSym) {
+            if (s < SPH) {
                 float2 yv[NR];
 #pragma unroll
                 for (int r = 0; r < NR; ++r) yv[r] = pf[i % PF][r];
                 const int sn = s + PF * G;
-                if (sn < kSym)
-                    load_bytes<NR * 8>(a.y + ((size_t)(slot * kSym + sn) * a.n_sc + sc) * NR,
+                if (sn < SPH)
+                    load_bytes<NR * 8>(a.y + ((size_t)(slot * SPH + sn) * a.n_sc + sc) * NR,
                                        reinterpret_cast<uint32_t*>(&pf[i % PF][0]));
-                apply_re<NR, NL, QM, LT, ZF>(a, o, yv, (size_t)(slot * kSym + s) * a.n_sc + sc);
+                apply_re<NR, NL, QM, LT, ZF>(a, o, yv, (size_t)(slot * SPH + s) * a.n_sc + sc);
             }
         }
     }
 }
 
-// Shared-memory layout: [14 mbarriers | pad to 128 B][y tile 14 x TU x NR float2]
+// Shared-memory layout: [SPH <= 14 mbarriers | pad to 128 B][y tile SPH x TU x NR float2]
 //                       [W~ broadcast: NL*NR float2 x TU][slopes: NL x TU] (SHARE only)
-template <int NR, int NL, int TU, int YL, bool SHARE>
+template <int NR, int NL, int TU, int YL, bool SHARE, int SPH>
 constexpr int smem_bytes() {
-    return 128 + (YL == kYLdg ? 0 : kSym * TU * NR * 8) + (SHARE ? TU * (NL * NR * 8 + NL * 4) : 0);
+    return 128 + (YL == kYLdg ? 0 : SPH * TU * NR * 8) + (SHARE ? TU * (NL * NR * 8 + NL * 4) : 0);
 }
 
 // SHARE: only warp 0 runs the setup and broadcasts W~ / slopes through shared
 // memory to the other G-1 warps (no duplicated fp64 work).
-template <int NR, int NL, int QM, int LT, int TU, int G, int YL, typename ST, bool SHARE>
+template <int NR, int NL, int QM, int LT, int TU, int G, int YL, typename ST, bool SHARE, int SPH>
 __global__ void __launch_bounds__(TU* G) k_tpu(DetectArgs a) {
     static_assert(NR % 2 == 0, "16-byte y rows");
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
     float2* sy = reinterpret_cast<float2*>(smem + 128);
-    float2* sW = reinterpret_cast<float2*>(smem + 128 + (YL == kYLdg ? 0 : kSym * TU * NR * 8));
+    float2* sW = reinterpret_cast<float2*>(smem + 128 + (YL == kYLdg ? 0 : SPH * TU * NR * 8));
     float* sSlope = reinterpret_cast<float*>(sW + NL * NR * TU);
-    constexpr int NS = (kSym + G - 1) / G;
+    constexpr int NS = (SPH + G - 1) / G;
 
     // PDL: let the next detect call on this stream start its (read-only) prologue now.
     pdl_launch_dependents();
@@ -344,16 +344,16 @@ __global__ void __launch_bounds__(TU* G) k_tpu(DetectArgs a) {
     if constexpr (YL == kYBulk) {
         if (t == 0) {
 #pragma unroll
-            for (int s = 0; s < kSym; ++s) mbar_init(&bars[s], 1);
+            for (int s = 0; s < SPH; ++s) mbar_init(&bars[s], 1);
             fence_mbar_init();
         }
         __syncthreads();
         if (t == 0) {
             const uint32_t row_bytes = (uint32_t)nvalid * NR * 8u;
 #pragma unroll 1
-            for (int s = 0; s < kSym; ++s) {
+            for (int s = 0; s < SPH; ++s) {
                 mbar_arrive_expect_tx(&bars[s], row_bytes);
-                bulk_g2s(sy + s * TU * NR, a.y + ((size_t)(slot * kSym + s) * a.n_sc + sc0) * NR, row_bytes,
+                bulk_g2s(sy + s * TU * NR, a.y + ((size_t)(slot * SPH + s) * a.n_sc + sc0) * NR, row_bytes,
                          &bars[s]);
             }
         }
@@ -362,8 +362,8 @@ __global__ void __launch_bounds__(TU* G) k_tpu(DetectArgs a) {
 #pragma unroll
             for (int i = 0; i < NS; ++i) {
                 const int s = g + i * G;
-                if (s < kSym) {
-                    const float2* src = a.y + ((size_t)(slot * kSym + s) * a.n_sc + sc) * NR;
+                if (s < SPH) {
+                    const float2* src = a.y + ((size_t)(slot * SPH + s) * a.n_sc + sc) * NR;
                     float2* dst = sy + (s * TU + ul) * NR;
 #pragma unroll
                     for (int c = 0; c < NR / 2; ++c) cp_async16(dst + 2 * c, src + 2 * c);
@@ -376,8 +376,8 @@ __global__ void __launch_bounds__(TU* G) k_tpu(DetectArgs a) {
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
                 const int s = g + i * G;
-                if (s < kSym)
-                    load_bytes<NR * 8>(a.y + ((size_t)(slot * kSym + s) * a.n_sc + sc) * NR,
+                if (s < SPH)
+                    load_bytes<NR * 8>(a.y + ((size_t)(slot * SPH + s) * a.n_sc + sc) * NR,
                                        reinterpret_cast<uint32_t*>(&pf[i][0]));
             }
         }
@@ -414,33 +414,34 @@ __global__ void __launch_bounds__(TU* G) k_tpu(DetectArgs a) {
         }
     }
     if (a.sigma2 > 0.f)
-        apply_symbols<NR, NL, QM, LT, TU, G, YL, false>(a, o, sy, bars, slot, sc, ul, g, active, pf);
+        apply_symbols<NR, NL, QM, LT, TU, G, YL, false, SPH>(a, o, sy, bars, slot, sc, ul, g, active, pf);
     else
-        apply_symbols<NR, NL, QM, LT, TU, G, YL, true>(a, o, sy, bars, slot, sc, ul, g, active, pf);
+        apply_symbols<NR, NL, QM, LT, TU, G, YL, true, SPH>(a, o, sy, bars, slot, sc, ul, g, active, pf);
 }
 
-template <int NR, int NL, int QM, int LT, int TU, int G, int YL, typename ST, bool SH>
+template <int NR, int NL, int QM, int LT, int TU, int G, int YL, typename ST, bool SH, int SPH>
 cudaError_t launch(const DetectArgs& a, cudaStream_t s) {
     if (a.n_sc <= 0 || a.n_slots <= 0) return cudaSuccess;
     dim3 grid((a.n_sc + TU - 1) / TU, a.n_slots);
-    return launch_kernel(k_tpu<NR, NL, QM, LT, TU, G, YL, ST, SH>, grid, dim3(TU * G),
-                         smem_bytes<NR, NL, TU, YL, SH>(), s, a.overlap, a);
+    return launch_kernel(k_tpu<NR, NL, QM, LT, TU, G, YL, ST, SH, SPH>, grid, dim3(TU * G),
+                         smem_bytes<NR, NL, TU, YL, SH, SPH>(), s, a.overlap, a);
 }
 
-template <int NR, int NL, int QM, int LT, int TU, int G, int YL, typename ST, bool SH>
+template <int NR, int NL, int QM, int LT, int TU, int G, int YL, typename ST, bool SH, int SPH>
 cudaError_t prepare() {
-    constexpr int smem = smem_bytes<NR, NL, TU, YL, SH>();
+    constexpr int smem = smem_bytes<NR, NL, TU, YL, SH, SPH>();
     if (smem > 48 * 1024)
-        return cudaFuncSetAttribute(k_tpu<NR, NL, QM, LT, TU, G, YL, ST, SH>,
+        return cudaFuncSetAttribute(k_tpu<NR, NL, QM, LT, TU, G, YL, ST, SH, SPH>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     return cudaSuccess;
 }
 
-#define TPU_ENTRY2(NAME, NR, NL, QM, LT, TU, G, YL, ST, SH)                                   \
+#define TPU_ENTRY3(NAME, NR, NL, QM, LT, TU, G, YL, ST, SH, SPH)                              \
     KernelEntry {                                                                              \
-        NAME, NR, NL, QM, 1, 14, LT, 32, 1, launch<NR, NL, QM, LT, TU, G, YL, ST, SH>,        \
-            prepare<NR, NL, QM, LT, TU, G, YL, ST, SH>                                         \
+        NAME, NR, NL, QM, 1, SPH, LT, 32, 1, launch<NR, NL, QM, LT, TU, G, YL, ST, SH, SPH>,  \
+            prepare<NR, NL, QM, LT, TU, G, YL, ST, SH, SPH>                                    \
     }
+#define TPU_ENTRY2(NAME, NR, NL, QM, LT, TU, G, YL, ST, SH) TPU_ENTRY3(NAME, NR, NL, QM, LT, TU, G, YL, ST, SH, 14)
 #define TPU_ENTRY(NAME, NR, NL, QM, LT, TU, G, YL, ST) TPU_ENTRY2(NAME, NR, NL, QM, LT, TU, G, YL, ST, false)
 
 // First entry matching a plan wins (the default); another entry of the same
@@ -456,6 +457,12 @@ const KernelEntry kEntries[] = {
     TPU_ENTRY2("tpu_4x4_q2_f32", 4, 4, 2, kLlrF32, 64, 2, kYBulk, double, true),
     TPU_ENTRY2("tpu_4x4_q6_f32", 4, 4, 6, kLlrF32, 64, 2, kYBulk, double, true),
     TPU_ENTRY2("tpu_4x4_q8_f32", 4, 4, 8, kLlrF32, 64, 2, kYBulk, double, true),
+    // time-varying channels (NEXT-3): H every SPH < 14 symbols; one CTA per (H block, 64 subcarriers)
+    TPU_ENTRY3("tpu_4x4_q4_f32_s7", 4, 4, 4, kLlrF32, 64, 2, kYBulk, double, true, 7),
+    TPU_ENTRY3("tpu_4x4_q4_f32_s2", 4, 4, 4, kLlrF32, 64, 1, kYBulk, double, false, 2),
+    TPU_ENTRY3("tpu_4x4_q4_f32_s1", 4, 4, 4, kLlrF32, 64, 1, kYBulk, double, false, 1),
+    TPU_ENTRY3("tpu_2x2_q2_f32_s7", 2, 2, 2, kLlrF32, 32, 1, kYBulk, double, false, 7),
+    TPU_ENTRY3("tpu_2x2_q2_f32_s1", 2, 2, 2, kLlrF32, 32, 1, kYBulk, double, false, 1),
 };
 
 }  // namespace

@@ -214,9 +214,24 @@ def test_host_path_c5_chunked():
     assert np.array_equal(out, g["llr"])
 
 
+@pytest.mark.parametrize("k,sph,kernel", [(2, 7, "tpu_4x4_q4_f32_s7"), (2, 2, "tpu_4x4_q4_f32_s2"),
+                                          (2, 1, "tpu_4x4_q4_f32_s1"), (1, 7, "tpu_2x2_q2_f32_s7"),
+                                          (1, 1, "tpu_2x2_q2_f32_s1")])
+def test_time_varying_fast_kernels(k, sph, kernel):
+    """NEXT-3 fast path: the per-subcarrier fast kernels with H constant over sph < 14 symbols, over
+    several CTA tiles and a ragged subcarrier tail (n_sc = 300 for C2), against the oracle."""
+    cfg = dict(synth.CONFIGS[k], sym_per_h=sph)
+    kw = dict(n_sc=300, n_slots=2) if k == 2 else dict(n_slots=2)
+    w = synth.generate(cfg, **kw)
+    g = parity.run_gpu(w, kernel=kernel)
+    assert g["kernel"] == kernel and g["n_failed"] == 0
+    parity.compare(w, g)
+
+
 @pytest.mark.parametrize("k,sph", [(2, 1), (2, 7), (3, 2), (4, 7), (1, 1)])
 def test_time_varying_channel(k, sph):
-    """NEXT-3: H changes every sph symbols (sym_per_h < 14; the generic kernel serves it)."""
+    """NEXT-3: H changes every sph symbols (sym_per_h < 14): the shape's default kernel (the fast
+    per-subcarrier kernels for C1 / C2, the generic kernel otherwise)."""
     cfg = dict(synth.CONFIGS[k], sym_per_h=sph)
     kw = dict(n_sc=48, n_slots=1) if k != 1 else {}
     w = synth.generate(cfg, **kw)
