@@ -141,15 +141,10 @@ __device__ __forceinline__ void demap_axis_i8(float u, float rs, uint32_t* q, in
 // (A persistent warp-specialised variant -- producer, MMA, readout and 12 worker warps
 // over a ring of unit slots -- measured 107-124 us against this kernel's 90, the
 // per-slot chain of H load, Gram round trip and inversion being sequential.)
-// Fused kernel: W~ records per CTA in the workspace ring (2 setup batches: the setup group runs at most
-// one batch ahead of the B builder, which consumes the records in order)
-#ifndef C5X_RING
-#define C5X_RING 16
-#endif
-#ifndef C5X_HINT
-#define C5X_HINT 0
-#endif
-constexpr int kC5Ring = C5X_RING;
+// Fused kernel: W~ records per CTA in the workspace ring (4 setup batches; the setup group waits for a
+// slot only when it is that far ahead of the B builder, which consumes the records in order. 8 slots
+// coupled the two and cost 15 us per C5 step; 16 are as fast as one record per unit and 4.6x smaller)
+constexpr int kC5Ring = 16;
 
 namespace su {
 constexpr int UPB = 4;                   // units per batch (= warps)
@@ -167,17 +162,12 @@ template <typename UnitF>
 __device__ __forceinline__ void setup_issue_h(const CUtensorMap* hmapp, uint32_t gaddr, uint64_t* bar_tma, int nv,
                                               UnitF unit_of) {
     mbar_arrive_expect_tx(bar_tma, (uint32_t)(nv * 64 * 16 * 8));
-    for (int s = 0; s < nv; ++s) {
-        if (C5X_HINT)  // H is read once
-            tc::tma_load_2d_hint(gaddr + (uint32_t)(su::BG + s * 8192), hmapp, 0, (int)(unit_of(s) * 64), bar_tma,
-                                 tc::policy_evict_first());
-        else
-            asm volatile(
-                "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
-                ::"r"(gaddr + (uint32_t)(su::BG + s * 8192)), "l"(reinterpret_cast<uint64_t>(hmapp)), "r"(0),
-                "r"((int)(unit_of(s) * 64)), "r"(smem_u32(bar_tma))
-                : "memory");
-    }
+    for (int s = 0; s < nv; ++s)
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+            ::"r"(gaddr + (uint32_t)(su::BG + s * 8192)), "l"(reinterpret_cast<uint64_t>(hmapp)), "r"(0),
+            "r"((int)(unit_of(s) * 64)), "r"(smem_u32(bar_tma))
+            : "memory");
 }
 
 // One batch of up to su::UPB = 4 H-units through rows a2-a5 (a1-a5 steps documented at k_c5_setup),
@@ -487,14 +477,8 @@ __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorM
                     o[2 * kq + 1] = v[16 + kq];
                 }
                 char* dst = reinterpret_cast<char*>(reinterpret_cast<float*>(a.ws) + rec_of(s) * WS) + (size_t)r * NL * 8;
-                if constexpr (PUB && C5X_HINT) {  // the fused kernel's ring records stay in L2
-                    const uint64_t pol = tc::policy_evict_last();
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) tc::st_v8_hint(dst + 32 * q, o + 8 * q, pol);
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) st_v8(dst + 32 * q, o + 8 * q);
-                }
+                for (int q = 0; q < 4; ++q) st_v8(dst + 32 * q, o + 8 * q);
             }
         }
         PROF_ADD(prof, 6, p6);
@@ -531,7 +515,7 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
     const uint32_t raw = smem_u32(smem_raw);
     const uint32_t base = (raw + 1023u) & ~1023u;
     unsigned char* g = smem_raw + (base - raw);
-    // workspace record of local unit i: FUSED = slot i % kC5Ring of this CTA's ring (L2-resident, reused),
+    // workspace record of local unit i: FUSED = slot i % kC5Ring of this CTA's ring (reused: 20 MB instead of 91),
     // otherwise the unit's own record (written by the setup kernel)
     auto rec_of = [&](long long i) -> long long {
         if constexpr (FUSED) return (long long)blockIdx.x * kC5Ring + i % kC5Ring;
@@ -594,7 +578,6 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
             PROF_DECL;
             PROF_T(tk0);
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ymap)) : "memory");
-            const uint64_t ypol = C5X_HINT ? tc::policy_evict_first() : 0;  // y is streamed once
             // !BEPI: W~ records (rows a2-a5 of the setup kernel) of units i = j + 2 are staged when the y
             // chunks of unit j start (BEPI: by the B builder, so that the y stream never waits on them); y
             // itself is this call's input and streams before the setup completes
@@ -630,12 +613,8 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                 const long long uu = u0 + (gg >> 2) * du;
                 const int slot = (int)(uu / a.n_fb), fb = (int)(uu % a.n_fb);
                 mbar_arrive_expect_tx(&yfull[st], (uint32_t)SM::chunk);
-                if (C5X_HINT)
-                    tc::tma_load_3d_hint(base + (uint32_t)(SM::y0 + st * SM::chunk), &ymap, 32 * (int)(gg & 3),
-                                         fb * kSc, slot * kSym, &yfull[st], ypol);
-                else
-                    tma_load_3d(base + (uint32_t)(SM::y0 + st * SM::chunk), &ymap, 32 * (int)(gg & 3), fb * kSc,
-                                slot * kSym, &yfull[st]);
+                tma_load_3d(base + (uint32_t)(SM::y0 + st * SM::chunk), &ymap, 32 * (int)(gg & 3), fb * kSc,
+                            slot * kSym, &yfull[st]);
             }
             PROF_ADD(prof, 31, tk0);
             PROF_FLUSH(true);
@@ -831,11 +810,7 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
         auto build_B = [&](long long i, int tid) {
             // thread = (B row n = lane, K quarter kt = warp): the 32 lanes of a warp read 16 distinct W~ entries
             // of one antenna row (no bank conflicts; n and n + 16 share theirs) and store one 16-byte piece each
-#ifdef C5X_OLDMAP
-            const int n = tid >> 2, kt = tid & 3, kk = n & 15, b = (int)(i & 1);
-#else
             const int n = tid & 31, kt = tid >> 5, kk = n & 15, b = (int)(i & 1);
-#endif
             const bool im_row = n >= 16;
             mbar_wait_sleep(&wfull[i & 1], (uint32_t)((i >> 1) & 1));
             const float2* src = reinterpret_cast<const float2*>(g + SM::wst + (i & 1) * SM::wrec);
@@ -941,12 +916,8 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                     asm volatile("fence.proxy.async.global;" ::: "memory");
                 }
                 mbar_arrive_expect_tx(&wfull[i & 1], (uint32_t)SM::wrec);
-                const float* src = reinterpret_cast<const float*>(a.ws) + rec_of(i) * WS;
-                if constexpr (FUSED && C5X_HINT)
-                    tc::bulk_g2s_hint(g + SM::wst + (i & 1) * SM::wrec, src, (uint32_t)SM::wrec, &wfull[i & 1],
-                                      tc::policy_evict_last());
-                else
-                    bulk_g2s(g + SM::wst + (i & 1) * SM::wrec, src, (uint32_t)SM::wrec, &wfull[i & 1]);
+                bulk_g2s(g + SM::wst + (i & 1) * SM::wrec, reinterpret_cast<const float*>(a.ws) + rec_of(i) * WS,
+                         (uint32_t)SM::wrec, &wfull[i & 1]);
             };
             if constexpr (BEPI) {
                 if (warp < 8) {
@@ -1008,14 +979,6 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
     tc::fence_before();
     __syncthreads();
     if (warp == CW) tc::dealloc<512>(tmem);
-#ifdef C5X_NODISCARD
-    if constexpr (false) {
-#else
-    if constexpr (FUSED) {  // the ring records are dead: drop their L2 lines instead of writing them back
-#endif
-        const char* r0 = reinterpret_cast<const char*>(reinterpret_cast<const float*>(a.ws) + rec_of(0) * WS);
-        for (int l = t; l < kC5Ring * WS * 4 / 128; l += blockDim.x) tc::discard_l2(r0 + 128 * l);
-    }
 }
 
 template <int QM>
@@ -1187,13 +1150,10 @@ size_t c5f_workspace(const DetectArgs& a) {
         NAME, 64, 16, QM, kSc, 14, LT, 32, 2, launch_c5<QM, LT, 6, S, NLO, TA, SETUP, BEPI>,               \
             prepare_c5<QM, LT, 6, S, NLO, TA, SETUP, BEPI>, c5_workspace                                   \
     }
-#ifndef C5X_FNLO
-#define C5X_FNLO 2
-#endif
 #define C5F_ENTRY(NAME, QM, LT, S)                                                                          \
     KernelEntry {                                                                                          \
-        NAME, 64, 16, QM, kSc, 14, LT, 32, 1, launch_c5<QM, LT, 6, S, C5X_FNLO, 4, 2, true, true>,         \
-            prepare_c5<QM, LT, 6, S, C5X_FNLO, 4, 2, true, true>, c5f_workspace                            \
+        NAME, 64, 16, QM, kSc, 14, LT, 32, 1, launch_c5<QM, LT, 6, S, 2, 4, 2, true, true>,         \
+            prepare_c5<QM, LT, 6, S, 2, 4, 2, true, true>, c5f_workspace                            \
     }
 
 // First entry of a shape = its default (mimo_api.cu select_fast); the others are selectable by name.

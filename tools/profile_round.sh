@@ -20,15 +20,16 @@ for k in 2 3 4 5; do
       --log-file $out/range_c$k.csv python tools/traffic_range.py --config $k --steps 8 > $out/ncu_range_c$k.log 2>&1
 done
 # full captures of the dominant kernels
-full() {  # config kernel-regex skip name
-  local k=$1 re=$2 skip=$3 name=$4
-  python bench.py --config $k --profile --steps 3 --warmup 2 > $out/plain_full_$name.log 2>&1 && \
+full() {  # config kernel-regex skip name [bench args]
+  local k=$1 re=$2 skip=$3 name=$4 extra=${5:-}
+  python bench.py --config $k --profile --steps 3 --warmup 2 $extra > $out/plain_full_$name.log 2>&1 && \
     timeout 600 ncu --set full --clock-control none --import-source on -k regex:$re -s $skip -c 1 -o $out/full_$name \
-        python bench.py --config $k --profile --steps 3 --warmup 2 > $out/ncu_full_$name.log 2>&1
+        python bench.py --config $k --profile --steps 3 --warmup 2 $extra > $out/ncu_full_$name.log 2>&1
 }
 full 2 k_tpu 2 c2
 full 3 k_apply_stream 2 c3
 full 4 k_lg3 2 c4
 full 5 k_c5_apply 1 c5
-full 5 k_c5_setup 1 c5_setup
+full 5 k_c5_setup 1 c5_setup "--kernel c5_bf16kc_tcs_be_64x16_q6_i8"  # the two-kernel variant's setup
+timeout 600 python tools/time_varying.py --out $out/time_varying.jsonl > $out/time_varying.log 2>&1
 ls -la $out
