@@ -510,6 +510,12 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
     static_assert(!FUSED || BEPI, "fused setup: the epilogue warps build the B sets");
     constexpr uint32_t kSetupCols = kAring + NLO * kAcols;  // FUSED: the setup group's 128 / 256 TMEM columns
     constexpr int CW = 4 + EW;                       // MMA warp; CW + 1: TMA producer
+    // T1C (fused): the 40-RE tile 1 is converted by its own epilogue warps 8-9 (which are otherwise
+    // idle two thirds of the time), so converter warps 0-1 no longer make a second pass per chunk
+#ifndef C5X_T1C
+#define C5X_T1C 1
+#endif
+    constexpr bool T1C = FUSED && C5X_T1C;
     constexpr int WS = BigWs<NR, NL>::stride;
     extern __shared__ unsigned char smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -544,7 +550,7 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
 
     pdl_launch_dependents();
     if (t == 0) {
-        constexpr uint32_t ngrp = 1;
+        constexpr uint32_t ngrp = T1C ? 2 : 1;  // converter group (+ the tile-1 group)
         for (int i = 0; i < S; ++i) {
             mbar_init(&yfull[i], 1);
             mbar_init(&yfree[i], ngrp);
@@ -889,7 +895,7 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                     PROF_T(t4);
                     tc::fence_after();
                     convert_row(st, lb, 0, 32 * warp + lane, warp);
-                    if (warp < 2) convert_row(st, lb, 1, min(128 + 32 * warp + lane, kRe - 1), warp);  // REs 128-167
+                    if (!T1C && warp < 2) convert_row(st, lb, 1, min(128 + 32 * warp + lane, kRe - 1), warp);  // REs 128-167
                     tc::wait_st();
                     PROF_ADD(prof, 20, t4);
                     PROF_T(t5);
@@ -903,8 +909,44 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                 }
             }
             PROF_FLUSH(t == 0);
+        } else if (T1C && warp >= 8) {
+            // ================= tile-1 group (warps 8-9 = lane quadrants 0-1): converts REs 128-167 of every
+            // chunk of unit i, then runs unit i - 1's tile-1 epilogue =================
+            const int qd = warp - 8;
+            const int row = 128 + 32 * qd + lane;
+#pragma unroll 1
+            for (long long i = 0; i <= n_my; ++i) {
+                if (i < n_my) {
+#pragma unroll 1
+                    for (int c = 0; c < 4; ++c) {
+                        const long long gg = 4 * i + c;
+                        const int st = (int)(gg % S), lb = (int)(gg % NLO);
+                        mbar_wait_sleep(&yfull[st], (uint32_t)((gg / S) & 1));
+                        if (gg >= NLO) mbar_wait_sleep(&afree[lb], (uint32_t)(((gg / NLO) + 1) & 1));
+                        tc::fence_after();
+                        convert_row(st, lb, 1, min(row, kRe - 1), qd);
+                        tc::wait_st();
+                        tc::fence_before();
+                        asm volatile("bar.sync 3, 64;" ::: "memory");
+                        if (t == 32 * 8) {
+                            mbar_arrive(&afull[lb]);
+                            mbar_arrive(&yfree[st]);
+                        }
+                    }
+                }
+                if (i >= 1) {
+                    const long long j = i - 1;
+                    const int b = (int)(j & 1);
+                    mbar_wait_sleep(&accfull[b], (uint32_t)((j >> 1) & 1));
+                    tc::fence_after();
+                    epilogue_row(j, b, 1, row, qd, row < kRe);
+                    tc::fence_before();
+                    asm volatile("bar.sync 3, 64;" ::: "memory");
+                    if (t == 32 * 8) mbar_arrive(&tfree[b]);
+                }
+            }
         } else {
-            // ================= epilogue: tile 0 on warps 4-7, compact tile 1 on warps 8-9 =================
+            // ================= epilogue: tile 0 on warps 4-7, compact tile 1 on warps 8-9 (unless T1C) =================
             // (BEPI: warps 4-7 also build the B set of unit i + 2 as soon as unit i's MMAs completed)
             const int e = warp - 4, we = e & 3, tile = e >> 2;
             PROF_DECL;
@@ -969,7 +1011,7 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                 PROF_ADD(prof, 25, t1);
                 PROF_T(t2);
                 tc::fence_before();
-                asm volatile("bar.sync 2, %0;" ::"r"(32 * EW) : "memory");
+                asm volatile("bar.sync 2, %0;" ::"r"(T1C ? 128 : 32 * EW) : "memory");
                 if (t == 128) mbar_arrive(&tfree[b]);
                 PROF_ADD(prof, 26, t2);
             }

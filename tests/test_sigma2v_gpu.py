@@ -54,7 +54,8 @@ def test_per_slot_sigma2_matches_oracle(k):
 
 
 def test_per_block_sigma2_time_varying_generic():
-    """sym_per_h = 7: one variance per H time block (two per slot), on the generic kernel."""
+    """sym_per_h = 7: one variance per H time block (two per slot), on the shape's sym_per_h = 7
+    kernel (tpu_4x4_q4_f32_s7)."""
     cfg = dict(synth.CONFIGS[2], n_sc=48, n_slots=2, sym_per_h=7)
     w = synth.generate(cfg, seed=5)
     s2v = _per_slot_sigma2(w, 6)
