@@ -145,6 +145,7 @@ __device__ __forceinline__ void demap_axis_i8(float u, float rs, uint32_t* q, in
 // slot only when it is that far ahead of the B builder, which consumes the records in order. 8 slots
 // coupled the two and cost 15 us per C5 step; 16 are as fast as one record per unit and 4.6x smaller)
 constexpr int kC5Ring = 16;
+constexpr int kSetupConvUnroll = 2;  // 4 and 8 measured slower
 
 namespace su {
 constexpr int UPB = 4;                   // units per batch (= warps)
@@ -206,7 +207,7 @@ __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorM
         mbar_wait(bar_tma, it & 1);
         PROF_ADD(prof, 0, p0);
         PROF_T(p1);
-#pragma unroll 2
+#pragma unroll (kSetupConvUnroll)
         for (int q = gt; q < su::UPB * 256; q += 128) {  // item = (unit, row r, 8 columns 8 cp .. 8 cp + 7)
             const int s = q >> 8, r = (q >> 2) & 63, cp = q & 3, sw = r & 7;
             const unsigned char* src = g + su::BG + s * 8192 + r * 128;
@@ -224,7 +225,11 @@ __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorM
         tc::fence_proxy_async();
         if constexpr (PUB) {
             if (it > 0) {  // the previous batch's W~ records (deferred, see above)
+#ifdef C5X_ACQREL
+                asm volatile("fence.acq_rel.gpu;" ::: "memory");
+#else
                 __threadfence();
+#endif
                 asm volatile("fence.proxy.async.global;" ::: "memory");
             }
         }
@@ -510,12 +515,6 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
     static_assert(!FUSED || BEPI, "fused setup: the epilogue warps build the B sets");
     constexpr uint32_t kSetupCols = kAring + NLO * kAcols;  // FUSED: the setup group's 128 / 256 TMEM columns
     constexpr int CW = 4 + EW;                       // MMA warp; CW + 1: TMA producer
-    // T1C (fused): the 40-RE tile 1 is converted by its own epilogue warps 8-9 (which are otherwise
-    // idle two thirds of the time), so converter warps 0-1 no longer make a second pass per chunk
-#ifndef C5X_T1C
-#define C5X_T1C 1
-#endif
-    constexpr bool T1C = FUSED && C5X_T1C;
     constexpr int WS = BigWs<NR, NL>::stride;
     extern __shared__ unsigned char smem_raw[];
     const uint32_t raw = smem_u32(smem_raw);
@@ -550,7 +549,7 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
 
     pdl_launch_dependents();
     if (t == 0) {
-        constexpr uint32_t ngrp = T1C ? 2 : 1;  // converter group (+ the tile-1 group)
+        constexpr uint32_t ngrp = 1;
         for (int i = 0; i < S; ++i) {
             mbar_init(&yfull[i], 1);
             mbar_init(&yfree[i], ngrp);
@@ -895,7 +894,7 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                     PROF_T(t4);
                     tc::fence_after();
                     convert_row(st, lb, 0, 32 * warp + lane, warp);
-                    if (!T1C && warp < 2) convert_row(st, lb, 1, min(128 + 32 * warp + lane, kRe - 1), warp);  // REs 128-167
+                    if (warp < 2) convert_row(st, lb, 1, min(128 + 32 * warp + lane, kRe - 1), warp);  // REs 128-167
                     tc::wait_st();
                     PROF_ADD(prof, 20, t4);
                     PROF_T(t5);
@@ -909,44 +908,8 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                 }
             }
             PROF_FLUSH(t == 0);
-        } else if (T1C && warp >= 8) {
-            // ================= tile-1 group (warps 8-9 = lane quadrants 0-1): converts REs 128-167 of every
-            // chunk of unit i, then runs unit i - 1's tile-1 epilogue =================
-            const int qd = warp - 8;
-            const int row = 128 + 32 * qd + lane;
-#pragma unroll 1
-            for (long long i = 0; i <= n_my; ++i) {
-                if (i < n_my) {
-#pragma unroll 1
-                    for (int c = 0; c < 4; ++c) {
-                        const long long gg = 4 * i + c;
-                        const int st = (int)(gg % S), lb = (int)(gg % NLO);
-                        mbar_wait_sleep(&yfull[st], (uint32_t)((gg / S) & 1));
-                        if (gg >= NLO) mbar_wait_sleep(&afree[lb], (uint32_t)(((gg / NLO) + 1) & 1));
-                        tc::fence_after();
-                        convert_row(st, lb, 1, min(row, kRe - 1), qd);
-                        tc::wait_st();
-                        tc::fence_before();
-                        asm volatile("bar.sync 3, 64;" ::: "memory");
-                        if (t == 32 * 8) {
-                            mbar_arrive(&afull[lb]);
-                            mbar_arrive(&yfree[st]);
-                        }
-                    }
-                }
-                if (i >= 1) {
-                    const long long j = i - 1;
-                    const int b = (int)(j & 1);
-                    mbar_wait_sleep(&accfull[b], (uint32_t)((j >> 1) & 1));
-                    tc::fence_after();
-                    epilogue_row(j, b, 1, row, qd, row < kRe);
-                    tc::fence_before();
-                    asm volatile("bar.sync 3, 64;" ::: "memory");
-                    if (t == 32 * 8) mbar_arrive(&tfree[b]);
-                }
-            }
         } else {
-            // ================= epilogue: tile 0 on warps 4-7, compact tile 1 on warps 8-9 (unless T1C) =================
+            // ================= epilogue: tile 0 on warps 4-7, compact tile 1 on warps 8-9 =================
             // (BEPI: warps 4-7 also build the B set of unit i + 2 as soon as unit i's MMAs completed)
             const int e = warp - 4, we = e & 3, tile = e >> 2;
             PROF_DECL;
@@ -1011,7 +974,7 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                 PROF_ADD(prof, 25, t1);
                 PROF_T(t2);
                 tc::fence_before();
-                asm volatile("bar.sync 2, %0;" ::"r"(T1C ? 128 : 32 * EW) : "memory");
+                asm volatile("bar.sync 2, %0;" ::"r"(32 * EW) : "memory");
                 if (t == 128) mbar_arrive(&tfree[b]);
                 PROF_ADD(prof, 26, t2);
             }

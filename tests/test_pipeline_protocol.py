@@ -35,14 +35,11 @@ def wait(b, idx):
         raise ABA(f"released at {b.phases} completions while waiting for completion #{idx}")
 
 
-def apply_roles(n_my, S, NLO, bepi=True, t1c=False):
-    """t1c: the fused kernel's tile-1 group (warps 8-9) converts the 40-RE tile of every chunk and then
-    runs the previous unit's tile-1 epilogue; yfree / afull / tfree then count two arrivals."""
+def apply_roles(n_my, S, NLO, bepi=True):
     B = lambda c=1: Barrier(c)
-    ng = 2 if t1c else 1
-    yfull, yfree = [B() for _ in range(S)], [B(ng) for _ in range(S)]
-    afull, afree = [B(ng) for _ in range(NLO)], [B() for _ in range(NLO)]
-    bready, accfull, tfree = [B() for _ in range(2)], [B() for _ in range(2)], [B(ng) for _ in range(2)]
+    yfull, yfree = [B() for _ in range(S)], [B() for _ in range(S)]
+    afull, afree = [B() for _ in range(NLO)], [B() for _ in range(NLO)]
+    bready, accfull, tfree = [B() for _ in range(2)], [B() for _ in range(2)], [B() for _ in range(2)]
     wfull, wfree = [B() for _ in range(2)], [B() for _ in range(2)]
     G = 4 * n_my
 
@@ -127,25 +124,7 @@ def apply_roles(n_my, S, NLO, bepi=True, t1c=False):
             tfree[b].arrive()
             yield "step"
 
-    def tile1():
-        for i in range(n_my + 1):
-            if i < n_my:
-                for c in range(4):
-                    gg = 4 * i + c
-                    st, lb = gg % S, gg % NLO
-                    yield from wait(yfull[st], gg // S)
-                    if gg >= NLO:
-                        yield from wait(afree[lb], gg // NLO - 1)
-                    afull[lb].arrive()
-                    yfree[st].arrive()
-                    yield "step"
-            if i >= 1:
-                j = i - 1
-                yield from wait(accfull[j & 1], j >> 1)
-                tfree[j & 1].arrive()
-                yield "step"
-
-    return [producer(), mma(), converters(), epilogue()] + ([tile1()] if t1c else [])
+    return [producer(), mma(), converters(), epilogue()]
 
 
 def run(roles, max_rounds=200000):
@@ -170,10 +149,10 @@ def run(roles, max_rounds=200000):
 
 
 @pytest.mark.parametrize("S,NLO", [(6, 4), (4, 2), (8, 4), (7, 4), (5, 2)])
-@pytest.mark.parametrize("bepi,t1c", [(True, False), (False, False), (True, True)])
+@pytest.mark.parametrize("bepi", [True, False])
 @pytest.mark.parametrize("n_my", [0, 1, 2, 3, 4, 5, 7, 8, 9, 13, 74])
-def test_apply_protocol_no_deadlock_no_aba(S, NLO, bepi, t1c, n_my):
-    assert run(apply_roles(n_my, S, NLO, bepi, t1c)), "protocol deadlocks"
+def test_apply_protocol_no_deadlock_no_aba(S, NLO, bepi, n_my):
+    assert run(apply_roles(n_my, S, NLO, bepi)), "protocol deadlocks"
 
 
 def test_model_detects_a_two_phase_runaway():
