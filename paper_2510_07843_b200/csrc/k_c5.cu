@@ -225,11 +225,7 @@ __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorM
         tc::fence_proxy_async();
         if constexpr (PUB) {
             if (it > 0) {  // the previous batch's W~ records (deferred, see above)
-#ifdef C5X_ACQREL
-                asm volatile("fence.acq_rel.gpu;" ::: "memory");
-#else
                 __threadfence();
-#endif
                 asm volatile("fence.proxy.async.global;" ::: "memory");
             }
         }
