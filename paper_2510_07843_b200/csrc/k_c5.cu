@@ -68,20 +68,20 @@ extern "C" int mimo_c5_sprof_read(unsigned long long* host) {
 namespace mimo {
 namespace {
 
-template <int S_, int NLO_, int TA_, bool FUSED_ = false>
+template <int S_, int NLO_, int TA_, bool FUSED_ = false, int NB_ = 2>
 struct C5Smem {
     static constexpr int S = S_;                              // y stages
     static constexpr int NLO = NLO_;                          // TMEM A ring slots (chunks)
     static constexpr size_t chunk = (size_t)kRe * 128;        // 21504 = 21 x 1024
     static constexpr size_t y0 = 0;
-    static constexpr size_t B = S * chunk;                    // 2 B sets (1024-aligned)
+    static constexpr size_t B = S * chunk;                    // NB_ B sets (1024-aligned)
     static constexpr size_t bset = TA_ == 1 ? 4 * 64 * 128 : 2 * 64 * 128;  // K atoms x 64 rows x 128 B
-    static constexpr size_t slope = B + 2 * bset;             // [4][16] slope | [4][16] sqrt(slope / 127)
-    static constexpr size_t wst = slope + 512;                // [2] W~ workspace records staged by TMA
+    static constexpr size_t slope = B + NB_ * bset;           // [8][16] slope | [8][16] sqrt(slope / 127)
+    static constexpr size_t wst = slope + 1024;               // [2] W~ workspace records staged by TMA
     static constexpr size_t wrec = (size_t)BigWs<64, 16>::stride * 4;
     static constexpr size_t setup = (wst + 2 * wrec + 1023) / 1024 * 1024;  // FUSED: the setup group's 64 KiB
     static constexpr size_t bars = setup + (FUSED_ ? 65536 : 0);
-    static constexpr int NBAR = 2 * S + 2 * NLO + 2 * 3 + 4 + 2;  // yfull, yfree | afull, afree | bready, accfull, tfree | wfull, wfree | setup tma, mma
+    static constexpr int NBAR = 2 * S + 2 * NLO + NB_ * 3 + 4 + 2;  // yfull, yfree | afull, afree | bready, accfull, tfree | wfull, wfree | setup tma, mma
     static constexpr size_t ready = bars + NBAR * 8;           // FUSED: [0] units whose W~ records are written,
                                                                //        [1] units whose B sets are built
     static constexpr size_t tslot = ready + 8;
@@ -490,11 +490,13 @@ __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorM
     PROF_SFLUSH(gt == 0);
 }
 
-template <int QM, int LT, int EW, int S_, int NLO_, int TA, bool BEPI, bool FUSED>
+// NACC = accumulators in TMEM = B sets in shared memory: unit i uses slot i % NACC, and its MMAs wait
+// for the epilogue of unit i - NACC (and for B set i % NACC, built after unit i - NACC's MMAs).
+template <int QM, int LT, int EW, int S_, int NLO_, int TA, bool BEPI, bool FUSED, int NACC = 2>
 __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
     k_c5_apply(DetectArgs a, const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap hmap) {
     constexpr int NR = 64, NL = 16;
-    using SM = C5Smem<S_, NLO_, TA, FUSED>;
+    using SM = C5Smem<S_, NLO_, TA, FUSED, NACC>;
     constexpr int S = S_, NLO = NLO_;
     static_assert(EW == 6, "6 epilogue warps (4 for tile 0, 2 for the compact tile 1)");
 
@@ -504,7 +506,7 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
     // two accumulators take 128 TMEM columns instead of 256
     constexpr bool KC = TA == 4;
     constexpr uint32_t kAccCols = KC ? 64u : 128u;   // TMEM columns per accumulator (2 row tiles)
-    constexpr uint32_t kAring = 2u * kAccCols;       // TMEM columns 0 .. kAring-1: 2 accumulators
+    constexpr uint32_t kAring = NACC * kAccCols;     // TMEM columns 0 .. kAring-1: NACC accumulators
     constexpr uint32_t kAcols = TA == 1 ? 128u : 64u;  // TMEM columns per A ring slot (one chunk, 2 tiles)
     constexpr bool kWide = kAring + NLO * kAcols + 256u <= 512u;  // FUSED: room for the wide setup products
     static_assert(kAring + NLO * kAcols + (FUSED ? 128u : 0u) <= 512u, "TMEM");
@@ -527,10 +529,10 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
     uint64_t* yfree = bar + S;         // [S]    converters done with the stage
     uint64_t* afull = bar + 2 * S;     // [NLO]  converters stored the chunk's A rows
     uint64_t* afree = afull + NLO;     // [NLO]  MMAs of the chunk completed
-    uint64_t* bready = afree + NLO;    // [2]    converters built B
-    uint64_t* accfull = bready + 2;    // [2]    the unit's last MMA completed
-    uint64_t* tfree = accfull + 2;     // [2]    epilogue done with the accumulator
-    uint64_t* wfull = tfree + 2;       // [2]    W~ record of unit i staged (TMA tx)
+    uint64_t* bready = afree + NLO;    // [NACC] B set built
+    uint64_t* accfull = bready + NACC; // [NACC] the unit's last MMA completed
+    uint64_t* tfree = accfull + NACC;  // [NACC] epilogue done with the accumulator
+    uint64_t* wfull = tfree + NACC;    // [2]    W~ record of unit i staged (TMA tx)
     uint64_t* wfree = wfull + 2;       // [2]    B set built from it
     uint64_t* stma = wfree + 2;        //        FUSED: setup group's H TMA
     uint64_t* smma = stma + 1;         //        FUSED: setup group's MMAs
@@ -554,10 +556,12 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
             mbar_init(&afull[i], ngrp);
             mbar_init(&afree[i], 1);
         }
-        for (int i = 0; i < 2; ++i) {
+        for (int i = 0; i < NACC; ++i) {
             mbar_init(&bready[i], 1);
             mbar_init(&accfull[i], 1);
             mbar_init(&tfree[i], ngrp);
+        }
+        for (int i = 0; i < 2; ++i) {
             mbar_init(&wfull[i], 1);
             mbar_init(&wfree[i], 1);
         }
@@ -667,12 +671,13 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
             PROF_DECL;
 #pragma unroll 1
             for (long long i = 0; i < n_my; ++i) {
-                const int b = (int)(i & 1);
+                const int b = (int)(i % NACC);
+                const uint32_t ph = (uint32_t)(i / NACC);  // completion index of this unit on slot b
                 PROF_T(t0);
-                mbar_wait_sleep(&bready[b], (uint32_t)((i >> 1) & 1));
+                mbar_wait_sleep(&bready[b], ph & 1u);
                 PROF_ADD(prof, 8, t0);
                 PROF_T(t1);
-                if (i >= 2) mbar_wait_sleep(&tfree[b], (uint32_t)(((i >> 1) + 1) & 1));
+                if (i >= NACC) mbar_wait_sleep(&tfree[b], (ph + 1u) & 1u);
                 PROF_ADD(prof, 9, t1);
                 const uint32_t acc = tmem + kAccCols * (uint32_t)b;
                 const uint64_t db = tc::desc_add(dB, (uint32_t)(b * SM::bset));
@@ -771,12 +776,12 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                 else x[k] = make_float2(__uint_as_float(hv[k]) + __uint_as_float(lv[k]),
                                         __uint_as_float(hv[16 + k]) + __uint_as_float(lv[16 + k]));
             }
-            const float* sl = sslope + (i & 3) * 16;
+            const float* sl = sslope + (i & 7) * 16;
             if (a.llr) {
                 uint32_t wd[(kRec + 3) / 4];
                 if (LT == kLlrI8 && !zf) {
                     uint32_t q[NL * QM];
-                    const float* rs = sslope + 64 + (i & 3) * 16;
+                    const float* rs = sslope + 128 + (i & 7) * 16;
 #pragma unroll
                     for (int k = 0; k < NL; ++k) {
                         demap_axis_i8<QM / 2>(x[k].x, rs[k], q + k * QM, 2);
@@ -806,12 +811,12 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
             }
         };
 
-        // B = [B_hi; B_lo] of unit i (bf16 or tf32 split of the real form of W~) into B set i & 1, and the
-        // unit's slopes into slope ring slot i & 3; tid in 0..127 of the building warp group
+        // B = [B_hi; B_lo] of unit i (bf16 or tf32 split of the real form of W~) into B set i % NACC, and the
+        // unit's slopes into slope ring slot i & 7; tid in 0..127 of the building warp group
         auto build_B = [&](long long i, int tid) {
             // thread = (B row n = lane, K quarter kt = warp): the 32 lanes of a warp read 16 distinct W~ entries
             // of one antenna row (no bank conflicts; n and n + 16 share theirs) and store one 16-byte piece each
-            const int n = tid & 31, kt = tid >> 5, kk = n & 15, b = (int)(i & 1);
+            const int n = tid & 31, kt = tid >> 5, kk = n & 15, b = (int)(i % NACC);
             const bool im_row = n >= 16;
             mbar_wait_sleep(&wfull[i & 1], (uint32_t)((i >> 1) & 1));
             const float2* src = reinterpret_cast<const float2*>(g + SM::wst + (i & 1) * SM::wrec);
@@ -849,8 +854,8 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
             }
             if (tid < NL) {
                 const float slv = reinterpret_cast<const float*>(src + NR * NL)[tid];
-                sslope[(i & 3) * 16 + tid] = slv;
-                sslope[64 + (i & 3) * 16 + tid] = sqrtf(slv * (1.f / 127.f));
+                sslope[(i & 7) * 16 + tid] = slv;
+                sslope[128 + (i & 7) * 16 + tid] = sqrtf(slv * (1.f / 127.f));
             }
             tc::fence_proxy_async();
         };
@@ -861,19 +866,19 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
             PROF_DECL;
 #pragma unroll 1
             for (long long i = 0; i < n_my; ++i) {
-                const int b = (int)(i & 1);
+                const int b = (int)(i % NACC);
                 if constexpr (!BEPI) {
-                    // B set b is free once unit i-2's MMAs completed; the slope ring slot i & 3 was last read
-                    // by epilogue(i-4), which finished before tfree(i-4) < accfull(i-2)
+                    // B set b is free once unit i-NACC's MMAs completed; the slope ring slot i & 7 was last read
+                    // by epilogue(i-8), which finished before tfree(i-8) < accfull(i-NACC)
                     PROF_T(t0);
-                    if (i >= 2) mbar_wait_sleep(&accfull[b], (uint32_t)(((i >> 1) + 1) & 1));
+                    if (i >= NACC) mbar_wait_sleep(&accfull[b], (uint32_t)(((i / NACC) + 1) & 1));
                     PROF_ADD(prof, 16, t0);
                     PROF_T(t1);
                     build_B(i, tc_);
                     asm volatile("bar.sync 1, 128;" ::: "memory");
                     if (tc_ == 0) {
                         mbar_arrive(&bready[b]);
-                        mbar_arrive(&wfree[b]);
+                        mbar_arrive(&wfree[i & 1]);
                     }
                     PROF_ADD(prof, 17, t1);
                 }
@@ -921,44 +926,46 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                          (uint32_t)SM::wrec, &wfull[i & 1]);
             };
             if constexpr (BEPI) {
-                if (warp < 8) {
+                if (warp < 8) {  // B sets of units 0 .. NACC-1; W stage j & 1 is refilled with unit j + 2's record
                     if (t == 128) {
                         pdl_wait();  // the setup (kernel or group) of this call writes the workspace
                         for (long long i0 = 0; i0 < 2 && i0 < n_my; ++i0) issue_w(i0);
                     }
-                    for (long long i0 = 0; i0 < 2 && i0 < n_my; ++i0) build_B(i0, t - 128);
-                    asm volatile("bar.sync 4, 128;" ::: "memory");
-                    if (t == 128) {
-                        for (long long i0 = 0; i0 < 2 && i0 < n_my; ++i0) mbar_arrive(&bready[i0]);
-                        if constexpr (FUSED) *units_built = (int)min(2ll, n_my);
-                        for (long long i0 = 2; i0 < 4 && i0 < n_my; ++i0) issue_w(i0);
+                    for (long long j = 0; j < NACC && j < n_my; ++j) {
+                        build_B(j, t - 128);
+                        asm volatile("bar.sync 4, 128;" ::: "memory");
+                        if (t == 128) {
+                            mbar_arrive(&bready[j]);
+                            if constexpr (FUSED) *units_built = (int)(j + 1);
+                            if (j + 2 < n_my) issue_w(j + 2);
+                        }
                     }
                 }
             }
 #pragma unroll 1
             for (long long i = 0; i < n_my; ++i) {
-                const int b = (int)(i & 1);
+                const int b = (int)(i % NACC);
                 PROF_T(t0);
-                mbar_wait_sleep(&accfull[b], (uint32_t)((i >> 1) & 1));
+                mbar_wait_sleep(&accfull[b], (uint32_t)((i / NACC) & 1));
                 PROF_ADD(prof, 24, t0);
                 tc::fence_after();
                 if constexpr (BEPI) {
-                    if (warp < 8 && i + 2 < n_my) {  // B set b is free: unit i's MMAs completed
+                    if (warp < 8 && i + NACC < n_my) {  // B set b is free: unit i's MMAs completed
                         PROF_T(tb);
 #ifdef C5_PROFILE
                         {
                             PROF_T(tw);
-                            mbar_wait_sleep(&wfull[b], (uint32_t)(((i + 2) >> 1) & 1));
+                            mbar_wait_sleep(&wfull[(i + NACC) & 1], (uint32_t)(((i + NACC) >> 1) & 1));
                             PROF_ADD(prof, 28, tw);
                         }
 #endif
-                        build_B(i + 2, t - 128);
+                        build_B(i + NACC, t - 128);
                         asm volatile("bar.sync 4, 128;" ::: "memory");
                         if (t == 128) {
                             mbar_arrive(&bready[b]);
-                            if constexpr (FUSED) *units_built = (int)(i + 3);
+                            if constexpr (FUSED) *units_built = (int)(i + NACC + 1);
                             PROF_T(ti);
-                            if (i + 4 < n_my) issue_w(i + 4);  // W stage b is read
+                            if (i + NACC + 2 < n_my) issue_w(i + NACC + 2);  // its W stage is read
                             PROF_ADD(prof, 29, ti);
                         }
                         PROF_ADD(prof, 27, tb);
@@ -1077,7 +1084,7 @@ cudaError_t prepare_setup() {
                                     (int)(4 * SetupSmem<64, 16, SETUP == 0 ? 0 : 1>::per_unit));
 }
 
-template <int QM, int LT, int EW, int S, int NLO, int TA, int SETUP, bool BEPI, bool FUSED = false>
+template <int QM, int LT, int EW, int S, int NLO, int TA, int SETUP, bool BEPI, bool FUSED = false, int NACC = 2>
 cudaError_t launch_c5(const DetectArgs& a, cudaStream_t s) {
     if (a.n_units <= 0) return cudaSuccess;
     static int n_sm = 0;
@@ -1113,24 +1120,24 @@ cudaError_t launch_c5(const DetectArgs& a, cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(a.n_units < n_sm ? a.n_units : n_sm));
     cfg.blockDim = dim3(32 * (6 + EW) + (FUSED ? 128 : 0));
-    cfg.dynamicSmemBytes = C5Smem<S, NLO, TA, FUSED>::total;
+    cfg.dynamicSmemBytes = C5Smem<S, NLO, TA, FUSED, NACC>::total;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = a.overlap ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, k_c5_apply<QM, LT, EW, S, NLO, TA, BEPI, FUSED>, a, ymap, hmap);
+    return cudaLaunchKernelEx(&cfg, k_c5_apply<QM, LT, EW, S, NLO, TA, BEPI, FUSED, NACC>, a, ymap, hmap);
 }
 
-template <int QM, int LT, int EW, int S, int NLO, int TA, int SETUP, bool BEPI, bool FUSED = false>
+template <int QM, int LT, int EW, int S, int NLO, int TA, int SETUP, bool BEPI, bool FUSED = false, int NACC = 2>
 cudaError_t prepare_c5() {
     if constexpr (!FUSED) {
         cudaError_t e = prepare_setup<QM, SETUP>();
         if (e != cudaSuccess) return e;
     }
-    return cudaFuncSetAttribute(k_c5_apply<QM, LT, EW, S, NLO, TA, BEPI, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)C5Smem<S, NLO, TA, FUSED>::total);
+    return cudaFuncSetAttribute(k_c5_apply<QM, LT, EW, S, NLO, TA, BEPI, FUSED, NACC>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C5Smem<S, NLO, TA, FUSED, NACC>::total);
 }
 
 size_t c5_workspace(const DetectArgs& a) { return (size_t)a.n_units * BigWs<64, 16>::stride * 4; }
@@ -1151,10 +1158,10 @@ size_t c5f_workspace(const DetectArgs& a) {
         NAME, 64, 16, QM, kSc, 14, LT, 32, 2, launch_c5<QM, LT, 6, S, NLO, TA, SETUP, BEPI>,               \
             prepare_c5<QM, LT, 6, S, NLO, TA, SETUP, BEPI>, c5_workspace                                   \
     }
-#define C5F_ENTRY(NAME, QM, LT, S)                                                                          \
+#define C5F_ENTRY(NAME, QM, LT, S, NACC)                                                                    \
     KernelEntry {                                                                                          \
-        NAME, 64, 16, QM, kSc, 14, LT, 32, 1, launch_c5<QM, LT, 6, S, 2, 4, 2, true, true>,         \
-            prepare_c5<QM, LT, 6, S, 2, 4, 2, true, true>, c5f_workspace                            \
+        NAME, 64, 16, QM, kSc, 14, LT, 32, 1, launch_c5<QM, LT, 6, S, 2, 4, 2, true, true, NACC>,          \
+            prepare_c5<QM, LT, 6, S, 2, 4, 2, true, true, NACC>, c5f_workspace                             \
     }
 
 // First entry of a shape = its default (mimo_api.cu select_fast); the others are selectable by name.
@@ -1163,7 +1170,8 @@ size_t c5f_workspace(const DetectArgs& a) {
 // contractions; gj = SIMT Gauss-Jordan; chol = SIMT Cholesky), be = the B sets built by the
 // (under-loaded) epilogue warps instead of the converter warps, which set the pace of the pipeline.
 const KernelEntry kEntries[] = {
-    C5F_ENTRY("c5_fused_64x16_q6_i8", 6, kLlrI8, 5),  // C5 default: setup warp group inside the apply kernel
+    C5F_ENTRY("c5_fused_64x16_q6_i8", 6, kLlrI8, 5, 2),  // C5 default: setup warp group inside the apply kernel
+    C5F_ENTRY("c5_fused3_64x16_q6_i8", 6, kLlrI8, 4, 3),  // 3 accumulators / B sets, 4 y stages, narrow setup
     C5_ENTRY("c5_bf16_tcs_be_64x16_q6_i8", 6, kLlrI8, 6, 4, 3, 2, true),  // two kernels: tensor-core setup + apply
     C5_ENTRY("c5_bf16kc_tcs_be_64x16_q6_i8", 6, kLlrI8, 6, 4, 4, 2, true),
     C5_ENTRY("c5_bf16_tcs_64x16_q6_i8", 6, kLlrI8, 6, 4, 3, 2, false),

@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 SMALL = {3: dict(n_sc=96, n_slots=1), 4: dict(n_sc=48, n_slots=1), 5: dict(n_sc=48, n_slots=1)}
 TYPE_MAX = {"i8": 127, "f16": 65504.0, "f32": np.finfo(np.float32).max}
 # (config, kernel): the default kernel of C3 / C4 / C5, plus every C5 setup route
-CASES = [(3, None), (4, None), (5, None), (5, "c5_bf16_tcs_be_64x16_q6_i8"), (5, "c5_bf16_gj_64x16_q6_i8"),
+CASES = [(3, None), (4, None), (5, None), (5, "c5_fused3_64x16_q6_i8"), (5, "c5_bf16_tcs_be_64x16_q6_i8"), (5, "c5_bf16_gj_64x16_q6_i8"),
          (5, "c5_bf16_chol_64x16_q6_i8"), (5, "c5_tf32_gj_64x16_q6_i8")]
 
 

@@ -35,11 +35,12 @@ def wait(b, idx):
         raise ABA(f"released at {b.phases} completions while waiting for completion #{idx}")
 
 
-def apply_roles(n_my, S, NLO, bepi=True):
+def apply_roles(n_my, S, NLO, bepi=True, nacc=2):
+    """nacc: accumulators = B sets (unit i uses slot i % nacc); the W~ staging ring stays 2 deep."""
     B = lambda c=1: Barrier(c)
     yfull, yfree = [B() for _ in range(S)], [B() for _ in range(S)]
     afull, afree = [B() for _ in range(NLO)], [B() for _ in range(NLO)]
-    bready, accfull, tfree = [B() for _ in range(2)], [B() for _ in range(2)], [B() for _ in range(2)]
+    bready, accfull, tfree = [B() for _ in range(nacc)], [B() for _ in range(nacc)], [B() for _ in range(nacc)]
     wfull, wfree = [B() for _ in range(2)], [B() for _ in range(2)]
     G = 4 * n_my
 
@@ -66,10 +67,10 @@ def apply_roles(n_my, S, NLO, bepi=True):
 
     def mma():
         for i in range(n_my):
-            b = i & 1
-            yield from wait(bready[b], i >> 1)
-            if i >= 2:
-                yield from wait(tfree[b], (i >> 1) - 1)
+            b = i % nacc
+            yield from wait(bready[b], i // nacc)
+            if i >= nacc:
+                yield from wait(tfree[b], i // nacc - 1)
             for c in range(4):
                 gg = 4 * i + c
                 lb = gg % NLO
@@ -84,13 +85,13 @@ def apply_roles(n_my, S, NLO, bepi=True):
 
     def converters():
         for i in range(n_my):
-            b = i & 1
+            b = i % nacc
             if not bepi:
-                if i >= 2:
-                    yield from wait(accfull[b], (i >> 1) - 1)
+                if i >= nacc:
+                    yield from wait(accfull[b], i // nacc - 1)
                 yield from build_b(i)
                 bready[b].arrive()
-                wfree[b].arrive()
+                wfree[i & 1].arrive()
             for c in range(4):
                 gg = 4 * i + c
                 st, lb = gg % S, gg % NLO
@@ -107,20 +108,19 @@ def apply_roles(n_my, S, NLO, bepi=True):
         if bepi:
             for i0 in range(min(2, n_my)):
                 stage_w(i0)
-            for i0 in range(min(2, n_my)):
-                yield from build_b(i0)
-            for i0 in range(min(2, n_my)):
-                bready[i0].arrive()
-            for i0 in range(2, min(4, n_my)):
-                stage_w(i0)
+            for j in range(min(nacc, n_my)):
+                yield from build_b(j)
+                bready[j].arrive()
+                if j + 2 < n_my:
+                    stage_w(j + 2)
         for i in range(n_my):
-            b = i & 1
-            yield from wait(accfull[b], i >> 1)
-            if bepi and i + 2 < n_my:
-                yield from build_b(i + 2)
+            b = i % nacc
+            yield from wait(accfull[b], i // nacc)
+            if bepi and i + nacc < n_my:
+                yield from build_b(i + nacc)
                 bready[b].arrive()
-                if i + 4 < n_my:
-                    stage_w(i + 4)
+                if i + nacc + 2 < n_my:
+                    stage_w(i + nacc + 2)
             tfree[b].arrive()
             yield "step"
 
@@ -149,10 +149,10 @@ def run(roles, max_rounds=200000):
 
 
 @pytest.mark.parametrize("S,NLO", [(6, 4), (4, 2), (8, 4), (7, 4), (5, 2)])
-@pytest.mark.parametrize("bepi", [True, False])
+@pytest.mark.parametrize("bepi,nacc", [(True, 2), (False, 2), (True, 3)])
 @pytest.mark.parametrize("n_my", [0, 1, 2, 3, 4, 5, 7, 8, 9, 13, 74])
-def test_apply_protocol_no_deadlock_no_aba(S, NLO, bepi, n_my):
-    assert run(apply_roles(n_my, S, NLO, bepi)), "protocol deadlocks"
+def test_apply_protocol_no_deadlock_no_aba(S, NLO, bepi, nacc, n_my):
+    assert run(apply_roles(n_my, S, NLO, bepi, nacc)), "protocol deadlocks"
 
 
 def test_model_detects_a_two_phase_runaway():

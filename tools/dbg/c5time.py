@@ -4,7 +4,7 @@ sys.path.insert(0, '.')
 from paper_2510_07843_b200 import mimo, synth
 mimo.load_library(os.environ['PROFLIB'])
 w = synth.generate(5)
-p = mimo.Plan(64, 16, 6, sc_per_h=12, llr_dtype="i8")
+p = mimo.Plan(64, 16, 6, sc_per_h=12, llr_dtype="i8", kernel=(sys.argv[1] if len(sys.argv) > 1 else None))
 sets = [(torch.from_numpy(w.H).cuda(), torch.from_numpy(w.y).cuda(),
          torch.empty(p.shapes(w.n_sc, w.n_sym)["llr"], dtype=torch.int8, device="cuda")) for _ in range(2)]
 for H, y, o in sets * 3:
