@@ -9,8 +9,9 @@ od=tools/dbg/obj$2
 mkdir -p $od
 for f in $C/*.cu; do
   o=$od/$(basename $f .cu).o
-  if [ "$(basename $f)" = "k_c5.cu" ]; then extra="$PROFDEF $1"; else extra=; fi
-  if [ "$(basename $f)" != "k_c5.cu" ] && [ -f tools/dbg/obj/$(basename $f .cu).o ] && [ "$od" != "tools/dbg/obj" ]; then cp tools/dbg/obj/$(basename $f .cu).o $o; continue; fi
+  tgt=${PROFFILE:-k_c5.cu}  # the file the extra flags apply to
+  if [ "$(basename $f)" = "$tgt" ]; then extra="$PROFDEF $1"; else extra=; fi
+  if [ "$(basename $f)" != "$tgt" ] && [ -f tools/dbg/obj/$(basename $f .cu).o ] && [ "$od" != "tools/dbg/obj" ]; then cp tools/dbg/obj/$(basename $f .cu).o $o; continue; fi
   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -Iinclude -I$C $extra -c $f -o $o &
 done
 wait
