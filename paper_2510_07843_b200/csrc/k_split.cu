@@ -545,8 +545,6 @@ cudaError_t launch(const DetectArgs& a, cudaStream_t s) {
 
 const KernelEntry kEntries[] = {
     STREAM_ENTRY_B("stream_8x4_q6_i8", 8, 4, 6, kLlrI8, 12, 16, 2, 2, 4),  // C3: <= 128 regs -> 4 CTAs/SM
-    STREAM_ENTRY_B("stream_8x4_q6_i8_g3", 8, 4, 6, kLlrI8, 12, 16, 3, 2, 4),
-    STREAM_ENTRY_B("stream_8x4_q6_i8_g4", 8, 4, 6, kLlrI8, 12, 16, 4, 2, 4),
     SPLIT_ENTRY("split_8x4_q6_i8", 8, 4, 6, kLlrI8, 12, 32, 7),
     SPLIT_ENTRY("split_8x4_q6_f32", 8, 4, 6, kLlrF32, 12, 32, 7),
     SPLIT_ENTRY("split_8x4_q6_f16", 8, 4, 6, kLlrF16, 12, 32, 7),

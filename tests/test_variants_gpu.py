@@ -14,7 +14,7 @@ C5_VARIANTS = ["c5_fused_64x16_q6_i8", "c5_fused3_64x16_q6_i8", "c5_bf16_tcs_be_
                "c5_bf16_tcs_64x16_q6_i8", "c5_bf16_gj_64x16_q6_i8", "c5_bf16_chol_64x16_q6_i8", "c5_tf32_gj_64x16_q6_i8",
                "big_64x16_q6_i8"]
 C4_VARIANTS = ["lg3hl_16x8_q8_f16", "lg3hl2_16x8_q8_f16", "lg3hq_16x8_q8_f16", "lg3hp_16x8_q8_f16", "lg3_16x8_q8_f16", "lg_16x8_q8_f16"]
-C3_VARIANTS = ["stream_8x4_q6_i8", "stream_8x4_q6_i8_g3", "stream_8x4_q6_i8_g4", "split_8x4_q6_i8", "prb_8x4_q6_i8"]
+C3_VARIANTS = ["stream_8x4_q6_i8", "split_8x4_q6_i8", "prb_8x4_q6_i8"]
 
 
 def _forced(monkeypatch, name, w, **kw):
