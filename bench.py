@@ -74,7 +74,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU budget of the oracle baseline")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no graphs, no e2e/cpu legs)")
     ap.add_argument("--bfp", type=int, default=0,
-                    help="NEXT-4: feed y as W-bit block-floating-point (mimo_detect_mmse_bfp; C3 shape only)")
+                    help="NEXT-4: feed y as W-bit block-floating-point (mimo_detect_mmse_bfp: decoded in the C3 apply "
+                         "loads, expanded by k_bfp_decode for the other shapes)")
     ap.add_argument("--overlap", type=int, default=1,
                     help="1: back-to-back calls overlap via PDL (MIMO_PLAN_OVERLAP_CALLS); 0: serialised")
     return ap.parse_args()
@@ -557,7 +558,8 @@ def run_ours(args, k):
     cfg = workload_desc(k)
     cfg.update({"l2_flush": f"{sh.n_sets} rotating buffer sets x {b['total'] / 1e6:.1f} MB = "
                             f"{sh.n_sets * b['total'] / 1e6:.0f} MB > 3x L2 ({sh.l2 / 1e6:.0f} MB)",
-                "graph_steps": S, "kernel": plan.kernel_name + (f" + BFP{args.bfp} y (k_apply_bfp)" if ybfp is not None else ""),
+                "graph_steps": S, "kernel": plan.kernel_name + ((f" + BFP{args.bfp} y (k_apply_bfp)" if k == 3 else f" + BFP{args.bfp} y (k_bfp_decode)")
+                                              if ybfp is not None else ""),
                 "y_format": f"BFP {args.bfp}-bit mantissas, block per (symbol, PRB, antenna) (reading R25)"
                             if ybfp is not None else "complex64",
                 "call_overlap": "PDL (MIMO_PLAN_OVERLAP_CALLS): call i+1 loads/sets up while call i stores"

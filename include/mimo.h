@@ -228,10 +228,12 @@ mimo_status_t mimo_detect_irc(mimo_plan_t plan, const void* H, const void* y, co
  *   then the 24 two's-complement iq_width-bit mantissas I0,Q0,...,I11,Q11 of the
  *   PRB's 12 subcarriers, packed MSB-first; value = m * 2^e * bfp_scale.
  *   y_bfp: DEVICE bytes [n_sym][n_sc/12][n_rx][block_bytes], 16-byte aligned.
- * iq_width in 8..16; bfp_scale finite > 0. Everything else as mimo_detect_mmse_ex.
- * Supported for n_rx = 8, n_layers = 4, sc_per_h = 12, sym_per_h = 14 (the C3
- * family; else MIMO_ERR_UNSUPPORTED). Asynchronous. Errors: INVALID_ARG,
- * UNSUPPORTED, CUDA, OOM (workspace). */
+ * iq_width in 8..16; bfp_scale finite > 0; n_sc a multiple of 12. Everything else as
+ * mimo_detect_mmse_ex. For n_rx = 8, n_layers = 4, sc_per_h = 12, sym_per_h = 14 (the C3
+ * family) the decode is fused into the apply kernel's y loads; every other shape has the blocks
+ * expanded by one kernel into a plan-owned complex64 y buffer (n_sym * n_sc * n_rx * 8 bytes,
+ * grown by a call outside graph capture) that the shape's detector then reads. Asynchronous.
+ * Errors: INVALID_ARG, CUDA, OOM (workspace / y buffer). */
 mimo_status_t mimo_detect_mmse_bfp(mimo_plan_t plan, const void* H, const void* y_bfp, float sigma2,
                                    int n_rx, int n_layers, int n_sc, int n_sym, int qam_order,
                                    int iq_width, float bfp_scale,
@@ -242,9 +244,10 @@ mimo_status_t mimo_detect_mmse_bfp(mimo_plan_t plan, const void* H, const void* 
  * slot-chunk pipeline as mimo_detect_mmse_host / _host_async (H and the compressed y cross PCIe,
  * are decompressed inside the apply kernel's loads, LLRs come back). This is where the fronthaul
  * format pays: y crosses the host link at 28 B instead of 96 B per (symbol, PRB, antenna) at
- * iq_width 9 (D-MIMO fronthaul). Same support and errors as mimo_detect_mmse_bfp
- * plus those of mimo_detect_mmse_host; the _async form returns after enqueuing (synchronise with
- * mimo_plan_sync_status). */
+ * iq_width 9 (D-MIMO fronthaul). Every shape: the C3 family decodes in its apply
+ * loads, the others expand each chunk's blocks into the chunk's complex64 y buffer on the kernel
+ * stream. Errors as mimo_detect_mmse_bfp plus those of mimo_detect_mmse_host; the _async form
+ * returns after enqueuing (synchronise with mimo_plan_sync_status). */
 mimo_status_t mimo_detect_mmse_bfp_host(mimo_plan_t plan, const void* H_host, const void* y_bfp_host, float sigma2,
                                         int n_rx, int n_layers, int n_sc, int n_sym, int qam_order, int iq_width,
                                         float bfp_scale, void* llr_host);

@@ -66,6 +66,9 @@ bool irc_supported(int n_rx, int n_layers);
 bool bfp_supported(int n_rx, int n_layers, int sc_per_h, int sym_per_h);
 size_t bfp_workspace(const DetectArgs& a);
 cudaError_t launch_bfp(const DetectArgs& a, const void* y_bfp, int iq_width, float scale, cudaStream_t s);
+// Any shape: BFP blocks [n_sym][n_sc/12][n_rx][block] -> complex64 y [n_sym][n_sc][n_rx] (k_bfp.cu).
+cudaError_t launch_bfp_decode(const void* y_bfp, float2* y, int n_rx, int n_sc, int n_sym, int iq_width, float scale,
+                              cudaStream_t s);
 cudaError_t launch_irc(const DetectArgs& a, const float2* Rnn, cudaStream_t s);
 size_t lu_route_workspace(int n_rx, long long n_units, int precision_bits);
 cudaError_t launch_lu_route(const DetectArgs& a, int precision_bits, cudaStream_t s, cudaEvent_t* ev);

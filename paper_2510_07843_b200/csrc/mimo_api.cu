@@ -44,11 +44,14 @@ struct mimo_plan_s {
     cudaStream_t hs[3] = {nullptr, nullptr, nullptr};  // H2D, kernels, D2H
     cudaEvent_t ev = nullptr;
     unsigned long long host_chunk = 0;  // host-path buffer ring position
-    size_t host_bh = 0, host_by = 0, host_bl = 0;  // host-path buffer layout of the ring in use
+    size_t host_bh = 0, host_by = 0, host_bd = 0, host_bl = 0;  // host-path buffer layout of the ring in use
     cudaEvent_t e_in[kNB] = {}, e_k[kNB] = {}, e_out[kNB] = {};
     // kernel workspaces: slot 0 for the plan's stream, 1..2 for the host path's streams
     void* kws[3] = {nullptr, nullptr, nullptr};
     size_t kws_bytes[3] = {0, 0, 0};
+    // BFP y on shapes without the fused decode: the expanded complex64 y (mimo_detect_mmse_bfp)
+    void* ydec = nullptr;
+    size_t ydec_bytes = 0;
     // paper-literal LU route (mimo_detect_lmmse_lu)
     void* lu_ws = nullptr;
     size_t lu_ws_bytes = 0;
@@ -351,13 +354,14 @@ static mimo_status_t host_path(mimo_plan_t p, const void* H_host, const void* y_
     if (!p) return arg_fail(nullptr, "null plan");
     mimo_status_t st = check_dims(p, sigma2, n_rx, n_layers, n_sc, n_sym, qm);
     if (st != MIMO_OK) return st;
+    // BFP y: decoded inside the apply loads (8 rx x 4 layers per PRB) or expanded by k_bfp_decode into
+    // the chunk's complex64 y buffer (every other shape)
+    bool bfp_fused = false;
     if (bfp.iq_width) {
         if (bfp.iq_width < 8 || bfp.iq_width > 16) return arg_fail(p, "iq_width must be in 8..16");
         if (!(bfp.scale > 0.f) || !std::isfinite(bfp.scale)) return arg_fail(p, "bfp_scale must be finite > 0");
-        if (!mimo::bfp_supported(n_rx, n_layers, p->d.sc_per_h, p->d.sym_per_h)) {
-            snprintf(p->err, sizeof(p->err), "BFP route: supported for 8 rx x 4 layers, H per PRB, 14 symbols");
-            return MIMO_ERR_UNSUPPORTED;
-        }
+        if (n_sc % 12) return arg_fail(p, "BFP y: n_sc must be a multiple of 12 (one block per PRB)");
+        bfp_fused = mimo::bfp_supported(n_rx, n_layers, p->d.sc_per_h, p->d.sym_per_h);
     }
     if ((long long)n_sc * n_sym == 0) return MIMO_OK;
     if (!H_host || !y_host || !llr_host) return arg_fail(p, "null host buffer");
@@ -384,7 +388,8 @@ static mimo_status_t host_path(mimo_plan_t p, const void* H_host, const void* y_
     if (cs > n_slots) cs = n_slots;
     auto up = [](size_t b) { return (b + 255) & ~(size_t)255; };
     const size_t bh = up(h_slot * cs), by = up(y_slot * cs), bl = up(l_slot * cs);
-    const size_t need = NB * (bh + by + bl);
+    const size_t bd = (bfp.iq_width && !bfp_fused) ? up((size_t)symph * n_sc * n_rx * 8 * cs) : 0;
+    const size_t need = NB * (bh + by + bd + bl);
     cudaError_t e;
     for (int i = 0; i < 3; ++i)
         if (!p->hs[i] && (e = cudaStreamCreateWithFlags(&p->hs[i], cudaStreamNonBlocking)) != cudaSuccess)
@@ -403,12 +408,13 @@ static mimo_status_t host_path(mimo_plan_t p, const void* H_host, const void* y_
     // layout: when it changes (other chunk size or call shape), drain every pending use of the
     // old layout and restart the ring before any buffer is reused (an earlier asynchronous call
     // may still be copying into / out of the region a new layout would overlap).
-    if (bh != p->host_bh || by != p->host_by || bl != p->host_bl) {
+    if (bh != p->host_bh || by != p->host_by || bd != p->host_bd || bl != p->host_bl) {
         for (int i = 0; i < 3; ++i)
             if ((e = cudaStreamSynchronize(p->hs[i])) != cudaSuccess) return cuda_fail(p, e, "cudaStreamSynchronize");
         p->host_chunk = 0;
         p->host_bh = bh;
         p->host_by = by;
+        p->host_bd = bd;
         p->host_bl = bl;
     }
     if (p->ws_bytes < need) {
@@ -431,8 +437,8 @@ static mimo_status_t host_path(mimo_plan_t p, const void* H_host, const void* y_
     for (int s0 = 0; s0 < n_slots; s0 += cs, ++chunk) {
         const int ns = (n_slots - s0) < cs ? (n_slots - s0) : cs;
         const int b = (int)(p->host_chunk++ % NB);  // the ring continues across (asynchronous) calls
-        char* base = p->ws + (size_t)b * (bh + by + bl);
-        char *dH = base, *dy = base + bh, *dl = base + bh + by;
+        char* base = p->ws + (size_t)b * (bh + by + bd + bl);
+        char *dH = base, *dy = base + bh, *dd = base + bh + by, *dl = base + bh + by + bd;
         // buffer b's previous use (this call's chunk - NB, or a previous asynchronous call's chunk) is
         // over: its inputs consumed / its outputs drained (waiting on a never-recorded event is a no-op)
         cudaStreamWaitEvent(s_in, p->e_k[b], 0);
@@ -443,9 +449,16 @@ static mimo_status_t host_path(mimo_plan_t p, const void* H_host, const void* y_
         if (e != cudaSuccess) return cuda_fail(p, e, "cudaMemcpyAsync H2D");
         cudaStreamWaitEvent(s_k, p->e_in[b], 0);
         cudaStreamWaitEvent(s_k, p->e_out[b], 0);
-        mimo::DetectArgs a = make_args(p, dH, bfp.iq_width ? nullptr : dy, sigma2, n_sc, ns * symph, dl, nullptr, nullptr);
+        mimo::DetectArgs a = make_args(p, dH, !bfp.iq_width ? dy : bfp_fused ? nullptr : dd, sigma2, n_sc, ns * symph,
+                                       dl, nullptr, nullptr);
         a.overlap = 0;
-        if (bfp.iq_width) {
+        if (bfp.iq_width && !bfp_fused) {
+            if ((e = mimo::launch_bfp_decode(dy, reinterpret_cast<float2*>(dd), n_rx, n_sc, ns * symph, bfp.iq_width,
+                                             bfp.scale, s_k)) != cudaSuccess)
+                return cuda_fail(p, e, "BFP decode");
+            st = launch(p, a, s_k, 1);
+            if (st != MIMO_OK) return st;
+        } else if (bfp.iq_width) {
             st = ensure_ws(p, 1, mimo::bfp_workspace(a), s_k);
             if (st != MIMO_OK) return st;
             a.ws = p->kws[1];
@@ -595,10 +608,8 @@ mimo_status_t mimo_detect_mmse_bfp(mimo_plan_t p, const void* H, const void* y_b
     if (st != MIMO_OK) return st;
     if (iq_width < 8 || iq_width > 16) return arg_fail(p, "iq_width must be in 8..16");
     if (!(bfp_scale > 0.f) || !std::isfinite(bfp_scale)) return arg_fail(p, "bfp_scale must be finite > 0");
-    if (!mimo::bfp_supported(n_rx, n_layers, p->d.sc_per_h, p->d.sym_per_h)) {
-        snprintf(p->err, sizeof(p->err), "BFP route: supported for 8 rx x 4 layers, H per PRB, 14 symbols");
-        return MIMO_ERR_UNSUPPORTED;
-    }
+    if (n_sc % 12) return arg_fail(p, "BFP y: n_sc must be a multiple of 12 (one block per PRB)");
+    const bool fused = mimo::bfp_supported(n_rx, n_layers, p->d.sc_per_h, p->d.sym_per_h);
     if ((long long)n_sc * n_sym == 0) return MIMO_OK;
     if (!H || !y_bfp) return arg_fail(p, "null H or y_bfp");
     if (!llr_out && !xhat_out && !sinr_out) return arg_fail(p, "no output requested");
@@ -611,6 +622,26 @@ mimo_status_t mimo_detect_mmse_bfp(mimo_plan_t p, const void* H, const void* y_b
         return arg_fail(p, "pointer is not device memory on the plan's device");
     DeviceGuard g(dev);
     if (g.err != cudaSuccess) return cuda_fail(p, g.err, "cudaSetDevice");
+    if (!fused) {  // expand into the plan's complex64 y buffer, then the shape's detector
+        const size_t need = (size_t)n_sym * n_sc * n_rx * 8;
+        if (p->ydec_bytes < need) {
+            cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+            if (p->stream) cudaStreamIsCapturing(p->stream, &cs);
+            if (cs != cudaStreamCaptureStatusNone)
+                return arg_fail(p, "BFP y buffer too small while capturing a graph: make one call before capturing");
+            cudaError_t e = cudaStreamSynchronize(p->stream);
+            if (e != cudaSuccess) return cuda_fail(p, e, "cudaStreamSynchronize");
+            cudaFree(p->ydec);
+            p->ydec = nullptr;
+            p->ydec_bytes = 0;
+            if ((e = cudaMalloc(&p->ydec, need)) != cudaSuccess) return cuda_fail(p, e, "cudaMalloc(BFP y buffer)");
+            p->ydec_bytes = need;
+        }
+        cudaError_t e = mimo::launch_bfp_decode(y_bfp, static_cast<float2*>(p->ydec), n_rx, n_sc, n_sym, iq_width,
+                                                bfp_scale, p->stream);
+        if (e != cudaSuccess) return cuda_fail(p, e, "BFP decode");
+        return launch(p, make_args(p, H, p->ydec, sigma2, n_sc, n_sym, llr_out, xhat_out, sinr_out), p->stream);
+    }
     mimo::DetectArgs a = make_args(p, H, nullptr, sigma2, n_sc, n_sym, llr_out, xhat_out, sinr_out);
     st = ensure_ws(p, 0, mimo::bfp_workspace(a), p->stream);
     if (st != MIMO_OK) return st;
@@ -667,6 +698,7 @@ mimo_status_t mimo_plan_destroy(mimo_plan_t p) {
         }
         if (p->ws) cudaFree(p->ws);
         if (p->lu_ws) cudaFree(p->lu_ws);
+        if (p->ydec) cudaFree(p->ydec);
         for (int i = 0; i <= MIMO_LU_STAGES; ++i)
             if (p->lu_ev[i]) cudaEventDestroy(p->lu_ev[i]);
         for (int i = 0; i < 3; ++i)

@@ -50,13 +50,45 @@ def test_bfp_full_size_sampled():
     print(parity.compare(w, g, units, y=decoded_y(w, 9)))
 
 
-def test_bfp_unsupported_shape():
+@pytest.mark.parametrize("k,kw", [(2, dict(n_sc=96, n_slots=2)), (4, dict(n_sc=48, n_slots=1)),
+                                  (5, dict(n_sc=48, n_slots=1)), (1, {})])
+def test_bfp_other_shapes_equal_detect_on_decoded_y(k, kw):
+    """Shapes without the fused decode: k_bfp_decode expands the blocks, then the shape's detector
+    runs. The LLRs are BIT-identical to the detector on the oracle's decode of the same bytes (which
+    pins the decode kernel bit-exactly), and within the north_star tolerances of the oracle."""
+    w = synth.generate(k, **kw)
+    if w.n_sc % 12:
+        pytest.skip("BFP blocks are per PRB")
+    g = run_bfp(w, 9)
+    yd = decoded_y(w, 9)
+    ref = parity.run_gpu(w, y=yd)
+    assert g["n_failed"] == 0
+    assert np.array_equal(g["llr"], ref["llr"])
+    assert np.array_equal(g["xhat"], ref["xhat"])
+    parity.compare(w, g, y=yd)
+
+
+def test_bfp_ragged_n_sc_rejected():
     p = mimo.Plan(4, 4, 4)
     w = synth.generate(2, n_sc=24, n_slots=1)
-    yb = torch.zeros((w.n_sym, 2, 4, 28), dtype=torch.uint8, device="cuda")
+    yb = torch.zeros((w.n_sym, 1, 4, 28), dtype=torch.uint8, device="cuda")
     with pytest.raises(mimo.MimoError) as e:
-        p.detect_bfp(torch.from_numpy(w.H).cuda(), yb, float(w.sigma2), n_sym=w.n_sym, n_sc=24)
-    assert e.value.status == mimo.MIMO_ERR_UNSUPPORTED
+        p.detect_bfp(torch.from_numpy(np.ascontiguousarray(w.H[:, :20])).cuda(), yb, float(w.sigma2), n_sym=w.n_sym,
+                     n_sc=20)
+    assert e.value.status == mimo.MIMO_ERR_INVALID_ARG
+
+
+def test_bfp_host_path_other_shape_bit_identical():
+    """The host path with per-chunk expansion (C5 shape) equals the device BFP call bit for bit."""
+    w = synth.generate(5, n_sc=48, n_slots=3)
+    ref = run_bfp(w, 9, xhat=False)["llr"]
+    p = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, llr_dtype=w.llr, host_chunk_bytes=200_000)
+    yb = torch.from_numpy(synth.bfp_compress(w.y, 9, SCALE)).pin_memory()
+    out = torch.empty(ref.shape, dtype=torch.int8).pin_memory()
+    p.detect_bfp_host(torch.from_numpy(w.H).pin_memory(), yb, float(w.sigma2), n_sym=w.n_sym, n_sc=w.n_sc,
+                      iq_width=9, bfp_scale=SCALE, out=out, wait=True)
+    assert p.sync_status() == 0
+    assert np.array_equal(out.numpy(), ref)
 
 
 @pytest.mark.parametrize("wait", [True, False])
