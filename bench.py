@@ -136,6 +136,7 @@ class ClockSampler:
 
     def __init__(self, torch_index: int, period: float = 0.05):
         self.samples, self.reasons, self.ok = [], set(), False
+        self.power, self.power_limit = [], None
         self.period = period
         self._stop = threading.Event()
         try:
@@ -154,6 +155,10 @@ class ClockSampler:
                 h = pynvml.nvmlDeviceGetHandleByIndex(torch_index)
             self.h, self.nvml = h, pynvml
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            try:
+                self.power_limit = pynvml.nvmlDeviceGetEnforcedPowerLimit(h) / 1000.0
+            except Exception:
+                self.power_limit = None
             self.ok = True
         except Exception as e:  # no NVML: report nothing rather than guess
             self.err = repr(e)
@@ -164,6 +169,10 @@ class ClockSampler:
         while not self._stop.is_set():
             try:
                 self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                try:
+                    self.power.append(nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0)
+                except Exception:
+                    pass
                 r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h) \
                     if hasattr(nv, "nvmlDeviceGetCurrentClocksEventReasons") \
                     else nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
@@ -188,8 +197,12 @@ class ClockSampler:
     def result(self) -> dict:
         if not self.ok or not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "note": "NVML unavailable"}
-        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
-                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        r = {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+             "reasons": sorted(self.reasons), "samples": len(self.samples)}
+        if self.power:  # board power under load vs the enforced limit (sw_power_cap = at the limit)
+            r["power_w"] = round(float(statistics.median(self.power)), 1)
+            r["power_limit_w"] = self.power_limit
+        return r
 
 
 # ------------------------------------------------------------ oracle legs --

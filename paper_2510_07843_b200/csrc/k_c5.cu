@@ -68,7 +68,7 @@ extern "C" int mimo_c5_sprof_read(unsigned long long* host) {
 namespace mimo {
 namespace {
 
-template <int S_, int NLO_, int TA_, bool FUSED_ = false, int NB_ = 2>
+template <int S_, int NLO_, int TA_, bool FUSED_ = false, int NB_ = 2, bool BI_ = false>
 struct C5Smem {
     static constexpr int S = S_;                              // y stages
     static constexpr int NLO = NLO_;                          // TMEM A ring slots (chunks)
@@ -79,7 +79,7 @@ struct C5Smem {
     static constexpr size_t slope = B + NB_ * bset;           // [8][16] slope | [8][16] sqrt(slope / 127)
     static constexpr size_t wst = slope + 1024;               // [2] W~ workspace records staged by TMA
     static constexpr size_t wrec = (size_t)BigWs<64, 16>::stride * 4;
-    static constexpr size_t setup = (wst + 2 * wrec + 1023) / 1024 * 1024;  // FUSED: the setup group's 64 KiB
+    static constexpr size_t setup = (wst + (BI_ ? 0 : 2 * wrec) + 1023) / 1024 * 1024;  // FUSED: the setup group's 64 KiB
     static constexpr size_t bars = setup + (FUSED_ ? 65536 : 0);
     static constexpr int NBAR = 2 * S + 2 * NLO + NB_ * 3 + 4 + 2;  // yfull, yfree | afull, afree | bready, accfull, tfree | wfull, wfree | setup tma, mma
     static constexpr size_t ready = bars + NBAR * 8;           // FUSED: [0] units whose W~ records are written,
@@ -146,6 +146,30 @@ __device__ __forceinline__ void demap_axis_i8(float u, float rs, uint32_t* q, in
 // coupled the two and cost 15 us per C5 step; 16 are as fast as one record per unit and 4.6x smaller)
 constexpr int kC5Ring = 16;
 constexpr int kSetupConvUnroll = 2;  // 4 and 8 measured slower
+// B-image records (the `bi` fused kernel): the setup group writes each unit's apply B operand itself -- the
+// bf16 hi / lo split of the real form of W~, MN-major SWIZZLE_128B, K = 128 rows of 128 B -- followed by the
+// 16 slopes and the 16 sqrt(slope / 127); the apply bulk-copies it straight into its B set (no B build)
+constexpr int kBiImg = 128 * 128;
+constexpr int kBiRec = kBiImg + 128;
+
+// K row R of a B image from 32 words (8 chunks of 16 B: hi pairs n 0..31, then lo), SWIZZLE_128B positions
+// (chunk q of row R at q ^ (R & 7)), as four 32-byte stores of chunk pairs; ODD = R & 1 (an odd row puts
+// chunk q0 + 1 before chunk q0)
+template <bool ODD>
+__device__ __forceinline__ void bi_store_row(char* img, int R, const uint32_t* w) {
+    const int sw = R & 7;
+#pragma unroll
+    for (int qp = 0; qp < 4; ++qp) {
+        const int q0 = 2 * qp, p = q0 ^ sw;
+        uint32_t o[8];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            o[e] = ODD ? w[4 * (q0 + 1) + e] : w[4 * q0 + e];
+            o[4 + e] = ODD ? w[4 * q0 + e] : w[4 * (q0 + 1) + e];
+        }
+        st_v8(img + R * 128 + ((p & ~1) << 4), o);
+    }
+}
 
 namespace su {
 constexpr int UPB = 4;                   // units per batch (= warps)
@@ -191,7 +215,7 @@ __device__ __forceinline__ void setup_issue_h(const CUtensorMap* hmapp, uint32_t
 // rec_of(s) = the workspace record (W~ + slopes) of batch slot s: the unit itself, or (fused) a slot of
 // the CTA's ring of records, which ring_wait() (called by every thread before the batch's first record
 // write) makes sure the apply has finished reading.
-template <int QM, bool PUB, bool WIDE, typename UnitF, typename SyncF, typename NextF, typename PubF, typename RecF,
+template <int QM, bool PUB, bool WIDE, bool BI, typename UnitF, typename SyncF, typename NextF, typename PubF, typename RecF,
           typename RingF>
 __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorMap* hmapp, unsigned char* g,
                                             uint32_t gaddr, uint64_t* bar_tma, uint64_t* bar_mma, uint32_t tmem,
@@ -297,7 +321,11 @@ __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorM
             pdl_wait();
             waited = true;
         }
+        PROF_ADD(prof, 8, p4);
+        PROF_T(p4r);
         ring_wait();
+        PROF_ADD(prof, 9, p4r);
+        PROF_T(p4g);
         {
             const int s = gw, k = lane >> 1, h = lane & 1;
             const bool valid = s < nv;
@@ -377,6 +405,8 @@ __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorM
                     }
                 }
             }
+            PROF_ADD(prof, 10, p4g);
+            PROF_T(p4b);
             // A_kk = [G^-1]_kk lives in lane (k, k / 8)
             float Ad = 0.f;
 #pragma unroll
@@ -420,15 +450,25 @@ __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorM
                 }
             }
             if (valid && h == 0) {
-                float* wsu = reinterpret_cast<float*>(a.ws) + rec_of(s) * WS;
-                wsu[NR * NL * 2 + k] = sinr / norm * a.llr_scale;
+                if constexpr (BI) {  // B-image record: slopes and sqrt(slope / 127) after the 16-KiB image
+                    float* wsu = reinterpret_cast<float*>(reinterpret_cast<char*>(a.ws) + rec_of(s) * kBiRec + kBiImg);
+                    const float slv = sinr / norm * a.llr_scale;
+                    wsu[k] = slv;
+                    wsu[16 + k] = sqrtf(slv * (1.f / 127.f));
+                } else {
+                    float* wsu = reinterpret_cast<float*>(a.ws) + rec_of(s) * WS;
+                    wsu[NR * NL * 2 + k] = sinr / norm * a.llr_scale;
+                }
                 if (a.sinr) a.sinr[u * NL + k] = sinr;
                 if (k == 0 && fail) atomicAdd(a.fail_count, 1ull);
             }
+            PROF_ADD(prof, 11, p4b);
         }
         tc::fence_proxy_async();
         tc::fence_before();
+        PROF_T(p4s);
         sync();
+        PROF_ADD(prof, 12, p4s);
         PROF_ADD(prof, 4, p4);
         PROF_T(p5);
         // ---- a4: W~^T = XB B'^T (K-major view of XB: K = 64 = hi | lo halves)
@@ -469,7 +509,25 @@ __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorM
                 tc::ld32(tmem + ((uint32_t)(32 * gw) << 16) + 32u * s, v);
                 tc::wait_ld();
             }
-            if (lane < 16) {
+            if (BI && lane < 16) {
+                // B image (MN-major SW128 bf16, K row = real input 2r | 2r + 1 of antenna r, 128 B = [hi n 0..31 |
+                // lo n 0..31]): K row 2r (x Re y_r) holds (Re W~_nr | Im W~_(n-16)r), K row 2r + 1 (x Im y_r)
+                // holds (-Im W~_nr | Re W~_(n-16)r) = row 2r's halves swapped, the first negated (RN split is odd)
+                const int r = 16 * gw + lane;
+                uint32_t w0[32], w1[32];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) tc::split_bf2(__uint_as_float(v[2 * j]), __uint_as_float(v[2 * j + 1]), w0[j], w0[16 + j]);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    w1[j] = w0[8 + j] ^ 0x80008000u;
+                    w1[16 + j] = w0[24 + j] ^ 0x80008000u;
+                    w1[8 + j] = w0[j];
+                    w1[24 + j] = w0[16 + j];
+                }
+                char* dst = reinterpret_cast<char*>(a.ws) + rec_of(s) * kBiRec;
+                bi_store_row<false>(dst, 2 * r, w0);
+                bi_store_row<true>(dst, 2 * r + 1, w1);
+            } else if (lane < 16) {
                 const int r = 16 * gw + lane;
                 uint32_t o[32];
 #pragma unroll
@@ -492,11 +550,12 @@ __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorM
 
 // NACC = accumulators in TMEM = B sets in shared memory: unit i uses slot i % NACC, and its MMAs wait
 // for the epilogue of unit i - NACC (and for B set i % NACC, built after unit i - NACC's MMAs).
-template <int QM, int LT, int EW, int S_, int NLO_, int TA, bool BEPI, bool FUSED, int NACC = 2>
+template <int QM, int LT, int EW, int S_, int NLO_, int TA, bool BEPI, bool FUSED, int NACC = 2, int BI = 0>
 __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
     k_c5_apply(DetectArgs a, const __grid_constant__ CUtensorMap ymap, const __grid_constant__ CUtensorMap hmap) {
     constexpr int NR = 64, NL = 16;
-    using SM = C5Smem<S_, NLO_, TA, FUSED, NACC>;
+    using SM = C5Smem<S_, NLO_, TA, FUSED, NACC, BI != 0>;
+    static_assert(!BI || (FUSED && TA == 4), "B-image records: fused kernel, single-accumulator bf16 split");
     constexpr int S = S_, NLO = NLO_;
     static_assert(EW == 6, "6 epilogue warps (4 for tile 0, 2 for the compact tile 1)");
 
@@ -639,7 +698,7 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
         for (long long j0 = 0; j0 < n_my; j0 += su::UPB, ++it) {
             const int nv = nv_of(j0);
             const long long jn = j0 + su::UPB;
-            setup_batch<QM, true, kWide>(a, &hmap, g + SM::setup, base + (uint32_t)SM::setup, stma, smma, tmem + kSetupCols, it,
+            setup_batch<QM, true, kWide, BI != 0>(a, &hmap, g + SM::setup, base + (uint32_t)SM::setup, stma, smma, tmem + kSetupCols, it,
                                   nv, gt, gw, lane, waited, [&](int s_) { return u0 + (j0 + s_) * du; },
                                   [] { asm volatile("bar.sync 5, 128;" ::: "memory"); },
                                   [&] {
@@ -653,7 +712,16 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                                   [&](int s_) { return rec_of(j0 + s_); },
                                   [&] {  // ring slots of units j0 .. j0 + nv - 1 held units j0 - kC5Ring ..: built?
                                       while (*units_built < (int)(j0 + nv - kC5Ring)) __nanosleep(32);
+                                      if constexpr (BI == 2) __threadfence_block();  // acquire: after the L2 discards
                                   });
+            if (j0 == 0 && nv < n_my) {
+                // the first batch is published at once (the others one batch late, see setup_batch): the apply
+                // pipeline idles until it is
+                __threadfence();
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                asm volatile("bar.sync 5, 128;" ::: "memory");
+                if (gt == 0) *units_ready = nv;
+            }
         }
         if (n_my > 0) {  // the last batch
             __threadfence();
@@ -666,7 +734,8 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
         // ================= MMA issuer =================
         if (lane == 0) {
             constexpr uint32_t f = TA == 1 ? tc::kFmtTF32 : tc::kFmtBF16;
-            constexpr uint32_t id64 = tc::idesc(f, 128, 64), id32 = tc::idesc(f, 128, 32);
+            // BI: B is the MN-major image (K row = real input, [hi n 0..31 | lo n 0..31])
+            constexpr uint32_t id64 = tc::idesc(f, 128, 64), id32 = tc::idesc(f, 128, 32, 0, BI ? 1 : 0);
             const uint64_t dB = tc::desc_sw128(base + (uint32_t)SM::B);
             PROF_DECL;
 #pragma unroll 1
@@ -704,8 +773,9 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                         for (int tile = 0; tile < 2; ++tile)
 #pragma unroll
                             for (int ks = 0; ks < 2; ++ks) {
-                                const uint64_t dk = tc::desc_add(db, (uint32_t)((c >> 1) * 8192 + (c & 1) * 64 + ks * 32));
-                                const uint64_t dkl = tc::desc_add(dk, 4096u);  // B_lo rows 32-63
+                                const uint64_t dk = BI ? tc::desc_add(db, (uint32_t)(c * 4096 + ks * 2048))
+                                                       : tc::desc_add(db, (uint32_t)((c >> 1) * 8192 + (c & 1) * 64 + ks * 32));
+                                const uint64_t dkl = tc::desc_add(dk, BI ? 64u : 4096u);  // B_lo (BI: the lo half of each K row)
                                 tc::mma_f16_ts(acc + 32u * tile, ab + 32u * tile + 8u * ks, dk, id32, (c | ks) ? 1u : 0u);
                                 tc::mma_f16_ts(acc + 32u * tile, ab + 32u * tile + 8u * ks, dkl, id32, 1u);
                                 tc::mma_f16_ts(acc + 32u * tile, ab + 32u * tile + 16u + 8u * ks, dk, id32, 1u);
@@ -776,12 +846,12 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                 else x[k] = make_float2(__uint_as_float(hv[k]) + __uint_as_float(lv[k]),
                                         __uint_as_float(hv[16 + k]) + __uint_as_float(lv[16 + k]));
             }
-            const float* sl = sslope + (i & 7) * 16;
+            const float* sl = sslope + (i & 7) * (BI ? 32 : 16);  // BI: [8][slope 16 | rs 16] (one copy per unit)
             if (a.llr) {
                 uint32_t wd[(kRec + 3) / 4];
                 if (LT == kLlrI8 && !zf) {
                     uint32_t q[NL * QM];
-                    const float* rs = sslope + 128 + (i & 7) * 16;
+                    const float* rs = BI ? sl + 16 : sslope + 128 + (i & 7) * 16;
 #pragma unroll
                     for (int k = 0; k < NL; ++k) {
                         demap_axis_i8<QM / 2>(x[k].x, rs[k], q + k * QM, 2);
@@ -925,7 +995,26 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                 bulk_g2s(g + SM::wst + (i & 1) * SM::wrec, reinterpret_cast<const float*>(a.ws) + rec_of(i) * WS,
                          (uint32_t)SM::wrec, &wfull[i & 1]);
             };
-            if constexpr (BEPI) {
+            // BI: thread 128 bulk-copies unit j's B image into B set j % NACC and its slopes into slope slot j & 7
+            // (once this CTA's setup group has published it; the B set's previous unit j - NACC has completed
+            // its MMAs, the slope slot's unit j - 8 its epilogue)
+            auto issue_b = [&](long long j) {
+                while (*units_ready <= j) __nanosleep(64);
+                asm volatile("fence.proxy.async.global;" ::: "memory");
+                const char* src = reinterpret_cast<const char*>(a.ws) + rec_of(j) * kBiRec;
+                uint64_t* bb = &bready[j % NACC];
+                mbar_arrive_expect_tx(bb, (uint32_t)kBiRec);
+                bulk_g2s(g + SM::B + (j % NACC) * SM::bset, src, (uint32_t)kBiImg, bb);
+                bulk_g2s(sslope + (j & 7) * 32, src + kBiImg, 128u, bb);
+            };
+            if constexpr (BI) {
+                if (t == 128) {
+                    PROF_T(ts);
+                    pdl_wait();
+                    for (long long j = 0; j < NACC && j < n_my; ++j) issue_b(j);
+                    PROF_ADD(prof, 30, ts);
+                }
+            } else if constexpr (BEPI) {
                 if (warp < 8) {  // B sets of units 0 .. NACC-1; W stage j & 1 is refilled with unit j + 2's record
                     if (t == 128) {
                         pdl_wait();  // the setup (kernel or group) of this call writes the workspace
@@ -949,7 +1038,27 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                 mbar_wait_sleep(&accfull[b], (uint32_t)((i / NACC) & 1));
                 PROF_ADD(prof, 24, t0);
                 tc::fence_after();
-                if constexpr (BEPI) {
+                if constexpr (BI) {
+                    if (t == 128 && i + NACC < n_my) {  // B set b is free: unit i's MMAs completed
+                        PROF_T(ti);
+                        issue_b(i + NACC);
+                        PROF_ADD(prof, 29, ti);
+                    }
+                    if (warp == 8) {
+                        // unit i's record has been copied (its MMAs read the B set): drop its L2 lines without
+                        // the write-back, then hand the ring slot back to the setup group
+                        if constexpr (BI == 2) {
+                            const char* rec = reinterpret_cast<const char*>(a.ws) + rec_of(i) * kBiRec;
+                            for (int l = lane; l < kBiRec / 128; l += 32)
+                                asm volatile("discard.global.L2 [%0], 128;" ::"l"(rec + 128 * l) : "memory");
+                        }
+                        __syncwarp();  // orders the warp's discards before lane 0's release (CTA scope: the
+                        if (lane == 0) {  // setup group that rewrites the slot is in this CTA)
+                            if constexpr (BI == 2) __threadfence_block();
+                            *units_built = (int)(i + 1);
+                        }
+                    }
+                } else if constexpr (BEPI) {
                     if (warp < 8 && i + NACC < n_my) {  // B set b is free: unit i's MMAs completed
                         PROF_T(tb);
 #ifdef C5_PROFILE
@@ -1021,7 +1130,7 @@ __global__ void __launch_bounds__(128, su::CTAS_PER_SM) k_c5_setup(DetectArgs a,
 #pragma unroll 1
     for (long long bt = blockIdx.x; bt < n_batch; bt += gridDim.x, ++it) {
         const long long ub = bt * su::UPB, bn = bt + gridDim.x;
-        setup_batch<QM, false, false>(a, &hmap, g, base, bar_tma, bar_mma, tmem, it, nv_of(bt), t, warp, lane, waited,
+        setup_batch<QM, false, false, false>(a, &hmap, g, base, bar_tma, bar_mma, tmem, it, nv_of(bt), t, warp, lane, waited,
                                [&](int s) { return ub + s; }, [] { __syncthreads(); },
                                [&] {
                                    if (bn < n_batch)
@@ -1084,7 +1193,7 @@ cudaError_t prepare_setup() {
                                     (int)(4 * SetupSmem<64, 16, SETUP == 0 ? 0 : 1>::per_unit));
 }
 
-template <int QM, int LT, int EW, int S, int NLO, int TA, int SETUP, bool BEPI, bool FUSED = false, int NACC = 2>
+template <int QM, int LT, int EW, int S, int NLO, int TA, int SETUP, bool BEPI, bool FUSED = false, int NACC = 2, int BI = 0>
 cudaError_t launch_c5(const DetectArgs& a, cudaStream_t s) {
     if (a.n_units <= 0) return cudaSuccess;
     static int n_sm = 0;
@@ -1120,24 +1229,24 @@ cudaError_t launch_c5(const DetectArgs& a, cudaStream_t s) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(a.n_units < n_sm ? a.n_units : n_sm));
     cfg.blockDim = dim3(32 * (6 + EW) + (FUSED ? 128 : 0));
-    cfg.dynamicSmemBytes = C5Smem<S, NLO, TA, FUSED, NACC>::total;
+    cfg.dynamicSmemBytes = C5Smem<S, NLO, TA, FUSED, NACC, BI != 0>::total;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = a.overlap ? 1 : 0;
-    return cudaLaunchKernelEx(&cfg, k_c5_apply<QM, LT, EW, S, NLO, TA, BEPI, FUSED, NACC>, a, ymap, hmap);
+    return cudaLaunchKernelEx(&cfg, k_c5_apply<QM, LT, EW, S, NLO, TA, BEPI, FUSED, NACC, BI>, a, ymap, hmap);
 }
 
-template <int QM, int LT, int EW, int S, int NLO, int TA, int SETUP, bool BEPI, bool FUSED = false, int NACC = 2>
+template <int QM, int LT, int EW, int S, int NLO, int TA, int SETUP, bool BEPI, bool FUSED = false, int NACC = 2, int BI = 0>
 cudaError_t prepare_c5() {
     if constexpr (!FUSED) {
         cudaError_t e = prepare_setup<QM, SETUP>();
         if (e != cudaSuccess) return e;
     }
-    return cudaFuncSetAttribute(k_c5_apply<QM, LT, EW, S, NLO, TA, BEPI, FUSED, NACC>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C5Smem<S, NLO, TA, FUSED, NACC>::total);
+    return cudaFuncSetAttribute(k_c5_apply<QM, LT, EW, S, NLO, TA, BEPI, FUSED, NACC, BI>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C5Smem<S, NLO, TA, FUSED, NACC, BI != 0>::total);
 }
 
 size_t c5_workspace(const DetectArgs& a) { return (size_t)a.n_units * BigWs<64, 16>::stride * 4; }
@@ -1152,11 +1261,22 @@ size_t c5f_workspace(const DetectArgs& a) {
     const long long ctas = a.n_units < n_sm ? a.n_units : n_sm;
     return (size_t)ctas * kC5Ring * BigWs<64, 16>::stride * 4;
 }
+// fused kernel with B-image records
+size_t c5fb_workspace(const DetectArgs& a) {
+    return c5f_workspace(a) / ((size_t)BigWs<64, 16>::stride * 4) * (size_t)kBiRec;
+}
 
 #define C5_ENTRY(NAME, QM, LT, S, NLO, TA, SETUP, BEPI)                                                   \
     KernelEntry {                                                                                          \
         NAME, 64, 16, QM, kSc, 14, LT, 32, 2, launch_c5<QM, LT, 6, S, NLO, TA, SETUP, BEPI>,               \
             prepare_c5<QM, LT, 6, S, NLO, TA, SETUP, BEPI>, c5_workspace                                   \
+    }
+// BI = 1: B-image records; 2: + the consumed records discarded from L2 (no dirty write-back) by the tile-1
+// epilogue warp
+#define C5FB_ENTRY(NAME, QM, LT, S, BI)                                                                     \
+    KernelEntry {                                                                                          \
+        NAME, 64, 16, QM, kSc, 14, LT, 32, 1, launch_c5<QM, LT, 6, S, 2, 4, 2, true, true, 2, BI>,         \
+            prepare_c5<QM, LT, 6, S, 2, 4, 2, true, true, 2, BI>, c5fb_workspace                           \
     }
 #define C5F_ENTRY(NAME, QM, LT, S, NACC)                                                                    \
     KernelEntry {                                                                                          \
@@ -1170,7 +1290,11 @@ size_t c5f_workspace(const DetectArgs& a) {
 // contractions; gj = SIMT Gauss-Jordan; chol = SIMT Cholesky), be = the B sets built by the
 // (under-loaded) epilogue warps instead of the converter warps, which set the pace of the pipeline.
 const KernelEntry kEntries[] = {
-    C5F_ENTRY("c5_fused_64x16_q6_i8", 6, kLlrI8, 5, 2),  // C5 default: setup warp group inside the apply kernel
+    // C5 default: setup warp group inside the apply kernel, writing B-image records that the apply copies
+    // straight into its B sets; consumed records discarded from L2
+    C5FB_ENTRY("c5_fusedbid_64x16_q6_i8", 6, kLlrI8, 5, 2),
+    C5FB_ENTRY("c5_fusedbi_64x16_q6_i8", 6, kLlrI8, 5, 1),  // B-image records, no discards
+    C5F_ENTRY("c5_fused_64x16_q6_i8", 6, kLlrI8, 5, 2),  // W~ records, B sets built by epilogue warps 4-7
     C5F_ENTRY("c5_fused3_64x16_q6_i8", 6, kLlrI8, 4, 3),  // 3 accumulators / B sets, 4 y stages, narrow setup
     C5_ENTRY("c5_bf16_tcs_be_64x16_q6_i8", 6, kLlrI8, 6, 4, 3, 2, true),  // two kernels: tensor-core setup + apply
     C5_ENTRY("c5_bf16kc_tcs_be_64x16_q6_i8", 6, kLlrI8, 6, 4, 4, 2, true),

@@ -4,7 +4,7 @@ from paper_2510_07843_b200 import mimo, synth
 L = mimo.load_library(os.environ.get('PROFLIB', 'tools/dbg/libmimo_prof.so'))
 w = synth.generate(5)
 H, y = torch.from_numpy(w.H).cuda(), torch.from_numpy(w.y).cuda()
-names = {0: "tma wait", 1: "convert", 2: "gram mma", 3: "gram readout", 4: "GJ + B'", 5: "W mma", 6: "W readout+store", 7: "fence+sync"}
+names = {0: "tma wait", 1: "convert", 2: "gram mma", 3: "gram readout", 4: "GJ + B'", 5: "W mma", 6: "W readout+store", 7: "fence+sync", 8: " GJ: pdl", 9: " GJ: ring_wait", 10: " GJ: C load + pivots", 11: " GJ: A, B', slopes", 12: " GJ: sync"}
 p = mimo.Plan(64, 16, 6, sc_per_h=12, llr_dtype="i8", kernel=sys.argv[1])
 out = torch.empty(p.shapes(w.n_sc, w.n_sym)["llr"], dtype=torch.int8, device="cuda")
 p.detect(H, y, float(w.sigma2), out=out); torch.cuda.synchronize()

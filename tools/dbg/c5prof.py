@@ -9,7 +9,7 @@ w = synth.generate(5)
 H, y = torch.from_numpy(w.H).cuda(), torch.from_numpy(w.y).cuda()
 names = {0: "prod.wait_yfree", 1: "prod.wait_setup(fused)", 31: "prod.total", 8: "mma.wait_bready", 9: "mma.wait_tfree", 10: "mma.wait_afull",
          16: "conv.wait_accfull(B)", 17: "conv.Bbuild", 18: "conv.wait_yfull", 19: "conv.wait_afree",
-         20: "conv.convert", 21: "conv.bar+arrive", 24: "epi.wait_accfull", 25: "epi.work", 26: "epi.bar", 27: "epi.Bbuild", 28: "epi.Bbuild.wfull", 29: "epi.Bbuild.issue_w(spin)"}
+         20: "conv.convert", 21: "conv.bar+arrive", 24: "epi.wait_accfull", 25: "epi.work", 26: "epi.bar", 27: "epi.Bbuild", 28: "epi.Bbuild.wfull", 29: "epi.Bbuild.issue_w(spin)", 30: "epi.BI first issue (startup)"}
 for kn in sys.argv[1:]:
     p = mimo.Plan(64, 16, 6, sc_per_h=12, llr_dtype="i8", kernel=kn)
     out = torch.empty(p.shapes(w.n_sc, w.n_sym)["llr"], dtype=torch.int8, device="cuda")

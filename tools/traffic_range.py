@@ -22,10 +22,11 @@ from paper_2510_07843_b200 import mimo, synth  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=5)
 ap.add_argument("--steps", type=int, default=8)
+ap.add_argument("--kernel", default=None)
 args = ap.parse_args()
 w = synth.generate(args.config)
 b = synth.config_algorithmic_bytes(args.config)
-p = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, llr_dtype=w.llr)
+p = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, llr_dtype=w.llr, kernel=args.kernel)
 n_sets = max(2, math.ceil(3 * torch.cuda.get_device_properties(0).L2_cache_size / b["total"]))
 H0, y0 = torch.from_numpy(w.H).cuda(), torch.from_numpy(w.y).cuda()
 sets = [(H0.clone(), y0.clone(), torch.empty(p.shapes(w.n_sc, w.n_sym)["llr"], dtype=p.llr_dtype, device="cuda"))
