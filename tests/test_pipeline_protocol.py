@@ -35,14 +35,39 @@ def wait(b, idx):
         raise ABA(f"released at {b.phases} completions while waiting for completion #{idx}")
 
 
-def apply_roles(n_my, S, NLO, bepi=True, nacc=2):
-    """nacc: accumulators = B sets (unit i uses slot i % nacc); the W~ staging ring stays 2 deep."""
+def apply_roles(n_my, S, NLO, bepi=True, nacc=2, bi=False, ring=16, upb=4):
+    """nacc: accumulators = B sets (unit i uses slot i % nacc); the W~ staging ring stays 2 deep.
+    bi: the default fused kernel with B-image records (k_c5.cu BI >= 1): a setup-group role publishes
+    units in batches of `upb` (the first at once, every other one after the next batch's conversion)
+    into a ring of `ring` records that it may only rewrite once the apply has consumed them
+    (units_built, set by epilogue warp 8 after accfull); thread 128 bulk-copies unit j's image into B
+    set j % nacc (bready completes by the copy's bytes) once the setup has published it."""
     B = lambda c=1: Barrier(c)
     yfull, yfree = [B() for _ in range(S)], [B() for _ in range(S)]
     afull, afree = [B() for _ in range(NLO)], [B() for _ in range(NLO)]
     bready, accfull, tfree = [B() for _ in range(nacc)], [B() for _ in range(nacc)], [B() for _ in range(nacc)]
     wfull, wfree = [B() for _ in range(2)], [B() for _ in range(2)]
     G = 4 * n_my
+    st8 = {"ready": 0, "built": 0}  # the kernel's shared-memory counters units_ready / units_built
+
+    def setup():  # fused setup group (bi): batch k = units 4k .. 4k + nv - 1
+        nb = (n_my + upb - 1) // upb
+        for k in range(nb):
+            j0, nv = upb * k, min(upb, n_my - upb * k)
+            if k > 0:
+                st8["ready"] = j0  # publish_prev after this batch's conversion
+            while st8["built"] < j0 + nv - ring:  # ring_wait before the batch's record writes
+                yield "wait"
+            yield "step"
+            if k == 0 and nv < n_my:
+                st8["ready"] = nv  # the first batch at once
+        if n_my > 0:
+            st8["ready"] = n_my
+
+    def issue_b(j):  # spin on units_ready, then the image copy completes bready
+        while st8["ready"] <= j:
+            yield "wait"
+        bready[j % nacc].arrive()
 
     def producer():
         def issue_w(i):
@@ -105,6 +130,18 @@ def apply_roles(n_my, S, NLO, bepi=True, nacc=2):
     def epilogue():  # warps 4-7 (and the B builder with BEPI); warps 8-9 share the tfree barrier sync
         def stage_w(i):  # BEPI: thread 128 issues the W~ TMA of unit i into stage i & 1 (completes at once)
             wfull[i & 1].arrive()
+        if bi:
+            for j in range(min(nacc, n_my)):
+                yield from issue_b(j)
+            for i in range(n_my):
+                b = i % nacc
+                yield from wait(accfull[b], i // nacc)
+                st8["built"] = i + 1  # warp 8 (not held by thread 128's spin below)
+                if i + nacc < n_my:
+                    yield from issue_b(i + nacc)
+                tfree[b].arrive()
+                yield "step"
+            return
         if bepi:
             for i0 in range(min(2, n_my)):
                 stage_w(i0)
@@ -124,7 +161,7 @@ def apply_roles(n_my, S, NLO, bepi=True, nacc=2):
             tfree[b].arrive()
             yield "step"
 
-    return [producer(), mma(), converters(), epilogue()]
+    return [producer(), mma(), converters(), epilogue()] + ([setup()] if bi else [])
 
 
 def run(roles, max_rounds=200000):
@@ -153,6 +190,20 @@ def run(roles, max_rounds=200000):
 @pytest.mark.parametrize("n_my", [0, 1, 2, 3, 4, 5, 7, 8, 9, 13, 74])
 def test_apply_protocol_no_deadlock_no_aba(S, NLO, bepi, nacc, n_my):
     assert run(apply_roles(n_my, S, NLO, bepi, nacc)), "protocol deadlocks"
+
+
+@pytest.mark.parametrize("S,NLO", [(5, 2), (6, 4)])
+@pytest.mark.parametrize("n_my", [0, 1, 2, 3, 4, 5, 7, 8, 9, 13, 16, 17, 21, 33, 74])
+@pytest.mark.parametrize("ring", [16, 8])
+def test_apply_protocol_b_images(S, NLO, n_my, ring):
+    """The default C5 kernel (B-image records, setup group in the loop): no deadlock, no ABA."""
+    assert run(apply_roles(n_my, S, NLO, bepi=True, nacc=2, bi=True, ring=ring)), "protocol deadlocks"
+
+
+def test_model_detects_a_ring_too_small():
+    """The checker itself: a ring shorter than one setup batch plus the apply's lookahead deadlocks
+    (the setup group waits for slots the apply can only free after the records it waits for)."""
+    assert not run(apply_roles(13, 5, 2, bepi=True, nacc=2, bi=True, ring=4))
 
 
 def test_model_detects_a_two_phase_runaway():
