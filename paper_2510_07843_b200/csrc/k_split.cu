@@ -278,9 +278,11 @@ __global__ void __launch_bounds__(128) k_apply_units(DetectArgs a) {
 // Streaming apply with a register prefetch ring: thread (g, sc) walks symbols
 // g, g+G, ... of its slot keeping PF y vectors in flight (continuous HBM
 // traffic instead of one burst per thread).
-template <int NR, int NL, int QM, int LT, int G, int PF, int SCPH, int MINB>
+// KS = symbols sharing one H (sym_per_h; 14 = one H per slot): a "slot" of this kernel is one H time block
+// of KS symbols (a.n_slots = n_sym / KS blocks), so time-varying channels (KS = 7, 2, 1) take the same code
+template <int NR, int NL, int QM, int LT, int G, int PF, int SCPH, int MINB, int KS = kSym>
 __global__ void __launch_bounds__(128, MINB) k_apply_stream(DetectArgs a) {
-    constexpr int NS = (kSym + G - 1) / G;
+    constexpr int NS = (KS + G - 1) / G;
     constexpr int WS = UnitWs<NR, NL>::stride;
     static_assert(PF >= 1 && PF <= NS, "prefetch distance");
     pdl_launch_dependents();
@@ -292,8 +294,8 @@ __global__ void __launch_bounds__(128, MINB) k_apply_stream(DetectArgs a) {
 #pragma unroll
         for (int i = 0; i < PF; ++i) {
             const int s = g + i * G;
-            if (s < kSym)
-                load_bytes<NR * 8>(a.y + ((size_t)(slot * kSym + s) * a.n_sc + sc) * NR,
+            if (s < KS)
+                load_bytes<NR * 8>(a.y + ((size_t)(slot * KS + s) * a.n_sc + sc) * NR,
                                    reinterpret_cast<uint32_t*>(&ring[i][0]));
         }
     }
@@ -314,13 +316,13 @@ __global__ void __launch_bounds__(128, MINB) k_apply_stream(DetectArgs a) {
 #pragma unroll
     for (int i = 0; i < NS; ++i) {
         const int s = g + i * G;
-        if (s >= kSym) break;
+        if (s >= KS) break;
         float2 yv[NR];
 #pragma unroll
         for (int r = 0; r < NR; ++r) yv[r] = ring[i % PF][r];
         const int sn = g + (i + PF) * G;
-        if (i + PF < NS && sn < kSym)
-            load_bytes<NR * 8>(a.y + ((size_t)(slot * kSym + sn) * a.n_sc + sc) * NR,
+        if (i + PF < NS && sn < KS)
+            load_bytes<NR * 8>(a.y + ((size_t)(slot * KS + sn) * a.n_sc + sc) * NR,
                                reinterpret_cast<uint32_t*>(&ring[i % PF][0]));
         float2 x[NL];
 #pragma unroll
@@ -331,7 +333,7 @@ __global__ void __launch_bounds__(128, MINB) k_apply_stream(DetectArgs a) {
 #pragma unroll
             for (int k = 0; k < NL; ++k) x[k] = cmac_y(x[k], w[k][r], yv[r], ny);
         }
-        const size_t re = (size_t)(slot * kSym + s) * a.n_sc + sc;
+        const size_t re = (size_t)(slot * KS + s) * a.n_sc + sc;
         if (a.llr) {
             float v[NL * QM];
             uint32_t wd[kWords];
@@ -505,14 +507,14 @@ cudaError_t launch_bfp_q(const DetectArgs& a, const uint32_t* yb, int W, float s
     }
 }
 
-template <int NR, int NL, int QM, int LT, int UPC, int G, int PF, int SCPH, int MINB>
+template <int NR, int NL, int QM, int LT, int UPC, int G, int PF, int SCPH, int MINB, int KS = kSym>
 cudaError_t launch_stream(const DetectArgs& a, cudaStream_t s) {
     if (a.n_units <= 0) return cudaSuccess;
     const unsigned g1 = (unsigned)((a.n_units + UPC - 1) / UPC);
     cudaError_t e = launch_kernel(k_setup_units<NR, NL, QM, UPC>, dim3(g1), dim3(128), 0, s, a.overlap, a);
     if (e != cudaSuccess) return e;
     dim3 g2((a.n_sc + 127) / 128, a.n_slots * G);
-    return launch_kernel(k_apply_stream<NR, NL, QM, LT, G, PF, SCPH, MINB>, g2, dim3(128), 0, s, a.overlap, a);
+    return launch_kernel(k_apply_stream<NR, NL, QM, LT, G, PF, SCPH, MINB, KS>, g2, dim3(128), 0, s, a.overlap, a);
 }
 
 template <int NR, int NL>
@@ -543,8 +545,19 @@ cudaError_t launch(const DetectArgs& a, cudaStream_t s) {
             nullptr, workspace<NR, NL>                                                               \
     }
 
+// time-varying channels on the C3 shape (SPEC.md:481 leaves per-slot vs per-symbol W open; NEXT-3): one H per
+// KS symbols and PRB, the setup per (block, PRB) unit and the streaming apply over blocks of KS symbols
+#define STREAM_TV_ENTRY(NAME, NR, NL, QM, LT, SCPH, UPC, G, PF, MINB, KS)                             \
+    KernelEntry {                                                                                    \
+        NAME, NR, NL, QM, SCPH, KS, LT, 32, 2, launch_stream<NR, NL, QM, LT, UPC, G, PF, SCPH, MINB, KS>, \
+            nullptr, workspace<NR, NL>                                                               \
+    }
+
 const KernelEntry kEntries[] = {
     STREAM_ENTRY_B("stream_8x4_q6_i8", 8, 4, 6, kLlrI8, 12, 16, 2, 2, 4),  // C3: <= 128 regs -> 4 CTAs/SM
+    STREAM_TV_ENTRY("stream_8x4_q6_i8_s7", 8, 4, 6, kLlrI8, 12, 16, 1, 2, 4, 7),
+    STREAM_TV_ENTRY("stream_8x4_q6_i8_s2", 8, 4, 6, kLlrI8, 12, 16, 1, 2, 4, 2),
+    STREAM_TV_ENTRY("stream_8x4_q6_i8_s1", 8, 4, 6, kLlrI8, 12, 16, 1, 1, 4, 1),
     SPLIT_ENTRY("split_8x4_q6_i8", 8, 4, 6, kLlrI8, 12, 32, 7),
     SPLIT_ENTRY("split_8x4_q6_f32", 8, 4, 6, kLlrF32, 12, 32, 7),
     SPLIT_ENTRY("split_8x4_q6_f16", 8, 4, 6, kLlrF16, 12, 32, 7),

@@ -1,5 +1,5 @@
 """Time the time-varying-channel kernels (NEXT-3: H constant over sym_per_h < 14 symbols) against
-the generic kernel on the full C1 / C2 grids, through the C ABI (mimo.Plan.detect), the way
+the generic kernel on the full C2 / C3 grids, through the C ABI (mimo.Plan.detect), the way
 bench.py times a step: rotating buffer sets > 3x L2, CUDA-graph replays, CUDA events on the
 launching stream. Writes one JSON line per (config, sym_per_h, kernel).
 
@@ -25,11 +25,14 @@ def main():
     hbm = float(peaks.get("hbm_gbs", 6547.2))
     lines = []
     for k, sph, kernels in ((2, 7, ["tpu_4x4_q4_f32_s7", "generic"]), (2, 2, ["tpu_4x4_q4_f32_s2", "generic"]),
-                            (2, 1, ["tpu_4x4_q4_f32_s1", "generic"]), (2, 14, ["tpu_4x4_q4_f32"])):
+                            (2, 1, ["tpu_4x4_q4_f32_s1", "generic"]), (2, 14, ["tpu_4x4_q4_f32"]),
+                            (3, 7, ["stream_8x4_q6_i8_s7", "generic"]), (3, 2, ["stream_8x4_q6_i8_s2", "generic"]),
+                            (3, 1, ["stream_8x4_q6_i8_s1", "generic"]), (3, 14, ["stream_8x4_q6_i8"])):
         cfg = dict(synth.CONFIGS[k], sym_per_h=sph)
         w = synth.generate(cfg)
         n_units = w.n_units
-        bytes_step = n_units * w.n_rx * w.n_layers * 8 + w.n_re * w.n_rx * 8 + w.n_re * w.n_layers * w.qm * 4
+        llr_b = {"f32": 4, "f16": 2, "i8": 1}[w.llr]
+        bytes_step = n_units * w.n_rx * w.n_layers * 8 + w.n_re * w.n_rx * 8 + w.n_re * w.n_layers * w.qm * llr_b
         nset = max(2, int(3 * 126e6 // bytes_step) + 1)
         for kn in kernels:
             plan = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, sym_per_h=sph, llr_dtype=w.llr,
@@ -38,7 +41,7 @@ def main():
             for _ in range(nset):
                 H = torch.from_numpy(w.H).cuda()
                 y = torch.from_numpy(w.y).cuda()
-                out = torch.empty(plan.shapes(w.n_sc, w.n_sym)["llr"], dtype=torch.float32, device="cuda")
+                out = torch.empty(plan.shapes(w.n_sc, w.n_sym)["llr"], dtype=plan.llr_dtype, device="cuda")
                 sets.append((H, y, out))
             stream = torch.cuda.Stream()
             with torch.cuda.stream(stream):
