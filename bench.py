@@ -420,6 +420,41 @@ def emulate_shards(mimo, w, k, args, dev, n_emul, full_llr):
             "bit_identical": bool(torch.equal(full, full_llr))}
 
 
+def result_placement(mimo, w, blk, sh, stream, dev, world, rank):
+    """N > 1, after (outside) the timed detection: every rank's LLR block goes point to point to
+    rank 0 (NCCL over NVLink) and is written into the full grid there (shard.place_blocks_p2p) --
+    the north_star's "result placement", timed on its own (CUDA events, max over ranks) and checked
+    bit-identical against rank 0 detecting the whole job on its own GPU."""
+    import torch
+    import torch.distributed as dist
+    n_prb = w.n_sc // shard.SC_PER_PRB
+    blocks = shard.block_partition(w.n_slots, n_prb, world)
+    local = sh.sets[0][2]
+    with torch.cuda.stream(stream):
+        sh.plan.detect(sh.sets[0][0], sh.sets[0][1], sh.s2, out=local)
+    stream.synchronize()
+    full_shape = (w.n_sym, w.n_sc) + tuple(local.shape[2:])
+    dist.barrier()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    full = shard.place_blocks_p2p(local, blocks, full_shape)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ms = shard.max_over_ranks(e0.elapsed_time(e1), device=dev)
+    nbytes = local.element_size() * int(torch.Size(full_shape).numel())
+    out = {"ms": ms, "bytes": nbytes, "GB_s": nbytes / (ms * 1e-3) / 1e9,
+           "how": "each rank's LLR block sent point to point to rank 0 (NCCL send/recv), placed into the full "
+                  "[sym][sc][layer][bit] grid in rank 0's HBM; not part of the detection step"}
+    if rank == 0:  # verification: the whole job on rank 0's GPU alone
+        p = mimo.Plan(w.n_rx, w.n_layers, w.qm, sc_per_h=w.sc_per_h, llr_dtype=w.llr, device=dev.index)
+        Hd, yd = torch.from_numpy(w.H).to(dev), torch.from_numpy(w.y).to(dev)
+        ref = p.detect(Hd, yd, float(w.sigma2))
+        torch.cuda.synchronize(dev)
+        out["bit_identical_to_1gpu"] = bool(torch.equal(ref, full))
+    return out
+
+
 def run_ours(args, k):
     import torch
     import torch.distributed as dist
@@ -490,6 +525,7 @@ def run_ours(args, k):
     del g1
 
     t_max_ms = shard.max_over_ranks(elapsed_ms, device=dev)
+    placement = result_placement(mimo, w, blk, sh, stream, dev, world, rank) if blk is not None else None
     wall_max = shard.max_over_ranks(wall_s, device=dev)
     n_re_job = synth.config_algorithmic_bytes(k)["n_re"]
     n_re_all = n_re_job * K * (world if scaling == "replicas" else 1)
@@ -600,6 +636,8 @@ def run_ours(args, k):
     }
     if emul is not None:
         line["emulated_multi_gpu"] = emul
+    if placement is not None:
+        line["placement"] = placement
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -72,6 +72,40 @@ def place_block(full, part, block: dict, sym_per_slot: int = 14):
     return full
 
 
+def block_llr_shape(block: dict, full_shape, sym_per_slot: int = 14) -> tuple:
+    """Shape of one rank's [sym][sc][...] output block inside the full grid `full_shape`."""
+    s0, s1 = block["slots"]
+    p0, p1 = block["prbs"]
+    return ((s1 - s0) * sym_per_slot, (p1 - p0) * SC_PER_PRB) + tuple(full_shape[2:])
+
+
+def place_blocks_p2p(local, blocks: list[dict], full_shape, dst: int = 0, sym_per_slot: int = 14):
+    """Result placement (north_star: "no collective beyond result placement"): every rank sends
+    its contiguous output block (torch tensor, e.g. the LLRs in its HBM) to rank `dst` point to
+    point (NCCL over NVLink between GPUs; gloo on CPU in the tests), and rank `dst` writes each
+    block into the full grid in its own memory. Returns the full grid on `dst`, None elsewhere.
+    Not part of detection: bench.py times it separately (`placement` in the JSON line)."""
+    import torch
+    import torch.distributed as dist
+    world = len(blocks)
+    if not (dist.is_available() and dist.is_initialized()) or world == 1:
+        return local
+    rank = dist.get_rank()
+    if rank != dst:
+        dist.send(local.contiguous(), dst)
+        return None
+    full = torch.empty(tuple(full_shape), dtype=local.dtype, device=local.device)
+    for r in range(world):
+        if r == dst:
+            part = local
+        else:
+            part = torch.empty(block_llr_shape(blocks[r], full_shape, sym_per_slot), dtype=local.dtype,
+                               device=local.device)
+            dist.recv(part, src=r)
+        place_block(full, part, blocks[r], sym_per_slot)
+    return full
+
+
 def shard_seed(base_seed: int, rank: int) -> int:
     """Seed of an independently drawn per-rank workload (replica runs only; the strong-scaling
     path slices one seeded job with block_partition instead)."""

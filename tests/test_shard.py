@@ -111,6 +111,16 @@ def _worker(rank, world, port, out_q):
             ref = oracle.detect(w.H_units(), w.y_units(), w.sigma2, w.qm)
             ref_grid = synth.unit_scatter(ref["llr"], n_slots, n_sc, 1)
             out_q.put((t, n, bool(np.array_equal(full, ref_grid)), full.shape))
+        # the placement bench.py times at N > 1: blocks sent point to point to rank 0 as tensors
+        import torch
+        blocks = shard.block_partition(n_slots, n_sc // 12, world)
+        full_shape = (n_slots * 14, n_sc, 4, 4)
+        assert tuple(local.shape) == shard.block_llr_shape(blk, full_shape)
+        placed = shard.place_blocks_p2p(torch.from_numpy(np.ascontiguousarray(local)), blocks, full_shape)
+        if rank == 0:
+            out_q.put(bool(np.array_equal(placed.numpy(), ref_grid)))
+        else:
+            assert placed is None
     finally:
         dist.destroy_process_group()
 
@@ -130,3 +140,4 @@ def test_gloo_two_ranks_shard_and_gather():
     assert t == 1.5            # max over ranks of 0.5 + rank
     assert n == 3 * 14 * 24    # every RE of the job processed exactly once
     assert equal and shape == (42, 24, 4, 4)
+    assert q.get(timeout=5)    # point-to-point placement into rank 0's full grid: bit-identical
