@@ -118,6 +118,32 @@ __device__ __forceinline__ void demap_axis_i8(float u, float rs, uint32_t* q, in
     }
 }
 
+// demap_axis_i8 for the I and Q axes of one layer as packed pairs (FADD2 / FFMA2 / FMUL2 with the free
+// |.| operand forms; only the saturating FMA and the sign select stay scalar): the same operations in the
+// same order, so bit-identical to two demap_axis_i8 calls; q[2 i] = I LLR i, q[2 i + 1] = Q LLR i
+template <int M>
+__device__ __forceinline__ void demap_pair_i8(float2 u, float rs, uint32_t* q) {
+    float2 t[M];
+    t[0] = u;
+#pragma unroll
+    for (int i = 1; i < M; ++i)
+        t[i] = fadd2_(make_float2(float(1 << (M - i)), float(1 << (M - i))),
+                      make_float2(-fabsf(t[i - 1].x), -fabsf(t[i - 1].y)));
+    const float2 rs2 = make_float2(rs, rs);
+    const float2 e = ffma2(make_float2(fabsf(t[M - 1].x), fabsf(t[M - 1].y)), rs2, make_float2(-rs, -rs));
+    const float2 nD = fmul2_(e, make_float2(-e.x, -e.y));  // -D, exactly
+#pragma unroll
+    for (int i = 0; i < M; ++i) {
+        const float2 at = ffma2(make_float2(fabsf(t[i].x), fabsf(t[i].y)), rs2, rs2);
+        const float mx = fma_sat(at.x, at.x, nD.x), my = fma_sat(at.y, at.y, nD.y);
+        const float2 s127 = make_float2(__uint_as_float((__float_as_uint(t[i].x) & 0x80000000u) | 0x42FE0000u),
+                                        __uint_as_float((__float_as_uint(t[i].y) & 0x80000000u) | 0x42FE0000u));
+        const float2 qq = ffma2(make_float2(mx, my), s127, make_float2(12582912.f, 12582912.f));
+        q[2 * i] = __float_as_uint(qq.x);
+        q[2 * i + 1] = __float_as_uint(qq.y);
+    }
+}
+
 // ------------------------------------------------------------------------
 // k_c5_setup: rows a2-a5 with both contractions on the tensor cores (BF16 split
 // operands, reading R28) and the 16 x 16 inversion on the FP32 pipe. One CTA =
@@ -215,7 +241,7 @@ __device__ __forceinline__ void setup_issue_h(const CUtensorMap* hmapp, uint32_t
 // rec_of(s) = the workspace record (W~ + slopes) of batch slot s: the unit itself, or (fused) a slot of
 // the CTA's ring of records, which ring_wait() (called by every thread before the batch's first record
 // write) makes sure the apply has finished reading.
-template <int QM, bool PUB, bool WIDE, bool BI, typename UnitF, typename SyncF, typename NextF, typename PubF, typename RecF,
+template <int QM, bool PUB, bool WIDE, int BI, typename UnitF, typename SyncF, typename NextF, typename PubF, typename RecF,
           typename RingF>
 __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorMap* hmapp, unsigned char* g,
                                             uint32_t gaddr, uint64_t* bar_tma, uint64_t* bar_mma, uint32_t tmem,
@@ -497,6 +523,46 @@ __device__ __forceinline__ void setup_batch(const DetectArgs& a, const CUtensorM
         tc::fence_after();
 #pragma unroll 1
         for (int s = 0; s < nv; ++s) {  // row r = 16 warp + lane of W~^T: cols k = Re W~_kr, 16 + k = Im W~_kr
+            if constexpr (BI == 2 && WIDE) {
+                // the whole warp: lane l < 16 takes antenna r = 16 warp + l, columns k (Re W~_kr), lane l + 16 the
+                // same antenna's columns 16 + k (Im W~_kr); hi + lo products summed, split into bf16 hi / lo, and
+                // each lane stores its halves of B-image rows 2r and 2r + 1 (Re lanes: row 2r chunks 0-1 | 4-5,
+                // row 2r + 1 chunks 2-3 | 6-7; Im lanes: the others, negated in row 2r + 1)
+                uint32_t v[16], v2[16];
+                const uint32_t ta = tmem + ((uint32_t)(32 * gw) << 16) + 64u * s;
+                tc::ld16x2_16<16>(ta, v);
+                tc::ld16x2_16<16>(ta + 32u, v2);
+                tc::wait_ld();
+                const bool im = lane >= 16;
+                const int r = 16 * gw + (lane & 15);
+                uint32_t h[8], l[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    tc::split_bf2(__uint_as_float(v[2 * j]) + __uint_as_float(v2[2 * j]),
+                                  __uint_as_float(v[2 * j + 1]) + __uint_as_float(v2[2 * j + 1]), h[j], l[j]);
+                char* img = reinterpret_cast<char*>(a.ws) + rec_of(s) * kBiRec;
+                // row 2r: this lane's chunk pair q0 = 0 (Re) / 2 (Im) for hi, + 4 for lo
+                {
+                    const int R = 2 * r, sw = R & 7, q0 = im ? 2 : 0;
+                    st_v8(img + R * 128 + ((q0 ^ sw) << 4), h);
+                    st_v8(img + R * 128 + (((4 + q0) ^ sw) << 4), l);
+                }
+                {
+                    const int R = 2 * r + 1, sw = R & 7, q0 = im ? 0 : 2;  // odd row: chunk q0 + 1 lands first
+                    const uint32_t sg = im ? 0x80008000u : 0u;
+                    uint32_t oh[8], ol[8];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        oh[e] = h[4 + e] ^ sg;
+                        oh[4 + e] = h[e] ^ sg;
+                        ol[e] = l[4 + e] ^ sg;
+                        ol[4 + e] = l[e] ^ sg;
+                    }
+                    st_v8(img + R * 128 + (((q0 ^ sw) & ~1) << 4), oh);
+                    st_v8(img + R * 128 + ((((4 + q0) ^ sw) & ~1) << 4), ol);
+                }
+                continue;
+            }
             uint32_t v[32];
             if constexpr (WIDE) {
                 uint32_t v2[32];
@@ -698,7 +764,7 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
         for (long long j0 = 0; j0 < n_my; j0 += su::UPB, ++it) {
             const int nv = nv_of(j0);
             const long long jn = j0 + su::UPB;
-            setup_batch<QM, true, kWide, BI != 0>(a, &hmap, g + SM::setup, base + (uint32_t)SM::setup, stma, smma, tmem + kSetupCols, it,
+            setup_batch<QM, true, kWide, BI == 3 ? 2 : (BI != 0 ? 1 : 0)>(a, &hmap, g + SM::setup, base + (uint32_t)SM::setup, stma, smma, tmem + kSetupCols, it,
                                   nv, gt, gw, lane, waited, [&](int s_) { return u0 + (j0 + s_) * du; },
                                   [] { asm volatile("bar.sync 5, 128;" ::: "memory"); },
                                   [&] {
@@ -712,7 +778,7 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                                   [&](int s_) { return rec_of(j0 + s_); },
                                   [&] {  // ring slots of units j0 .. j0 + nv - 1 held units j0 - kC5Ring ..: built?
                                       while (*units_built < (int)(j0 + nv - kC5Ring)) __nanosleep(32);
-                                      if constexpr (BI == 2) __threadfence_block();  // acquire: after the L2 discards
+                                      if constexpr (BI >= 2) __threadfence_block();  // acquire: after the L2 discards
                                   });
             if (j0 == 0 && nv < n_my) {
                 // the first batch is published at once (the others one batch late, see setup_batch): the apply
@@ -853,10 +919,7 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                     uint32_t q[NL * QM];
                     const float* rs = BI ? sl + 16 : sslope + 128 + (i & 7) * 16;
 #pragma unroll
-                    for (int k = 0; k < NL; ++k) {
-                        demap_axis_i8<QM / 2>(x[k].x, rs[k], q + k * QM, 2);
-                        demap_axis_i8<QM / 2>(x[k].y, rs[k], q + k * QM + 1, 2);
-                    }
+                    for (int k = 0; k < NL; ++k) demap_pair_i8<QM / 2>(x[k], rs[k], q + k * QM);
 #pragma unroll
                     for (int w4 = 0; w4 < NL * QM / 4; ++w4)
                         wd[w4] = __byte_perm(__byte_perm(q[4 * w4], q[4 * w4 + 1], 0x0040),
@@ -1047,14 +1110,14 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                     if (warp == 8) {
                         // unit i's record has been copied (its MMAs read the B set): drop its L2 lines without
                         // the write-back, then hand the ring slot back to the setup group
-                        if constexpr (BI == 2) {
+                        if constexpr (BI >= 2) {
                             const char* rec = reinterpret_cast<const char*>(a.ws) + rec_of(i) * kBiRec;
                             for (int l = lane; l < kBiRec / 128; l += 32)
                                 asm volatile("discard.global.L2 [%0], 128;" ::"l"(rec + 128 * l) : "memory");
                         }
                         __syncwarp();  // orders the warp's discards before lane 0's release (CTA scope: the
                         if (lane == 0) {  // setup group that rewrites the slot is in this CTA)
-                            if constexpr (BI == 2) __threadfence_block();
+                            if constexpr (BI >= 2) __threadfence_block();
                             *units_built = (int)(i + 1);
                         }
                     }
@@ -1130,7 +1193,7 @@ __global__ void __launch_bounds__(128, su::CTAS_PER_SM) k_c5_setup(DetectArgs a,
 #pragma unroll 1
     for (long long bt = blockIdx.x; bt < n_batch; bt += gridDim.x, ++it) {
         const long long ub = bt * su::UPB, bn = bt + gridDim.x;
-        setup_batch<QM, false, false, false>(a, &hmap, g, base, bar_tma, bar_mma, tmem, it, nv_of(bt), t, warp, lane, waited,
+        setup_batch<QM, false, false, 0>(a, &hmap, g, base, bar_tma, bar_mma, tmem, it, nv_of(bt), t, warp, lane, waited,
                                [&](int s) { return ub + s; }, [] { __syncthreads(); },
                                [&] {
                                    if (bn < n_batch)
@@ -1272,7 +1335,7 @@ size_t c5fb_workspace(const DetectArgs& a) {
             prepare_c5<QM, LT, 6, S, NLO, TA, SETUP, BEPI>, c5_workspace                                   \
     }
 // BI = 1: B-image records; 2: + the consumed records discarded from L2 (no dirty write-back) by the tile-1
-// epilogue warp
+// epilogue warp; 3: 2 + the setup group's image readout by whole warps (16x32bx2 TMEM loads)
 #define C5FB_ENTRY(NAME, QM, LT, S, BI)                                                                     \
     KernelEntry {                                                                                          \
         NAME, 64, 16, QM, kSc, 14, LT, 32, 1, launch_c5<QM, LT, 6, S, 2, 4, 2, true, true, 2, BI>,         \
@@ -1290,9 +1353,10 @@ size_t c5fb_workspace(const DetectArgs& a) {
 // contractions; gj = SIMT Gauss-Jordan; chol = SIMT Cholesky), be = the B sets built by the
 // (under-loaded) epilogue warps instead of the converter warps, which set the pace of the pipeline.
 const KernelEntry kEntries[] = {
-    // C5 default: setup warp group inside the apply kernel, writing B-image records that the apply copies
-    // straight into its B sets; consumed records discarded from L2
-    C5FB_ENTRY("c5_fusedbid_64x16_q6_i8", 6, kLlrI8, 5, 2),
+    // C5 default: setup warp group inside the apply kernel, writing B-image records (read out of TMEM by whole
+    // warps) that the apply copies straight into its B sets; consumed records discarded from L2
+    C5FB_ENTRY("c5_fusedbiw_64x16_q6_i8", 6, kLlrI8, 5, 3),
+    C5FB_ENTRY("c5_fusedbid_64x16_q6_i8", 6, kLlrI8, 5, 2),  // image readout by half warps (lanes 0-15)
     C5FB_ENTRY("c5_fusedbi_64x16_q6_i8", 6, kLlrI8, 5, 1),  // B-image records, no discards
     C5F_ENTRY("c5_fused_64x16_q6_i8", 6, kLlrI8, 5, 2),  // W~ records, B sets built by epilogue warps 4-7
     C5F_ENTRY("c5_fused3_64x16_q6_i8", 6, kLlrI8, 4, 3),  // 3 accumulators / B sets, 4 y stages, narrow setup
