@@ -22,7 +22,7 @@ namespace {
 
 constexpr int kSym = 14;
 
-template <int NR, int NL, int NW>
+template <int NR, int NL, int NW, int KS = kSym>
 struct LgSmem {
     static constexpr int UPW = 32 / NL;
     static constexpr int TU = UPW * NW;
@@ -32,7 +32,7 @@ struct LgSmem {
     static constexpr int LS = NL * NL + 4;                              // float2 per unit L / X
     static constexpr size_t bars = 0;                                   // 15 mbarriers
     static constexpr size_t y = 128;                                    // [14][TU][YS]
-    static constexpr size_t H = y + (size_t)kSym * TU * YS * 8;         // [TU][HS]
+    static constexpr size_t H = y + (size_t)KS * TU * YS * 8;           // [TU][HS]
     static constexpr size_t LX = H + (size_t)TU * HS * 8;               // [TU][LS]  L rows, then X
     static constexpr size_t dinv = LX + (size_t)TU * LS * 8;            // [TU][NL] float
     static constexpr size_t total = dinv + (size_t)TU * NL * 4;
@@ -42,9 +42,11 @@ __device__ __forceinline__ float2 shfl2(float2 v, int src) {
     return make_float2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
 }
 
-template <int NR, int NL, int QM, int LT, int NW>
+// KS = symbols sharing one H (sym_per_h): a "slot" of this kernel is one H time block of KS symbols
+// (a.n_slots = n_sym / KS), so time-varying channels (KS = 7, 2, 1) take the same code
+template <int NR, int NL, int QM, int LT, int NW, int KS = kSym>
 __global__ void __launch_bounds__(32 * NW) k_lg(DetectArgs a) {
-    using SM = LgSmem<NR, NL, NW>;
+    using SM = LgSmem<NR, NL, NW, KS>;
     constexpr int UPW = SM::UPW;
     constexpr int TU = SM::TU;
     static_assert(32 % NL == 0, "NL must divide 32");
@@ -71,25 +73,25 @@ __global__ void __launch_bounds__(32 * NW) k_lg(DetectArgs a) {
 
     if (t == 0) {
 #pragma unroll
-        for (int s = 0; s <= kSym; ++s) mbar_init(&bars[s], 1);
+        for (int s = 0; s <= KS; ++s) mbar_init(&bars[s], 1);
         fence_mbar_init();
     }
     __syncthreads();
     if (t == 0) {
-        mbar_arrive_expect_tx(&bars[kSym], (uint32_t)nvalid * NR * NL * 8u);
+        mbar_arrive_expect_tx(&bars[KS], (uint32_t)nvalid * NR * NL * 8u);
 #pragma unroll 1
-        for (int s = 0; s < kSym; ++s) mbar_arrive_expect_tx(&bars[s], (uint32_t)nvalid * NR * 8u);
+        for (int s = 0; s < KS; ++s) mbar_arrive_expect_tx(&bars[s], (uint32_t)nvalid * NR * 8u);
     }
     __syncthreads();
     // the group leader of each unit copies its H and its 14 y vectors into padded slots
     if (k == 0 && active) {
-        bulk_g2s(sH + ul * SM::HS, a.H + ((size_t)slot * a.n_sc + sc) * NR * NL, NR * NL * 8u, &bars[kSym]);
+        bulk_g2s(sH + ul * SM::HS, a.H + ((size_t)slot * a.n_sc + sc) * NR * NL, NR * NL * 8u, &bars[KS]);
 #pragma unroll 1
-        for (int s = 0; s < kSym; ++s)
-            bulk_g2s(sy + (s * TU + ul) * SM::YS, a.y + ((size_t)(slot * kSym + s) * a.n_sc + sc) * NR, NR * 8u,
+        for (int s = 0; s < KS; ++s)
+            bulk_g2s(sy + (s * TU + ul) * SM::YS, a.y + ((size_t)(slot * KS + s) * a.n_sc + sc) * NR, NR * 8u,
                      &bars[s]);
     }
-    mbar_wait(&bars[kSym], 0);
+    mbar_wait(&bars[KS], 0);
 
     const float2* hU = sH + ul * SM::HS;  // H[r][l] of this lane's unit (garbage but in-bounds if !active)
     // a2: row k of G
@@ -217,14 +219,14 @@ __global__ void __launch_bounds__(32 * NW) k_lg(DetectArgs a) {
     const float ia = rsqrtf(norm);
     const bool zf = !(s2 > 0.f);
 #pragma unroll 1
-    for (int s = 0; s < kSym; ++s) {
+    for (int s = 0; s < KS; ++s) {
         mbar_wait(&bars[s], 0);
         if (!active) continue;
         const float2* ys = sy + (s * TU + ul) * SM::YS;
         float2 acc = make_float2(0.f, 0.f);
 #pragma unroll
         for (int r = 0; r < NR; ++r) acc = cmac(acc, w[r], ys[r]);
-        const size_t re = (size_t)(slot * kSym + s) * a.n_sc + sc;
+        const size_t re = (size_t)(slot * KS + s) * a.n_sc + sc;
         if (a.llr) {
             float v[QM];
             uint32_t wd[kWords];
@@ -656,24 +658,27 @@ cudaError_t prepare3() {
     return cudaSuccess;
 }
 
-template <int NR, int NL, int QM, int LT, int NW>
+template <int NR, int NL, int QM, int LT, int NW, int KS = kSym>
 cudaError_t launch(const DetectArgs& a, cudaStream_t s) {
     if (a.n_sc <= 0 || a.n_slots <= 0) return cudaSuccess;
-    constexpr int TU = LgSmem<NR, NL, NW>::TU;
+    constexpr int TU = LgSmem<NR, NL, NW, KS>::TU;
     dim3 grid((a.n_sc + TU - 1) / TU, a.n_slots);
-    return launch_kernel(k_lg<NR, NL, QM, LT, NW>, grid, dim3(32 * NW), LgSmem<NR, NL, NW>::total, s, a.overlap, a);
+    return launch_kernel(k_lg<NR, NL, QM, LT, NW, KS>, grid, dim3(32 * NW), LgSmem<NR, NL, NW, KS>::total, s, a.overlap, a);
 }
 
-template <int NR, int NL, int QM, int LT, int NW>
+template <int NR, int NL, int QM, int LT, int NW, int KS = kSym>
 cudaError_t prepare() {
-    constexpr size_t smem = LgSmem<NR, NL, NW>::total;
+    constexpr size_t smem = LgSmem<NR, NL, NW, KS>::total;
     if (smem > 48 * 1024)
-        return cudaFuncSetAttribute(k_lg<NR, NL, QM, LT, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        return cudaFuncSetAttribute(k_lg<NR, NL, QM, LT, NW, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     return cudaSuccess;
 }
 
 #define LG_ENTRY(NAME, NR, NL, QM, LT, NW) \
     KernelEntry { NAME, NR, NL, QM, 1, 14, LT, 32, 1, launch<NR, NL, QM, LT, NW>, prepare<NR, NL, QM, LT, NW> }
+// time-varying channels on the 16 x 8 per-subcarrier shape (NEXT-3): one H per KS symbols
+#define LG_TV_ENTRY(NAME, NR, NL, QM, LT, NW, KS) \
+    KernelEntry { NAME, NR, NL, QM, 1, KS, LT, 32, 1, launch<NR, NL, QM, LT, NW, KS>, prepare<NR, NL, QM, LT, NW, KS> }
 
 #define LG3_ENTRY(NAME, NR, NL, QM, LT, NW) LG3P_ENTRY(NAME, NR, NL, QM, LT, NW, 0)
 #define LG3P_ENTRY(NAME, NR, NL, QM, LT, NW, PFD)                                                      \
@@ -699,6 +704,9 @@ const KernelEntry kEntries[] = {
                 prepare3<16, 8, 8, kLlrF16, 4, 0, 2>},
     LG3_ENTRY("lg3_16x8_q8_f16", 16, 8, 8, kLlrF16, 2),  // y by TMA, H by per-unit bulk copies
     LG_ENTRY("lg_16x8_q8_f16", 16, 8, 8, kLlrF16, 2),
+    LG_TV_ENTRY("lg_16x8_q8_f16_s7", 16, 8, 8, kLlrF16, 2, 7),
+    LG_TV_ENTRY("lg_16x8_q8_f16_s2", 16, 8, 8, kLlrF16, 2, 2),
+    LG_TV_ENTRY("lg_16x8_q8_f16_s1", 16, 8, 8, kLlrF16, 2, 1),
     LG_ENTRY("lg_16x8_q8_f32", 16, 8, 8, kLlrF32, 2),
     LG_ENTRY("lg_16x8_q8_i8", 16, 8, 8, kLlrI8, 2),
     LG_ENTRY("lg_16x8_q6_f16", 16, 8, 6, kLlrF16, 2),

@@ -27,7 +27,9 @@ def main():
     for k, sph, kernels in ((2, 7, ["tpu_4x4_q4_f32_s7", "generic"]), (2, 2, ["tpu_4x4_q4_f32_s2", "generic"]),
                             (2, 1, ["tpu_4x4_q4_f32_s1", "generic"]), (2, 14, ["tpu_4x4_q4_f32"]),
                             (3, 7, ["stream_8x4_q6_i8_s7", "generic"]), (3, 2, ["stream_8x4_q6_i8_s2", "generic"]),
-                            (3, 1, ["stream_8x4_q6_i8_s1", "generic"]), (3, 14, ["stream_8x4_q6_i8"])):
+                            (3, 1, ["stream_8x4_q6_i8_s1", "generic"]), (3, 14, ["stream_8x4_q6_i8"]),
+                            (4, 7, ["lg_16x8_q8_f16_s7", "generic"]), (4, 2, ["lg_16x8_q8_f16_s2"]),
+                            (4, 1, ["lg_16x8_q8_f16_s1"]), (4, 14, ["lg_16x8_q8_f16", "lg3hl_16x8_q8_f16"])):
         cfg = dict(synth.CONFIGS[k], sym_per_h=sph)
         w = synth.generate(cfg)
         n_units = w.n_units
