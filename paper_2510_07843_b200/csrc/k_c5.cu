@@ -178,6 +178,27 @@ constexpr int kSetupConvUnroll = 2;  // 4 and 8 measured slower
 constexpr int kBiImg = 128 * 128;
 constexpr int kBiRec = kBiImg + 128;
 
+// L2 eviction-priority helpers (BI == 4): y tiles and LLR records are streamed once; marking them
+// evict-first keeps the B-image records (written a few units ahead of their copy) resident until consumed
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void tma_load_3d_hint(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                 uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void st_v8_hint(void* p, const uint32_t* w, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8}, %9;" ::"l"(p), "r"(w[0]), "r"(w[1]),
+                 "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "l"(pol)
+                 : "memory");
+}
+
 // K row R of a B image from 32 words (8 chunks of 16 B: hi pairs n 0..31, then lo), SWIZZLE_128B positions
 // (chunk q of row R at q ^ (R & 7)), as four 32-byte stores of chunk pairs; ODD = R & 1 (an odd row puts
 // chunk q0 + 1 before chunk q0)
@@ -743,8 +764,12 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                 const long long uu = u0 + (gg >> 2) * du;
                 const int slot = (int)(uu / a.n_fb), fb = (int)(uu % a.n_fb);
                 mbar_arrive_expect_tx(&yfull[st], (uint32_t)SM::chunk);
-                tma_load_3d(base + (uint32_t)(SM::y0 + st * SM::chunk), &ymap, 32 * (int)(gg & 3), fb * kSc,
-                            slot * kSym, &yfull[st]);
+                if constexpr (BI == 4)
+                    tma_load_3d_hint(base + (uint32_t)(SM::y0 + st * SM::chunk), &ymap, 32 * (int)(gg & 3), fb * kSc,
+                                     slot * kSym, &yfull[st], l2_evict_first_policy());
+                else
+                    tma_load_3d(base + (uint32_t)(SM::y0 + st * SM::chunk), &ymap, 32 * (int)(gg & 3), fb * kSc,
+                                slot * kSym, &yfull[st]);
             }
             PROF_ADD(prof, 31, tk0);
             PROF_FLUSH(true);
@@ -764,7 +789,7 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
         for (long long j0 = 0; j0 < n_my; j0 += su::UPB, ++it) {
             const int nv = nv_of(j0);
             const long long jn = j0 + su::UPB;
-            setup_batch<QM, true, kWide, BI == 3 ? 2 : (BI != 0 ? 1 : 0)>(a, &hmap, g + SM::setup, base + (uint32_t)SM::setup, stma, smma, tmem + kSetupCols, it,
+            setup_batch<QM, true, kWide, (BI == 3 || BI == 4) ? 2 : (BI != 0 ? 1 : 0)>(a, &hmap, g + SM::setup, base + (uint32_t)SM::setup, stma, smma, tmem + kSetupCols, it,
                                   nv, gt, gw, lane, waited, [&](int s_) { return u0 + (j0 + s_) * du; },
                                   [] { asm volatile("bar.sync 5, 128;" ::: "memory"); },
                                   [&] {
@@ -936,7 +961,13 @@ __global__ void __launch_bounds__(32 * (6 + EW) + (FUSED ? 128 : 0), 1)
                         pack_llr<LT, NL * QM, true>(v, wd);
                     }
                 }
-                store_bytes<kRec>((char*)a.llr + re * kRec, wd);
+                if constexpr (BI == 4 && kRec % 32 == 0) {
+                    const uint64_t pol = l2_evict_first_policy();
+#pragma unroll
+                    for (int q = 0; q < kRec / 32; ++q) st_v8_hint((char*)a.llr + re * kRec + 32 * q, wd + 8 * q, pol);
+                } else {
+                    store_bytes<kRec>((char*)a.llr + re * kRec, wd);
+                }
             }
             if (a.xhat) {
 #pragma unroll
@@ -1335,7 +1366,8 @@ size_t c5fb_workspace(const DetectArgs& a) {
             prepare_c5<QM, LT, 6, S, NLO, TA, SETUP, BEPI>, c5_workspace                                   \
     }
 // BI = 1: B-image records; 2: + the consumed records discarded from L2 (no dirty write-back) by the tile-1
-// epilogue warp; 3: 2 + the setup group's image readout by whole warps (16x32bx2 TMEM loads)
+// epilogue warp; 3: 2 + the setup group's image readout by whole warps (16x32bx2 TMEM loads); 4: 3 + y tiles and
+// LLR stores with an L2 evict-first policy
 #define C5FB_ENTRY(NAME, QM, LT, S, BI)                                                                     \
     KernelEntry {                                                                                          \
         NAME, 64, 16, QM, kSc, 14, LT, 32, 1, launch_c5<QM, LT, 6, S, 2, 4, 2, true, true, 2, BI>,         \
@@ -1354,8 +1386,10 @@ size_t c5fb_workspace(const DetectArgs& a) {
 // (under-loaded) epilogue warps instead of the converter warps, which set the pace of the pipeline.
 const KernelEntry kEntries[] = {
     // C5 default: setup warp group inside the apply kernel, writing B-image records (read out of TMEM by whole
-    // warps) that the apply copies straight into its B sets; consumed records discarded from L2
-    C5FB_ENTRY("c5_fusedbiw_64x16_q6_i8", 6, kLlrI8, 5, 3),
+    // warps) that the apply copies straight into its B sets; consumed records discarded from L2; the streamed
+    // y tiles and LLR stores marked L2 evict-first so that the records stay resident until they are copied
+    C5FB_ENTRY("c5_fusedbie_64x16_q6_i8", 6, kLlrI8, 5, 4),
+    C5FB_ENTRY("c5_fusedbiw_64x16_q6_i8", 6, kLlrI8, 5, 3),  // without the evict-first hints
     C5FB_ENTRY("c5_fusedbid_64x16_q6_i8", 6, kLlrI8, 5, 2),  // image readout by half warps (lanes 0-15)
     C5FB_ENTRY("c5_fusedbi_64x16_q6_i8", 6, kLlrI8, 5, 1),  // B-image records, no discards
     C5F_ENTRY("c5_fused_64x16_q6_i8", 6, kLlrI8, 5, 2),  // W~ records, B sets built by epilogue warps 4-7

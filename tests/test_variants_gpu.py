@@ -10,7 +10,7 @@ from paper_2510_07843_b200 import synth
 
 pytestmark = pytest.mark.gpu
 
-C5_VARIANTS = ["c5_fused_64x16_q6_i8", "c5_fusedbi_64x16_q6_i8", "c5_fusedbid_64x16_q6_i8", "c5_fusedbiw_64x16_q6_i8", "c5_fused3_64x16_q6_i8", "c5_bf16_tcs_be_64x16_q6_i8", "c5_bf16kc_tcs_be_64x16_q6_i8",
+C5_VARIANTS = ["c5_fused_64x16_q6_i8", "c5_fusedbi_64x16_q6_i8", "c5_fusedbid_64x16_q6_i8", "c5_fusedbiw_64x16_q6_i8", "c5_fusedbie_64x16_q6_i8", "c5_fused3_64x16_q6_i8", "c5_bf16_tcs_be_64x16_q6_i8", "c5_bf16kc_tcs_be_64x16_q6_i8",
                "c5_bf16_tcs_64x16_q6_i8", "c5_bf16_gj_64x16_q6_i8", "c5_bf16_chol_64x16_q6_i8", "c5_tf32_gj_64x16_q6_i8",
                "big_64x16_q6_i8"]
 C4_VARIANTS = ["lg3hl_16x8_q8_f16", "lg3hl2_16x8_q8_f16", "lg3hq_16x8_q8_f16", "lg3hp_16x8_q8_f16", "lg3_16x8_q8_f16", "lg_16x8_q8_f16"]
