@@ -2,7 +2,9 @@
 // any Qm and LLR type): the SIMT setup of big_setup.cuh (rows a2-a5, W~ to the
 // plan workspace), then k_big_apply (rows a6-a7): one CTA per PRB-unit, the
 // unit's 168 y vectors bulk-copied at a padded 528-byte stride, thread (RE pair,
-// layer half) accumulates 2 x 8 complex outputs. The C5 configuration itself
+// layer half) accumulates 2 x 8 complex outputs; with H constant over sym_per_h
+// = 7 / 2 / 1 symbols one CTA serves 14 / sym_per_h H-units (the _s7/_s2/_s1
+// entries, the default of the C5 shape at those sym_per_h). The C5 configuration itself
 // (64 x 16, 64-QAM, int8) runs on the tcgen05 pipeline of k_c5.cu by default.
 
 #include "big_setup.cuh"
@@ -10,31 +12,38 @@
 namespace mimo {
 namespace {
 
-template <int NR, int NL>
+template <int NR, int NL, int SPH>
 struct BigSmem {
+    static constexpr int G = kSym / SPH;                   // H-units per CTA (168 REs in all)
     static constexpr int YS = NR * 8 + 16;                 // bytes per RE (padded 16 B)
     static constexpr size_t bar = 0;
     static constexpr size_t y = 128;                       // [168][YS]
-    static constexpr size_t W = y + (size_t)kRe * YS;      // [NR][NL] float2
-    static constexpr size_t total = W + (size_t)NR * NL * 8;
+    static constexpr size_t W = y + (size_t)kRe * YS;      // [G][NR][NL] float2
+    static constexpr size_t total = W + (size_t)G * NR * NL * 8;
 };
 
-// thread (pair p, half h): REs 2p, 2p+1 of the unit, layers 8h .. 8h+7
-template <int NR, int NL, int QM, int LT>
+// thread (pair p, half h): REs 2p, 2p+1 of the CTA's 168, layers 8h .. 8h+7. With H constant over
+// SPH < 14 symbols (NEXT-3) the CTA serves G = 14 / SPH consecutive H-units of
+// 12 x SPH REs each, every unit with its own W~ in shared memory.
+template <int NR, int NL, int QM, int LT, int SPH>
 __global__ void __launch_bounds__(kRe) k_big_apply(DetectArgs a) {
     static_assert(NL == 16 && NR % 2 == 0, "k_big_apply: 16 layers");
-    using SM = BigSmem<NR, NL>;
+    static_assert(kSym % SPH == 0, "k_big_apply: SPH divides 14");
+    using SM = BigSmem<NR, NL, SPH>;
     constexpr int WS = BigWs<NR, NL>::stride;
     constexpr int KH = NL / 2;
+    constexpr int RU = kSc * SPH;  // REs per H-unit
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SM::bar);
     unsigned char* sy = smem + SM::y;
-    const float2* sW = reinterpret_cast<const float2*>(smem + SM::W);
 
     pdl_launch_dependents();
     const int t = threadIdx.x;
-    const long long u = blockIdx.x;
-    const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);
+    const long long u0 = (long long)blockIdx.x * SM::G;
+    const int nv = (int)min((long long)SM::G, a.n_units - u0);  // valid units of this CTA
+    const int g = t / RU;
+    const long long u = u0 + g;
+    const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);  // slot = H time block
     if (t == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -42,18 +51,22 @@ __global__ void __launch_bounds__(kRe) k_big_apply(DetectArgs a) {
     }
     __syncthreads();
     if (t == 0) {
-        mbar_arrive_expect_tx(&bar[0], (uint32_t)kRe * NR * 8u);
-        mbar_arrive_expect_tx(&bar[1], (uint32_t)NR * NL * 8u);
+        mbar_arrive_expect_tx(&bar[0], (uint32_t)(nv * RU) * NR * 8u);
+        mbar_arrive_expect_tx(&bar[1], (uint32_t)nv * NR * NL * 8u);
     }
     __syncthreads();
-    {  // thread t copies RE t (symbol t / 12, subcarrier t % 12) into its padded slot
-        const int s = t / kSc, f = t % kSc;
-        bulk_g2s(sy + (size_t)t * SM::YS, a.y + ((size_t)(slot * kSym + s) * a.n_sc + fb * kSc + f) * NR, NR * 8u,
+    if (g >= nv) return;  // ragged last CTA (no later block-wide barrier)
+    {  // thread t copies RE t (symbol (t % RU) / 12, subcarrier t % 12 of its unit) into its padded slot
+        const int s = (t % RU) / kSc, f = t % kSc;
+        bulk_g2s(sy + (size_t)t * SM::YS, a.y + ((size_t)(slot * SPH + s) * a.n_sc + fb * kSc + f) * NR, NR * 8u,
                  &bar[0]);
     }
     pdl_wait();  // W~ of this call's setup kernel is complete
     if (t == 0)
-        bulk_g2s(smem + SM::W, reinterpret_cast<const float*>(a.ws) + u * WS, NR * NL * 8u, &bar[1]);
+        for (int i = 0; i < nv; ++i)
+            bulk_g2s(smem + SM::W + (size_t)i * NR * NL * 8, reinterpret_cast<const float*>(a.ws) + (u0 + i) * WS,
+                     NR * NL * 8u, &bar[1]);
+    const float2* sW = reinterpret_cast<const float2*>(smem + SM::W + (size_t)g * NR * NL * 8);
     const int p = t >> 1, h = t & 1;
     float slope[KH];
     {
@@ -95,9 +108,9 @@ __global__ void __launch_bounds__(kRe) k_big_apply(DetectArgs a) {
     const float ia = rsqrtf((float)qam_norm(QM));
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
-        const int ri = 2 * p + e;
+        const int ri = (2 * p + e) % RU;
         const int s = ri / kSc, f = ri % kSc;
-        const size_t re = (size_t)(slot * kSym + s) * a.n_sc + fb * kSc + f;
+        const size_t re = (size_t)(slot * SPH + s) * a.n_sc + fb * kSc + f;
         const float2* acc = e ? acc1 : acc0;
         if (a.llr) {
             float v[KH * QM];
@@ -125,36 +138,44 @@ size_t workspace(const DetectArgs& a) {
     return (size_t)a.n_units * BigWs<NR, NL>::stride * 4;
 }
 
-template <int NR, int NL, int QM, int LT>
+template <int NR, int NL, int QM, int LT, int SPH>
 cudaError_t launch(const DetectArgs& a, cudaStream_t s) {
     if (a.n_units <= 0) return cudaSuccess;
     constexpr int UPB = 4;
+    constexpr int G = BigSmem<NR, NL, SPH>::G;
     cudaError_t e = launch_kernel(k_big_setup<NR, NL, QM, UPB>, dim3((unsigned)((a.n_units + UPB - 1) / UPB)),
                                   dim3(32 * UPB), UPB * SetupSmem<NR, NL>::per_unit, s, a.overlap, a);
     if (e != cudaSuccess) return e;
-    return launch_kernel(k_big_apply<NR, NL, QM, LT>, dim3((unsigned)a.n_units), dim3(kRe), BigSmem<NR, NL>::total, s,
-                         a.overlap, a);
+    return launch_kernel(k_big_apply<NR, NL, QM, LT, SPH>, dim3((unsigned)((a.n_units + G - 1) / G)), dim3(kRe),
+                         BigSmem<NR, NL, SPH>::total, s, a.overlap, a);
 }
 
-template <int NR, int NL, int QM, int LT>
+template <int NR, int NL, int QM, int LT, int SPH>
 cudaError_t prepare() {
     cudaError_t e = cudaFuncSetAttribute(k_big_setup<NR, NL, QM, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)(4 * SetupSmem<NR, NL>::per_unit));
     if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(k_big_apply<NR, NL, QM, LT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)BigSmem<NR, NL>::total);
+    return cudaFuncSetAttribute(k_big_apply<NR, NL, QM, LT, SPH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)BigSmem<NR, NL, SPH>::total);
 }
 
-#define BIG_ENTRY(NAME, NR, NL, QM, LT) \
-    KernelEntry { NAME, NR, NL, QM, kSc, 14, LT, 32, 2, launch<NR, NL, QM, LT>, prepare<NR, NL, QM, LT>, workspace<NR, NL> }
+#define BIG_ENTRY(NAME, NR, NL, QM, LT, SPH)                                                                  \
+    KernelEntry {                                                                                             \
+        NAME, NR, NL, QM, kSc, SPH, LT, 32, 2, launch<NR, NL, QM, LT, SPH>, prepare<NR, NL, QM, LT, SPH>,     \
+            workspace<NR, NL>                                                                                 \
+    }
 
 const KernelEntry kEntries[] = {
-    BIG_ENTRY("big_64x16_q6_i8", 64, 16, 6, kLlrI8),  // C5 shape on SIMT (alternative to the c5 tcgen05 pipeline)
-    BIG_ENTRY("big_64x16_q6_f16", 64, 16, 6, kLlrF16),
-    BIG_ENTRY("big_64x16_q6_f32", 64, 16, 6, kLlrF32),
-    BIG_ENTRY("big_64x16_q8_i8", 64, 16, 8, kLlrI8),
-    BIG_ENTRY("big_64x16_q4_i8", 64, 16, 4, kLlrI8),
-    BIG_ENTRY("big_32x16_q6_i8", 32, 16, 6, kLlrI8),
+    BIG_ENTRY("big_64x16_q6_i8", 64, 16, 6, kLlrI8, 14),  // C5 shape on SIMT (alternative to the c5 tcgen05 pipeline)
+    BIG_ENTRY("big_64x16_q6_f16", 64, 16, 6, kLlrF16, 14),
+    BIG_ENTRY("big_64x16_q6_f32", 64, 16, 6, kLlrF32, 14),
+    BIG_ENTRY("big_64x16_q8_i8", 64, 16, 8, kLlrI8, 14),
+    BIG_ENTRY("big_64x16_q4_i8", 64, 16, 4, kLlrI8, 14),
+    BIG_ENTRY("big_32x16_q6_i8", 32, 16, 6, kLlrI8, 14),
+    // time-varying H on the C5 shape (NEXT-3): 14 / SPH H-units per CTA
+    BIG_ENTRY("big_64x16_q6_i8_s7", 64, 16, 6, kLlrI8, 7),
+    BIG_ENTRY("big_64x16_q6_i8_s2", 64, 16, 6, kLlrI8, 2),
+    BIG_ENTRY("big_64x16_q6_i8_s1", 64, 16, 6, kLlrI8, 1),
 };
 
 }  // namespace

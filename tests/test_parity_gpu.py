@@ -219,13 +219,14 @@ def test_host_path_c5_chunked():
                                           (1, 1, "tpu_2x2_q2_f32_s1"), (3, 7, "stream_8x4_q6_i8_s7"),
                                           (3, 2, "stream_8x4_q6_i8_s2"), (3, 1, "stream_8x4_q6_i8_s1"),
                                           (4, 7, "lg_16x8_q8_f16_s7"), (4, 2, "lg_16x8_q8_f16_s2"),
-                                          (4, 1, "lg_16x8_q8_f16_s1")])
+                                          (4, 1, "lg_16x8_q8_f16_s1"), (5, 7, "big_64x16_q6_i8_s7"),
+                                          (5, 2, "big_64x16_q6_i8_s2"), (5, 1, "big_64x16_q6_i8_s1")])
 def test_time_varying_fast_kernels(k, sph, kernel):
-    """NEXT-3 fast path: the per-subcarrier (C1 / C2 / C4) and per-PRB (C3 stream) kernels with H constant
-    over sph < 14 symbols, over several CTA tiles and a ragged subcarrier tail (n_sc = 300 for C2 - C4),
-    against the oracle."""
+    """NEXT-3 fast path: the per-subcarrier (C1 / C2 / C4) and per-PRB (C3 stream, C5 big) kernels with H
+    constant over sph < 14 symbols, over several CTA tiles and a ragged subcarrier tail (n_sc = 300 for
+    C2 - C4), against the oracle."""
     cfg = dict(synth.CONFIGS[k], sym_per_h=sph)
-    kw = dict(n_sc=300, n_slots=2) if k in (2, 3, 4) else dict(n_slots=2)
+    kw = dict(n_sc=300, n_slots=2) if k in (2, 3, 4) else dict(n_sc=300, n_slots=1) if k == 5 else dict(n_slots=2)
     w = synth.generate(cfg, **kw)
     g = parity.run_gpu(w, kernel=kernel)
     assert g["kernel"] == kernel and g["n_failed"] == 0

@@ -1,9 +1,9 @@
 """Time the time-varying-channel kernels (NEXT-3: H constant over sym_per_h < 14 symbols) against
-the generic kernel on the full C2 / C3 grids, through the C ABI (mimo.Plan.detect), the way
+the generic kernel on the full C2 - C5 grids, through the C ABI (mimo.Plan.detect), the way
 bench.py times a step: rotating buffer sets > 3x L2, CUDA-graph replays, CUDA events on the
 launching stream. Writes one JSON line per (config, sym_per_h, kernel).
 
-    python tools/time_varying.py [--out profiles/r02/time_varying.jsonl]
+    python tools/time_varying.py [--configs 2 3 4 5] [--out profiles/r02/time_varying.jsonl]
 """
 import argparse
 import json
@@ -20,6 +20,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--configs", type=int, nargs="*", default=[2, 3, 4, 5])
     args = ap.parse_args()
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     hbm = float(peaks.get("hbm_gbs", 6547.2))
@@ -29,7 +30,11 @@ def main():
                             (3, 7, ["stream_8x4_q6_i8_s7", "generic"]), (3, 2, ["stream_8x4_q6_i8_s2", "generic"]),
                             (3, 1, ["stream_8x4_q6_i8_s1", "generic"]), (3, 14, ["stream_8x4_q6_i8"]),
                             (4, 7, ["lg_16x8_q8_f16_s7", "generic"]), (4, 2, ["lg_16x8_q8_f16_s2"]),
-                            (4, 1, ["lg_16x8_q8_f16_s1"]), (4, 14, ["lg_16x8_q8_f16", "lg3hl_16x8_q8_f16"])):
+                            (4, 1, ["lg_16x8_q8_f16_s1"]), (4, 14, ["lg_16x8_q8_f16", "lg3hl_16x8_q8_f16"]),
+                            (5, 7, ["big_64x16_q6_i8_s7", "generic"]), (5, 2, ["big_64x16_q6_i8_s2"]),
+                            (5, 1, ["big_64x16_q6_i8_s1"]), (5, 14, ["big_64x16_q6_i8", None])):
+        if k not in args.configs:
+            continue
         cfg = dict(synth.CONFIGS[k], sym_per_h=sph)
         w = synth.generate(cfg)
         n_units = w.n_units
