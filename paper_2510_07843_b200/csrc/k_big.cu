@@ -90,15 +90,16 @@ __global__ void __launch_bounds__(kRe) k_big_apply(DetectArgs a) {
         for (int c = 0; c < 2; ++c) {
             const float2 va = c ? make_float2(ya.z, ya.w) : make_float2(ya.x, ya.y);
             const float2 vb = c ? make_float2(yb.z, yb.w) : make_float2(yb.x, yb.y);
+            const float2 nva = make_float2(-va.y, va.x), nvb = make_float2(-vb.y, vb.x);
             const float4* wr = wq + (2 * r2 + c) * (NL / 2);
 #pragma unroll
-            for (int k2 = 0; k2 < KH / 2; ++k2) {
+            for (int k2 = 0; k2 < KH / 2; ++k2) {  // packed FFMA2 (same FMA order as cmac)
                 const float4 w2 = wr[k2];
                 const float2 wa = make_float2(w2.x, w2.y), wb = make_float2(w2.z, w2.w);
-                acc0[2 * k2] = cmac(acc0[2 * k2], wa, va);
-                acc0[2 * k2 + 1] = cmac(acc0[2 * k2 + 1], wb, va);
-                acc1[2 * k2] = cmac(acc1[2 * k2], wa, vb);
-                acc1[2 * k2 + 1] = cmac(acc1[2 * k2 + 1], wb, vb);
+                acc0[2 * k2] = cmac_y(acc0[2 * k2], wa, va, nva);
+                acc0[2 * k2 + 1] = cmac_y(acc0[2 * k2 + 1], wb, va, nva);
+                acc1[2 * k2] = cmac_y(acc1[2 * k2], wa, vb, nvb);
+                acc1[2 * k2 + 1] = cmac_y(acc1[2 * k2 + 1], wb, vb, nvb);
             }
         }
     }
