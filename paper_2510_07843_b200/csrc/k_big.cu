@@ -2,7 +2,7 @@
 // any Qm and LLR type): the SIMT setup of big_setup.cuh (rows a2-a5, W~ to the
 // plan workspace), then k_big_apply (rows a6-a7): one CTA per PRB-unit, the
 // unit's 168 y vectors bulk-copied at a padded 528-byte stride, thread (RE pair,
-// layer half) accumulates 2 x 8 complex outputs; with H constant over sym_per_h
+// layer quarter) accumulates 2 x 4 complex outputs; with H constant over sym_per_h
 // = 7 / 2 / 1 symbols one CTA serves 14 / sym_per_h H-units (the _s7/_s2/_s1
 // entries, the default of the C5 shape at those sym_per_h). The C5 configuration itself
 // (64 x 16, 64-QAM, int8) runs on the tcgen05 pipeline of k_c5.cu by default.
@@ -22,16 +22,19 @@ struct BigSmem {
     static constexpr size_t total = W + (size_t)G * NR * NL * 8;
 };
 
-// thread (pair p, half h): REs 2p, 2p+1 of the CTA's 168, layers 8h .. 8h+7. With H constant over
-// SPH < 14 symbols (NEXT-3) the CTA serves G = 14 / SPH consecutive H-units of
-// 12 x SPH REs each, every unit with its own W~ in shared memory.
+// thread (pair p, quarter h): REs 2p, 2p+1 of the CTA's 168, layers 4h .. 4h+3 (336 threads: four
+// threads per RE pair so the FP32 pipe sees 2 x the warps of one per RE at the same shared-memory
+// footprint). With H constant over SPH < 14 symbols (NEXT-3) the CTA serves
+// G = 14 / SPH consecutive H-units of 12 x SPH REs each, every unit with its own W~ in shared memory.
+constexpr int kBigLs = 4;                   // threads per RE pair (layer split)
+constexpr int kBigThreads = kRe / 2 * kBigLs;
 template <int NR, int NL, int QM, int LT, int SPH>
-__global__ void __launch_bounds__(kRe) k_big_apply(DetectArgs a) {
+__global__ void __launch_bounds__(kBigThreads) k_big_apply(DetectArgs a) {
     static_assert(NL == 16 && NR % 2 == 0, "k_big_apply: 16 layers");
     static_assert(kSym % SPH == 0, "k_big_apply: SPH divides 14");
     using SM = BigSmem<NR, NL, SPH>;
     constexpr int WS = BigWs<NR, NL>::stride;
-    constexpr int KH = NL / 2;
+    constexpr int KH = NL / kBigLs;
     constexpr int RU = kSc * SPH;  // REs per H-unit
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + SM::bar);
@@ -41,9 +44,6 @@ __global__ void __launch_bounds__(kRe) k_big_apply(DetectArgs a) {
     const int t = threadIdx.x;
     const long long u0 = (long long)blockIdx.x * SM::G;
     const int nv = (int)min((long long)SM::G, a.n_units - u0);  // valid units of this CTA
-    const int g = t / RU;
-    const long long u = u0 + g;
-    const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);  // slot = H time block
     if (t == 0) {
         mbar_init(&bar[0], 1);
         mbar_init(&bar[1], 1);
@@ -55,10 +55,11 @@ __global__ void __launch_bounds__(kRe) k_big_apply(DetectArgs a) {
         mbar_arrive_expect_tx(&bar[1], (uint32_t)nv * NR * NL * 8u);
     }
     __syncthreads();
-    if (g >= nv) return;  // ragged last CTA (no later block-wide barrier)
-    {  // thread t copies RE t (symbol (t % RU) / 12, subcarrier t % 12 of its unit) into its padded slot
+    if (t < kRe && t / RU < nv) {  // thread t copies RE t (symbol (t % RU) / 12, subcarrier t % 12 of its unit)
+        const long long uc = u0 + t / RU;
+        const int sc = (int)(uc / a.n_fb), fc = (int)(uc % a.n_fb);
         const int s = (t % RU) / kSc, f = t % kSc;
-        bulk_g2s(sy + (size_t)t * SM::YS, a.y + ((size_t)(slot * SPH + s) * a.n_sc + fb * kSc + f) * NR, NR * 8u,
+        bulk_g2s(sy + (size_t)t * SM::YS, a.y + ((size_t)(sc * SPH + s) * a.n_sc + fc * kSc + f) * NR, NR * 8u,
                  &bar[0]);
     }
     pdl_wait();  // W~ of this call's setup kernel is complete
@@ -66,8 +67,12 @@ __global__ void __launch_bounds__(kRe) k_big_apply(DetectArgs a) {
         for (int i = 0; i < nv; ++i)
             bulk_g2s(smem + SM::W + (size_t)i * NR * NL * 8, reinterpret_cast<const float*>(a.ws) + (u0 + i) * WS,
                      NR * NL * 8u, &bar[1]);
+    const int p = t / kBigLs, h = t % kBigLs;
+    const int g = (2 * p) / RU;  // this thread's unit
+    if (g >= nv) return;         // ragged last CTA (no later block-wide barrier)
+    const long long u = u0 + g;
+    const int slot = (int)(u / a.n_fb), fb = (int)(u % a.n_fb);  // slot = H time block
     const float2* sW = reinterpret_cast<const float2*>(smem + SM::W + (size_t)g * NR * NL * 8);
-    const int p = t >> 1, h = t & 1;
     float slope[KH];
     {
         const float* wsu = reinterpret_cast<const float*>(a.ws) + u * WS + NR * NL * 2;
@@ -103,7 +108,7 @@ __global__ void __launch_bounds__(kRe) k_big_apply(DetectArgs a) {
             }
         }
     }
-    constexpr int kBytes = KH * QM * LlrTraits<LT>::bytes;  // this thread's half of an RE record
+    constexpr int kBytes = KH * QM * LlrTraits<LT>::bytes;  // this thread's quarter of an RE record
     constexpr int kWords = (kBytes + 3) / 4;
     const bool zf = !(a.sigma2 > 0.f);
     const float ia = rsqrtf((float)qam_norm(QM));
@@ -147,7 +152,7 @@ cudaError_t launch(const DetectArgs& a, cudaStream_t s) {
     cudaError_t e = launch_kernel(k_big_setup<NR, NL, QM, UPB>, dim3((unsigned)((a.n_units + UPB - 1) / UPB)),
                                   dim3(32 * UPB), UPB * SetupSmem<NR, NL>::per_unit, s, a.overlap, a);
     if (e != cudaSuccess) return e;
-    return launch_kernel(k_big_apply<NR, NL, QM, LT, SPH>, dim3((unsigned)((a.n_units + G - 1) / G)), dim3(kRe),
+    return launch_kernel(k_big_apply<NR, NL, QM, LT, SPH>, dim3((unsigned)((a.n_units + G - 1) / G)), dim3(kBigThreads),
                          BigSmem<NR, NL, SPH>::total, s, a.overlap, a);
 }
 
